@@ -1,0 +1,75 @@
+// Exact small-modulus arithmetic shared by the split, GEMM-epilogue and CRT
+// kernels. All reductions are exact for any modulus 2 <= m <= 2^16 (Barrett
+// with a 32-bit magic and one correction step).
+#pragma once
+
+#include <cstdint>
+
+namespace irl {
+
+// Per-modulus constants handed to kernels by value.
+struct ModConst {
+    uint32_t p;        // digit base (prime)
+    uint32_t m;        // full modulus p^e (e = 1 or 2)
+    uint32_t magic_p;  // floor(2^32 / p)
+    uint32_t magic_m;  // floor(2^32 / m)
+    uint32_t off_p;    // 2^31 mod p
+    uint32_t off_m;    // 2^31 mod m
+    uint32_t e;        // exponent 1 or 2
+    uint32_t pad;
+};
+
+__host__ __device__ inline ModConst make_modconst(uint32_t p, uint32_t e) {
+    ModConst c{};
+    c.p = p;
+    c.e = e;
+    c.m = e == 2 ? p * p : p;
+    c.magic_p = static_cast<uint32_t>((1ull << 32) / p);
+    c.magic_m = static_cast<uint32_t>((1ull << 32) / c.m);
+    c.off_p = static_cast<uint32_t>((1ull << 31) % p);
+    c.off_m = static_cast<uint32_t>((1ull << 31) % c.m);
+    return c;
+}
+
+// u mod m for u in [0, 2^32).
+__device__ __forceinline__ uint32_t mod_u32(uint32_t u, uint32_t m, uint32_t magic) {
+    const uint32_t q = __umulhi(u, magic);
+    uint32_t r = u - q * m;
+    return r >= m ? r - m : r;
+}
+
+// x mod m in [0, m) for any signed 32-bit x (floor semantics).
+__device__ __forceinline__ uint32_t mod_s32(int32_t x, uint32_t m, uint32_t magic, uint32_t off) {
+    const uint32_t u = static_cast<uint32_t>(x) + 0x80000000u;  // x + 2^31
+    const uint32_t r = mod_u32(u, m, magic);
+    return r >= off ? r - off : r + m - off;
+}
+
+// Reference epilogue of gemm_mod_psq (modmat.cpp:150-158):
+// (t00 + p (t01 + t10)) mod p^2, with acc2 = t01 + t10 already fused.
+__device__ __forceinline__ uint32_t combine_psq(int32_t acc1, int32_t acc2, const ModConst& c) {
+    const uint32_t r2 = mod_s32(acc2, c.p, c.magic_p, c.off_p);
+    const uint32_t r1 = mod_s32(acc1, c.m, c.magic_m, c.off_m);
+    uint32_t v = r1 + c.p * r2;  // < 2 p^2
+    return v >= c.m ? v - c.m : v;
+}
+
+// Centred digit split of v in [0, p^2) (modmat.cpp:86-106):
+// d0 = centre(v mod p), d1 = centre(((v - d0) / p) mod p).
+__device__ __forceinline__ void digit_split(uint32_t v, const ModConst& c, int32_t& d0,
+                                            int32_t& d1) {
+    const int32_t p = static_cast<int32_t>(c.p);
+    const int32_t half = (p - 1) / 2;
+    int32_t a = static_cast<int32_t>(mod_u32(v, c.p, c.magic_p));
+    if (a > half) a -= p;
+    // (v - d0) is an exact multiple of p in [0, p^2]; Barrett quotient + fix.
+    const uint32_t u = static_cast<uint32_t>(static_cast<int32_t>(v) - a);
+    uint32_t hi = __umulhi(u, c.magic_p);
+    if (u - hi * c.p >= c.p) ++hi;
+    int32_t b = static_cast<int32_t>(hi >= c.p ? hi - c.p : hi);
+    if (b > half) b -= p;
+    d0 = a;
+    d1 = b;
+}
+
+}  // namespace irl

@@ -1,0 +1,34 @@
+// Internal (CUDA-side) interface of the PPMM engine kernels. Not part of the
+// public C ABI (see include/irl_capi.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "modarith.cuh"
+
+namespace irl {
+
+constexpr uint32_t kMaxPrimesPerLaunch = 32;
+
+// One batched PPMM launch over `parts` database parts and `nprimes` moduli.
+//   a_planes: [parts][nprimes][2][M][ldk] int8 centred digits (K-major)
+//   b_planes: [nprimes][2][N][ldk]        int8 centred digits (K-major)
+//   out:      [parts][nprimes][N][M]      uint16 residues mod p^2
+struct PpmmLaunch {
+    const int8_t* a_planes = nullptr;
+    const int8_t* b_planes = nullptr;
+    uint16_t* out = nullptr;
+    uint32_t M = 0, N = 0, K = 0, ldk = 0;
+    uint32_t parts = 1, nprimes = 0;
+    int accumulate = 0;          // out = (out + result) mod p^2
+    uint32_t max_clusters = 0;   // 0 = one CTA pair per SM pair
+    ModConst mc[kMaxPrimesPerLaunch];
+};
+
+cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream);
+size_t ppmm_smem_bytes();
+
+}  // namespace irl
