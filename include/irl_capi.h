@@ -1,0 +1,162 @@
+/* irl_capi.h — C ABI of the B200-native PPMM / RGSW-CCMM engine.
+ *
+ * This is the drop-in boundary for the hot path of the reference
+ * (/root/reference/proj, namespace irislab::modmat and emu::Emulator::ccmm_twin).
+ * Every entry point names the reference interface it replaces (file:line
+ * relative to /root/reference/proj). Signatures carry plain pointers and
+ * sizes only: no torch, no C++ types. Two families:
+ *
+ *   (1) Blocking host-buffer calls that mirror the reference free functions
+ *       value-for-value (row-major int32 SmallMatrix, fixed-width
+ *       little-endian BigMatrix entries as in modmat.cpp:216-231);
+ *   (2) the device-resident CCMM engine: database digit planes registered
+ *       once in HBM, queries streamed per batch (host or device buffers).
+ *
+ * Errors: every call returns an irl_status. Codes 1-5 are the reference's
+ * exception taxonomy (include/irislab/errors.hpp:9-53) and are raised under
+ * exactly the conditions the reference throws; irl_last_error() returns the
+ * message. There is no CPU fallback: without a usable sm_100 device,
+ * irl_ctx_create fails with IRL_ERR_NO_DEVICE. */
+#ifndef IRL_CAPI_H
+#define IRL_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IRL_ABI_VERSION 1
+
+typedef enum irl_status {
+    IRL_OK = 0,
+    IRL_ERR_SHAPE_MISMATCH = 1,             /* irislab::ShapeMismatch            errors.hpp:22 */
+    IRL_ERR_MODULUS_TOO_LARGE = 2,          /* irislab::ModulusTooLarge          errors.hpp:27 */
+    IRL_ERR_ACCUMULATION_OVERFLOW_RISK = 3, /* irislab::AccumulationOverflowRisk errors.hpp:30 */
+    IRL_ERR_NOT_COPRIME = 4,                /* irislab::Error("CRT basis is not coprime") modmat.cpp:184 */
+    IRL_ERR_MODULUS_BUDGET = 5,             /* irislab::ModulusBudget            errors.hpp:52 */
+    IRL_ERR_INVALID_ARGUMENT = 6,
+    IRL_ERR_CUDA = 7,
+    IRL_ERR_NO_DEVICE = 8,
+    IRL_ERR_OUT_OF_MEMORY = 9,
+    IRL_ERR_UNSUPPORTED = 10
+} irl_status;
+
+typedef struct irl_ctx irl_ctx;
+typedef struct irl_ccmm irl_ccmm;
+
+/* ---- context ------------------------------------------------------------ */
+int irl_abi_version(void);
+/* Binds `device`, creates a stream and workspace. IRL_ERR_NO_DEVICE if the
+ * device is absent or not sm_100. */
+int irl_ctx_create(int device, irl_ctx** out);
+int irl_ctx_destroy(irl_ctx* ctx);
+/* Message of the last failed call on this context ("" if none). */
+const char* irl_last_error(const irl_ctx* ctx);
+const char* irl_status_string(int status);
+/* Kernels this context launched since creation (instrumentation). */
+uint64_t irl_kernel_launches(const irl_ctx* ctx);
+/* Stream used by the blocking calls (a cudaStream_t). */
+void* irl_ctx_stream(const irl_ctx* ctx);
+
+/* ---- RNS basis helpers (modmat.cpp:8-63) -------------------------------- */
+/* Primes 127..253 with e = 2 (build_paper_basis, modmat.cpp:37-45). Returns count. */
+size_t irl_paper_basis(uint32_t* primes, uint32_t* exps, size_t cap);
+/* Q = prod p^e, little-endian bytes; returns ceil(log256 Q) (modmat.cpp:219). */
+size_t irl_basis_Q_bytes(const uint32_t* primes, const uint32_t* exps, size_t nmod, uint8_t* out,
+                         size_t cap);
+
+/* ---- blocking host-buffer mirrors of irislab::modmat --------------------- */
+/* digit_decompose (modmat.hpp:72, modmat.cpp:86-106): rows*cols entries. */
+int irl_digit_decompose(irl_ctx* ctx, const int32_t* m, size_t rows, size_t cols, uint32_t p,
+                        int32_t* d0, int32_t* d1);
+/* digit_recompose (modmat.hpp:73, modmat.cpp:108-118). */
+int irl_digit_recompose(irl_ctx* ctx, const int32_t* d0, const int32_t* d1, size_t rows,
+                        size_t cols, uint32_t p, int32_t* out);
+/* small_gemm (modmat.hpp:77, modmat.cpp:120-141): C = A B, int32 accumulate,
+ * same data-dependent AccumulationOverflowRisk precheck. Row-major. */
+int irl_small_gemm(irl_ctx* ctx, const int32_t* a, const int32_t* b, int32_t* c, size_t m,
+                   size_t k, size_t n);
+/* gemm_mod_psq (modmat.hpp:80, modmat.cpp:143-160): C = A B mod p^2 in [0, p^2). */
+int irl_gemm_mod_psq(irl_ctx* ctx, const int32_t* a, const int32_t* b, int32_t* c, size_t m,
+                     size_t k, size_t n, uint32_t p);
+/* gemm_mod_Q (modmat.hpp:83, modmat.cpp:162-195). Entries are `width`-byte
+ * little-endian integers in [0, Q); basis = (primes[i], exps[i]). */
+int irl_gemm_mod_Q(irl_ctx* ctx, const uint8_t* a, const uint8_t* b, uint8_t* c, size_t m,
+                   size_t k, size_t n, size_t width, const uint32_t* primes, const uint32_t* exps,
+                   size_t nmod);
+
+/* ---- device-level building blocks (device pointers, stream-ordered) ------
+ * Digit planes: [nmod][2][rows][ldk] int8, K-major, ldk % 16 == 0, zero
+ * padded for k >= K. Residues: uint16 in [0, m). `stream` is a cudaStream_t
+ * (NULL = the context stream). */
+int irl_split_rows_u16(irl_ctx* ctx, const uint16_t* res, size_t ld_res, size_t plane_stride,
+                       size_t rows, size_t cols, const uint32_t* primes, const uint32_t* exps,
+                       size_t nmod, int8_t* planes, size_t ldk, void* stream);
+/* Transposing split of a K x N residue matrix (reference B layout) into
+ * [nmod][2][N][ldk] planes. */
+int irl_split_cols_u16(irl_ctx* ctx, const uint16_t* res, size_t ld_res, size_t plane_stride,
+                       size_t k, size_t n, const uint32_t* primes, const uint32_t* exps,
+                       size_t nmod, int8_t* planes, size_t ldk, void* stream);
+/* Residue extraction + split of width-byte mod-Q entries (modmat.cpp:168-176
+ * fused with :86-106). transpose=0: rows x cols matrix -> [nmod][2][rows][ldk];
+ * transpose=1: K x N matrix -> [nmod][2][N][ldk]. */
+int irl_split_bigint(irl_ctx* ctx, const uint8_t* entries, size_t width, size_t rows, size_t cols,
+                     int transpose, const uint32_t* primes, const uint32_t* exps, size_t nmod,
+                     int8_t* planes, size_t ldk, void* stream);
+/* Batched PPMM over planes: out[g][i][n][m] = (A_g,i B_i^T) mod p_i^e.
+ * a_planes [parts][nmod][2][M][ldk], b_planes [nmod][2][N][ldk],
+ * out [parts][nmod][N][M]; accumulate=1 adds into out mod p^e. */
+int irl_ppmm_planes(irl_ctx* ctx, const int8_t* a_planes, const int8_t* b_planes, uint16_t* out,
+                    size_t parts, size_t m, size_t n, size_t k, size_t ldk,
+                    const uint32_t* primes, const uint32_t* exps, size_t nmod, int accumulate,
+                    void* stream);
+/* CRT lift (modmat.cpp:178-193): residues [nmod][N][M] -> width-byte entries
+ * of the M x N row-major result mod Q. */
+int irl_crt_lift(irl_ctx* ctx, const uint16_t* res, size_t m, size_t n, uint8_t* out,
+                 size_t width, const uint32_t* primes, const uint32_t* exps, size_t nmod,
+                 void* stream);
+
+/* ---- synthetic inputs (counter-based, identical on host and device) ------ */
+/* residue = floor(hi32(mix64(key ^ mix64(seed))) * m / 2^32),
+ * key = stream<<56 | plane<<48 | row<<24 | col. */
+uint32_t irl_synth_residue(uint64_t seed, uint32_t stream, uint32_t plane, uint32_t row,
+                           uint32_t col, uint32_t m);
+void irl_synth_residues_host(uint64_t seed, uint32_t stream, uint32_t plane, uint32_t row0,
+                             uint32_t nrows, uint32_t col0, uint32_t ncols, uint32_t m,
+                             uint16_t* out);
+
+/* ---- RGSW CCMM engine (caller emulator.cpp:389-447)
+ * A database of `parts` parts (paper layout: part 0 = shared a-part
+ * [A1|A2], parts 1.. = b-part slices [B1|B2]); each part is M x K with
+ * K = d2 + N_qry, stored once as digit planes in HBM. A query batch is the
+ * K x N residue matrix [Bq; Aq] per modulus. One run computes, per part and
+ * modulus, out = [X1|X2] [Bq; Aq] mod p^e — the two PPMMs of that part fused
+ * by K-concatenation — with outputs [parts][nmod][N][M] (column n of part g
+ * is the coefficient vector of the n-th output ciphertext block). */
+int irl_ccmm_create(irl_ctx* ctx, size_t parts, size_t m, size_t k, size_t max_n,
+                    const uint32_t* primes, const uint32_t* exps, size_t nmod, irl_ccmm** out);
+int irl_ccmm_destroy(irl_ccmm* e);
+/* Register part `part` from residues [nmod][M][K] (host or device pointer). */
+int irl_ccmm_load_part(irl_ccmm* e, size_t part, const uint16_t* res, int res_on_device);
+/* Register part `part` from width-byte mod-Q entries [M][K] (host pointer). */
+int irl_ccmm_load_part_bigint(irl_ccmm* e, size_t part, const uint8_t* entries, size_t width);
+/* Fill every part with synthetic residues irl_synth_residue(seed, part, i, row, col, m_i). */
+int irl_ccmm_synth_db(irl_ccmm* e, uint64_t seed);
+/* End-to-end call with HOST buffers: q_res [nmod][K][N] -> out [parts][nmod][N][M].
+ * Copies in, splits, multiplies every part, copies out; blocks. */
+int irl_ccmm_run(irl_ccmm* e, const uint16_t* q_res_host, size_t n, uint16_t* out_host);
+/* Device-resident variant over parts [part0, part0 + nparts): q_res_dev
+ * [nmod][K][N] (split into the engine's query planes unless q_ready != 0),
+ * out_dev [nparts][nmod][N][M]; stream-ordered, does not block. */
+int irl_ccmm_run_device(irl_ccmm* e, const uint16_t* q_res_dev, int q_ready, size_t n,
+                        size_t part0, size_t nparts, uint16_t* out_dev, void* stream);
+/* Bytes of HBM the engine holds (planes + workspace). */
+uint64_t irl_ccmm_device_bytes(const irl_ccmm* e);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* IRL_CAPI_H */

@@ -1,0 +1,222 @@
+"""Generate tests/golden/ fixtures from the UNMODIFIED reference.
+
+Runs the reference hot path (oracle/_ref/libirl_ref.so, built by
+`make -C oracle ref` from /root/reference/proj/src/modmat.cpp and
+iris_core.cpp) on the inputs of the reference's own known-answer tests and
+writes the results as small fixtures, so parity stays pinned on machines
+where /root/reference is absent (the GPU box). Test infrastructure only.
+
+    python oracle/gen_golden.py
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT / "tests"))
+import oracle_lib as ol  # noqa: E402
+
+GOLDEN = ROOT / "tests" / "golden"
+
+
+def ref_call_i32(fn, *args):
+    st = fn(*args)
+    msg = ol.ref().ref_last_error().decode() if st else ""
+    return st, msg
+
+
+def digit_case(p, rows, cols, vals):
+    a = np.array(vals, np.int32).reshape(rows, cols)
+    d0 = np.zeros_like(a)
+    d1 = np.zeros_like(a)
+    st, msg = ref_call_i32(ol.ref().ref_digit_decompose, ol.ptr(a, ol.i32p), rows, cols, p,
+                           ol.ptr(d0, ol.i32p), ol.ptr(d1, ol.i32p))
+    return {"p": p, "rows": rows, "cols": cols, "input": a.ravel().tolist(), "status": st,
+            "message": msg, "d0": d0.ravel().tolist() if st == 0 else None,
+            "d1": d1.ravel().tolist() if st == 0 else None}
+
+
+def small_gemm_case(a, b, note):
+    a = np.ascontiguousarray(a, np.int32)
+    b = np.ascontiguousarray(b, np.int32)
+    m, k = a.shape
+    _, n = b.shape
+    c = np.zeros((m, n), np.int32)
+    st, msg = ref_call_i32(ol.ref().ref_small_gemm, ol.ptr(a, ol.i32p), ol.ptr(b, ol.i32p),
+                           ol.ptr(c, ol.i32p), m, k, n)
+    big = a.size > 4096
+    return {"note": note, "m": m, "k": k, "n": n,
+            "a": None if big else a.ravel().tolist(), "b": None if big else b.ravel().tolist(),
+            "a_fill": int(a.flat[0]) if big else None, "b_fill": int(b.flat[0]) if big else None,
+            "status": st, "message": msg, "c": c.ravel().tolist() if st == 0 else None}
+
+
+def psq_case(a, b, p, note):
+    a = np.ascontiguousarray(a, np.int32)
+    b = np.ascontiguousarray(b, np.int32)
+    m, k = a.shape
+    _, n = b.shape
+    c = np.zeros((m, n), np.int32)
+    st, msg = ref_call_i32(ol.ref().ref_gemm_mod_psq, ol.ptr(a, ol.i32p), ol.ptr(b, ol.i32p),
+                           ol.ptr(c, ol.i32p), m, k, n, p)
+    return {"note": note, "p": p, "m": m, "k": k, "n": n, "a": a.ravel().tolist(),
+            "b": b.ravel().tolist(), "status": st, "message": msg,
+            "c": c.ravel().tolist() if st == 0 else None}
+
+
+def ref_gemm_mod_Q(a_le, b_le, m, k, n, width, primes, exps):
+    c = np.zeros((m * n, width), np.uint8)
+    st = ol.ref().ref_gemm_mod_Q(ol.ptr(a_le, ol.u8p), ol.ptr(b_le, ol.u8p), ol.ptr(c, ol.u8p), m, k,
+                                 n, width, ol.ptr(primes, ol.u32p), ol.ptr(exps, ol.u32p), len(primes))
+    assert st == 0, ol.ref().ref_last_error()
+    return c
+
+
+def main():
+    assert ol.ref_available(), "build the reference first: make -C oracle ref"
+    GOLDEN.mkdir(parents=True, exist_ok=True)
+    R = ol.ref()
+    primes = np.zeros(64, np.uint32)
+    exps = np.zeros(64, np.uint32)
+    n = R.ref_paper_basis(ol.ptr(primes, ol.u32p), ol.ptr(exps, ol.u32p), 64)
+    primes, exps = primes[:n].copy(), exps[:n].copy()
+    qbuf = np.zeros(64, np.uint8)
+    width = R.ref_paper_Q_bytes(ol.ptr(qbuf, ol.u8p), 64)
+    Q = int.from_bytes(bytes(qbuf[:width]), "little")
+    assert Q == ol.basis_Q(primes, exps)
+
+    kat = {"generator": "oracle/gen_golden.py via oracle/_ref (unmodified reference modmat.cpp)"}
+    # test_modmat.cpp:26-53, acceptance.cpp:124-136
+    kat["basis"] = {"primes": primes.tolist(), "exps": exps.tolist(),
+                    "digit_planes": int(R.ref_digit_planes()), "log2_Q": R.ref_log2_Q(),
+                    "capacity": R.ref_max_int8_rns_capacity(),
+                    "pure_planes": int(R.ref_pure_rns_plane_count()), "Q_hex": hex(Q),
+                    "width": int(width)}
+
+    # test_modmat.cpp:55-76
+    rng5 = ol.MT19937_64(5)
+    rnd8 = [int(rng5() % (251 * 251)) for _ in range(64)]
+    rngx = np.random.default_rng(55)
+    kat["digit_decompose"] = [
+        digit_case(127, 1, 1, [0]),
+        digit_case(127, 1, 1, [16128]),
+        digit_case(257, 1, 1, [0]),
+        digit_case(251, 8, 8, rnd8),
+        digit_case(127, 6, 7, rngx.integers(-2**31, 2**31, 42, dtype=np.int64).tolist()),
+        digit_case(3, 4, 4, rngx.integers(-50, 50, 16).tolist()),
+        digit_case(255, 3, 5, rngx.integers(0, 255 * 255, 15).tolist()),
+    ]
+
+    # test_modmat.cpp:79-95
+    k_bad = 1 << 18
+    kat["small_gemm"] = [
+        small_gemm_case(np.array([[1, 0], [0, 1]]), np.array([[3, -4], [5, 6]]), "identity"),
+        small_gemm_case(np.array([[126]]), np.array([[126]]), "126*126"),
+        small_gemm_case(np.full((1, k_bad), 126), np.full((k_bad, 1), 126), "overflow K=2^18"),
+        small_gemm_case(rngx.integers(-1000, 1000, (5, 9)), rngx.integers(-1000, 1000, (9, 4)),
+                        "wide entries"),
+    ]
+
+    # test_modmat.cpp:97-123
+    rng6 = ol.MT19937_64(6)
+    p149 = 149 * 149
+    x = np.array([rng6() % p149 for _ in range(256)], np.int64).reshape(16, 16)
+    y = np.array([rng6() % p149 for _ in range(256)], np.int64).reshape(16, 16)
+    kat["gemm_mod_psq"] = [
+        psq_case(np.eye(2), np.eye(2), 127, "identity"),
+        psq_case(np.array([[300]]), np.array([[500]]), 127, "300*500 mod 127^2"),
+        psq_case(x, y, 149, "random 16x16 p=149 seed 6"),
+        psq_case(rngx.integers(-2**31, 2**31, (7, 33), dtype=np.int64),
+                 rngx.integers(-2**31, 2**31, (33, 5), dtype=np.int64), 251, "negative/wide inputs"),
+        psq_case(rngx.integers(0, 127 * 127, (3, 40)), rngx.integers(0, 127 * 127, (40, 2)), 300,
+                 "p >= 256 -> ModulusTooLarge"),
+    ]
+
+    # test_modmat.cpp:125-145: seed 7 stream; digests of the reference outputs.
+    rng7 = ol.MT19937_64(7)
+    bq = ol.random_big(rng7, 8, 8, Q)
+    cases = []
+    ident = [1 if i == j else 0 for i in range(8) for j in range(8)]
+    zero = [0] * 64
+    for name, av, bv, m, kk, nn in [("identity", ident, bq, 8, 8, 8), ("zero", zero, bq, 8, 8, 8)]:
+        out = ref_gemm_mod_Q(ol.ints_to_le(av, width), ol.ints_to_le(bv, width), m, kk, nn, width,
+                             primes, exps)
+        cases.append({"name": name, "sha256": hashlib.sha256(out.tobytes()).hexdigest()})
+    for it in range(5):
+        xa = ol.random_big(rng7, 32, 32, Q)
+        ya = ol.random_big(rng7, 32, 32, Q)
+        out = ref_gemm_mod_Q(ol.ints_to_le(xa, width), ol.ints_to_le(ya, width), 32, 32, 32, width,
+                             primes, exps)
+        assert ol.le_to_ints(out, width) == ol.schoolbook_mod(xa, ya, 32, 32, 32, Q)
+        cases.append({"name": f"random32 #{it}", "sha256": hashlib.sha256(out.tobytes()).hexdigest()})
+    kat["gemm_mod_Q_seed7"] = cases
+
+    # test_modmat.cpp:147-160: file format bytes for random_big(seed 8, 5x3).
+    rng8 = ol.MT19937_64(8)
+    m8 = ol.random_big(rng8, 5, 3, Q)
+    ent = ol.ints_to_le(m8, width)
+    back = np.zeros_like(ent)
+    path = str(GOLDEN / "_tmp_bigmat.bin")
+    st = R.ref_save_load_roundtrip(path.encode(), ol.ptr(ent, ol.u8p), 5, 3, width,
+                                   ol.ptr(back, ol.u8p))
+    assert st == 0 and (back == ent).all()
+    blob = Path(path).read_bytes()
+    Path(path).unlink()
+    kat["bigmatrix_file"] = {"rows": 5, "cols": 3, "entries_hex": ent.tobytes().hex(),
+                             "file_hex": blob.hex()}
+
+    # emulator ccmm_twin KAT (test_emulator.cpp:215-245): exact values.
+    kat["ccmm_twin"] = {"d1": 4, "d2": 3, "d3": 2, "n_db": 2, "n_qry": 3,
+                        "db": [1, 0, 2, 0, 1, 0, 3, 0, 0, 0, 0, 1], "qry": [1, 2, 3, 4, 5, 6],
+                        "col0": [11, 3, 3, 5], "col1": [14, 4, 6, 6], "outputs": 4}
+    (GOLDEN / "modmat_kats.json").write_text(json.dumps(kat, indent=1))
+
+    # acceptance.cpp:96-120 criterion 2: the exact gmp_randclass(seed 2) stream;
+    # keep the first instances (in stream order) whose total size is small.
+    R.ref_crit2_reset()
+    keep = {}
+    for idx in range(200):
+        m_ = ol.sz()
+        k_ = ol.sz()
+        n_ = ol.sz()
+        abuf = np.zeros((64 * 64, width), np.uint8)
+        bbuf = np.zeros((64 * 64, width), np.uint8)
+        R.ref_crit2_next(m_, k_, n_, ol.ptr(abuf, ol.u8p), ol.ptr(bbuf, ol.u8p), width)
+        m, kk, nn = m_.value, k_.value, n_.value
+        if m * kk + kk * nn + m * nn > 700 or len(keep) // 3 >= 12:
+            continue
+        a = abuf[: m * kk].copy()
+        b = bbuf[: kk * nn].copy()
+        c = ref_gemm_mod_Q(a, b, m, kk, nn, width, primes, exps)
+        c2 = np.zeros_like(c)
+        R.ref_oracle_gemm_mod_Q(ol.ptr(a, ol.u8p), ol.ptr(b, ol.u8p), ol.ptr(c2, ol.u8p), m, kk, nn,
+                                width, ol.ptr(primes, ol.u32p), ol.ptr(exps, ol.u32p), len(primes))
+        assert (c == c2).all()
+        keep[f"i{idx}_a"] = a.reshape(m, kk, width)
+        keep[f"i{idx}_b"] = b.reshape(kk, nn, width)
+        keep[f"i{idx}_c"] = c.reshape(m, nn, width)
+    np.savez_compressed(GOLDEN / "crit2_instances.npz", **keep)
+
+    # iris KAT inputs (iris_core.cpp:92-112 synth_db, :28-35 to_masked, :65-76
+    # rotate) from the reference's own libstdc++ Bernoulli stream.
+    n_db, d, eyes, rho = 96, 256, 2, 31
+    db = np.zeros((n_db, d), np.int8)
+    R.ref_synth_masked(n_db, d, 0.8, 11, ol.ptr(db, ol.i8p))
+    qry = np.zeros((d, eyes * rho), np.int8)
+    for r in range(rho):
+        q = np.zeros((eyes, d), np.int8)
+        R.ref_synth_masked_rotated(eyes, d, 0.8, 12, r, ol.ptr(q, ol.i8p))
+        for e in range(eyes):
+            qry[:, e * rho + r] = q[e]
+    prod = db.astype(np.int64) @ qry.astype(np.int64)
+    np.savez_compressed(GOLDEN / "iris_kat.npz", db=db, qry=qry, prod=prod)
+    print("wrote", sorted(p.name for p in GOLDEN.iterdir()))
+
+
+if __name__ == "__main__":
+    main()

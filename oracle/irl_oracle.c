@@ -1,0 +1,487 @@
+/* irl_oracle.c — CPU restatement of the reference hot path. TEST
+ * INFRASTRUCTURE ONLY (see irl_oracle.h): the product never links this.
+ *
+ * Reference line numbers are relative to /root/reference/proj. Big integers
+ * are little-endian arrays of 32-bit limbs; no GMP. */
+#include "irl_oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+#include <unistd.h>
+
+#include "../include/irl_capi.h"
+
+/* ---------------------------------------------------------------------------
+ * RNS basis — modmat.cpp:8-63
+ * ------------------------------------------------------------------------- */
+
+/* primes_in_range (modmat.cpp:8-21): trial division, n from max(lo,2). */
+size_t orc_primes_in_range(uint32_t lo, uint32_t hi, uint32_t* out, size_t cap) {
+    size_t cnt = 0;
+    for (uint32_t n = lo > 2 ? lo : 2; n <= hi; ++n) {
+        int prime = 1;
+        for (uint32_t q = 2; q * q <= n; ++q) {
+            if (n % q == 0) {
+                prime = 0;
+                break;
+            }
+        }
+        if (prime) {
+            if (out && cnt < cap) out[cnt] = n;
+            ++cnt;
+        }
+    }
+    return cnt;
+}
+
+/* build_paper_basis (modmat.cpp:37-45): every prime 127..253 squared. */
+size_t orc_paper_basis(uint32_t* primes, uint32_t* exps, size_t cap) {
+    uint32_t ps[64];
+    const size_t n = orc_primes_in_range(127, 253, ps, 64);
+    for (size_t i = 0; i < n && i < cap; ++i) {
+        primes[i] = ps[i];
+        exps[i] = 2;
+    }
+    return n;
+}
+
+/* RnsBasis::log2_Q (modmat.cpp:29-35) computes log2 of the exact product
+ * through mpf; the sum of e*log2(p) is the same quantity (test_modmat.cpp:38-40
+ * pins the equality to 1e-9). */
+double orc_log2_Q(const uint32_t* primes, const uint32_t* exps, size_t n) {
+    double s = 0.0;
+    for (size_t i = 0; i < n; ++i) s += (double)exps[i] * log2((double)primes[i]);
+    return s;
+}
+
+/* max_int8_rns_capacity (modmat.cpp:47-59). */
+double orc_max_int8_rns_capacity(void) {
+    uint32_t ps[64];
+    const size_t n = orc_primes_in_range(3, 253, ps, 64);
+    double total = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+        uint32_t e = 0;
+        uint64_t pw = 1;
+        while (pw * ps[i] < 256) {
+            pw *= ps[i];
+            ++e;
+        }
+        total += e * log2((double)ps[i]);
+    }
+    return total;
+}
+
+/* pure_rns_plane_count (modmat.cpp:61-63). */
+size_t orc_pure_rns_plane_count(void) { return orc_primes_in_range(3, 253, NULL, 0); }
+
+/* ---------------------------------------------------------------------------
+ * Little-endian 32-bit-limb big integers
+ * ------------------------------------------------------------------------- */
+
+#define BN_MAX 96
+
+static void bn_from_le(const uint8_t* b, size_t w, uint32_t* x, size_t L) {
+    memset(x, 0, L * sizeof(uint32_t));
+    for (size_t i = 0; i < w && i / 4 < L; ++i) x[i / 4] |= (uint32_t)b[i] << (8 * (i % 4));
+}
+
+static void bn_to_le(const uint32_t* x, size_t L, uint8_t* b, size_t w) {
+    for (size_t i = 0; i < w; ++i) b[i] = i / 4 < L ? (uint8_t)(x[i / 4] >> (8 * (i % 4))) : 0;
+}
+
+static uint32_t bn_mod_small(const uint32_t* x, size_t L, uint32_t m) {
+    uint64_t r = 0;
+    for (size_t i = L; i-- > 0;) r = ((r << 32) | x[i]) % m;
+    return (uint32_t)r;
+}
+
+/* x /= m in place, returns the remainder. */
+static uint32_t bn_divmod_small(uint32_t* x, size_t L, uint32_t m) {
+    uint64_t r = 0;
+    for (size_t i = L; i-- > 0;) {
+        const uint64_t cur = (r << 32) | x[i];
+        x[i] = (uint32_t)(cur / m);
+        r = cur % m;
+    }
+    return (uint32_t)r;
+}
+
+static int bn_cmp(const uint32_t* a, const uint32_t* b, size_t L) {
+    for (size_t i = L; i-- > 0;) {
+        if (a[i] != b[i]) return a[i] < b[i] ? -1 : 1;
+    }
+    return 0;
+}
+
+static uint32_t bn_sub(uint32_t* a, const uint32_t* b, size_t L) {
+    uint64_t borrow = 0;
+    for (size_t i = 0; i < L; ++i) {
+        const uint64_t t = (uint64_t)a[i] - b[i] - borrow;
+        a[i] = (uint32_t)t;
+        borrow = (t >> 63) & 1;
+    }
+    return (uint32_t)borrow;
+}
+
+/* acc += x * s (acc has L limbs; x has Lx <= L limbs). */
+static void bn_addmul_small(uint32_t* acc, size_t L, const uint32_t* x, size_t Lx, uint32_t s) {
+    uint64_t carry = 0;
+    for (size_t i = 0; i < L; ++i) {
+        const uint64_t xi = i < Lx ? x[i] : 0;
+        const uint64_t t = (uint64_t)acc[i] + xi * s + carry;
+        acc[i] = (uint32_t)t;
+        carry = t >> 32;
+        if (i >= Lx && carry == 0) break;
+    }
+}
+
+/* acc (La limbs) += a (L) * b (L). */
+static void bn_addmul(uint32_t* acc, size_t La, const uint32_t* a, const uint32_t* b, size_t L) {
+    for (size_t i = 0; i < L; ++i) {
+        if (a[i] == 0) continue;
+        uint64_t carry = 0;
+        size_t j = 0;
+        for (; j < L; ++j) {
+            const uint64_t t = (uint64_t)acc[i + j] + (uint64_t)a[i] * b[j] + carry;
+            acc[i + j] = (uint32_t)t;
+            carry = t >> 32;
+        }
+        for (size_t t = i + j; carry && t < La; ++t) {
+            const uint64_t s = (uint64_t)acc[t] + carry;
+            acc[t] = (uint32_t)s;
+            carry = s >> 32;
+        }
+    }
+}
+
+/* r (LQ limbs) = x (Lx limbs) mod Q (LQ limbs) by binary long division. */
+static void bn_mod(const uint32_t* x, size_t Lx, const uint32_t* Q, size_t LQ, uint32_t* r) {
+    uint32_t cur[BN_MAX + 1];
+    memset(cur, 0, sizeof(cur));
+    for (size_t bit = Lx * 32; bit-- > 0;) {
+        /* cur = 2 cur + bit */
+        uint32_t c = (x[bit / 32] >> (bit % 32)) & 1u;
+        for (size_t i = 0; i <= LQ; ++i) {
+            const uint32_t nc = cur[i] >> 31;
+            cur[i] = (cur[i] << 1) | c;
+            c = nc;
+        }
+        uint32_t qx[BN_MAX + 1];
+        memcpy(qx, Q, LQ * sizeof(uint32_t));
+        qx[LQ] = 0;
+        if (bn_cmp(cur, qx, LQ + 1) >= 0) bn_sub(cur, qx, LQ + 1);
+    }
+    memcpy(r, cur, LQ * sizeof(uint32_t));
+}
+
+static size_t basis_Q_limbs(const uint32_t* primes, const uint32_t* exps, size_t n, uint32_t* Q) {
+    memset(Q, 0, BN_MAX * sizeof(uint32_t));
+    Q[0] = 1;
+    for (size_t i = 0; i < n; ++i) {
+        for (uint32_t e = 0; e < exps[i]; ++e) {
+            uint32_t tmp[BN_MAX] = {0};
+            bn_addmul_small(tmp, BN_MAX, Q, BN_MAX, primes[i]);
+            memcpy(Q, tmp, sizeof(tmp));
+        }
+    }
+    size_t L = BN_MAX;
+    while (L > 1 && Q[L - 1] == 0) --L;
+    return L;
+}
+
+static size_t bn_byte_width(const uint32_t* x, size_t L) {
+    size_t bits = 0;
+    for (size_t i = L; i-- > 0;) {
+        if (x[i]) {
+            uint32_t v = x[i];
+            size_t b = 0;
+            while (v) {
+                ++b;
+                v >>= 1;
+            }
+            bits = i * 32 + b;
+            break;
+        }
+    }
+    return bits ? (bits + 7) / 8 : 1;
+}
+
+size_t orc_basis_Q_bytes(const uint32_t* primes, const uint32_t* exps, size_t n, uint8_t* out,
+                         size_t cap) {
+    uint32_t Q[BN_MAX];
+    const size_t L = basis_Q_limbs(primes, exps, n, Q);
+    const size_t w = bn_byte_width(Q, L);
+    if (out) bn_to_le(Q, L, out, w < cap ? w : cap);
+    return w;
+}
+
+/* ---------------------------------------------------------------------------
+ * Digits and small GEMMs — modmat.cpp:86-160
+ * ------------------------------------------------------------------------- */
+
+/* digit_decompose (modmat.cpp:86-106). */
+int orc_digit_decompose(const int32_t* m, size_t count, uint32_t p, int32_t* d0, int32_t* d1) {
+    if (p >= 256) return IRL_ERR_MODULUS_TOO_LARGE; /* :87 */
+    const int32_t psq = (int32_t)(p * p);
+    const int32_t half = (int32_t)((p - 1) / 2);
+    for (size_t i = 0; i < count; ++i) {
+        int32_t v = m[i] % psq;
+        if (v < 0) v += psq;
+        int32_t a = v % (int32_t)p;
+        if (a > half) a -= (int32_t)p;
+        int32_t b = ((v - a) / (int32_t)p) % (int32_t)p;
+        if (b > half) b -= (int32_t)p;
+        d0[i] = a;
+        d1[i] = b;
+    }
+    return IRL_OK;
+}
+
+/* digit_recompose (modmat.cpp:108-118). */
+void orc_digit_recompose(const int32_t* d0, const int32_t* d1, size_t count, uint32_t p,
+                         int32_t* out) {
+    const int32_t pp = (int32_t)p, psq = pp * pp;
+    for (size_t i = 0; i < count; ++i) {
+        int32_t v = (d0[i] + pp * d1[i]) % psq;
+        if (v < 0) v += psq;
+        out[i] = v;
+    }
+}
+
+static int64_t max_abs(const int32_t* x, size_t n) {
+    int64_t m = 0;
+    for (size_t i = 0; i < n; ++i) {
+        const int64_t v = x[i] < 0 ? -(int64_t)x[i] : x[i];
+        if (v > m) m = v;
+    }
+    return m;
+}
+
+/* small_gemm (modmat.cpp:120-141): precheck, then i-k-j int32 accumulation
+ * (wrap-free by the precheck). */
+int orc_small_gemm(const int32_t* a, const int32_t* b, int32_t* c, size_t m, size_t k, size_t n,
+                   int64_t* bound) {
+    const int64_t bnd = (int64_t)k * max_abs(a, m * k) * max_abs(b, k * n);
+    if (bound) *bound = bnd;
+    if (bnd >= ((int64_t)1 << 31)) return IRL_ERR_ACCUMULATION_OVERFLOW_RISK;
+    memset(c, 0, m * n * sizeof(int32_t));
+    for (size_t i = 0; i < m; ++i) {
+        int32_t* crow = c + i * n;
+        for (size_t kk = 0; kk < k; ++kk) {
+            const int32_t aik = a[i * k + kk];
+            if (aik == 0) continue;
+            const int32_t* brow = b + kk * n;
+            for (size_t j = 0; j < n; ++j) crow[j] += aik * brow[j];
+        }
+    }
+    return IRL_OK;
+}
+
+/* gemm_mod_psq (modmat.cpp:143-160): A0B0, A0B1, A1B0 then
+ * (t00 + p (t01 + t10)) mod p^2 in int64. */
+int orc_gemm_mod_psq(const int32_t* a, const int32_t* b, int32_t* c, size_t m, size_t k, size_t n,
+                     uint32_t p) {
+    int st = IRL_OK;
+    int32_t *a0 = malloc(m * k * 4 + 1), *a1 = malloc(m * k * 4 + 1);
+    int32_t *b0 = malloc(k * n * 4 + 1), *b1 = malloc(k * n * 4 + 1);
+    int32_t *t00 = malloc(m * n * 4 + 1), *t01 = malloc(m * n * 4 + 1), *t10 = malloc(m * n * 4 + 1);
+    if ((st = orc_digit_decompose(a, m * k, p, a0, a1)) != IRL_OK) goto done;
+    if ((st = orc_digit_decompose(b, k * n, p, b0, b1)) != IRL_OK) goto done;
+    if ((st = orc_small_gemm(a0, b0, t00, m, k, n, NULL)) != IRL_OK) goto done;
+    if ((st = orc_small_gemm(a0, b1, t01, m, k, n, NULL)) != IRL_OK) goto done;
+    if ((st = orc_small_gemm(a1, b0, t10, m, k, n, NULL)) != IRL_OK) goto done;
+    {
+        const int64_t psq = (int64_t)p * p;
+        for (size_t i = 0; i < m * n; ++i) {
+            int64_t v = ((int64_t)t00[i] + (int64_t)p * ((int64_t)t01[i] + t10[i])) % psq;
+            if (v < 0) v += psq;
+            c[i] = (int32_t)v;
+        }
+    }
+done:
+    free(a0);
+    free(a1);
+    free(b0);
+    free(b1);
+    free(t00);
+    free(t01);
+    free(t10);
+    return st;
+}
+
+/* ---------------------------------------------------------------------------
+ * mod-Q path — modmat.cpp:162-212
+ * ------------------------------------------------------------------------- */
+
+static uint32_t inv_mod(uint32_t a, uint32_t m, int* ok) {
+    int64_t t = 0, nt = 1, r = m, nr = a % m;
+    while (nr) {
+        const int64_t q = r / nr, tt = t - q * nt, rr = r - q * nr;
+        t = nt;
+        nt = tt;
+        r = nr;
+        nr = rr;
+    }
+    *ok = (r == 1) || (m == 1);
+    if (t < 0) t += m;
+    return (uint32_t)t;
+}
+
+/* gemm_mod_Q (modmat.cpp:162-195): per modulus (in basis order) residues
+ * via x mod m (:168-176), gemm_mod_psq or small_gemm (:177-178), CRT lift
+ * c += (Q/m) * ((Q/m)^-1 r mod m) (:180-191), final reduce (:193). */
+int orc_gemm_mod_Q(const uint8_t* a, const uint8_t* b, uint8_t* c, size_t m, size_t k, size_t n,
+                   size_t width, const uint32_t* primes, const uint32_t* exps, size_t nmod) {
+    uint32_t Q[BN_MAX];
+    const size_t LQ = basis_Q_limbs(primes, exps, nmod, Q);
+    const size_t Lw = (width + 3) / 4 > LQ ? (width + 3) / 4 : LQ;
+    const size_t Lc = LQ + 2;
+    int st = IRL_OK;
+    uint32_t* A = calloc(m * k * Lw + 1, 4);
+    uint32_t* B = calloc(k * n * Lw + 1, 4);
+    uint32_t* C = calloc(m * n * Lc + 1, 4);
+    int32_t* ra = malloc(m * k * 4 + 1);
+    int32_t* rb = malloc(k * n * 4 + 1);
+    int32_t* rc = malloc(m * n * 4 + 1);
+    for (size_t i = 0; i < m * k; ++i) bn_from_le(a + i * width, width, A + i * Lw, Lw);
+    for (size_t i = 0; i < k * n; ++i) bn_from_le(b + i * width, width, B + i * Lw, Lw);
+    for (size_t t = 0; t < nmod; ++t) {
+        const uint32_t mod = exps[t] == 2 ? primes[t] * primes[t] : primes[t];
+        for (size_t i = 0; i < m * k; ++i) ra[i] = (int32_t)bn_mod_small(A + i * Lw, Lw, mod);
+        for (size_t i = 0; i < k * n; ++i) rb[i] = (int32_t)bn_mod_small(B + i * Lw, Lw, mod);
+        st = exps[t] == 2 ? orc_gemm_mod_psq(ra, rb, rc, m, k, n, primes[t])
+                          : orc_small_gemm(ra, rb, rc, m, k, n, NULL);
+        if (st != IRL_OK) goto done;
+        uint32_t qi[BN_MAX];
+        memcpy(qi, Q, sizeof(qi));
+        bn_divmod_small(qi, LQ, mod);
+        int ok = 0;
+        const uint32_t inv = inv_mod(bn_mod_small(qi, LQ, mod), mod, &ok);
+        if (!ok) {
+            st = IRL_ERR_NOT_COPRIME;
+            goto done;
+        }
+        for (size_t i = 0; i < m * n; ++i) {
+            uint64_t r = (uint64_t)(uint32_t)rc[i] % mod;
+            r = (r * inv) % mod;
+            bn_addmul_small(C + i * Lc, Lc, qi, LQ, (uint32_t)r);
+        }
+    }
+    for (size_t i = 0; i < m * n; ++i) {
+        uint32_t r[BN_MAX];
+        bn_mod(C + i * Lc, Lc, Q, LQ, r);
+        bn_to_le(r, LQ, c + i * width, width);
+    }
+done:
+    free(A);
+    free(B);
+    free(C);
+    free(ra);
+    free(rb);
+    free(rc);
+    return st;
+}
+
+/* oracle_gemm_mod_Q (modmat.cpp:197-212): schoolbook sum then mod Q. */
+int orc_oracle_gemm_mod_Q(const uint8_t* a, const uint8_t* b, uint8_t* c, size_t m, size_t k,
+                          size_t n, size_t width, const uint32_t* primes, const uint32_t* exps,
+                          size_t nmod) {
+    uint32_t Q[BN_MAX];
+    const size_t LQ = basis_Q_limbs(primes, exps, nmod, Q);
+    const size_t Lw = (width + 3) / 4 > LQ ? (width + 3) / 4 : LQ;
+    const size_t La = 2 * Lw + 2;
+    if (La > BN_MAX) return IRL_ERR_INVALID_ARGUMENT;
+    uint32_t* A = calloc(m * k * Lw + 1, 4);
+    uint32_t* B = calloc(k * n * Lw + 1, 4);
+    for (size_t i = 0; i < m * k; ++i) bn_from_le(a + i * width, width, A + i * Lw, Lw);
+    for (size_t i = 0; i < k * n; ++i) bn_from_le(b + i * width, width, B + i * Lw, Lw);
+    for (size_t i = 0; i < m; ++i) {
+        for (size_t j = 0; j < n; ++j) {
+            uint32_t acc[BN_MAX];
+            memset(acc, 0, sizeof(acc));
+            for (size_t kk = 0; kk < k; ++kk) bn_addmul(acc, La, A + (i * k + kk) * Lw, B + (kk * n + j) * Lw, Lw);
+            uint32_t r[BN_MAX];
+            bn_mod(acc, La, Q, LQ, r);
+            bn_to_le(r, LQ, c + (i * n + j) * width, width);
+        }
+    }
+    free(A);
+    free(B);
+    return IRL_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * PPMM over residues (CCMM building block)
+ * ------------------------------------------------------------------------- */
+
+struct ppmm_job {
+    const uint16_t *a, *bt;
+    size_t lda, ldb, nrows, N, K;
+    const uint32_t* rows;
+    uint32_t m;
+    uint16_t* out;
+    size_t next; /* shared work counter (guarded by mu) */
+    pthread_mutex_t mu;
+};
+
+static void* ppmm_worker(void* arg) {
+    struct ppmm_job* j = (struct ppmm_job*)arg;
+    for (;;) {
+        pthread_mutex_lock(&j->mu);
+        const size_t ri = j->next++;
+        pthread_mutex_unlock(&j->mu);
+        if (ri >= j->nrows) break;
+        const uint16_t* ar = j->a + (size_t)j->rows[ri] * j->lda;
+        for (size_t nn = 0; nn < j->N; ++nn) {
+            const uint16_t* br = j->bt + nn * j->ldb;
+            uint64_t acc = 0;
+            for (size_t kk = 0; kk < j->K; ++kk) acc += (uint64_t)ar[kk] * br[kk];
+            j->out[ri * j->N + nn] = (uint16_t)(acc % j->m);
+        }
+    }
+    return NULL;
+}
+
+/* Schoolbook: every product < 2^32, K < 2^31 terms fit uint64. Rows are
+ * spread over the host cores with pthreads. */
+void orc_ppmm_rows_direct(const uint16_t* a, size_t lda, const uint16_t* bt, size_t ldb,
+                          const uint32_t* rows, size_t nrows, size_t N, size_t K, uint32_t m,
+                          uint16_t* out) {
+    struct ppmm_job j = {a, bt, lda, ldb, nrows, N, K, rows, m, out, 0, PTHREAD_MUTEX_INITIALIZER};
+    long nt = sysconf(_SC_NPROCESSORS_ONLN);
+    if (nt < 1) nt = 1;
+    if ((size_t)nt > nrows) nt = (long)(nrows ? nrows : 1);
+    pthread_t th[256];
+    if (nt > 256) nt = 256;
+    for (long t = 0; t < nt; ++t) pthread_create(&th[t], NULL, ppmm_worker, &j);
+    for (long t = 0; t < nt; ++t) pthread_join(th[t], NULL);
+}
+
+/* ---------------------------------------------------------------------------
+ * Counter-based synthetic residues
+ * ------------------------------------------------------------------------- */
+
+static uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+uint32_t orc_synth_residue(uint64_t seed, uint32_t stream, uint32_t plane, uint32_t row,
+                           uint32_t col, uint32_t m) {
+    const uint64_t key = ((uint64_t)(stream & 0xFF) << 56) | ((uint64_t)(plane & 0xFF) << 48) |
+                         ((uint64_t)(row & 0xFFFFFF) << 24) | (uint64_t)(col & 0xFFFFFF);
+    const uint64_t x = mix64(key ^ mix64(seed));
+    return (uint32_t)(((x >> 32) * (uint64_t)m) >> 32);
+}
+
+void orc_synth_block(uint64_t seed, uint32_t stream, uint32_t plane, uint32_t row0,
+                     uint32_t nrows, uint32_t col0, uint32_t ncols, uint32_t m, uint16_t* out) {
+    for (uint32_t r = 0; r < nrows; ++r)
+        for (uint32_t c = 0; c < ncols; ++c)
+            out[(size_t)r * ncols + c] =
+                (uint16_t)orc_synth_residue(seed, stream, plane, row0 + r, col0 + c, m);
+}

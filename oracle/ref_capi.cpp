@@ -1,0 +1,306 @@
+// extern "C" wrappers around the UNMODIFIED reference hot path
+// (/root/reference/proj/src/modmat.cpp, iris_core.cpp), compiled together
+// into oracle/_ref/libirl_ref.so by oracle/Makefile. TEST INFRASTRUCTURE:
+// used by tests/ (parity pinning, golden-vector generation) and by bench.py's
+// CPU-baseline / --impl reference leg. Never linked by the product.
+//
+// Big matrices cross this boundary as fixed-width little-endian entries
+// (the reference's own file format, modmat.cpp:216-231).
+#include <cstdint>
+#include <atomic>
+#include <cstring>
+#include <exception>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "irislab/errors.hpp"
+#include "irislab/iris_core.hpp"
+#include "irislab/modmat.hpp"
+
+using namespace irislab;
+using modmat::BigMatrix;
+using modmat::SmallMatrix;
+
+namespace {
+
+thread_local std::string g_err;
+
+int map_exception() {
+    try {
+        throw;
+    } catch (const ShapeMismatch& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const ModulusTooLarge& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const AccumulationOverflowRisk& e) {
+        g_err = e.what();
+        return 3;
+    } catch (const ModulusBudget& e) {
+        g_err = e.what();
+        return 5;
+    } catch (const Error& e) {
+        g_err = e.what();
+        return std::string(e.what()).find("coprime") != std::string::npos ? 4 : 6;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 6;
+    }
+}
+
+SmallMatrix to_small(const int32_t* p, size_t r, size_t c) {
+    SmallMatrix m{r, c, std::vector<int32_t>(r * c)};
+    if (r * c) std::memcpy(m.a.data(), p, r * c * 4);
+    return m;
+}
+
+void to_big(BigMatrix& m, const uint8_t* p, size_t width) {
+    for (size_t i = 0; i < m.a.size(); ++i)
+        mpz_import(m.a[i].get_mpz_t(), width, -1, 1, -1, 0, p + i * width);
+}
+
+void from_big(const BigMatrix& m, uint8_t* p, size_t width) {
+    for (size_t i = 0; i < m.a.size(); ++i) {
+        std::memset(p + i * width, 0, width);
+        size_t count = 0;
+        mpz_export(p + i * width, &count, -1, 1, -1, 0, m.a[i].get_mpz_t());
+    }
+}
+
+modmat::RnsBasis make_basis(const uint32_t* primes, const uint32_t* exps, size_t n) {
+    modmat::RnsBasis b;
+    b.Q = 1;
+    for (size_t i = 0; i < n; ++i) {
+        b.moduli.push_back({primes[i], exps[i]});
+        b.Q *= mpz_class(b.moduli.back().value());
+    }
+    return b;
+}
+
+// Acceptance criterion 2 stream (acceptance.cpp:96-120), replayed.
+struct Crit2 {
+    modmat::RnsBasis basis = modmat::build_paper_basis();
+    gmp_randclass rng{gmp_randinit_default};
+    std::mt19937_64 dims{2};
+    std::uniform_int_distribution<int> dim{1, 64};
+    Crit2() { rng.seed(2); }
+};
+Crit2* g_crit2 = nullptr;
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+size_t ref_paper_basis(uint32_t* primes, uint32_t* exps, size_t cap) {
+    auto b = modmat::build_paper_basis();
+    for (size_t i = 0; i < b.moduli.size() && i < cap; ++i) {
+        primes[i] = b.moduli[i].p;
+        exps[i] = b.moduli[i].e;
+    }
+    return b.moduli.size();
+}
+size_t ref_digit_planes() { return modmat::build_paper_basis().digit_planes(); }
+double ref_log2_Q() { return modmat::build_paper_basis().log2_Q(); }
+double ref_max_int8_rns_capacity() { return modmat::max_int8_rns_capacity(); }
+size_t ref_pure_rns_plane_count() { return modmat::pure_rns_plane_count(); }
+size_t ref_paper_Q_bytes(uint8_t* out, size_t cap) {
+    auto b = modmat::build_paper_basis();
+    const size_t w = (mpz_sizeinbase(b.Q.get_mpz_t(), 2) + 7) / 8;
+    if (out && cap >= w) {
+        size_t count = 0;
+        std::memset(out, 0, w);
+        mpz_export(out, &count, -1, 1, -1, 0, b.Q.get_mpz_t());
+    }
+    return w;
+}
+
+int ref_digit_decompose(const int32_t* m, size_t rows, size_t cols, uint32_t p, int32_t* d0,
+                        int32_t* d1) {
+    try {
+        auto d = modmat::digit_decompose(to_small(m, rows, cols), p);
+        if (rows * cols) {
+            std::memcpy(d0, d.m0.a.data(), rows * cols * 4);
+            std::memcpy(d1, d.m1.a.data(), rows * cols * 4);
+        }
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+int ref_digit_recompose(const int32_t* d0, const int32_t* d1, size_t rows, size_t cols,
+                        uint32_t p, int32_t* out) {
+    try {
+        modmat::DigitMatrices d{p, to_small(d0, rows, cols), to_small(d1, rows, cols)};
+        auto m = modmat::digit_recompose(d);
+        if (rows * cols) std::memcpy(out, m.a.data(), rows * cols * 4);
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+int ref_small_gemm(const int32_t* a, const int32_t* b, int32_t* c, size_t m, size_t k, size_t n) {
+    try {
+        auto r = modmat::small_gemm(to_small(a, m, k), to_small(b, k, n));
+        if (m * n) std::memcpy(c, r.a.data(), m * n * 4);
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+int ref_gemm_mod_psq(const int32_t* a, const int32_t* b, int32_t* c, size_t m, size_t k, size_t n,
+                     uint32_t p) {
+    try {
+        auto r = modmat::gemm_mod_psq(to_small(a, m, k), to_small(b, k, n), p);
+        if (m * n) std::memcpy(c, r.a.data(), m * n * 4);
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// Multi-threaded driver for the CPU baseline: independent gemm_mod_psq calls
+// (one per task), each task = (a_i, b_i, c_i, p_i); the function is pure
+// (SPEC.md:214-215), so tasks run on `threads` host threads.
+int ref_gemm_mod_psq_batch(const int32_t* const* a, const int32_t* const* b, int32_t* const* c,
+                           const uint32_t* p, size_t ntasks, size_t m, size_t k, size_t n,
+                           int threads) {
+    std::vector<int> st(ntasks, 0);
+    std::vector<std::thread> pool;
+    std::atomic<size_t> next{0};
+    const int nt = threads > 0 ? threads : 1;
+    for (int t = 0; t < nt; ++t) {
+        pool.emplace_back([&] {
+            for (size_t i; (i = next.fetch_add(1)) < ntasks;) {
+                st[i] = ref_gemm_mod_psq(a[i], b[i], c[i], m, k, n, p[i]);
+            }
+        });
+    }
+    for (auto& th : pool) th.join();
+    for (int s : st)
+        if (s) return s;
+    return 0;
+}
+
+int ref_gemm_mod_Q(const uint8_t* a, const uint8_t* b, uint8_t* c, size_t m, size_t k, size_t n,
+                   size_t width, const uint32_t* primes, const uint32_t* exps, size_t nmod) {
+    try {
+        auto basis = make_basis(primes, exps, nmod);
+        BigMatrix A = BigMatrix::zeros(m, k), B = BigMatrix::zeros(k, n);
+        to_big(A, a, width);
+        to_big(B, b, width);
+        auto C = modmat::gemm_mod_Q(A, B, basis);
+        from_big(C, c, width);
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+int ref_oracle_gemm_mod_Q(const uint8_t* a, const uint8_t* b, uint8_t* c, size_t m, size_t k,
+                          size_t n, size_t width, const uint32_t* primes, const uint32_t* exps,
+                          size_t nmod) {
+    try {
+        auto basis = make_basis(primes, exps, nmod);
+        BigMatrix A = BigMatrix::zeros(m, k), B = BigMatrix::zeros(k, n);
+        to_big(A, a, width);
+        to_big(B, b, width);
+        auto C = modmat::oracle_gemm_mod_Q(A, B, basis.Q);
+        from_big(C, c, width);
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// Replays acceptance criterion 2's input stream. ref_crit2_reset() then
+// repeated ref_crit2_next(): writes dims, then (if buffers are large enough:
+// 64*64*width each) the entries of A (m x k) and B (k x n).
+void ref_crit2_reset() {
+    delete g_crit2;
+    g_crit2 = new Crit2();
+}
+int ref_crit2_next(size_t* m, size_t* k, size_t* n, uint8_t* a, uint8_t* b, size_t width) {
+    if (!g_crit2) ref_crit2_reset();
+    Crit2& s = *g_crit2;
+    *m = static_cast<size_t>(s.dim(s.dims));
+    *k = static_cast<size_t>(s.dim(s.dims));
+    *n = static_cast<size_t>(s.dim(s.dims));
+    BigMatrix A = BigMatrix::zeros(*m, *k), B = BigMatrix::zeros(*k, *n);
+    for (auto& v : A.a) v = s.rng.get_z_range(s.basis.Q);
+    for (auto& v : B.a) v = s.rng.get_z_range(s.basis.Q);
+    from_big(A, a, width);
+    from_big(B, b, width);
+    return 0;
+}
+
+// test_modmat.cpp:12-22 random_big with mt19937_64(seed): rows*cols entries.
+void ref_random_big(uint64_t seed, size_t skip, size_t rows, size_t cols, uint8_t* out,
+                    size_t width) {
+    auto basis = modmat::build_paper_basis();
+    std::mt19937_64 rng(seed);
+    for (size_t s = 0; s < skip; ++s) rng();
+    BigMatrix m = BigMatrix::zeros(rows, cols);
+    for (auto& v : m.a) {
+        mpz_class x = 0;
+        for (int w = 0; w < 6; ++w)
+            x = (x << 32) + static_cast<unsigned long>(rng() & 0xffffffffULL);
+        v = x % basis.Q;
+    }
+    from_big(m, out, width);
+}
+
+int ref_save_load_roundtrip(const char* path, const uint8_t* entries, size_t rows, size_t cols,
+                            size_t width, uint8_t* back) {
+    try {
+        auto basis = modmat::build_paper_basis();
+        BigMatrix m = BigMatrix::zeros(rows, cols);
+        to_big(m, entries, width);
+        modmat::save_big_matrix(path, m, basis.Q);
+        mpz_class q;
+        auto r = modmat::load_big_matrix(path, &q);
+        from_big(r, back, width);
+        return q == basis.Q ? 0 : 6;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// iris_core.cpp:92-112 synth_db + :28-35 to_masked: ternary values
+// out[t*d + i] in {-1, 0, 1} for n templates of dimension d.
+int ref_synth_masked(size_t n, size_t d, double mask_density, uint64_t seed, int8_t* out) {
+    try {
+        auto db = iris::synth_db(n, d, mask_density, seed);
+        for (size_t t = 0; t < n; ++t) {
+            auto mv = iris::to_masked(db[t]);
+            std::memcpy(out + t * d, mv.values.data(), d);
+        }
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// iris_core.cpp:65-76 rotate followed by to_masked.
+int ref_synth_masked_rotated(size_t n, size_t d, double mask_density, uint64_t seed, size_t rot,
+                             int8_t* out) {
+    try {
+        auto db = iris::synth_db(n, d, mask_density, seed);
+        for (size_t t = 0; t < n; ++t) {
+            auto mv = iris::to_masked(iris::rotate(db[t], rot));
+            std::memcpy(out + t * d, mv.values.data(), d);
+        }
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+}  // extern "C"

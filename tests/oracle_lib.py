@@ -1,0 +1,227 @@
+"""ctypes bindings for the TEST oracle (oracle/libirl_oracle.so) and, when it
+was built in this container, the unmodified reference (oracle/_ref/libirl_ref.so).
+
+Test infrastructure only: the product package never imports this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+ORACLE_SO = ROOT / "oracle" / "libirl_oracle.so"
+REF_SO = ROOT / "oracle" / "_ref" / "libirl_ref.so"
+
+M64 = (1 << 64) - 1
+
+u8p = C.POINTER(C.c_uint8)
+i8p = C.POINTER(C.c_int8)
+u16p = C.POINTER(C.c_uint16)
+i32p = C.POINTER(C.c_int32)
+u32p = C.POINTER(C.c_uint32)
+i64p = C.POINTER(C.c_int64)
+sz = C.c_size_t
+
+
+def ptr(a: np.ndarray, t):
+    return a.ctypes.data_as(t)
+
+
+_oracle = None
+_ref = None
+
+
+def oracle() -> C.CDLL:
+    global _oracle
+    if _oracle is None:
+        if not ORACLE_SO.exists():
+            subprocess.run(["make", "-s", "-C", str(ROOT / "oracle")], check=True)
+        lib = C.CDLL(str(ORACLE_SO))
+        lib.orc_primes_in_range.restype = sz
+        lib.orc_primes_in_range.argtypes = [C.c_uint32, C.c_uint32, u32p, sz]
+        lib.orc_paper_basis.restype = sz
+        lib.orc_paper_basis.argtypes = [u32p, u32p, sz]
+        lib.orc_log2_Q.restype = C.c_double
+        lib.orc_log2_Q.argtypes = [u32p, u32p, sz]
+        lib.orc_max_int8_rns_capacity.restype = C.c_double
+        lib.orc_pure_rns_plane_count.restype = sz
+        lib.orc_basis_Q_bytes.restype = sz
+        lib.orc_basis_Q_bytes.argtypes = [u32p, u32p, sz, u8p, sz]
+        lib.orc_digit_decompose.argtypes = [i32p, sz, C.c_uint32, i32p, i32p]
+        lib.orc_digit_recompose.argtypes = [i32p, i32p, sz, C.c_uint32, i32p]
+        lib.orc_small_gemm.argtypes = [i32p, i32p, i32p, sz, sz, sz, i64p]
+        lib.orc_gemm_mod_psq.argtypes = [i32p, i32p, i32p, sz, sz, sz, C.c_uint32]
+        lib.orc_gemm_mod_Q.argtypes = [u8p, u8p, u8p, sz, sz, sz, sz, u32p, u32p, sz]
+        lib.orc_oracle_gemm_mod_Q.argtypes = [u8p, u8p, u8p, sz, sz, sz, sz, u32p, u32p, sz]
+        lib.orc_ppmm_rows_direct.argtypes = [u16p, sz, u16p, sz, u32p, sz, sz, sz, C.c_uint32, u16p]
+        lib.orc_synth_residue.restype = C.c_uint32
+        lib.orc_synth_residue.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]
+        lib.orc_synth_block.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                        C.c_uint32, C.c_uint32, C.c_uint32, u16p]
+        _oracle = lib
+    return _oracle
+
+
+def ref_available() -> bool:
+    return REF_SO.exists()
+
+
+def ref() -> C.CDLL:
+    global _ref
+    if _ref is None:
+        lib = C.CDLL(str(REF_SO))
+        lib.ref_last_error.restype = C.c_char_p
+        lib.ref_paper_basis.restype = sz
+        lib.ref_paper_basis.argtypes = [u32p, u32p, sz]
+        lib.ref_digit_planes.restype = sz
+        lib.ref_log2_Q.restype = C.c_double
+        lib.ref_max_int8_rns_capacity.restype = C.c_double
+        lib.ref_pure_rns_plane_count.restype = sz
+        lib.ref_paper_Q_bytes.restype = sz
+        lib.ref_paper_Q_bytes.argtypes = [u8p, sz]
+        lib.ref_digit_decompose.argtypes = [i32p, sz, sz, C.c_uint32, i32p, i32p]
+        lib.ref_digit_recompose.argtypes = [i32p, i32p, sz, sz, C.c_uint32, i32p]
+        lib.ref_small_gemm.argtypes = [i32p, i32p, i32p, sz, sz, sz]
+        lib.ref_gemm_mod_psq.argtypes = [i32p, i32p, i32p, sz, sz, sz, C.c_uint32]
+        lib.ref_gemm_mod_psq_batch.argtypes = [C.POINTER(i32p), C.POINTER(i32p), C.POINTER(i32p), u32p,
+                                               sz, sz, sz, sz, C.c_int]
+        lib.ref_gemm_mod_Q.argtypes = [u8p, u8p, u8p, sz, sz, sz, sz, u32p, u32p, sz]
+        lib.ref_oracle_gemm_mod_Q.argtypes = [u8p, u8p, u8p, sz, sz, sz, sz, u32p, u32p, sz]
+        lib.ref_crit2_next.argtypes = [C.POINTER(sz), C.POINTER(sz), C.POINTER(sz), u8p, u8p, sz]
+        lib.ref_random_big.argtypes = [C.c_uint64, sz, sz, sz, u8p, sz]
+        lib.ref_save_load_roundtrip.argtypes = [C.c_char_p, u8p, sz, sz, sz, u8p]
+        lib.ref_synth_masked.argtypes = [sz, sz, C.c_double, C.c_uint64, i8p]
+        lib.ref_synth_masked_rotated.argtypes = [sz, sz, C.c_double, C.c_uint64, sz, i8p]
+        _ref = lib
+    return _ref
+
+
+# --------------------------------------------------------------------------
+# Basis and big-integer helpers (Python ints)
+# --------------------------------------------------------------------------
+
+def paper_basis():
+    p = np.zeros(64, np.uint32)
+    e = np.zeros(64, np.uint32)
+    n = oracle().orc_paper_basis(ptr(p, u32p), ptr(e, u32p), 64)
+    return p[:n].copy(), e[:n].copy()
+
+
+def basis_Q(primes, exps) -> int:
+    q = 1
+    for p, e in zip(primes, exps):
+        q *= int(p) ** int(e)
+    return q
+
+
+def width_of(Q: int) -> int:
+    return (Q.bit_length() + 7) // 8
+
+
+def ints_to_le(vals, width: int) -> np.ndarray:
+    out = np.zeros((len(vals), width), np.uint8)
+    for i, v in enumerate(vals):
+        out[i] = np.frombuffer(int(v).to_bytes(width, "little"), np.uint8)
+    return out
+
+
+def le_to_ints(arr: np.ndarray, width: int):
+    flat = np.ascontiguousarray(arr).reshape(-1, width)
+    return [int.from_bytes(bytes(row), "little") for row in flat]
+
+
+class MT19937_64:
+    """std::mt19937_64 (used by the reference tests' generators)."""
+
+    def __init__(self, seed: int):
+        self.mt = [0] * 312
+        self.mt[0] = seed & M64
+        for i in range(1, 312):
+            prev = self.mt[i - 1]
+            self.mt[i] = (6364136223846793005 * (prev ^ (prev >> 62)) + i) & M64
+        self.idx = 312
+
+    def _twist(self):
+        mt = self.mt
+        for i in range(312):
+            x = (mt[i] & 0xFFFFFFFF80000000) | (mt[(i + 1) % 312] & 0x7FFFFFFF)
+            xa = x >> 1
+            if x & 1:
+                xa ^= 0xB5026F5AA96619E9
+            mt[i] = mt[(i + 156) % 312] ^ xa
+        self.idx = 0
+
+    def __call__(self) -> int:
+        if self.idx >= 312:
+            self._twist()
+        y = self.mt[self.idx]
+        self.idx += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEDA60000
+        y ^= (y << 37) & 0xFFF7EEE000000000
+        y ^= y >> 43
+        return y & M64
+
+
+def random_big(rng: MT19937_64, rows: int, cols: int, Q: int):
+    """tests/test_modmat.cpp:12-22: six 32-bit words, big-endian concat, mod Q."""
+    out = []
+    for _ in range(rows * cols):
+        x = 0
+        for _w in range(6):
+            x = (x << 32) + (rng() & 0xFFFFFFFF)
+        out.append(x % Q)
+    return out
+
+
+def schoolbook_mod(a, b, m, k, n, Q):
+    """Arbitrary-precision reference product (oracle_gemm_mod_Q semantics)."""
+    out = []
+    for i in range(m):
+        for j in range(n):
+            out.append(sum(a[i * k + t] * b[t * n + j] for t in range(k)) % Q)
+    return out
+
+
+# --------------------------------------------------------------------------
+# Oracle wrappers (numpy in/out)
+# --------------------------------------------------------------------------
+
+def orc_gemm_mod_psq(a: np.ndarray, b: np.ndarray, p: int):
+    a = np.ascontiguousarray(a, np.int32)
+    b = np.ascontiguousarray(b, np.int32)
+    m, k = a.shape
+    k2, n = b.shape
+    assert k == k2
+    c = np.zeros((m, n), np.int32)
+    st = oracle().orc_gemm_mod_psq(ptr(a, i32p), ptr(b, i32p), ptr(c, i32p), m, k, n, p)
+    return st, c
+
+
+def orc_gemm_mod_Q(a_le, b_le, m, k, n, width, primes, exps):
+    c = np.zeros((m * n, width), np.uint8)
+    st = oracle().orc_gemm_mod_Q(ptr(a_le, u8p), ptr(b_le, u8p), ptr(c, u8p), m, k, n, width,
+                                 ptr(primes, u32p), ptr(exps, u32p), len(primes))
+    return st, c
+
+
+def synth_block(seed, stream, plane, row0, nrows, col0, ncols, m):
+    out = np.zeros((nrows, ncols), np.uint16)
+    oracle().orc_synth_block(seed, stream, plane, row0, nrows, col0, ncols, m, ptr(out, u16p))
+    return out
+
+
+def ppmm_rows_direct(a: np.ndarray, bt: np.ndarray, rows, m: int):
+    """a [R][K] uint16, bt [N][K] uint16 -> out [len(rows)][N] = a[rows] bt^T mod m."""
+    a = np.ascontiguousarray(a, np.uint16)
+    bt = np.ascontiguousarray(bt, np.uint16)
+    rows = np.ascontiguousarray(rows, np.uint32)
+    N, K = bt.shape
+    out = np.zeros((len(rows), N), np.uint16)
+    oracle().orc_ppmm_rows_direct(ptr(a, u16p), a.shape[1], ptr(bt, u16p), K, ptr(rows, u32p),
+                                  len(rows), N, K, m, ptr(out, u16p))
+    return out
