@@ -1,0 +1,91 @@
+"""In-tree build of the B200 engine: nvcc for sm_100a -> libirl_b200.so.
+
+    python -m paper_2601_17561_b200.build [--debug]
+
+The shared library is written next to this file so it ships with the repo
+snapshot to the GPU box. Objects go to build/ at the repo root.
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+HOST = PKG / "host"
+OUT = PKG / "libirl_b200.so"
+BUILD = ROOT / "build"
+
+CUDA_SOURCES = ["ppmm_gemm.cu", "kernels_aux.cu", "capi.cu"]
+HOST_SOURCES = ["modmat_b200.cpp"]
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if cand and Path(cand).exists():
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def _host_cxx() -> str:
+    # /usr/bin/g++ links the shared libstdc++ the Python process already uses.
+    return "/usr/bin/g++" if Path("/usr/bin/g++").exists() else (shutil.which("g++") or "g++")
+
+
+def _compile(cmd):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("build failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)
+    return r.stderr
+
+
+def build(debug: bool = False, verbose: bool = False) -> Path:
+    BUILD.mkdir(exist_ok=True)
+    nvcc = _nvcc()
+    cxx = _host_cxx()
+    common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-ccbin", cxx,
+              f"-I{ROOT / 'include'}", f"-I{CSRC}", f"-I{HOST}"]
+    if debug:
+        common.append("-DIRL_WAIT_TIMEOUT")
+    jobs = []
+    objs = []
+    for src in CUDA_SOURCES:
+        obj = BUILD / (Path(src).stem + ".o")
+        objs.append(obj)
+        jobs.append([nvcc, *ARCH, *common, "-Xptxas", "-v", "-c", str(CSRC / src), "-o", str(obj)])
+    for src in HOST_SOURCES:
+        if not (HOST / src).exists():
+            continue
+        obj = BUILD / (Path(src).stem + ".o")
+        objs.append(obj)
+        jobs.append([cxx, "-O2", "-std=c++17", "-fPIC", f"-I{ROOT / 'include'}", f"-I{HOST}",
+                     "-I/usr/local/cuda/include", "-c", str(HOST / src), "-o", str(obj)])
+    with cf.ThreadPoolExecutor(max_workers=len(jobs)) as ex:
+        logs = list(ex.map(_compile, jobs))
+    if verbose:
+        for log in logs:
+            sys.stderr.write(log)
+    link = [nvcc, *ARCH, "-shared", "-ccbin", cxx, "-o", str(OUT), *map(str, objs), "-lcudart_static",
+            "-lrt", "-ldl", "-lpthread"]
+    _compile(link)
+    return OUT
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--debug", action="store_true", help="trap on stuck mbarrier waits")
+    ap.add_argument("-v", "--verbose", action="store_true")
+    a = ap.parse_args()
+    print(build(debug=a.debug, verbose=a.verbose))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,108 @@
+"""RGSW-based CCMM engine on the B200.
+
+The encrypted database (MSRLWE-RGSW) is four matrices mod Q:
+A1 (N_db x d2), B1 (d1 x d2), A2 (N_db x N_qry), B2 (d1 x N_qry); the query is
+Aq (N_qry x d3) and Bq (d2 x d3). The product is two matrices
+
+    out_A = A1 Bq + A2 Aq   (N_db x d3)      -- the shared a-part
+    out_B = B1 Bq + B2 Aq   (d1 x d3)        -- one b-part per DB slice
+
+i.e. four PPMMs mod Q. Each part is ONE K-concatenated GEMM
+[X1 | X2] [Bq ; Aq] with K = d2 + N_qry, run per RNS modulus as three fused
+int8 tensor-core GEMMs. Parts follow the paper's 8-slice layout: part 0 is the
+a-part, parts 1..7 are b-part slices of 2^14 templates.
+
+Outputs are residues mod p_i^2, laid out [part][modulus][column n][row m]:
+column n of a part is the coefficient vector of the ciphertext(s) that hold
+output column n (each ciphertext = N_db consecutive rows of one column, as in
+Emulator::ccmm_twin, emulator.cpp:422-446).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+
+from . import capi
+from .modmat import Context, RnsBasis, build_paper_basis, default_context
+
+
+class CcmmEngine:
+    def __init__(self, parts: int, m: int, k: int, max_n: int, basis: Optional[RnsBasis] = None,
+                 ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.basis = basis or build_paper_basis()
+        self.parts, self.M, self.K, self.max_n = parts, m, k, max_n
+        self.primes, self.exps = self.basis.arrays()
+        self.nmod = len(self.primes)
+        h = C.c_void_p()
+        self.ctx.check(capi.lib().irl_ccmm_create(
+            self.ctx.handle, parts, m, k, max_n, capi.ptr(self.primes, capi.u32p),
+            capi.ptr(self.exps, capi.u32p), self.nmod, C.byref(h)))
+        self.handle = h
+
+    @property
+    def moduli(self):
+        return [int(p) ** int(e) for p, e in zip(self.primes, self.exps)]
+
+    @property
+    def device_bytes(self) -> int:
+        return int(capi.lib().irl_ccmm_device_bytes(self.handle))
+
+    def load_part(self, part: int, residues):
+        """residues: [nmod][M][K] uint16 (numpy host array or CUDA torch tensor)."""
+        on_dev = hasattr(residues, "data_ptr") and getattr(residues, "is_cuda", False)
+        if not on_dev:
+            residues = np.ascontiguousarray(residues, np.uint16)
+            assert residues.shape == (self.nmod, self.M, self.K)
+        self.ctx.check(capi.lib().irl_ccmm_load_part(self.handle, part, capi.ptr(residues), int(on_dev)))
+
+    def load_part_bigint(self, part: int, entries: np.ndarray, width: int):
+        """entries: [M][K] fixed-width little-endian integers mod Q."""
+        entries = np.ascontiguousarray(entries, np.uint8)
+        self.ctx.check(capi.lib().irl_ccmm_load_part_bigint(self.handle, part, capi.ptr(entries, capi.u8p),
+                                                            width))
+
+    def synth_db(self, seed: int):
+        """Counter-based synthetic residues, identical to oracle's orc_synth_residue."""
+        self.ctx.check(capi.lib().irl_ccmm_synth_db(self.handle, seed))
+
+    def run(self, q_res: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """End-to-end with host buffers: q_res [nmod][K][N] -> [parts][nmod][N][M]."""
+        assert q_res.dtype == np.uint16 and q_res.flags.c_contiguous
+        n = q_res.shape[2]
+        assert q_res.shape == (self.nmod, self.K, n)
+        if out is None:
+            out = np.empty((self.parts, self.nmod, n, self.M), np.uint16)
+        self.ctx.check(capi.lib().irl_ccmm_run(self.handle, capi.ptr(q_res), n, capi.ptr(out)))
+        return out
+
+    def run_device(self, q_res_dev, n: int, out_dev, part0: int = 0, nparts: Optional[int] = None,
+                   q_ready: bool = False, stream=None):
+        """Device-resident run on torch CUDA tensors; stream-ordered, non-blocking."""
+        nparts = self.parts - part0 if nparts is None else nparts
+        s = C.c_void_p(stream) if stream is not None else None
+        self.ctx.check(capi.lib().irl_ccmm_run_device(
+            self.handle, capi.ptr(q_res_dev) if q_res_dev is not None else None, int(q_ready), n,
+            part0, nparts, capi.ptr(out_dev), s))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            capi.lib().irl_ccmm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def synth_query(seed: int, k: int, n: int, moduli, stream: int = 0xFF) -> np.ndarray:
+    """Synthetic query residues [nmod][K][N] from the shared counter generator."""
+    out = np.empty((len(moduli), k, n), np.uint16)
+    L = capi.lib()
+    for i, m in enumerate(moduli):
+        L.irl_synth_residues_host(seed, stream, i, 0, k, 0, n, m, capi.ptr(out[i], capi.u16p))
+    return out

@@ -1,0 +1,932 @@
+// C ABI of the B200 PPMM / RGSW-CCMM engine (include/irl_capi.h).
+//
+// Host-buffer calls mirror irislab::modmat (reference proj/src/modmat.cpp)
+// value-for-value, including its exception taxonomy and messages; all the
+// arithmetic runs in this library's sm_100a kernels. There is no CPU compute
+// path: validation only reads the split kernels' device-side statistics.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/irl_capi.h"
+#include "kernels_aux.cuh"
+#include "ppmm.h"
+
+using namespace irl;
+
+// ---------------------------------------------------------------------------
+// Context
+// ---------------------------------------------------------------------------
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        const size_t want = std::max<size_t>(bytes, 1 << 20);
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct Status {
+    int code;
+    std::string msg;
+};
+
+}  // namespace
+
+struct irl_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    uint64_t launches = 0;
+    std::recursive_mutex mu;
+    DevBuf ws[8];
+    SplitStats* d_stats = nullptr;
+    SplitStats* h_stats = nullptr;
+    int32_t* d_absmax = nullptr;
+    int32_t* h_absmax = nullptr;
+};
+
+struct irl_ccmm {
+    irl_ctx* ctx = nullptr;
+    size_t parts = 0, M = 0, K = 0, ldk = 0, max_n = 0, nmod = 0;
+    ModTable mt{};
+    int8_t* db = nullptr;       // [parts][nmod][2][M][ldk]
+    int8_t* qplanes = nullptr;  // [nmod][2][max_n][ldk]
+    uint16_t* qres = nullptr;   // [nmod][K][max_n]
+    uint16_t* out = nullptr;    // [parts][nmod][max_n][M]
+    uint32_t kchunk = 0;        // K chunk keeping the fused int32 accumulators exact
+    cudaStream_t copy_stream = nullptr;
+    std::vector<cudaEvent_t> part_done;
+    uint64_t bytes = 0;
+};
+
+namespace {
+
+int set_err(irl_ctx* ctx, int code, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return code;
+}
+
+int cuda_fail(irl_ctx* ctx, cudaError_t e, const char* where) {
+    cudaGetLastError();  // clear sticky non-fatal state
+    const int code = e == cudaErrorMemoryAllocation ? IRL_ERR_OUT_OF_MEMORY : IRL_ERR_CUDA;
+    return set_err(ctx, code, std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e));
+}
+
+#define IRL_CK(ctx, expr)                                              \
+    do {                                                               \
+        cudaError_t e__ = (expr);                                      \
+        if (e__ != cudaSuccess) return cuda_fail((ctx), e__, #expr);   \
+    } while (0)
+
+#define IRL_LAUNCH(ctx, expr)                                          \
+    do {                                                               \
+        cudaError_t e__ = (expr);                                      \
+        if (e__ != cudaSuccess) return cuda_fail((ctx), e__, #expr);   \
+        ++(ctx)->launches;                                             \
+    } while (0)
+
+struct Guard {
+    irl_ctx* c;
+    std::lock_guard<std::recursive_mutex> lk;
+    explicit Guard(irl_ctx* ctx) : c(ctx), lk(ctx->mu) {
+        cudaSetDevice(ctx->device);
+        ctx->err.clear();
+    }
+};
+
+cudaStream_t pick_stream(irl_ctx* ctx, void* s) {
+    return s ? static_cast<cudaStream_t>(s) : ctx->stream;
+}
+
+const char* kOverflowMsg = "int32 accumulation bound exceeded: K*|A|*|B| = ";
+
+// Reference precheck of small_gemm (modmat.cpp:122-129).
+bool overflow(int64_t k, int64_t ma, int64_t mb, int64_t* bound) {
+    *bound = k * ma * mb;
+    return *bound >= (int64_t{1} << 31);
+}
+
+int validate_moduli(irl_ctx* ctx, const uint32_t* primes, const uint32_t* exps, size_t nmod) {
+    if (nmod > kMaxModuli) return set_err(ctx, IRL_ERR_UNSUPPORTED, "at most 32 moduli per basis");
+    for (size_t i = 0; i < nmod; ++i) {
+        if (exps[i] != 1 && exps[i] != 2)
+            return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "modulus exponent must be 1 or 2");
+        if (primes[i] < 2) return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "modulus base must be >= 2");
+        const uint64_t m = exps[i] == 2 ? uint64_t(primes[i]) * primes[i] : primes[i];
+        if (m > 65535) return set_err(ctx, IRL_ERR_UNSUPPORTED, "moduli above 2^16 are not supported");
+    }
+    return IRL_OK;
+}
+
+ModTable make_table(const uint32_t* primes, const uint32_t* exps, size_t nmod) {
+    ModTable t{};
+    t.n = static_cast<uint32_t>(nmod);
+    for (size_t i = 0; i < nmod; ++i) t.mc[i] = make_modconst(primes[i], exps[i]);
+    return t;
+}
+
+PpmmLaunch make_launch(const ModTable& mt) {
+    PpmmLaunch L;
+    L.nprimes = mt.n;
+    for (uint32_t i = 0; i < mt.n; ++i) L.mc[i] = mt.mc[i];
+    return L;
+}
+
+// K chunk such that acc2 = sum X0 Y1 + X1 Y0 and acc1 = sum X0 Y0 stay
+// exact in int32 for digit maxima (a0, a1, b0, b1); multiple of 128.
+uint32_t safe_kchunk(int64_t a0, int64_t a1, int64_t b0, int64_t b1, uint32_t K) {
+    const int64_t per = std::max<int64_t>(std::max<int64_t>(a0 * b1 + a1 * b0, a0 * b0), 1);
+    int64_t kc = ((int64_t{1} << 31) - 1) / per;
+    if (kc >= K) return K;
+    kc = (kc / 128) * 128;
+    return static_cast<uint32_t>(std::max<int64_t>(kc, 128));
+}
+
+// One PPMM over planes with K chunking (accumulate mode for chunks > 0).
+int run_ppmm(irl_ctx* ctx, PpmmLaunch L, uint32_t kchunk, cudaStream_t s) {
+    const uint32_t K = L.K;
+    if (K == 0) {
+        // Empty inner dimension: the product is zero (modmat.cpp:137 never runs).
+        const size_t bytes = size_t(L.parts) * L.nprimes * L.N * L.M * sizeof(uint16_t);
+        if (!L.accumulate) IRL_CK(ctx, cudaMemsetAsync(L.out, 0, bytes, s));
+        return IRL_OK;
+    }
+    if (kchunk == 0 || kchunk > K) kchunk = K;
+    const int8_t* a0 = L.a_planes;
+    const int8_t* b0 = L.b_planes;
+    for (uint32_t k0 = 0; k0 < K; k0 += kchunk) {
+        L.a_planes = a0 + k0;
+        L.b_planes = b0 + k0;
+        L.K = std::min(kchunk, K - k0);
+        L.accumulate = (k0 > 0) || L.accumulate;
+        IRL_LAUNCH(ctx, launch_ppmm_planes(L, s));
+    }
+    return IRL_OK;
+}
+
+size_t round16(size_t x) { return (x + 15) / 16 * 16; }
+
+// Big-integer helpers for CRT constants (host, 32-bit limbs).
+using Limbs = std::vector<uint32_t>;
+
+Limbs basis_Q(const uint32_t* primes, const uint32_t* exps, size_t nmod) {
+    Limbs q{1};
+    for (size_t i = 0; i < nmod; ++i) {
+        for (uint32_t e = 0; e < exps[i]; ++e) {
+            uint64_t carry = 0;
+            for (auto& l : q) {
+                const uint64_t t = uint64_t(l) * primes[i] + carry;
+                l = uint32_t(t);
+                carry = t >> 32;
+            }
+            if (carry) q.push_back(uint32_t(carry));
+        }
+    }
+    return q;
+}
+
+uint32_t divmod_small(Limbs& x, uint32_t m) {
+    uint64_t r = 0;
+    for (size_t i = x.size(); i-- > 0;) {
+        const uint64_t cur = (r << 32) | x[i];
+        x[i] = uint32_t(cur / m);
+        r = cur % m;
+    }
+    return uint32_t(r);
+}
+
+size_t byte_width(const Limbs& q) {
+    size_t bits = 0;
+    for (size_t i = q.size(); i-- > 0;) {
+        if (q[i]) {
+            bits = i * 32 + (32 - __builtin_clz(q[i]));
+            break;
+        }
+    }
+    return bits ? (bits + 7) / 8 : 1;
+}
+
+bool inv_mod(uint32_t a, uint32_t m, uint32_t* out) {
+    int64_t t = 0, nt = 1, r = m, nr = a % m;
+    while (nr) {
+        const int64_t q = r / nr, tt = t - q * nt, rr = r - q * nr;
+        t = nt;
+        nt = tt;
+        r = nr;
+        nr = rr;
+    }
+    if (r != 1 && m != 1) return false;
+    if (t < 0) t += m;
+    *out = uint32_t(t);
+    return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+int irl_abi_version(void) { return IRL_ABI_VERSION; }
+
+const char* irl_status_string(int s) {
+    switch (s) {
+        case IRL_OK: return "ok";
+        case IRL_ERR_SHAPE_MISMATCH: return "ShapeMismatch";
+        case IRL_ERR_MODULUS_TOO_LARGE: return "ModulusTooLarge";
+        case IRL_ERR_ACCUMULATION_OVERFLOW_RISK: return "AccumulationOverflowRisk";
+        case IRL_ERR_NOT_COPRIME: return "Error";
+        case IRL_ERR_MODULUS_BUDGET: return "ModulusBudget";
+        case IRL_ERR_INVALID_ARGUMENT: return "InvalidArgument";
+        case IRL_ERR_CUDA: return "CudaError";
+        case IRL_ERR_NO_DEVICE: return "NoDevice";
+        case IRL_ERR_OUT_OF_MEMORY: return "OutOfMemory";
+        case IRL_ERR_UNSUPPORTED: return "Unsupported";
+        default: return "unknown";
+    }
+}
+
+int irl_ctx_create(int device, irl_ctx** out) {
+    if (!out) return IRL_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+        cudaGetLastError();
+        return IRL_ERR_NO_DEVICE;
+    }
+    cudaDeviceProp prop{};
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10) {
+        return IRL_ERR_NO_DEVICE;  // built for sm_100a only
+    }
+    auto* ctx = new irl_ctx();
+    ctx->device = device;
+    if (cudaSetDevice(device) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMalloc(&ctx->d_stats, sizeof(SplitStats)) != cudaSuccess ||
+        cudaMallocHost(&ctx->h_stats, sizeof(SplitStats)) != cudaSuccess ||
+        cudaMalloc(&ctx->d_absmax, 2 * sizeof(int32_t)) != cudaSuccess ||
+        cudaMallocHost(&ctx->h_absmax, 2 * sizeof(int32_t)) != cudaSuccess) {
+        delete ctx;
+        return IRL_ERR_CUDA;
+    }
+    *out = ctx;
+    return IRL_OK;
+}
+
+int irl_ctx_destroy(irl_ctx* ctx) {
+    if (!ctx) return IRL_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& b : ctx->ws) b.release();
+    cudaFree(ctx->d_stats);
+    cudaFreeHost(ctx->h_stats);
+    cudaFree(ctx->d_absmax);
+    cudaFreeHost(ctx->h_absmax);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return IRL_OK;
+}
+
+const char* irl_last_error(const irl_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+uint64_t irl_kernel_launches(const irl_ctx* ctx) { return ctx ? ctx->launches : 0; }
+void* irl_ctx_stream(const irl_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+size_t irl_paper_basis(uint32_t* primes, uint32_t* exps, size_t cap) {
+    // build_paper_basis (modmat.cpp:37-45): primes in [127, 253], e = 2.
+    size_t n = 0;
+    for (uint32_t v = 127; v <= 253; ++v) {
+        bool prime = true;
+        for (uint32_t q = 2; q * q <= v; ++q)
+            if (v % q == 0) {
+                prime = false;
+                break;
+            }
+        if (!prime) continue;
+        if (n < cap) {
+            primes[n] = v;
+            exps[n] = 2;
+        }
+        ++n;
+    }
+    return n;
+}
+
+size_t irl_basis_Q_bytes(const uint32_t* primes, const uint32_t* exps, size_t nmod, uint8_t* out,
+                         size_t cap) {
+    const Limbs q = basis_Q(primes, exps, nmod);
+    const size_t w = byte_width(q);
+    if (out)
+        for (size_t b = 0; b < std::min(w, cap); ++b)
+            out[b] = b / 4 < q.size() ? uint8_t(q[b / 4] >> (8 * (b % 4))) : 0;
+    return w;
+}
+
+uint32_t irl_synth_residue(uint64_t seed, uint32_t stream, uint32_t plane, uint32_t row,
+                           uint32_t col, uint32_t m) {
+    return synth_residue_host(seed, stream, plane, row, col, m);
+}
+
+void irl_synth_residues_host(uint64_t seed, uint32_t stream, uint32_t plane, uint32_t row0,
+                             uint32_t nrows, uint32_t col0, uint32_t ncols, uint32_t m,
+                             uint16_t* out) {
+    for (uint32_t r = 0; r < nrows; ++r)
+        for (uint32_t c = 0; c < ncols; ++c)
+            out[size_t(r) * ncols + c] =
+                uint16_t(synth_residue_host(seed, stream, plane, row0 + r, col0 + c, m));
+}
+
+// ---------------------------------------------------------------------------
+// digit_decompose / digit_recompose (modmat.cpp:86-118)
+// ---------------------------------------------------------------------------
+
+int irl_digit_decompose(irl_ctx* ctx, const int32_t* m, size_t rows, size_t cols, uint32_t p,
+                        int32_t* d0, int32_t* d1) {
+    if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
+    Guard g(ctx);
+    if (p >= 256) return set_err(ctx, IRL_ERR_MODULUS_TOO_LARGE, "digit base must be < 2^8");
+    if (p == 0) return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "digit base must be positive");
+    const size_t n = rows * cols;
+    if (n == 0) return IRL_OK;
+    const size_t bytes = n * sizeof(int32_t);
+    IRL_CK(ctx, ctx->ws[0].ensure(3 * bytes));
+    int32_t* din = ctx->ws[0].as<int32_t>();
+    IRL_CK(ctx, cudaMemcpyAsync(din, m, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    IRL_LAUNCH(ctx, launch_digit_decompose(din, n, make_modconst(p, 2), din + n, din + 2 * n, ctx->stream));
+    IRL_CK(ctx, cudaMemcpyAsync(d0, din + n, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    IRL_CK(ctx, cudaMemcpyAsync(d1, din + 2 * n, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    return IRL_OK;
+}
+
+int irl_digit_recompose(irl_ctx* ctx, const int32_t* d0, const int32_t* d1, size_t rows,
+                        size_t cols, uint32_t p, int32_t* out) {
+    if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
+    Guard g(ctx);
+    if (p == 0 || p > 46340)
+        return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "p^2 must fit a positive int32");
+    const size_t n = rows * cols;
+    if (n == 0) return IRL_OK;
+    const size_t bytes = n * sizeof(int32_t);
+    IRL_CK(ctx, ctx->ws[0].ensure(3 * bytes));
+    int32_t* b = ctx->ws[0].as<int32_t>();
+    IRL_CK(ctx, cudaMemcpyAsync(b, d0, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    IRL_CK(ctx, cudaMemcpyAsync(b + n, d1, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    IRL_LAUNCH(ctx, launch_digit_recompose(b, b + n, n, make_modconst(p, 2), b + 2 * n, ctx->stream));
+    IRL_CK(ctx, cudaMemcpyAsync(out, b + 2 * n, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    return IRL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// small_gemm (modmat.cpp:120-141)
+// ---------------------------------------------------------------------------
+
+int irl_small_gemm(irl_ctx* ctx, const int32_t* a, const int32_t* b, int32_t* c, size_t m,
+                   size_t k, size_t n) {
+    if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
+    Guard g(ctx);
+    if (m > UINT32_MAX || k > UINT32_MAX || n > UINT32_MAX)
+        return set_err(ctx, IRL_ERR_UNSUPPORTED, "dimension above 2^32");
+    const size_t na = m * k, nb = k * n, nc = m * n;
+    IRL_CK(ctx, ctx->ws[0].ensure((na + nb + nc + 1) * sizeof(int32_t)));
+    int32_t* da = ctx->ws[0].as<int32_t>();
+    int32_t* db = da + na;
+    int32_t* dc = db + nb;
+    if (na) IRL_CK(ctx, cudaMemcpyAsync(da, a, na * 4, cudaMemcpyHostToDevice, ctx->stream));
+    if (nb) IRL_CK(ctx, cudaMemcpyAsync(db, b, nb * 4, cudaMemcpyHostToDevice, ctx->stream));
+    IRL_CK(ctx, cudaMemsetAsync(ctx->d_absmax, 0, 2 * sizeof(int32_t), ctx->stream));
+    IRL_LAUNCH(ctx, launch_absmax_i32(da, na, ctx->d_absmax, ctx->stream));
+    IRL_LAUNCH(ctx, launch_absmax_i32(db, nb, ctx->d_absmax + 1, ctx->stream));
+    IRL_CK(ctx, cudaMemcpyAsync(ctx->h_absmax, ctx->d_absmax, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    int64_t bound = 0;
+    if (overflow(int64_t(k), ctx->h_absmax[0], ctx->h_absmax[1], &bound))
+        return set_err(ctx, IRL_ERR_ACCUMULATION_OVERFLOW_RISK, kOverflowMsg + std::to_string(bound));
+    if (nc == 0) return IRL_OK;
+    IRL_LAUNCH(ctx, launch_gemm_i32(da, db, dc, uint32_t(m), uint32_t(k), uint32_t(n), ctx->stream));
+    IRL_CK(ctx, cudaMemcpyAsync(c, dc, nc * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    return IRL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// gemm_mod_psq (modmat.cpp:143-160)
+// ---------------------------------------------------------------------------
+
+int irl_gemm_mod_psq(irl_ctx* ctx, const int32_t* a, const int32_t* b, int32_t* c, size_t m,
+                     size_t k, size_t n, uint32_t p) {
+    if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
+    Guard g(ctx);
+    // digit_decompose(a, p) throws first (modmat.cpp:87, :145).
+    if (p >= 256) return set_err(ctx, IRL_ERR_MODULUS_TOO_LARGE, "digit base must be < 2^8");
+    if (p == 0) return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "digit base must be positive");
+    if (m >= (1u << 30) || n >= (1u << 30) || k >= (1u << 30))
+        return set_err(ctx, IRL_ERR_UNSUPPORTED, "dimension above 2^30");
+    const size_t ldk = round16(std::max<size_t>(k, 1));
+    const size_t na = m * k, nb = k * n;
+    const size_t pa = 2 * m * ldk, pb = 2 * n * ldk;  // plane bytes
+    const size_t off_b = na * 4, off_pa = off_b + nb * 4, off_pb = round16(off_pa + pa),
+                 off_o = round16(off_pb + pb), off_c = round16(off_o + m * n * 2);
+    IRL_CK(ctx, ctx->ws[0].ensure(off_c + m * n * 4 + 16));
+    uint8_t* base = ctx->ws[0].as<uint8_t>();
+    int32_t* da = reinterpret_cast<int32_t*>(base);
+    int32_t* db = reinterpret_cast<int32_t*>(base + off_b);
+    int8_t* pla = reinterpret_cast<int8_t*>(base + off_pa);
+    int8_t* plb = reinterpret_cast<int8_t*>(base + off_pb);
+    uint16_t* dout = reinterpret_cast<uint16_t*>(base + off_o);
+    int32_t* dc = reinterpret_cast<int32_t*>(base + off_c);
+    if (na) IRL_CK(ctx, cudaMemcpyAsync(da, a, na * 4, cudaMemcpyHostToDevice, ctx->stream));
+    if (nb) IRL_CK(ctx, cudaMemcpyAsync(db, b, nb * 4, cudaMemcpyHostToDevice, ctx->stream));
+    ModTable mt{};
+    mt.n = 1;
+    mt.mc[0] = make_modconst(p, 2);
+    IRL_CK(ctx, cudaMemsetAsync(ctx->d_stats, 0, 2 * sizeof(SplitStats::v[0]), ctx->stream));
+    SplitStats* sa = ctx->d_stats;
+    // B's stats go to slot 1 of the stats table (a second "modulus" row).
+    SplitStats* sb = reinterpret_cast<SplitStats*>(reinterpret_cast<int32_t*>(ctx->d_stats) + 3);
+    if (k > 0) {
+        IRL_LAUNCH(ctx, launch_split_rows<int32_t>(da, k, 0, uint32_t(m), uint32_t(k), mt, pla, ldk, sa, ctx->stream));
+        IRL_LAUNCH(ctx, launch_split_cols<int32_t>(db, n, 0, uint32_t(k), uint32_t(n), mt, plb, ldk, sb, ctx->stream));
+    }
+    IRL_CK(ctx, cudaMemcpyAsync(ctx->h_stats, ctx->d_stats, 6 * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    const int64_t a0 = ctx->h_stats->v[0][0], a1 = ctx->h_stats->v[0][1];
+    const int64_t b0 = ctx->h_stats->v[1][0], b1 = ctx->h_stats->v[1][1];
+    // small_gemm prechecks in the reference's order: A0B0, A0B1, A1B0 (:147-149).
+    int64_t bound = 0;
+    if (overflow(int64_t(k), a0, b0, &bound) || overflow(int64_t(k), a0, b1, &bound) ||
+        overflow(int64_t(k), a1, b0, &bound))
+        return set_err(ctx, IRL_ERR_ACCUMULATION_OVERFLOW_RISK, kOverflowMsg + std::to_string(bound));
+    if (m == 0 || n == 0) return IRL_OK;
+    PpmmLaunch L = make_launch(mt);
+    L.a_planes = pla;
+    L.b_planes = plb;
+    L.out = dout;
+    L.M = uint32_t(m);
+    L.N = uint32_t(n);
+    L.K = uint32_t(k);
+    L.ldk = uint32_t(ldk);
+    L.parts = 1;
+    int st = run_ppmm(ctx, L, safe_kchunk(a0, a1, b0, b1, uint32_t(k)), ctx->stream);
+    if (st) return st;
+    IRL_LAUNCH(ctx, launch_transpose_u16_to_i32(dout, uint32_t(m), uint32_t(n), dc, ctx->stream));
+    IRL_CK(ctx, cudaMemcpyAsync(c, dc, m * n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    return IRL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// gemm_mod_Q (modmat.cpp:162-195)
+// ---------------------------------------------------------------------------
+
+int irl_gemm_mod_Q(irl_ctx* ctx, const uint8_t* a, const uint8_t* b, uint8_t* c, size_t m,
+                   size_t k, size_t n, size_t width, const uint32_t* primes, const uint32_t* exps,
+                   size_t nmod) {
+    if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
+    Guard g(ctx);
+    int st = validate_moduli(ctx, primes, exps, nmod);
+    if (st) return st;
+    const Limbs Q = basis_Q(primes, exps, nmod);
+    if (Q.size() > kMaxQLimbs) return set_err(ctx, IRL_ERR_UNSUPPORTED, "Q above 2^384 is not supported");
+    if (width == 0 || width > kMaxWidth || width < byte_width(Q))
+        return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "entry width must be ceil(log256 Q) .. 48 bytes");
+    if (m >= (1u << 28) || n >= (1u << 28) || k >= (1u << 28))
+        return set_err(ctx, IRL_ERR_UNSUPPORTED, "dimension above 2^28");
+    const ModTable mt = make_table(primes, exps, nmod);
+    const size_t ldk = round16(std::max<size_t>(k, 1));
+    const size_t ba = m * k * width, bb = k * n * width;
+    const size_t pa = nmod * 2 * m * ldk, pb = nmod * 2 * n * ldk;
+    const size_t raw_a = nmod * m * k * 4, raw_b = nmod * k * n * 4, raw_c = m * n * 4;
+    const size_t res = nmod * m * n * 2, outb = m * n * width;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off = round16(off + bytes);
+        return o;
+    };
+    const size_t o_a = take(ba), o_b = take(bb), o_pa = take(pa), o_pb = take(pb),
+                 o_ra = take(raw_a), o_rb = take(raw_b), o_rc = take(raw_c), o_res = take(res),
+                 o_out = take(outb);
+    IRL_CK(ctx, ctx->ws[0].ensure(off + 16));
+    uint8_t* base = ctx->ws[0].as<uint8_t>();
+    uint8_t* dA = base + o_a;
+    uint8_t* dB = base + o_b;
+    int8_t* pla = reinterpret_cast<int8_t*>(base + o_pa);
+    int8_t* plb = reinterpret_cast<int8_t*>(base + o_pb);
+    int32_t* ra = reinterpret_cast<int32_t*>(base + o_ra);
+    int32_t* rb = reinterpret_cast<int32_t*>(base + o_rb);
+    int32_t* rc = reinterpret_cast<int32_t*>(base + o_rc);
+    uint16_t* dres = reinterpret_cast<uint16_t*>(base + o_res);
+    uint8_t* dout = base + o_out;
+    if (ba) IRL_CK(ctx, cudaMemcpyAsync(dA, a, ba, cudaMemcpyHostToDevice, ctx->stream));
+    if (bb) IRL_CK(ctx, cudaMemcpyAsync(dB, b, bb, cudaMemcpyHostToDevice, ctx->stream));
+    IRL_CK(ctx, cudaMemsetAsync(pla, 0, pa, ctx->stream));
+    IRL_CK(ctx, cudaMemsetAsync(plb, 0, pb, ctx->stream));
+    // Two stats tables: A in d_stats[0..], B in the workspace tail.
+    IRL_CK(ctx, ctx->ws[1].ensure(sizeof(SplitStats)));
+    SplitStats* sa = ctx->d_stats;
+    SplitStats* sb = ctx->ws[1].as<SplitStats>();
+    IRL_CK(ctx, cudaMemsetAsync(sa, 0, sizeof(SplitStats), ctx->stream));
+    IRL_CK(ctx, cudaMemsetAsync(sb, 0, sizeof(SplitStats), ctx->stream));
+    // Residue extraction (:168-176) fused with the digit split.
+    IRL_LAUNCH(ctx, launch_split_bigint(dA, uint32_t(width), uint32_t(m), uint32_t(k), 0, mt, pla, ldk,
+                                        uint32_t(m), 0, ra, sa, ctx->stream));
+    IRL_LAUNCH(ctx, launch_split_bigint(dB, uint32_t(width), uint32_t(k), uint32_t(n), 1, mt, plb, ldk,
+                                        uint32_t(n), 0, rb, sb, ctx->stream));
+    std::vector<SplitStats> hs(2);
+    IRL_CK(ctx, cudaMemcpyAsync(&hs[0], sa, sizeof(SplitStats), cudaMemcpyDeviceToHost, ctx->stream));
+    IRL_CK(ctx, cudaMemcpyAsync(&hs[1], sb, sizeof(SplitStats), cudaMemcpyDeviceToHost, ctx->stream));
+    IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
+
+    // Per-modulus checks in basis order, as the reference loop would raise them.
+    int64_t a0m = 1, a1m = 0, b0m = 1, b1m = 0;
+    std::vector<uint32_t> inv(nmod);
+    for (size_t i = 0; i < nmod; ++i) {
+        const uint32_t mod = mt.mc[i].m;
+        int64_t bound = 0;
+        if (exps[i] == 2) {
+            if (primes[i] >= 256)
+                return set_err(ctx, IRL_ERR_MODULUS_TOO_LARGE, "digit base must be < 2^8");
+            const int64_t A0 = hs[0].v[i][0], A1 = hs[0].v[i][1];
+            const int64_t B0 = hs[1].v[i][0], B1 = hs[1].v[i][1];
+            if (overflow(int64_t(k), A0, B0, &bound) || overflow(int64_t(k), A0, B1, &bound) ||
+                overflow(int64_t(k), A1, B0, &bound))
+                return set_err(ctx, IRL_ERR_ACCUMULATION_OVERFLOW_RISK, kOverflowMsg + std::to_string(bound));
+            a0m = std::max(a0m, A0);
+            a1m = std::max(a1m, A1);
+            b0m = std::max(b0m, B0);
+            b1m = std::max(b1m, B1);
+        } else if (overflow(int64_t(k), hs[0].v[i][2], hs[1].v[i][2], &bound)) {
+            return set_err(ctx, IRL_ERR_ACCUMULATION_OVERFLOW_RISK, kOverflowMsg + std::to_string(bound));
+        }
+        Limbs qi = Q;
+        divmod_small(qi, mod);
+        Limbs tmp = qi;
+        const uint32_t rem = divmod_small(tmp, mod);  // (Q/m) mod m
+        if (!inv_mod(rem, mod, &inv[i]))
+            return set_err(ctx, IRL_ERR_NOT_COPRIME, "CRT basis is not coprime");
+    }
+    if (m == 0 || n == 0) return IRL_OK;
+
+    // e = 2 moduli: tcgen05 PPMM over all planes (e = 1 slots are zero planes
+    // and are overwritten below by the exact int32 path).
+    PpmmLaunch L = make_launch(mt);
+    L.a_planes = pla;
+    L.b_planes = plb;
+    L.out = dres;
+    L.M = uint32_t(m);
+    L.N = uint32_t(n);
+    L.K = uint32_t(k);
+    L.ldk = uint32_t(ldk);
+    L.parts = 1;
+    st = run_ppmm(ctx, L, safe_kchunk(a0m, a1m, b0m, b1m, uint32_t(k)), ctx->stream);
+    if (st) return st;
+    for (size_t i = 0; i < nmod; ++i) {
+        if (exps[i] != 1) continue;
+        IRL_LAUNCH(ctx, launch_gemm_i32(ra + i * m * k, rb + i * k * n, rc, uint32_t(m), uint32_t(k),
+                                        uint32_t(n), ctx->stream));
+        IRL_LAUNCH(ctx, launch_reduce_raw(rc, uint32_t(m), uint32_t(n), uint32_t(i), mt.mc[i], dres, ctx->stream));
+    }
+    // CRT lift (:180-193).
+    CrtTable t{};
+    t.nmod = uint32_t(nmod);
+    t.limbs = uint32_t(Q.size());
+    t.width = uint32_t(width);
+    for (size_t i = 0; i < nmod; ++i) {
+        t.m[i] = mt.mc[i].m;
+        t.inv[i] = inv[i];
+        Limbs qi = Q;
+        divmod_small(qi, t.m[i]);
+        for (size_t j = 0; j < qi.size() && j < kMaxQLimbs; ++j) t.qi[i][j] = qi[j];
+    }
+    for (int s = 0; s < 5; ++s) {
+        const uint32_t mul = 16u >> s;
+        uint64_t carry = 0;
+        for (size_t j = 0; j <= Q.size(); ++j) {
+            const uint64_t v = (j < Q.size() ? uint64_t(Q[j]) * mul : 0) + carry;
+            t.qmul[s][j] = uint32_t(v);
+            carry = v >> 32;
+        }
+    }
+    IRL_LAUNCH(ctx, launch_crt_lift(dres, uint32_t(m), uint32_t(n), t, dout, ctx->stream));
+    IRL_CK(ctx, cudaMemcpyAsync(c, dout, outb, cudaMemcpyDeviceToHost, ctx->stream));
+    IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    return IRL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Device-level building blocks
+// ---------------------------------------------------------------------------
+
+int irl_split_rows_u16(irl_ctx* ctx, const uint16_t* res, size_t ld_res, size_t plane_stride,
+                       size_t rows, size_t cols, const uint32_t* primes, const uint32_t* exps,
+                       size_t nmod, int8_t* planes, size_t ldk, void* stream) {
+    if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
+    Guard g(ctx);
+    int st = validate_moduli(ctx, primes, exps, nmod);
+    if (st) return st;
+    if (ldk % 16 || ldk < cols) return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "ldk must be >= cols and a multiple of 16");
+    IRL_LAUNCH(ctx, launch_split_rows<uint16_t>(res, ld_res, plane_stride, uint32_t(rows), uint32_t(cols),
+                                                make_table(primes, exps, nmod), planes, ldk, nullptr,
+                                                pick_stream(ctx, stream)));
+    return IRL_OK;
+}
+
+int irl_split_cols_u16(irl_ctx* ctx, const uint16_t* res, size_t ld_res, size_t plane_stride,
+                       size_t k, size_t n, const uint32_t* primes, const uint32_t* exps,
+                       size_t nmod, int8_t* planes, size_t ldk, void* stream) {
+    if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
+    Guard g(ctx);
+    int st = validate_moduli(ctx, primes, exps, nmod);
+    if (st) return st;
+    if (ldk % 16 || ldk < k) return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "ldk must be >= k and a multiple of 16");
+    IRL_LAUNCH(ctx, launch_split_cols<uint16_t>(res, ld_res, plane_stride, uint32_t(k), uint32_t(n),
+                                                make_table(primes, exps, nmod), planes, ldk, nullptr,
+                                                pick_stream(ctx, stream)));
+    return IRL_OK;
+}
+
+int irl_split_bigint(irl_ctx* ctx, const uint8_t* entries, size_t width, size_t rows, size_t cols,
+                     int transpose, const uint32_t* primes, const uint32_t* exps, size_t nmod,
+                     int8_t* planes, size_t ldk, void* stream) {
+    if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
+    Guard g(ctx);
+    int st = validate_moduli(ctx, primes, exps, nmod);
+    if (st) return st;
+    for (size_t i = 0; i < nmod; ++i)
+        if (exps[i] != 2 || primes[i] >= 256)
+            return set_err(ctx, IRL_ERR_UNSUPPORTED, "plane split needs e = 2 and p < 256");
+    if (width == 0 || width > kMaxWidth) return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "width must be 1..48");
+    IRL_LAUNCH(ctx, launch_split_bigint(entries, uint32_t(width), uint32_t(rows), uint32_t(cols), transpose,
+                                        make_table(primes, exps, nmod), planes, ldk,
+                                        uint32_t(transpose ? cols : rows), 0, nullptr, nullptr,
+                                        pick_stream(ctx, stream)));
+    return IRL_OK;
+}
+
+int irl_ppmm_planes(irl_ctx* ctx, const int8_t* a_planes, const int8_t* b_planes, uint16_t* out,
+                    size_t parts, size_t m, size_t n, size_t k, size_t ldk,
+                    const uint32_t* primes, const uint32_t* exps, size_t nmod, int accumulate,
+                    void* stream) {
+    if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
+    Guard g(ctx);
+    int st = validate_moduli(ctx, primes, exps, nmod);
+    if (st) return st;
+    if (ldk % 16 || ldk < k) return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "ldk must be >= k and a multiple of 16");
+    const ModTable mt = make_table(primes, exps, nmod);
+    PpmmLaunch L = make_launch(mt);
+    L.a_planes = a_planes;
+    L.b_planes = b_planes;
+    L.out = out;
+    L.M = uint32_t(m);
+    L.N = uint32_t(n);
+    L.K = uint32_t(k);
+    L.ldk = uint32_t(ldk);
+    L.parts = uint32_t(parts);
+    L.accumulate = accumulate;
+    int64_t h = 0;
+    for (size_t i = 0; i < nmod; ++i) h = std::max<int64_t>(h, (primes[i] - 1) / 2 + (primes[i] % 2 == 0));
+    return run_ppmm(ctx, L, safe_kchunk(h, h, h, h, uint32_t(k)), pick_stream(ctx, stream));
+}
+
+int irl_crt_lift(irl_ctx* ctx, const uint16_t* res, size_t m, size_t n, uint8_t* out,
+                 size_t width, const uint32_t* primes, const uint32_t* exps, size_t nmod,
+                 void* stream) {
+    if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
+    Guard g(ctx);
+    int st = validate_moduli(ctx, primes, exps, nmod);
+    if (st) return st;
+    const Limbs Q = basis_Q(primes, exps, nmod);
+    if (Q.size() > kMaxQLimbs || width > kMaxWidth || width < byte_width(Q))
+        return set_err(ctx, IRL_ERR_UNSUPPORTED, "Q / width out of range");
+    CrtTable t{};
+    t.nmod = uint32_t(nmod);
+    t.limbs = uint32_t(Q.size());
+    t.width = uint32_t(width);
+    for (size_t i = 0; i < nmod; ++i) {
+        t.m[i] = exps[i] == 2 ? primes[i] * primes[i] : primes[i];
+        Limbs qi = Q;
+        divmod_small(qi, t.m[i]);
+        Limbs tmp = qi;
+        if (!inv_mod(divmod_small(tmp, t.m[i]), t.m[i], &t.inv[i]))
+            return set_err(ctx, IRL_ERR_NOT_COPRIME, "CRT basis is not coprime");
+        for (size_t j = 0; j < qi.size() && j < kMaxQLimbs; ++j) t.qi[i][j] = qi[j];
+    }
+    for (int s = 0; s < 5; ++s) {
+        const uint32_t mul = 16u >> s;
+        uint64_t carry = 0;
+        for (size_t j = 0; j <= Q.size(); ++j) {
+            const uint64_t v = (j < Q.size() ? uint64_t(Q[j]) * mul : 0) + carry;
+            t.qmul[s][j] = uint32_t(v);
+            carry = v >> 32;
+        }
+    }
+    IRL_LAUNCH(ctx, launch_crt_lift(res, uint32_t(m), uint32_t(n), t, out, pick_stream(ctx, stream)));
+    return IRL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// RGSW CCMM engine
+// ---------------------------------------------------------------------------
+
+int irl_ccmm_create(irl_ctx* ctx, size_t parts, size_t m, size_t k, size_t max_n,
+                    const uint32_t* primes, const uint32_t* exps, size_t nmod, irl_ccmm** out) {
+    if (!ctx || !out) return IRL_ERR_INVALID_ARGUMENT;
+    Guard g(ctx);
+    *out = nullptr;
+    int st = validate_moduli(ctx, primes, exps, nmod);
+    if (st) return st;
+    for (size_t i = 0; i < nmod; ++i)
+        if (primes[i] >= 256) return set_err(ctx, IRL_ERR_MODULUS_TOO_LARGE, "digit base must be < 2^8");
+    if (parts == 0 || m == 0 || k == 0 || max_n == 0 || nmod == 0)
+        return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: nonpositive dimensions");
+    if (m >= (1u << 24) || k >= (1u << 24) || max_n >= (1u << 24) || parts > 255)
+        return set_err(ctx, IRL_ERR_UNSUPPORTED, "ccmm: dimension out of range");
+    auto* e = new irl_ccmm();
+    e->ctx = ctx;
+    e->parts = parts;
+    e->M = m;
+    e->K = k;
+    e->ldk = round16(k);
+    e->max_n = max_n;
+    e->nmod = nmod;
+    e->mt = make_table(primes, exps, nmod);
+    int64_t h = 0;
+    for (size_t i = 0; i < nmod; ++i) h = std::max<int64_t>(h, (primes[i] - 1) / 2 + (primes[i] % 2 == 0));
+    e->kchunk = safe_kchunk(h, h, h, h, uint32_t(k));
+    const size_t db_b = parts * nmod * 2 * m * e->ldk, qp_b = nmod * 2 * max_n * e->ldk,
+                 qr_b = nmod * k * max_n * 2, out_b = parts * nmod * max_n * m * 2;
+    cudaError_t err = cudaMalloc(&e->db, db_b);
+    if (err == cudaSuccess) err = cudaMalloc(&e->qplanes, qp_b);
+    if (err == cudaSuccess) err = cudaMalloc(&e->qres, qr_b);
+    if (err == cudaSuccess) err = cudaMalloc(&e->out, out_b);
+    if (err == cudaSuccess) err = cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking);
+    if (err == cudaSuccess) err = cudaMemsetAsync(e->db, 0, db_b, ctx->stream);
+    e->part_done.resize(parts);
+    for (size_t i = 0; err == cudaSuccess && i < parts; ++i)
+        err = cudaEventCreateWithFlags(&e->part_done[i], cudaEventDisableTiming);
+    if (err != cudaSuccess) {
+        irl_ccmm_destroy(e);
+        return cuda_fail(ctx, err, "irl_ccmm_create");
+    }
+    e->bytes = db_b + qp_b + qr_b + out_b;
+    *out = e;
+    return IRL_OK;
+}
+
+int irl_ccmm_destroy(irl_ccmm* e) {
+    if (!e) return IRL_OK;
+    cudaSetDevice(e->ctx->device);
+    cudaStreamSynchronize(e->ctx->stream);
+    if (e->copy_stream) cudaStreamSynchronize(e->copy_stream);
+    for (auto ev : e->part_done)
+        if (ev) cudaEventDestroy(ev);
+    if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
+    cudaFree(e->db);
+    cudaFree(e->qplanes);
+    cudaFree(e->qres);
+    cudaFree(e->out);
+    delete e;
+    return IRL_OK;
+}
+
+uint64_t irl_ccmm_device_bytes(const irl_ccmm* e) { return e ? e->bytes : 0; }
+
+int irl_ccmm_load_part(irl_ccmm* e, size_t part, const uint16_t* res, int res_on_device) {
+    if (!e) return IRL_ERR_INVALID_ARGUMENT;
+    irl_ctx* ctx = e->ctx;
+    Guard g(ctx);
+    if (part >= e->parts) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: part index out of range");
+    const size_t plane_elems = e->M * e->K;
+    int8_t* dst = e->db + part * e->nmod * 2 * e->M * e->ldk;
+    for (size_t i = 0; i < e->nmod; ++i) {
+        const uint16_t* src = res + i * plane_elems;
+        if (!res_on_device) {
+            IRL_CK(ctx, ctx->ws[2].ensure(plane_elems * 2));
+            IRL_CK(ctx, cudaMemcpyAsync(ctx->ws[2].p, src, plane_elems * 2, cudaMemcpyHostToDevice, ctx->stream));
+            src = ctx->ws[2].as<uint16_t>();
+        }
+        ModTable one{};
+        one.n = 1;
+        one.mc[0] = e->mt.mc[i];
+        IRL_LAUNCH(ctx, launch_split_rows<uint16_t>(src, e->K, 0, uint32_t(e->M), uint32_t(e->K), one,
+                                                    dst + i * 2 * e->M * e->ldk, e->ldk, nullptr, ctx->stream));
+    }
+    IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    return IRL_OK;
+}
+
+int irl_ccmm_load_part_bigint(irl_ccmm* e, size_t part, const uint8_t* entries, size_t width) {
+    if (!e) return IRL_ERR_INVALID_ARGUMENT;
+    irl_ctx* ctx = e->ctx;
+    Guard g(ctx);
+    if (part >= e->parts) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: part index out of range");
+    if (width == 0 || width > kMaxWidth) return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "width must be 1..48");
+    for (size_t i = 0; i < e->nmod; ++i)
+        if (e->mt.mc[i].e != 2) return set_err(ctx, IRL_ERR_UNSUPPORTED, "bigint ingest needs e = 2");
+    int8_t* dst = e->db + part * e->nmod * 2 * e->M * e->ldk;
+    const size_t row_bytes = e->K * width;
+    const size_t chunk = std::max<size_t>(1, std::min<size_t>(e->M, (size_t(256) << 20) / row_bytes));
+    IRL_CK(ctx, ctx->ws[2].ensure(chunk * row_bytes));
+    for (size_t r0 = 0; r0 < e->M; r0 += chunk) {
+        const size_t rows = std::min(chunk, e->M - r0);
+        IRL_CK(ctx, cudaMemcpyAsync(ctx->ws[2].p, entries + r0 * row_bytes, rows * row_bytes,
+                                    cudaMemcpyHostToDevice, ctx->stream));
+        IRL_LAUNCH(ctx, launch_split_bigint(ctx->ws[2].as<uint8_t>(), uint32_t(width), uint32_t(rows),
+                                            uint32_t(e->K), 0, e->mt, dst, e->ldk, uint32_t(e->M),
+                                            uint32_t(r0), nullptr, nullptr, ctx->stream));
+        IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    return IRL_OK;
+}
+
+int irl_ccmm_synth_db(irl_ccmm* e, uint64_t seed) {
+    if (!e) return IRL_ERR_INVALID_ARGUMENT;
+    irl_ctx* ctx = e->ctx;
+    Guard g(ctx);
+    for (size_t p = 0; p < e->parts; ++p) {
+        IRL_LAUNCH(ctx, launch_synth_planes(seed, uint32_t(p), 1, uint32_t(e->M), uint32_t(e->K), e->mt,
+                                            e->db + p * e->nmod * 2 * e->M * e->ldk, e->ldk, ctx->stream));
+    }
+    IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    return IRL_OK;
+}
+
+static int ccmm_parts(irl_ccmm* e, size_t n, size_t part0, size_t nparts, uint16_t* out,
+                      cudaStream_t s) {
+    irl_ctx* ctx = e->ctx;
+    PpmmLaunch L = make_launch(e->mt);
+    L.a_planes = e->db + part0 * e->nmod * 2 * e->M * e->ldk;
+    L.b_planes = e->qplanes;
+    L.out = out;
+    L.M = uint32_t(e->M);
+    L.N = uint32_t(n);
+    L.K = uint32_t(e->K);
+    L.ldk = uint32_t(e->ldk);
+    L.parts = uint32_t(nparts);
+    return run_ppmm(ctx, L, e->kchunk, s);
+}
+
+int irl_ccmm_run_device(irl_ccmm* e, const uint16_t* q_res_dev, int q_ready, size_t n,
+                        size_t part0, size_t nparts, uint16_t* out_dev, void* stream) {
+    if (!e) return IRL_ERR_INVALID_ARGUMENT;
+    irl_ctx* ctx = e->ctx;
+    Guard g(ctx);
+    if (n == 0 || n > e->max_n) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: query width out of range");
+    if (part0 + nparts > e->parts) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: part range out of range");
+    cudaStream_t s = pick_stream(ctx, stream);
+    if (!q_ready) {
+        IRL_LAUNCH(ctx, launch_split_cols<uint16_t>(q_res_dev, n, e->K * n, uint32_t(e->K), uint32_t(n), e->mt,
+                                                    e->qplanes, e->ldk, nullptr, s));
+    }
+    // qplanes rows are laid out with stride n (not max_n): [nmod][2][n][ldk].
+    return ccmm_parts(e, n, part0, nparts, out_dev, s);
+}
+
+int irl_ccmm_run(irl_ccmm* e, const uint16_t* q_res_host, size_t n, uint16_t* out_host) {
+    if (!e) return IRL_ERR_INVALID_ARGUMENT;
+    irl_ctx* ctx = e->ctx;
+    Guard g(ctx);
+    if (n == 0 || n > e->max_n) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: query width out of range");
+    cudaStream_t s = ctx->stream;
+    IRL_CK(ctx, cudaMemcpyAsync(e->qres, q_res_host, e->nmod * e->K * n * 2, cudaMemcpyHostToDevice, s));
+    IRL_LAUNCH(ctx, launch_split_cols<uint16_t>(e->qres, n, e->K * n, uint32_t(e->K), uint32_t(n), e->mt,
+                                                e->qplanes, e->ldk, nullptr, s));
+    const size_t part_elems = e->nmod * n * e->M;
+    for (size_t p = 0; p < e->parts; ++p) {
+        int st = ccmm_parts(e, n, p, 1, e->out + p * part_elems, s);
+        if (st) return st;
+        IRL_CK(ctx, cudaEventRecord(e->part_done[p], s));
+        IRL_CK(ctx, cudaStreamWaitEvent(e->copy_stream, e->part_done[p], 0));
+        IRL_CK(ctx, cudaMemcpyAsync(out_host + p * part_elems, e->out + p * part_elems, part_elems * 2,
+                                    cudaMemcpyDeviceToHost, e->copy_stream));
+    }
+    IRL_CK(ctx, cudaStreamSynchronize(e->copy_stream));
+    IRL_CK(ctx, cudaStreamSynchronize(s));
+    return IRL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,566 @@
+// HBM-bound kernels around the PPMM GEMM: residue / digit split (the
+// reference's digit_decompose, modmat.cpp:86-106, and residue extraction,
+// modmat.cpp:168-176), CRT lift (modmat.cpp:178-193), synthetic planes,
+// and small helpers. All kernels are written for sm_100a: 16-byte vector
+// accesses where the layout allows, grids sized by the data.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels_aux.cuh"
+
+namespace irl {
+
+namespace {
+
+__device__ __forceinline__ void warp_max_atomic(int32_t v, int32_t* dst) {
+    v = __reduce_max_sync(0xffffffffu, v);
+    if ((threadIdx.x & 31) == 0 && dst) atomicMax(dst, v);
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t reduce_input(T x, const ModConst& c) {
+    if constexpr (sizeof(T) == 4) {
+        return mod_s32(static_cast<int32_t>(x), c.m, c.magic_m, c.off_m);
+    } else {
+        const uint32_t u = static_cast<uint32_t>(x);
+        return u < c.m ? u : mod_u32(u, c.m, c.magic_m);
+    }
+}
+
+// v in [0, m) -> (d0, d1); e == 1 keeps the residue in one centred digit.
+__device__ __forceinline__ void split_value(uint32_t v, const ModConst& c, int32_t& d0,
+                                            int32_t& d1) {
+    if (c.e == 2) {
+        digit_split(v, c, d0, d1);
+    } else {
+        const int32_t half = static_cast<int32_t>((c.p - 1) / 2);
+        d0 = static_cast<int32_t>(v) > half ? static_cast<int32_t>(v) - static_cast<int32_t>(c.p)
+                                            : static_cast<int32_t>(v);
+        d1 = 0;
+    }
+}
+
+__device__ __forceinline__ uint32_t pack4(int32_t a, int32_t b, int32_t c, int32_t d) {
+    return (static_cast<uint32_t>(a) & 0xFF) | ((static_cast<uint32_t>(b) & 0xFF) << 8) |
+           ((static_cast<uint32_t>(c) & 0xFF) << 16) | ((static_cast<uint32_t>(d) & 0xFF) << 24);
+}
+
+// ---------------------------------------------------------------------------
+// Row split: each thread produces 16 consecutive K positions of one row.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) split_rows_kernel(const T* __restrict__ in, size_t ld_in,
+                                                         size_t plane_stride, uint32_t rows,
+                                                         uint32_t cols, uint32_t groups,
+                                                         const __grid_constant__ ModTable mt,
+                                                         int8_t* __restrict__ planes,
+                                                         size_t ldk, SplitStats* stats) {
+    const uint32_t i = blockIdx.y;
+    const ModConst c = mt.mc[i];
+    const size_t gid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    int32_t m0 = 0, m1 = 0, mr = 0;
+    if (gid < static_cast<size_t>(rows) * groups) {
+        const uint32_t r = static_cast<uint32_t>(gid / groups);
+        const uint32_t c0 = static_cast<uint32_t>(gid % groups) * 16;
+        const T* src = in + i * plane_stride + static_cast<size_t>(r) * ld_in;
+        int32_t d0[16], d1[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const uint32_t col = c0 + j;
+            if (col < cols) {
+                const uint32_t v = reduce_input<T>(src[col], c);
+                split_value(v, c, d0[j], d1[j]);
+                m0 = max(m0, abs(d0[j]));
+                m1 = max(m1, abs(d1[j]));
+                mr = max(mr, static_cast<int32_t>(v));
+            } else {
+                d0[j] = 0;
+                d1[j] = 0;
+            }
+        }
+        int8_t* p0 = planes + (static_cast<size_t>(i) * 2 * rows + r) * ldk + c0;
+        int8_t* p1 = p0 + static_cast<size_t>(rows) * ldk;
+        uint4 w0, w1;
+        w0.x = pack4(d0[0], d0[1], d0[2], d0[3]);
+        w0.y = pack4(d0[4], d0[5], d0[6], d0[7]);
+        w0.z = pack4(d0[8], d0[9], d0[10], d0[11]);
+        w0.w = pack4(d0[12], d0[13], d0[14], d0[15]);
+        w1.x = pack4(d1[0], d1[1], d1[2], d1[3]);
+        w1.y = pack4(d1[4], d1[5], d1[6], d1[7]);
+        w1.z = pack4(d1[8], d1[9], d1[10], d1[11]);
+        w1.w = pack4(d1[12], d1[13], d1[14], d1[15]);
+        *reinterpret_cast<uint4*>(p0) = w0;
+        *reinterpret_cast<uint4*>(p1) = w1;
+    }
+    if (stats) {
+        warp_max_atomic(m0, &stats->v[i][0]);
+        warp_max_atomic(m1, &stats->v[i][1]);
+        warp_max_atomic(mr, &stats->v[i][2]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Transposing split of a K x N matrix: 64 (k) x 64 (n) tiles through smem.
+// ---------------------------------------------------------------------------
+constexpr int kTT = 64;
+constexpr int kTStride = 68;  // bytes per n-row in smem (17 words: conflict-free)
+
+template <typename T>
+__global__ void __launch_bounds__(256) split_cols_kernel(const T* __restrict__ in, size_t ld_in,
+                                                         size_t plane_stride, uint32_t K,
+                                                         uint32_t N,
+                                                         const __grid_constant__ ModTable mt,
+                                                         int8_t* __restrict__ planes,
+                                                         size_t ldk, SplitStats* stats) {
+    __shared__ __align__(16) int8_t s0[kTT * kTStride];
+    __shared__ __align__(16) int8_t s1[kTT * kTStride];
+    const uint32_t i = blockIdx.z;
+    const ModConst c = mt.mc[i];
+    const uint32_t k0 = blockIdx.x * kTT, n0 = blockIdx.y * kTT;
+    const uint32_t tn = threadIdx.x % kTT, tk = threadIdx.x / kTT;  // tk in 0..3
+    const T* src = in + i * plane_stride;
+    int32_t m0 = 0, m1 = 0, mr = 0;
+#pragma unroll 4
+    for (int kk = 0; kk < 16; ++kk) {
+        const uint32_t kl = tk * 16 + kk;
+        const uint32_t k = k0 + kl, n = n0 + tn;
+        int32_t d0 = 0, d1 = 0;
+        if (k < K && n < N) {
+            const uint32_t v = reduce_input<T>(src[static_cast<size_t>(k) * ld_in + n], c);
+            split_value(v, c, d0, d1);
+            m0 = max(m0, abs(d0));
+            m1 = max(m1, abs(d1));
+            mr = max(mr, static_cast<int32_t>(v));
+        }
+        s0[tn * kTStride + kl] = static_cast<int8_t>(d0);
+        s1[tn * kTStride + kl] = static_cast<int8_t>(d1);
+    }
+    __syncthreads();
+    const uint32_t nl = threadIdx.x / 4, chunk = threadIdx.x % 4;
+    const uint32_t n = n0 + nl, k = k0 + chunk * 16;
+    if (n < N && k < ldk) {
+        const uint32_t* a0 = reinterpret_cast<const uint32_t*>(s0 + nl * kTStride + chunk * 16);
+        const uint32_t* a1 = reinterpret_cast<const uint32_t*>(s1 + nl * kTStride + chunk * 16);
+        int8_t* p0 = planes + (static_cast<size_t>(i) * 2 * N + n) * ldk + k;
+        int8_t* p1 = p0 + static_cast<size_t>(N) * ldk;
+        *reinterpret_cast<uint4*>(p0) = make_uint4(a0[0], a0[1], a0[2], a0[3]);
+        *reinterpret_cast<uint4*>(p1) = make_uint4(a1[0], a1[1], a1[2], a1[3]);
+    }
+    if (stats) {
+        warp_max_atomic(m0, &stats->v[i][0]);
+        warp_max_atomic(m1, &stats->v[i][1]);
+        warp_max_atomic(mr, &stats->v[i][2]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Big-integer residue extraction + split.
+// x mod m = sum_j b_j (256^j mod m) mod m; the sum stays < 2^30 for
+// width <= 48 and m <= 2^16, so one Barrett reduction finishes it.
+// ---------------------------------------------------------------------------
+struct BigSplitArgs {
+    ModTable mt;
+    uint32_t coef[kMaxModuli][kMaxWidth];  // 256^j mod m_i
+};
+
+__global__ void __launch_bounds__(256) split_bigint_kernel(
+    const uint8_t* __restrict__ in, uint32_t width, uint32_t rows, uint32_t cols, int transpose,
+    const __grid_constant__ BigSplitArgs a, int8_t* __restrict__ planes, size_t ldk,
+    uint32_t dst_rows, uint32_t dst_row0, int32_t* __restrict__ raw_out, SplitStats* stats) {
+    const size_t gid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t total = static_cast<size_t>(rows) * cols;
+    const bool ok = gid < total;
+    // transpose: threads walk k fastest so plane writes stay coalesced.
+    uint32_t r = 0, cidx = 0;
+    if (ok) {
+        if (transpose) {
+            r = static_cast<uint32_t>(gid % rows);     // k
+            cidx = static_cast<uint32_t>(gid / rows);  // n
+        } else {
+            r = static_cast<uint32_t>(gid / cols);
+            cidx = static_cast<uint32_t>(gid % cols);
+        }
+    }
+    uint8_t bytes[kMaxWidth];
+    if (ok) {
+        const uint8_t* src = in + (static_cast<size_t>(r) * cols + cidx) * width;
+#pragma unroll 8
+        for (uint32_t j = 0; j < width; ++j) bytes[j] = src[j];
+    }
+    for (uint32_t i = 0; i < a.mt.n; ++i) {
+        const ModConst c = a.mt.mc[i];
+        int32_t d0 = 0, d1 = 0, v = 0;
+        if (ok) {
+            uint32_t s = 0;
+            for (uint32_t j = 0; j < width; ++j) s += bytes[j] * a.coef[i][j];
+            v = static_cast<int32_t>(mod_u32(s, c.m, c.magic_m));
+            if (c.e == 2) {
+                digit_split(static_cast<uint32_t>(v), c, d0, d1);
+            }
+        }
+        if (c.e == 2) {
+            if (ok) {
+                const uint32_t prow = (transpose ? cidx : r) + dst_row0;
+                const uint32_t pcol = transpose ? r : cidx;
+                const uint32_t prows = dst_rows;
+                int8_t* p0 = planes + (static_cast<size_t>(i) * 2 * prows + prow) * ldk + pcol;
+                p0[0] = static_cast<int8_t>(d0);
+                p0[static_cast<size_t>(prows) * ldk] = static_cast<int8_t>(d1);
+            }
+            if (stats) {
+                warp_max_atomic(abs(d0), &stats->v[i][0]);
+                warp_max_atomic(abs(d1), &stats->v[i][1]);
+            }
+        } else if (raw_out) {
+            if (ok) raw_out[static_cast<size_t>(i) * total + static_cast<size_t>(r) * cols + cidx] = v;
+        }
+        if (stats) warp_max_atomic(v, &stats->v[i][2]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// CRT lift. acc = sum_i (Q/m_i) * ((Q/m_i)^-1 r_i mod m_i) < nmod * Q <= 32 Q,
+// then conditional subtraction of 16Q, 8Q, 4Q, 2Q, Q.
+// ---------------------------------------------------------------------------
+struct CrtArgs {
+    CrtTable t;
+    ModConst mc[kMaxModuli];
+};
+
+__global__ void __launch_bounds__(256) crt_lift_kernel(const uint16_t* __restrict__ res,
+                                                       uint32_t M, uint32_t N,
+                                                       const __grid_constant__ CrtArgs a,
+                                                       uint8_t* __restrict__ out) {
+    const size_t gid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (gid >= static_cast<size_t>(M) * N) return;
+    const uint32_t m = static_cast<uint32_t>(gid % M), n = static_cast<uint32_t>(gid / M);
+    const uint32_t L = a.t.limbs;
+    uint32_t acc[kMaxQLimbs + 1];
+#pragma unroll
+    for (uint32_t j = 0; j <= kMaxQLimbs; ++j) acc[j] = 0;
+    for (uint32_t i = 0; i < a.t.nmod; ++i) {
+        const ModConst c = a.mc[i];
+        uint32_t r = res[(static_cast<size_t>(i) * N + n) * M + m];
+        r = r < c.m ? r : mod_u32(r, c.m, c.magic_m);
+        const uint32_t t = mod_u32(r * a.t.inv[i], c.m, c.magic_m);
+        uint64_t carry = 0;
+#pragma unroll
+        for (uint32_t j = 0; j < kMaxQLimbs; ++j) {
+            if (j < L) {
+                const uint64_t s = static_cast<uint64_t>(a.t.qi[i][j]) * t + acc[j] + carry;
+                acc[j] = static_cast<uint32_t>(s);
+                carry = s >> 32;
+            }
+        }
+        // propagate into the top limb(s)
+        for (uint32_t j = L; j <= kMaxQLimbs && carry; ++j) {
+            const uint64_t s = static_cast<uint64_t>(acc[j]) + carry;
+            acc[j] = static_cast<uint32_t>(s);
+            carry = s >> 32;
+        }
+    }
+    for (int s = 0; s < 5; ++s) {
+        const uint32_t* q = a.t.qmul[s];
+        // compare acc (L+1 limbs) >= q
+        int ge = 1;
+        for (int j = static_cast<int>(L); j >= 0; --j) {
+            if (acc[j] != q[j]) {
+                ge = acc[j] > q[j];
+                break;
+            }
+        }
+        if (ge) {
+            uint64_t borrow = 0;
+            for (uint32_t j = 0; j <= L; ++j) {
+                const uint64_t d = static_cast<uint64_t>(acc[j]) - q[j] - borrow;
+                acc[j] = static_cast<uint32_t>(d);
+                borrow = (d >> 63) & 1;
+            }
+        }
+    }
+    uint8_t* dst = out + (static_cast<size_t>(m) * N + n) * a.t.width;
+    for (uint32_t b = 0; b < a.t.width; ++b) {
+        const uint32_t limb = b / 4;
+        dst[b] = limb <= L ? static_cast<uint8_t>(acc[limb] >> (8 * (b % 4))) : 0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Counter-based synthetic residues (bit-identical to irl_synth_residue).
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__host__ __device__ __forceinline__ uint32_t synth_residue(uint64_t seed_mixed, uint32_t stream,
+                                                           uint32_t plane, uint32_t row,
+                                                           uint32_t col, uint32_t m) {
+    const uint64_t key = (static_cast<uint64_t>(stream & 0xFF) << 56) |
+                         (static_cast<uint64_t>(plane & 0xFF) << 48) |
+                         (static_cast<uint64_t>(row & 0xFFFFFF) << 24) |
+                         static_cast<uint64_t>(col & 0xFFFFFF);
+    const uint64_t x = mix64(key ^ seed_mixed);
+    return static_cast<uint32_t>(((x >> 32) * static_cast<uint64_t>(m)) >> 32);
+}
+
+__global__ void __launch_bounds__(256) synth_planes_kernel(uint64_t seed_mixed, uint32_t part0,
+                                                           uint32_t rows, uint32_t cols,
+                                                           uint32_t groups,
+                                                           const __grid_constant__ ModTable mt,
+                                                           int8_t* __restrict__ planes,
+                                                           size_t ldk) {
+    const uint32_t i = blockIdx.y, g = blockIdx.z;
+    const ModConst c = mt.mc[i];
+    const size_t gid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (gid >= static_cast<size_t>(rows) * groups) return;
+    const uint32_t r = static_cast<uint32_t>(gid / groups);
+    const uint32_t c0 = static_cast<uint32_t>(gid % groups) * 16;
+    int32_t d0[16], d1[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        if (c0 + j < cols) {
+            const uint32_t v = synth_residue(seed_mixed, part0 + g, i, r, c0 + j, c.m);
+            split_value(v, c, d0[j], d1[j]);
+        } else {
+            d0[j] = 0;
+            d1[j] = 0;
+        }
+    }
+    int8_t* p0 =
+        planes + ((static_cast<size_t>(g) * mt.n + i) * 2 * rows + r) * ldk + c0;
+    int8_t* p1 = p0 + static_cast<size_t>(rows) * ldk;
+    uint4 w0, w1;
+    w0.x = pack4(d0[0], d0[1], d0[2], d0[3]);
+    w0.y = pack4(d0[4], d0[5], d0[6], d0[7]);
+    w0.z = pack4(d0[8], d0[9], d0[10], d0[11]);
+    w0.w = pack4(d0[12], d0[13], d0[14], d0[15]);
+    w1.x = pack4(d1[0], d1[1], d1[2], d1[3]);
+    w1.y = pack4(d1[4], d1[5], d1[6], d1[7]);
+    w1.z = pack4(d1[8], d1[9], d1[10], d1[11]);
+    w1.w = pack4(d1[12], d1[13], d1[14], d1[15]);
+    *reinterpret_cast<uint4*>(p0) = w0;
+    *reinterpret_cast<uint4*>(p1) = w1;
+}
+
+// ---------------------------------------------------------------------------
+// Small helpers
+// ---------------------------------------------------------------------------
+__global__ void gemm_i32_kernel(const int32_t* __restrict__ a, const int32_t* __restrict__ b,
+                                int32_t* __restrict__ c, uint32_t M, uint32_t K, uint32_t N) {
+    __shared__ int32_t sa[16][17], sb[16][17];
+    const uint32_t row = blockIdx.y * 16 + threadIdx.y, col = blockIdx.x * 16 + threadIdx.x;
+    uint32_t acc = 0;  // wrap-around int32 arithmetic, like the reference's int32 loop
+    for (uint32_t k0 = 0; k0 < K; k0 += 16) {
+        sa[threadIdx.y][threadIdx.x] =
+            (row < M && k0 + threadIdx.x < K) ? a[static_cast<size_t>(row) * K + k0 + threadIdx.x] : 0;
+        sb[threadIdx.y][threadIdx.x] =
+            (col < N && k0 + threadIdx.y < K) ? b[static_cast<size_t>(k0 + threadIdx.y) * N + col] : 0;
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < 16; ++t)
+            acc += static_cast<uint32_t>(sa[threadIdx.y][t]) * static_cast<uint32_t>(sb[t][threadIdx.x]);
+        __syncthreads();
+    }
+    if (row < M && col < N) c[static_cast<size_t>(row) * N + col] = static_cast<int32_t>(acc);
+}
+
+__global__ void transpose_u16_i32_kernel(const uint16_t* __restrict__ in, uint32_t M, uint32_t N,
+                                         int32_t* __restrict__ out) {
+    __shared__ uint16_t t[32][33];
+    const uint32_t m0 = blockIdx.x * 32, n0 = blockIdx.y * 32;
+    for (uint32_t j = threadIdx.y; j < 32; j += 8) {
+        const uint32_t n = n0 + j, m = m0 + threadIdx.x;
+        t[j][threadIdx.x] = (n < N && m < M) ? in[static_cast<size_t>(n) * M + m] : 0;
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.y; j < 32; j += 8) {
+        const uint32_t m = m0 + j, n = n0 + threadIdx.x;
+        if (m < M && n < N) out[static_cast<size_t>(m) * N + n] = t[threadIdx.x][j];
+    }
+}
+
+__global__ void reduce_raw_kernel(const int32_t* __restrict__ raw, uint32_t M, uint32_t N,
+                                  uint32_t idx, ModConst c, uint16_t* __restrict__ res) {
+    const size_t gid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (gid >= static_cast<size_t>(M) * N) return;
+    const uint32_t m = static_cast<uint32_t>(gid % M), n = static_cast<uint32_t>(gid / M);
+    const int32_t v = raw[static_cast<size_t>(m) * N + n];
+    res[(static_cast<size_t>(idx) * N + n) * M + m] =
+        static_cast<uint16_t>(mod_s32(v, c.m, c.magic_m, c.off_m));
+}
+
+__global__ void digit_decompose_kernel(const int32_t* __restrict__ in, size_t count, ModConst c,
+                                       int32_t* __restrict__ d0, int32_t* __restrict__ d1) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const uint32_t v = mod_s32(in[i], c.m, c.magic_m, c.off_m);
+    int32_t a, b;
+    digit_split(v, c, a, b);
+    d0[i] = a;
+    d1[i] = b;
+}
+
+__global__ void digit_recompose_kernel(const int32_t* __restrict__ d0,
+                                       const int32_t* __restrict__ d1, size_t count, ModConst c,
+                                       int32_t* __restrict__ out) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    // int32 arithmetic exactly as modmat.cpp:112-116 (wrapping multiply-add,
+    // truncating %, then shift into [0, p^2)).
+    const int32_t v = static_cast<int32_t>(static_cast<uint32_t>(d0[i]) +
+                                           c.p * static_cast<uint32_t>(d1[i]));
+    int32_t r = v % static_cast<int32_t>(c.m);
+    if (r < 0) r += static_cast<int32_t>(c.m);
+    out[i] = static_cast<int32_t>(r);
+}
+
+__global__ void absmax_kernel(const int32_t* __restrict__ x, size_t count, int32_t* dst) {
+    int32_t m = 0;
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int32_t v = x[i];
+        // |INT32_MIN| saturates to INT32_MAX: still far beyond any valid bound.
+        m = max(m, v == INT32_MIN ? INT32_MAX : abs(v));
+    }
+    warp_max_atomic(m, dst);
+}
+
+inline unsigned blocks_for(size_t n, unsigned t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+}  // namespace
+
+template <typename T>
+cudaError_t launch_split_rows(const T* in, size_t ld_in, size_t plane_stride, uint32_t rows,
+                              uint32_t cols, const ModTable& mt, int8_t* planes, size_t ldk,
+                              SplitStats* stats, cudaStream_t s) {
+    if (rows == 0 || ldk == 0 || mt.n == 0) return cudaSuccess;
+    const uint32_t groups = static_cast<uint32_t>(ldk / 16);
+    const dim3 grid(blocks_for(static_cast<size_t>(rows) * groups, 256), mt.n);
+    split_rows_kernel<T><<<grid, 256, 0, s>>>(in, ld_in, plane_stride, rows, cols, groups, mt,
+                                              planes, ldk, stats);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_split_cols(const T* in, size_t ld_in, size_t plane_stride, uint32_t k,
+                              uint32_t n, const ModTable& mt, int8_t* planes, size_t ldk,
+                              SplitStats* stats, cudaStream_t s) {
+    if (n == 0 || ldk == 0 || mt.n == 0) return cudaSuccess;
+    const dim3 grid(blocks_for(ldk, kTT), blocks_for(n, kTT), mt.n);
+    split_cols_kernel<T><<<grid, 256, 0, s>>>(in, ld_in, plane_stride, k, n, mt, planes, ldk, stats);
+    return cudaGetLastError();
+}
+
+template cudaError_t launch_split_rows<uint16_t>(const uint16_t*, size_t, size_t, uint32_t,
+                                                 uint32_t, const ModTable&, int8_t*, size_t,
+                                                 SplitStats*, cudaStream_t);
+template cudaError_t launch_split_rows<int32_t>(const int32_t*, size_t, size_t, uint32_t, uint32_t,
+                                                const ModTable&, int8_t*, size_t, SplitStats*,
+                                                cudaStream_t);
+template cudaError_t launch_split_cols<uint16_t>(const uint16_t*, size_t, size_t, uint32_t,
+                                                 uint32_t, const ModTable&, int8_t*, size_t,
+                                                 SplitStats*, cudaStream_t);
+template cudaError_t launch_split_cols<int32_t>(const int32_t*, size_t, size_t, uint32_t, uint32_t,
+                                                const ModTable&, int8_t*, size_t, SplitStats*,
+                                                cudaStream_t);
+
+cudaError_t launch_split_bigint(const uint8_t* in, uint32_t width, uint32_t rows, uint32_t cols,
+                                int transpose, const ModTable& mt, int8_t* planes, size_t ldk,
+                                uint32_t dst_rows, uint32_t dst_row0, int32_t* raw_out,
+                                SplitStats* stats, cudaStream_t s) {
+    if (width > kMaxWidth || mt.n > kMaxModuli) return cudaErrorInvalidValue;
+    const size_t total = static_cast<size_t>(rows) * cols;
+    if (total == 0) return cudaSuccess;
+    BigSplitArgs a{};
+    a.mt = mt;
+    for (uint32_t i = 0; i < mt.n; ++i) {
+        uint64_t pw = 1 % mt.mc[i].m;
+        for (uint32_t j = 0; j < width; ++j) {
+            a.coef[i][j] = static_cast<uint32_t>(pw);
+            pw = (pw * 256) % mt.mc[i].m;
+        }
+    }
+    split_bigint_kernel<<<blocks_for(total, 256), 256, 0, s>>>(
+        in, width, rows, cols, transpose, a, planes, ldk, dst_rows, dst_row0, raw_out, stats);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_crt_lift(const uint16_t* res, uint32_t M, uint32_t N, const CrtTable& t,
+                            uint8_t* out, cudaStream_t s) {
+    const size_t total = static_cast<size_t>(M) * N;
+    if (total == 0) return cudaSuccess;
+    CrtArgs a{};
+    a.t = t;
+    for (uint32_t i = 0; i < t.nmod; ++i) {
+        a.mc[i] = make_modconst(t.m[i], 1);
+    }
+    crt_lift_kernel<<<blocks_for(total, 256), 256, 0, s>>>(res, M, N, a, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_synth_planes(uint64_t seed, uint32_t part0, uint32_t parts, uint32_t rows,
+                                uint32_t cols, const ModTable& mt, int8_t* planes, size_t ldk,
+                                cudaStream_t s) {
+    if (rows == 0 || parts == 0 || mt.n == 0) return cudaSuccess;
+    const uint32_t groups = static_cast<uint32_t>(ldk / 16);
+    const dim3 grid(blocks_for(static_cast<size_t>(rows) * groups, 256), mt.n, parts);
+    synth_planes_kernel<<<grid, 256, 0, s>>>(mix64(seed), part0, rows, cols, groups, mt, planes, ldk);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_i32(const int32_t* a, const int32_t* b, int32_t* c, uint32_t m, uint32_t k,
+                            uint32_t n, cudaStream_t s) {
+    if (m == 0 || n == 0) return cudaSuccess;
+    const dim3 grid(blocks_for(n, 16), blocks_for(m, 16));
+    gemm_i32_kernel<<<grid, dim3(16, 16), 0, s>>>(a, b, c, m, k, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_transpose_u16_to_i32(const uint16_t* in, uint32_t M, uint32_t N, int32_t* out,
+                                        cudaStream_t s) {
+    if (M == 0 || N == 0) return cudaSuccess;
+    const dim3 grid(blocks_for(M, 32), blocks_for(N, 32));
+    transpose_u16_i32_kernel<<<grid, dim3(32, 8), 0, s>>>(in, M, N, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_raw(const int32_t* raw, uint32_t M, uint32_t N, uint32_t mod_index,
+                              const ModConst& mc, uint16_t* res, cudaStream_t s) {
+    const size_t total = static_cast<size_t>(M) * N;
+    if (total == 0) return cudaSuccess;
+    reduce_raw_kernel<<<blocks_for(total, 256), 256, 0, s>>>(raw, M, N, mod_index, mc, res);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_digit_decompose(const int32_t* in, size_t count, const ModConst& mc,
+                                   int32_t* d0, int32_t* d1, cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    digit_decompose_kernel<<<blocks_for(count, 256), 256, 0, s>>>(in, count, mc, d0, d1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_digit_recompose(const int32_t* d0, const int32_t* d1, size_t count,
+                                   const ModConst& mc, int32_t* out, cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    digit_recompose_kernel<<<blocks_for(count, 256), 256, 0, s>>>(d0, d1, count, mc, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_absmax_i32(const int32_t* x, size_t count, int32_t* dst, cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    unsigned b = blocks_for(count, 256);
+    if (b > 4096) b = 4096;
+    absmax_kernel<<<b, 256, 0, s>>>(x, count, dst);
+    return cudaGetLastError();
+}
+
+uint32_t synth_residue_host(uint64_t seed, uint32_t stream, uint32_t plane, uint32_t row,
+                            uint32_t col, uint32_t m) {
+    return synth_residue(mix64(seed), stream, plane, row, col, m);
+}
+
+}  // namespace irl

@@ -1,0 +1,96 @@
+// Internal launch interface of the HBM-bound kernels around the PPMM GEMM.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "modarith.cuh"
+
+namespace irl {
+
+constexpr uint32_t kMaxModuli = 32;
+constexpr uint32_t kMaxQLimbs = 12;  // Q < 2^384
+constexpr uint32_t kMaxWidth = 48;   // bytes per mod-Q entry
+
+// Per-modulus running maxima gathered by the split kernels, used for the
+// reference's data-dependent AccumulationOverflowRisk precheck
+// (modmat.cpp:122-129): [0] = max|d0|, [1] = max|d1|, [2] = max raw residue.
+struct SplitStats {
+    int32_t v[kMaxModuli][3];
+};
+
+struct ModTable {
+    uint32_t n;
+    ModConst mc[kMaxModuli];
+};
+
+// Residues (or arbitrary int32) -> centred digit planes, no transpose:
+// in[i][r][c] (ld_in, plane stride in elements) -> planes[i][d][r][ldk].
+template <typename T>
+cudaError_t launch_split_rows(const T* in, size_t ld_in, size_t plane_stride, uint32_t rows,
+                              uint32_t cols, const ModTable& mt, int8_t* planes, size_t ldk,
+                              SplitStats* stats, cudaStream_t s);
+
+// Transposing variant: in[i][k][n] (a K x N matrix) -> planes[i][d][n][ldk].
+template <typename T>
+cudaError_t launch_split_cols(const T* in, size_t ld_in, size_t plane_stride, uint32_t k,
+                              uint32_t n, const ModTable& mt, int8_t* planes, size_t ldk,
+                              SplitStats* stats, cudaStream_t s);
+
+// width-byte little-endian mod-Q entries -> residues mod m_i -> digit planes.
+// transpose=0: [rows][cols] -> planes[i][d][rows][ldk];
+// transpose=1: [rows=K][cols=N] -> planes[i][d][N][ldk].
+// Moduli with e == 1 are emitted as raw residues into raw_out[i][rows][cols]
+// (int32) instead of planes (nullptr if none).
+// dst_rows / dst_row0: row count of each destination plane and the row
+// offset this call writes at (lets a large matrix be split in row chunks).
+cudaError_t launch_split_bigint(const uint8_t* in, uint32_t width, uint32_t rows, uint32_t cols,
+                                int transpose, const ModTable& mt, int8_t* planes, size_t ldk,
+                                uint32_t dst_rows, uint32_t dst_row0, int32_t* raw_out,
+                                SplitStats* stats, cudaStream_t s);
+
+// max |x| over an int32 array, atomically folded into *dst.
+cudaError_t launch_absmax_i32(const int32_t* x, size_t count, int32_t* dst, cudaStream_t s);
+
+// CRT lift: res[i][N][M] (uint16 residues) -> out[m][n] width-byte entries mod Q.
+struct CrtTable {
+    uint32_t nmod, limbs, width;
+    uint32_t m[kMaxModuli];
+    uint32_t inv[kMaxModuli];                     // (Q/m_i)^-1 mod m_i
+    uint32_t qi[kMaxModuli][kMaxQLimbs];          // Q/m_i
+    uint32_t qmul[5][kMaxQLimbs + 1];             // 16Q, 8Q, 4Q, 2Q, Q
+};
+cudaError_t launch_crt_lift(const uint16_t* res, uint32_t M, uint32_t N, const CrtTable& t,
+                            uint8_t* out, cudaStream_t s);
+
+// Synthetic database planes: planes[g][i][d][r][ldk] from the counter RNG,
+// residue = synth(seed, stream=part0+g, plane=i, row, col, m_i).
+cudaError_t launch_synth_planes(uint64_t seed, uint32_t part0, uint32_t parts, uint32_t rows,
+                                uint32_t cols, const ModTable& mt, int8_t* planes, size_t ldk,
+                                cudaStream_t s);
+
+// int32 GEMM with int32 (wrapping) accumulation, row-major: C = A B.
+cudaError_t launch_gemm_i32(const int32_t* a, const int32_t* b, int32_t* c, uint32_t m,
+                            uint32_t k, uint32_t n, cudaStream_t s);
+
+// out[r][c] (int32, row-major M x N) = in[c][r] (uint16 [N][M]); optional mod.
+cudaError_t launch_transpose_u16_to_i32(const uint16_t* in, uint32_t M, uint32_t N, int32_t* out,
+                                        cudaStream_t s);
+
+// res[i][n][m] (uint16) = raw[i][m][n] mod m_i  (int32 raw products of e=1 moduli).
+cudaError_t launch_reduce_raw(const int32_t* raw, uint32_t M, uint32_t N, uint32_t mod_index,
+                              const ModConst& mc, uint16_t* res, cudaStream_t s);
+
+// Elementwise digit_decompose / digit_recompose on int32 arrays.
+cudaError_t launch_digit_decompose(const int32_t* in, size_t count, const ModConst& mc,
+                                   int32_t* d0, int32_t* d1, cudaStream_t s);
+cudaError_t launch_digit_recompose(const int32_t* d0, const int32_t* d1, size_t count,
+                                   const ModConst& mc, int32_t* out, cudaStream_t s);
+
+// Host mirror of the device generator.
+uint32_t synth_residue_host(uint64_t seed, uint32_t stream, uint32_t plane, uint32_t row,
+                            uint32_t col, uint32_t m);
+
+}  // namespace irl

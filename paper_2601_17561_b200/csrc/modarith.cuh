@@ -24,8 +24,9 @@ __host__ __device__ inline ModConst make_modconst(uint32_t p, uint32_t e) {
     c.p = p;
     c.e = e;
     c.m = e == 2 ? p * p : p;
-    c.magic_p = static_cast<uint32_t>((1ull << 32) / p);
-    c.magic_m = static_cast<uint32_t>((1ull << 32) / c.m);
+    // m = 1 would need 2^32; 0xFFFFFFFF still leaves r in [0, 2m) (exact).
+    c.magic_p = p > 1 ? static_cast<uint32_t>((1ull << 32) / p) : 0xFFFFFFFFu;
+    c.magic_m = c.m > 1 ? static_cast<uint32_t>((1ull << 32) / c.m) : 0xFFFFFFFFu;
     c.off_p = static_cast<uint32_t>((1ull << 31) % p);
     c.off_m = static_cast<uint32_t>((1ull << 31) % c.m);
     return c;
