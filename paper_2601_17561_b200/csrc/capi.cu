@@ -448,11 +448,17 @@ int irl_gemm_mod_psq(irl_ctx* ctx, const int32_t* a, const int32_t* b, int32_t* 
     const size_t ldk = round16(std::max<size_t>(k, 1));
     const size_t na = m * k, nb = k * n;
     const size_t pa = 2 * m * ldk, pb = 2 * n * ldk;  // plane bytes
-    const size_t off_b = na * 4, off_pa = off_b + nb * 4, off_pb = round16(off_pa + pa),
-                 off_o = round16(off_pb + pb), off_c = round16(off_o + m * n * 2);
-    IRL_CK(ctx, ctx->ws[0].ensure(off_c + m * n * 4 + 16));
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off = (off + bytes + 127) / 128 * 128;  // TMA / 16-byte vector alignment
+        return o;
+    };
+    const size_t off_a = take(na * 4), off_b = take(nb * 4), off_pa = take(pa), off_pb = take(pb),
+                 off_o = take(m * n * 2), off_c = take(m * n * 4);
+    IRL_CK(ctx, ctx->ws[0].ensure(off + 16));
     uint8_t* base = ctx->ws[0].as<uint8_t>();
-    int32_t* da = reinterpret_cast<int32_t*>(base);
+    int32_t* da = reinterpret_cast<int32_t*>(base + off_a);
     int32_t* db = reinterpret_cast<int32_t*>(base + off_b);
     int8_t* pla = reinterpret_cast<int8_t*>(base + off_pa);
     int8_t* plb = reinterpret_cast<int8_t*>(base + off_pb);
@@ -524,7 +530,7 @@ int irl_gemm_mod_Q(irl_ctx* ctx, const uint8_t* a, const uint8_t* b, uint8_t* c,
     size_t off = 0;
     auto take = [&](size_t bytes) {
         const size_t o = off;
-        off = round16(off + bytes);
+        off = (off + bytes + 127) / 128 * 128;
         return o;
     };
     const size_t o_a = take(ba), o_b = take(bb), o_pa = take(pa), o_pb = take(pb),
