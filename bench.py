@@ -1,0 +1,392 @@
+"""Benchmark of the RGSW CCMM hot path on B200 (BASELINE.json north star).
+
+Workload (BASELINE.json configs[3] at N GPUs; configs[1-2] are its per-slice
+pieces): a 32-eye x 31-rotation query batch (N = 992 columns) against the full
+database of 7 * 2^14 templates in the paper's 8-part layout (shared a-part +
+7 b-part slices of 2^14 rows), K = d2 + N_qry = 2^14 + 2^13 = 24576, modulus
+Q = prod_{127<=p<=253} p^2 (24 primes, 361 bits). One step = split the query
+into digit planes + 8 K-concatenated PPMMs mod Q (4 RGSW PPMMs per a/b pair)
++ the a-part result broadcast (N > 1). Inputs are synthetic residues from the
+counter generator (uniform mod p^2), DB planes resident in HBM (144 GiB at
+N = 1, far above L2, so no flush is needed between steps).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = ("CCMM latency per 32×31 query batch vs 7·2^14 DB; int8 TOPS and % of tensor peak")
+UNIT = "int8 TOPS (6*P*M*N*K per part, unpadded)"
+DATASHEET_INT8_TOPS = 4500.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--parts", type=int, default=8)
+    ap.add_argument("--rows", type=int, default=1 << 14, help="templates per part (M)")
+    ap.add_argument("--k", type=int, default=(1 << 14) + (1 << 13), help="d2 + N_qry")
+    ap.add_argument("--eyes", type=int, default=32)
+    ap.add_argument("--rot", type=int, default=31)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-rows", type=int, default=32, help="DB rows per task in the CPU sample")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference leg (oracle/_ref = unmodified reference modmat.cpp; else the port)
+# ---------------------------------------------------------------------------
+
+def cpu_reference_sample(args, moduli, q_host=None, rows=None, threads=None, parts=(0, 1)):
+    """Times the reference gemm_mod_psq (modmat.cpp:143-160) on a bounded sample
+    of the same workload: `rows` DB rows x full K x all N query columns, for
+    every modulus of parts `parts`; tasks spread over host threads (the
+    function is pure). Returns rates in the bench's unit."""
+    import ctypes as C
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as ol
+
+    rows = rows or args.cpu_rows
+    threads = threads or os.cpu_count() or 1
+    K, N = args.k, args.eyes * args.rot
+    if q_host is None:
+        from paper_2601_17561_b200.ccmm import synth_query
+        q_host = synth_query(2, K, N, moduli)
+    kind = "reference" if ol.ref_available() else "port"
+    A, B, Cc, P = [], [], [], []
+    for part in parts:
+        for i, m in enumerate(moduli):
+            A.append(np.ascontiguousarray(ol.synth_block(args.seed, part, i, 0, rows, 0, K, m).astype(np.int32)))
+            B.append(np.ascontiguousarray(q_host[i].astype(np.int32)))
+            Cc.append(np.zeros((rows, N), np.int32))
+            P.append(int(round(m ** 0.5)))
+    ntasks = len(A)
+    t0 = time.perf_counter()
+    if kind == "reference":
+        lib = ol.ref()
+        arr = lambda xs: (ol.i32p * len(xs))(*[x.ctypes.data_as(ol.i32p) for x in xs])  # noqa: E731
+        st = lib.ref_gemm_mod_psq_batch(arr(A), arr(B), arr(Cc), (C.c_uint32 * ntasks)(*P), ntasks, rows, K, N,
+                                        threads)
+        assert st == 0, lib.ref_last_error()
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+
+        def task(j):
+            st, c = ol.orc_gemm_mod_psq(A[j], B[j], P[j])
+            assert st == 0
+            Cc[j][...] = c
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(task, range(ntasks)))
+    secs = time.perf_counter() - t0
+    ops = 6.0 * rows * N * K * ntasks
+    return {"kind": kind, "seconds": secs, "ops": ops, "tops": ops / secs / 1e12, "threads": threads,
+            "rows": rows, "tasks": ntasks, "outputs": Cc, "parts": parts,
+            "sample": (f"{rows} DB rows x K={K} x N={N} for each of {len(moduli)} moduli of parts "
+                       f"{list(parts)} ({ntasks} gemm_mod_psq calls, {kind} code, {threads} threads); "
+                       f"rate extrapolated linearly in M (cost ~ M*N*K)")}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2601_17561_b200.modmat import build_paper_basis
+    b = build_paper_basis()
+    moduli = [m.value() for m in b.moduli]
+    N = args.eyes * args.rot
+    total_ops = 6.0 * len(moduli) * args.rows * N * args.k * args.parts
+    sys.path.insert(0, str(ROOT / "tests"))
+    from paper_2601_17561_b200.ccmm import synth_query  # host-side generator only
+    q = synth_query(2, args.k, N, moduli)
+    rates = []
+    last = None
+    for it in range(args.warmup + args.steps):
+        r = cpu_reference_sample(args, moduli, q_host=q, rows=max(8, args.cpu_rows // 2))
+        if it >= args.warmup:
+            rates.append(r["tops"])
+        last = r
+    v = statistics.median(rates)
+    ms = total_ops / (v * 1e12) * 1e3
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int32 (int8 digits)", "data": "synthetic",
+            "impl": "reference",
+            "config": config_dict(args, len(moduli)),
+            "ccmm_latency_ms": ms,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": last["threads"], "kind": last["kind"],
+                             "sample": last["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(args, nmod):
+    N = args.eyes * args.rot
+    return {"workload": "c4: 32x31 query batch vs full DB 7*2^14 templates, 8-part RGSW layout (a-part + 7 b-parts)",
+            "parts": args.parts, "templates_per_part": args.rows, "K": args.k, "query_columns": N,
+            "eyes": args.eyes, "rotations": args.rot, "moduli": nmod, "log2_Q": 360.8156,
+            "digit_planes": 2 * nmod, "parallelism": f"db-slices over {args.gpus} GPU(s)",
+            "l2": "inputs larger than L2 (DB digit planes, 18 GiB per part)"}
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2601_17561_b200.ccmm import CcmmEngine, staging_tensors, synth_query
+    from paper_2601_17561_b200.dist import ShardedStep, part_range
+    from paper_2601_17561_b200.modmat import Context, build_paper_basis
+
+    basis = build_paper_basis()
+    nmod = len(basis.moduli)
+    N = args.eyes * args.rot
+    M, K = args.rows, args.k
+    local_parts = part_range(rank, world, args.parts)
+    ctx = Context(local)
+    eng = CcmmEngine(parts=local_parts.count, m=M, k=K, max_n=N, basis=basis, ctx=ctx)
+    eng.synth_db(seed=args.seed, first_part=local_parts.first)
+    moduli = eng.moduli
+    q_host = synth_query(2, K, N, moduli)
+    q_pinned = torch.from_numpy(q_host.view(np.int16)).pin_memory()
+    q_dev, out_dev = staging_tensors(eng, N)
+    q_dev.copy_(q_pinned)
+    a_recv = None
+    if world > 1 and rank != 0:
+        a_recv = torch.empty((nmod, N, M), dtype=torch.int16, device="cuda")
+    stream = torch.cuda.current_stream()
+    gemm_events = []
+
+    def run_parts(first_local, count):
+        # split the query into digit planes once per step (before the first
+        # local PPMM), then time the PPMM launch itself for the roofline
+        if first_local == 0:
+            eng.run_device(None, N, None, part0=0, nparts=0, q_ready=False, stream=stream.cuda_stream)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.run_device(None, N, None, part0=first_local, nparts=count, q_ready=True, stream=stream.cuda_stream)
+        e1.record(stream)
+        gemm_events.append((e0, e1, count))
+
+    def a_out():
+        return out_dev[0] if rank == 0 else a_recv
+
+    step = ShardedStep(rank, world, run_parts, a_out, parts=args.parts)
+
+    def one_step():
+        w = step()
+        if w is not None:
+            w.wait()
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    gemm_events.clear()
+    if world > 1:
+        dist.barrier()
+    launches0 = ctx.launches
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        t_start.record(stream)
+        for _ in range(args.steps):
+            one_step()
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = ctx.launches - launches0
+    ms = t_start.elapsed_time(t_end) / args.steps
+    t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    total_ops = 6.0 * nmod * M * N * K * args.parts
+    value = total_ops / (ms_max * 1e-3) / 1e12
+
+    # dominant kernel: the PPMM launch (split is fused into the first launch's
+    # stream slot but measured separately below)
+    g_ms = [a.elapsed_time(b) for a, b, _ in gemm_events]
+    g_parts = [c for _, _, c in gemm_events]
+    ops_per_part = 6.0 * nmod * M * N * K
+    launch_ops = statistics.mean(g_parts) * ops_per_part
+    launch_ms = statistics.mean(g_ms)
+    achieved = launch_ops / (launch_ms * 1e-3) / 1e12
+    peaks = {}
+    pk_path = ROOT / "MEASURED_PEAKS.json"
+    if pk_path.exists():
+        peaks = json.loads(pk_path.read_text())
+    if "bf16_tflops_sustained" in peaks:
+        peak = 2.0 * float(peaks["bf16_tflops_sustained"])
+        peak_src = "2 x measured cuBLAS bf16 sustained (MEASURED_PEAKS.json); int8 dense = 2x bf16 dense on sm_100"
+    else:
+        peak = 2.0 * 1400.0
+        peak_src = "2 x fallback bf16 sustained 1.4 PF/s (B200_PROFILING.md)"
+    traffic = None
+    tr_path = ROOT / "profiles" / "ppmm_traffic.json"
+    if tr_path.exists():
+        tr = json.loads(tr_path.read_text())
+        traffic = tr.get("bytes_per_part", 0) * statistics.mean(g_parts) or None
+
+    # ---- end to end through the public C ABI with host buffers -------------
+    e2e = None
+    if not args.no_e2e:
+        out_host = torch.empty((local_parts.count, nmod, N, M), dtype=torch.int16).pin_memory()
+        q_np = q_pinned.numpy().view(np.uint16)
+        o_np = out_host.numpy().view(np.uint16)
+        if world > 1:
+            dist.barrier()
+        for _ in range(max(1, args.warmup - 1)):
+            eng.run(q_np, o_np)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            eng.run(q_np, o_np)  # H2D query, split, all local PPMMs, D2H outputs
+            if world > 1:
+                # the a-part result exchange stays on the device
+                w = dist.broadcast(a_out(), src=0, async_op=True)
+                w.wait()
+                torch.cuda.synchronize()
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+        tt = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+        e2e = {"value": total_ops / (e2e_ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(q_host.nbytes),
+               "d2h_bytes_per_step": int(local_parts.count * nmod * N * M * 2),
+               "call": "irl_ccmm_run (include/irl_capi.h) with pinned host buffers"}
+
+    # ---- CPU baseline (rank 0, N = 1) with a bit-exact check of its rows ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = cpu_reference_sample(args, moduli, q_host=q_host)
+        gpu_rows = out_dev[:, :, :, : r["rows"]].cpu().numpy().view(np.uint16)
+        exact = True
+        j = 0
+        for part in r["parts"]:
+            for i in range(nmod):
+                exact &= bool((r["outputs"][j] == gpu_rows[part, i].T).all())
+                j += 1
+        cpu = {"value": r["tops"], "unit": UNIT, "cores": r["threads"], "kind": r["kind"],
+               "sample": r["sample"], "seconds": r["seconds"], "bit_exact_vs_gpu": exact,
+               "extrapolated_ccmm_latency_s": total_ops / (r["tops"] * 1e12)}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "int8 digits, int32 accumulate",
+                "data": "synthetic residues (counter RNG, uniform mod p^2)",
+                "config": config_dict(args, nmod),
+                "ccmm_latency_ms": ms_max,
+                "tensor_peak_frac": value / peak,
+                "tensor_peak_frac_datasheet": value / DATASHEET_INT8_TOPS,
+                "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS",
+                             "frac": achieved / peak, "traffic": traffic,
+                             "kernel": "ppmm_i8_sm100_kernel", "launch_ms": launch_ms,
+                             "ops_per_launch": launch_ops, "peak_source": peak_src,
+                             "frac_of_datasheet_4500": achieved / DATASHEET_INT8_TOPS},
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

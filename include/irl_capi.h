@@ -142,8 +142,9 @@ int irl_ccmm_destroy(irl_ccmm* e);
 int irl_ccmm_load_part(irl_ccmm* e, size_t part, const uint16_t* res, int res_on_device);
 /* Register part `part` from width-byte mod-Q entries [M][K] (host pointer). */
 int irl_ccmm_load_part_bigint(irl_ccmm* e, size_t part, const uint8_t* entries, size_t width);
-/* Fill every part with synthetic residues irl_synth_residue(seed, part, i, row, col, m_i). */
-int irl_ccmm_synth_db(irl_ccmm* e, uint64_t seed);
+/* Fill every part with synthetic residues irl_synth_residue(seed, first_part + part,
+ * i, row, col, m_i); first_part is the global id of local part 0 (multi-GPU). */
+int irl_ccmm_synth_db(irl_ccmm* e, uint64_t seed, uint32_t first_part);
 /* End-to-end call with HOST buffers: q_res [nmod][K][N] -> out [parts][nmod][N][M].
  * Copies in, splits, multiplies every part, copies out; blocks. */
 int irl_ccmm_run(irl_ccmm* e, const uint16_t* q_res_host, size_t n, uint16_t* out_host);
@@ -152,6 +153,10 @@ int irl_ccmm_run(irl_ccmm* e, const uint16_t* q_res_host, size_t n, uint16_t* ou
  * out_dev [nparts][nmod][N][M]; stream-ordered, does not block. */
 int irl_ccmm_run_device(irl_ccmm* e, const uint16_t* q_res_dev, int q_ready, size_t n,
                         size_t part0, size_t nparts, uint16_t* out_dev, void* stream);
+/* Device staging buffers owned by the engine: query residues [nmod][K][max_n]
+ * and outputs [parts][nmod][n][M] (written by irl_ccmm_run, and by
+ * irl_ccmm_run_device when out_dev is NULL; q_res_dev NULL reads *qres). */
+int irl_ccmm_buffers(irl_ccmm* e, void** qres, void** out);
 /* Bytes of HBM the engine holds (planes + workspace). */
 uint64_t irl_ccmm_device_bytes(const irl_ccmm* e);
 

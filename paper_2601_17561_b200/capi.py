@@ -60,9 +60,10 @@ SIGNATURES = {
     "irl_ccmm_destroy": (C.c_int, [vp]),
     "irl_ccmm_load_part": (C.c_int, [vp, sz, vp, C.c_int]),
     "irl_ccmm_load_part_bigint": (C.c_int, [vp, sz, u8p, sz]),
-    "irl_ccmm_synth_db": (C.c_int, [vp, C.c_uint64]),
+    "irl_ccmm_synth_db": (C.c_int, [vp, C.c_uint64, C.c_uint32]),
     "irl_ccmm_run": (C.c_int, [vp, vp, sz, vp]),
     "irl_ccmm_run_device": (C.c_int, [vp, vp, C.c_int, sz, sz, sz, vp, vp]),
+    "irl_ccmm_buffers": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp)]),
     "irl_ccmm_device_bytes": (C.c_uint64, [vp]),
 }
 

@@ -64,9 +64,10 @@ class CcmmEngine:
         self.ctx.check(capi.lib().irl_ccmm_load_part_bigint(self.handle, part, capi.ptr(entries, capi.u8p),
                                                             width))
 
-    def synth_db(self, seed: int):
-        """Counter-based synthetic residues, identical to oracle's orc_synth_residue."""
-        self.ctx.check(capi.lib().irl_ccmm_synth_db(self.handle, seed))
+    def synth_db(self, seed: int, first_part: int = 0):
+        """Counter-based synthetic residues, identical to oracle's orc_synth_residue;
+        local part g is global part first_part + g."""
+        self.ctx.check(capi.lib().irl_ccmm_synth_db(self.handle, seed, first_part))
 
     def run(self, q_res: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
         """End-to-end with host buffers: q_res [nmod][K][N] -> [parts][nmod][N][M]."""
@@ -106,3 +107,24 @@ def synth_query(seed: int, k: int, n: int, moduli, stream: int = 0xFF) -> np.nda
     for i, m in enumerate(moduli):
         L.irl_synth_residues_host(seed, stream, i, 0, k, 0, n, m, capi.ptr(out[i], capi.u16p))
     return out
+
+
+class _CudaArray:
+    """Minimal __cuda_array_interface__ view of engine-owned device memory."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+def staging_tensors(engine: CcmmEngine, n: int):
+    """torch views (int16 bit patterns of the uint16 residues) of the engine's
+    device staging buffers: query residues [nmod][K][n] and outputs
+    [parts][nmod][n][M]. Zero-copy; valid while the engine lives."""
+    import torch
+    qp, op = C.c_void_p(), C.c_void_p()
+    engine.ctx.check(capi.lib().irl_ccmm_buffers(engine.handle, C.byref(qp), C.byref(op)))
+    dev = f"cuda:{engine.ctx.device}"
+    q = torch.as_tensor(_CudaArray(qp.value, (engine.nmod, engine.K, n), "<i2"), device=dev)
+    o = torch.as_tensor(_CudaArray(op.value, (engine.parts, engine.nmod, n, engine.M), "<i2"), device=dev)
+    return q, o

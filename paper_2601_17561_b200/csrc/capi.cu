@@ -821,6 +821,13 @@ int irl_ccmm_destroy(irl_ccmm* e) {
 
 uint64_t irl_ccmm_device_bytes(const irl_ccmm* e) { return e ? e->bytes : 0; }
 
+int irl_ccmm_buffers(irl_ccmm* e, void** qres, void** out) {
+    if (!e) return IRL_ERR_INVALID_ARGUMENT;
+    if (qres) *qres = e->qres;
+    if (out) *out = e->out;
+    return IRL_OK;
+}
+
 int irl_ccmm_load_part(irl_ccmm* e, size_t part, const uint16_t* res, int res_on_device) {
     if (!e) return IRL_ERR_INVALID_ARGUMENT;
     irl_ctx* ctx = e->ctx;
@@ -869,12 +876,12 @@ int irl_ccmm_load_part_bigint(irl_ccmm* e, size_t part, const uint8_t* entries, 
     return IRL_OK;
 }
 
-int irl_ccmm_synth_db(irl_ccmm* e, uint64_t seed) {
+int irl_ccmm_synth_db(irl_ccmm* e, uint64_t seed, uint32_t first_part) {
     if (!e) return IRL_ERR_INVALID_ARGUMENT;
     irl_ctx* ctx = e->ctx;
     Guard g(ctx);
     for (size_t p = 0; p < e->parts; ++p) {
-        IRL_LAUNCH(ctx, launch_synth_planes(seed, uint32_t(p), 1, uint32_t(e->M), uint32_t(e->K), e->mt,
+        IRL_LAUNCH(ctx, launch_synth_planes(seed, first_part + uint32_t(p), 1, uint32_t(e->M), uint32_t(e->K), e->mt,
                                             e->db + p * e->nmod * 2 * e->M * e->ldk, e->ldk, ctx->stream));
     }
     IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
@@ -904,11 +911,14 @@ int irl_ccmm_run_device(irl_ccmm* e, const uint16_t* q_res_dev, int q_ready, siz
     if (n == 0 || n > e->max_n) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: query width out of range");
     if (part0 + nparts > e->parts) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: part range out of range");
     cudaStream_t s = pick_stream(ctx, stream);
+    if (!q_res_dev) q_res_dev = e->qres;
+    if (!out_dev) out_dev = e->out + part0 * e->nmod * n * e->M;
     if (!q_ready) {
         IRL_LAUNCH(ctx, launch_split_cols<uint16_t>(q_res_dev, n, e->K * n, uint32_t(e->K), uint32_t(n), e->mt,
                                                     e->qplanes, e->ldk, nullptr, s));
     }
     // qplanes rows are laid out with stride n (not max_n): [nmod][2][n][ldk].
+    if (nparts == 0) return IRL_OK;  // split only
     return ccmm_parts(e, n, part0, nparts, out_dev, s);
 }
 
