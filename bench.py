@@ -242,10 +242,14 @@ def main():
     q_pinned = torch.from_numpy(q_host.view(np.int16)).pin_memory()
     q_dev, out_dev = staging_tensors(eng, N)
     q_dev.copy_(q_pinned)
+    torch.cuda.synchronize()
     a_recv = None
     if world > 1 and rank != 0:
         a_recv = torch.empty((nmod, N, M), dtype=torch.int16, device="cuda")
-    stream = torch.cuda.current_stream()
+    # a dedicated stream: the engine runs on the stream it is handed, and the
+    # CUDA events below are recorded on that same stream
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     gemm_events = []
 
     def run_parts(first_local, count):

@@ -86,7 +86,7 @@ class CcmmEngine:
         s = C.c_void_p(stream) if stream is not None else None
         self.ctx.check(capi.lib().irl_ccmm_run_device(
             self.handle, capi.ptr(q_res_dev) if q_res_dev is not None else None, int(q_ready), n,
-            part0, nparts, capi.ptr(out_dev), s))
+            part0, nparts, capi.ptr(out_dev) if out_dev is not None else None, s))
 
     def close(self):
         if getattr(self, "handle", None):

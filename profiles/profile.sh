@@ -1,0 +1,22 @@
+#!/bin/bash
+# ncu evidence for the bench's dominant kernel (run under gpurun, 1 GPU).
+#   bash profiles/profile.sh <tag>
+# Outputs land in gpurun_out/ (scratch); summaries are copied to profiles/.
+set -x
+TAG=${1:-r01}
+OUT=gpurun_out
+mkdir -p $OUT
+NCU=/usr/local/cuda/bin/ncu
+# 1) launch list of the bench command (cold-cache, serialised: shares only)
+timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file $OUT/launches_$TAG.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline \
+  > $OUT/launches_$TAG.log 2>&1
+# 2) full capture of one PPMM launch (1 part = one DB slice, c2/c3 geometry)
+timeout 900 $NCU --set full --clock-control none --import-source on -k regex:ppmm -s 1 -c 1 \
+  -o $OUT/ppmm_full_$TAG -f python bench.py --parts 1 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline \
+  > $OUT/ppmm_full_$TAG.log 2>&1
+# 3) DRAM traffic of the full 8-part launch (single-pass metric group)
+timeout 900 $NCU --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+  -k regex:ppmm -s 1 -c 1 --csv --log-file $OUT/ppmm_dram_$TAG.csv \
+  python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ppmm_dram_$TAG.log 2>&1
+ls -la $OUT
