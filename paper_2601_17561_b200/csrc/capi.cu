@@ -68,6 +68,7 @@ struct irl_ctx {
     SplitStats* h_stats = nullptr;
     int32_t* d_absmax = nullptr;
     int32_t* h_absmax = nullptr;
+    uint32_t* d_progress = nullptr;  // group-gating scratch of the PPMM kernel
 };
 
 struct irl_ccmm {
@@ -79,6 +80,7 @@ struct irl_ccmm {
     uint16_t* qres = nullptr;   // [nmod][K][max_n]
     uint16_t* out = nullptr;    // [parts][nmod][max_n][M]
     uint32_t kchunk = 0;        // K chunk keeping the fused int32 accumulators exact
+    uint32_t* progress = nullptr;  // group-gating scratch of this engine's PPMM launches
     cudaStream_t copy_stream = nullptr;
     std::vector<cudaEvent_t> part_done;
     uint64_t bytes = 0;
@@ -177,6 +179,7 @@ int run_ppmm(irl_ctx* ctx, PpmmLaunch L, uint32_t kchunk, cudaStream_t s) {
         return IRL_OK;
     }
     if (kchunk == 0 || kchunk > K) kchunk = K;
+    if (!L.progress) L.progress = ctx->d_progress;
     const int8_t* a0 = L.a_planes;
     const int8_t* b0 = L.b_planes;
     for (uint32_t k0 = 0; k0 < K; k0 += kchunk) {
@@ -288,6 +291,7 @@ int irl_ctx_create(int device, irl_ctx** out) {
         cudaMalloc(&ctx->d_stats, sizeof(SplitStats)) != cudaSuccess ||
         cudaMallocHost(&ctx->h_stats, sizeof(SplitStats)) != cudaSuccess ||
         cudaMalloc(&ctx->d_absmax, 2 * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&ctx->d_progress, 1024 * sizeof(uint32_t)) != cudaSuccess ||
         cudaMallocHost(&ctx->h_absmax, 2 * sizeof(int32_t)) != cudaSuccess) {
         delete ctx;
         return IRL_ERR_CUDA;
@@ -305,6 +309,7 @@ int irl_ctx_destroy(irl_ctx* ctx) {
     cudaFreeHost(ctx->h_stats);
     cudaFree(ctx->d_absmax);
     cudaFreeHost(ctx->h_absmax);
+    cudaFree(ctx->d_progress);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
     return IRL_OK;
@@ -789,6 +794,7 @@ int irl_ccmm_create(irl_ctx* ctx, size_t parts, size_t m, size_t k, size_t max_n
     if (err == cudaSuccess) err = cudaMalloc(&e->qplanes, qp_b);
     if (err == cudaSuccess) err = cudaMalloc(&e->qres, qr_b);
     if (err == cudaSuccess) err = cudaMalloc(&e->out, out_b);
+    if (err == cudaSuccess) err = cudaMalloc(&e->progress, 1024 * sizeof(uint32_t));
     if (err == cudaSuccess) err = cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking);
     if (err == cudaSuccess) err = cudaMemsetAsync(e->db, 0, db_b, ctx->stream);
     e->part_done.resize(parts);
@@ -815,6 +821,7 @@ int irl_ccmm_destroy(irl_ccmm* e) {
     cudaFree(e->qplanes);
     cudaFree(e->qres);
     cudaFree(e->out);
+    cudaFree(e->progress);
     delete e;
     return IRL_OK;
 }
@@ -900,6 +907,7 @@ static int ccmm_parts(irl_ccmm* e, size_t n, size_t part0, size_t nparts, uint16
     L.K = uint32_t(e->K);
     L.ldk = uint32_t(e->ldk);
     L.parts = uint32_t(nparts);
+    L.progress = e->progress;
     return run_ppmm(ctx, L, e->kchunk, s);
 }
 

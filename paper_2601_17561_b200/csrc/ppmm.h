@@ -25,6 +25,7 @@ struct PpmmLaunch {
     uint32_t parts = 1, nprimes = 0;
     int accumulate = 0;          // out = (out + result) mod p^2
     uint32_t max_clusters = 0;   // 0 = one CTA pair per SM pair
+    uint32_t* progress = nullptr;  // >= 74 words of scratch: enables group progress gating
     ModConst mc[kMaxPrimesPerLaunch];
 };
 

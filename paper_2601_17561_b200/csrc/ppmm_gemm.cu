@@ -15,11 +15,15 @@
 //   * TMEM holds two int32 accumulators per tile: acc1 = X0 Y0 in columns
 //     [0, 256) and acc2 = X0 Y1 + X1 Y0 in [256, 512);
 //   * warp 0 = TMA producer (both CTAs load their half of A and B),
-//     warp 1 = MMA issuer (leader CTA) + TMEM owner, warps 2..5 = epilogue;
+//     warp 1 = MMA issuer (leader CTA) + TMEM owner, warps 2..9 = epilogue
+//     (two warps per TMEM lane quarter, each draining half the columns);
 //   * 3-stage smem ring of 128-byte K blocks, 128B-swizzled, mbarrier-paced;
-//   * persistent static tile scheduler, tiles ordered (prime, part, m, n)
-//     so the per-prime query planes stay L2-resident and every database
-//     tile is streamed from HBM once.
+//   * persistent static schedule over "units" (one 256-row block of one
+//     (prime, part)), ordered prime-major so a prime's query planes stay
+//     L2-resident. The n-tiles of a unit run on a GROUP of CTA pairs at the
+//     same time, and each group's TMA producers are kept within a few K blocks
+//     of each other (progress flags in global memory, bounded spin), so every
+//     database tile crosses HBM once and is re-read from L2 by its peers.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -27,6 +31,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -45,18 +50,23 @@ constexpr int kStages = 3;
 constexpr int kUmmaK = 32;         // K per tcgen05.mma for 8-bit inputs
 constexpr int kPlaneTileBytes = kRowsPerCta * kBlockK;          // 16 KB
 constexpr int kStageBytes = 4 * kPlaneTileBytes;                // X0 X1 Y0 Y1
-constexpr int kNumThreads = 192;
-constexpr int kEpiWarp0 = 2;
+constexpr int kEpiWarps = 8;
+constexpr int kNumThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kAcc2Col = 256;
 constexpr size_t kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr uint32_t kGateLead = 12;                // max K blocks a pair may lead its group
+constexpr long long kGateSpinCycles = 200000;     // then proceed ungated (forward progress)
 
 struct __align__(64) GemmArgs {
     uint32_t M, N, K;
     uint32_t parts, nprimes;
-    uint32_t m_blocks, n_blocks, num_tiles;
+    uint32_t m_blocks, n_blocks, units;
+    // group schedule (see tile_of)
+    uint32_t G, F, L, R, super_units, active_clusters;  // R unused (= G)
     uint32_t accumulate;
     uint16_t* out;
+    uint32_t* progress;  // [clusters] K blocks issued by each pair's leader producer
     ModConst mc[kMaxPrimesPerLaunch];
 };
 
@@ -64,20 +74,43 @@ struct TileCoord {
     uint32_t prime, part, m0, n0, n_size;
 };
 
-__device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, uint32_t t) {
-    TileCoord c;
-    const uint32_t nb = t % a.n_blocks;
-    uint32_t r = t / a.n_blocks;
-    const uint32_t mb = r % a.m_blocks;
-    r /= a.m_blocks;
-    c.part = r % a.parts;
-    c.prime = r / a.parts;
-    c.m0 = mb * 2 * kRowsPerCta;
-    c.n0 = nb * kMaxTileN;
-    const uint32_t rem = a.N - c.n0;
+// Local tile j of cluster c. Super-rounds of G tiles per pair: each of the F
+// full groups (G pairs, G = n_blocks) runs G units, one n-tile per pair per
+// unit, in lock-step; each of the L leftover pairs runs one unit alone,
+// sweeping its G n-tiles. Units are prime-major. Returns false past the end.
+__device__ __forceinline__ bool tile_of(const GemmArgs& a, uint32_t c, uint32_t j, TileCoord& t) {
+    const uint32_t sr = j / a.G, r = j % a.G;
+    uint32_t unit, nb;
+    if (c < a.F * a.G) {
+        unit = sr * a.super_units + (c / a.G) * a.G + r;
+        nb = c % a.G;
+    } else {
+        unit = sr * a.super_units + a.F * a.G + (c - a.F * a.G);
+        nb = r;
+    }
+    if (unit >= a.units) return false;
+    const uint32_t mb = unit % a.m_blocks;
+    const uint32_t pp = unit / a.m_blocks;
+    t.part = pp % a.parts;
+    t.prime = pp / a.parts;
+    t.m0 = mb * 2 * kRowsPerCta;
+    t.n0 = nb * kMaxTileN;
+    const uint32_t rem = a.N - t.n0;
     const uint32_t ns = rem < kMaxTileN ? rem : kMaxTileN;
-    c.n_size = (ns + 31u) & ~31u;  // cta_group::2 kind::i8 needs N % 32 == 0
-    return c;
+    t.n_size = (ns + 31u) & ~31u;  // cta_group::2 kind::i8 needs N % 32 == 0
+    return true;
+}
+
+// Group members of cluster c: [first, first + size) (leftover pairs: size 1).
+__device__ __forceinline__ void group_of(const GemmArgs& a, uint32_t c, uint32_t& first,
+                                         uint32_t& size) {
+    if (c < a.F * a.G) {
+        first = (c / a.G) * a.G;
+        size = a.G;
+    } else {
+        first = c;
+        size = 1;
+    }
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
@@ -98,7 +131,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
     const uint32_t rank = ptx::cluster_ctarank();
     const bool leader = rank == 0;
     const uint32_t cluster_id = blockIdx.x / 2;
-    const uint32_t num_clusters = gridDim.x / 2;
+    const bool active = cluster_id < args.active_clusters;
 
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmap_a);
@@ -108,7 +141,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
             ptx::mbar_init(&empty_bar[s], 1);
         }
         ptx::mbar_init(tmem_full_bar, 1);
-        ptx::mbar_init(tmem_empty_bar, 2 * 4);  // 4 epilogue warps in each CTA
+        ptx::mbar_init(tmem_empty_bar, 2 * kEpiWarps);
         ptx::fence_barrier_init();
     }
     if (warp == 1) {
@@ -119,19 +152,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_base_slot;
 
-    if (warp == 0) {
+    if (!active) {
+        // idle pair (group schedule leftover): nothing to do
+    } else if (warp == 0) {
         // ---------------- TMA producer (both CTAs) ----------------
         if (lane == 0) {
             const uint32_t num_kb = (args.K + kBlockK - 1) / kBlockK;
+            uint32_t gfirst, gsize;
+            group_of(args, cluster_id, gfirst, gsize);
+            const bool gate = leader && args.progress != nullptr && gsize > 1;
+            uint32_t issued = 0;  // cumulative K blocks (comparable across the group)
+            uint32_t seen = 0;    // last observed minimum of the peers' counters
             uint32_t stage = 0, phase = 0;
-            for (uint32_t t = cluster_id; t < args.num_tiles; t += num_clusters) {
-                const TileCoord tc = decode_tile(args, t);
+            TileCoord tc;
+            for (uint32_t j = 0; tile_of(args, cluster_id, j, tc); ++j) {
                 const uint32_t a_row0 =
                     ((tc.part * args.nprimes + tc.prime) * 2) * args.M + tc.m0 + rank * kRowsPerCta;
                 const uint32_t half_n = tc.n_size / 2;
                 const uint32_t b_row0 = (tc.prime * 2) * args.N + tc.n0 + rank * half_n;
-                for (uint32_t kb = 0; kb < num_kb; ++kb) {
+                for (uint32_t kb = 0; kb < num_kb; ++kb, ++issued) {
                     ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+                    if (gate && issued > seen + kGateLead) {
+                        // Stay within kGateLead K blocks of the slowest group peer.
+                        // `seen` caches the last observed minimum, so the L2
+                        // round trip is paid about once per kGateLead blocks.
+                        const long long t0 = clock64();
+                        for (;;) {
+                            uint32_t lo = 0xFFFFFFFFu;
+                            for (uint32_t p = gfirst; p < gfirst + gsize; ++p)
+                                if (p != cluster_id) lo = min(lo, ptx::ld_relaxed_gpu(args.progress + p));
+                            seen = lo;
+                            if (lo + kGateLead >= issued) break;
+                            if (clock64() - t0 > kGateSpinCycles) {
+                                seen = issued;  // give up for kGateLead blocks (forward progress)
+                                break;
+                            }
+                            __nanosleep(32);
+                        }
+                    }
                     const uint32_t leader_full =
                         ptx::mapa_shared(ptx::smem_u32(&full_bar[stage]), 0);
                     if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * kStageBytes);
@@ -142,11 +200,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
                     ptx::tma_load_2d_pair(ptx::smem_u32(st + kPlaneTileBytes), &tmap_a,
                                           leader_full, k0,
                                           static_cast<int32_t>(a_row0 + args.M));
-                    ptx::tma_load_2d_pair(ptx::smem_u32(st + 2 * kPlaneTileBytes), &tmap_b,
-                                          leader_full, k0, static_cast<int32_t>(b_row0));
-                    ptx::tma_load_2d_pair(ptx::smem_u32(st + 3 * kPlaneTileBytes), &tmap_b,
-                                          leader_full, k0,
-                                          static_cast<int32_t>(b_row0 + args.N));
+                    ptx::tma_load_2d_pair_hint(ptx::smem_u32(st + 2 * kPlaneTileBytes), &tmap_b,
+                                               leader_full, k0, static_cast<int32_t>(b_row0),
+                                               ptx::kL2EvictLast);
+                    ptx::tma_load_2d_pair_hint(ptx::smem_u32(st + 3 * kPlaneTileBytes), &tmap_b,
+                                               leader_full, k0,
+                                               static_cast<int32_t>(b_row0 + args.N),
+                                               ptx::kL2EvictLast);
+                    if (gate) ptx::st_relaxed_gpu(args.progress + cluster_id, issued + 1);
                     if (++stage == kStages) {
                         stage = 0;
                         phase ^= 1;
@@ -160,12 +221,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
             const uint32_t num_kb = (args.K + kBlockK - 1) / kBlockK;
             const uint32_t acc1 = tmem_base;
             const uint32_t acc2 = tmem_base + kAcc2Col;
-            uint32_t stage = 0, phase = 0, local_tile = 0;
-            for (uint32_t t = cluster_id; t < args.num_tiles; t += num_clusters, ++local_tile) {
-                const TileCoord tc = decode_tile(args, t);
+            uint32_t stage = 0, phase = 0;
+            TileCoord tc;
+            for (uint32_t j = 0; tile_of(args, cluster_id, j, tc); ++j) {
                 const uint32_t idesc = ptx::idesc_i8(2 * kRowsPerCta, tc.n_size);
                 // Wait until the epilogue of the previous tile drained TMEM.
-                ptx::mbar_wait(tmem_empty_bar, (local_tile & 1) ^ 1);
+                ptx::mbar_wait(tmem_empty_bar, (j & 1) ^ 1);
                 ptx::tc_fence_after();
                 for (uint32_t kb = 0; kb < num_kb; ++kb) {
                     ptx::mbar_wait(&full_bar[stage], phase);
@@ -195,14 +256,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
             }
         }
     } else {
-        // ---------------- Epilogue (both CTAs) ----------------
-        const uint32_t quarter = warp % 4;  // TMEM lane quarter this warp may access
+        // ---------------- Epilogue (both CTAs, 8 warps) ----------------
+        const uint32_t quarter = warp % 4;        // TMEM lane quarter this warp may access
+        const uint32_t half = (warp - 2) / 4;     // which half of the tile's columns
         const uint32_t leader_tmem_empty = ptx::mapa_shared(ptx::smem_u32(tmem_empty_bar), 0);
-        uint32_t local_tile = 0;
-        for (uint32_t t = cluster_id; t < args.num_tiles; t += num_clusters, ++local_tile) {
-            const TileCoord tc = decode_tile(args, t);
+        TileCoord tc;
+        for (uint32_t j = 0; tile_of(args, cluster_id, j, tc); ++j) {
             const ModConst mc = args.mc[tc.prime];
-            ptx::mbar_wait(tmem_full_bar, local_tile & 1);
+            ptx::mbar_wait(tmem_full_bar, j & 1);
             ptx::tc_fence_after();
             const uint32_t row = rank * kRowsPerCta + quarter * 32 + lane;
             const uint32_t m = tc.m0 + row;
@@ -212,18 +273,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
                                 static_cast<size_t>(args.N) * args.M +
                             m;
             const uint32_t lane_base = tmem_base + ((quarter * 32u) << 16);
-            for (uint32_t c = 0; c < tc.n_size; c += 32) {
-                uint32_t a1[32], a2[32];
-                ptx::tmem_ld_32x32b_x32(lane_base + c, a1);
-                ptx::tmem_ld_32x32b_x32(lane_base + kAcc2Col + c, a2);
+            const uint32_t cols = tc.n_size / 2;  // multiple of 16
+            const uint32_t c_begin = half * cols;
+            for (uint32_t c = c_begin; c < c_begin + cols; c += 16) {
+                uint32_t a1[16], a2[16];
+                ptx::tmem_ld_32x32b_x16(lane_base + c, a1);
+                ptx::tmem_ld_32x32b_x16(lane_base + kAcc2Col + c, a2);
                 ptx::tmem_ld_wait();
                 if (row_ok) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const uint32_t n = tc.n0 + c + j;
+                    for (int jj = 0; jj < 16; ++jj) {
+                        const uint32_t n = tc.n0 + c + jj;
                         if (n < args.N) {
-                            uint32_t v = combine_psq(static_cast<int32_t>(a1[j]),
-                                                     static_cast<int32_t>(a2[j]), mc);
+                            uint32_t v = combine_psq(static_cast<int32_t>(a1[jj]),
+                                                     static_cast<int32_t>(a2[jj]), mc);
                             uint16_t* dst = out + static_cast<size_t>(n) * args.M;
                             if (args.accumulate) {
                                 v += *dst;
@@ -250,29 +313,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
+    static std::once_flag once;
+    std::call_once(once, [] {
         void* p = nullptr;
         cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
-                cudaSuccess ||
-            q != cudaDriverEntryPointSuccess || p == nullptr) {
-            throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
-        }
-        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    if (!fn) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
     return fn;
 }
 
-void make_plane_map(CUtensorMap* map, const void* base, uint64_t k, uint64_t rows, uint64_t ldk) {
+bool make_plane_map(CUtensorMap* map, const void* base, uint64_t k, uint64_t rows, uint64_t ldk) {
     const cuuint64_t dims[2] = {k, rows};
     const cuuint64_t strides[1] = {ldk};
     const cuuint32_t box[2] = {kBlockK, kRowsPerCta};
     const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = get_encode_fn()(
-        map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
-        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return get_encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -288,8 +350,9 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     if (a_rows >= (1ull << 31) || b_rows >= (1ull << 31)) return cudaErrorInvalidValue;
 
     CUtensorMap ma, mb;
-    make_plane_map(&ma, L.a_planes, L.K, a_rows, L.ldk);
-    make_plane_map(&mb, L.b_planes, L.K, b_rows, L.ldk);
+    if (!make_plane_map(&ma, L.a_planes, L.K, a_rows, L.ldk) ||
+        !make_plane_map(&mb, L.b_planes, L.K, b_rows, L.ldk))
+        return cudaErrorInvalidValue;
 
     GemmArgs args;
     std::memset(&args, 0, sizeof(args));
@@ -300,25 +363,41 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     args.nprimes = L.nprimes;
     args.m_blocks = (L.M + 2 * kRowsPerCta - 1) / (2 * kRowsPerCta);
     args.n_blocks = (L.N + kMaxTileN - 1) / kMaxTileN;
-    args.num_tiles = args.m_blocks * args.n_blocks * L.parts * L.nprimes;
+    args.units = args.m_blocks * L.parts * L.nprimes;
     args.accumulate = L.accumulate ? 1u : 0u;
     args.out = L.out;
     for (uint32_t i = 0; i < L.nprimes; ++i) args.mc[i] = L.mc[i];
 
-    static bool attr_set = false;
-    if (!attr_set) {
+    static int attr_dev = -1;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    if (attr_dev != dev) {
         cudaError_t e = cudaFuncSetAttribute(ppmm_i8_sm100_kernel,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(kSmemBytes));
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_dev = dev;
     }
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     uint32_t clusters = static_cast<uint32_t>(sms / 2);
     if (L.max_clusters > 0) clusters = std::min<uint32_t>(clusters, L.max_clusters);
-    clusters = std::min<uint32_t>(clusters, args.num_tiles);
+
+    // Group schedule: G = n_blocks pairs share each unit's A tile (one n-tile
+    // each); never more pairs than there are tiles.
+    const uint64_t tiles = static_cast<uint64_t>(args.units) * args.n_blocks;
+    clusters = static_cast<uint32_t>(std::min<uint64_t>(clusters, tiles));
+    const uint32_t G = args.n_blocks;
+    args.G = G;
+    args.F = clusters / G;
+    args.L = clusters % G;
+    args.R = G;
+    args.super_units = args.F * G + args.L;
+    args.active_clusters = clusters;
+    args.progress = L.progress;
+    if (L.progress) {
+        cudaError_t e = cudaMemsetAsync(L.progress, 0, clusters * sizeof(uint32_t), stream);
+        if (e != cudaSuccess) return e;
+    }
 
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * clusters);

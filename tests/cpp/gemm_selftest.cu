@@ -73,6 +73,9 @@ static int run_case(uint32_t parts, uint32_t nprimes, uint32_t M, uint32_t N, ui
     L.ldk = ldk;
     L.parts = parts;
     L.nprimes = nprimes;
+    uint32_t* prog = nullptr;
+    CK(cudaMalloc(&prog, 4096));
+    L.progress = prog;
     for (uint32_t i = 0; i < nprimes; ++i) L.mc[i] = make_modconst(kPrimes[i], 2);
     CK(launch_ppmm_planes(L, 0));
     CK(cudaDeviceSynchronize());
@@ -144,6 +147,7 @@ static int run_case(uint32_t parts, uint32_t nprimes, uint32_t M, uint32_t N, ui
     CK(cudaFree(da));
     CK(cudaFree(db));
     CK(cudaFree(dout));
+    CK(cudaFree(prog));
     return bad == 0 ? 0 : 1;
 }
 
