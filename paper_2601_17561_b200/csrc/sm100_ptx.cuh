@@ -212,6 +212,17 @@ __device__ __forceinline__ uint64_t smem_desc_k_sw128(uint32_t smem_addr) {
     return d;
 }
 
+// Same for the 64-byte swizzle (rows of 64 B, 8-row atoms of 512 B).
+__device__ __forceinline__ uint64_t smem_desc_k_sw64(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4);  // start address
+    d |= static_cast<uint64_t>(1) << 16;                       // LBO (unused for swizzled K-major)
+    d |= static_cast<uint64_t>(512 >> 4) << 32;                // SBO: 8 rows x 64 B
+    d |= static_cast<uint64_t>(1) << 46;                       // descriptor version (sm_100)
+    d |= static_cast<uint64_t>(4) << 61;                       // SWIZZLE_64B
+    return d;
+}
+
 // Instruction descriptor: kind::i8, signed A/B, S32 accumulate, K-major A/B.
 __host__ __device__ constexpr uint32_t idesc_i8(uint32_t m, uint32_t n) {
     return (2u << 4)            // D format S32
