@@ -343,7 +343,7 @@ def main():
             eng.run(q_np, o_np)  # H2D query, split, all local PPMMs, D2H outputs
             if world > 1:
                 # the a-part result exchange stays on the device
-                w = dist.broadcast(a_out(), src=0, async_op=True)
+                w = dist.broadcast(a_out().view(torch.uint8), src=0, async_op=True)
                 w.wait()
                 torch.cuda.synchronize()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps

@@ -64,17 +64,24 @@ class ShardedStep:
         self.a_out = a_out
         self.group = group
 
-    def __call__(self):
+    def _bcast(self):
+        import torch
         import torch.distributed as dist
+        buf = self.a_out()
+        # residues are uint16 bit patterns; exchange them as bytes (gloo and
+        # NCCL both carry uint8)
+        return dist.broadcast(buf.view(torch.uint8), src=self.owner, group=self.group, async_op=True)
+
+    def __call__(self):
         work = None
         if self.world > 1:
             if self.rank == self.owner:
                 self.run_parts(0, 1)  # a-part first
-                work = dist.broadcast(self.a_out(), src=self.owner, group=self.group, async_op=True)
+                work = self._bcast()
                 if self.local.count > 1:
                     self.run_parts(1, self.local.count - 1)
             else:
-                work = dist.broadcast(self.a_out(), src=self.owner, group=self.group, async_op=True)
+                work = self._bcast()
                 self.run_parts(0, self.local.count)
         else:
             self.run_parts(0, self.local.count)

@@ -1,0 +1,89 @@
+"""Multi-rank layout of the CCMM (paper's 8-slice DB, a-part broadcast) on CPU
+with the gloo backend. The per-part PPMM is stood in by the CPU oracle (test
+infrastructure) so the orchestration (part dealing, broadcast overlap, result
+placement) is exercised exactly as bench.py drives it on NCCL."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle_lib as ol
+from paper_2601_17561_b200.dist import PAPER_PARTS, ShardedStep, a_part_owner, part_range
+
+M, K, N = 40, 96, 12
+MODS = [127 * 127, 251 * 251]
+SEED = 3
+
+
+def test_part_ranges_cover_db_once():
+    for world in (1, 2, 4, 8, 3, 5):
+        seen = []
+        for r in range(world):
+            seen += list(part_range(r, world))
+        assert sorted(seen) == list(range(PAPER_PARTS))
+        assert a_part_owner(world) == 0
+    assert [part_range(r, 8).count for r in range(8)] == [1] * 8
+    assert [part_range(r, 2).first for r in range(2)] == [0, 4]
+    with pytest.raises(ValueError):
+        part_range(0, 9)
+
+
+def oracle_part(part, q):
+    out = np.zeros((len(MODS), N, M), np.uint16)
+    for i, m in enumerate(MODS):
+        a = ol.synth_block(SEED, part, i, 0, M, 0, K, m)
+        out[i] = ol.ppmm_rows_direct(a, np.ascontiguousarray(q[i].T), np.arange(M, dtype=np.uint32), m).T
+    return out
+
+
+def _worker(rank, world, port, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    q = np.stack([ol.synth_block(9, 0xFF, i, 0, K, 0, N, m) for i, m in enumerate(MODS)])
+    local = part_range(rank, world)
+    out = torch.zeros((local.count, len(MODS), N, M), dtype=torch.int16)
+    a_recv = torch.zeros((len(MODS), N, M), dtype=torch.int16)
+    calls = []
+
+    def run_parts(first_local, count):
+        calls.append((first_local, count))
+        for g in range(first_local, first_local + count):
+            out[g] = torch.from_numpy(oracle_part(local.first + g, q).view(np.int16))
+
+    def a_out():
+        return out[0] if rank == a_part_owner(world) else a_recv
+
+    step = ShardedStep(rank, world, run_parts, a_out)
+    w = step()
+    if w is not None:
+        w.wait()
+    ok_local = all((out[g].numpy().view(np.uint16) == oracle_part(local.first + g, q)).all()
+                   for g in range(local.count))
+    ok_a = bool((a_out().numpy().view(np.uint16) == oracle_part(0, q)).all())
+    results[rank] = (ok_local, ok_a, calls)
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_step_gloo(world):
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), results), nprocs=world, join=True)
+    assert sorted(results.keys()) == list(range(world))
+    for r in range(world):
+        ok_local, ok_a, calls = results[r]
+        assert ok_local and ok_a, r
+        if r == 0:
+            # the a-part GEMM is issued first, then the broadcast, then the b-parts
+            assert calls[0] == (0, 1)
