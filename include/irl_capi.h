@@ -59,6 +59,11 @@ const char* irl_status_string(int status);
 uint64_t irl_kernel_launches(const irl_ctx* ctx);
 /* Stream used by the blocking calls (a cudaStream_t). */
 void* irl_ctx_stream(const irl_ctx* ctx);
+/* Diagnostics: enable per-CTA-pair cycle counters in the PPMM kernel for later
+ * launches on this context; if out != NULL, first copy the last launch's
+ * counters ([pair][16] uint64: producer empty/gate waits, MMA full/tmem waits,
+ * MMA cycles, epilogue wait/busy, globaltimer start/end, tiles). */
+int irl_diag_ppmm(irl_ctx* ctx, int enable, uint64_t* out, size_t cap);
 
 /* ---- RNS basis helpers (modmat.cpp:8-63) -------------------------------- */
 /* Primes 127..253 with e = 2 (build_paper_basis, modmat.cpp:37-45). Returns count. */

@@ -41,6 +41,7 @@ SIGNATURES = {
     "irl_status_string": (C.c_char_p, [C.c_int]),
     "irl_kernel_launches": (C.c_uint64, [vp]),
     "irl_ctx_stream": (vp, [vp]),
+    "irl_diag_ppmm": (C.c_int, [vp, C.c_int, C.POINTER(C.c_uint64), sz]),
     "irl_paper_basis": (sz, [u32p, u32p, sz]),
     "irl_basis_Q_bytes": (sz, [u32p, u32p, sz, u8p, sz]),
     "irl_digit_decompose": (C.c_int, [vp, i32p, sz, sz, C.c_uint32, i32p, i32p]),

@@ -69,6 +69,8 @@ struct irl_ctx {
     int32_t* d_absmax = nullptr;
     int32_t* h_absmax = nullptr;
     uint32_t* d_progress = nullptr;  // group-gating scratch of the PPMM kernel
+    uint64_t* d_diag = nullptr;      // PPMM diagnostics (irl_diag_ppmm), lazily allocated
+    bool diag = false;
 };
 
 struct irl_ccmm {
@@ -160,10 +162,11 @@ PpmmLaunch make_launch(const ModTable& mt) {
 }
 
 // K chunk such that acc2 = sum X0 Y1 + X1 Y0 and acc1 = sum X0 Y0 stay
-// exact in int32 for digit maxima (a0, a1, b0, b1); multiple of 128.
+// within |acc| <= 2^31 - 2^17 (the fused epilogue's exact range, see
+// combine_psq_fast) for digit maxima (a0, a1, b0, b1); multiple of 128.
 uint32_t safe_kchunk(int64_t a0, int64_t a1, int64_t b0, int64_t b1, uint32_t K) {
     const int64_t per = std::max<int64_t>(std::max<int64_t>(a0 * b1 + a1 * b0, a0 * b0), 1);
-    int64_t kc = ((int64_t{1} << 31) - 1) / per;
+    int64_t kc = ((int64_t{1} << 31) - (int64_t{1} << 17)) / per;
     if (kc >= K) return K;
     kc = (kc / 128) * 128;
     return static_cast<uint32_t>(std::max<int64_t>(kc, 128));
@@ -180,6 +183,10 @@ int run_ppmm(irl_ctx* ctx, PpmmLaunch L, uint32_t kchunk, cudaStream_t s) {
     }
     if (kchunk == 0 || kchunk > K) kchunk = K;
     if (!L.progress) L.progress = ctx->d_progress;
+    if (ctx->diag && ctx->d_diag) {
+        L.stats = ctx->d_diag;
+        IRL_CK(ctx, cudaMemsetAsync(ctx->d_diag, 0, 1024 * kStatSlots * sizeof(uint64_t), s));
+    }
     const int8_t* a0 = L.a_planes;
     const int8_t* b0 = L.b_planes;
     for (uint32_t k0 = 0; k0 < K; k0 += kchunk) {
@@ -310,12 +317,26 @@ int irl_ctx_destroy(irl_ctx* ctx) {
     cudaFree(ctx->d_absmax);
     cudaFreeHost(ctx->h_absmax);
     cudaFree(ctx->d_progress);
+    cudaFree(ctx->d_diag);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
     return IRL_OK;
 }
 
 const char* irl_last_error(const irl_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+int irl_diag_ppmm(irl_ctx* ctx, int enable, uint64_t* out, size_t cap) {
+    if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
+    Guard g(ctx);
+    if (enable && !ctx->d_diag) IRL_CK(ctx, cudaMalloc(&ctx->d_diag, 1024 * kStatSlots * sizeof(uint64_t)));
+    if (out && ctx->d_diag) {
+        IRL_CK(ctx, cudaDeviceSynchronize());
+        IRL_CK(ctx, cudaMemcpy(out, ctx->d_diag, std::min<size_t>(cap, 1024 * kStatSlots) * sizeof(uint64_t),
+                               cudaMemcpyDeviceToHost));
+    }
+    ctx->diag = enable != 0;
+    return IRL_OK;
+}
 uint64_t irl_kernel_launches(const irl_ctx* ctx) { return ctx ? ctx->launches : 0; }
 void* irl_ctx_stream(const irl_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
 

@@ -17,6 +17,8 @@ struct ModConst {
     uint32_t off_m;    // 2^31 mod m
     uint32_t e;        // exponent 1 or 2
     uint32_t pad;
+    uint32_t c_p;      // p * ceil(2^31 / p): shifts |x| < 2^31 - 2^17 into [0, 2^32)
+    uint32_t c_m;      // m * ceil(2^31 / m)
 };
 
 __host__ __device__ inline ModConst make_modconst(uint32_t p, uint32_t e) {
@@ -29,14 +31,17 @@ __host__ __device__ inline ModConst make_modconst(uint32_t p, uint32_t e) {
     c.magic_m = c.m > 1 ? static_cast<uint32_t>((1ull << 32) / c.m) : 0xFFFFFFFFu;
     c.off_p = static_cast<uint32_t>((1ull << 31) % p);
     c.off_m = static_cast<uint32_t>((1ull << 31) % c.m);
+    c.c_p = static_cast<uint32_t>(((1ull << 31) + p - 1) / p * p);
+    c.c_m = static_cast<uint32_t>(((1ull << 31) + c.m - 1) / c.m * c.m);
     return c;
 }
 
-// u mod m for u in [0, 2^32).
+// u mod m for u in [0, 2^32): Barrett quotient (low by at most one), then
+// r = min_u32(r, r - m) picks the reduced value (r - m wraps when r < m).
 __device__ __forceinline__ uint32_t mod_u32(uint32_t u, uint32_t m, uint32_t magic) {
     const uint32_t q = __umulhi(u, magic);
-    uint32_t r = u - q * m;
-    return r >= m ? r - m : r;
+    const uint32_t r = u - q * m;
+    return min(r, r - m);
 }
 
 // x mod m in [0, m) for any signed 32-bit x (floor semantics).
@@ -53,6 +58,20 @@ __device__ __forceinline__ uint32_t combine_psq(int32_t acc1, int32_t acc2, cons
     const uint32_t r1 = mod_s32(acc1, c.m, c.magic_m, c.off_m);
     uint32_t v = r1 + c.p * r2;  // < 2 p^2
     return v >= c.m ? v - c.m : v;
+}
+
+// Fast epilogue combine for accumulators bounded by |acc| <= 2^31 - 2^17
+// (guaranteed by the launcher's K chunking): ~11 integer instructions.
+//   r2 = acc2 mod p;  result = (acc1 + p r2) mod p^2
+// using the multiples c_p, c_m of p, p^2 to make both operands non-negative
+// without signed fix-ups.
+__device__ __forceinline__ uint32_t combine_psq_fast(int32_t acc1, int32_t acc2, uint32_t p,
+                                                     uint32_t m, uint32_t magic_p,
+                                                     uint32_t magic_m, uint32_t c_p,
+                                                     uint32_t c_m) {
+    const uint32_t r2 = mod_u32(static_cast<uint32_t>(acc2) + c_p, p, magic_p);
+    const uint32_t u = static_cast<uint32_t>(acc1) + c_m + p * r2;
+    return mod_u32(u, m, magic_m);
 }
 
 // Centred digit split of v in [0, p^2) (modmat.cpp:86-106):

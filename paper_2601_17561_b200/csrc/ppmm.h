@@ -12,6 +12,11 @@
 namespace irl {
 
 constexpr uint32_t kMaxPrimesPerLaunch = 32;
+// Diagnostics slots per CTA pair (PpmmLaunch::stats): 0 producer empty-wait
+// cycles, 1 producer gate cycles, 2 MMA full-wait cycles, 3 MMA tmem-empty
+// wait cycles, 4 MMA thread total cycles, 5 epilogue tmem-full wait cycles,
+// 6 epilogue busy cycles, 7/8 globaltimer start/end (ns), 11 tiles.
+constexpr uint32_t kStatSlots = 16;
 
 // One batched PPMM launch over `parts` database parts and `nprimes` moduli.
 //   a_planes: [parts][nprimes][2][M][ldk] int8 centred digits (K-major)
@@ -26,6 +31,7 @@ struct PpmmLaunch {
     int accumulate = 0;          // out = (out + result) mod p^2
     uint32_t max_clusters = 0;   // 0 = one CTA pair per SM pair
     uint32_t* progress = nullptr;  // >= 74 words of scratch: enables group progress gating
+    uint64_t* stats = nullptr;     // optional [pairs][kStatSlots] diagnostics
     ModConst mc[kMaxPrimesPerLaunch];
 };
 

@@ -68,8 +68,27 @@ struct __align__(64) GemmArgs {
     uint32_t accumulate;
     uint16_t* out;
     uint32_t* progress;  // [clusters] K blocks issued by each pair's leader producer
+    unsigned long long* stats;  // optional [clusters][kStatSlots] diagnostics (see ppmm.h)
     ModConst mc[kMaxPrimesPerLaunch];
 };
+
+// Diagnostics: wait on a barrier and add the cycles spent to *acc.
+__device__ __forceinline__ void timed_wait(uint64_t* bar, uint32_t parity, bool on,
+                                           unsigned long long& acc) {
+    if (!on) {
+        ptx::mbar_wait(bar, parity);
+        return;
+    }
+    const long long t0 = clock64();
+    ptx::mbar_wait(bar, parity);
+    acc += static_cast<unsigned long long>(clock64() - t0);
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 struct TileCoord {
     uint32_t prime, part, m0, n0, n_size;
@@ -165,6 +184,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
             uint32_t issued = 0;  // cumulative K blocks (comparable across the group)
             uint32_t seen = 0;    // last observed minimum of the peers' counters
             uint32_t stage = 0, phase = 0;
+            const bool diag = args.stats != nullptr && leader;
+            unsigned long long w_empty = 0, w_gate = 0;
             TileCoord tc;
             for (uint32_t j = 0; tile_of(args, cluster_id, j, tc); ++j) {
                 const uint32_t a_row0 =
@@ -172,7 +193,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
                 const uint32_t half_n = tc.n_size / 2;
                 const uint32_t b_row0 = (tc.prime * 2) * args.N + tc.n0 + rank * half_n;
                 for (uint32_t kb = 0; kb < num_kb; ++kb, ++issued) {
-                    ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+                    timed_wait(&empty_bar[stage], phase ^ 1, diag, w_empty);
                     if (gate && issued > seen + kGateLead) {
                         // Stay within kGateLead K blocks of the slowest group peer.
                         // `seen` caches the last observed minimum, so the L2
@@ -190,6 +211,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
                             }
                             __nanosleep(32);
                         }
+                        if (diag) w_gate += static_cast<unsigned long long>(clock64() - t0);
                     }
                     const uint32_t leader_full =
                         ptx::mapa_shared(ptx::smem_u32(&full_bar[stage]), 0);
@@ -215,6 +237,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
                     }
                 }
             }
+            if (diag) {
+                unsigned long long* st = args.stats + cluster_id * kStatSlots;
+                st[0] = w_empty;
+                st[1] = w_gate;
+            }
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer (leader CTA only) ----------------
@@ -223,14 +250,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
             const uint32_t acc1 = tmem_base;
             const uint32_t acc2 = tmem_base + kAcc2Col;
             uint32_t stage = 0, phase = 0;
+            const bool diag = args.stats != nullptr;
+            unsigned long long w_full = 0, w_tmem = 0;
+            const long long c_start = clock64();
+            const unsigned long long g_start = diag ? globaltimer() : 0;
+            uint32_t tiles = 0;
             TileCoord tc;
-            for (uint32_t j = 0; tile_of(args, cluster_id, j, tc); ++j) {
+            for (uint32_t j = 0; tile_of(args, cluster_id, j, tc); ++j, ++tiles) {
                 const uint32_t idesc = ptx::idesc_i8(2 * kRowsPerCta, tc.n_size);
                 // Wait until the epilogue of the previous tile drained TMEM.
-                ptx::mbar_wait(tmem_empty_bar, (j & 1) ^ 1);
+                timed_wait(tmem_empty_bar, (j & 1) ^ 1, diag, w_tmem);
                 ptx::tc_fence_after();
                 for (uint32_t kb = 0; kb < num_kb; ++kb) {
-                    ptx::mbar_wait(&full_bar[stage], phase);
+                    timed_wait(&full_bar[stage], phase, diag, w_full);
                     ptx::tc_fence_after();
                     const uint32_t st = ptx::smem_u32(smem + stage * kStageBytes);
 #pragma unroll
@@ -255,16 +287,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
                 }
                 ptx::mma_commit_pair(tmem_full_bar, 0x3);
             }
+            if (diag) {
+                // wait for the last tile's MMAs so the end stamps cover them
+                timed_wait(tmem_empty_bar, (tiles & 1) ^ 1, false, w_tmem);
+                unsigned long long* st = args.stats + cluster_id * kStatSlots;
+                st[2] = w_full;
+                st[3] = w_tmem;
+                st[4] = static_cast<unsigned long long>(clock64() - c_start);
+                st[7] = g_start;
+                st[8] = globaltimer();
+                st[11] = tiles;
+            }
         }
     } else {
         // ---------------- Epilogue (both CTAs, 8 warps) ----------------
         const uint32_t quarter = warp % 4;        // TMEM lane quarter this warp may access
         const uint32_t half = (warp - 2) / 4;     // which half of the tile's columns
         const uint32_t leader_tmem_empty = ptx::mapa_shared(ptx::smem_u32(tmem_empty_bar), 0);
+        const bool diag = args.stats != nullptr && leader && warp == 2 && lane == 0;
+        unsigned long long w_epi = 0, busy_epi = 0;
         TileCoord tc;
         for (uint32_t j = 0; tile_of(args, cluster_id, j, tc); ++j) {
             const ModConst mc = args.mc[tc.prime];
-            ptx::mbar_wait(tmem_full_bar, j & 1);
+            timed_wait(tmem_full_bar, j & 1, diag, w_epi);
+            const long long e0 = clock64();
             ptx::tc_fence_after();
             const uint32_t row = rank * kRowsPerCta + quarter * 32 + lane;
             const uint32_t m = tc.m0 + row;
@@ -281,26 +327,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
                 ptx::tmem_ld_32x32b_x16(lane_base + c, a1);
                 ptx::tmem_ld_32x32b_x16(lane_base + kAcc2Col + c, a2);
                 ptx::tmem_ld_wait();
-                if (row_ok) {
+                if (!row_ok) continue;
+                uint16_t* dst = out + static_cast<size_t>(tc.n0 + c) * args.M;
+                if (!args.accumulate && tc.n0 + c + 16 <= args.N) {
+                    // fast path: whole 16-column chunk in range, overwrite
 #pragma unroll
                     for (int jj = 0; jj < 16; ++jj) {
-                        const uint32_t n = tc.n0 + c + jj;
-                        if (n < args.N) {
-                            uint32_t v = combine_psq(static_cast<int32_t>(a1[jj]),
-                                                     static_cast<int32_t>(a2[jj]), mc);
-                            uint16_t* dst = out + static_cast<size_t>(n) * args.M;
-                            if (args.accumulate) {
-                                v += *dst;
-                                v = v >= mc.m ? v - mc.m : v;
-                            }
-                            *dst = static_cast<uint16_t>(v);
+                        dst[static_cast<size_t>(jj) * args.M] = static_cast<uint16_t>(
+                            combine_psq_fast(static_cast<int32_t>(a1[jj]), static_cast<int32_t>(a2[jj]),
+                                             mc.p, mc.m, mc.magic_p, mc.magic_m, mc.c_p, mc.c_m));
+                    }
+                } else {
+                    for (int jj = 0; jj < 16; ++jj) {
+                        if (tc.n0 + c + jj >= args.N) break;
+                        uint32_t v = combine_psq_fast(static_cast<int32_t>(a1[jj]),
+                                                      static_cast<int32_t>(a2[jj]), mc.p, mc.m,
+                                                      mc.magic_p, mc.magic_m, mc.c_p, mc.c_m);
+                        uint16_t* d = dst + static_cast<size_t>(jj) * args.M;
+                        if (args.accumulate) {
+                            v += *d;
+                            v = min(v, v - mc.m);
                         }
+                        *d = static_cast<uint16_t>(v);
                     }
                 }
             }
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_cluster(leader_tmem_empty);
+            if (diag) busy_epi += static_cast<unsigned long long>(clock64() - e0);
+        }
+        if (diag) {
+            unsigned long long* st = args.stats + cluster_id * kStatSlots;
+            st[5] = w_epi;
+            st[6] = busy_epi;
         }
     }
 
@@ -395,6 +455,7 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     args.super_units = args.F * G + args.L;
     args.active_clusters = clusters;
     args.progress = L.progress;
+    args.stats = reinterpret_cast<unsigned long long*>(L.stats);
     if (L.progress) {
         cudaError_t e = cudaMemsetAsync(L.progress, 0, clusters * sizeof(uint32_t), stream);
         if (e != cudaSuccess) return e;
