@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -183,6 +184,8 @@ int run_ppmm(irl_ctx* ctx, PpmmLaunch L, uint32_t kchunk, cudaStream_t s) {
     }
     if (kchunk == 0 || kchunk > K) kchunk = K;
     if (!L.progress) L.progress = ctx->d_progress;
+    if (const char* sch = std::getenv("IRL_PPMM_SCHEDULE")) L.dynamic_schedule = std::strcmp(sch, "static") != 0;
+    if (const char* gl = std::getenv("IRL_PPMM_GATE")) L.gate_lead = std::atoi(gl);
     if (ctx->diag && ctx->d_diag) {
         L.stats = ctx->d_diag;
         IRL_CK(ctx, cudaMemsetAsync(ctx->d_diag, 0, 1024 * kStatSlots * sizeof(uint64_t), s));
@@ -298,7 +301,7 @@ int irl_ctx_create(int device, irl_ctx** out) {
         cudaMalloc(&ctx->d_stats, sizeof(SplitStats)) != cudaSuccess ||
         cudaMallocHost(&ctx->h_stats, sizeof(SplitStats)) != cudaSuccess ||
         cudaMalloc(&ctx->d_absmax, 2 * sizeof(int32_t)) != cudaSuccess ||
-        cudaMalloc(&ctx->d_progress, 1024 * sizeof(uint32_t)) != cudaSuccess ||
+        cudaMalloc(&ctx->d_progress, kScheduleScratchBytes) != cudaSuccess ||
         cudaMallocHost(&ctx->h_absmax, 2 * sizeof(int32_t)) != cudaSuccess) {
         delete ctx;
         return IRL_ERR_CUDA;
@@ -815,7 +818,7 @@ int irl_ccmm_create(irl_ctx* ctx, size_t parts, size_t m, size_t k, size_t max_n
     if (err == cudaSuccess) err = cudaMalloc(&e->qplanes, qp_b);
     if (err == cudaSuccess) err = cudaMalloc(&e->qres, qr_b);
     if (err == cudaSuccess) err = cudaMalloc(&e->out, out_b);
-    if (err == cudaSuccess) err = cudaMalloc(&e->progress, 1024 * sizeof(uint32_t));
+    if (err == cudaSuccess) err = cudaMalloc(&e->progress, kScheduleScratchBytes);
     if (err == cudaSuccess) err = cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking);
     if (err == cudaSuccess) err = cudaMemsetAsync(e->db, 0, db_b, ctx->stream);
     e->part_done.resize(parts);

@@ -17,6 +17,9 @@ constexpr uint32_t kMaxPrimesPerLaunch = 32;
 // wait cycles, 4 MMA thread total cycles, 5 epilogue tmem-full wait cycles,
 // 6 epilogue busy cycles, 7/8 globaltimer start/end (ns), 11 tiles.
 constexpr uint32_t kStatSlots = 16;
+// Device scratch the PPMM launcher needs (progress counters, unit counter,
+// per-group unit mailboxes); zeroed by every launch.
+constexpr size_t kScheduleScratchBytes = 64 * 1024;
 
 // One batched PPMM launch over `parts` database parts and `nprimes` moduli.
 //   a_planes: [parts][nprimes][2][M][ldk] int8 centred digits (K-major)
@@ -30,8 +33,10 @@ struct PpmmLaunch {
     uint32_t parts = 1, nprimes = 0;
     int accumulate = 0;          // out = (out + result) mod p^2
     uint32_t max_clusters = 0;   // 0 = one CTA pair per SM pair
-    uint32_t* progress = nullptr;  // >= 74 words of scratch: enables group progress gating
+    uint32_t* progress = nullptr;  // kScheduleScratchBytes of device scratch (required)
     uint64_t* stats = nullptr;     // optional [pairs][kStatSlots] diagnostics
+    int dynamic_schedule = 1;      // units from an atomic counter (0: static super-rounds)
+    int gate_lead = -1;            // K blocks a pair may lead its group; -1 default, 0 off
     ModConst mc[kMaxPrimesPerLaunch];
 };
 

@@ -56,21 +56,30 @@ constexpr int kNumThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kAcc2Col = 256;
 constexpr size_t kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
-constexpr uint32_t kGateLead = 12;                // max K blocks a pair may lead its group
+constexpr uint32_t kGateLead = 48;                // max K blocks a pair may lead its group (swept: 6..96)
 constexpr long long kGateSpinCycles = 200000;     // then proceed ungated (forward progress)
+constexpr uint32_t kProgressWords = 1024;        // per-pair progress counters
 
 struct __align__(64) GemmArgs {
     uint32_t M, N, K;
     uint32_t parts, nprimes;
     uint32_t m_blocks, n_blocks, units;
-    // group schedule (see tile_of)
-    uint32_t G, F, L, R, super_units, active_clusters;  // R unused (= G)
+    // group schedule (see group_of)
+    uint32_t G, F, L, active_clusters;
+    uint32_t dynamic;                 // 1: units from an atomic counter; 0: static super-rounds
+    uint32_t gate_lead;               // max K blocks a pair may lead its group (0: no gating)
     uint32_t accumulate;
     uint16_t* out;
-    uint32_t* progress;  // [clusters] K blocks issued by each pair's leader producer
-    unsigned long long* stats;  // optional [clusters][kStatSlots] diagnostics (see ppmm.h)
+    uint32_t* progress;               // [clusters] K blocks issued by each pair's leader producer
+    uint32_t* counter;                // next unit to hand out (dynamic schedule)
+    unsigned long long* mailbox;      // [groups][kMail] ((seq+1) << 32 | unit) published per group
+    unsigned long long* stats;        // optional [clusters][kStatSlots] diagnostics (see ppmm.h)
     ModConst mc[kMaxPrimesPerLaunch];
 };
+
+constexpr int kRing = 4;              // tile-descriptor ring (producer -> MMA / epilogue)
+constexpr uint32_t kMail = 64;        // mailbox slots per group
+constexpr uint32_t kEnd = 0xFFFFFFFFu;
 
 // Diagnostics: wait on a barrier and add the cycles spent to *acc.
 __device__ __forceinline__ void timed_wait(uint64_t* bar, uint32_t parity, bool on,
@@ -94,21 +103,10 @@ struct TileCoord {
     uint32_t prime, part, m0, n0, n_size;
 };
 
-// Local tile j of cluster c. Super-rounds of G tiles per pair: each of the F
-// full groups (G pairs, G = n_blocks) runs G units, one n-tile per pair per
-// unit, in lock-step; each of the L leftover pairs runs one unit alone,
-// sweeping its G n-tiles. Units are prime-major. Returns false past the end.
-__device__ __forceinline__ bool tile_of(const GemmArgs& a, uint32_t c, uint32_t j, TileCoord& t) {
-    const uint32_t sr = j / a.G, r = j % a.G;
-    uint32_t unit, nb;
-    if (c < a.F * a.G) {
-        unit = sr * a.super_units + (c / a.G) * a.G + r;
-        nb = c % a.G;
-    } else {
-        unit = sr * a.super_units + a.F * a.G + (c - a.F * a.G);
-        nb = r;
-    }
-    if (unit >= a.units) return false;
+// A unit is one 256-row block of one (prime, part); units are prime-major so
+// a prime's query planes stay L2-resident while its units are in flight.
+__device__ __forceinline__ TileCoord decode(const GemmArgs& a, uint32_t unit, uint32_t nb) {
+    TileCoord t;
     const uint32_t mb = unit % a.m_blocks;
     const uint32_t pp = unit / a.m_blocks;
     t.part = pp % a.parts;
@@ -118,19 +116,41 @@ __device__ __forceinline__ bool tile_of(const GemmArgs& a, uint32_t c, uint32_t 
     const uint32_t rem = a.N - t.n0;
     const uint32_t ns = rem < kMaxTileN ? rem : kMaxTileN;
     t.n_size = (ns + 31u) & ~31u;  // cta_group::2 kind::i8 needs N % 32 == 0
-    return true;
+    return t;
 }
 
-// Group members of cluster c: [first, first + size) (leftover pairs: size 1).
-__device__ __forceinline__ void group_of(const GemmArgs& a, uint32_t c, uint32_t& first,
-                                         uint32_t& size) {
+// Groups: F full groups of G = n_blocks pairs (pair i of a group computes
+// n-tile i of every unit the group takes, all pairs in lock-step), then L
+// solo pairs that sweep all G n-tiles of their units themselves.
+struct GroupInfo {
+    uint32_t id, first, size, member;
+    bool solo;
+};
+__device__ __forceinline__ GroupInfo group_of(const GemmArgs& a, uint32_t c) {
+    GroupInfo g;
     if (c < a.F * a.G) {
-        first = (c / a.G) * a.G;
-        size = a.G;
+        g.id = c / a.G;
+        g.first = g.id * a.G;
+        g.size = a.G;
+        g.member = c % a.G;
+        g.solo = a.G == 1;
     } else {
-        first = c;
-        size = 1;
+        g.id = a.F + (c - a.F * a.G);
+        g.first = c;
+        g.size = 1;
+        g.member = 0;
+        g.solo = true;
     }
+    return g;
+}
+
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
@@ -144,14 +164,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
     uint64_t* empty_bar = full_bar + kStages;
     uint64_t* tmem_full_bar = empty_bar + kStages;
     uint64_t* tmem_empty_bar = tmem_full_bar + 1;
-    uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty_bar + 1);
+    uint64_t* ring_full = tmem_empty_bar + 1;
+    uint64_t* ring_empty = ring_full + kRing;
+    uint32_t* ring_tile = reinterpret_cast<uint32_t*>(ring_empty + kRing);  // [kRing][2]
+    uint32_t* tmem_base_slot = ring_tile + 2 * kRing;
 
     const uint32_t warp = threadIdx.x / 32;
     const uint32_t lane = threadIdx.x % 32;
     const uint32_t rank = ptx::cluster_ctarank();
     const bool leader = rank == 0;
     const uint32_t cluster_id = blockIdx.x / 2;
-    const bool active = cluster_id < args.active_clusters;
 
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmap_a);
@@ -162,6 +184,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
         }
         ptx::mbar_init(tmem_full_bar, 1);
         ptx::mbar_init(tmem_empty_bar, 2 * kEpiWarps);
+        for (int s = 0; s < kRing; ++s) {
+            ptx::mbar_init(&ring_full[s], 1);
+            ptx::mbar_init(&ring_empty[s], (leader ? 1 : 0) + kEpiWarps);
+        }
         ptx::fence_barrier_init();
     }
     if (warp == 1) {
@@ -172,68 +198,133 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_base_slot;
 
-    if (!active) {
-        // idle pair (group schedule leftover): nothing to do
-    } else if (warp == 0) {
-        // ---------------- TMA producer (both CTAs) ----------------
+    if (warp == 0) {
+        // ---------------- TMA producer + scheduler (both CTAs) ----------------
         if (lane == 0) {
             const uint32_t num_kb = (args.K + kBlockK - 1) / kBlockK;
-            uint32_t gfirst, gsize;
-            group_of(args, cluster_id, gfirst, gsize);
-            const bool gate = leader && args.progress != nullptr && gsize > 1;
+            const GroupInfo grp = group_of(args, cluster_id);
+            const bool gate = leader && grp.size > 1 && args.gate_lead > 0;
+            const uint32_t lead = args.gate_lead;
+            const bool writer = leader && grp.member == 0;  // takes units for the group
+            unsigned long long* mbox = args.mailbox + static_cast<size_t>(grp.id) * kMail;
+            const uint32_t tiles_per_unit = grp.solo ? args.G : 1;
             uint32_t issued = 0;  // cumulative K blocks (comparable across the group)
             uint32_t seen = 0;    // last observed minimum of the peers' counters
-            uint32_t stage = 0, phase = 0;
+            uint32_t stage = 0, phase = 0, tile_i = 0;
             const bool diag = args.stats != nullptr && leader;
             unsigned long long w_empty = 0, w_gate = 0;
-            TileCoord tc;
-            for (uint32_t j = 0; tile_of(args, cluster_id, j, tc); ++j) {
-                const uint32_t a_row0 =
-                    ((tc.part * args.nprimes + tc.prime) * 2) * args.M + tc.m0 + rank * kRowsPerCta;
-                const uint32_t half_n = tc.n_size / 2;
-                const uint32_t b_row0 = (tc.prime * 2) * args.N + tc.n0 + rank * half_n;
-                for (uint32_t kb = 0; kb < num_kb; ++kb, ++issued) {
-                    timed_wait(&empty_bar[stage], phase ^ 1, diag, w_empty);
-                    if (gate && issued > seen + kGateLead) {
-                        // Stay within kGateLead K blocks of the slowest group peer.
-                        // `seen` caches the last observed minimum, so the L2
-                        // round trip is paid about once per kGateLead blocks.
-                        const long long t0 = clock64();
-                        for (;;) {
-                            uint32_t lo = 0xFFFFFFFFu;
-                            for (uint32_t p = gfirst; p < gfirst + gsize; ++p)
-                                if (p != cluster_id) lo = min(lo, ptx::ld_relaxed_gpu(args.progress + p));
-                            seen = lo;
-                            if (lo + kGateLead >= issued) break;
-                            if (clock64() - t0 > kGateSpinCycles) {
-                                seen = issued;  // give up for kGateLead blocks (forward progress)
-                                break;
-                            }
-                            __nanosleep(32);
-                        }
-                        if (diag) w_gate += static_cast<unsigned long long>(clock64() - t0);
+
+            auto grab = [&]() -> uint32_t {
+                if (grp.solo && grp.size == 1 && args.G > 1) {
+                    // a solo pair needs G tile-times per unit: stop before the
+                    // tail so it never finishes last
+                    if (ptx::ld_relaxed_gpu(args.counter) + args.G * args.F >= args.units) return kEnd;
+                }
+                const uint32_t u = atomicAdd(args.counter, 1u);
+                return u < args.units ? u : kEnd;
+            };
+            // static schedule (args.dynamic == 0): the super-round layout
+            const uint32_t super_units = args.F * args.G + args.L;
+            auto static_unit = [&](uint32_t seq) -> uint32_t {
+                const uint32_t u = cluster_id < args.F * args.G
+                                       ? (seq / args.G) * super_units + grp.id * args.G + seq % args.G
+                                       : seq * super_units + args.F * args.G + (grp.id - args.F);
+                return u < args.units ? u : kEnd;
+            };
+            auto publish = [&](uint32_t seq, uint32_t u) {
+                // tag = seq + 1 so the zeroed mailbox never matches
+                st_relaxed_u64(mbox + seq % kMail,
+                               (static_cast<unsigned long long>(seq + 1) << 32) | u);
+            };
+            auto push_tile = [&](uint32_t u, uint32_t nb) {
+                const uint32_t slot = tile_i % kRing;
+                ptx::mbar_wait(&ring_empty[slot], ((tile_i / kRing) & 1) ^ 1);
+                ring_tile[2 * slot] = u;
+                ring_tile[2 * slot + 1] = nb;
+                asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(
+                                 ptx::smem_u32(&ring_full[slot]))
+                             : "memory");
+                ++tile_i;
+            };
+
+            uint32_t u_next = 0;
+            if (writer && args.dynamic) {
+                u_next = grab();
+                publish(0, u_next);
+            }
+            for (uint32_t seq = 0;; ++seq) {
+                uint32_t u;
+                if (!args.dynamic) {
+                    u = static_unit(seq);
+                } else if (writer) {
+                    u = u_next;
+                    if (u != kEnd) {
+                        u_next = grab();  // prefetch: members never wait at a unit boundary
+                        publish(seq + 1, u_next);
                     }
-                    const uint32_t leader_full =
-                        ptx::mapa_shared(ptx::smem_u32(&full_bar[stage]), 0);
-                    if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * kStageBytes);
-                    uint8_t* st = smem + stage * kStageBytes;
-                    const int32_t k0 = static_cast<int32_t>(kb * kBlockK);
-                    ptx::tma_load_2d_pair(ptx::smem_u32(st), &tmap_a, leader_full, k0,
-                                          static_cast<int32_t>(a_row0));
-                    ptx::tma_load_2d_pair(ptx::smem_u32(st + kPlaneTileBytes), &tmap_a,
-                                          leader_full, k0,
-                                          static_cast<int32_t>(a_row0 + args.M));
-                    ptx::tma_load_2d_pair_hint(ptx::smem_u32(st + 2 * kPlaneTileBytes), &tmap_b,
-                                               leader_full, k0, static_cast<int32_t>(b_row0),
-                                               ptx::kL2EvictLast);
-                    ptx::tma_load_2d_pair_hint(ptx::smem_u32(st + 3 * kPlaneTileBytes), &tmap_b,
-                                               leader_full, k0,
-                                               static_cast<int32_t>(b_row0 + args.N),
-                                               ptx::kL2EvictLast);
-                    if (gate) ptx::st_relaxed_gpu(args.progress + cluster_id, issued + 1);
-                    if (++stage == kStages) {
-                        stage = 0;
-                        phase ^= 1;
+                } else {
+                    unsigned long long v;
+                    while (((v = ld_relaxed_u64(mbox + seq % kMail)) >> 32) != seq + 1) {
+                        __nanosleep(64);
+                    }
+                    u = static_cast<uint32_t>(v);
+                }
+                if (u == kEnd) {
+                    push_tile(kEnd, 0);
+                    break;
+                }
+                for (uint32_t r = 0; r < tiles_per_unit; ++r) {
+                    const uint32_t nb = grp.solo ? r : grp.member;
+                    push_tile(u, nb);
+                    const TileCoord tc = decode(args, u, nb);
+                    const uint32_t a_row0 = ((tc.part * args.nprimes + tc.prime) * 2) * args.M +
+                                            tc.m0 + rank * kRowsPerCta;
+                    const uint32_t half_n = tc.n_size / 2;
+                    const uint32_t b_row0 = (tc.prime * 2) * args.N + tc.n0 + rank * half_n;
+                    for (uint32_t kb = 0; kb < num_kb; ++kb, ++issued) {
+                        timed_wait(&empty_bar[stage], phase ^ 1, diag, w_empty);
+                        if (gate && issued > seen + lead) {
+                            // Stay within kGateLead K blocks of the slowest group peer.
+                            // `seen` caches the last observed minimum, so the L2
+                            // round trip is paid about once per kGateLead blocks.
+                            const long long t0 = clock64();
+                            for (;;) {
+                                uint32_t lo = 0xFFFFFFFFu;
+                                for (uint32_t p = grp.first; p < grp.first + grp.size; ++p)
+                                    if (p != cluster_id)
+                                        lo = min(lo, ptx::ld_relaxed_gpu(args.progress + p));
+                                seen = lo;
+                                if (lo + lead >= issued) break;
+                                if (clock64() - t0 > kGateSpinCycles) {
+                                    seen = issued;  // give up for kGateLead blocks (forward progress)
+                                    break;
+                                }
+                                __nanosleep(32);
+                            }
+                            if (diag) w_gate += static_cast<unsigned long long>(clock64() - t0);
+                        }
+                        const uint32_t leader_full =
+                            ptx::mapa_shared(ptx::smem_u32(&full_bar[stage]), 0);
+                        if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * kStageBytes);
+                        uint8_t* st = smem + stage * kStageBytes;
+                        const int32_t k0 = static_cast<int32_t>(kb * kBlockK);
+                        ptx::tma_load_2d_pair(ptx::smem_u32(st), &tmap_a, leader_full, k0,
+                                              static_cast<int32_t>(a_row0));
+                        ptx::tma_load_2d_pair(ptx::smem_u32(st + kPlaneTileBytes), &tmap_a,
+                                              leader_full, k0,
+                                              static_cast<int32_t>(a_row0 + args.M));
+                        ptx::tma_load_2d_pair_hint(ptx::smem_u32(st + 2 * kPlaneTileBytes),
+                                                   &tmap_b, leader_full, k0,
+                                                   static_cast<int32_t>(b_row0), ptx::kL2EvictLast);
+                        ptx::tma_load_2d_pair_hint(ptx::smem_u32(st + 3 * kPlaneTileBytes),
+                                                   &tmap_b, leader_full, k0,
+                                                   static_cast<int32_t>(b_row0 + args.N),
+                                                   ptx::kL2EvictLast);
+                        if (gate) ptx::st_relaxed_gpu(args.progress + cluster_id, issued + 1);
+                        if (++stage == kStages) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
                     }
                 }
             }
@@ -254,9 +345,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
             unsigned long long w_full = 0, w_tmem = 0;
             const long long c_start = clock64();
             const unsigned long long g_start = diag ? globaltimer() : 0;
-            uint32_t tiles = 0;
-            TileCoord tc;
-            for (uint32_t j = 0; tile_of(args, cluster_id, j, tc); ++j, ++tiles) {
+            uint32_t j = 0;
+            for (;; ++j) {
+                const uint32_t slot = j % kRing;
+                ptx::mbar_wait(&ring_full[slot], (j / kRing) & 1);
+                const uint32_t u = ring_tile[2 * slot], nb = ring_tile[2 * slot + 1];
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                                 ptx::smem_u32(&ring_empty[slot]))
+                             : "memory");
+                if (u == kEnd) break;
+                const TileCoord tc = decode(args, u, nb);
                 const uint32_t idesc = ptx::idesc_i8(2 * kRowsPerCta, tc.n_size);
                 // Wait until the epilogue of the previous tile drained TMEM.
                 timed_wait(tmem_empty_bar, (j & 1) ^ 1, diag, w_tmem);
@@ -288,15 +386,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
                 ptx::mma_commit_pair(tmem_full_bar, 0x3);
             }
             if (diag) {
-                // wait for the last tile's MMAs so the end stamps cover them
-                timed_wait(tmem_empty_bar, (tiles & 1) ^ 1, false, w_tmem);
+                // wait for the last tile's drain so the end stamps cover it
+                if (j > 0) timed_wait(tmem_empty_bar, (j & 1) ^ 1, false, w_tmem);
                 unsigned long long* st = args.stats + cluster_id * kStatSlots;
                 st[2] = w_full;
                 st[3] = w_tmem;
                 st[4] = static_cast<unsigned long long>(clock64() - c_start);
                 st[7] = g_start;
                 st[8] = globaltimer();
-                st[11] = tiles;
+                st[11] = j;
             }
         }
     } else {
@@ -306,8 +404,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
         const uint32_t leader_tmem_empty = ptx::mapa_shared(ptx::smem_u32(tmem_empty_bar), 0);
         const bool diag = args.stats != nullptr && leader && warp == 2 && lane == 0;
         unsigned long long w_epi = 0, busy_epi = 0;
-        TileCoord tc;
-        for (uint32_t j = 0; tile_of(args, cluster_id, j, tc); ++j) {
+        for (uint32_t j = 0;; ++j) {
+            const uint32_t slot = j % kRing;
+            ptx::mbar_wait(&ring_full[slot], (j / kRing) & 1);
+            const uint32_t u = ring_tile[2 * slot], nb = ring_tile[2 * slot + 1];
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                                 ptx::smem_u32(&ring_empty[slot]))
+                             : "memory");
+            if (u == kEnd) break;
+            const TileCoord tc = decode(args, u, nb);
             const ModConst mc = args.mc[tc.prime];
             timed_wait(tmem_full_bar, j & 1, diag, w_epi);
             const long long e0 = clock64();
@@ -444,20 +551,29 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     if (L.max_clusters > 0) clusters = std::min<uint32_t>(clusters, L.max_clusters);
 
     // Group schedule: G = n_blocks pairs share each unit's A tile (one n-tile
-    // each); never more pairs than there are tiles.
+    // each); never more pairs than there are tiles. Units are handed out
+    // dynamically (args.counter), so faster groups take more of them.
     const uint64_t tiles = static_cast<uint64_t>(args.units) * args.n_blocks;
     clusters = static_cast<uint32_t>(std::min<uint64_t>(clusters, tiles));
     const uint32_t G = args.n_blocks;
     args.G = G;
     args.F = clusters / G;
     args.L = clusters % G;
-    args.R = G;
-    args.super_units = args.F * G + args.L;
     args.active_clusters = clusters;
+    args.dynamic = L.dynamic_schedule ? 1u : 0u;
+    args.gate_lead = L.gate_lead < 0 ? kGateLead : static_cast<uint32_t>(L.gate_lead);
+    const uint32_t groups = args.F + args.L;
+    if (!L.progress) return cudaErrorInvalidValue;
     args.progress = L.progress;
+    args.counter = L.progress + kProgressWords;
+    args.mailbox = reinterpret_cast<unsigned long long*>(L.progress + kProgressWords + 32);
+    if ((kProgressWords + 32) * 4 + static_cast<size_t>(groups) * kMail * 8 > kScheduleScratchBytes)
+        return cudaErrorInvalidValue;
     args.stats = reinterpret_cast<unsigned long long*>(L.stats);
-    if (L.progress) {
-        cudaError_t e = cudaMemsetAsync(L.progress, 0, clusters * sizeof(uint32_t), stream);
+    {
+        cudaError_t e = cudaMemsetAsync(L.progress, 0,
+                                        (kProgressWords + 32) * 4 + static_cast<size_t>(groups) * kMail * 8,
+                                        stream);
         if (e != cudaSuccess) return e;
     }
 

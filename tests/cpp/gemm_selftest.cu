@@ -74,7 +74,7 @@ static int run_case(uint32_t parts, uint32_t nprimes, uint32_t M, uint32_t N, ui
     L.parts = parts;
     L.nprimes = nprimes;
     uint32_t* prog = nullptr;
-    CK(cudaMalloc(&prog, 4096));
+    CK(cudaMalloc(&prog, kScheduleScratchBytes));
     L.progress = prog;
     for (uint32_t i = 0; i < nprimes; ++i) L.mc[i] = make_modconst(kPrimes[i], 2);
     CK(launch_ppmm_planes(L, 0));
