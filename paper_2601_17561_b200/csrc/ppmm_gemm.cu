@@ -395,6 +395,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
                 st[7] = g_start;
                 st[8] = globaltimer();
                 st[11] = j;
+                unsigned smid;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                st[12] = smid;
             }
         }
     } else {

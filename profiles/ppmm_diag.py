@@ -64,6 +64,7 @@ def main():
             "slowest_pairs": [(int(i), round(float((st[i, 8] - st[i, 7]) / 1e6), 2))
                               for i in np.argsort(-(st[:, 8] - st[:, 7]) * act)[:6]],
             "pair_ms_by_id": [round(float(x / 1e6), 1) for x in (st[:, 8] - st[:, 7])[act]],
+            "smid_by_pair": [int(x) for x in st[:, 12][act]],
         })
     L.irl_diag_ppmm(eng.ctx.handle, 0, None, 0)
     ops = 6.0 * eng.nmod * a.rows * a.n * a.k * a.parts
