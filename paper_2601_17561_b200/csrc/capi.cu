@@ -186,6 +186,7 @@ int run_ppmm(irl_ctx* ctx, PpmmLaunch L, uint32_t kchunk, cudaStream_t s) {
     if (!L.progress) L.progress = ctx->d_progress;
     if (const char* sch = std::getenv("IRL_PPMM_SCHEDULE")) L.dynamic_schedule = std::strcmp(sch, "static") != 0;
     if (const char* gl = std::getenv("IRL_PPMM_GATE")) L.gate_lead = std::atoi(gl);
+    if (const char* cl = std::getenv("IRL_PPMM_CLUSTER")) L.cluster_ctas = std::atoi(cl);
     if (ctx->diag && ctx->d_diag) {
         L.stats = ctx->d_diag;
         IRL_CK(ctx, cudaMemsetAsync(ctx->d_diag, 0, 1024 * kStatSlots * sizeof(uint64_t), s));

@@ -37,6 +37,7 @@ struct PpmmLaunch {
     uint64_t* stats = nullptr;     // optional [pairs][kStatSlots] diagnostics
     int dynamic_schedule = 1;      // units from an atomic counter (0: static super-rounds)
     int gate_lead = -1;            // K blocks a pair may lead its group; -1 default, 0 off
+    int cluster_ctas = 4;          // 4: two pairs per cluster multicasting A (+2-CTA filler); 2: one pair
     ModConst mc[kMaxPrimesPerLaunch];
 };
 

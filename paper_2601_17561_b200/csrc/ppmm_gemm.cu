@@ -64,7 +64,7 @@ struct __align__(64) GemmArgs {
     uint32_t M, N, K;
     uint32_t parts, nprimes;
     uint32_t m_blocks, n_blocks, units;
-    // group schedule (see group_of)
+    // group schedule (see group_of): G = clusters per full group
     uint32_t G, F, L, active_clusters;
     uint32_t dynamic;                 // 1: units from an atomic counter; 0: static super-rounds
     uint32_t gate_lead;               // max K blocks a pair may lead its group (0: no gating)
@@ -119,16 +119,17 @@ __device__ __forceinline__ TileCoord decode(const GemmArgs& a, uint32_t unit, ui
     return t;
 }
 
-// Groups: F full groups of G = n_blocks pairs (pair i of a group computes
-// n-tile i of every unit the group takes, all pairs in lock-step), then L
-// solo pairs that sweep all G n-tiles of their units themselves.
+// Groups (cluster granularity): each cluster holds P CTA pairs. F full groups
+// of Gc = G / P clusters split a unit's G = n_blocks n-tiles (pair p of group
+// member c computes n-tile c*P + p of every unit the group takes, in
+// lock-step); then L solo clusters that sweep a unit's n-tiles in G / P passes.
 struct GroupInfo {
     uint32_t id, first, size, member;
     bool solo;
 };
 __device__ __forceinline__ GroupInfo group_of(const GemmArgs& a, uint32_t c) {
     GroupInfo g;
-    if (c < a.F * a.G) {
+    if (c < a.F * a.G) {  // here a.G = clusters per full group
         g.id = c / a.G;
         g.first = g.id * a.G;
         g.size = a.G;
@@ -153,10 +154,15 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
     return v;
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
+// kCtas = CTAs per cluster: 2 (one pair) or 4 (two pairs sharing each A tile
+// through TMA multicast: each CTA loads half of its 128-row A block and
+// multicasts it to the CTA with the same role in the other pair).
+template <int kCtas>
+__global__ void __launch_bounds__(kNumThreads, 1)
     ppmm_i8_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a,
                          const __grid_constant__ CUtensorMap tmap_b,
                          const __grid_constant__ GemmArgs args) {
+    constexpr uint32_t kPairs = kCtas / 2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -172,15 +178,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
     const uint32_t warp = threadIdx.x / 32;
     const uint32_t lane = threadIdx.x % 32;
     const uint32_t rank = ptx::cluster_ctarank();
-    const bool leader = rank == 0;
-    const uint32_t cluster_id = blockIdx.x / 2;
+    const uint32_t pair = rank >> 1;          // pair within the cluster
+    const uint32_t half_rank = rank & 1;      // CTA within the pair
+    const bool leader = half_rank == 0;       // pair leader (issues the MMAs)
+    const uint32_t cluster_id = blockIdx.x / kCtas;
 
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmap_a);
         ptx::prefetch_tmap(&tmap_b);
         for (int s = 0; s < kStages; ++s) {
             ptx::mbar_init(&full_bar[s], 1);
-            ptx::mbar_init(&empty_bar[s], 1);
+            ptx::mbar_init(&empty_bar[s], kPairs);  // one commit per pair reading this stage
         }
         ptx::mbar_init(tmem_full_bar, 1);
         ptx::mbar_init(tmem_empty_bar, 2 * kEpiWarps);
@@ -203,11 +211,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
         if (lane == 0) {
             const uint32_t num_kb = (args.K + kBlockK - 1) / kBlockK;
             const GroupInfo grp = group_of(args, cluster_id);
-            const bool gate = leader && grp.size > 1 && args.gate_lead > 0;
+            const bool gate = rank == 0 && grp.size > 1 && args.gate_lead > 0;
             const uint32_t lead = args.gate_lead;
-            const bool writer = leader && grp.member == 0;  // takes units for the group
+            const bool writer = rank == 0 && grp.member == 0;  // takes units for the group
             unsigned long long* mbox = args.mailbox + static_cast<size_t>(grp.id) * kMail;
-            const uint32_t tiles_per_unit = grp.solo ? args.G : 1;
+            const uint32_t tiles_per_unit = grp.solo ? args.n_blocks / kPairs : 1;
             uint32_t issued = 0;  // cumulative K blocks (comparable across the group)
             uint32_t seen = 0;    // last observed minimum of the peers' counters
             uint32_t stage = 0, phase = 0, tile_i = 0;
@@ -216,7 +224,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
 
             auto grab = [&]() -> uint32_t {
                 if (grp.solo && grp.size == 1 && args.G > 1) {
-                    // a solo pair needs G tile-times per unit: stop before the
+                    // a solo cluster needs G tile-times per unit: stop before the
                     // tail so it never finishes last
                     if (ptx::ld_relaxed_gpu(args.counter) + args.G * args.F >= args.units) return kEnd;
                 }
@@ -274,13 +282,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
                     break;
                 }
                 for (uint32_t r = 0; r < tiles_per_unit; ++r) {
-                    const uint32_t nb = grp.solo ? r : grp.member;
+                    const uint32_t nb = (grp.solo ? r : grp.member) * kPairs + pair;
                     push_tile(u, nb);
                     const TileCoord tc = decode(args, u, nb);
                     const uint32_t a_row0 = ((tc.part * args.nprimes + tc.prime) * 2) * args.M +
-                                            tc.m0 + rank * kRowsPerCta;
+                                            tc.m0 + half_rank * kRowsPerCta;
                     const uint32_t half_n = tc.n_size / 2;
-                    const uint32_t b_row0 = (tc.prime * 2) * args.N + tc.n0 + rank * half_n;
+                    const uint32_t b_row0 = (tc.prime * 2) * args.N + tc.n0 + half_rank * half_n;
                     for (uint32_t kb = 0; kb < num_kb; ++kb, ++issued) {
                         timed_wait(&empty_bar[stage], phase ^ 1, diag, w_empty);
                         if (gate && issued > seen + lead) {
@@ -303,16 +311,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
                             }
                             if (diag) w_gate += static_cast<unsigned long long>(clock64() - t0);
                         }
-                        const uint32_t leader_full =
-                            ptx::mapa_shared(ptx::smem_u32(&full_bar[stage]), 0);
+                        // completion bytes land on the pair leader's barrier
+                        const uint32_t leader_full = ptx::smem_u32(&full_bar[stage]) & 0xFEFFFFFFu;
                         if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * kStageBytes);
                         uint8_t* st = smem + stage * kStageBytes;
                         const int32_t k0 = static_cast<int32_t>(kb * kBlockK);
-                        ptx::tma_load_2d_pair(ptx::smem_u32(st), &tmap_a, leader_full, k0,
-                                              static_cast<int32_t>(a_row0));
-                        ptx::tma_load_2d_pair(ptx::smem_u32(st + kPlaneTileBytes), &tmap_a,
-                                              leader_full, k0,
-                                              static_cast<int32_t>(a_row0 + args.M));
+                        if constexpr (kCtas == 2) {
+                            ptx::tma_load_2d_pair(ptx::smem_u32(st), &tmap_a, leader_full, k0,
+                                                  static_cast<int32_t>(a_row0));
+                            ptx::tma_load_2d_pair(ptx::smem_u32(st + kPlaneTileBytes), &tmap_a,
+                                                  leader_full, k0,
+                                                  static_cast<int32_t>(a_row0 + args.M));
+                        } else {
+                            // this CTA loads rows [64 pair, +64) of both A planes for
+                            // itself and the same-role CTA of the other pair
+                            const uint16_t mask = static_cast<uint16_t>((1u << rank) | (1u << (rank ^ 2)));
+                            const uint32_t sub = pair * (kPlaneTileBytes / 2);
+                            ptx::tma_load_2d_pair_mcast(ptx::smem_u32(st) + sub, &tmap_a, leader_full, k0,
+                                                        static_cast<int32_t>(a_row0 + pair * 64), mask);
+                            ptx::tma_load_2d_pair_mcast(ptx::smem_u32(st + kPlaneTileBytes) + sub, &tmap_a,
+                                                        leader_full, k0,
+                                                        static_cast<int32_t>(a_row0 + args.M + pair * 64),
+                                                        mask);
+                        }
                         ptx::tma_load_2d_pair_hint(ptx::smem_u32(st + 2 * kPlaneTileBytes),
                                                    &tmap_b, leader_full, k0,
                                                    static_cast<int32_t>(b_row0), ptx::kL2EvictLast);
@@ -329,7 +350,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
                 }
             }
             if (diag) {
-                unsigned long long* st = args.stats + cluster_id * kStatSlots;
+                unsigned long long* st = args.stats + (blockIdx.x >> 1) * kStatSlots;
                 st[0] = w_empty;
                 st[1] = w_gate;
             }
@@ -377,18 +398,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
                         ptx::mma_i8_pair(acc2, dx0, dy1, idesc, accum);  // X0 Y1
                         ptx::mma_i8_pair(acc2, dx1, dy0, idesc, 1u);     // + X1 Y0
                     }
-                    ptx::mma_commit_pair(&empty_bar[stage], 0x3);
+                    // release the stage in every CTA that wrote into it
+                    ptx::mma_commit_pair(&empty_bar[stage], kCtas == 2 ? 0x3 : 0xF);
                     if (++stage == kStages) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                ptx::mma_commit_pair(tmem_full_bar, 0x3);
+                ptx::mma_commit_pair(tmem_full_bar, static_cast<uint16_t>(0x3u << (2 * pair)));
             }
             if (diag) {
                 // wait for the last tile's drain so the end stamps cover it
                 if (j > 0) timed_wait(tmem_empty_bar, (j & 1) ^ 1, false, w_tmem);
-                unsigned long long* st = args.stats + cluster_id * kStatSlots;
+                unsigned long long* st = args.stats + (blockIdx.x >> 1) * kStatSlots;
                 st[2] = w_full;
                 st[3] = w_tmem;
                 st[4] = static_cast<unsigned long long>(clock64() - c_start);
@@ -404,7 +426,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
         // ---------------- Epilogue (both CTAs, 8 warps) ----------------
         const uint32_t quarter = warp % 4;        // TMEM lane quarter this warp may access
         const uint32_t half = (warp - 2) / 4;     // which half of the tile's columns
-        const uint32_t leader_tmem_empty = ptx::mapa_shared(ptx::smem_u32(tmem_empty_bar), 0);
+        const uint32_t leader_tmem_empty = ptx::mapa_shared(ptx::smem_u32(tmem_empty_bar), rank & ~1u);
         const bool diag = args.stats != nullptr && leader && warp == 2 && lane == 0;
         unsigned long long w_epi = 0, busy_epi = 0;
         for (uint32_t j = 0;; ++j) {
@@ -422,7 +444,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
             timed_wait(tmem_full_bar, j & 1, diag, w_epi);
             const long long e0 = clock64();
             ptx::tc_fence_after();
-            const uint32_t row = rank * kRowsPerCta + quarter * 32 + lane;
+            const uint32_t row = half_rank * kRowsPerCta + quarter * 32 + lane;
             const uint32_t m = tc.m0 + row;
             const bool row_ok = m < args.M;
             uint16_t* out = args.out +
@@ -468,7 +490,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
             if (diag) busy_epi += static_cast<unsigned long long>(clock64() - e0);
         }
         if (diag) {
-            unsigned long long* st = args.stats + cluster_id * kStatSlots;
+            unsigned long long* st = args.stats + (blockIdx.x >> 1) * kStatSlots;
             st[5] = w_epi;
             st[6] = busy_epi;
         }
@@ -497,15 +519,69 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
     return fn;
 }
 
-bool make_plane_map(CUtensorMap* map, const void* base, uint64_t k, uint64_t rows, uint64_t ldk) {
+bool make_plane_map(CUtensorMap* map, const void* base, uint64_t k, uint64_t rows, uint64_t ldk,
+                    uint32_t box_rows) {
     const cuuint64_t dims[2] = {k, rows};
     const cuuint64_t strides[1] = {ldk};
-    const cuuint32_t box[2] = {kBlockK, kRowsPerCta};
+    const cuuint32_t box[2] = {kBlockK, box_rows};
     const cuuint32_t estr[2] = {1, 1};
     return get_encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims,
                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Co-resident clusters of `ctas` CTAs with this kernel's footprint (cached per device).
+uint32_t max_active_clusters(int ctas, int dev) {
+    static std::mutex mu;
+    static int cache[64][2];
+    static bool init = false;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!init) {
+        for (auto& c : cache) c[0] = c[1] = -1;
+        init = true;
+    }
+    const int vi = ctas == 4 ? 1 : 0;
+    if (dev < 0 || dev >= 64) return 0;
+    if (cache[dev][vi] >= 0) return static_cast<uint32_t>(cache[dev][vi]);
+    auto kfn = ctas == 4 ? ppmm_i8_sm100_kernel<4> : ppmm_i8_sm100_kernel<2>;
+    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kSmemBytes)) != cudaSuccess)
+        return 0;
+    cudaLaunchConfig_t q{};
+    q.gridDim = dim3(static_cast<unsigned>(ctas) * 64);
+    q.blockDim = dim3(kNumThreads);
+    q.dynamicSmemBytes = kSmemBytes;
+    cudaLaunchAttribute qa[1];
+    qa[0].id = cudaLaunchAttributeClusterDimension;
+    qa[0].val.clusterDim.x = static_cast<unsigned>(ctas);
+    qa[0].val.clusterDim.y = 1;
+    qa[0].val.clusterDim.z = 1;
+    q.attrs = qa;
+    q.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kfn, &q) != cudaSuccess) n = 0;
+    cache[dev][vi] = n;
+    return static_cast<uint32_t>(n);
+}
+
+// Per-device side stream + fork/join events for the filler launch.
+cudaError_t side_stream(int dev, cudaStream_t* s, cudaEvent_t* fork, cudaEvent_t* join) {
+    static std::mutex mu;
+    static cudaStream_t streams[64] = {};
+    static cudaEvent_t forks[64] = {}, joins[64] = {};
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!streams[dev]) {
+        cudaError_t e = cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&forks[dev], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&joins[dev], cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+    }
+    *s = streams[dev];
+    *fork = forks[dev];
+    *join = joins[dev];
+    return cudaSuccess;
 }
 
 }  // namespace
@@ -519,11 +595,6 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     const uint64_t a_rows = static_cast<uint64_t>(L.parts) * L.nprimes * 2 * L.M;
     const uint64_t b_rows = static_cast<uint64_t>(L.nprimes) * 2 * L.N;
     if (a_rows >= (1ull << 31) || b_rows >= (1ull << 31)) return cudaErrorInvalidValue;
-
-    CUtensorMap ma, mb;
-    if (!make_plane_map(&ma, L.a_planes, L.K, a_rows, L.ldk) ||
-        !make_plane_map(&mb, L.b_planes, L.K, b_rows, L.ldk))
-        return cudaErrorInvalidValue;
 
     GemmArgs args;
     std::memset(&args, 0, sizeof(args));
@@ -539,60 +610,100 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     args.out = L.out;
     for (uint32_t i = 0; i < L.nprimes; ++i) args.mc[i] = L.mc[i];
 
-    static int attr_dev = -1;
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    if (attr_dev != dev) {
-        cudaError_t e = cudaFuncSetAttribute(ppmm_i8_sm100_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(kSmemBytes));
-        if (e != cudaSuccess) return e;
-        attr_dev = dev;
-    }
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    uint32_t clusters = static_cast<uint32_t>(sms / 2);
-    if (L.max_clusters > 0) clusters = std::min<uint32_t>(clusters, L.max_clusters);
-
-    // Group schedule: G = n_blocks pairs share each unit's A tile (one n-tile
-    // each); never more pairs than there are tiles. Units are handed out
-    // dynamically (args.counter), so faster groups take more of them.
-    const uint64_t tiles = static_cast<uint64_t>(args.units) * args.n_blocks;
-    clusters = static_cast<uint32_t>(std::min<uint64_t>(clusters, tiles));
-    const uint32_t G = args.n_blocks;
-    args.G = G;
-    args.F = clusters / G;
-    args.L = clusters % G;
-    args.active_clusters = clusters;
+    if (!L.progress) return cudaErrorInvalidValue;
     args.dynamic = L.dynamic_schedule ? 1u : 0u;
     args.gate_lead = L.gate_lead < 0 ? kGateLead : static_cast<uint32_t>(L.gate_lead);
-    const uint32_t groups = args.F + args.L;
-    if (!L.progress) return cudaErrorInvalidValue;
-    args.progress = L.progress;
-    args.counter = L.progress + kProgressWords;
-    args.mailbox = reinterpret_cast<unsigned long long*>(L.progress + kProgressWords + 32);
-    if ((kProgressWords + 32) * 4 + static_cast<size_t>(groups) * kMail * 8 > kScheduleScratchBytes)
-        return cudaErrorInvalidValue;
-    args.stats = reinterpret_cast<unsigned long long*>(L.stats);
-    {
-        cudaError_t e = cudaMemsetAsync(L.progress, 0,
-                                        (kProgressWords + 32) * 4 + static_cast<size_t>(groups) * kMail * 8,
-                                        stream);
+    args.counter = L.progress + kProgressWords;  // shared by every launch of this call
+
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const bool want4 = L.cluster_ctas == 4 && args.n_blocks % 2 == 0;
+    const uint32_t occ2 = max_active_clusters(2, dev);
+    const uint32_t occ4 = want4 ? max_active_clusters(4, dev) : 0;
+    if (occ2 == 0 || (want4 && occ4 == 0)) return cudaErrorInvalidConfiguration;
+
+    // Cluster layouts: the main launch uses 4-CTA clusters (two pairs
+    // multicasting each A tile) when requested; 4-CTA clusters strand SMs
+    // (132 of 148 CTAs on B200), so a 2-CTA "filler" launch on a side stream
+    // takes the remaining SM pairs. Both pull units from the same counter.
+    struct Part {
+        int ctas;
+        uint32_t clusters, pair0, group0;
+    } parts[2];
+    int nparts = 0;
+    uint32_t pairs_used = 0, groups_used = 0;
+    auto plan = [&](int ctas, uint32_t max_cl) {
+        const uint32_t ppc = static_cast<uint32_t>(ctas / 2);
+        const uint32_t G = args.n_blocks / ppc;
+        const uint64_t items = static_cast<uint64_t>(args.units) * G;
+        uint32_t cl = static_cast<uint32_t>(std::min<uint64_t>(max_cl, items));
+        if (L.max_clusters > 0) cl = std::min<uint32_t>(cl, L.max_clusters);
+        if (cl == 0) return;
+        parts[nparts++] = {ctas, cl, pairs_used, groups_used};
+        pairs_used += cl * ppc;
+        groups_used += cl / G + cl % G;
+    };
+    if (want4) {
+        plan(4, occ4);
+        const uint32_t spare_pairs = occ2 > 2 * occ4 ? occ2 - 2 * occ4 : 0;
+        if (L.max_clusters == 0 && spare_pairs > 0) plan(2, spare_pairs);
+    } else {
+        plan(2, occ2);
+    }
+    const size_t scratch = (kProgressWords + 32) * 4 + static_cast<size_t>(groups_used) * kMail * 8;
+    if (scratch > kScheduleScratchBytes || pairs_used > kProgressWords) return cudaErrorInvalidValue;
+    cudaError_t e = cudaMemsetAsync(L.progress, 0, scratch, stream);
+    if (e != cudaSuccess) return e;
+
+    CUtensorMap mb;
+    if (!make_plane_map(&mb, L.b_planes, L.K, b_rows, L.ldk, kRowsPerCta)) return cudaErrorInvalidValue;
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    if (nparts > 1) {
+        e = side_stream(dev, &side, &fork, &join);
+        if (e != cudaSuccess) return e;
+        e = cudaEventRecord(fork, stream);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(side, fork, 0);
         if (e != cudaSuccess) return e;
     }
-
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(2 * clusters);
-    cfg.blockDim = dim3(kNumThreads);
-    cfg.dynamicSmemBytes = kSmemBytes;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, ppmm_i8_sm100_kernel, ma, mb, args);
+    for (int i = 0; i < nparts; ++i) {
+        const Part& pt = parts[i];
+        GemmArgs a = args;
+        const uint32_t ppc = static_cast<uint32_t>(pt.ctas / 2);
+        a.G = args.n_blocks / ppc;
+        a.F = pt.clusters / a.G;
+        a.L = pt.clusters % a.G;
+        a.active_clusters = pt.clusters;
+        a.progress = L.progress + pt.pair0;  // indexed by cluster id (< pairs of this launch)
+        a.mailbox = reinterpret_cast<unsigned long long*>(L.progress + kProgressWords + 32) +
+                    static_cast<size_t>(pt.group0) * kMail;
+        a.stats = L.stats ? reinterpret_cast<unsigned long long*>(L.stats) + pt.pair0 * kStatSlots
+                          : nullptr;
+        CUtensorMap ma;
+        if (!make_plane_map(&ma, L.a_planes, L.K, a_rows, L.ldk,
+                            pt.ctas == 4 ? kRowsPerCta / 2 : kRowsPerCta))
+            return cudaErrorInvalidValue;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(pt.ctas) * pt.clusters);
+        cfg.blockDim = dim3(kNumThreads);
+        cfg.dynamicSmemBytes = kSmemBytes;
+        cfg.stream = i == 0 ? stream : side;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = static_cast<unsigned>(pt.ctas);
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = pt.ctas == 4 ? cudaLaunchKernelEx(&cfg, ppmm_i8_sm100_kernel<4>, ma, mb, a)
+                         : cudaLaunchKernelEx(&cfg, ppmm_i8_sm100_kernel<2>, ma, mb, a);
+        if (e != cudaSuccess) return e;
+    }
+    if (nparts > 1) {
+        e = cudaEventRecord(join, side);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, join, 0);
+    }
+    return e;
 }
 
 }  // namespace irl

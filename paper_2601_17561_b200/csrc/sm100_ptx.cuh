@@ -117,6 +117,19 @@ __device__ __forceinline__ void tma_load_2d_pair_hint(uint32_t smem_dst, const v
         : "memory");
 }
 
+// Multicast variant: the tile lands at the same smem offset in every CTA of
+// `cta_mask`; completion bytes go to each destination pair leader's barrier
+// at offset `mbar` (pass the local barrier address with the peer bit cleared).
+__device__ __forceinline__ void tma_load_2d_pair_mcast(uint32_t smem_dst, const void* tmap,
+                                                       uint32_t mbar, int32_t c0, int32_t c1,
+                                                       uint16_t cta_mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_dst),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(mbar), "r"(c0), "r"(c1), "h"(cta_mask)
+        : "memory");
+}
+
 // ---- cross-CTA progress flags (global memory) ---------------------------------
 
 __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
