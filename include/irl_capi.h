@@ -162,6 +162,19 @@ int irl_ccmm_run_device(irl_ccmm* e, const uint16_t* q_res_dev, int q_ready, siz
  * and outputs [parts][nmod][n][M] (written by irl_ccmm_run, and by
  * irl_ccmm_run_device when out_dev is NULL; q_res_dev NULL reads *qres). */
 int irl_ccmm_buffers(irl_ccmm* e, void** qres, void** out);
+/* ---- CCMM caller drop-in (emulator.cpp:389-447, Emulator::ccmm_twin) -----
+ * Validates exactly like ccmm_twin (ShapeMismatch for non-positive dims,
+ * d1 % n_db, d2 % n_qry, slot output without ci; ModulusBudget for
+ * db_bits < 2 q_bits - delta and out_level outside [0, top_level]) and
+ * computes the exact product db (d1 x d2) . qry (d2 x d3) of integer-valued
+ * doubles on the PPMM engine (residues mod a prefix of the paper basis, centred
+ * CRT on device). msgs receives the d1*d3/n_db output ciphertext messages in
+ * ccmm_twin's order: msgs[(c*(d1/n_db) + b)*n_db + i] = prod[(b*n_db + i)*d3 + c].
+ * IRL_ERR_UNSUPPORTED if an entry is not an integer or |product| could reach 2^53. */
+int irl_ccmm_twin(irl_ctx* ctx, long d1, long d2, long d3, long n_db, long n_qry,
+                  double db_modulus_bits, double qry_modulus_bits, double scale_bits,
+                  int out_level, int top_level, int out_slot_encoding, int out_ci,
+                  const double* db, const double* qry, double* msgs);
 /* Bytes of HBM the engine holds (planes + workspace). */
 uint64_t irl_ccmm_device_bytes(const irl_ccmm* e);
 

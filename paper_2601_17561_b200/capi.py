@@ -66,6 +66,9 @@ SIGNATURES = {
     "irl_ccmm_run_device": (C.c_int, [vp, vp, C.c_int, sz, sz, sz, vp, vp]),
     "irl_ccmm_buffers": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp)]),
     "irl_ccmm_device_bytes": (C.c_uint64, [vp]),
+    "irl_ccmm_twin": (C.c_int, [vp, C.c_long, C.c_long, C.c_long, C.c_long, C.c_long, C.c_double, C.c_double,
+                                C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double),
+                                C.POINTER(C.c_double), C.POINTER(C.c_double)]),
 }
 
 _lib = None

@@ -128,3 +128,61 @@ def staging_tensors(engine: CcmmEngine, n: int):
     q = torch.as_tensor(_CudaArray(qp.value, (engine.nmod, engine.K, n), "<i2"), device=dev)
     o = torch.as_tensor(_CudaArray(op.value, (engine.parts, engine.nmod, n, engine.M), "<i2"), device=dev)
     return q, o
+
+
+# ---------------------------------------------------------------------------
+# Caller drop-in: Emulator::ccmm_twin (reference emulator.hpp:85-97, 135-140;
+# emulator.cpp:389-447) with the product computed by the PPMM engine.
+# ---------------------------------------------------------------------------
+
+from dataclasses import dataclass
+
+
+@dataclass
+class CcmmSpec:
+    d1: int = 0
+    d2: int = 0
+    d3: int = 0
+    n_db: int = 0
+    n_qry: int = 0
+    db_modulus_bits: float = 0.0
+    qry_modulus_bits: float = 0.0
+    scale_bits: float = 0.0
+    out_level: int = 0
+    out_encoding: str = "coeff"   # "coeff" | "slot"
+    out_ci: bool = False
+
+
+@dataclass
+class CcmmOutput:
+    """d1*d3/n_db ciphertexts in ccmm_twin's order (column-major over (c, b)):
+    messages[k] is the n_db-slot message of output ciphertext k."""
+    messages: np.ndarray           # [d3 * d1 / n_db][n_db] float64
+    level: int
+    encoding: str
+    ci: bool
+    log_ring_degree: int
+    scale_bits: float
+
+
+def ccmm_twin(spec: CcmmSpec, db, qry, top_level: int, ctx: Optional[Context] = None) -> CcmmOutput:
+    """Exact product db (d1 x d2) . qry (d2 x d3) packed as ccmm_twin packs it,
+    with its shape / modulus-budget checks and exception types."""
+    ctx = ctx or default_context()
+    db = np.ascontiguousarray(db, np.float64).ravel()
+    qry = np.ascontiguousarray(qry, np.float64).ravel()
+    if spec.d1 > 0 and spec.d2 > 0 and spec.d3 > 0 and spec.n_db > 0 and spec.n_qry > 0 and \
+            spec.d1 % spec.n_db == 0 and spec.d2 % spec.n_qry == 0 and \
+            (db.size != spec.d1 * spec.d2 or qry.size != spec.d2 * spec.d3):
+        from .modmat import ShapeMismatch
+        raise ShapeMismatch("ccmm: matrix buffer sizes do not match dimensions")
+    out = np.empty(max(spec.d1 * spec.d3, 1), np.float64)
+    dp = C.POINTER(C.c_double)
+    ctx.check(capi.lib().irl_ccmm_twin(
+        ctx.handle, spec.d1, spec.d2, spec.d3, spec.n_db, spec.n_qry, spec.db_modulus_bits,
+        spec.qry_modulus_bits, spec.scale_bits, spec.out_level, top_level,
+        int(spec.out_encoding == "slot"), int(spec.out_ci), db.ctypes.data_as(dp), qry.ctypes.data_as(dp),
+        out.ctypes.data_as(dp)))
+    return CcmmOutput(messages=out.reshape(-1, spec.n_db), level=spec.out_level, encoding=spec.out_encoding,
+                      ci=spec.out_ci, log_ring_degree=int(spec.n_db).bit_length() - 1,
+                      scale_bits=spec.scale_bits)

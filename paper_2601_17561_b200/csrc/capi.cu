@@ -84,8 +84,10 @@ struct irl_ccmm {
     uint16_t* out = nullptr;    // [parts][nmod][max_n][M]
     uint32_t kchunk = 0;        // K chunk keeping the fused int32 accumulators exact
     uint32_t* progress = nullptr;  // group-gating scratch of this engine's PPMM launches
-    cudaStream_t copy_stream = nullptr;
-    std::vector<cudaEvent_t> part_done;
+    cudaStream_t copy_stream = nullptr;  // device -> host
+    cudaStream_t h2d_stream = nullptr;   // host -> device
+    std::vector<cudaEvent_t> part_done;  // per modulus chunk: PPMMs done
+    std::vector<cudaEvent_t> h2d_done;   // per modulus chunk: query residues landed
     uint64_t bytes = 0;
 };
 
@@ -821,10 +823,14 @@ int irl_ccmm_create(irl_ctx* ctx, size_t parts, size_t m, size_t k, size_t max_n
     if (err == cudaSuccess) err = cudaMalloc(&e->out, out_b);
     if (err == cudaSuccess) err = cudaMalloc(&e->progress, kScheduleScratchBytes);
     if (err == cudaSuccess) err = cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking);
+    if (err == cudaSuccess) err = cudaStreamCreateWithFlags(&e->h2d_stream, cudaStreamNonBlocking);
     if (err == cudaSuccess) err = cudaMemsetAsync(e->db, 0, db_b, ctx->stream);
-    e->part_done.resize(parts);
-    for (size_t i = 0; err == cudaSuccess && i < parts; ++i)
+    e->part_done.resize(nmod);
+    e->h2d_done.resize(nmod);
+    for (size_t i = 0; err == cudaSuccess && i < nmod; ++i) {
         err = cudaEventCreateWithFlags(&e->part_done[i], cudaEventDisableTiming);
+        if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e->h2d_done[i], cudaEventDisableTiming);
+    }
     if (err != cudaSuccess) {
         irl_ccmm_destroy(e);
         return cuda_fail(ctx, err, "irl_ccmm_create");
@@ -839,9 +845,13 @@ int irl_ccmm_destroy(irl_ccmm* e) {
     cudaSetDevice(e->ctx->device);
     cudaStreamSynchronize(e->ctx->stream);
     if (e->copy_stream) cudaStreamSynchronize(e->copy_stream);
+    if (e->h2d_stream) cudaStreamSynchronize(e->h2d_stream);
     for (auto ev : e->part_done)
         if (ev) cudaEventDestroy(ev);
+    for (auto ev : e->h2d_done)
+        if (ev) cudaEventDestroy(ev);
     if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
+    if (e->h2d_stream) cudaStreamDestroy(e->h2d_stream);
     cudaFree(e->db);
     cudaFree(e->qplanes);
     cudaFree(e->qres);
@@ -920,18 +930,26 @@ int irl_ccmm_synth_db(irl_ccmm* e, uint64_t seed, uint32_t first_part) {
     return IRL_OK;
 }
 
+// PPMMs of parts [part0, part0 + nparts) for moduli [m0, m0 + nm); `out`
+// points at the [part0][0][0][0] corner of a [parts][nmod][n][M] tensor.
 static int ccmm_parts(irl_ccmm* e, size_t n, size_t part0, size_t nparts, uint16_t* out,
-                      cudaStream_t s) {
+                      cudaStream_t s, size_t m0 = 0, size_t nm = 0) {
     irl_ctx* ctx = e->ctx;
-    PpmmLaunch L = make_launch(e->mt);
-    L.a_planes = e->db + part0 * e->nmod * 2 * e->M * e->ldk;
-    L.b_planes = e->qplanes;
-    L.out = out;
+    if (nm == 0) nm = e->nmod;
+    ModTable sub{};
+    sub.n = uint32_t(nm);
+    for (size_t i = 0; i < nm; ++i) sub.mc[i] = e->mt.mc[m0 + i];
+    PpmmLaunch L = make_launch(sub);
+    L.a_planes = e->db + (part0 * e->nmod + m0) * 2 * e->M * e->ldk;
+    L.b_planes = e->qplanes + m0 * 2 * n * e->ldk;
+    L.out = out + m0 * n * e->M;
     L.M = uint32_t(e->M);
     L.N = uint32_t(n);
     L.K = uint32_t(e->K);
     L.ldk = uint32_t(e->ldk);
     L.parts = uint32_t(nparts);
+    L.a_part_rows = e->nmod * 2 * e->M;
+    L.out_part_elems = e->nmod * n * e->M;
     L.progress = e->progress;
     return run_ppmm(ctx, L, e->kchunk, s);
 }
@@ -960,21 +978,148 @@ int irl_ccmm_run(irl_ccmm* e, const uint16_t* q_res_host, size_t n, uint16_t* ou
     irl_ctx* ctx = e->ctx;
     Guard g(ctx);
     if (n == 0 || n > e->max_n) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: query width out of range");
+    // Pipelined by modulus chunks: H2D of chunk c+1 and D2H of chunk c-1 run
+    // on their own streams while chunk c is split and multiplied.
     cudaStream_t s = ctx->stream;
-    IRL_CK(ctx, cudaMemcpyAsync(e->qres, q_res_host, e->nmod * e->K * n * 2, cudaMemcpyHostToDevice, s));
-    IRL_LAUNCH(ctx, launch_split_cols<uint16_t>(e->qres, n, e->K * n, uint32_t(e->K), uint32_t(n), e->mt,
-                                                e->qplanes, e->ldk, nullptr, s));
-    const size_t part_elems = e->nmod * n * e->M;
-    for (size_t p = 0; p < e->parts; ++p) {
-        int st = ccmm_parts(e, n, p, 1, e->out + p * part_elems, s);
+    const size_t nmod = e->nmod, K = e->K, M = e->M;
+    const size_t chunk = (nmod + 7) / 8;
+    IRL_CK(ctx, cudaEventRecord(e->part_done[0], s));  // order after prior work on s
+    IRL_CK(ctx, cudaStreamWaitEvent(e->h2d_stream, e->part_done[0], 0));
+    for (size_t c0 = 0, ci = 0; c0 < nmod; c0 += chunk, ++ci) {
+        const size_t nc = std::min(chunk, nmod - c0);
+        IRL_CK(ctx, cudaMemcpyAsync(e->qres + c0 * K * n, q_res_host + c0 * K * n, nc * K * n * 2,
+                                    cudaMemcpyHostToDevice, e->h2d_stream));
+        IRL_CK(ctx, cudaEventRecord(e->h2d_done[ci], e->h2d_stream));
+    }
+    for (size_t c0 = 0, ci = 0; c0 < nmod; c0 += chunk, ++ci) {
+        const size_t nc = std::min(chunk, nmod - c0);
+        IRL_CK(ctx, cudaStreamWaitEvent(s, e->h2d_done[ci], 0));
+        ModTable sub{};
+        sub.n = uint32_t(nc);
+        for (size_t i = 0; i < nc; ++i) sub.mc[i] = e->mt.mc[c0 + i];
+        IRL_LAUNCH(ctx, launch_split_cols<uint16_t>(e->qres + c0 * K * n, n, K * n, uint32_t(K), uint32_t(n), sub,
+                                                    e->qplanes + c0 * 2 * n * e->ldk, e->ldk, nullptr, s));
+        int st = ccmm_parts(e, n, 0, e->parts, e->out, s, c0, nc);
         if (st) return st;
-        IRL_CK(ctx, cudaEventRecord(e->part_done[p], s));
-        IRL_CK(ctx, cudaStreamWaitEvent(e->copy_stream, e->part_done[p], 0));
-        IRL_CK(ctx, cudaMemcpyAsync(out_host + p * part_elems, e->out + p * part_elems, part_elems * 2,
-                                    cudaMemcpyDeviceToHost, e->copy_stream));
+        IRL_CK(ctx, cudaEventRecord(e->part_done[ci], s));
+        IRL_CK(ctx, cudaStreamWaitEvent(e->copy_stream, e->part_done[ci], 0));
+        for (size_t p = 0; p < e->parts; ++p) {
+            const size_t off = (p * nmod + c0) * n * M;
+            IRL_CK(ctx, cudaMemcpyAsync(out_host + off, e->out + off, nc * n * M * 2, cudaMemcpyDeviceToHost,
+                                        e->copy_stream));
+        }
     }
     IRL_CK(ctx, cudaStreamSynchronize(e->copy_stream));
     IRL_CK(ctx, cudaStreamSynchronize(s));
+    return IRL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// CCMM caller drop-in: the exact product behind Emulator::ccmm_twin
+// ---------------------------------------------------------------------------
+
+int irl_ccmm_twin(irl_ctx* ctx, long d1, long d2, long d3, long n_db, long n_qry,
+                  double db_modulus_bits, double qry_modulus_bits, double scale_bits,
+                  int out_level, int top_level, int out_slot_encoding, int out_ci,
+                  const double* db, const double* qry, double* msgs) {
+    if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
+    Guard g(ctx);
+    // emulator.cpp:392-410, same order and messages
+    if (d1 <= 0 || d2 <= 0 || d3 <= 0) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: nonpositive dimensions");
+    if (n_db <= 0 || n_qry <= 0 || d1 % n_db != 0 || d2 % n_qry != 0)
+        return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: d1 must be a multiple of n_db, d2 of n_qry");
+    if (db_modulus_bits < 2.0 * qry_modulus_bits - scale_bits)
+        return set_err(ctx, IRL_ERR_MODULUS_BUDGET, "ccmm: database modulus below 2q - delta");
+    if (out_level < 0 || out_level > top_level)
+        return set_err(ctx, IRL_ERR_MODULUS_BUDGET, "ccmm: output level outside the modulus chain");
+    if (out_slot_encoding && !out_ci)
+        return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: slot-encoded output must be conjugate-invariant");
+    if (d1 >= (1l << 30) || d2 >= (1l << 30) || d3 >= (1l << 30))
+        return set_err(ctx, IRL_ERR_UNSUPPORTED, "ccmm: dimension above 2^30");
+    const size_t M = size_t(d1), K = size_t(d2), N = size_t(d3);
+    // Device buffers: inputs, residues, planes, output residues, doubles.
+    // Paper-basis prefix with Q > 2 * bound, Q < 2^64 (<= 4 moduli).
+    uint32_t P[64], E[64];
+    irl_paper_basis(P, E, 64);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off = (off + bytes + 127) / 128 * 128;
+        return o;
+    };
+    const size_t ldk = round16(K);
+    const size_t o_db = take(M * K * 8), o_q = take(K * N * 8), o_ra = take(4 * M * K * 2),
+                 o_rb = take(4 * K * N * 2), o_pa = take(4 * 2 * M * ldk), o_pb = take(4 * 2 * N * ldk),
+                 o_res = take(4 * N * M * 2), o_out = take(N * M * 8), o_bad = take(16);
+    IRL_CK(ctx, ctx->ws[0].ensure(off));
+    uint8_t* base = ctx->ws[0].as<uint8_t>();
+    double* ddb = reinterpret_cast<double*>(base + o_db);
+    double* dq = reinterpret_cast<double*>(base + o_q);
+    int* dbad = reinterpret_cast<int*>(base + o_bad);
+    IRL_CK(ctx, cudaMemcpyAsync(ddb, db, M * K * 8, cudaMemcpyHostToDevice, ctx->stream));
+    IRL_CK(ctx, cudaMemcpyAsync(dq, qry, K * N * 8, cudaMemcpyHostToDevice, ctx->stream));
+    IRL_CK(ctx, cudaMemsetAsync(dbad, 0, 4, ctx->stream));
+    // Modulus count: |product| <= K max|db| max|qry| must stay inside the
+    // centred range of Q (validation of the host inputs' magnitudes only;
+    // integrality is checked on device by the residue kernel).
+    ModTable mt{};
+    double amax = 0, bmax = 0;
+    for (size_t i = 0; i < M * K; ++i) amax = std::max(amax, std::fabs(db[i]));
+    for (size_t i = 0; i < K * N; ++i) bmax = std::max(bmax, std::fabs(qry[i]));
+    const double bound = double(K) * amax * bmax;
+    if (bound >= 4503599627370496.0)  // 2^52: keep the centred result exact in double
+        return set_err(ctx, IRL_ERR_UNSUPPORTED, "ccmm: |product| may exceed 2^52");
+    uint32_t nm = 1;
+    double q = double(P[0]) * P[0];
+    while (q <= 2.0 * bound + 1.0 && nm < 4) {
+        q *= double(P[nm]) * P[nm];
+        ++nm;
+    }
+    mt.n = nm;
+    for (uint32_t i = 0; i < nm; ++i) mt.mc[i] = make_modconst(P[i], 2);
+    uint16_t* ra = reinterpret_cast<uint16_t*>(base + o_ra);
+    uint16_t* rb = reinterpret_cast<uint16_t*>(base + o_rb);
+    IRL_LAUNCH(ctx, launch_double_to_residues(ddb, uint32_t(M), uint32_t(K), mt, ra, dbad, ctx->stream));
+    IRL_LAUNCH(ctx, launch_double_to_residues(dq, uint32_t(K), uint32_t(N), mt, rb, dbad, ctx->stream));
+    int bad = 0;
+    IRL_CK(ctx, cudaMemcpyAsync(&bad, dbad, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    if (bad) return set_err(ctx, IRL_ERR_UNSUPPORTED, "ccmm: messages must be integers below 2^53");
+    int8_t* pa = reinterpret_cast<int8_t*>(base + o_pa);
+    int8_t* pb = reinterpret_cast<int8_t*>(base + o_pb);
+    IRL_LAUNCH(ctx, launch_split_rows<uint16_t>(ra, K, M * K, uint32_t(M), uint32_t(K), mt, pa, ldk, nullptr, ctx->stream));
+    IRL_LAUNCH(ctx, launch_split_cols<uint16_t>(rb, N, K * N, uint32_t(K), uint32_t(N), mt, pb, ldk, nullptr, ctx->stream));
+    uint16_t* res = reinterpret_cast<uint16_t*>(base + o_res);
+    PpmmLaunch L = make_launch(mt);
+    L.a_planes = pa;
+    L.b_planes = pb;
+    L.out = res;
+    L.M = uint32_t(M);
+    L.N = uint32_t(N);
+    L.K = uint32_t(K);
+    L.ldk = uint32_t(ldk);
+    L.parts = 1;
+    int64_t h = 0;
+    for (uint32_t i = 0; i < nm; ++i) h = std::max<int64_t>(h, (P[i] - 1) / 2);
+    int st = run_ppmm(ctx, L, safe_kchunk(h, h, h, h, uint32_t(K)), ctx->stream);
+    if (st) return st;
+    Crt64Table t{};
+    t.nmod = nm;
+    unsigned long long Qv = 1;
+    for (uint32_t i = 0; i < nm; ++i) Qv *= uint64_t(P[i]) * P[i];
+    t.Q = Qv;
+    for (uint32_t i = 0; i < nm; ++i) {
+        const uint32_t m = P[i] * P[i];
+        t.mc[i] = make_modconst(P[i], 2);
+        t.qi[i] = Qv / m;
+        if (!inv_mod(uint32_t(t.qi[i] % m), m, &t.inv[i]))
+            return set_err(ctx, IRL_ERR_NOT_COPRIME, "CRT basis is not coprime");
+    }
+    double* dout = reinterpret_cast<double*>(base + o_out);
+    IRL_LAUNCH(ctx, launch_crt_centred_double(res, uint32_t(M), uint32_t(N), t, dout, ctx->stream));
+    // [N][M] column-major product == ccmm_twin's ciphertext message order
+    IRL_CK(ctx, cudaMemcpyAsync(msgs, dout, N * M * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
     return IRL_OK;
 }
 

@@ -429,6 +429,43 @@ __global__ void absmax_kernel(const int32_t* __restrict__ x, size_t count, int32
     warp_max_atomic(m, dst);
 }
 
+__global__ void double_to_residues_kernel(const double* __restrict__ x, size_t count,
+                                          const __grid_constant__ ModTable mt,
+                                          uint16_t* __restrict__ out, int* bad) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const double v = x[i];
+    const bool ok = v == floor(v) && fabs(v) < 9007199254740992.0;  // 2^53
+    if (!ok) {
+        *bad = 1;
+        return;
+    }
+    const long long iv = static_cast<long long>(v);
+    for (uint32_t j = 0; j < mt.n; ++j) {
+        long long r = iv % static_cast<long long>(mt.mc[j].m);
+        if (r < 0) r += mt.mc[j].m;
+        out[static_cast<size_t>(j) * count + i] = static_cast<uint16_t>(r);
+    }
+}
+
+__global__ void crt_centred_double_kernel(const uint16_t* __restrict__ res, uint32_t M, uint32_t N,
+                                          const __grid_constant__ Crt64Table t,
+                                          double* __restrict__ out) {
+    const size_t gid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (gid >= static_cast<size_t>(M) * N) return;
+    unsigned __int128 acc = 0;
+    for (uint32_t i = 0; i < t.nmod; ++i) {
+        const ModConst& c = t.mc[i];
+        uint32_t r = res[static_cast<size_t>(i) * M * N + gid];
+        r = r < c.m ? r : mod_u32(r, c.m, c.magic_m);
+        const uint32_t tt = mod_u32(r * t.inv[i], c.m, c.magic_m);
+        acc += static_cast<unsigned __int128>(t.qi[i]) * tt;
+    }
+    const unsigned long long x = static_cast<unsigned long long>(acc % t.Q);
+    const double v = x > t.Q / 2 ? -static_cast<double>(t.Q - x) : static_cast<double>(x);
+    out[gid] = v;  // out[n][m] shares the [N][M] indexing of res
+}
+
 inline unsigned blocks_for(size_t n, unsigned t) { return static_cast<unsigned>((n + t - 1) / t); }
 
 }  // namespace
@@ -555,6 +592,22 @@ cudaError_t launch_absmax_i32(const int32_t* x, size_t count, int32_t* dst, cuda
     unsigned b = blocks_for(count, 256);
     if (b > 4096) b = 4096;
     absmax_kernel<<<b, 256, 0, s>>>(x, count, dst);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_double_to_residues(const double* x, uint32_t rows, uint32_t cols,
+                                      const ModTable& mt, uint16_t* out, int* bad, cudaStream_t s) {
+    const size_t count = static_cast<size_t>(rows) * cols;
+    if (count == 0) return cudaSuccess;
+    double_to_residues_kernel<<<blocks_for(count, 256), 256, 0, s>>>(x, count, mt, out, bad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_crt_centred_double(const uint16_t* res, uint32_t M, uint32_t N,
+                                      const Crt64Table& t, double* out, cudaStream_t s) {
+    const size_t count = static_cast<size_t>(M) * N;
+    if (count == 0) return cudaSuccess;
+    crt_centred_double_kernel<<<blocks_for(count, 256), 256, 0, s>>>(res, M, N, t, out);
     return cudaGetLastError();
 }
 

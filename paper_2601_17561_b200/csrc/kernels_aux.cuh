@@ -89,6 +89,22 @@ cudaError_t launch_digit_decompose(const int32_t* in, size_t count, const ModCon
 cudaError_t launch_digit_recompose(const int32_t* d0, const int32_t* d1, size_t count,
                                    const ModConst& mc, int32_t* out, cudaStream_t s);
 
+// Integer-valued doubles -> residues: out[i][r][c] = x[r][c] mod m_i (uint16);
+// sets *bad = 1 if any entry is not an integer of magnitude < 2^53.
+cudaError_t launch_double_to_residues(const double* x, uint32_t rows, uint32_t cols,
+                                      const ModTable& mt, uint16_t* out, int* bad, cudaStream_t s);
+// Centred CRT for bases with Q < 2^64: res[i][N][M] -> out[n][m] (double),
+// value in (-Q/2, Q/2].
+struct Crt64Table {
+    uint32_t nmod;
+    unsigned long long Q;
+    unsigned long long qi[kMaxModuli];   // Q / m_i
+    uint32_t inv[kMaxModuli];            // (Q/m_i)^-1 mod m_i
+    ModConst mc[kMaxModuli];
+};
+cudaError_t launch_crt_centred_double(const uint16_t* res, uint32_t M, uint32_t N,
+                                      const Crt64Table& t, double* out, cudaStream_t s);
+
 // Host mirror of the device generator.
 uint32_t synth_residue_host(uint64_t seed, uint32_t stream, uint32_t plane, uint32_t row,
                             uint32_t col, uint32_t m);

@@ -37,6 +37,10 @@ struct PpmmLaunch {
     uint64_t* stats = nullptr;     // optional [pairs][kStatSlots] diagnostics
     int dynamic_schedule = 1;      // units from an atomic counter (0: static super-rounds)
     int gate_lead = -1;            // K blocks a pair may lead its group; -1 default, 0 off
+    // Part strides for launches over a modulus subset of every part
+    // (0 = dense: nprimes * 2 * M rows, nprimes * N * M outputs).
+    uint64_t a_part_rows = 0;
+    uint64_t out_part_elems = 0;
     int cluster_ctas = 4;          // 4: two pairs per cluster multicasting A (+2-CTA filler); 2: one pair
     ModConst mc[kMaxPrimesPerLaunch];
 };

@@ -69,6 +69,8 @@ struct __align__(64) GemmArgs {
     uint32_t dynamic;                 // 1: units from an atomic counter; 0: static super-rounds
     uint32_t gate_lead;               // max K blocks a pair may lead its group (0: no gating)
     uint32_t accumulate;
+    uint32_t a_part_rows;             // plane rows between consecutive parts of A
+    unsigned long long out_part;      // output elements between consecutive parts
     uint16_t* out;
     uint32_t* progress;               // [clusters] K blocks issued by each pair's leader producer
     uint32_t* counter;                // next unit to hand out (dynamic schedule)
@@ -285,7 +287,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                     const uint32_t nb = (grp.solo ? r : grp.member) * kPairs + pair;
                     push_tile(u, nb);
                     const TileCoord tc = decode(args, u, nb);
-                    const uint32_t a_row0 = ((tc.part * args.nprimes + tc.prime) * 2) * args.M +
+                    const uint32_t a_row0 = tc.part * args.a_part_rows + tc.prime * 2 * args.M +
                                             tc.m0 + half_rank * kRowsPerCta;
                     const uint32_t half_n = tc.n_size / 2;
                     const uint32_t b_row0 = (tc.prime * 2) * args.N + tc.n0 + half_rank * half_n;
@@ -447,9 +449,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             const uint32_t row = half_rank * kRowsPerCta + quarter * 32 + lane;
             const uint32_t m = tc.m0 + row;
             const bool row_ok = m < args.M;
-            uint16_t* out = args.out +
-                            (static_cast<size_t>(tc.part) * args.nprimes + tc.prime) *
-                                static_cast<size_t>(args.N) * args.M +
+            uint16_t* out = args.out + tc.part * args.out_part +
+                            static_cast<size_t>(tc.prime) * args.N * args.M +
                             m;
             const uint32_t lane_base = tmem_base + ((quarter * 32u) << 16);
             const uint32_t cols = tc.n_size / 2;  // multiple of 16
@@ -592,7 +593,8 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     if (L.nprimes == 0 || L.parts == 0 || L.M == 0 || L.N == 0) return cudaSuccess;
     if (L.nprimes > kMaxPrimesPerLaunch) return cudaErrorInvalidValue;
     if (L.ldk % 16 != 0 || L.ldk < L.K) return cudaErrorInvalidValue;
-    const uint64_t a_rows = static_cast<uint64_t>(L.parts) * L.nprimes * 2 * L.M;
+    const uint64_t a_part_rows = L.a_part_rows ? L.a_part_rows : static_cast<uint64_t>(L.nprimes) * 2 * L.M;
+    const uint64_t a_rows = (L.parts - 1) * a_part_rows + static_cast<uint64_t>(L.nprimes) * 2 * L.M;
     const uint64_t b_rows = static_cast<uint64_t>(L.nprimes) * 2 * L.N;
     if (a_rows >= (1ull << 31) || b_rows >= (1ull << 31)) return cudaErrorInvalidValue;
 
@@ -607,6 +609,9 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     args.n_blocks = (L.N + kMaxTileN - 1) / kMaxTileN;
     args.units = args.m_blocks * L.parts * L.nprimes;
     args.accumulate = L.accumulate ? 1u : 0u;
+    args.a_part_rows = static_cast<uint32_t>(a_part_rows);
+    args.out_part = L.out_part_elems ? L.out_part_elems
+                                     : static_cast<unsigned long long>(L.nprimes) * L.N * L.M;
     args.out = L.out;
     for (uint32_t i = 0; i < L.nprimes; ++i) args.mc[i] = L.mc[i];
 

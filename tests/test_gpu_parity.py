@@ -237,3 +237,50 @@ def test_launch_counter_and_native_path(mm):
     before = ctx.launches
     mm.gemm_mod_psq(np.eye(4, dtype=np.int32), np.eye(4, dtype=np.int32), 127)
     assert ctx.launches > before
+
+
+# ------------------------------------------------ caller drop-in (f1) ------
+
+def _spec(**kw):
+    from paper_2601_17561_b200.ccmm import CcmmSpec
+    s = CcmmSpec(d1=4, d2=3, d3=2, n_db=2, n_qry=3, qry_modulus_bits=36.0, scale_bits=23.0,
+                 db_modulus_bits=2 * 36.0 - 23.0)
+    for k, v in kw.items():
+        setattr(s, k, v)
+    return s
+
+
+def test_ccmm_twin_kat_and_errors(mm):
+    # test_emulator.cpp:215-270 through the GPU product
+    from paper_2601_17561_b200.ccmm import ccmm_twin
+    g = GOLD["ccmm_twin"]
+    out = ccmm_twin(_spec(), g["db"], g["qry"], top_level=9)
+    assert out.messages.shape == (g["outputs"], 2)
+    assert out.messages[0].tolist() == [11.0, 3.0] and out.messages[1].tolist() == [3.0, 5.0]
+    assert out.messages[2].tolist() == [14.0, 4.0] and out.messages[3][1] == 6.0
+    assert out.encoding == "coeff" and out.level == 0
+    with pytest.raises(mm.ModulusBudget):
+        ccmm_twin(_spec(db_modulus_bits=36.0), g["db"], g["qry"], top_level=9)
+    with pytest.raises(mm.ModulusBudget):
+        ccmm_twin(_spec(out_level=99), g["db"], g["qry"], top_level=9)
+    with pytest.raises(mm.ShapeMismatch):
+        ccmm_twin(_spec(out_encoding="slot"), g["db"], g["qry"], top_level=9)
+    with pytest.raises(mm.ShapeMismatch):
+        ccmm_twin(_spec(d1=5), g["db"], g["qry"], top_level=9)
+    raised = ccmm_twin(_spec(out_level=5, out_encoding="slot", out_ci=True), g["db"], g["qry"], top_level=9)
+    assert raised.level == 5 and raised.encoding == "slot" and raised.ci and raised.messages[0][0] == 11.0
+
+
+def test_ccmm_twin_pipeline_sizes_exact():
+    # acceptance criteria 6/7 geometry (acceptance.cpp:197-217): n_db=4096,
+    # d=1024, batch 4 x rho 31, ternary iris values -> exact product
+    from paper_2601_17561_b200.ccmm import ccmm_twin
+    rng = np.random.default_rng(11)
+    d1, d2, d3 = 4096, 1024, 124
+    db = rng.integers(-1, 2, (d1, d2)).astype(np.float64)
+    qry = rng.integers(-1, 2, (d2, d3)).astype(np.float64)
+    spec = _spec(d1=d1, d2=d2, d3=d3, n_db=d2, n_qry=d2)
+    out = ccmm_twin(spec, db, qry, top_level=9)
+    prod = (db.astype(np.int64) @ qry.astype(np.int64))
+    want = prod.T.reshape(d3, d1 // d2, d2).reshape(-1, d2)  # ct(c, b).message[i] = prod[(b n_db + i), c]
+    assert (out.messages == want).all()
