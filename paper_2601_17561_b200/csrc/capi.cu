@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -188,7 +189,16 @@ int run_ppmm(irl_ctx* ctx, PpmmLaunch L, uint32_t kchunk, cudaStream_t s) {
     if (!L.progress) L.progress = ctx->d_progress;
     if (const char* sch = std::getenv("IRL_PPMM_SCHEDULE")) L.dynamic_schedule = std::strcmp(sch, "static") != 0;
     if (const char* gl = std::getenv("IRL_PPMM_GATE")) L.gate_lead = std::atoi(gl);
-    if (const char* cl = std::getenv("IRL_PPMM_CLUSTER")) L.cluster_ctas = std::atoi(cl);
+    if (const char* cl = std::getenv("IRL_PPMM_CLUSTER")) {
+        // "PMxPN" (pairs along M x pairs along N) or a CTA count 2/4/8 (1 x count/2)
+        int pm = 1, pn = 1;
+        if (std::sscanf(cl, "%dx%d", &pm, &pn) != 2) {
+            pm = 1;
+            pn = std::max(1, std::atoi(cl) / 2);
+        }
+        L.cluster_pm = pm;
+        L.cluster_pn = pn;
+    }
     if (ctx->diag && ctx->d_diag) {
         L.stats = ctx->d_diag;
         IRL_CK(ctx, cudaMemsetAsync(ctx->d_diag, 0, 1024 * kStatSlots * sizeof(uint64_t), s));

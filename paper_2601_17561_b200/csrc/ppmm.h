@@ -41,7 +41,12 @@ struct PpmmLaunch {
     // (0 = dense: nprimes * 2 * M rows, nprimes * N * M outputs).
     uint64_t a_part_rows = 0;
     uint64_t out_part_elems = 0;
-    int cluster_ctas = 4;          // 4: two pairs per cluster multicasting A (+2-CTA filler); 2: one pair
+    // Cluster shape in CTA pairs: cluster_pm pairs along M (sharing each query
+    // tile by TMA multicast) x cluster_pn pairs along N (sharing each database
+    // tile). 1x1 is a plain CTA pair; SMs a multi-pair shape strands are taken
+    // by a 1x1 filler launch pulling from the same unit counter.
+    int cluster_pm = 1;
+    int cluster_pn = 4;
     ModConst mc[kMaxPrimesPerLaunch];
 };
 

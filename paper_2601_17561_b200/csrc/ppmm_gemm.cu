@@ -64,6 +64,8 @@ struct __align__(64) GemmArgs {
     uint32_t M, N, K;
     uint32_t parts, nprimes;
     uint32_t m_blocks, n_blocks, units;
+    uint32_t unit_mblocks;            // 256-row blocks per unit (the main launch's cluster_pm)
+    uint32_t m_units;                 // units per (prime, part) = ceil(m_blocks / unit_mblocks)
     // group schedule (see group_of): G = clusters per full group
     uint32_t G, F, L, active_clusters;
     uint32_t dynamic;                 // 1: units from an atomic counter; 0: static super-rounds
@@ -105,15 +107,17 @@ struct TileCoord {
     uint32_t prime, part, m0, n0, n_size;
 };
 
-// A unit is one 256-row block of one (prime, part); units are prime-major so
-// a prime's query planes stay L2-resident while its units are in flight.
-__device__ __forceinline__ TileCoord decode(const GemmArgs& a, uint32_t unit, uint32_t nb) {
+// A unit is `unit_mblocks` consecutive 256-row blocks of one (prime, part);
+// units are prime-major so a prime's query planes stay L2-resident while its
+// units are in flight. A tile is (unit, m-block within the unit, n-tile).
+__device__ __forceinline__ TileCoord decode(const GemmArgs& a, uint32_t unit, uint32_t mb_sub,
+                                            uint32_t nb) {
     TileCoord t;
-    const uint32_t mb = unit % a.m_blocks;
-    const uint32_t pp = unit / a.m_blocks;
+    const uint32_t mu = unit % a.m_units;
+    const uint32_t pp = unit / a.m_units;
     t.part = pp % a.parts;
     t.prime = pp / a.parts;
-    t.m0 = mb * 2 * kRowsPerCta;
+    t.m0 = (mu * a.unit_mblocks + mb_sub) * 2 * kRowsPerCta;
     t.n0 = nb * kMaxTileN;
     const uint32_t rem = a.N - t.n0;
     const uint32_t ns = rem < kMaxTileN ? rem : kMaxTileN;
@@ -156,15 +160,20 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
     return v;
 }
 
-// kCtas = CTAs per cluster: 2 (one pair) or 4 (two pairs sharing each A tile
-// through TMA multicast: each CTA loads half of its 128-row A block and
-// multicasts it to the CTA with the same role in the other pair).
-template <int kCtas>
+// Cluster = kPM x kPN CTA pairs; pair index = pm * kPN + pn, CTA rank =
+// 2 * pair + half. The kPN pairs with the same pm compute the same m-block
+// (different n-tiles): each of their CTAs loads 1/kPN of its 128-row A block
+// and multicasts it to the same-role CTAs of those pairs. Likewise the kPM
+// pairs with the same pn share each B (query) tile. Every stage is released
+// only when all pairs of the cluster have consumed it (commit multicast), so
+// the cluster runs in lock-step over K.
+template <int kPM, int kPN>
 __global__ void __launch_bounds__(kNumThreads, 1)
     ppmm_i8_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a,
                          const __grid_constant__ CUtensorMap tmap_b,
                          const __grid_constant__ GemmArgs args) {
-    constexpr uint32_t kPairs = kCtas / 2;
+    constexpr uint32_t kPairs = kPM * kPN;
+    constexpr int kCtas = 2 * kPairs;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -181,6 +190,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     const uint32_t lane = threadIdx.x % 32;
     const uint32_t rank = ptx::cluster_ctarank();
     const uint32_t pair = rank >> 1;          // pair within the cluster
+    const uint32_t pm = pair / kPN, pn = pair % kPN;
     const uint32_t half_rank = rank & 1;      // CTA within the pair
     const bool leader = half_rank == 0;       // pair leader (issues the MMAs)
     const uint32_t cluster_id = blockIdx.x / kCtas;
@@ -217,7 +227,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             const uint32_t lead = args.gate_lead;
             const bool writer = rank == 0 && grp.member == 0;  // takes units for the group
             unsigned long long* mbox = args.mailbox + static_cast<size_t>(grp.id) * kMail;
-            const uint32_t tiles_per_unit = grp.solo ? args.n_blocks / kPairs : 1;
+            const uint32_t tiles_per_unit = grp.solo ? args.n_blocks / kPN : 1;
+            const uint32_t m_passes = args.unit_mblocks / kPM;
             uint32_t issued = 0;  // cumulative K blocks (comparable across the group)
             uint32_t seen = 0;    // last observed minimum of the peers' counters
             uint32_t stage = 0, phase = 0, tile_i = 0;
@@ -246,11 +257,11 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                 st_relaxed_u64(mbox + seq % kMail,
                                (static_cast<unsigned long long>(seq + 1) << 32) | u);
             };
-            auto push_tile = [&](uint32_t u, uint32_t nb) {
+            auto push_tile = [&](uint32_t u, uint32_t mb_sub, uint32_t nb) {
                 const uint32_t slot = tile_i % kRing;
                 ptx::mbar_wait(&ring_empty[slot], ((tile_i / kRing) & 1) ^ 1);
                 ring_tile[2 * slot] = u;
-                ring_tile[2 * slot + 1] = nb;
+                ring_tile[2 * slot + 1] = nb | (mb_sub << 16);
                 asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(
                                  ptx::smem_u32(&ring_full[slot]))
                              : "memory");
@@ -280,13 +291,15 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                     u = static_cast<uint32_t>(v);
                 }
                 if (u == kEnd) {
-                    push_tile(kEnd, 0);
+                    push_tile(kEnd, 0, 0);
                     break;
                 }
-                for (uint32_t r = 0; r < tiles_per_unit; ++r) {
-                    const uint32_t nb = (grp.solo ? r : grp.member) * kPairs + pair;
-                    push_tile(u, nb);
-                    const TileCoord tc = decode(args, u, nb);
+                for (uint32_t t = 0; t < m_passes * tiles_per_unit; ++t) {
+                    const uint32_t r = t % tiles_per_unit;
+                    const uint32_t mb_sub = (t / tiles_per_unit) * kPM + pm;
+                    const uint32_t nb = (grp.solo ? r : grp.member) * kPN + pn;
+                    push_tile(u, mb_sub, nb);
+                    const TileCoord tc = decode(args, u, mb_sub, nb);
                     const uint32_t a_row0 = tc.part * args.a_part_rows + tc.prime * 2 * args.M +
                                             tc.m0 + half_rank * kRowsPerCta;
                     const uint32_t half_n = tc.n_size / 2;
@@ -318,31 +331,51 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                         if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * kStageBytes);
                         uint8_t* st = smem + stage * kStageBytes;
                         const int32_t k0 = static_cast<int32_t>(kb * kBlockK);
-                        if constexpr (kCtas == 2) {
+                        if constexpr (kPN == 1) {
                             ptx::tma_load_2d_pair(ptx::smem_u32(st), &tmap_a, leader_full, k0,
                                                   static_cast<int32_t>(a_row0));
                             ptx::tma_load_2d_pair(ptx::smem_u32(st + kPlaneTileBytes), &tmap_a,
                                                   leader_full, k0,
                                                   static_cast<int32_t>(a_row0 + args.M));
                         } else {
-                            // this CTA loads rows [64 pair, +64) of both A planes for
-                            // itself and the same-role CTA of the other pair
-                            const uint16_t mask = static_cast<uint16_t>((1u << rank) | (1u << (rank ^ 2)));
-                            const uint32_t sub = pair * (kPlaneTileBytes / 2);
+                            // rows [pn * kSubA, +kSubA) of this CTA's A block, for
+                            // itself and the same-role CTAs of the pairs sharing pm
+                            constexpr uint32_t kSubA = kRowsPerCta / kPN;
+                            uint16_t mask = 0;
+#pragma unroll
+                            for (uint32_t j = 0; j < kPN; ++j) mask |= 1u << (2 * (pm * kPN + j) + half_rank);
+                            const uint32_t sub = pn * kSubA * kBlockK;
                             ptx::tma_load_2d_pair_mcast(ptx::smem_u32(st) + sub, &tmap_a, leader_full, k0,
-                                                        static_cast<int32_t>(a_row0 + pair * 64), mask);
+                                                        static_cast<int32_t>(a_row0 + pn * kSubA), mask);
                             ptx::tma_load_2d_pair_mcast(ptx::smem_u32(st + kPlaneTileBytes) + sub, &tmap_a,
                                                         leader_full, k0,
-                                                        static_cast<int32_t>(a_row0 + args.M + pair * 64),
+                                                        static_cast<int32_t>(a_row0 + args.M + pn * kSubA),
                                                         mask);
                         }
-                        ptx::tma_load_2d_pair_hint(ptx::smem_u32(st + 2 * kPlaneTileBytes),
-                                                   &tmap_b, leader_full, k0,
-                                                   static_cast<int32_t>(b_row0), ptx::kL2EvictLast);
-                        ptx::tma_load_2d_pair_hint(ptx::smem_u32(st + 3 * kPlaneTileBytes),
-                                                   &tmap_b, leader_full, k0,
-                                                   static_cast<int32_t>(b_row0 + args.N),
-                                                   ptx::kL2EvictLast);
+                        if constexpr (kPM == 1) {
+                            ptx::tma_load_2d_pair_hint(ptx::smem_u32(st + 2 * kPlaneTileBytes),
+                                                       &tmap_b, leader_full, k0,
+                                                       static_cast<int32_t>(b_row0), ptx::kL2EvictLast);
+                            ptx::tma_load_2d_pair_hint(ptx::smem_u32(st + 3 * kPlaneTileBytes),
+                                                       &tmap_b, leader_full, k0,
+                                                       static_cast<int32_t>(b_row0 + args.N),
+                                                       ptx::kL2EvictLast);
+                        } else {
+                            // rows [pm * kSubB, +kSubB) of this CTA's B block, shared
+                            // with the same-role CTAs of the pairs sharing pn
+                            constexpr uint32_t kSubB = kRowsPerCta / kPM;
+                            uint16_t mask = 0;
+#pragma unroll
+                            for (uint32_t j = 0; j < kPM; ++j) mask |= 1u << (2 * (j * kPN + pn) + half_rank);
+                            const uint32_t sub = pm * kSubB * kBlockK;
+                            ptx::tma_load_2d_pair_mcast(ptx::smem_u32(st + 2 * kPlaneTileBytes) + sub, &tmap_b,
+                                                        leader_full, k0,
+                                                        static_cast<int32_t>(b_row0 + pm * kSubB), mask);
+                            ptx::tma_load_2d_pair_mcast(ptx::smem_u32(st + 3 * kPlaneTileBytes) + sub, &tmap_b,
+                                                        leader_full, k0,
+                                                        static_cast<int32_t>(b_row0 + args.N + pm * kSubB),
+                                                        mask);
+                        }
                         if (gate) ptx::st_relaxed_gpu(args.progress + cluster_id, issued + 1);
                         if (++stage == kStages) {
                             stage = 0;
@@ -372,12 +405,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             for (;; ++j) {
                 const uint32_t slot = j % kRing;
                 ptx::mbar_wait(&ring_full[slot], (j / kRing) & 1);
-                const uint32_t u = ring_tile[2 * slot], nb = ring_tile[2 * slot + 1];
+                const uint32_t u = ring_tile[2 * slot], nbm = ring_tile[2 * slot + 1];
                 asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
                                  ptx::smem_u32(&ring_empty[slot]))
                              : "memory");
                 if (u == kEnd) break;
-                const TileCoord tc = decode(args, u, nb);
+                const TileCoord tc = decode(args, u, nbm >> 16, nbm & 0xFFFFu);
                 const uint32_t idesc = ptx::idesc_i8(2 * kRowsPerCta, tc.n_size);
                 // Wait until the epilogue of the previous tile drained TMEM.
                 timed_wait(tmem_empty_bar, (j & 1) ^ 1, diag, w_tmem);
@@ -401,7 +434,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                         ptx::mma_i8_pair(acc2, dx1, dy0, idesc, 1u);     // + X1 Y0
                     }
                     // release the stage in every CTA that wrote into it
-                    ptx::mma_commit_pair(&empty_bar[stage], kCtas == 2 ? 0x3 : 0xF);
+                    ptx::mma_commit_pair(&empty_bar[stage], static_cast<uint16_t>((1u << kCtas) - 1));
                     if (++stage == kStages) {
                         stage = 0;
                         phase ^= 1;
@@ -434,14 +467,14 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         for (uint32_t j = 0;; ++j) {
             const uint32_t slot = j % kRing;
             ptx::mbar_wait(&ring_full[slot], (j / kRing) & 1);
-            const uint32_t u = ring_tile[2 * slot], nb = ring_tile[2 * slot + 1];
+            const uint32_t u = ring_tile[2 * slot], nbm = ring_tile[2 * slot + 1];
             __syncwarp();
             if (lane == 0)
                 asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
                                  ptx::smem_u32(&ring_empty[slot]))
                              : "memory");
             if (u == kEnd) break;
-            const TileCoord tc = decode(args, u, nb);
+            const TileCoord tc = decode(args, u, nbm >> 16, nbm & 0xFFFFu);
             const ModConst mc = args.mc[tc.prime];
             timed_wait(tmem_full_bar, j & 1, diag, w_epi);
             const long long e0 = clock64();
@@ -532,25 +565,59 @@ bool make_plane_map(CUtensorMap* map, const void* base, uint64_t k, uint64_t row
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Co-resident clusters of `ctas` CTAs with this kernel's footprint (cached per device).
-uint32_t max_active_clusters(int ctas, int dev) {
+// Kernel variants by cluster shape (pairs along M x pairs along N).
+struct Shape {
+    int pm, pn;
+    int ctas() const { return 2 * pm * pn; }
+};
+using KernelFn = void (*)(CUtensorMap, CUtensorMap, GemmArgs);
+constexpr Shape kShapes[] = {{1, 1}, {1, 2}, {1, 4}, {2, 2}, {2, 4}, {1, 8}};
+constexpr int kNumShapes = sizeof(kShapes) / sizeof(kShapes[0]);
+
+int shape_index(int pm, int pn) {
+    for (int i = 0; i < kNumShapes; ++i)
+        if (kShapes[i].pm == pm && kShapes[i].pn == pn) return i;
+    return -1;
+}
+
+KernelFn kernel_for(int si) {
+    switch (si) {
+        case 0: return ppmm_i8_sm100_kernel<1, 1>;
+        case 1: return ppmm_i8_sm100_kernel<1, 2>;
+        case 2: return ppmm_i8_sm100_kernel<1, 4>;
+        case 3: return ppmm_i8_sm100_kernel<2, 2>;
+        case 4: return ppmm_i8_sm100_kernel<2, 4>;
+        case 5: return ppmm_i8_sm100_kernel<1, 8>;
+    }
+    return nullptr;
+}
+
+// Co-resident clusters of a shape with this kernel's footprint (cached per device).
+uint32_t max_active_clusters(int si, int dev) {
     static std::mutex mu;
-    static int cache[64][2];
+    static int cache[64][kNumShapes];
     static bool init = false;
     std::lock_guard<std::mutex> lk(mu);
     if (!init) {
-        for (auto& c : cache) c[0] = c[1] = -1;
+        for (auto& c : cache)
+            for (int& v : c) v = -1;
         init = true;
     }
-    const int vi = ctas == 4 ? 1 : 0;
-    if (dev < 0 || dev >= 64) return 0;
-    if (cache[dev][vi] >= 0) return static_cast<uint32_t>(cache[dev][vi]);
-    auto kfn = ctas == 4 ? ppmm_i8_sm100_kernel<4> : ppmm_i8_sm100_kernel<2>;
+    if (dev < 0 || dev >= 64 || si < 0) return 0;
+    if (cache[dev][si] >= 0) return static_cast<uint32_t>(cache[dev][si]);
+    const int ctas = kShapes[si].ctas();
+    KernelFn kfn = kernel_for(si);
     if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(kSmemBytes)) != cudaSuccess)
         return 0;
+    if (ctas > 8 && cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                        cudaSuccess) {
+        cudaGetLastError();
+        cache[dev][si] = 0;
+        return 0;
+    }
     cudaLaunchConfig_t q{};
-    q.gridDim = dim3(static_cast<unsigned>(ctas) * 64);
+    q.gridDim = dim3(static_cast<unsigned>(ctas) * 8);
     q.blockDim = dim3(kNumThreads);
     q.dynamicSmemBytes = kSmemBytes;
     cudaLaunchAttribute qa[1];
@@ -561,8 +628,11 @@ uint32_t max_active_clusters(int ctas, int dev) {
     q.attrs = qa;
     q.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, kfn, &q) != cudaSuccess) n = 0;
-    cache[dev][vi] = n;
+    if (cudaOccupancyMaxActiveClusters(&n, kfn, &q) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+    }
+    cache[dev][si] = n;
     return static_cast<uint32_t>(n);
 }
 
@@ -607,7 +677,23 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     args.nprimes = L.nprimes;
     args.m_blocks = (L.M + 2 * kRowsPerCta - 1) / (2 * kRowsPerCta);
     args.n_blocks = (L.N + kMaxTileN - 1) / kMaxTileN;
-    args.units = args.m_blocks * L.parts * L.nprimes;
+
+    int dev = 0;
+    cudaGetDevice(&dev);
+    // cluster shape: needs n_blocks % pn == 0; falls back to a plain pair
+    int si = shape_index(L.cluster_pm, L.cluster_pn);
+    if (si < 0 || args.n_blocks % kShapes[si].pn != 0) si = 0;
+    const uint32_t occ2 = max_active_clusters(0, dev);
+    uint32_t occ_main = si == 0 ? occ2 : max_active_clusters(si, dev);
+    if (occ_main == 0) {
+        si = 0;
+        occ_main = occ2;
+    }
+    if (occ2 == 0) return cudaErrorInvalidConfiguration;
+    const Shape shp = kShapes[si];
+    args.unit_mblocks = static_cast<uint32_t>(shp.pm);
+    args.m_units = (args.m_blocks + args.unit_mblocks - 1) / args.unit_mblocks;
+    args.units = args.m_units * L.parts * L.nprimes;
     args.accumulate = L.accumulate ? 1u : 0u;
     args.a_part_rows = static_cast<uint32_t>(a_part_rows);
     args.out_part = L.out_part_elems ? L.out_part_elems
@@ -620,48 +706,39 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     args.gate_lead = L.gate_lead < 0 ? kGateLead : static_cast<uint32_t>(L.gate_lead);
     args.counter = L.progress + kProgressWords;  // shared by every launch of this call
 
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const bool want4 = L.cluster_ctas == 4 && args.n_blocks % 2 == 0;
-    const uint32_t occ2 = max_active_clusters(2, dev);
-    const uint32_t occ4 = want4 ? max_active_clusters(4, dev) : 0;
-    if (occ2 == 0 || (want4 && occ4 == 0)) return cudaErrorInvalidConfiguration;
-
-    // Cluster layouts: the main launch uses 4-CTA clusters (two pairs
-    // multicasting each A tile) when requested; 4-CTA clusters strand SMs
-    // (132 of 148 CTAs on B200), so a 2-CTA "filler" launch on a side stream
-    // takes the remaining SM pairs. Both pull units from the same counter.
+    // Cluster layouts: the main launch uses the requested multi-pair shape;
+    // those strand SMs (e.g. 132 of 148 CTAs with 4-CTA clusters on B200), so
+    // a 1x1 "filler" launch on a side stream takes the remaining SM pairs.
+    // Both pull units from the same counter.
     struct Part {
-        int ctas;
+        int si;
         uint32_t clusters, pair0, group0;
     } parts[2];
     int nparts = 0;
     uint32_t pairs_used = 0, groups_used = 0;
-    auto plan = [&](int ctas, uint32_t max_cl) {
-        const uint32_t ppc = static_cast<uint32_t>(ctas / 2);
-        const uint32_t G = args.n_blocks / ppc;
+    auto plan = [&](int s_idx, uint32_t max_cl) {
+        const Shape sh = kShapes[s_idx];
+        const uint32_t ppc = static_cast<uint32_t>(sh.pm * sh.pn);
+        const uint32_t G = args.n_blocks / sh.pn;
         const uint64_t items = static_cast<uint64_t>(args.units) * G;
         uint32_t cl = static_cast<uint32_t>(std::min<uint64_t>(max_cl, items));
         if (L.max_clusters > 0) cl = std::min<uint32_t>(cl, L.max_clusters);
         if (cl == 0) return;
-        parts[nparts++] = {ctas, cl, pairs_used, groups_used};
+        parts[nparts++] = {s_idx, cl, pairs_used, groups_used};
         pairs_used += cl * ppc;
         groups_used += cl / G + cl % G;
     };
-    if (want4) {
-        plan(4, occ4);
-        const uint32_t spare_pairs = occ2 > 2 * occ4 ? occ2 - 2 * occ4 : 0;
-        if (L.max_clusters == 0 && spare_pairs > 0) plan(2, spare_pairs);
-    } else {
-        plan(2, occ2);
+    plan(si, occ_main);
+    if (si != 0) {
+        const uint32_t ppc = static_cast<uint32_t>(shp.pm * shp.pn);
+        const uint32_t spare_pairs = occ2 > ppc * occ_main ? occ2 - ppc * occ_main : 0;
+        if (L.max_clusters == 0 && spare_pairs > 0) plan(0, spare_pairs);
     }
     const size_t scratch = (kProgressWords + 32) * 4 + static_cast<size_t>(groups_used) * kMail * 8;
     if (scratch > kScheduleScratchBytes || pairs_used > kProgressWords) return cudaErrorInvalidValue;
     cudaError_t e = cudaMemsetAsync(L.progress, 0, scratch, stream);
     if (e != cudaSuccess) return e;
 
-    CUtensorMap mb;
-    if (!make_plane_map(&mb, L.b_planes, L.K, b_rows, L.ldk, kRowsPerCta)) return cudaErrorInvalidValue;
     cudaStream_t side = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
     if (nparts > 1) {
@@ -674,8 +751,8 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     for (int i = 0; i < nparts; ++i) {
         const Part& pt = parts[i];
         GemmArgs a = args;
-        const uint32_t ppc = static_cast<uint32_t>(pt.ctas / 2);
-        a.G = args.n_blocks / ppc;
+        const Shape sh = kShapes[pt.si];
+        a.G = args.n_blocks / static_cast<uint32_t>(sh.pn);
         a.F = pt.clusters / a.G;
         a.L = pt.clusters % a.G;
         a.active_clusters = pt.clusters;
@@ -684,24 +761,23 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
                     static_cast<size_t>(pt.group0) * kMail;
         a.stats = L.stats ? reinterpret_cast<unsigned long long*>(L.stats) + pt.pair0 * kStatSlots
                           : nullptr;
-        CUtensorMap ma;
-        if (!make_plane_map(&ma, L.a_planes, L.K, a_rows, L.ldk,
-                            pt.ctas == 4 ? kRowsPerCta / 2 : kRowsPerCta))
+        CUtensorMap ma, mb;
+        if (!make_plane_map(&ma, L.a_planes, L.K, a_rows, L.ldk, kRowsPerCta / sh.pn) ||
+            !make_plane_map(&mb, L.b_planes, L.K, b_rows, L.ldk, kRowsPerCta / sh.pm))
             return cudaErrorInvalidValue;
         cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(static_cast<unsigned>(pt.ctas) * pt.clusters);
+        cfg.gridDim = dim3(static_cast<unsigned>(sh.ctas()) * pt.clusters);
         cfg.blockDim = dim3(kNumThreads);
         cfg.dynamicSmemBytes = kSmemBytes;
         cfg.stream = i == 0 ? stream : side;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = static_cast<unsigned>(pt.ctas);
+        attr[0].val.clusterDim.x = static_cast<unsigned>(sh.ctas());
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        e = pt.ctas == 4 ? cudaLaunchKernelEx(&cfg, ppmm_i8_sm100_kernel<4>, ma, mb, a)
-                         : cudaLaunchKernelEx(&cfg, ppmm_i8_sm100_kernel<2>, ma, mb, a);
+        e = cudaLaunchKernelEx(&cfg, kernel_for(pt.si), ma, mb, a);
         if (e != cudaSuccess) return e;
     }
     if (nparts > 1) {
