@@ -47,24 +47,29 @@ def _compile(cmd):
     return r.stderr
 
 
-def build(debug: bool = False, verbose: bool = False) -> Path:
-    BUILD.mkdir(exist_ok=True)
+def build(debug: bool = False, verbose: bool = False, defines=(), out: Path = OUT) -> Path:
+    """defines / out: experiment variants (e.g. -DIRL_EPI_WARPS=8 into build/variants/),
+    loaded with IRL_B200_LIB=<path>; the product library is always OUT."""
+    out = Path(out)
+    bdir = BUILD if out == OUT else out.parent / (out.stem + ".obj")
+    bdir.mkdir(parents=True, exist_ok=True)
     nvcc = _nvcc()
     cxx = _host_cxx()
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-ccbin", cxx,
               f"-I{ROOT / 'include'}", f"-I{CSRC}", f"-I{HOST}"]
     if debug:
         common.append("-DIRL_WAIT_TIMEOUT")
+    common += [f"-D{d}" for d in defines]
     jobs = []
     objs = []
     for src in CUDA_SOURCES:
-        obj = BUILD / (Path(src).stem + ".o")
+        obj = bdir / (Path(src).stem + ".o")
         objs.append(obj)
         jobs.append([nvcc, *ARCH, *common, "-Xptxas", "-v", "-c", str(CSRC / src), "-o", str(obj)])
     for src in HOST_SOURCES:
         if not (HOST / src).exists():
             continue
-        obj = BUILD / (Path(src).stem + ".o")
+        obj = bdir / (Path(src).stem + ".o")
         objs.append(obj)
         jobs.append([cxx, "-O2", "-std=c++17", "-fPIC", f"-I{ROOT / 'include'}", f"-I{HOST}",
                      "-I/usr/local/cuda/include", "-c", str(HOST / src), "-o", str(obj)])
@@ -73,18 +78,20 @@ def build(debug: bool = False, verbose: bool = False) -> Path:
     if verbose:
         for log in logs:
             sys.stderr.write(log)
-    link = [nvcc, *ARCH, "-shared", "-ccbin", cxx, "-o", str(OUT), *map(str, objs), "-lcudart_static",
+    link = [nvcc, *ARCH, "-shared", "-ccbin", cxx, "-o", str(out), *map(str, objs), "-lcudart_static",
             "-lrt", "-ldl", "-lpthread"]
     _compile(link)
-    return OUT
+    return out
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--debug", action="store_true", help="trap on stuck mbarrier waits")
     ap.add_argument("-v", "--verbose", action="store_true")
+    ap.add_argument("-D", dest="defines", action="append", default=[], help="experiment define")
+    ap.add_argument("--out", default=str(OUT), help="variant library path (load with IRL_B200_LIB)")
     a = ap.parse_args()
-    print(build(debug=a.debug, verbose=a.verbose))
+    print(build(debug=a.debug, verbose=a.verbose, defines=a.defines, out=Path(a.out)))
 
 
 if __name__ == "__main__":

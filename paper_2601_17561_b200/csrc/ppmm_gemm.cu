@@ -16,7 +16,7 @@
 //     [0, 256) and acc2 = X0 Y1 + X1 Y0 in [256, 512);
 //   * warp 0 = TMA producer (both CTAs load their half of A and B),
 //     warp 1 = MMA issuer (leader CTA) + TMEM owner, warps 2..9 = epilogue
-//     (two warps per TMEM lane quarter, each draining half the columns);
+//     (kEpiWarps / 4 warps per TMEM lane quarter, interleaved over 16-column chunks);
 //   * 3-stage smem ring of 128-byte K blocks, 128B-swizzled, mbarrier-paced;
 //   * persistent static schedule over "units" (one 256-row block of one
 //     (prime, part)), ordered prime-major so a prime's query planes stay
@@ -30,6 +30,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -51,7 +53,14 @@ constexpr int kStages = 3;         // 3 x 64 KB ring (SW128 is the fast UMMA lay
 constexpr int kUmmaK = 32;         // K per tcgen05.mma for 8-bit inputs
 constexpr int kPlaneTileBytes = kRowsPerCta * kBlockK;          // 16 KB
 constexpr int kStageBytes = 4 * kPlaneTileBytes;                // X0 X1 Y0 Y1
-constexpr int kEpiWarps = 8;
+#ifndef IRL_A_REUSE
+#define IRL_A_REUSE 1  // reuse X0 from the tensor core's A collector (tcgen05 collector::a)
+#endif
+#ifndef IRL_EPI_WARPS
+#define IRL_EPI_WARPS 16
+#endif
+constexpr int kEpiWarps = IRL_EPI_WARPS;  // multiple of 4: kEpiWarps / 4 warps per TMEM lane quarter
+constexpr int kEpiGroups = kEpiWarps / 4;
 constexpr int kNumThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kAcc2Col = 256;
@@ -429,8 +438,14 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                         const uint64_t dy1 =
                             ptx::smem_desc_k_sw128(st + 3 * kPlaneTileBytes + koff);
                         const uint32_t accum = (kb | k) != 0;
+#if IRL_A_REUSE
+                        // X0 stays in the A collector for the second product
+                        ptx::mma_i8_pair_ca<ptx::CollectorA::kFill>(acc1, dx0, dy0, idesc, accum);     // X0 Y0
+                        ptx::mma_i8_pair_ca<ptx::CollectorA::kLastUse>(acc2, dx0, dy1, idesc, accum);  // X0 Y1
+#else
                         ptx::mma_i8_pair(acc1, dx0, dy0, idesc, accum);  // X0 Y0
                         ptx::mma_i8_pair(acc2, dx0, dy1, idesc, accum);  // X0 Y1
+#endif
                         ptx::mma_i8_pair(acc2, dx1, dy0, idesc, 1u);     // + X1 Y0
                     }
                     // release the stage in every CTA that wrote into it
@@ -460,7 +475,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     } else {
         // ---------------- Epilogue (both CTAs, 8 warps) ----------------
         const uint32_t quarter = warp % 4;        // TMEM lane quarter this warp may access
-        const uint32_t half = (warp - 2) / 4;     // which half of the tile's columns
+        const uint32_t cgrp = (warp - 2) / 4;     // which 16-column chunks of the tile (interleaved)
         const uint32_t leader_tmem_empty = ptx::mapa_shared(ptx::smem_u32(tmem_empty_bar), rank & ~1u);
         const bool diag = args.stats != nullptr && leader && warp == 2 && lane == 0;
         unsigned long long w_epi = 0, busy_epi = 0;
@@ -486,9 +501,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                             static_cast<size_t>(tc.prime) * args.N * args.M +
                             m;
             const uint32_t lane_base = tmem_base + ((quarter * 32u) << 16);
-            const uint32_t cols = tc.n_size / 2;  // multiple of 16
-            const uint32_t c_begin = half * cols;
-            for (uint32_t c = c_begin; c < c_begin + cols; c += 16) {
+            for (uint32_t c = cgrp * 16; c < tc.n_size; c += 16 * kEpiGroups) {
                 uint32_t a1[16], a2[16];
                 ptx::tmem_ld_32x32b_x16(lane_base + c, a1);
                 ptx::tmem_ld_32x32b_x16(lane_base + kAcc2Col + c, a2);
@@ -733,6 +746,12 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
         const uint32_t ppc = static_cast<uint32_t>(shp.pm * shp.pn);
         const uint32_t spare_pairs = occ2 > ppc * occ_main ? occ2 - ppc * occ_main : 0;
         if (L.max_clusters == 0 && spare_pairs > 0) plan(0, spare_pairs);
+    }
+    if (std::getenv("IRL_PPMM_VERBOSE")) {
+        for (int i = 0; i < nparts; ++i)
+            std::fprintf(stderr, "[irl] ppmm launch %d: cluster %dx%d pairs, %u clusters (%u CTAs), units %u\n", i,
+                         kShapes[parts[i].si].pm, kShapes[parts[i].si].pn, parts[i].clusters,
+                         parts[i].clusters * kShapes[parts[i].si].ctas(), args.units);
     }
     const size_t scratch = (kProgressWords + 32) * 4 + static_cast<size_t>(groups_used) * kMail * 8;
     if (scratch > kScheduleScratchBytes || pairs_used > kProgressWords) return cudaErrorInvalidValue;

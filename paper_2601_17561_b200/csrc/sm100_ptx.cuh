@@ -161,6 +161,30 @@ __device__ __forceinline__ void tc_fence_after() {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
+// Same with the A-operand collector: kFill keeps A in the tensor core's
+// collector buffer after this MMA, kLastUse reads it from there (no second
+// shared-memory read of the same A tile) and releases it.
+enum class CollectorA { kFill, kLastUse };
+template <CollectorA kOp>
+__device__ __forceinline__ void mma_i8_pair_ca(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                               uint32_t idesc, uint32_t accumulate) {
+    if constexpr (kOp == CollectorA::kFill) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::i8.collector::a::fill [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+            "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::i8.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+            "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+            : "memory");
+    }
+}
+
 // D[tmem] (+)= A[smem] * B[smem]^T, signed int8 inputs, int32 accumulators,
 // issued once for the CTA pair (M = 256 spread over both CTAs' TMEM).
 __device__ __forceinline__ void mma_i8_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
