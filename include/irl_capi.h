@@ -40,7 +40,8 @@ typedef enum irl_status {
     IRL_ERR_CUDA = 7,
     IRL_ERR_NO_DEVICE = 8,
     IRL_ERR_OUT_OF_MEMORY = 9,
-    IRL_ERR_UNSUPPORTED = 10
+    IRL_ERR_UNSUPPORTED = 10,
+    IRL_ERR_ZERO_OVERLAP = 11               /* irislab::ZeroOverlap              errors.hpp:18 */
 } irl_status;
 
 typedef struct irl_ctx irl_ctx;
@@ -177,6 +178,32 @@ int irl_ccmm_twin(irl_ctx* ctx, long d1, long d2, long d3, long n_db, long n_qry
                   const double* db, const double* qry, double* msgs);
 /* Bytes of HBM the engine holds (planes + workspace). */
 uint64_t irl_ccmm_device_bytes(const irl_ccmm* e);
+
+/* ---- plaintext iris scoring stage ---------------------------
+ * Templates are packed bit planes in pack_bits order (pipeline.cpp:70-76):
+ * bit i of template t is bit (i % 64) of word t*words + i/64, words =
+ * ceil(d/64); code and mask planes separate. The query side is n_eyes
+ * templates; column c = e*rho + r of the query batch is rotate(q_e, r)
+ * (iris_core.cpp:65-76), as in pipeline::prepare (pipeline.cpp:121-138).
+ * Both sums are int8 GEMMs on the tensor cores (PPMM kernel, inner mode).
+ *
+ * inner[c][j]   = <to_masked(q_c), to_masked(db_j)>    (iris_core.cpp:37-51)
+ * overlap[c][j] = |m_q(c) AND m_db(j)|                  (overlap_count, pipeline.cpp:78-82;
+ *                 prepare's overlaps[c*blocks + b][i] = overlap[c][b*d_blk + i], :140-151)
+ * Either output may be NULL. ShapeMismatch if d == 0 (IrisTemplate::validate). */
+int irl_iris_inner_overlap(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db_mask, size_t n_db,
+                           const uint64_t* q_code, const uint64_t* q_mask, size_t n_eyes, size_t rho,
+                           size_t d, int32_t* inner, int32_t* overlap);
+/* Scores and matching (iris_core.cpp:55-59, 78-90): score = inner / overlap in
+ * IEEE double. match_bits[e][j] = OR over r of score(c = e*rho + r, j) in
+ * [p_lo, p_hi]; eye_result[e] = match_db_reference(rotations of eye e, db):
+ * 1 match, 0 none, -1 ZeroOverlap (the first evaluated score in its
+ * rotation-major loop order had an empty overlap before any match). Returns
+ * IRL_ERR_ZERO_OVERLAP if any eye hit that case (outputs still written).
+ * scores[c][j] (optional) is NaN where the overlap is empty. */
+int irl_iris_match(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db_mask, size_t n_db,
+                   const uint64_t* q_code, const uint64_t* q_mask, size_t n_eyes, size_t rho, size_t d,
+                   double p_lo, double p_hi, uint8_t* match_bits, int32_t* eye_result, double* scores);
 
 #ifdef __cplusplus
 }

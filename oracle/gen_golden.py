@@ -215,8 +215,48 @@ def main():
             qry[:, e * rho + r] = q[e]
     prod = db.astype(np.int64) @ qry.astype(np.int64)
     np.savez_compressed(GOLDEN / "iris_kat.npz", db=db, qry=qry, prod=prod)
+    gen_iris_scores()
     print("wrote", sorted(p.name for p in GOLDEN.iterdir()))
 
 
+IRIS_INTERVALS = [(0.15, 1.0), (0.5, 1.0), (0.99, 1.0), (-1.0, 1.0)]
+
+
+def gen_iris_scores():
+    """Plaintext iris scoring KATs from the reference's own iris::score,
+    iris::rotate and iris::match_db_reference (iris_core.cpp:55-90) on
+    synth_db templates (:92-112): a dense-mask set (0.8, with eye 0 planted
+    as template 5 so exact matches exist) and a sparse-mask sets (0.1, 0.05) in
+    which empty overlaps (ZeroOverlap) occur."""
+    out = {}
+    d, n_db, eyes, rho = 200, 48, 3, 7
+    for tag, dens, s0 in (("dense", 0.8, 21), ("sparse", 0.1, 23), ("sparser", 0.05, 25)):
+        dc, dm = ol.ref_synth_templates(n_db, d, dens, s0)
+        qc, qm = ol.ref_synth_templates(eyes, d, dens, s0 + 1)
+        if tag == "dense":
+            dc[5], dm[5] = ol.ref_rotate(qc[0], qm[0], 3)  # matches eye 0 at rotation 3
+        rc = np.zeros((eyes * rho, d), np.uint8)
+        rm = np.zeros((eyes * rho, d), np.uint8)
+        for e in range(eyes):
+            for r in range(rho):
+                rc[e * rho + r], rm[e * rho + r] = ol.ref_rotate(qc[e], qm[e], r)
+        out[f"{tag}_db_code"], out[f"{tag}_db_mask"] = dc, dm
+        out[f"{tag}_q_code"], out[f"{tag}_q_mask"] = qc, qm
+        out[f"{tag}_scores"] = ol.ref_scores(rc, rm, dc, dm)
+        match = np.zeros((len(IRIS_INTERVALS), eyes), np.int32)
+        for k, (lo, hi) in enumerate(IRIS_INTERVALS):
+            for e in range(eyes):
+                sl = slice(e * rho, (e + 1) * rho)
+                match[k, e] = ol.ref_match(rc[sl], rm[sl], dc, dm, lo, hi)
+        out[f"{tag}_match"] = match
+    out["intervals"] = np.array(IRIS_INTERVALS)
+    out["rho"] = np.array(rho)
+    np.savez_compressed(GOLDEN / "iris_scores.npz", **out)
+
+
 if __name__ == "__main__":
-    main()
+    import sys as _sys
+    if "--iris-only" in _sys.argv:
+        gen_iris_scores()
+    else:
+        main()

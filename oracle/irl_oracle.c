@@ -485,3 +485,33 @@ void orc_synth_block(uint64_t seed, uint32_t stream, uint32_t plane, uint32_t ro
             out[(size_t)r * ncols + c] =
                 (uint16_t)orc_synth_residue(seed, stream, plane, row0 + r, col0 + c, m);
 }
+
+/* ---- plaintext iris scoring ------------------------------------------------
+ * inner_and_overlap (iris_core.cpp:37-51): av = m - 2 (c & m) per entry
+ * (to_masked, :28-35), inner = sum av*bv, overlap = sum (m_a & m_b) =
+ * overlap_count of the packed masks (pipeline.cpp:78-82). The query column
+ * c = e*rho + r is rotate(q_e, r) (iris_core.cpp:65-76): out[(i + r) % d] =
+ * t[i], i.e. entry k of the rotated template is t[(k - r) mod d]. */
+void orc_iris_inner_overlap(const uint8_t* db_code, const uint8_t* db_mask, size_t n_db, const uint8_t* q_code,
+                            const uint8_t* q_mask, size_t n_eyes, size_t rho, size_t d, int32_t* inner,
+                            int32_t* overlap) {
+    for (size_t e = 0; e < n_eyes; ++e)
+        for (size_t r = 0; r < rho; ++r) {
+            const size_t c = e * rho + r, rr = d ? r % d : 0;
+            for (size_t j = 0; j < n_db; ++j) {
+                long in = 0, ov = 0;
+                const uint8_t* ac = db_code + j * d;
+                const uint8_t* am = db_mask + j * d;
+                for (size_t k = 0; k < d; ++k) {
+                    const size_t i = k >= rr ? k - rr : k + d - rr;
+                    const int bc = q_code[e * d + i], bm = q_mask[e * d + i];
+                    const int av = am[k] - 2 * (ac[k] & am[k]);
+                    const int bv = bm - 2 * (bc & bm);
+                    in += av * bv;
+                    ov += am[k] & bm;
+                }
+                inner[c * n_db + j] = (int32_t)in;
+                overlap[c * n_db + j] = (int32_t)ov;
+            }
+        }
+}

@@ -67,6 +67,13 @@ void orc_synth_block(uint64_t seed, uint32_t stream, uint32_t plane, uint32_t ro
                      uint32_t nrows, uint32_t col0, uint32_t ncols, uint32_t m,
                      uint16_t* out /* [nrows][ncols] */);
 
+/* ---- plaintext iris scoring (iris_core.cpp:28-59, 65-76; pipeline.cpp:78-82) ----
+ * db / query templates as unpacked {0,1} bytes [n][d]; query column c =
+ * e*rho + r is rotate(q_e, r). inner/overlap: int32 [n_eyes*rho][n_db]. */
+void orc_iris_inner_overlap(const uint8_t* db_code, const uint8_t* db_mask, size_t n_db, const uint8_t* q_code,
+                            const uint8_t* q_mask, size_t n_eyes, size_t rho, size_t d, int32_t* inner,
+                            int32_t* overlap);
+
 #ifdef __cplusplus
 }
 #endif

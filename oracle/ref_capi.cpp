@@ -10,6 +10,7 @@
 #include <atomic>
 #include <cstring>
 #include <exception>
+#include <limits>
 #include <random>
 #include <string>
 #include <thread>
@@ -42,6 +43,9 @@ int map_exception() {
     } catch (const ModulusBudget& e) {
         g_err = e.what();
         return 5;
+    } catch (const ZeroOverlap& e) {
+        g_err = e.what();
+        return 11;
     } catch (const Error& e) {
         g_err = e.what();
         return std::string(e.what()).find("coprime") != std::string::npos ? 4 : 6;
@@ -297,6 +301,75 @@ int ref_synth_masked_rotated(size_t n, size_t d, double mask_density, uint64_t s
             auto mv = iris::to_masked(iris::rotate(db[t], rot));
             std::memcpy(out + t * d, mv.values.data(), d);
         }
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// Raw synth_db templates (iris_core.cpp:92-112): code / mask bits [n][d].
+int ref_synth_templates(size_t n, size_t d, double mask_density, uint64_t seed, uint8_t* code, uint8_t* mask) {
+    try {
+        auto db = iris::synth_db(n, d, mask_density, seed);
+        for (size_t t = 0; t < n; ++t) {
+            std::memcpy(code + t * d, db[t].code.data(), d);
+            std::memcpy(mask + t * d, db[t].mask.data(), d);
+        }
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+namespace {
+std::vector<iris::IrisTemplate> to_templates(const uint8_t* code, const uint8_t* mask, size_t n, size_t d) {
+    std::vector<iris::IrisTemplate> ts(n);
+    for (size_t t = 0; t < n; ++t) {
+        ts[t].code.assign(code + t * d, code + (t + 1) * d);
+        ts[t].mask.assign(mask + t * d, mask + (t + 1) * d);
+    }
+    return ts;
+}
+}  // namespace
+
+// iris::score (iris_core.cpp:55-59) for every (query c, template j):
+// out[c * n_db + j]; NaN where it throws ZeroOverlap. Returns 0.
+int ref_iris_scores(const uint8_t* q_code, const uint8_t* q_mask, size_t nq, const uint8_t* db_code,
+                    const uint8_t* db_mask, size_t n_db, size_t d, double* out) {
+    try {
+        auto q = to_templates(q_code, q_mask, nq, d);
+        auto db = to_templates(db_code, db_mask, n_db, d);
+        for (size_t c = 0; c < nq; ++c)
+            for (size_t j = 0; j < n_db; ++j) {
+                try {
+                    out[c * n_db + j] = iris::score(q[c], db[j]);
+                } catch (const ZeroOverlap&) {
+                    out[c * n_db + j] = std::numeric_limits<double>::quiet_NaN();
+                }
+            }
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// iris::rotate (iris_core.cpp:65-76) of one template.
+void ref_iris_rotate(const uint8_t* code, const uint8_t* mask, size_t d, size_t r, uint8_t* out_code,
+                     uint8_t* out_mask) {
+    auto t = to_templates(code, mask, 1, d);
+    auto o = iris::rotate(t[0], r);
+    std::memcpy(out_code, o.code.data(), d);
+    std::memcpy(out_mask, o.mask.data(), d);
+}
+
+// iris::match_db_reference (iris_core.cpp:78-90): *out = 0/1; status 11 on ZeroOverlap.
+int ref_match_db_reference(const uint8_t* q_code, const uint8_t* q_mask, size_t nq, const uint8_t* db_code,
+                           const uint8_t* db_mask, size_t n_db, size_t d, double n_lo, double n_hi,
+                           double p_lo, double p_hi, int* out) {
+    try {
+        auto q = to_templates(q_code, q_mask, nq, d);
+        auto db = to_templates(db_code, db_mask, n_db, d);
+        *out = iris::match_db_reference(q, db, iris::Interval{n_lo, n_hi}, iris::Interval{p_lo, p_hi}) ? 1 : 0;
         return 0;
     } catch (...) {
         return map_exception();

@@ -31,6 +31,7 @@ IRL_ERR_CUDA = 7
 IRL_ERR_NO_DEVICE = 8
 IRL_ERR_OUT_OF_MEMORY = 9
 IRL_ERR_UNSUPPORTED = 10
+IRL_ERR_ZERO_OVERLAP = 11
 
 # Every symbol include/irl_capi.h declares, with (restype, argtypes).
 SIGNATURES = {
@@ -69,6 +70,8 @@ SIGNATURES = {
     "irl_ccmm_twin": (C.c_int, [vp, C.c_long, C.c_long, C.c_long, C.c_long, C.c_long, C.c_double, C.c_double,
                                 C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double),
                                 C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "irl_iris_inner_overlap": (C.c_int, [vp, vp, vp, sz, vp, vp, sz, sz, sz, vp, vp]),
+    "irl_iris_match": (C.c_int, [vp, vp, vp, sz, vp, vp, sz, sz, sz, C.c_double, C.c_double, vp, vp, vp]),
 }
 
 _lib = None

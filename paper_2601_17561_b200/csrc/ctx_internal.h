@@ -1,0 +1,105 @@
+// Internal: the context object behind the C ABI and the error / launch
+// helpers shared by the C-ABI translation units (capi.cu, iris.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <mutex>
+#include <string>
+
+#include "../../include/irl_capi.h"
+#include "kernels_aux.cuh"
+#include "ppmm.h"
+
+namespace irl {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        const size_t want = std::max<size_t>(bytes, 1 << 20);
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct Status {
+    int code;
+    std::string msg;
+};
+
+}  // namespace irl
+
+struct irl_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    uint64_t launches = 0;
+    std::recursive_mutex mu;
+    irl::DevBuf ws[8];
+    irl::SplitStats* d_stats = nullptr;
+    irl::SplitStats* h_stats = nullptr;
+    int32_t* d_absmax = nullptr;
+    int32_t* h_absmax = nullptr;
+    uint32_t* d_progress = nullptr;  // group-gating scratch of the PPMM kernel
+    uint64_t* d_diag = nullptr;      // PPMM diagnostics (irl_diag_ppmm), lazily allocated
+    bool diag = false;
+};
+
+
+namespace irl {
+
+inline int set_err(irl_ctx* ctx, int code, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return code;
+}
+
+inline int cuda_fail(irl_ctx* ctx, cudaError_t e, const char* where) {
+    cudaGetLastError();  // clear sticky non-fatal state
+    const int code = e == cudaErrorMemoryAllocation ? IRL_ERR_OUT_OF_MEMORY : IRL_ERR_CUDA;
+    return set_err(ctx, code, std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e));
+}
+
+#define IRL_CK(ctx, expr)                                              \
+    do {                                                               \
+        cudaError_t e__ = (expr);                                      \
+        if (e__ != cudaSuccess) return cuda_fail((ctx), e__, #expr);   \
+    } while (0)
+
+#define IRL_LAUNCH(ctx, expr)                                          \
+    do {                                                               \
+        cudaError_t e__ = (expr);                                      \
+        if (e__ != cudaSuccess) return cuda_fail((ctx), e__, #expr);   \
+        ++(ctx)->launches;                                             \
+    } while (0)
+
+struct Guard {
+    irl_ctx* c;
+    std::lock_guard<std::recursive_mutex> lk;
+    explicit Guard(irl_ctx* ctx) : c(ctx), lk(ctx->mu) {
+        cudaSetDevice(ctx->device);
+        ctx->err.clear();
+    }
+};
+
+inline cudaStream_t pick_stream(irl_ctx* ctx, void* s) {
+    return s ? static_cast<cudaStream_t>(s) : ctx->stream;
+}
+
+}  // namespace irl

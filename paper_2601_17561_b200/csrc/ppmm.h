@@ -12,6 +12,11 @@
 namespace irl {
 
 constexpr uint32_t kMaxPrimesPerLaunch = 32;
+// Kernel modes: kModePsq = the fused mod-p^2 PPMM (uint16 residues out);
+// kModeInner = two independent int8 products acc1 = X0 Y0, acc2 = X1 Y1 with
+// raw int32 outputs (mask overlaps and ternary inner products, iris.cu).
+constexpr int kModePsq = 0;
+constexpr int kModeInner = 1;
 // Diagnostics slots per CTA pair (PpmmLaunch::stats): 0 producer empty-wait
 // cycles, 1 producer gate cycles, 2 MMA full-wait cycles, 3 MMA tmem-empty
 // wait cycles, 4 MMA thread total cycles, 5 epilogue tmem-full wait cycles,
@@ -45,6 +50,8 @@ struct PpmmLaunch {
     // tile by TMA multicast) x cluster_pn pairs along N (sharing each database
     // tile). 1x1 is a plain CTA pair; SMs a multi-pair shape strands are taken
     // by a 1x1 filler launch pulling from the same unit counter.
+    int mode = kModePsq;
+    int32_t* out_i32[2] = {nullptr, nullptr};  // kModeInner outputs [parts][nprimes][N][M]
     int cluster_pm = 1;
     int cluster_pn = 4;
     ModConst mc[kMaxPrimesPerLaunch];

@@ -83,6 +83,7 @@ struct __align__(64) GemmArgs {
     uint32_t a_part_rows;             // plane rows between consecutive parts of A
     unsigned long long out_part;      // output elements between consecutive parts
     uint16_t* out;
+    int32_t* out_i32[2];              // kMode == kModeInner: acc1 / acc2 as int32 [n][m] (nullable)
     uint32_t* progress;               // [clusters] K blocks issued by each pair's leader producer
     uint32_t* counter;                // next unit to hand out (dynamic schedule)
     unsigned long long* mailbox;      // [groups][kMail] ((seq+1) << 32 | unit) published per group
@@ -176,7 +177,7 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
 // pairs with the same pn share each B (query) tile. Every stage is released
 // only when all pairs of the cluster have consumed it (commit multicast), so
 // the cluster runs in lock-step over K.
-template <int kPM, int kPN>
+template <int kPM, int kPN, int kMode>
 __global__ void __launch_bounds__(kNumThreads, 1)
     ppmm_i8_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a,
                          const __grid_constant__ CUtensorMap tmap_b,
@@ -438,6 +439,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                         const uint64_t dy1 =
                             ptx::smem_desc_k_sw128(st + 3 * kPlaneTileBytes + koff);
                         const uint32_t accum = (kb | k) != 0;
+                        if constexpr (kMode == kModeInner) {
+                            // two independent products: acc1 = X0 Y0, acc2 = X1 Y1
+                            ptx::mma_i8_pair(acc1, dx0, dy0, idesc, accum);
+                            ptx::mma_i8_pair(acc2, dx1, dy1, idesc, accum);
+                            continue;
+                        }
 #if IRL_A_REUSE
                         // X0 stays in the A collector for the second product
                         ptx::mma_i8_pair_ca<ptx::CollectorA::kFill>(acc1, dx0, dy0, idesc, accum);     // X0 Y0
@@ -507,6 +514,17 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                 ptx::tmem_ld_32x32b_x16(lane_base + kAcc2Col + c, a2);
                 ptx::tmem_ld_wait();
                 if (!row_ok) continue;
+                if constexpr (kMode == kModeInner) {
+                    const size_t base = tc.part * args.out_part + static_cast<size_t>(tc.prime) * args.N * args.M +
+                                        static_cast<size_t>(tc.n0 + c) * args.M + m;
+                    for (int jj = 0; jj < 16; ++jj) {
+                        if (tc.n0 + c + jj >= args.N) break;
+                        const size_t o = base + static_cast<size_t>(jj) * args.M;
+                        if (args.out_i32[0]) args.out_i32[0][o] = static_cast<int32_t>(a1[jj]);
+                        if (args.out_i32[1]) args.out_i32[1][o] = static_cast<int32_t>(a2[jj]);
+                    }
+                    continue;
+                }
                 uint16_t* dst = out + static_cast<size_t>(tc.n0 + c) * args.M;
                 if (!args.accumulate && tc.n0 + c + 16 <= args.N) {
                     // fast path: whole 16-column chunk in range, overwrite
@@ -593,14 +611,21 @@ int shape_index(int pm, int pn) {
     return -1;
 }
 
-KernelFn kernel_for(int si) {
+KernelFn kernel_for(int si, int mode = kModePsq) {
+    if (mode == kModeInner) {
+        switch (si) {
+            case 0: return ppmm_i8_sm100_kernel<1, 1, kModeInner>;
+            case 2: return ppmm_i8_sm100_kernel<1, 4, kModeInner>;
+        }
+        return nullptr;
+    }
     switch (si) {
-        case 0: return ppmm_i8_sm100_kernel<1, 1>;
-        case 1: return ppmm_i8_sm100_kernel<1, 2>;
-        case 2: return ppmm_i8_sm100_kernel<1, 4>;
-        case 3: return ppmm_i8_sm100_kernel<2, 2>;
-        case 4: return ppmm_i8_sm100_kernel<2, 4>;
-        case 5: return ppmm_i8_sm100_kernel<1, 8>;
+        case 0: return ppmm_i8_sm100_kernel<1, 1, kModePsq>;
+        case 1: return ppmm_i8_sm100_kernel<1, 2, kModePsq>;
+        case 2: return ppmm_i8_sm100_kernel<1, 4, kModePsq>;
+        case 3: return ppmm_i8_sm100_kernel<2, 2, kModePsq>;
+        case 4: return ppmm_i8_sm100_kernel<2, 4, kModePsq>;
+        case 5: return ppmm_i8_sm100_kernel<1, 8, kModePsq>;
     }
     return nullptr;
 }
@@ -695,6 +720,7 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     cudaGetDevice(&dev);
     // cluster shape: needs n_blocks % pn == 0; falls back to a plain pair
     int si = shape_index(L.cluster_pm, L.cluster_pn);
+    if (L.mode == kModeInner && si != 0) si = 2;  // inner-product mode is built for 1x1 and 1x4
     if (si < 0 || args.n_blocks % kShapes[si].pn != 0) si = 0;
     const uint32_t occ2 = max_active_clusters(0, dev);
     uint32_t occ_main = si == 0 ? occ2 : max_active_clusters(si, dev);
@@ -712,6 +738,9 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     args.out_part = L.out_part_elems ? L.out_part_elems
                                      : static_cast<unsigned long long>(L.nprimes) * L.N * L.M;
     args.out = L.out;
+    args.out_i32[0] = L.out_i32[0];
+    args.out_i32[1] = L.out_i32[1];
+    if (L.mode == kModeInner && L.accumulate) return cudaErrorInvalidValue;
     for (uint32_t i = 0; i < L.nprimes; ++i) args.mc[i] = L.mc[i];
 
     if (!L.progress) return cudaErrorInvalidValue;
@@ -796,7 +825,13 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, kernel_for(pt.si), ma, mb, a);
+        KernelFn kfn = kernel_for(pt.si, L.mode);
+        if (!kfn) return cudaErrorInvalidValue;
+        if (L.mode != kModePsq) {
+            e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+            if (e != cudaSuccess) return e;
+        }
+        e = cudaLaunchKernelEx(&cfg, kfn, ma, mb, a);
         if (e != cudaSuccess) return e;
     }
     if (nparts > 1) {

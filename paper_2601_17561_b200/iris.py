@@ -1,0 +1,135 @@
+"""Host mirror of the reference's plaintext iris scoring (irislab::iris,
+iris_core.hpp / iris_core.cpp, and the overlaps of pipeline::prepare,
+pipeline.cpp:92-153) on the B200 engine (C ABI irl_iris_*, csrc/iris.cu).
+
+Templates are numpy uint8 {0,1} arrays (code, mask) of length d, like the
+reference's IrisTemplate. Every sum is computed by the tcgen05 kernel; this
+module only packs bits (pack_bits, pipeline.cpp:70-76) and calls the ABI.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import capi
+from .modmat import Context, ShapeMismatch, ZeroOverlap, default_context
+
+
+@dataclass
+class IrisTemplate:
+    """iris_core.hpp: code and mask bits of the same length d."""
+    code: np.ndarray
+    mask: np.ndarray
+
+    def size(self) -> int:
+        return int(self.code.shape[0])
+
+    def validate(self):
+        # IrisTemplate::validate (iris_core.cpp:10-19)
+        if self.code.shape != self.mask.shape or self.code.size == 0:
+            raise ShapeMismatch("code and mask must have identical nonzero length")
+        if (self.code > 1).any() or (self.mask > 1).any():
+            raise ShapeMismatch("template entries must be bits")
+
+
+@dataclass
+class Interval:
+    lo: float = 0.0
+    hi: float = 0.0
+
+    def contains(self, x: float) -> bool:
+        return self.lo <= x <= self.hi
+
+
+def pack_bits(bits: np.ndarray) -> np.ndarray:
+    """[n][d] {0,1} -> [n][ceil(d/64)] uint64, bit i of a row at word i/64,
+    bit i%64 (pipeline.cpp:70-76)."""
+    bits = np.ascontiguousarray(bits, np.uint8)
+    n, d = bits.shape
+    words = (d + 63) // 64
+    padded = np.zeros((n, words * 64), np.uint8)
+    padded[:, :d] = bits
+    return np.packbits(padded.reshape(n, words, 8, 8)[:, :, ::-1, ::-1].reshape(n, words * 64),
+                       axis=1, bitorder="big").view(">u8").astype(np.uint64).reshape(n, words)
+
+
+def _stack(ts: Sequence[IrisTemplate]):
+    d = ts[0].size() if ts else 0
+    for t in ts:
+        if t.size() != d:
+            raise ShapeMismatch("template lengths differ")
+    code = np.stack([t.code for t in ts]).astype(np.uint8) if ts else np.zeros((0, d), np.uint8)
+    mask = np.stack([t.mask for t in ts]).astype(np.uint8) if ts else np.zeros((0, d), np.uint8)
+    return pack_bits(code), pack_bits(mask), d
+
+
+def _p(a):
+    return capi.ptr(a) if a is not None and a.size else None
+
+
+def inner_overlap(db: Sequence[IrisTemplate], eyes: Sequence[IrisTemplate], rho: int = 1,
+                  ctx: Optional[Context] = None):
+    """(inner, overlap), each int32 [len(eyes)*rho][len(db)]: for query column
+    c = e*rho + r (rotate(eyes[e], r)) and template j, inner = <a', b'> and
+    overlap = |m_a AND m_b| (iris_core.cpp:37-51; pipeline.cpp:78-82, 140-151)."""
+    ctx = ctx or default_context()
+    dc, dm, d = _stack(db)
+    qc, qm, dq = _stack(eyes)
+    if db and eyes and d != dq:
+        raise ShapeMismatch("template lengths differ")
+    d = d or dq
+    cols = len(eyes) * rho
+    inner = np.zeros((cols, len(db)), np.int32)
+    ovl = np.zeros((cols, len(db)), np.int32)
+    ctx.check(capi.lib().irl_iris_inner_overlap(ctx.handle, _p(dc), _p(dm), len(db), _p(qc), _p(qm),
+                                                len(eyes), rho, d, _p(inner), _p(ovl)))
+    return inner, ovl
+
+
+def match_eyes(db: Sequence[IrisTemplate], eyes: Sequence[IrisTemplate], rho: int, p_int: Interval,
+               ctx: Optional[Context] = None, want_scores: bool = False):
+    """Per eye e: match_db_reference([rotate(eyes[e], r) for r < rho], db, ., p_int)
+    as 1 / 0 / -1 (ZeroOverlap); per-(eye, template) match bits; optional
+    scores [cols][n_db] (NaN where the overlap is empty). Does not raise."""
+    ctx = ctx or default_context()
+    dc, dm, d = _stack(db)
+    qc, qm, dq = _stack(eyes)
+    if db and eyes and d != dq:
+        raise ShapeMismatch("template lengths differ")
+    d = d or dq
+    bits = np.zeros((len(eyes), len(db)), np.uint8)
+    res = np.zeros(len(eyes), np.int32)
+    sc = np.zeros((len(eyes) * rho, len(db)), np.float64) if want_scores else None
+    st = capi.lib().irl_iris_match(ctx.handle, _p(dc), _p(dm), len(db), _p(qc), _p(qm), len(eyes), rho, d,
+                                   float(p_int.lo), float(p_int.hi), _p(bits), _p(res), _p(sc))
+    if st not in (capi.IRL_OK, capi.IRL_ERR_ZERO_OVERLAP):
+        ctx.check(st)
+    return res, bits, sc
+
+
+def match_db_reference(query: Sequence[IrisTemplate], db: Sequence[IrisTemplate], n_int: Interval,
+                       p_int: Interval, ctx: Optional[Context] = None) -> bool:
+    """iris::match_db_reference (iris_core.cpp:78-90): True at the first
+    (query, entry) score in p_int, ZeroOverlap if an empty overlap comes first
+    in that loop order, else False."""
+    if not query or not db:
+        return False
+    res, _, _ = match_eyes(db, query, 1, p_int, ctx)
+    for r in res:  # query-major order: the first eye with an event decides
+        if r == 1:
+            return True
+        if r == -1:
+            raise ZeroOverlap("mask overlap is empty, score undefined")
+    return False
+
+
+def score(a: IrisTemplate, b: IrisTemplate, ctx: Optional[Context] = None) -> float:
+    """iris::score (iris_core.cpp:55-59)."""
+    if a.size() != b.size():
+        raise ShapeMismatch("template lengths differ")
+    inner, ovl = inner_overlap([b], [a], 1, ctx)
+    if ovl[0, 0] == 0:
+        raise ZeroOverlap("mask overlap is empty, score undefined")
+    return float(inner[0, 0]) / float(ovl[0, 0])

@@ -41,6 +41,10 @@ class ModulusBudget(Error):
     pass
 
 
+class ZeroOverlap(Error):
+    """errors.hpp:18-20: mask overlap is empty, score undefined."""
+
+
 class DeviceError(Error):
     """CUDA / device failures (no reference counterpart)."""
 
@@ -51,6 +55,7 @@ _STATUS_EXC = {
     capi.IRL_ERR_ACCUMULATION_OVERFLOW_RISK: AccumulationOverflowRisk,
     capi.IRL_ERR_NOT_COPRIME: Error,
     capi.IRL_ERR_MODULUS_BUDGET: ModulusBudget,
+    capi.IRL_ERR_ZERO_OVERLAP: ZeroOverlap,
 }
 
 

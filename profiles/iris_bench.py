@@ -1,0 +1,60 @@
+"""Times the plaintext iris scoring stage (irl_iris_match) at the paper's
+scale: 7 * 2^14 templates, 32 eyes x 31 rotations, d = 2^14, host buffers in
+and out (H2D of the packed templates inside the timed region).
+
+    python profiles/iris_bench.py [--n-db 114688] [--eyes 32] [--rho 31] [--d 16384]
+"""
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n-db", type=int, default=7 << 14)
+    ap.add_argument("--eyes", type=int, default=32)
+    ap.add_argument("--rho", type=int, default=31)
+    ap.add_argument("--d", type=int, default=1 << 14)
+    ap.add_argument("--reps", type=int, default=5)
+    a = ap.parse_args()
+    import ctypes as C
+    from paper_2601_17561_b200 import capi
+    from paper_2601_17561_b200.iris import pack_bits
+    from paper_2601_17561_b200.modmat import default_context
+    ctx = default_context()
+    rng = np.random.default_rng(1)
+    dc = pack_bits(rng.integers(0, 2, (a.n_db, a.d), dtype=np.uint8))
+    dm = pack_bits((rng.random((a.n_db, a.d)) < 0.8).astype(np.uint8))
+    qc = pack_bits(rng.integers(0, 2, (a.eyes, a.d), dtype=np.uint8))
+    qm = pack_bits((rng.random((a.eyes, a.d)) < 0.8).astype(np.uint8))
+    bits = np.zeros((a.eyes, a.n_db), np.uint8)
+    res = np.zeros(a.eyes, np.int32)
+    L = capi.lib()
+    p = capi.ptr
+
+    def run():
+        st = L.irl_iris_match(ctx.handle, p(dc), p(dm), a.n_db, p(qc), p(qm), a.eyes, a.rho, a.d, 0.35, 1.0,
+                              p(bits), p(res), None)
+        assert st in (0, capi.IRL_ERR_ZERO_OVERLAP), st
+
+    run()
+    ts = []
+    for _ in range(a.reps):
+        t0 = time.perf_counter()
+        run()
+        ts.append(time.perf_counter() - t0)
+    ms = float(np.median(ts) * 1e3)
+    ops = 4.0 * a.n_db * a.eyes * a.rho * a.d  # two int8 GEMMs, 2 ops / MAC
+    print(json.dumps({"stage": "iris_match (overlaps + inner + scores + match bits)", "n_db": a.n_db,
+                      "cols": a.eyes * a.rho, "d": a.d, "ms_e2e": ms, "tops_e2e": ops / ms / 1e9,
+                      "h2d_bytes": int(dc.nbytes * 2 + qc.nbytes * 2), "matches": int(bits.sum())}))
+
+
+if __name__ == "__main__":
+    main()

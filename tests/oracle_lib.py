@@ -60,6 +60,7 @@ def oracle() -> C.CDLL:
         lib.orc_ppmm_rows_direct.argtypes = [u16p, sz, u16p, sz, u32p, sz, sz, sz, C.c_uint32, u16p]
         lib.orc_synth_residue.restype = C.c_uint32
         lib.orc_synth_residue.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]
+        lib.orc_iris_inner_overlap.argtypes = [u8p, u8p, sz, u8p, u8p, sz, sz, sz, i32p, i32p]
         lib.orc_synth_block.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                         C.c_uint32, C.c_uint32, C.c_uint32, u16p]
         _oracle = lib
@@ -96,6 +97,12 @@ def ref() -> C.CDLL:
         lib.ref_save_load_roundtrip.argtypes = [C.c_char_p, u8p, sz, sz, sz, u8p]
         lib.ref_synth_masked.argtypes = [sz, sz, C.c_double, C.c_uint64, i8p]
         lib.ref_synth_masked_rotated.argtypes = [sz, sz, C.c_double, C.c_uint64, sz, i8p]
+        lib.ref_synth_templates.argtypes = [sz, sz, C.c_double, C.c_uint64, u8p, u8p]
+        f64p = C.POINTER(C.c_double)
+        lib.ref_iris_scores.argtypes = [u8p, u8p, sz, u8p, u8p, sz, sz, f64p]
+        lib.ref_iris_rotate.argtypes = [u8p, u8p, sz, sz, u8p, u8p]
+        lib.ref_match_db_reference.argtypes = [u8p, u8p, sz, u8p, u8p, sz, sz, C.c_double, C.c_double,
+                                               C.c_double, C.c_double, C.POINTER(C.c_int)]
         _ref = lib
     return _ref
 
@@ -225,3 +232,61 @@ def ppmm_rows_direct(a: np.ndarray, bt: np.ndarray, rows, m: int):
     oracle().orc_ppmm_rows_direct(ptr(a, u16p), a.shape[1], ptr(bt, u16p), K, ptr(rows, u32p),
                                   len(rows), N, K, m, ptr(out, u16p))
     return out
+
+
+# --------------------------------------------------------------------------
+# Plaintext iris scoring (oracle restatement + reference wrappers)
+# --------------------------------------------------------------------------
+
+def iris_inner_overlap(db_code, db_mask, q_code, q_mask, rho):
+    """Oracle: int32 inner, overlap [n_eyes*rho][n_db] (iris_core.cpp:37-51)."""
+    db_code, db_mask = (np.ascontiguousarray(x, np.uint8) for x in (db_code, db_mask))
+    q_code, q_mask = (np.ascontiguousarray(x, np.uint8) for x in (q_code, q_mask))
+    n_db, d = db_code.shape
+    ne = q_code.shape[0]
+    inner = np.zeros((ne * rho, n_db), np.int32)
+    ovl = np.zeros((ne * rho, n_db), np.int32)
+    oracle().orc_iris_inner_overlap(ptr(db_code, u8p), ptr(db_mask, u8p), n_db, ptr(q_code, u8p),
+                                    ptr(q_mask, u8p), ne, rho, d, ptr(inner, i32p), ptr(ovl, i32p))
+    return inner, ovl
+
+
+def ref_synth_templates(n, d, density, seed):
+    code = np.zeros((n, d), np.uint8)
+    mask = np.zeros((n, d), np.uint8)
+    st = ref().ref_synth_templates(n, d, density, seed, ptr(code, u8p), ptr(mask, u8p))
+    assert st == 0
+    return code, mask
+
+
+def ref_rotate(code, mask, r):
+    d = code.shape[0]
+    oc, om = np.zeros(d, np.uint8), np.zeros(d, np.uint8)
+    code, mask = np.ascontiguousarray(code, np.uint8), np.ascontiguousarray(mask, np.uint8)
+    ref().ref_iris_rotate(ptr(code, u8p), ptr(mask, u8p), d, r, ptr(oc, u8p), ptr(om, u8p))
+    return oc, om
+
+
+def ref_scores(q_code, q_mask, db_code, db_mask):
+    nq, d = q_code.shape
+    n_db = db_code.shape[0]
+    out = np.zeros((nq, n_db), np.float64)
+    args = [np.ascontiguousarray(x, np.uint8) for x in (q_code, q_mask, db_code, db_mask)]
+    st = ref().ref_iris_scores(ptr(args[0], u8p), ptr(args[1], u8p), nq, ptr(args[2], u8p), ptr(args[3], u8p),
+                               n_db, d, out.ctypes.data_as(C.POINTER(C.c_double)))
+    assert st == 0
+    return out
+
+
+def ref_match(q_code, q_mask, db_code, db_mask, p_lo, p_hi, n_lo=-1.0, n_hi=0.1):
+    """-> 1 / 0, or -1 for ZeroOverlap (status 11)."""
+    nq, d = q_code.shape
+    n_db = db_code.shape[0]
+    args = [np.ascontiguousarray(x, np.uint8) for x in (q_code, q_mask, db_code, db_mask)]
+    out = C.c_int(0)
+    st = ref().ref_match_db_reference(ptr(args[0], u8p), ptr(args[1], u8p), nq, ptr(args[2], u8p),
+                                      ptr(args[3], u8p), n_db, d, n_lo, n_hi, p_lo, p_hi, C.byref(out))
+    if st == 11:
+        return -1
+    assert st == 0, st
+    return out.value
