@@ -152,7 +152,10 @@ int irl_ccmm_load_part_bigint(irl_ccmm* e, size_t part, const uint8_t* entries, 
  * i, row, col, m_i); first_part is the global id of local part 0 (multi-GPU). */
 int irl_ccmm_synth_db(irl_ccmm* e, uint64_t seed, uint32_t first_part);
 /* End-to-end call with HOST buffers: q_res [nmod][K][N] -> out [parts][nmod][N][M].
- * Copies in, splits, multiplies every part, copies out; blocks. */
+ * Copies in, splits, multiplies every part, copies out; blocks. N may exceed
+ * max_n: the batch then streams through the engine in column chunks
+ * (max_n rounded down to whole 256-column tiles), e.g. the c5 corner of 256
+ * eyes x 31 rotations against 2^17-template slices. */
 int irl_ccmm_run(irl_ccmm* e, const uint16_t* q_res_host, size_t n, uint16_t* out_host);
 /* Device-resident variant over parts [part0, part0 + nparts): q_res_dev
  * [nmod][K][N] (split into the engine's query planes unless q_ready != 0),

@@ -899,13 +899,12 @@ int irl_ccmm_run_device(irl_ccmm* e, const uint16_t* q_res_dev, int q_ready, siz
     return ccmm_parts(e, n, part0, nparts, out_dev, s);
 }
 
-int irl_ccmm_run(irl_ccmm* e, const uint16_t* q_res_host, size_t n, uint16_t* out_host) {
-    if (!e) return IRL_ERR_INVALID_ARGUMENT;
+// One column chunk [n0, n0 + w) of an e2e run (query columns of the host
+// batch of width n), pipelined by modulus chunks: H2D of chunk c+1 and D2H of
+// chunk c-1 run on their own streams while chunk c is split and multiplied.
+static int ccmm_run_columns(irl_ccmm* e, const uint16_t* q_res_host, size_t n, size_t n0, size_t w,
+                            uint16_t* out_host) {
     irl_ctx* ctx = e->ctx;
-    Guard g(ctx);
-    if (n == 0 || n > e->max_n) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: query width out of range");
-    // Pipelined by modulus chunks: H2D of chunk c+1 and D2H of chunk c-1 run
-    // on their own streams while chunk c is split and multiplied.
     cudaStream_t s = ctx->stream;
     const size_t nmod = e->nmod, K = e->K, M = e->M;
     const size_t chunk = (nmod + 7) / 8;
@@ -913,8 +912,9 @@ int irl_ccmm_run(irl_ccmm* e, const uint16_t* q_res_host, size_t n, uint16_t* ou
     IRL_CK(ctx, cudaStreamWaitEvent(e->h2d_stream, e->part_done[0], 0));
     for (size_t c0 = 0, ci = 0; c0 < nmod; c0 += chunk, ++ci) {
         const size_t nc = std::min(chunk, nmod - c0);
-        IRL_CK(ctx, cudaMemcpyAsync(e->qres + c0 * K * n, q_res_host + c0 * K * n, nc * K * n * 2,
-                                    cudaMemcpyHostToDevice, e->h2d_stream));
+        // rows (modulus, k) of the host [nmod][K][n] batch, columns [n0, n0 + w)
+        IRL_CK(ctx, cudaMemcpy2DAsync(e->qres + c0 * K * w, w * 2, q_res_host + c0 * K * n + n0, n * 2, w * 2,
+                                      nc * K, cudaMemcpyHostToDevice, e->h2d_stream));
         IRL_CK(ctx, cudaEventRecord(e->h2d_done[ci], e->h2d_stream));
     }
     for (size_t c0 = 0, ci = 0; c0 < nmod; c0 += chunk, ++ci) {
@@ -923,20 +923,36 @@ int irl_ccmm_run(irl_ccmm* e, const uint16_t* q_res_host, size_t n, uint16_t* ou
         ModTable sub{};
         sub.n = uint32_t(nc);
         for (size_t i = 0; i < nc; ++i) sub.mc[i] = e->mt.mc[c0 + i];
-        IRL_LAUNCH(ctx, launch_split_cols<uint16_t>(e->qres + c0 * K * n, n, K * n, uint32_t(K), uint32_t(n), sub,
-                                                    e->qplanes + c0 * 2 * n * e->ldk, e->ldk, nullptr, s));
-        int st = ccmm_parts(e, n, 0, e->parts, e->out, s, c0, nc);
+        IRL_LAUNCH(ctx, launch_split_cols<uint16_t>(e->qres + c0 * K * w, w, K * w, uint32_t(K), uint32_t(w), sub,
+                                                    e->qplanes + c0 * 2 * w * e->ldk, e->ldk, nullptr, s));
+        int st = ccmm_parts(e, w, 0, e->parts, e->out, s, c0, nc);
         if (st) return st;
         IRL_CK(ctx, cudaEventRecord(e->part_done[ci], s));
         IRL_CK(ctx, cudaStreamWaitEvent(e->copy_stream, e->part_done[ci], 0));
         for (size_t p = 0; p < e->parts; ++p) {
-            const size_t off = (p * nmod + c0) * n * M;
-            IRL_CK(ctx, cudaMemcpyAsync(out_host + off, e->out + off, nc * n * M * 2, cudaMemcpyDeviceToHost,
-                                        e->copy_stream));
+            // device [p][i][w][M] -> host [p][i][n][M] at column n0
+            IRL_CK(ctx, cudaMemcpy2DAsync(out_host + ((p * nmod + c0) * n + n0) * M, n * M * 2,
+                                          e->out + (p * nmod + c0) * w * M, w * M * 2, w * M * 2, nc,
+                                          cudaMemcpyDeviceToHost, e->copy_stream));
         }
     }
     IRL_CK(ctx, cudaStreamSynchronize(e->copy_stream));
     IRL_CK(ctx, cudaStreamSynchronize(s));
+    return IRL_OK;
+}
+
+int irl_ccmm_run(irl_ccmm* e, const uint16_t* q_res_host, size_t n, uint16_t* out_host) {
+    if (!e) return IRL_ERR_INVALID_ARGUMENT;
+    irl_ctx* ctx = e->ctx;
+    Guard g(ctx);
+    if (n == 0) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: query width out of range");
+    // Query batches wider than the engine's staging capacity stream through it
+    // in column chunks (whole 256-column tiles when max_n allows).
+    size_t w = n <= e->max_n ? n : (e->max_n >= 256 ? e->max_n / 256 * 256 : e->max_n);
+    for (size_t n0 = 0; n0 < n; n0 += w) {
+        int st = ccmm_run_columns(e, q_res_host, n, n0, std::min(w, n - n0), out_host);
+        if (st) return st;
+    }
     return IRL_OK;
 }
 

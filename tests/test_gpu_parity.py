@@ -190,6 +190,21 @@ def test_ccmm_load_part_equals_synth():
     assert (eng2.run(q) == want).all()
 
 
+@pytest.mark.parametrize("max_n,n", [(256, 600), (100, 333), (64, 64)])
+def test_ccmm_column_chunked_run(max_n, n):
+    # query batches wider than the engine's staging capacity (c5: 256 eyes)
+    # stream through it in column chunks; result identical to one wide engine
+    from paper_2601_17561_b200.ccmm import CcmmEngine, synth_query
+    eng = CcmmEngine(parts=2, m=280, k=900, max_n=max_n)
+    eng.synth_db(seed=3)
+    q = synth_query(4, eng.K, n, eng.moduli)
+    out = eng.run(q)
+    wide = CcmmEngine(parts=2, m=280, k=900, max_n=n)
+    wide.synth_db(seed=3)
+    assert (wide.run(q) == out).all()
+    _check_ccmm(eng, 3, q, out, np.array([0, 5, 279], np.uint32))
+
+
 @pytest.mark.slow
 def test_ccmm_slice_shape_sampled_rows():
     # c3 slice geometry (N_db = 2^14, K = d2 + N_qry = 24576, N = 32 x 31 = 992),
