@@ -73,6 +73,7 @@ struct __align__(64) GemmArgs {
     uint32_t M, N, K;
     uint32_t parts, nprimes;
     uint32_t m_blocks, n_blocks, units;
+    uint32_t n_chunks, chunk_tiles;   // a unit covers chunk_tiles n-tiles; n_chunks of them span N
     uint32_t unit_mblocks;            // 256-row blocks per unit (the main launch's cluster_pm)
     uint32_t m_units;                 // units per (prime, part) = ceil(m_blocks / unit_mblocks)
     // group schedule (see group_of): G = clusters per full group
@@ -117,19 +118,25 @@ struct TileCoord {
     uint32_t prime, part, m0, n0, n_size;
 };
 
-// A unit is `unit_mblocks` consecutive 256-row blocks of one (prime, part);
-// units are prime-major so a prime's query planes stay L2-resident while its
-// units are in flight. A tile is (unit, m-block within the unit, n-tile).
+// A unit is `unit_mblocks` consecutive 256-row blocks x one n-chunk
+// (chunk_tiles n-tiles) of one (prime, part). Units are ordered prime, part,
+// n-chunk, m-block (fastest): the units in flight at once share one n-chunk
+// of a prime's query planes, which stays L2-resident while the database
+// streams through once per n-chunk. A tile is (unit, m-block within the unit,
+// n-tile within the chunk). Tiles past N (padding of the last chunk) get
+// n_size 32 and store nothing.
 __device__ __forceinline__ TileCoord decode(const GemmArgs& a, uint32_t unit, uint32_t mb_sub,
                                             uint32_t nb) {
     TileCoord t;
     const uint32_t mu = unit % a.m_units;
-    const uint32_t pp = unit / a.m_units;
-    t.part = pp % a.parts;
-    t.prime = pp / a.parts;
+    uint32_t rest = unit / a.m_units;
+    const uint32_t nc = rest % a.n_chunks;
+    rest /= a.n_chunks;
+    t.part = rest % a.parts;
+    t.prime = rest / a.parts;
     t.m0 = (mu * a.unit_mblocks + mb_sub) * 2 * kRowsPerCta;
-    t.n0 = nb * kMaxTileN;
-    const uint32_t rem = a.N - t.n0;
+    t.n0 = (nc * a.chunk_tiles + nb) * kMaxTileN;
+    const uint32_t rem = a.N > t.n0 ? a.N - t.n0 : 1u;
     const uint32_t ns = rem < kMaxTileN ? rem : kMaxTileN;
     t.n_size = (ns + 31u) & ~31u;  // cta_group::2 kind::i8 needs N % 32 == 0
     return t;
@@ -237,7 +244,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             const uint32_t lead = args.gate_lead;
             const bool writer = rank == 0 && grp.member == 0;  // takes units for the group
             unsigned long long* mbox = args.mailbox + static_cast<size_t>(grp.id) * kMail;
-            const uint32_t tiles_per_unit = grp.solo ? args.n_blocks / kPN : 1;
+            const uint32_t tiles_per_unit = grp.solo ? args.chunk_tiles / kPN : 1;
             const uint32_t m_passes = args.unit_mblocks / kPM;
             uint32_t issued = 0;  // cumulative K blocks (comparable across the group)
             uint32_t seen = 0;    // last observed minimum of the peers' counters
@@ -718,10 +725,13 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
 
     int dev = 0;
     cudaGetDevice(&dev);
-    // cluster shape: needs n_blocks % pn == 0; falls back to a plain pair
+    // cluster shape: a multi-pair shape needs at least pn n-tiles; otherwise
+    // the widest shape that divides the n-tiles (1x2 or a plain pair)
     int si = shape_index(L.cluster_pm, L.cluster_pn);
     if (L.mode == kModeInner && si != 0) si = 2;  // inner-product mode is built for 1x1 and 1x4
-    if (si < 0 || args.n_blocks % kShapes[si].pn != 0) si = 0;
+    if (si < 0) si = 0;
+    if (args.n_blocks < static_cast<uint32_t>(kShapes[si].pn))
+        si = (L.mode == kModePsq && args.n_blocks % 2 == 0 && kShapes[si].pm == 1) ? 1 : 0;
     const uint32_t occ2 = max_active_clusters(0, dev);
     uint32_t occ_main = si == 0 ? occ2 : max_active_clusters(si, dev);
     if (occ_main == 0) {
@@ -732,7 +742,18 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     const Shape shp = kShapes[si];
     args.unit_mblocks = static_cast<uint32_t>(shp.pm);
     args.m_units = (args.m_blocks + args.unit_mblocks - 1) / args.unit_mblocks;
-    args.units = args.m_units * L.parts * L.nprimes;
+    // n-chunks: with multi-pair clusters a unit is one cluster-wide n-chunk
+    // (pn tiles; the last chunk padded); plain pairs keep the whole N per unit
+    // and split it over a gated group of pairs.
+    if (si != 0 && !std::getenv("IRL_PPMM_NO_NCHUNK")) {
+        args.chunk_tiles = static_cast<uint32_t>(shp.pn);
+        args.n_chunks = (args.n_blocks + args.chunk_tiles - 1) / args.chunk_tiles;
+    } else {
+        args.chunk_tiles = args.n_blocks;
+        args.n_chunks = 1;
+        if (si != 0 && args.n_blocks % shp.pn != 0) return cudaErrorInvalidValue;
+    }
+    args.units = args.m_units * args.n_chunks * L.parts * L.nprimes;
     args.accumulate = L.accumulate ? 1u : 0u;
     args.a_part_rows = static_cast<uint32_t>(a_part_rows);
     args.out_part = L.out_part_elems ? L.out_part_elems
@@ -761,7 +782,7 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     auto plan = [&](int s_idx, uint32_t max_cl) {
         const Shape sh = kShapes[s_idx];
         const uint32_t ppc = static_cast<uint32_t>(sh.pm * sh.pn);
-        const uint32_t G = args.n_blocks / sh.pn;
+        const uint32_t G = args.chunk_tiles / sh.pn;
         const uint64_t items = static_cast<uint64_t>(args.units) * G;
         uint32_t cl = static_cast<uint32_t>(std::min<uint64_t>(max_cl, items));
         if (L.max_clusters > 0) cl = std::min<uint32_t>(cl, L.max_clusters);
@@ -800,7 +821,7 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
         const Part& pt = parts[i];
         GemmArgs a = args;
         const Shape sh = kShapes[pt.si];
-        a.G = args.n_blocks / static_cast<uint32_t>(sh.pn);
+        a.G = args.chunk_tiles / static_cast<uint32_t>(sh.pn);
         a.F = pt.clusters / a.G;
         a.L = pt.clusters % a.G;
         a.active_clusters = pt.clusters;
