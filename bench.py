@@ -325,6 +325,24 @@ def main():
         tr = json.loads(tr_path.read_text())
         traffic = tr.get("bytes_per_part", 0) * statistics.mean(g_parts) or None
 
+    # ---- the query split (HBM-bound): 2 B read + 2 B written per (entry, modulus)
+    s0 = torch.cuda.Event(enable_timing=True)
+    s1 = torch.cuda.Event(enable_timing=True)
+    eng.run_device(None, N, None, part0=0, nparts=0, q_ready=False, stream=stream.cuda_stream)
+    s0.record(stream)
+    for _ in range(10):
+        eng.run_device(None, N, None, part0=0, nparts=0, q_ready=False, stream=stream.cuda_stream)
+    s1.record(stream)
+    torch.cuda.synchronize()
+    split_ms = s0.elapsed_time(s1) / 10
+    split_bytes = 4.0 * nmod * K * N
+    hbm_peak = float(peaks.get("hbm_gbs", 6457.4))
+    split_roof = {"bound": "hbm", "kernel": "split_cols_u16_vec_kernel", "launch_ms": split_ms,
+                  "achieved": split_bytes / (split_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                  "frac": split_bytes / (split_ms * 1e-3) / 1e9 / hbm_peak, "bytes_per_launch": split_bytes,
+                  "note": "10 back-to-back query splits, CUDA events; input and output (1.17 GB each) "
+                          "exceed L2"}
+
     # ---- end to end through the public C ABI with host buffers -------------
     e2e = None
     if not args.no_e2e:
@@ -385,6 +403,7 @@ def main():
                              "kernel": "ppmm_i8_sm100_kernel", "launch_ms": launch_ms,
                              "ops_per_launch": launch_ops, "peak_source": peak_src,
                              "frac_of_datasheet_4500": achieved / DATASHEET_INT8_TOPS},
+                "split_roofline": split_roof,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)

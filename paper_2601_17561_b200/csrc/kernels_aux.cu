@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <type_traits>
 
 #include "kernels_aux.cuh"
 
@@ -148,6 +150,97 @@ __global__ void __launch_bounds__(256) split_cols_kernel(const T* __restrict__ i
         *reinterpret_cast<uint4*>(p1) = make_uint4(a1[0], a1[1], a1[2], a1[3]);
     }
     if (stats) {
+        warp_max_atomic(m0, &stats->v[i][0]);
+        warp_max_atomic(m1, &stats->v[i][1]);
+        warp_max_atomic(mr, &stats->v[i][2]);
+    }
+}
+
+// Vectorised transposing split for uint16 residues (the per-step query
+// split, the dominant HBM kernel besides the GEMM). Tile 128 (k) x 64 (n):
+// each thread loads 4 rows x 8 columns as 16-byte vectors, packs the 4
+// k-bytes of every column into one word per plane in shared memory, and the
+// block writes 64 rows x 128 bytes per plane as 16-byte stores.
+// Needs N, ld_in and plane_stride multiples of 8 and a 16-byte aligned input.
+
+constexpr int kSplitTileDefault = 0;
+
+template <bool kStats, bool kOdd, int kVK, int kVN>
+__global__ void __launch_bounds__(256) split_cols_u16_vec_kernel(const uint16_t* __restrict__ in, size_t ld_in,
+                                                                 size_t plane_stride, uint32_t K, uint32_t N,
+                                                                 const __grid_constant__ ModTable mt,
+                                                                 int8_t* __restrict__ planes, size_t ldk,
+                                                                 SplitStats* stats) {
+    constexpr int kVW = kVK / 4 + 1;  // words per n-row (odd: conflict-light)
+    constexpr int kSlots = (kVK / 4) * (kVN / 8) / 256;
+    __shared__ uint32_t s0[kVN * kVW], s1[kVN * kVW];
+    const uint32_t i = blockIdx.z;
+    const ModConst c = mt.mc[i];
+    const uint32_t k0 = blockIdx.x * kVK, n0 = blockIdx.y * kVN;
+    const uint16_t* src = in + i * plane_stride;
+    int32_t m0 = 0, m1 = 0, mr = 0;
+    const uint32_t mm1 = c.magic_m + 1u, mp1 = c.magic_p + 1u, h = (c.p - 1) / 2;
+#pragma unroll
+    for (int sl = 0; sl < kSlots; ++sl) {
+    const uint32_t slot = threadIdx.x + 256 * sl;
+    const uint32_t kq = slot / (kVN / 8), v = slot % (kVN / 8);
+    const uint32_t n = n0 + 8 * v;
+    uint32_t w0[8], w1[8];
+    uint4 q[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const uint32_t k = k0 + 4 * kq + r;
+        q[r] = (k < K && n < N) ? __ldg(reinterpret_cast<const uint4*>(src + static_cast<size_t>(k) * ld_in + n))
+                                : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        int32_t d0[4], d1[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const uint32_t word = j < 2 ? (r == 0 ? q[0].x : r == 1 ? q[1].x : r == 2 ? q[2].x : q[3].x)
+                                : j < 4 ? (r == 0 ? q[0].y : r == 1 ? q[1].y : r == 2 ? q[2].y : q[3].y)
+                                : j < 6 ? (r == 0 ? q[0].z : r == 1 ? q[1].z : r == 2 ? q[2].z : q[3].z)
+                                        : (r == 0 ? q[0].w : r == 1 ? q[1].w : r == 2 ? q[2].w : q[3].w);
+            const uint32_t x = (j & 1) ? word >> 16 : word & 0xFFFFu;
+            if constexpr (kOdd) {  // every modulus of the launch is p^2 with p odd
+                const uint32_t vv = x - c.m * __umulhi(x, mm1);
+                digit_split_odd(vv, c.p, h, mp1, d0[r], d1[r]);
+            } else {
+                digit_split_u16(x, c, d0[r], d1[r]);
+            }
+            if constexpr (kStats) {
+                m0 = max(m0, abs(d0[r]));
+                m1 = max(m1, abs(d1[r]));
+                mr = max(mr, static_cast<int32_t>(x - c.m * __umulhi(x, mm1)));
+            }
+        }
+        // rows beyond K were zero-filled above and split to digits (0, 0)
+        w0[j] = __byte_perm(__byte_perm(d0[0], d0[1], 0x0040), __byte_perm(d0[2], d0[3], 0x0040), 0x5410);
+        w1[j] = __byte_perm(__byte_perm(d1[0], d1[1], 0x0040), __byte_perm(d1[2], d1[3], 0x0040), 0x5410);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        s0[(8 * v + j) * kVW + kq] = w0[j];
+        s1[(8 * v + j) * kVW + kq] = w1[j];
+    }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < kVN * (kVK / 16) / 256; ++it) {
+        const uint32_t idx = threadIdx.x + 256 * it;
+        const uint32_t row = idx / (kVK / 16), ch = idx % (kVK / 16);
+        const uint32_t nn = n0 + row, k = k0 + 16 * ch;
+        if (nn < N && k < ldk) {
+            const uint32_t* a0 = s0 + row * kVW + 4 * ch;
+            const uint32_t* a1 = s1 + row * kVW + 4 * ch;
+            int8_t* p0 = planes + (static_cast<size_t>(i) * 2 * N + nn) * ldk + k;
+            int8_t* p1 = p0 + static_cast<size_t>(N) * ldk;
+            *reinterpret_cast<uint4*>(p0) = make_uint4(a0[0], a0[1], a0[2], a0[3]);
+            *reinterpret_cast<uint4*>(p1) = make_uint4(a1[0], a1[1], a1[2], a1[3]);
+        }
+    }
+    if constexpr (kStats) {
         warp_max_atomic(m0, &stats->v[i][0]);
         warp_max_atomic(m1, &stats->v[i][1]);
         warp_max_atomic(mr, &stats->v[i][2]);
@@ -487,6 +580,32 @@ cudaError_t launch_split_cols(const T* in, size_t ld_in, size_t plane_stride, ui
                               uint32_t n, const ModTable& mt, int8_t* planes, size_t ldk,
                               SplitStats* stats, cudaStream_t s) {
     if (n == 0 || ldk == 0 || mt.n == 0) return cudaSuccess;
+    if constexpr (sizeof(T) == 2) {
+        if (n % 8 == 0 && ld_in % 8 == 0 && plane_stride % 8 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+            bool odd = true;
+            for (uint32_t i = 0; i < mt.n; ++i) odd &= mt.mc[i].e == 2 && (mt.mc[i].p & 1u);
+            static const int tile = [] {
+                const char* t = std::getenv("IRL_SPLIT_TILE");  // experiment knob: 0 128x64, 1 128x128, 2 256x64
+                return t ? std::atoi(t) : kSplitTileDefault;
+            }();
+            auto pick = [&](auto kvk, auto kvn) {
+                constexpr int KT = decltype(kvk)::value, NT = decltype(kvn)::value;
+                const dim3 g(blocks_for(ldk, KT), blocks_for(n, NT), mt.n);
+                auto kfn = stats ? (odd ? split_cols_u16_vec_kernel<true, true, KT, NT>
+                                        : split_cols_u16_vec_kernel<true, false, KT, NT>)
+                                 : (odd ? split_cols_u16_vec_kernel<false, true, KT, NT>
+                                        : split_cols_u16_vec_kernel<false, false, KT, NT>);
+                kfn<<<g, 256, 0, s>>>(in, ld_in, plane_stride, k, n, mt, planes, ldk, stats);
+            };
+            if (tile == 1)
+                pick(std::integral_constant<int, 128>{}, std::integral_constant<int, 128>{});
+            else if (tile == 2)
+                pick(std::integral_constant<int, 256>{}, std::integral_constant<int, 64>{});
+            else
+                pick(std::integral_constant<int, 128>{}, std::integral_constant<int, 64>{});
+            return cudaGetLastError();
+        }
+    }
     const dim3 grid(blocks_for(ldk, kTT), blocks_for(n, kTT), mt.n);
     split_cols_kernel<T><<<grid, 256, 0, s>>>(in, ld_in, plane_stride, k, n, mt, planes, ldk, stats);
     return cudaGetLastError();

@@ -92,4 +92,40 @@ __device__ __forceinline__ void digit_split(uint32_t v, const ModConst& c, int32
     d1 = b;
 }
 
+// Fast centred split of a 16-bit input x (any value < 2^16, reduced mod m
+// first), ~12 integer instructions. floor(x / d) = umulhi(x, floor(2^32/d) + 1)
+// is exact for x < 2^16 and 2 <= d < 2^16: the rounding error x*delta/2^32 <
+// 2^-16 stays below 1/d, the smallest gap from frac(x/d) to 1.
+// d0 = centre(v mod p); v - d0 = p * (q + carry) with q = floor(v / p) and
+// carry = [v mod p > (p-1)/2], so d1 = centre((q + carry) mod p) where
+// q + carry <= p (the value p maps to 0, which centring also yields).
+__device__ __forceinline__ void digit_split_u16(uint32_t x, const ModConst& c, int32_t& d0, int32_t& d1) {
+    const uint32_t v = x - c.m * __umulhi(x, c.magic_m + 1u);
+    const int32_t p = static_cast<int32_t>(c.p);
+    const int32_t half = (p - 1) / 2;
+    if (c.e == 2) {
+        const uint32_t q = __umulhi(v, c.magic_p + 1u);
+        const int32_t r = static_cast<int32_t>(v - q * c.p);
+        const bool up = r > half;
+        d0 = up ? r - p : r;
+        const int32_t q1 = static_cast<int32_t>(q) + (up ? 1 : 0);
+        d1 = q1 > half ? q1 - p : q1;
+    } else {
+        const int32_t r = static_cast<int32_t>(v);
+        d0 = r > half ? r - p : r;
+        d1 = 0;
+    }
+}
+
+// Odd-p variant of digit_split_u16 with the centring folded into the
+// quotient: for odd p, centre(a) = ((a + h) mod p) - h with h = (p-1)/2, so
+// q1 = floor((v + h) / p) and d0 = v - p q1 directly, and d1 = centre(q1)
+// with q1 <= p. Inputs v < p^2 (already reduced). ~7 instructions.
+__device__ __forceinline__ void digit_split_odd(uint32_t v, uint32_t p, uint32_t h, uint32_t magic_p1,
+                                                int32_t& d0, int32_t& d1) {
+    const uint32_t q1 = __umulhi(v + h, magic_p1);
+    d0 = static_cast<int32_t>(v - q1 * p);
+    d1 = static_cast<int32_t>(q1 > h ? q1 - p : q1);
+}
+
 }  // namespace irl

@@ -299,3 +299,54 @@ def test_ccmm_twin_pipeline_sizes_exact():
     prod = (db.astype(np.int64) @ qry.astype(np.int64))
     want = prod.T.reshape(d3, d1 // d2, d2).reshape(-1, d2)  # ct(c, b).message[i] = prod[(b n_db + i), c]
     assert (out.messages == want).all()
+
+
+@pytest.mark.parametrize("basis_kind", ["paper", "mixed"])
+@pytest.mark.parametrize("k,n", [(300, 64), (130, 992), (77, 70), (5, 8)])
+def test_split_cols_u16_all_paths(basis_kind, k, n):
+    # The query split (irl_split_cols_u16): vectorised kernel (N % 8 == 0; odd
+    # p^2 bases take the folded-centring fast path, others the general one)
+    # and the scalar kernel; raw uint16 inputs over the full 16-bit range so
+    # the reduction mod m is exercised. Digits follow digit_decompose
+    # (modmat.cpp:86-106); e = 1 moduli keep one centred digit.
+    import ctypes as C
+    import torch
+    from paper_2601_17561_b200 import capi
+    from paper_2601_17561_b200.modmat import default_context
+    if basis_kind == "paper":
+        primes, exps = ol.paper_basis()
+    else:
+        primes = np.array([2, 2, 3, 251, 127, 5], np.uint32)
+        exps = np.array([1, 2, 2, 1, 2, 2], np.uint32)
+    nmod = len(primes)
+    rng = np.random.default_rng(k * 1000 + n)
+    res = rng.integers(0, 65536, (nmod, k, n), dtype=np.uint32).astype(np.uint16)
+    ldk = (k + 15) // 16 * 16
+    dres = torch.from_numpy(res.view(np.int16)).cuda()
+    planes = torch.full((nmod, 2, n, ldk), 77, dtype=torch.int8, device="cuda")
+    ctx = default_context()
+    ctx.check(capi.lib().irl_split_cols_u16(ctx.handle, C.c_void_p(dres.data_ptr()), n, k * n, k, n,
+                                            capi.ptr(primes, capi.u32p), capi.ptr(exps, capi.u32p), nmod,
+                                            C.c_void_p(planes.data_ptr()), ldk, None))
+    torch.cuda.synchronize()
+    got = planes.cpu().numpy()
+    for i in range(nmod):
+        p, e = int(primes[i]), int(exps[i])
+        x = res[i].astype(np.int64).T  # [n][k]
+        half = (p - 1) // 2
+        if e == 2:
+            d0 = np.zeros(x.shape, np.int32)
+            d1 = np.zeros(x.shape, np.int32)
+            flat = np.ascontiguousarray(x.reshape(-1).astype(np.int32))
+            a0 = np.zeros_like(flat)
+            a1 = np.zeros_like(flat)
+            assert ol.oracle().orc_digit_decompose(ol.ptr(flat, ol.i32p), flat.size, p, ol.ptr(a0, ol.i32p),
+                                                   ol.ptr(a1, ol.i32p)) == 0
+            d0, d1 = a0.reshape(x.shape), a1.reshape(x.shape)
+        else:
+            a = x % p
+            d0 = np.where(a > half, a - p, a)
+            d1 = np.zeros_like(d0)
+        assert (got[i, 0, :, :k] == d0).all(), (basis_kind, i)
+        assert (got[i, 1, :, :k] == d1).all(), (basis_kind, i)
+        assert (got[i, :, :, k:] == 0).all()
