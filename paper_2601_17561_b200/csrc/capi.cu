@@ -907,18 +907,36 @@ static int ccmm_run_columns(irl_ccmm* e, const uint16_t* q_res_host, size_t n, s
     irl_ctx* ctx = e->ctx;
     cudaStream_t s = ctx->stream;
     const size_t nmod = e->nmod, K = e->K, M = e->M;
-    const size_t chunk = (nmod + 7) / 8;
+    // Modulus chunks graded 1, 2, 3, ..., 3, 2, 1: the first H2D and the last
+    // D2H (the unhidden head and tail of the pipeline) move one modulus.
+    std::vector<size_t> bounds{0};
+    {
+        std::vector<size_t> sizes;
+        size_t left = nmod;
+        for (size_t g : {1, 2})
+            if (left > 2 * g) sizes.push_back(g), left -= g;
+        std::vector<size_t> tail;
+        for (size_t g : {1, 2})
+            if (left > g + 2) tail.push_back(g), left -= g;
+        while (left > 0) {
+            const size_t g = std::min<size_t>(3, left);
+            sizes.push_back(g);
+            left -= g;
+        }
+        sizes.insert(sizes.end(), tail.rbegin(), tail.rend());
+        for (size_t g : sizes) bounds.push_back(bounds.back() + g);
+    }
     IRL_CK(ctx, cudaEventRecord(e->part_done[0], s));  // order after prior work on s
     IRL_CK(ctx, cudaStreamWaitEvent(e->h2d_stream, e->part_done[0], 0));
-    for (size_t c0 = 0, ci = 0; c0 < nmod; c0 += chunk, ++ci) {
-        const size_t nc = std::min(chunk, nmod - c0);
+    for (size_t ci = 0; ci + 1 < bounds.size(); ++ci) {
+        const size_t c0 = bounds[ci], nc = bounds[ci + 1] - c0;
         // rows (modulus, k) of the host [nmod][K][n] batch, columns [n0, n0 + w)
         IRL_CK(ctx, cudaMemcpy2DAsync(e->qres + c0 * K * w, w * 2, q_res_host + c0 * K * n + n0, n * 2, w * 2,
                                       nc * K, cudaMemcpyHostToDevice, e->h2d_stream));
         IRL_CK(ctx, cudaEventRecord(e->h2d_done[ci], e->h2d_stream));
     }
-    for (size_t c0 = 0, ci = 0; c0 < nmod; c0 += chunk, ++ci) {
-        const size_t nc = std::min(chunk, nmod - c0);
+    for (size_t ci = 0; ci + 1 < bounds.size(); ++ci) {
+        const size_t c0 = bounds[ci], nc = bounds[ci + 1] - c0;
         IRL_CK(ctx, cudaStreamWaitEvent(s, e->h2d_done[ci], 0));
         ModTable sub{};
         sub.n = uint32_t(nc);
