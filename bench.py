@@ -343,6 +343,25 @@ def main():
                   "note": "10 back-to-back query splits, CUDA events; input and output (1.17 GB each) "
                           "exceed L2"}
 
+    # ---- ModDown of the step's outputs (f2; HBM-bound): drop the last 3 moduli
+    drop = 3
+    md_dst = torch.empty((1, nmod - drop, N, M), dtype=torch.int16, device="cuda")
+    for p_ in range(local_parts.count):
+        eng.rescale(N, md_dst, drop, True, part0=p_, nparts=1, stream=stream.cuda_stream)
+    s0.record(stream)
+    for p_ in range(local_parts.count):
+        eng.rescale(N, md_dst, drop, True, part0=p_, nparts=1, stream=stream.cuda_stream)
+    s1.record(stream)
+    torch.cuda.synchronize()
+    md_ms = s0.elapsed_time(s1)
+    md_bytes = 2.0 * (2 * nmod - drop) * N * M * local_parts.count
+    moddown = {"bound": "hbm", "kernel": "rescale_kernel", "drop_moduli": drop, "ms_per_step": md_ms,
+               "achieved": md_bytes / (md_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+               "frac": md_bytes / (md_ms * 1e-3) / 1e9 / hbm_peak, "bytes": md_bytes,
+               "note": "not part of the CCMM step: f2 rescale of all local outputs to Q/Delta, "
+                       "Delta = product of the last 3 moduli (~2^47)"}
+    del md_dst
+
     # ---- end to end through the public C ABI with host buffers -------------
     e2e = None
     if not args.no_e2e:
@@ -403,7 +422,7 @@ def main():
                              "kernel": "ppmm_i8_sm100_kernel", "launch_ms": launch_ms,
                              "ops_per_launch": launch_ops, "peak_source": peak_src,
                              "frac_of_datasheet_4500": achieved / DATASHEET_INT8_TOPS},
-                "split_roofline": split_roof,
+                "split_roofline": split_roof, "moddown": moddown,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)

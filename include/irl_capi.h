@@ -118,6 +118,16 @@ int irl_ppmm_planes(irl_ctx* ctx, const int8_t* a_planes, const int8_t* b_planes
                     size_t parts, size_t m, size_t n, size_t k, size_t ldk,
                     const uint32_t* primes, const uint32_t* exps, size_t nmod, int accumulate,
                     void* stream);
+/* RNS rescale / ModDown toward Q / Delta (the
+ * CCMM result lives modulo ~Q/Delta). Delta = product of the LAST `drop`
+ * moduli (< 2^48). For every element e, the residues in[i*ld_in + e] of
+ * x mod Q (the CRT lift of modmat.cpp:178-193) become the residues
+ * out[i*ld_out + e], i < nmod - drop, of floor((x + (round ? floor(Delta/2) : 0)) / Delta)
+ * mod Q/Delta. Device pointers, stream-ordered. Inputs may be any uint16
+ * (reduced mod m_i first). Error("CRT basis is not coprime") as the lift. */
+int irl_rescale_residues(irl_ctx* ctx, const uint16_t* in, size_t ld_in, size_t count, const uint32_t* primes,
+                         const uint32_t* exps, size_t nmod, size_t drop, int round, uint16_t* out, size_t ld_out,
+                         void* stream);
 /* CRT lift (modmat.cpp:178-193): residues [nmod][N][M] -> width-byte entries
  * of the M x N row-major result mod Q. */
 int irl_crt_lift(irl_ctx* ctx, const uint16_t* res, size_t m, size_t n, uint8_t* out,
@@ -179,6 +189,11 @@ int irl_ccmm_twin(irl_ctx* ctx, long d1, long d2, long d3, long n_db, long n_qry
                   double db_modulus_bits, double qry_modulus_bits, double scale_bits,
                   int out_level, int top_level, int out_slot_encoding, int out_ci,
                   const double* db, const double* qry, double* msgs);
+/* ModDown of the engine's outputs (after irl_ccmm_run_device wrote them to the
+ * engine buffer, n columns): parts [part0, part0 + nparts) of [parts][nmod][n][M]
+ * -> dst [nparts][nmod - drop][n][M] (device), see irl_rescale_residues. */
+int irl_ccmm_rescale(irl_ccmm* e, size_t n, size_t part0, size_t nparts, size_t drop, int round, uint16_t* dst,
+                     void* stream);
 /* Bytes of HBM the engine holds (planes + workspace). */
 uint64_t irl_ccmm_device_bytes(const irl_ccmm* e);
 

@@ -88,6 +88,15 @@ class CcmmEngine:
             self.handle, capi.ptr(q_res_dev) if q_res_dev is not None else None, int(q_ready), n,
             part0, nparts, capi.ptr(out_dev) if out_dev is not None else None, s))
 
+    def rescale(self, n: int, dst, drop: int, round_: bool = True, part0: int = 0,
+                nparts: Optional[int] = None, stream=None):
+        """ModDown (f2) of the engine outputs of the last device run: parts
+        [part0, part0 + nparts) -> dst [nparts][nmod - drop][n][M] (CUDA tensor)."""
+        nparts = self.parts - part0 if nparts is None else nparts
+        s = C.c_void_p(stream) if stream is not None else None
+        self.ctx.check(capi.lib().irl_ccmm_rescale(self.handle, n, part0, nparts, drop, int(round_),
+                                                   capi.ptr(dst), s))
+
     def close(self):
         if getattr(self, "handle", None):
             capi.lib().irl_ccmm_destroy(self.handle)

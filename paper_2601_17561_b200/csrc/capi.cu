@@ -712,6 +712,49 @@ int irl_crt_lift(irl_ctx* ctx, const uint16_t* res, size_t m, size_t n, uint8_t*
     return IRL_OK;
 }
 
+int irl_rescale_residues(irl_ctx* ctx, const uint16_t* in, size_t ld_in, size_t count, const uint32_t* primes,
+                         const uint32_t* exps, size_t nmod, size_t drop, int round, uint16_t* out, size_t ld_out,
+                         void* stream) {
+    if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
+    Guard g(ctx);
+    int st = validate_moduli(ctx, primes, exps, nmod);
+    if (st) return st;
+    if (drop == 0 || drop >= nmod) return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "rescale: need 0 < drop < nmod");
+    RescaleTable t{};
+    t.nmod = uint32_t(nmod);
+    t.drop = uint32_t(drop);
+    unsigned long long delta = 1;
+    for (size_t i = 0; i < nmod; ++i) {
+        t.m[i] = exps[i] == 2 ? primes[i] * primes[i] : primes[i];
+        t.magic[i] = static_cast<uint32_t>((1ull << 32) / t.m[i]);
+        t.c32[i] = static_cast<uint32_t>((1ull << 32) % t.m[i]);
+        if (i >= nmod - drop) {
+            if (delta >= (1ull << 48) / t.m[i])
+                return set_err(ctx, IRL_ERR_UNSUPPORTED, "rescale: Delta must stay below 2^48");
+            delta *= t.m[i];
+        }
+    }
+    t.delta = delta;
+    auto inv = [](unsigned long long a, uint32_t m, uint32_t* out) {
+        uint32_t v = 0;
+        if (!inv_mod(static_cast<uint32_t>(a % m), m, &v)) return false;
+        *out = v;
+        return true;
+    };
+    for (size_t i = 0; i < nmod; ++i) {
+        const uint32_t m = t.m[i];
+        t.add[i] = round ? static_cast<uint32_t>((delta / 2) % m) : 0;
+        if (i < nmod - drop) {
+            if (!inv(delta, m, &t.dinv[i])) return set_err(ctx, IRL_ERR_NOT_COPRIME, "CRT basis is not coprime");
+        } else {
+            t.cq[i] = delta / m;
+            if (!inv(t.cq[i], m, &t.cinv[i])) return set_err(ctx, IRL_ERR_NOT_COPRIME, "CRT basis is not coprime");
+        }
+    }
+    IRL_LAUNCH(ctx, launch_rescale(in, ld_in, count, t, out, ld_out, pick_stream(ctx, stream)));
+    return IRL_OK;
+}
+
 // ---------------------------------------------------------------------------
 // RGSW CCMM engine
 // ---------------------------------------------------------------------------
@@ -969,6 +1012,28 @@ int irl_ccmm_run(irl_ccmm* e, const uint16_t* q_res_host, size_t n, uint16_t* ou
     size_t w = n <= e->max_n ? n : (e->max_n >= 256 ? e->max_n / 256 * 256 : e->max_n);
     for (size_t n0 = 0; n0 < n; n0 += w) {
         int st = ccmm_run_columns(e, q_res_host, n, n0, std::min(w, n - n0), out_host);
+        if (st) return st;
+    }
+    return IRL_OK;
+}
+
+int irl_ccmm_rescale(irl_ccmm* e, size_t n, size_t part0, size_t nparts, size_t drop, int round, uint16_t* dst,
+                     void* stream) {
+    if (!e || !dst) return IRL_ERR_INVALID_ARGUMENT;
+    irl_ctx* ctx = e->ctx;
+    Guard g(ctx);
+    if (n == 0 || n > e->max_n || part0 + nparts > e->parts)
+        return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: rescale range out of range");
+    std::vector<uint32_t> primes(e->nmod), exps(e->nmod);
+    for (size_t i = 0; i < e->nmod; ++i) {
+        primes[i] = e->mt.mc[i].p;
+        exps[i] = e->mt.mc[i].e;
+    }
+    const size_t plane = n * e->M;
+    for (size_t p = 0; p < nparts; ++p) {
+        int st = irl_rescale_residues(ctx, e->out + (part0 + p) * e->nmod * plane, plane, plane, primes.data(),
+                                      exps.data(), e->nmod, drop, round, dst + p * (e->nmod - drop) * plane, plane,
+                                      stream);
         if (st) return st;
     }
     return IRL_OK;

@@ -248,6 +248,41 @@ __global__ void __launch_bounds__(256) split_cols_u16_vec_kernel(const uint16_t*
 }
 
 // ---------------------------------------------------------------------------
+// RNS rescale by Delta (ModDown, result modulo ~Q/Delta).
+// With x' = x + add (residue-wise, mod m_i): r = x' mod Delta from the
+// dropped residues by CRT (exact in 64 bits, Delta < 2^48), then for every
+// kept modulus y_i = (x'_i - r mod m_i) * Delta^-1 mod m_i, i.e. the residues
+// of floor(x' / Delta) (congruent mod Q/Delta even when x + add wraps Q).
+// One thread per element; reads nmod x 2 B, writes (nmod - drop) x 2 B.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) rescale_kernel(const uint16_t* __restrict__ in, size_t ld_in, size_t count,
+                                                      const __grid_constant__ RescaleTable t,
+                                                      uint16_t* __restrict__ out, size_t ld_out) {
+    const size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= count) return;
+    const uint32_t keep = t.nmod - t.drop;
+    unsigned long long r = 0;
+    for (uint32_t j = keep; j < t.nmod; ++j) {
+        const uint32_t m = t.m[j];
+        uint32_t x = mod_u32(in[j * ld_in + e], m, t.magic[j]) + t.add[j];
+        x = x >= m ? x - m : x;
+        const uint32_t u = mod_u32(x * t.cinv[j], m, t.magic[j]);  // < 2^32: x, cinv < 2^16
+        r += static_cast<unsigned long long>(u) * t.cq[j];            // < drop * Delta < 2^50
+    }
+    while (r >= t.delta) r -= t.delta;  // at most drop - 1 times
+    const uint32_t r_lo = static_cast<uint32_t>(r), r_hi = static_cast<uint32_t>(r >> 32);
+    for (uint32_t i = 0; i < keep; ++i) {
+        const uint32_t m = t.m[i];
+        uint32_t x = mod_u32(in[i * ld_in + e], m, t.magic[i]) + t.add[i];
+        x = x >= m ? x - m : x;
+        uint32_t rm = mod_u32(r_lo, m, t.magic[i]) + mod_u32(r_hi * t.c32[i], m, t.magic[i]);
+        rm = rm >= m ? rm - m : rm;
+        const uint32_t d = x >= rm ? x - rm : x + m - rm;
+        out[i * ld_out + e] = static_cast<uint16_t>(mod_u32(d * t.dinv[i], m, t.magic[i]));
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Big-integer residue extraction + split.
 // x mod m = sum_j b_j (256^j mod m) mod m; the sum stays < 2^30 for
 // width <= 48 and m <= 2^16, so one Barrett reduction finishes it.
@@ -642,6 +677,13 @@ cudaError_t launch_split_bigint(const uint8_t* in, uint32_t width, uint32_t rows
     }
     split_bigint_kernel<<<blocks_for(total, 256), 256, 0, s>>>(
         in, width, rows, cols, transpose, a, planes, ldk, dst_rows, dst_row0, raw_out, stats);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rescale(const uint16_t* in, size_t ld_in, size_t count, const RescaleTable& t, uint16_t* out,
+                           size_t ld_out, cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    rescale_kernel<<<blocks_for(count, 256), 256, 0, s>>>(in, ld_in, count, t, out, ld_out);
     return cudaGetLastError();
 }
 

@@ -65,6 +65,23 @@ struct CrtTable {
 cudaError_t launch_crt_lift(const uint16_t* res, uint32_t M, uint32_t N, const CrtTable& t,
                             uint8_t* out, cudaStream_t s);
 
+// Exact RNS rescale (ModDown) by Delta = product of the last `drop` moduli:
+// residues of x mod Q -> residues of floor((x + add) / Delta) mod Q / Delta
+// (add = floor(Delta / 2) rounds). in[i][count] (stride ld_in), out[i][count]
+// (stride ld_out) for the nmod - drop kept moduli. Delta < 2^48.
+struct RescaleTable {
+    uint32_t nmod, drop;
+    uint32_t m[kMaxModuli], magic[kMaxModuli];
+    uint32_t add[kMaxModuli];      // floor(Delta/2) mod m_i (0: floor)
+    uint32_t dinv[kMaxModuli];     // Delta^-1 mod m_i (kept moduli)
+    uint32_t c32[kMaxModuli];      // 2^32 mod m_i
+    uint32_t cinv[kMaxModuli];     // (Delta/m_j)^-1 mod m_j (dropped moduli)
+    unsigned long long cq[kMaxModuli];  // Delta / m_j (dropped moduli)
+    unsigned long long delta;
+};
+cudaError_t launch_rescale(const uint16_t* in, size_t ld_in, size_t count, const RescaleTable& t, uint16_t* out,
+                           size_t ld_out, cudaStream_t s);
+
 // Synthetic database planes: planes[g][i][d][r][ldk] from the counter RNG,
 // residue = synth(seed, stream=part0+g, plane=i, row, col, m_i).
 cudaError_t launch_synth_planes(uint64_t seed, uint32_t part0, uint32_t parts, uint32_t rows,

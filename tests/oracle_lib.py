@@ -290,3 +290,30 @@ def ref_match(q_code, q_mask, db_code, db_mask, p_lo, p_hi, n_lo=-1.0, n_hi=0.1)
         return -1
     assert st == 0, st
     return out.value
+
+
+def rescale_oracle(res, moduli, drop, round_):
+    """ModDown restated with Python integers (test-only, small cases): CRT lift
+    of each element (modmat.cpp:178-193), y = floor((x + h) / Delta) mod Q/Delta
+    with h = floor(Delta/2) if round_ else 0, residues mod the kept moduli.
+    res: [nmod][count] ints."""
+    moduli = [int(m) for m in moduli]
+    Q = 1
+    for m in moduli:
+        Q *= m
+    delta = 1
+    for m in moduli[len(moduli) - drop:]:
+        delta *= m
+    q2 = Q // delta
+    h = delta // 2 if round_ else 0
+    coef = []
+    for m in moduli:
+        qi = Q // m
+        coef.append(qi * pow(qi % m, -1, m))
+    out = np.zeros((len(moduli) - drop, res.shape[1]), np.uint16)
+    for e in range(res.shape[1]):
+        x = sum(int(res[i, e]) % m * c for i, (m, c) in enumerate(zip(moduli, coef))) % Q
+        y = ((x + h) % Q) // delta % q2
+        for i, m in enumerate(moduli[:len(moduli) - drop]):
+            out[i, e] = y % m
+    return out

@@ -350,3 +350,51 @@ def test_split_cols_u16_all_paths(basis_kind, k, n):
         assert (got[i, 0, :, :k] == d0).all(), (basis_kind, i)
         assert (got[i, 1, :, :k] == d1).all(), (basis_kind, i)
         assert (got[i, :, :, k:] == 0).all()
+
+
+@pytest.mark.parametrize("drop,round_", [(1, 0), (1, 1), (2, 1), (3, 0), (3, 1)])
+def test_rescale_residues_vs_bigint(drop, round_):
+    # f2: ModDown by the product of the last `drop` moduli, exact against
+    # Python big integers (CRT lift, floor / round division, re-reduction)
+    import ctypes as C
+    import torch
+    from paper_2601_17561_b200 import capi
+    from paper_2601_17561_b200.modmat import default_context
+    primes, exps = ol.paper_basis()
+    moduli = [int(p) ** int(e) for p, e in zip(primes, exps)]
+    nmod, count = len(moduli), 777
+    rng = np.random.default_rng(drop * 10 + round_)
+    res = np.stack([rng.integers(0, m, count) for m in moduli]).astype(np.uint16)
+    res[:, 0] = 0                                         # x = 0
+    res[:, 1] = [(m - 1) for m in moduli]                 # x = Q - 1 (wraps when rounding)
+    res[:, 2] = [65535 for m in moduli]                   # unreduced inputs
+    want = ol.rescale_oracle(res, moduli, drop, round_)
+    din = torch.from_numpy(res.view(np.int16)).cuda()
+    dout = torch.zeros((nmod - drop, count), dtype=torch.int16, device="cuda")
+    ctx = default_context()
+    ctx.check(capi.lib().irl_rescale_residues(ctx.handle, C.c_void_p(din.data_ptr()), count, count,
+                                              capi.ptr(primes, capi.u32p), capi.ptr(exps, capi.u32p), nmod, drop,
+                                              round_, C.c_void_p(dout.data_ptr()), count, None))
+    torch.cuda.synchronize()
+    assert (dout.cpu().numpy().view(np.uint16) == want).all()
+
+
+def test_ccmm_rescale_matches_bigint():
+    # f2 on the engine: ModDown of real CCMM outputs (drop 3, rounding)
+    import torch
+    from paper_2601_17561_b200.ccmm import CcmmEngine, staging_tensors, synth_query
+    eng = CcmmEngine(parts=2, m=300, k=500, max_n=40)
+    eng.synth_db(seed=9)
+    q = synth_query(3, eng.K, 40, eng.moduli)
+    qd, od = staging_tensors(eng, 40)
+    qd.copy_(torch.from_numpy(q.view(np.int16)))
+    eng.run_device(None, 40, None)
+    dst = torch.zeros((2, eng.nmod - 3, 40, 300), dtype=torch.int16, device="cuda")
+    eng.rescale(40, dst, 3, True)
+    torch.cuda.synchronize()
+    out = od.cpu().numpy().view(np.uint16)
+    got = dst.cpu().numpy().view(np.uint16)
+    for part in range(2):
+        cols = out[part][:, :3, :].reshape(eng.nmod, -1)  # 3 columns x 300 rows
+        want = ol.rescale_oracle(cols, eng.moduli, 3, True)
+        assert (got[part][:, :3, :].reshape(eng.nmod - 3, -1) == want).all()

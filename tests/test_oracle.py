@@ -230,3 +230,18 @@ def test_oracle_equals_reference_not_coprime():
     str_ = ol.ref().ref_gemm_mod_Q(ol.ptr(al, ol.u8p), ol.ptr(bl, ol.u8p), ol.ptr(cr, ol.u8p), 1, 2, 1, 1,
                                    ol.ptr(primes, ol.u32p), ol.ptr(exps, ol.u32p), 2)
     assert st == str_ == 4
+
+
+def test_rescale_oracle_bruteforce():
+    # the f2 ModDown restatement against exhaustive search on a tiny basis
+    moduli = [7, 9, 11, 13]
+    Q = 7 * 9 * 11 * 13
+    xs = np.arange(0, Q, 37)
+    res = np.array([[x % m for x in xs] for m in moduli])
+    for drop in (1, 2):
+        delta = int(np.prod(moduli[len(moduli) - drop:]))
+        for rnd in (0, 1):
+            got = ol.rescale_oracle(res, moduli, drop, rnd)
+            for e, x in enumerate(xs):
+                y = ((int(x) + (delta // 2 if rnd else 0)) % Q) // delta
+                assert [y % m for m in moduli[:len(moduli) - drop]] == got[:, e].tolist()
