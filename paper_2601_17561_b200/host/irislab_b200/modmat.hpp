@@ -114,5 +114,12 @@ void set_device(int device);
 /// Number of kernels the engine launched through the free functions.
 uint64_t kernel_launches();
 }  // namespace b200
+}  // namespace irislab
+struct irl_ctx;
+namespace irislab {
+namespace b200 {
+/// The process-wide device context behind the free functions (created lazily).
+irl_ctx* context();
+}  // namespace b200
 
 }  // namespace irislab

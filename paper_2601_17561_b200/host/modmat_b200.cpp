@@ -82,6 +82,7 @@ void set_device(int device) {
     g_device = device;
 }
 uint64_t kernel_launches() { return g_ctx ? irl_kernel_launches(g_ctx) : 0; }
+irl_ctx* context() { return ctx(); }
 }  // namespace b200
 
 namespace modmat {

@@ -10,6 +10,20 @@ import pytest
 ROOT = Path(__file__).resolve().parent.parent
 PKG = ROOT / "paper_2601_17561_b200"
 BIN = ROOT / "build" / "test_modmat_b200"
+BIN_IRIS = ROOT / "build" / "test_iris_b200"
+
+
+def _build_driver(src, out):
+    cmd = ["/usr/bin/g++", "-O2", "-std=c++17", f"-I{PKG / 'host'}", str(src), "-o", str(out), f"-L{PKG}",
+           "-lirl_b200", f"-L{ROOT / 'oracle'}", "-l:libirl_oracle.so", f"-Wl,-rpath,{PKG}",
+           f"-Wl,-rpath,{ROOT / 'oracle'}"]
+    subprocess.run(cmd, check=True)
+
+
+@pytest.fixture(scope="module")
+def iris_binary(binary):
+    _build_driver(ROOT / "tests/cpp/test_iris_b200.cpp", BIN_IRIS)
+    return BIN_IRIS
 
 
 @pytest.fixture(scope="module")
@@ -37,6 +51,21 @@ def test_cpp_mirror_builds_and_links(binary):
 @pytest.mark.gpu
 def test_cpp_mirror_reference_unit_suite(binary):
     r = subprocess.run([str(binary)], capture_output=True, text=True, timeout=600, cwd=ROOT / "build")
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failed" in r.stdout
+
+
+def test_cpp_iris_mirror_builds(iris_binary):
+    assert iris_binary.exists()
+    syms = subprocess.run(["nm", "-DC", str(PKG / "libirl_b200.so")], capture_output=True, text=True).stdout
+    for fn in ["irislab::iris::score", "irislab::iris::match_db_reference", "irislab::iris::inner_and_overlap"]:
+        assert fn in syms
+
+
+@pytest.mark.gpu
+def test_cpp_iris_mirror_reference_unit_suite(iris_binary):
+    r = subprocess.run([str(iris_binary)], capture_output=True, text=True, timeout=600, cwd=ROOT / "build")
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
