@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=32, help="DB rows per task in the CPU sample")
+    ap.add_argument("--no-int8-ref", action="store_true", help="skip the live cuBLASLt int8 comparison")
     return ap.parse_args()
 
 
@@ -408,6 +409,32 @@ def main():
                "sample": r["sample"], "seconds": r["seconds"], "bit_exact_vs_gpu": exact,
                "extrapolated_ccmm_latency_s": total_ops / (r["tops"] * 1e12)}
 
+    # ---- live library comparison: cuBLASLt int8 GEMM (torch._int_mm) on this box,
+    # same operand distribution, back to back for 3 s after the timed region
+    int8_ref = None
+    if rank == 0 and not args.no_int8_ref:
+        torch.cuda.set_stream(torch.cuda.default_stream())
+        A8 = torch.randint(-125, 126, (8192, 8192), dtype=torch.int8, device="cuda")
+        B8 = torch.randint(-125, 126, (8192, 8192), dtype=torch.int8, device="cuda").t()
+        for _ in range(3):
+            torch._int_mm(A8, B8)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        cnt, t0 = 0, time.time()
+        e0.record()
+        while time.time() - t0 < 3.0:
+            for _ in range(8):
+                torch._int_mm(A8, B8)
+            cnt += 8
+            torch.cuda.synchronize()
+        e1.record()
+        torch.cuda.synchronize()
+        int8_ref = {"library": "cuBLASLt int8 GEMM via torch._int_mm, 8192^3, operands uniform in [-125, 125]",
+                    "sustained_tops": 2.0 * 8192 ** 3 / (e0.elapsed_time(e1) / cnt) / 1e9,
+                    "note": "a plain int8 GEMM (1 product); the PPMM does 3 fused products + mod-p^2 epilogue"}
+        del A8, B8
+
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
@@ -422,7 +449,7 @@ def main():
                              "kernel": "ppmm_i8_sm100_kernel", "launch_ms": launch_ms,
                              "ops_per_launch": launch_ops, "peak_source": peak_src,
                              "frac_of_datasheet_4500": achieved / DATASHEET_INT8_TOPS},
-                "split_roofline": split_roof, "moddown": moddown,
+                "split_roofline": split_roof, "moddown": moddown, "int8_library_ref": int8_ref,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
