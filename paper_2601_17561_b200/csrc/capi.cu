@@ -751,6 +751,13 @@ int irl_rescale_residues(irl_ctx* ctx, const uint16_t* in, size_t ld_in, size_t 
             if (!inv(t.cq[i], m, &t.cinv[i])) return set_err(ctx, IRL_ERR_NOT_COPRIME, "CRT basis is not coprime");
         }
     }
+    for (size_t jj = 0; jj < drop && jj < 3; ++jj) {
+        const size_t j = nmod - drop + jj;
+        for (size_t i = 0; i < nmod - drop; ++i) {
+            const uint64_t v = (t.cq[j] % t.m[i]) * t.dinv[i] % t.m[i];
+            t.w[jj][i] = static_cast<uint32_t>((t.m[i] - v) % t.m[i]);
+        }
+    }
     IRL_LAUNCH(ctx, launch_rescale(in, ld_in, count, t, out, ld_out, pick_stream(ctx, stream)));
     return IRL_OK;
 }

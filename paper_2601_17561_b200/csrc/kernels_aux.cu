@@ -255,6 +255,68 @@ __global__ void __launch_bounds__(256) split_cols_u16_vec_kernel(const uint16_t*
 // of floor(x' / Delta) (congruent mod Q/Delta even when x + add wraps Q).
 // One thread per element; reads nmod x 2 B, writes (nmod - drop) x 2 B.
 // ---------------------------------------------------------------------------
+// Vectorised rescale: 8 consecutive elements per thread (16-byte loads and
+// stores per modulus plane), the CRT correction folded into one 64-bit
+// multiply-accumulate chain per kept modulus (RescaleTable::w).
+__device__ __forceinline__ uint32_t mod_u35(unsigned long long a, uint32_t m, uint32_t magic, uint32_t c32) {
+    // a < 2^35: (hi * (2^32 mod m) + lo) mod m with hi < 8
+    const uint32_t t = mod_u32(static_cast<uint32_t>(a), m, magic) + static_cast<uint32_t>(a >> 32) * c32;
+    return mod_u32(t, m, magic);
+}
+
+__global__ void __launch_bounds__(256) rescale_vec_kernel(const uint16_t* __restrict__ in, size_t ld_in, size_t groups,
+                                                          const __grid_constant__ RescaleTable t,
+                                                          uint16_t* __restrict__ out, size_t ld_out) {
+    const size_t g = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (g >= groups) return;
+    const size_t e0 = g * 8;
+    const uint32_t keep = t.nmod - t.drop;
+    uint32_t u[3][8];
+    unsigned long long S[8];
+#pragma unroll
+    for (int l = 0; l < 8; ++l) S[l] = 0;
+#pragma unroll
+    for (uint32_t jj = 0; jj < 3; ++jj) {
+        if (jj >= t.drop) {
+#pragma unroll
+            for (int l = 0; l < 8; ++l) u[jj][l] = 0;
+            continue;
+        }
+        const uint32_t j = keep + jj, m = t.m[j];
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(in + j * ld_in + e0));
+        const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int l = 0; l < 8; ++l) {
+            const uint32_t x = (qw[l / 2] >> (16 * (l % 2))) & 0xFFFFu;
+            uint32_t xa = x - m * __umulhi(x, t.magic[j] + 1u) + t.add[j];  // x mod m + add < 2m
+            xa = xa >= m ? xa - m : xa;
+            u[jj][l] = mod_u32(xa * t.cinv[j], m, t.magic[j]);  // xa, cinv < 2^16
+            S[l] += static_cast<unsigned long long>(u[jj][l]) * t.cq[j];
+        }
+    }
+    uint32_t k[8];
+#pragma unroll
+    for (int l = 0; l < 8; ++l) k[l] = (S[l] >= t.delta) + (S[l] >= 2 * t.delta);
+    for (uint32_t i = 0; i < keep; ++i) {
+        const uint32_t m = t.m[i], mg = t.magic[i], c32 = t.c32[i], dinv = t.dinv[i], ad = t.add[i];
+        const uint32_t w0 = t.w[0][i], w1 = t.w[1][i], w2 = t.w[2][i];
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(in + i * ld_in + e0));
+        const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
+        uint32_t y[8];
+#pragma unroll
+        for (int l = 0; l < 8; ++l) {
+            const uint32_t x = (qw[l / 2] >> (16 * (l % 2))) & 0xFFFFu;
+            unsigned long long acc = static_cast<unsigned long long>(x + ad) * dinv + k[l];
+            acc += static_cast<unsigned long long>(u[0][l]) * w0;
+            acc += static_cast<unsigned long long>(u[1][l]) * w1;
+            acc += static_cast<unsigned long long>(u[2][l]) * w2;
+            y[l] = mod_u35(acc, m, mg, c32);
+        }
+        *reinterpret_cast<uint4*>(out + i * ld_out + e0) =
+            make_uint4(y[0] | (y[1] << 16), y[2] | (y[3] << 16), y[4] | (y[5] << 16), y[6] | (y[7] << 16));
+    }
+}
+
 __global__ void __launch_bounds__(256) rescale_kernel(const uint16_t* __restrict__ in, size_t ld_in, size_t count,
                                                       const __grid_constant__ RescaleTable t,
                                                       uint16_t* __restrict__ out, size_t ld_out) {
@@ -683,6 +745,11 @@ cudaError_t launch_split_bigint(const uint8_t* in, uint32_t width, uint32_t rows
 cudaError_t launch_rescale(const uint16_t* in, size_t ld_in, size_t count, const RescaleTable& t, uint16_t* out,
                            size_t ld_out, cudaStream_t s) {
     if (count == 0) return cudaSuccess;
+    if (count % 8 == 0 && ld_in % 8 == 0 && ld_out % 8 == 0 && t.drop <= 3 &&
+        ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
+        rescale_vec_kernel<<<blocks_for(count / 8, 256), 256, 0, s>>>(in, ld_in, count / 8, t, out, ld_out);
+        return cudaGetLastError();
+    }
     rescale_kernel<<<blocks_for(count, 256), 256, 0, s>>>(in, ld_in, count, t, out, ld_out);
     return cudaGetLastError();
 }

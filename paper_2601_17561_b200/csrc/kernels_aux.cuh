@@ -78,6 +78,10 @@ struct RescaleTable {
     uint32_t cinv[kMaxModuli];     // (Delta/m_j)^-1 mod m_j (dropped moduli)
     unsigned long long cq[kMaxModuli];  // Delta / m_j (dropped moduli)
     unsigned long long delta;
+    // folded form: y_i = ((x_i + add_i) dinv_i + sum_j u_j w[j][i] + k) mod m_i with
+    // u_j = (x_j + add_j) cinv_j mod m_j, k = floor(sum_j u_j cq_j / Delta),
+    // w[j][i] = -(cq_j dinv_i) mod m_i (j indexes the dropped moduli)
+    uint32_t w[3][kMaxModuli];
 };
 cudaError_t launch_rescale(const uint16_t* in, size_t ld_in, size_t count, const RescaleTable& t, uint16_t* out,
                            size_t ld_out, cudaStream_t s);

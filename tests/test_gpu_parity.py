@@ -352,8 +352,9 @@ def test_split_cols_u16_all_paths(basis_kind, k, n):
         assert (got[i, :, :, k:] == 0).all()
 
 
+@pytest.mark.parametrize("count", [777, 800])  # scalar path / vectorised path
 @pytest.mark.parametrize("drop,round_", [(1, 0), (1, 1), (2, 1), (3, 0), (3, 1)])
-def test_rescale_residues_vs_bigint(drop, round_):
+def test_rescale_residues_vs_bigint(drop, round_, count):
     # f2: ModDown by the product of the last `drop` moduli, exact against
     # Python big integers (CRT lift, floor / round division, re-reduction)
     import ctypes as C
@@ -362,7 +363,7 @@ def test_rescale_residues_vs_bigint(drop, round_):
     from paper_2601_17561_b200.modmat import default_context
     primes, exps = ol.paper_basis()
     moduli = [int(p) ** int(e) for p, e in zip(primes, exps)]
-    nmod, count = len(moduli), 777
+    nmod = len(moduli)
     rng = np.random.default_rng(drop * 10 + round_)
     res = np.stack([rng.integers(0, m, count) for m in moduli]).astype(np.uint16)
     res[:, 0] = 0                                         # x = 0
