@@ -46,6 +46,7 @@ typedef enum irl_status {
 
 typedef struct irl_ctx irl_ctx;
 typedef struct irl_ccmm irl_ccmm;
+typedef struct irl_iris_db irl_iris_db;
 
 /* ---- context ------------------------------------------------------------ */
 int irl_abi_version(void);
@@ -222,6 +223,14 @@ int irl_iris_inner_overlap(irl_ctx* ctx, const uint64_t* db_code, const uint64_t
 int irl_iris_match(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db_mask, size_t n_db,
                    const uint64_t* q_code, const uint64_t* q_mask, size_t n_eyes, size_t rho, size_t d,
                    double p_lo, double p_hi, uint8_t* match_bits, int32_t* eye_result, double* scores);
+/* Device-resident template database: the enrolled templates become int8
+ * planes in HBM once; each irl_iris_db_match moves only the query eyes' bits
+ * (same outputs and semantics as irl_iris_match; n_eyes * rho <= max_cols). */
+int irl_iris_db_create(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db_mask, size_t n_db, size_t d,
+                       size_t max_cols, irl_iris_db** out);
+int irl_iris_db_destroy(irl_iris_db* e);
+int irl_iris_db_match(irl_iris_db* e, const uint64_t* q_code, const uint64_t* q_mask, size_t n_eyes, size_t rho,
+                      double p_lo, double p_hi, uint8_t* match_bits, int32_t* eye_result, double* scores);
 
 #ifdef __cplusplus
 }

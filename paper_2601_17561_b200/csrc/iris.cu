@@ -98,49 +98,10 @@ __global__ void iris_match_kernel(const int32_t* __restrict__ inner, const int32
 
 size_t round16(size_t x) { return (x + 15) / 16 * 16; }
 
-// Shared front half: planes for the DB and the rotated queries, and the
-// kModeInner GEMM into device inner / overlap [cols][n_db].
-int inner_overlap_device(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db_mask, size_t n_db,
-                         const uint64_t* q_code, const uint64_t* q_mask, size_t n_eyes, size_t rho, size_t d,
-                         int32_t** d_inner, int32_t** d_overlap) {
-    cudaStream_t s = ctx->stream;
-    const size_t words = (d + 63) / 64, ldk = round16(d), cols = n_eyes * rho;
-    if (d > (1u << 30) || n_db >= (1u << 29) || cols >= (1u << 29))
-        return set_err(ctx, IRL_ERR_UNSUPPORTED, "iris: dimensions too large");
-    const size_t db_bits = n_db * words * 8, q_bits = n_eyes * words * 8;
-    const size_t db_planes = 2 * n_db * ldk, q_planes = 2 * cols * ldk, outs = cols * n_db * 4;
-    IRL_CK(ctx, ctx->ws[0].ensure(2 * db_bits + 2 * q_bits));
-    IRL_CK(ctx, ctx->ws[1].ensure(db_planes));
-    IRL_CK(ctx, ctx->ws[2].ensure(q_planes));
-    IRL_CK(ctx, ctx->ws[3].ensure(2 * outs));
-    uint8_t* bitbuf = ctx->ws[0].as<uint8_t>();
-    uint64_t* dc = reinterpret_cast<uint64_t*>(bitbuf);
-    uint64_t* dm = reinterpret_cast<uint64_t*>(bitbuf + db_bits);
-    uint64_t* qc = reinterpret_cast<uint64_t*>(bitbuf + 2 * db_bits);
-    uint64_t* qm = reinterpret_cast<uint64_t*>(bitbuf + 2 * db_bits + q_bits);
-    IRL_CK(ctx, cudaMemcpyAsync(dc, db_code, db_bits, cudaMemcpyHostToDevice, s));
-    IRL_CK(ctx, cudaMemcpyAsync(dm, db_mask, db_bits, cudaMemcpyHostToDevice, s));
-    IRL_CK(ctx, cudaMemcpyAsync(qc, q_code, q_bits, cudaMemcpyHostToDevice, s));
-    IRL_CK(ctx, cudaMemcpyAsync(qm, q_mask, q_bits, cudaMemcpyHostToDevice, s));
-    int8_t* xp = ctx->ws[1].as<int8_t>();
-    int8_t* yp = ctx->ws[2].as<int8_t>();
-    const uint32_t T = 256;
-    {
-        const size_t n = n_db * (ldk / 16);
-        iris_planes_kernel<<<static_cast<unsigned>((n + T - 1) / T), T, 0, s>>>(
-            dc, dm, static_cast<uint32_t>(words), static_cast<uint32_t>(d), 1u, static_cast<uint32_t>(n_db),
-            static_cast<uint32_t>(ldk), xp);
-        IRL_LAUNCH(ctx, cudaGetLastError());
-    }
-    {
-        const size_t n = cols * (ldk / 16);
-        iris_planes_kernel<<<static_cast<unsigned>((n + T - 1) / T), T, 0, s>>>(
-            qc, qm, static_cast<uint32_t>(words), static_cast<uint32_t>(d), static_cast<uint32_t>(rho),
-            static_cast<uint32_t>(cols), static_cast<uint32_t>(ldk), yp);
-        IRL_LAUNCH(ctx, cudaGetLastError());
-    }
-    int32_t* inner = ctx->ws[3].as<int32_t>();
-    int32_t* ovl = inner + cols * n_db;
+// kModeInner GEMM of device planes x (DB, [2][n_db][ldk]) and y (queries,
+// [2][cols][ldk]) into inner / overlap [cols][n_db].
+int inner_overlap_gemm(irl_ctx* ctx, const int8_t* xp, const int8_t* yp, size_t n_db, size_t cols, size_t d,
+                       size_t ldk, int32_t* inner, int32_t* ovl, uint32_t* progress, cudaStream_t s) {
     PpmmLaunch L;
     L.mode = kModeInner;
     L.a_planes = xp;
@@ -154,8 +115,95 @@ int inner_overlap_device(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* 
     L.parts = 1;
     L.nprimes = 1;
     L.mc[0] = make_modconst(2, 1);  // unused by kModeInner
-    L.progress = ctx->d_progress;
+    L.progress = progress;
     IRL_LAUNCH(ctx, launch_ppmm_planes(L, s));
+    return IRL_OK;
+}
+
+int build_planes(irl_ctx* ctx, const uint64_t* code, const uint64_t* mask, size_t n, size_t rho, size_t d,
+                 int8_t* planes, cudaStream_t s) {
+    const size_t words = (d + 63) / 64, ldk = round16(d), cols = n * rho;
+    const size_t total = cols * (ldk / 16);
+    if (total == 0) return IRL_OK;
+    iris_planes_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
+        code, mask, static_cast<uint32_t>(words), static_cast<uint32_t>(d), static_cast<uint32_t>(rho),
+        static_cast<uint32_t>(cols), static_cast<uint32_t>(ldk), planes);
+    IRL_LAUNCH(ctx, cudaGetLastError());
+    return IRL_OK;
+}
+
+// Score + match pass over device inner / overlap (see iris_match_kernel),
+// results to host buffers; blocks. Returns IRL_ERR_ZERO_OVERLAP if any eye's
+// first evaluated score had an empty overlap.
+int match_device(irl_ctx* ctx, const int32_t* di, const int32_t* dov, size_t n_db, size_t n_eyes, size_t rho,
+                 double p_lo, double p_hi, uint8_t* match_bits, int32_t* eye_result, double* scores,
+                 irl::DevBuf& ws, cudaStream_t s) {
+    const size_t cols = n_eyes * rho, nbits = n_eyes * n_db, nsc = cols * n_db;
+    const size_t off_sc = (16 * n_eyes + nbits + 15) / 16 * 16;
+    IRL_CK(ctx, ws.ensure(off_sc + (scores ? nsc * 8 : 0)));
+    auto* first = ws.as<unsigned long long>();
+    uint8_t* dbits = reinterpret_cast<uint8_t*>(first + 2 * n_eyes);
+    double* dsc = scores ? reinterpret_cast<double*>(ws.as<uint8_t>() + off_sc) : nullptr;
+    IRL_CK(ctx, cudaMemsetAsync(first, 0xFF, 16 * n_eyes, s));
+    const uint32_t T = 256;
+    iris_match_kernel<<<static_cast<unsigned>((nbits + T - 1) / T), T, 0, s>>>(
+        di, dov, static_cast<uint32_t>(n_db), static_cast<uint32_t>(n_eyes), static_cast<uint32_t>(rho), p_lo,
+        p_hi, dbits, dsc, first);
+    IRL_LAUNCH(ctx, cudaGetLastError());
+    std::vector<unsigned long long> h(2 * n_eyes);
+    IRL_CK(ctx, cudaMemcpyAsync(h.data(), first, 16 * n_eyes, cudaMemcpyDeviceToHost, s));
+    if (match_bits) IRL_CK(ctx, cudaMemcpyAsync(match_bits, dbits, nbits, cudaMemcpyDeviceToHost, s));
+    if (scores) IRL_CK(ctx, cudaMemcpyAsync(scores, dsc, nsc * 8, cudaMemcpyDeviceToHost, s));
+    IRL_CK(ctx, cudaStreamSynchronize(s));
+    int status = IRL_OK;
+    for (size_t e = 0; e < n_eyes; ++e) {
+        const unsigned long long fm = h[2 * e], fz = h[2 * e + 1];
+        // match_db_reference: the first evaluated score either matches (return
+        // true) or throws ZeroOverlap, whichever comes first in loop order
+        const int32_t res = fz < fm ? -1 : (fm != ~0ull ? 1 : 0);
+        if (eye_result) eye_result[e] = res;
+        if (res < 0 && status == IRL_OK)
+            status = set_err(ctx, IRL_ERR_ZERO_OVERLAP, "mask overlap is empty, score undefined");
+    }
+    return status;
+}
+
+int check_dims(irl_ctx* ctx, size_t n_db, size_t cols, size_t d) {
+    if (d > (1u << 30) || n_db >= (1u << 29) || cols >= (1u << 29))
+        return set_err(ctx, IRL_ERR_UNSUPPORTED, "iris: dimensions too large");
+    return IRL_OK;
+}
+
+// One-shot path (host templates in, device scratch of the context):
+// planes for the DB and the rotated queries, then the kModeInner GEMM into
+// device inner / overlap [cols][n_db].
+int inner_overlap_device(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db_mask, size_t n_db,
+                         const uint64_t* q_code, const uint64_t* q_mask, size_t n_eyes, size_t rho, size_t d,
+                         int32_t** d_inner, int32_t** d_overlap) {
+    cudaStream_t s = ctx->stream;
+    const size_t words = (d + 63) / 64, ldk = round16(d), cols = n_eyes * rho;
+    if (int st = check_dims(ctx, n_db, cols, d)) return st;
+    const size_t db_bits = n_db * words * 8, q_bits = n_eyes * words * 8;
+    IRL_CK(ctx, ctx->ws[0].ensure(2 * db_bits + 2 * q_bits));
+    IRL_CK(ctx, ctx->ws[1].ensure(2 * n_db * ldk));
+    IRL_CK(ctx, ctx->ws[2].ensure(2 * cols * ldk));
+    IRL_CK(ctx, ctx->ws[3].ensure(2 * cols * n_db * 4));
+    uint8_t* bitbuf = ctx->ws[0].as<uint8_t>();
+    auto* dc = reinterpret_cast<uint64_t*>(bitbuf);
+    auto* dm = reinterpret_cast<uint64_t*>(bitbuf + db_bits);
+    auto* qc = reinterpret_cast<uint64_t*>(bitbuf + 2 * db_bits);
+    auto* qm = reinterpret_cast<uint64_t*>(bitbuf + 2 * db_bits + q_bits);
+    IRL_CK(ctx, cudaMemcpyAsync(dc, db_code, db_bits, cudaMemcpyHostToDevice, s));
+    IRL_CK(ctx, cudaMemcpyAsync(dm, db_mask, db_bits, cudaMemcpyHostToDevice, s));
+    IRL_CK(ctx, cudaMemcpyAsync(qc, q_code, q_bits, cudaMemcpyHostToDevice, s));
+    IRL_CK(ctx, cudaMemcpyAsync(qm, q_mask, q_bits, cudaMemcpyHostToDevice, s));
+    int8_t* xp = ctx->ws[1].as<int8_t>();
+    int8_t* yp = ctx->ws[2].as<int8_t>();
+    if (int st = build_planes(ctx, dc, dm, n_db, 1, d, xp, s)) return st;
+    if (int st = build_planes(ctx, qc, qm, n_eyes, rho, d, yp, s)) return st;
+    int32_t* inner = ctx->ws[3].as<int32_t>();
+    int32_t* ovl = inner + cols * n_db;
+    if (int st = inner_overlap_gemm(ctx, xp, yp, n_db, cols, d, ldk, inner, ovl, ctx->d_progress, s)) return st;
     *d_inner = inner;
     *d_overlap = ovl;
     return IRL_OK;
@@ -172,6 +220,19 @@ int check_args(irl_ctx* ctx, const void* dbc, const void* dbm, size_t n_db, cons
 }
 
 }  // namespace
+
+// Device-resident template database (the server keeps its enrolled templates
+// in HBM as int8 planes; each query batch then moves only the eyes' bits).
+struct irl_iris_db {
+    irl_ctx* ctx = nullptr;
+    size_t n_db = 0, d = 0, ldk = 0, max_cols = 0;
+    int8_t* planes = nullptr;    // [2][n_db][ldk]
+    int8_t* qplanes = nullptr;   // [2][max_cols][ldk]
+    uint64_t* qbits = nullptr;   // eyes' code + mask words
+    int32_t* io = nullptr;       // inner, overlap [max_cols][n_db]
+    uint32_t* progress = nullptr;
+    irl::DevBuf match_ws;
+};
 
 extern "C" {
 
@@ -207,35 +268,86 @@ int irl_iris_match(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db_mas
     int32_t *di = nullptr, *dov = nullptr;
     if (int st = inner_overlap_device(ctx, db_code, db_mask, n_db, q_code, q_mask, n_eyes, rho, d, &di, &dov))
         return st;
-    cudaStream_t s = ctx->stream;
-    const size_t nbits = n_eyes * n_db, nsc = cols * n_db;
-    IRL_CK(ctx, ctx->ws[4].ensure(16 * n_eyes + nbits + (scores ? nsc * 8 : 0) + 16));
-    auto* first = ctx->ws[4].as<unsigned long long>();
-    uint8_t* dbits = reinterpret_cast<uint8_t*>(first + 2 * n_eyes);
-    double* dsc = scores ? reinterpret_cast<double*>(ctx->ws[4].as<uint8_t>() + ((16 * n_eyes + nbits + 15) / 16 * 16))
-                         : nullptr;
-    IRL_CK(ctx, cudaMemsetAsync(first, 0xFF, 16 * n_eyes, s));
-    const uint32_t T = 256;
-    iris_match_kernel<<<static_cast<unsigned>((nbits + T - 1) / T), T, 0, s>>>(
-        di, dov, static_cast<uint32_t>(n_db), static_cast<uint32_t>(n_eyes), static_cast<uint32_t>(rho), p_lo,
-        p_hi, dbits, dsc, first);
-    IRL_LAUNCH(ctx, cudaGetLastError());
-    std::vector<unsigned long long> h(2 * n_eyes);
-    IRL_CK(ctx, cudaMemcpyAsync(h.data(), first, 16 * n_eyes, cudaMemcpyDeviceToHost, s));
-    if (match_bits) IRL_CK(ctx, cudaMemcpyAsync(match_bits, dbits, nbits, cudaMemcpyDeviceToHost, s));
-    if (scores) IRL_CK(ctx, cudaMemcpyAsync(scores, dsc, nsc * 8, cudaMemcpyDeviceToHost, s));
-    IRL_CK(ctx, cudaStreamSynchronize(s));
-    int status = IRL_OK;
-    for (size_t e = 0; e < n_eyes; ++e) {
-        const unsigned long long fm = h[2 * e], fz = h[2 * e + 1];
-        // match_db_reference: the first evaluated score either matches (return
-        // true) or throws ZeroOverlap, whichever comes first in loop order
-        const int32_t res = fz < fm ? -1 : (fm != ~0ull ? 1 : 0);
-        if (eye_result) eye_result[e] = res;
-        if (res < 0 && status == IRL_OK)
-            status = set_err(ctx, IRL_ERR_ZERO_OVERLAP, "mask overlap is empty, score undefined");
+    return match_device(ctx, di, dov, n_db, n_eyes, rho, p_lo, p_hi, match_bits, eye_result, scores, ctx->ws[4],
+                        ctx->stream);
+}
+
+int irl_iris_db_create(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db_mask, size_t n_db, size_t d,
+                       size_t max_cols, irl_iris_db** out) {
+    if (!out) return IRL_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    if (int st = check_args(ctx, db_code, db_mask, n_db, db_code, db_mask, 0, d)) return st;
+    Guard g(ctx);
+    if (n_db == 0 || max_cols == 0) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "iris db: empty database or batch");
+    if (int st = check_dims(ctx, n_db, max_cols, d)) return st;
+    auto* e = new irl_iris_db();
+    e->ctx = ctx;
+    e->n_db = n_db;
+    e->d = d;
+    e->ldk = round16(d);
+    e->max_cols = max_cols;
+    const size_t words = (d + 63) / 64, db_bits = n_db * words * 8;
+    uint64_t* staging = nullptr;
+    cudaError_t err = cudaMalloc(&e->planes, 2 * n_db * e->ldk);
+    if (err == cudaSuccess) err = cudaMalloc(&e->qplanes, 2 * max_cols * e->ldk);
+    if (err == cudaSuccess) err = cudaMalloc(&e->qbits, 2 * max_cols * words * 8);
+    if (err == cudaSuccess) err = cudaMalloc(&e->io, 2 * max_cols * n_db * 4);
+    if (err == cudaSuccess) err = cudaMalloc(&e->progress, kScheduleScratchBytes);
+    if (err == cudaSuccess) err = cudaMalloc(&staging, 2 * db_bits);
+    if (err == cudaSuccess) err = cudaMemcpyAsync(staging, db_code, db_bits, cudaMemcpyHostToDevice, ctx->stream);
+    if (err == cudaSuccess)
+        err = cudaMemcpyAsync(staging + db_bits / 8, db_mask, db_bits, cudaMemcpyHostToDevice, ctx->stream);
+    int st = IRL_OK;
+    if (err == cudaSuccess) st = build_planes(ctx, staging, staging + db_bits / 8, n_db, 1, d, e->planes, ctx->stream);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(ctx->stream);
+    cudaFree(staging);
+    if (err != cudaSuccess || st != IRL_OK) {
+        irl_iris_db_destroy(e);
+        return err != cudaSuccess ? cuda_fail(ctx, err, "irl_iris_db_create") : st;
     }
-    return status;
+    *out = e;
+    return IRL_OK;
+}
+
+int irl_iris_db_destroy(irl_iris_db* e) {
+    if (!e) return IRL_OK;
+    cudaSetDevice(e->ctx->device);
+    cudaStreamSynchronize(e->ctx->stream);
+    cudaFree(e->planes);
+    cudaFree(e->qplanes);
+    cudaFree(e->qbits);
+    cudaFree(e->io);
+    cudaFree(e->progress);
+    e->match_ws.release();
+    delete e;
+    return IRL_OK;
+}
+
+int irl_iris_db_match(irl_iris_db* e, const uint64_t* q_code, const uint64_t* q_mask, size_t n_eyes, size_t rho,
+                      double p_lo, double p_hi, uint8_t* match_bits, int32_t* eye_result, double* scores) {
+    if (!e) return IRL_ERR_INVALID_ARGUMENT;
+    irl_ctx* ctx = e->ctx;
+    if (int st = check_args(ctx, q_code, q_mask, 0, q_code, q_mask, n_eyes, e->d)) return st;
+    Guard g(ctx);
+    const size_t cols = n_eyes * rho;
+    if (cols == 0) {
+        if (eye_result) std::memset(eye_result, 0, n_eyes * sizeof(int32_t));
+        if (match_bits) std::memset(match_bits, 0, n_eyes * e->n_db);
+        return IRL_OK;
+    }
+    if (cols > e->max_cols) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "iris db: query batch wider than max_cols");
+    cudaStream_t s = ctx->stream;
+    const size_t words = (e->d + 63) / 64, qb = n_eyes * words * 8;
+    IRL_CK(ctx, cudaMemcpyAsync(e->qbits, q_code, qb, cudaMemcpyHostToDevice, s));
+    IRL_CK(ctx, cudaMemcpyAsync(e->qbits + n_eyes * words, q_mask, qb, cudaMemcpyHostToDevice, s));
+    if (int st = build_planes(ctx, e->qbits, e->qbits + n_eyes * words, n_eyes, rho, e->d, e->qplanes, s)) return st;
+    int32_t* inner = e->io;
+    int32_t* ovl = e->io + cols * e->n_db;
+    if (int st = inner_overlap_gemm(ctx, e->planes, e->qplanes, e->n_db, cols, e->d, e->ldk, inner, ovl,
+                                    e->progress, s))
+        return st;
+    return match_device(ctx, inner, ovl, e->n_db, n_eyes, rho, p_lo, p_hi, match_bits, eye_result, scores,
+                        e->match_ws, s);
 }
 
 }  // extern "C"

@@ -133,3 +133,59 @@ def score(a: IrisTemplate, b: IrisTemplate, ctx: Optional[Context] = None) -> fl
     if ovl[0, 0] == 0:
         raise ZeroOverlap("mask overlap is empty, score undefined")
     return float(inner[0, 0]) / float(ovl[0, 0])
+
+
+class IrisDatabase:
+    """Device-resident enrolled templates (irl_iris_db_*): planes built once in
+    HBM; each match() moves only the query eyes' bits to the device."""
+
+    def __init__(self, db: Sequence[IrisTemplate], max_cols: int, ctx: Optional[Context] = None):
+        import ctypes as C
+        self.ctx = ctx or default_context()
+        dc, dm, d = _stack(db)
+        self.n_db, self.d, self.max_cols = len(db), d, max_cols
+        h = C.c_void_p()
+        self.ctx.check(capi.lib().irl_iris_db_create(self.ctx.handle, _p(dc), _p(dm), len(db), d, max_cols,
+                                                     C.byref(h)))
+        self.handle = h
+
+    @classmethod
+    def from_packed(cls, code: np.ndarray, mask: np.ndarray, d: int, max_cols: int,
+                    ctx: Optional[Context] = None) -> "IrisDatabase":
+        import ctypes as C
+        self = cls.__new__(cls)
+        self.ctx = ctx or default_context()
+        self.n_db, self.d, self.max_cols = code.shape[0], d, max_cols
+        h = C.c_void_p()
+        self.ctx.check(capi.lib().irl_iris_db_create(self.ctx.handle, _p(code), _p(mask), code.shape[0], d,
+                                                     max_cols, C.byref(h)))
+        self.handle = h
+        return self
+
+    def match_packed(self, q_code, q_mask, n_eyes: int, rho: int, p_int: Interval, want_scores=False):
+        bits = np.zeros((n_eyes, self.n_db), np.uint8)
+        res = np.zeros(n_eyes, np.int32)
+        sc = np.zeros((n_eyes * rho, self.n_db), np.float64) if want_scores else None
+        st = capi.lib().irl_iris_db_match(self.handle, _p(q_code), _p(q_mask), n_eyes, rho, float(p_int.lo),
+                                          float(p_int.hi), _p(bits), _p(res), _p(sc))
+        if st not in (capi.IRL_OK, capi.IRL_ERR_ZERO_OVERLAP):
+            self.ctx.check(st)
+        return res, bits, sc
+
+    def match(self, eyes: Sequence[IrisTemplate], rho: int, p_int: Interval, want_scores=False):
+        """Same outputs as match_eyes(db, eyes, rho, p_int)."""
+        qc, qm, d = _stack(eyes)
+        if eyes and d != self.d:
+            raise ShapeMismatch("template lengths differ")
+        return self.match_packed(qc, qm, len(eyes), rho, p_int, want_scores)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            capi.lib().irl_iris_db_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
