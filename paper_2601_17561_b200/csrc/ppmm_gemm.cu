@@ -80,6 +80,7 @@ struct __align__(64) GemmArgs {
     uint32_t G, F, L, active_clusters;
     uint32_t dynamic;                 // 1: units from an atomic counter; 0: static super-rounds
     uint32_t gate_lead;               // max K blocks a pair may lead its group (0: no gating)
+    uint32_t a_evict_first;           // DB tiles read exactly once from L2 (G == 1): evict-first policy
     uint32_t accumulate;
     uint32_t a_part_rows;             // plane rows between consecutive parts of A
     unsigned long long out_part;      // output elements between consecutive parts
@@ -362,12 +363,21 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 #pragma unroll
                             for (uint32_t j = 0; j < kPN; ++j) mask |= 1u << (2 * (pm * kPN + j) + half_rank);
                             const uint32_t sub = pn * kSubA * kBlockK;
-                            ptx::tma_load_2d_pair_mcast(ptx::smem_u32(st) + sub, &tmap_a, leader_full, k0,
-                                                        static_cast<int32_t>(a_row0 + pn * kSubA), mask);
-                            ptx::tma_load_2d_pair_mcast(ptx::smem_u32(st + kPlaneTileBytes) + sub, &tmap_a,
-                                                        leader_full, k0,
-                                                        static_cast<int32_t>(a_row0 + args.M + pn * kSubA),
-                                                        mask);
+                            if (args.a_evict_first) {
+                                ptx::tma_load_2d_pair_mcast_hint(ptx::smem_u32(st) + sub, &tmap_a, leader_full, k0,
+                                                                 static_cast<int32_t>(a_row0 + pn * kSubA), mask,
+                                                                 ptx::kL2EvictFirst);
+                                ptx::tma_load_2d_pair_mcast_hint(
+                                    ptx::smem_u32(st + kPlaneTileBytes) + sub, &tmap_a, leader_full, k0,
+                                    static_cast<int32_t>(a_row0 + args.M + pn * kSubA), mask, ptx::kL2EvictFirst);
+                            } else {
+                                ptx::tma_load_2d_pair_mcast(ptx::smem_u32(st) + sub, &tmap_a, leader_full, k0,
+                                                            static_cast<int32_t>(a_row0 + pn * kSubA), mask);
+                                ptx::tma_load_2d_pair_mcast(ptx::smem_u32(st + kPlaneTileBytes) + sub, &tmap_a,
+                                                            leader_full, k0,
+                                                            static_cast<int32_t>(a_row0 + args.M + pn * kSubA),
+                                                            mask);
+                            }
                         }
                         if constexpr (kPM == 1) {
                             ptx::tma_load_2d_pair_hint(ptx::smem_u32(st + 2 * kPlaneTileBytes),
@@ -825,6 +835,9 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
         a.F = pt.clusters / a.G;
         a.L = pt.clusters % a.G;
         a.active_clusters = pt.clusters;
+        // a cluster that covers a whole n-chunk (G == 1, multi-pair) is the only
+        // reader of its DB tile: stream it evict-first so the query stays in L2
+        a.a_evict_first = (sh.pn > 1 && a.G == 1 && !std::getenv("IRL_PPMM_A_NORMAL")) ? 1u : 0u;
         a.progress = L.progress + pt.pair0;  // indexed by cluster id (< pairs of this launch)
         a.mailbox = reinterpret_cast<unsigned long long*>(L.progress + kProgressWords + 32) +
                     static_cast<size_t>(pt.group0) * kMail;

@@ -130,6 +130,16 @@ __device__ __forceinline__ void tma_load_2d_pair_mcast(uint32_t smem_dst, const 
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load_2d_pair_mcast_hint(uint32_t smem_dst, const void* tmap, uint32_t mbar,
+                                                            int32_t c0, int32_t c1, uint16_t cta_mask,
+                                                            uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".multicast::cluster.L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_dst),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(mbar), "r"(c0), "r"(c1), "h"(cta_mask), "l"(policy)
+        : "memory");
+}
+
 // ---- cross-CTA progress flags (global memory) ---------------------------------
 
 __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {

@@ -399,3 +399,31 @@ def test_ccmm_rescale_matches_bigint():
         cols = out[part][:, :3, :].reshape(eng.nmod, -1)  # 3 columns x 300 rows
         want = ol.rescale_oracle(cols, eng.moduli, 3, True)
         assert (got[part][:, :3, :].reshape(eng.nmod - 3, -1) == want).all()
+
+
+@pytest.mark.slow
+def test_ccmm_linearity_full_slice_every_element():
+    # Size-independent property at the c3 slice geometry (2 parts x 2^14 rows,
+    # K = 24576, N = 992): CCMM(db, q1 + q2) == CCMM(db, q1) + CCMM(db, q2)
+    # mod p^2 for every one of the 2 x 24 x 992 x 2^14 outputs (the oracle
+    # checks sampled rows; linearity covers the rest on the device).
+    import torch
+    from paper_2601_17561_b200.ccmm import CcmmEngine, staging_tensors, synth_query
+    N = 992
+    eng = CcmmEngine(parts=2, m=1 << 14, k=24576, max_n=N)
+    eng.synth_db(seed=1)
+    q1 = synth_query(2, eng.K, N, eng.moduli)
+    q2 = synth_query(3, eng.K, N, eng.moduli)
+    mods = torch.tensor(eng.moduli, dtype=torch.int32, device="cuda").view(-1, 1, 1)
+    qd, od = staging_tensors(eng, N)
+    outs = []
+    t1 = torch.from_numpy(q1.astype(np.int32)).cuda()
+    t2 = torch.from_numpy(q2.astype(np.int32)).cuda()
+    for q in (t1, t2, (t1 + t2) % mods):
+        qd.copy_(q.to(torch.int16))
+        eng.run_device(None, N, None)
+        torch.cuda.synchronize()
+        outs.append(od.to(torch.int32) & 0xFFFF)
+    m4 = mods.view(1, -1, 1, 1)
+    assert torch.equal((outs[0] + outs[1]) % m4, outs[2])
+    assert bool((outs[2] < m4).all())
