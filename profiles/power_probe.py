@@ -113,6 +113,26 @@ def main():
             zeroed = True
             torch.cuda.synchronize()
             r = run({}, a.secs)
+        elif v.startswith("db_"):
+            # DB digit distribution experiments: residues v = d0 + p d1 (mod p^2)
+            # with both centred digits drawn from a sub-range (energy vs data)
+            kind = v[3:]
+            g = torch.Generator(device="cuda").manual_seed(5)
+            res = torch.empty((eng.nmod, a.rows, a.k), dtype=torch.int16, device="cuda")
+            for i, (pp, ee) in enumerate(zip(eng.primes, eng.exps)):
+                pp = int(pp)
+                h = (pp - 1) // 2
+                lo, hi = {"pos": (0, h), "neg": (-h, 0), "small": (-(h // 2), h // 2),
+                          "full": (-h, h), "tiny": (-3, 3)}[kind]
+                d0 = torch.randint(lo, hi + 1, (a.rows, a.k), generator=g, device="cuda", dtype=torch.int32)
+                d1 = torch.randint(lo, hi + 1, (a.rows, a.k), generator=g, device="cuda", dtype=torch.int32)
+                res[i] = ((d0 + pp * d1) % (pp * pp)).to(torch.int16)
+            for gi in range(a.parts):
+                eng.load_part(gi, res)
+            del res
+            zeroed = True
+            torch.cuda.synchronize()
+            r = run({}, a.secs)
         elif v == "zero_both":
             q_dev.zero_()
             r = run({}, a.secs)
