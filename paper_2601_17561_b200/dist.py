@@ -51,8 +51,16 @@ class ShardedStep:
     run_parts(first_local, count) launches the local PPMMs for local parts
     [first_local, first_local + count) (stream-ordered, non-blocking);
     a_out() returns this rank's buffer for the a-part result: on the owner it
-    is the local output of part 0, elsewhere a receive buffer. The broadcast
-    is posted right after the a-part GEMM so it overlaps the b-part GEMMs.
+    is the local output of part 0, elsewhere a receive buffer.
+
+    Every rank posts the broadcast after its local GEMMs are queued. The
+    PPMM is persistent and holds every SM (1 CTA per SM, 8-CTA clusters), and
+    NCCL's broadcast kernels need SMs: a receive posted before the GEMM would
+    park its CTAs on SMs for the whole step and knock whole clusters out of the
+    GEMM, and an owner's send posted between its a-part and b-part GEMMs would
+    wait on receivers in the same way. Posted last, the NCCL stream waits for
+    the GEMMs and then runs the 744 MiB exchange with the whole GPU (~1 ms
+    over NVLink, <= 5% of an 8-GPU step).
     """
 
     def __init__(self, rank: int, world: int, run_parts: Callable[[int, int], None],
@@ -77,12 +85,11 @@ class ShardedStep:
         if self.world > 1:
             if self.rank == self.owner:
                 self.run_parts(0, 1)  # a-part first
-                work = self._bcast()
                 if self.local.count > 1:
                     self.run_parts(1, self.local.count - 1)
             else:
-                work = self._bcast()
                 self.run_parts(0, self.local.count)
+            work = self._bcast()
         else:
             self.run_parts(0, self.local.count)
         return work

@@ -1,6 +1,6 @@
 """Multi-rank layout of the CCMM (paper's 8-slice DB, a-part broadcast) on CPU
 with the gloo backend. The per-part PPMM is stood in by the CPU oracle (test
-infrastructure) so the orchestration (part dealing, broadcast overlap, result
+infrastructure) so the orchestration (part dealing, broadcast ordering, result
 placement) is exercised exactly as bench.py drives it on NCCL."""
 import os
 import socket
@@ -85,5 +85,6 @@ def test_sharded_step_gloo(world):
         ok_local, ok_a, calls = results[r]
         assert ok_local and ok_a, r
         if r == 0:
-            # the a-part GEMM is issued first, then the broadcast, then the b-parts
+            # the a-part GEMM is issued first, then the b-parts; the broadcast
+            # is posted once every local GEMM is queued
             assert calls[0] == (0, 1)
