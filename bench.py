@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=32, help="DB rows per task in the CPU sample")
     ap.add_argument("--no-int8-ref", action="store_true", help="skip the live cuBLASLt int8 comparison")
+    ap.add_argument("--exchange", choices=["auto", "mirror", "broadcast"], default="auto",
+                    help="a-part exchange at N>1: fused P2P epilogue stores (mirror, validated in warm-up, "
+                         "falls back to broadcast) or the NCCL broadcast")
     return ap.parse_args()
 
 
@@ -244,9 +247,37 @@ def main():
     q_dev, out_dev = staging_tensors(eng, N)
     q_dev.copy_(q_pinned)
     torch.cuda.synchronize()
+    # ---- a-part exchange -------------------------------------
+    # "mirror": receivers export an engine-owned receive buffer (CUDA IPC); the
+    # owner's a-part PPMM epilogue stores every tile into all of them over
+    # NVLink while it computes. Falls back to the NCCL broadcast when peer
+    # mapping fails or the warm-up checksum disagrees.
     a_recv = None
-    if world > 1 and rank != 0:
-        a_recv = torch.empty((nmod, N, M), dtype=torch.int16, device="cuda")
+    exchange, exch_note = "broadcast", None
+    if world > 1:
+        if args.exchange != "broadcast":
+            handle = None
+            try:
+                if rank != 0:
+                    a_recv, handle = eng.alloc_recv(N)
+            except Exception as ex:  # noqa: BLE001
+                exch_note = f"receive buffer: {ex}"
+            handles = [None] * world
+            dist.all_gather_object(handles, handle)
+            ok = all(h is not None for r, h in enumerate(handles) if r != 0)
+            if ok and rank == 0:
+                try:
+                    eng.set_mirrors(0, N, [h for r, h in enumerate(handles) if r != 0])
+                except Exception as ex:  # noqa: BLE001
+                    ok, exch_note = False, f"peer mapping: {ex}"
+            flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device="cuda")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 1:
+                exchange = "mirror"
+            elif rank == 0:
+                eng.set_mirrors(0, N, [])
+        if rank != 0 and a_recv is None:
+            a_recv = torch.empty((nmod, N, M), dtype=torch.int16, device="cuda")
     # a dedicated stream: the engine runs on the stream it is handed, and the
     # CUDA events below are recorded on that same stream
     stream = torch.cuda.Stream()
@@ -268,12 +299,35 @@ def main():
     def a_out():
         return out_dev[0] if rank == 0 else a_recv
 
-    step = ShardedStep(rank, world, run_parts, a_out, parts=args.parts)
+    step = ShardedStep(rank, world, run_parts, a_out, parts=args.parts, exchange=exchange)
 
     def one_step():
         w = step()
         if w is not None:
             w.wait()
+
+    def a_checksum():
+        # sum + exact head/tail samples of this rank's copy of the a-part result
+        buf = a_out()
+        flat = buf.view(-1)
+        return torch.cat([torch.sum(buf.to(torch.int32), dtype=torch.int64).view(1),
+                          flat[:512].to(torch.int64), flat[-512:].to(torch.int64)])
+
+    if exchange == "mirror":
+        # validate the fused exchange once before timing; fall back if any
+        # receiver's copy differs from the owner's
+        one_step()
+        torch.cuda.synchronize()
+        mine = a_checksum()
+        src = mine.clone()
+        dist.broadcast(src, src=0)
+        flag = torch.tensor([1 if torch.equal(mine, src) else 0], dtype=torch.int32, device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) != 1:
+            exchange, exch_note = "broadcast", "warm-up checksum mismatch on a receiver"
+            if rank == 0:
+                eng.set_mirrors(0, N, [])
+            step = ShardedStep(rank, world, run_parts, a_out, parts=args.parts, exchange=exchange)
 
     for _ in range(args.warmup):
         one_step()
@@ -381,7 +435,10 @@ def main():
             eng.run(q_np, o_np)  # H2D query, split, all local PPMMs, D2H outputs
             if world > 1:
                 # the a-part result exchange stays on the device
-                w = dist.broadcast(a_out().view(torch.uint8), src=0, async_op=True)
+                if exchange == "mirror":  # the owner's epilogue already stored out_A into the peers
+                    w = dist.all_reduce(torch.zeros(1, dtype=torch.int32, device="cuda"), async_op=True)
+                else:
+                    w = dist.broadcast(a_out().view(torch.uint8), src=0, async_op=True)
                 w.wait()
                 torch.cuda.synchronize()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
@@ -450,6 +507,9 @@ def main():
                              "ops_per_launch": launch_ops, "peak_source": peak_src,
                              "frac_of_datasheet_4500": achieved / DATASHEET_INT8_TOPS},
                 "split_roofline": split_roof, "moddown": moddown, "int8_library_ref": int8_ref,
+                "exchange": None if world == 1 else {
+                    "kind": "fused P2P stores in the a-part PPMM epilogue (CUDA IPC, NVLink)" if exchange == "mirror"
+                    else "NCCL broadcast after the local GEMMs", "note": exch_note},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)

@@ -190,6 +190,21 @@ int irl_ccmm_twin(irl_ctx* ctx, long d1, long d2, long d3, long n_db, long n_qry
                   double db_modulus_bits, double qry_modulus_bits, double scale_bits,
                   int out_level, int top_level, int out_slot_encoding, int out_ci,
                   const double* db, const double* qry, double* msgs);
+/* ---- fused a-part exchange (replaces the NCCL broadcast) -----
+ * Receivers allocate an engine-owned receive buffer [nmod][n][M] uint16 and
+ * export its CUDA IPC handle (64 bytes); the owner of part `part` opens the
+ * peers' handles, and from then on the epilogue of that part's PPMM stores
+ * every output tile both locally and into each peer buffer (NVLink P2P
+ * stores, overlapped with the GEMM; a system-scope fence per tile). The data
+ * is complete in a peer once the owner's launch has completed: order the
+ * peers' reads after it with any cross-GPU signal (e.g. a tiny NCCL
+ * all-reduce posted after the GEMM). Mirroring applies to device runs and
+ * single-column-chunk e2e runs of width n; count 0 disables it. At most 7. */
+int irl_ccmm_alloc_recv(irl_ccmm* e, size_t n, void** dev_ptr, uint8_t* ipc_handle /* 64 B, nullable */);
+int irl_ccmm_set_mirrors(irl_ccmm* e, size_t part, size_t n, const uint8_t* ipc_handles /* count x 64 B */,
+                         size_t count);
+/* Same with raw device pointers (same-process peers / tests). */
+int irl_ccmm_set_mirror_ptrs(irl_ccmm* e, size_t part, size_t n, uint16_t* const* dev_ptrs, size_t count);
 /* ModDown of the engine's outputs (after irl_ccmm_run_device wrote them to the
  * engine buffer, n columns): parts [part0, part0 + nparts) of [parts][nmod][n][M]
  * -> dst [nparts][nmod - drop][n][M] (device), see irl_rescale_residues. */

@@ -75,6 +75,9 @@ SIGNATURES = {
     "irl_iris_db_create": (C.c_int, [vp, vp, vp, sz, sz, sz, C.POINTER(vp)]),
     "irl_iris_db_destroy": (C.c_int, [vp]),
     "irl_iris_db_match": (C.c_int, [vp, vp, vp, sz, sz, C.c_double, C.c_double, vp, vp, vp]),
+    "irl_ccmm_alloc_recv": (C.c_int, [vp, sz, C.POINTER(vp), vp]),
+    "irl_ccmm_set_mirrors": (C.c_int, [vp, sz, sz, vp, sz]),
+    "irl_ccmm_set_mirror_ptrs": (C.c_int, [vp, sz, sz, C.POINTER(vp), sz]),
     "irl_iris_inner_overlap": (C.c_int, [vp, vp, vp, sz, vp, vp, sz, sz, sz, vp, vp]),
     "irl_iris_match": (C.c_int, [vp, vp, vp, sz, vp, vp, sz, sz, sz, C.c_double, C.c_double, vp, vp, vp]),
 }

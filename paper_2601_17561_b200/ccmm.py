@@ -97,6 +97,29 @@ class CcmmEngine:
         self.ctx.check(capi.lib().irl_ccmm_rescale(self.handle, n, part0, nparts, drop, int(round_),
                                                    capi.ptr(dst), s))
 
+    # ---- fused a-part exchange (irl_ccmm_alloc_recv / set_mirrors) ----------
+
+    def alloc_recv(self, n: int):
+        """Engine-owned receive buffer [nmod][n][M] for the a-part: returns a
+        torch view (int16 bit patterns) and its 64-byte CUDA IPC handle."""
+        import torch
+        p = C.c_void_p()
+        h = (C.c_uint8 * 64)()
+        self.ctx.check(capi.lib().irl_ccmm_alloc_recv(self.handle, n, C.byref(p), h))
+        view = torch.as_tensor(_CudaArray(p.value, (self.nmod, n, self.M), "<i2"),
+                               device=f"cuda:{self.ctx.device}")
+        return view, bytes(h)
+
+    def set_mirrors(self, part: int, n: int, handles):
+        """Store part `part`'s outputs also into the peers' buffers (IPC handles)."""
+        buf = (C.c_uint8 * (64 * len(handles)))(*b"".join(handles)) if handles else None
+        self.ctx.check(capi.lib().irl_ccmm_set_mirrors(self.handle, part, n, buf, len(handles)))
+
+    def set_mirror_ptrs(self, part: int, n: int, tensors):
+        """Same with device tensors of this process (tests)."""
+        arr = (C.c_void_p * max(1, len(tensors)))(*[t.data_ptr() for t in tensors])
+        self.ctx.check(capi.lib().irl_ccmm_set_mirror_ptrs(self.handle, part, n, arr, len(tensors)))
+
     def close(self):
         if getattr(self, "handle", None):
             capi.lib().irl_ccmm_destroy(self.handle)

@@ -42,6 +42,13 @@ struct irl_ccmm {
     std::vector<cudaEvent_t> part_done;  // per modulus chunk: PPMMs done
     std::vector<cudaEvent_t> h2d_done;   // per modulus chunk: query residues landed
     uint64_t bytes = 0;
+    // fused a-part exchange: this engine's receive buffer (peers store into it)
+    // and the peers' buffers this engine stores into (IPC-mapped or raw)
+    uint16_t* recv = nullptr;
+    size_t recv_n = 0;
+    size_t mirror_part = 0, mirror_n = 0, n_mirror = 0;
+    uint16_t* mirror[kMaxMirrors] = {};
+    bool mirror_ipc[kMaxMirrors] = {};
 };
 
 namespace {
@@ -126,6 +133,7 @@ int run_ppmm(irl_ctx* ctx, PpmmLaunch L, uint32_t kchunk, cudaStream_t s) {
         L.K = std::min(kchunk, K - k0);
         L.accumulate = (k0 > 0) || L.accumulate;
         IRL_LAUNCH(ctx, launch_ppmm_planes(L, s));
+        ctx->launches += ppmm_kernels_last_launch() > 1 ? ppmm_kernels_last_launch() - 1 : 0;  // + filler
     }
     return IRL_OK;
 }
@@ -833,8 +841,76 @@ int irl_ccmm_destroy(irl_ccmm* e) {
     cudaFree(e->qres);
     cudaFree(e->out);
     cudaFree(e->progress);
+    for (size_t i = 0; i < e->n_mirror; ++i)
+        if (e->mirror_ipc[i]) cudaIpcCloseMemHandle(e->mirror[i]);
+    cudaFree(e->recv);
     delete e;
     return IRL_OK;
+}
+
+// ---- fused a-part exchange: the a-part PPMM epilogue stores its
+// tiles straight into the peers' receive buffers over NVLink ------------------
+
+int irl_ccmm_alloc_recv(irl_ccmm* e, size_t n, void** dev_ptr, uint8_t* ipc_handle) {
+    if (!e || !dev_ptr) return IRL_ERR_INVALID_ARGUMENT;
+    irl_ctx* ctx = e->ctx;
+    Guard g(ctx);
+    if (n == 0 || n > e->max_n) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: receive width out of range");
+    if (e->recv) cudaFree(e->recv);
+    e->recv = nullptr;
+    IRL_CK(ctx, cudaMalloc(&e->recv, e->nmod * n * e->M * sizeof(uint16_t)));
+    IRL_CK(ctx, cudaMemset(e->recv, 0, e->nmod * n * e->M * sizeof(uint16_t)));
+    e->recv_n = n;
+    *dev_ptr = e->recv;
+    if (ipc_handle) {
+        cudaIpcMemHandle_t h;
+        IRL_CK(ctx, cudaIpcGetMemHandle(&h, e->recv));
+        std::memcpy(ipc_handle, &h, sizeof(h));
+    }
+    return IRL_OK;
+}
+
+static int set_mirrors(irl_ccmm* e, size_t part, size_t n, uint16_t* const* ptrs, const uint8_t* handles,
+                       size_t count) {
+    irl_ctx* ctx = e->ctx;
+    if (count > kMaxMirrors || part >= e->parts || (count && (n == 0 || n > e->max_n)))
+        return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "ccmm: bad mirror set");
+    for (size_t i = 0; i < e->n_mirror; ++i)
+        if (e->mirror_ipc[i]) cudaIpcCloseMemHandle(e->mirror[i]);
+    e->n_mirror = 0;
+    for (size_t i = 0; i < count; ++i) {
+        if (handles) {
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, handles + i * sizeof(h), sizeof(h));
+            void* p = nullptr;
+            const cudaError_t err = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+            if (err != cudaSuccess) {
+                for (size_t j = 0; j < i; ++j) cudaIpcCloseMemHandle(e->mirror[j]);
+                return cuda_fail(ctx, err, "cudaIpcOpenMemHandle");
+            }
+            e->mirror[i] = static_cast<uint16_t*>(p);
+            e->mirror_ipc[i] = true;
+        } else {
+            e->mirror[i] = ptrs[i];
+            e->mirror_ipc[i] = false;
+        }
+    }
+    e->n_mirror = count;
+    e->mirror_part = part;
+    e->mirror_n = n;
+    return IRL_OK;
+}
+
+int irl_ccmm_set_mirrors(irl_ccmm* e, size_t part, size_t n, const uint8_t* ipc_handles, size_t count) {
+    if (!e || (count && !ipc_handles)) return IRL_ERR_INVALID_ARGUMENT;
+    Guard g(e->ctx);
+    return set_mirrors(e, part, n, nullptr, ipc_handles, count);
+}
+
+int irl_ccmm_set_mirror_ptrs(irl_ccmm* e, size_t part, size_t n, uint16_t* const* dev_ptrs, size_t count) {
+    if (!e || (count && !dev_ptrs)) return IRL_ERR_INVALID_ARGUMENT;
+    Guard g(e->ctx);
+    return set_mirrors(e, part, n, dev_ptrs, nullptr, count);
 }
 
 uint64_t irl_ccmm_device_bytes(const irl_ccmm* e) { return e ? e->bytes : 0; }
@@ -927,6 +1003,11 @@ static int ccmm_parts(irl_ccmm* e, size_t n, size_t part0, size_t nparts, uint16
     L.a_part_rows = e->nmod * 2 * e->M;
     L.out_part_elems = e->nmod * n * e->M;
     L.progress = e->progress;
+    if (e->n_mirror && n == e->mirror_n && e->mirror_part >= part0 && e->mirror_part < part0 + nparts) {
+        L.n_mirror = static_cast<uint32_t>(e->n_mirror);
+        L.mirror_part = static_cast<uint32_t>(e->mirror_part - part0);
+        for (size_t i = 0; i < e->n_mirror; ++i) L.mirror[i] = e->mirror[i] + m0 * n * e->M;
+    }
     return run_ppmm(ctx, L, e->kchunk, s);
 }
 

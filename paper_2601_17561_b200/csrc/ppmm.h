@@ -16,6 +16,7 @@ constexpr uint32_t kMaxPrimesPerLaunch = 32;
 // kModeInner = two independent int8 products acc1 = X0 Y0, acc2 = X1 Y1 with
 // raw int32 outputs (mask overlaps and ternary inner products, iris.cu).
 constexpr int kModePsq = 0;
+constexpr uint32_t kMaxMirrors = 7;
 constexpr int kModeInner = 1;
 // Diagnostics slots per CTA pair (PpmmLaunch::stats): 0 producer empty-wait
 // cycles, 1 producer gate cycles, 2 MMA full-wait cycles, 3 MMA tmem-empty
@@ -50,6 +51,12 @@ struct PpmmLaunch {
     // tile by TMA multicast) x cluster_pn pairs along N (sharing each database
     // tile). 1x1 is a plain CTA pair; SMs a multi-pair shape strands are taken
     // by a 1x1 filler launch pulling from the same unit counter.
+    // Mirrors (fused a-part exchange): outputs of part `mirror_part` (relative to
+    // this launch) are also stored, same offsets within the part, to each of
+    // mirror[0..n_mirror) -- peer GPUs' receive buffers mapped over NVLink.
+    uint16_t* mirror[kMaxMirrors] = {};
+    uint32_t n_mirror = 0;
+    uint32_t mirror_part = 0;
     int mode = kModePsq;
     int32_t* out_i32[2] = {nullptr, nullptr};  // kModeInner outputs [parts][nprimes][N][M]
     int cluster_pm = 1;
@@ -58,6 +65,8 @@ struct PpmmLaunch {
 };
 
 cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream);
+// Kernels the calling thread's last launch_ppmm_planes issued (main + filler).
+uint32_t ppmm_kernels_last_launch();
 size_t ppmm_smem_bytes();
 
 }  // namespace irl

@@ -86,6 +86,8 @@ struct __align__(64) GemmArgs {
     unsigned long long out_part;      // output elements between consecutive parts
     uint16_t* out;
     int32_t* out_i32[2];              // kMode == kModeInner: acc1 / acc2 as int32 [n][m] (nullable)
+    uint16_t* mirror[kMaxMirrors];    // peer copies of part mirror_part's outputs (see PpmmLaunch)
+    uint32_t n_mirror, mirror_part;
     uint32_t* progress;               // [clusters] K blocks issued by each pair's leader producer
     uint32_t* counter;                // next unit to hand out (dynamic schedule)
     unsigned long long* mailbox;      // [groups][kMail] ((seq+1) << 32 | unit) published per group
@@ -524,6 +526,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             uint16_t* out = args.out + tc.part * args.out_part +
                             static_cast<size_t>(tc.prime) * args.N * args.M +
                             m;
+            const bool mirror_tile = args.n_mirror != 0 && tc.part == args.mirror_part;
             const uint32_t lane_base = tmem_base + ((quarter * 32u) << 16);
             for (uint32_t c = cgrp * 16; c < tc.n_size; c += 16 * kEpiGroups) {
                 uint32_t a1[16], a2[16];
@@ -543,13 +546,25 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                     continue;
                 }
                 uint16_t* dst = out + static_cast<size_t>(tc.n0 + c) * args.M;
+                // offset of this chunk inside its part (same in the peers' mirrors)
+                const size_t moff = static_cast<size_t>(tc.prime) * args.N * args.M +
+                                    static_cast<size_t>(tc.n0 + c) * args.M + m;
                 if (!args.accumulate && tc.n0 + c + 16 <= args.N) {
                     // fast path: whole 16-column chunk in range, overwrite
+                    uint16_t vals[16];
 #pragma unroll
                     for (int jj = 0; jj < 16; ++jj) {
-                        dst[static_cast<size_t>(jj) * args.M] = static_cast<uint16_t>(
+                        vals[jj] = static_cast<uint16_t>(
                             combine_psq_fast(static_cast<int32_t>(a1[jj]), static_cast<int32_t>(a2[jj]),
                                              mc.p, mc.m, mc.magic_p, mc.magic_m, mc.c_p, mc.c_m));
+                        dst[static_cast<size_t>(jj) * args.M] = vals[jj];
+                    }
+                    if (mirror_tile) {
+                        for (uint32_t mi = 0; mi < args.n_mirror; ++mi) {
+                            uint16_t* md = args.mirror[mi] + moff;
+#pragma unroll
+                            for (int jj = 0; jj < 16; ++jj) md[static_cast<size_t>(jj) * args.M] = vals[jj];
+                        }
                     }
                 } else {
                     for (int jj = 0; jj < 16; ++jj) {
@@ -563,9 +578,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                             v = min(v, v - mc.m);
                         }
                         *d = static_cast<uint16_t>(v);
+                        if (mirror_tile)
+                            for (uint32_t mi = 0; mi < args.n_mirror; ++mi)
+                                args.mirror[mi][moff + static_cast<size_t>(jj) * args.M] = static_cast<uint16_t>(v);
                     }
                 }
             }
+            if (mirror_tile) __threadfence_system();  // peer stores performed before the tile is released
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_cluster(leader_tmem_empty);
@@ -714,7 +733,13 @@ cudaError_t side_stream(int dev, cudaStream_t* s, cudaEvent_t* fork, cudaEvent_t
 
 size_t ppmm_smem_bytes() { return kSmemBytes; }
 
+namespace {
+thread_local uint32_t g_last_kernels = 0;
+}
+uint32_t ppmm_kernels_last_launch() { return g_last_kernels; }
+
 cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
+    g_last_kernels = 0;
     if (L.nprimes == 0 || L.parts == 0 || L.M == 0 || L.N == 0) return cudaSuccess;
     if (L.nprimes > kMaxPrimesPerLaunch) return cudaErrorInvalidValue;
     if (L.ldk % 16 != 0 || L.ldk < L.K) return cudaErrorInvalidValue;
@@ -769,6 +794,10 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     args.out_part = L.out_part_elems ? L.out_part_elems
                                      : static_cast<unsigned long long>(L.nprimes) * L.N * L.M;
     args.out = L.out;
+    if (L.n_mirror > kMaxMirrors || (L.n_mirror && L.mode != kModePsq)) return cudaErrorInvalidValue;
+    args.n_mirror = L.n_mirror;
+    args.mirror_part = L.mirror_part;
+    for (uint32_t i = 0; i < L.n_mirror; ++i) args.mirror[i] = L.mirror[i];
     args.out_i32[0] = L.out_i32[0];
     args.out_i32[1] = L.out_i32[1];
     if (L.mode == kModeInner && L.accumulate) return cudaErrorInvalidValue;
@@ -867,6 +896,7 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
         }
         e = cudaLaunchKernelEx(&cfg, kfn, ma, mb, a);
         if (e != cudaSuccess) return e;
+        ++g_last_kernels;
     }
     if (nparts > 1) {
         e = cudaEventRecord(join, side);

@@ -61,10 +61,21 @@ class ShardedStep:
     wait on receivers in the same way. Posted last, the NCCL stream waits for
     the GEMMs and then runs the 744 MiB exchange with the whole GPU (~1 ms
     over NVLink, <= 5% of an 8-GPU step).
+
+    exchange: "broadcast" (NCCL broadcast of the a-part result) or "mirror"
+    (the owner's a-part PPMM epilogue already stored it into every peer's
+    receive buffer over NVLink, irl_ccmm_set_mirrors; the step then only posts
+    a 4-byte all-reduce so peers' later reads are ordered after the owner's
+    GEMM).
     """
 
     def __init__(self, rank: int, world: int, run_parts: Callable[[int, int], None],
-                 a_out: Callable[[], object], parts: int = PAPER_PARTS, group=None):
+                 a_out: Callable[[], object], parts: int = PAPER_PARTS, group=None,
+                 exchange: str = "broadcast"):
+        if exchange not in ("broadcast", "mirror"):
+            raise ValueError(exchange)
+        self.exchange = exchange
+        self._flag = None
         self.rank, self.world = rank, world
         self.local = part_range(rank, world, parts)
         self.owner = a_part_owner(world, parts)
@@ -80,6 +91,14 @@ class ShardedStep:
         # NCCL both carry uint8)
         return dist.broadcast(buf.view(torch.uint8), src=self.owner, group=self.group, async_op=True)
 
+    def _signal(self):
+        import torch
+        import torch.distributed as dist
+        if self._flag is None:
+            buf = self.a_out()
+            self._flag = torch.zeros(1, dtype=torch.int32, device=buf.device)
+        return dist.all_reduce(self._flag, group=self.group, async_op=True)
+
     def __call__(self):
         work = None
         if self.world > 1:
@@ -89,7 +108,7 @@ class ShardedStep:
                     self.run_parts(1, self.local.count - 1)
             else:
                 self.run_parts(0, self.local.count)
-            work = self._bcast()
+            work = self._bcast() if self.exchange == "broadcast" else self._signal()
         else:
             self.run_parts(0, self.local.count)
         return work

@@ -88,3 +88,33 @@ def test_sharded_step_gloo(world):
             # the a-part GEMM is issued first, then the b-parts; the broadcast
             # is posted once every local GEMM is queued
             assert calls[0] == (0, 1)
+
+
+def _worker_mirror(rank, world, port, results):
+    # exchange="mirror": no broadcast; the step posts a 4-byte all-reduce as the
+    # completion signal (the data itself moves inside the owner's GEMM epilogue,
+    # stood in here by the owner copying into a shared-memory "peer" buffer)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    calls = []
+    buf = torch.zeros(4, dtype=torch.int16)
+
+    def run_parts(first_local, count):
+        calls.append((first_local, count))
+
+    step = ShardedStep(rank, world, run_parts, lambda: buf, exchange="mirror")
+    w = step()
+    w.wait()
+    results[rank] = (calls, int(step._flag.item()))
+    dist.destroy_process_group()
+
+
+def test_sharded_step_mirror_signal_gloo():
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_worker_mirror, args=(2, _free_port(), results), nprocs=2, join=True)
+    assert results[0][0] == [(0, 1), (1, 3)] and results[1][0] == [(0, 4)]
+    assert results[0][1] == 0 and results[1][1] == 0
+    with pytest.raises(ValueError):
+        ShardedStep(0, 1, lambda a, b: None, lambda: None, exchange="nccl")

@@ -427,3 +427,43 @@ def test_ccmm_linearity_full_slice_every_element():
     m4 = mods.view(1, -1, 1, 1)
     assert torch.equal((outs[0] + outs[1]) % m4, outs[2])
     assert bool((outs[2] < m4).all())
+
+
+def test_ccmm_fused_exchange_mirrors():
+    # The fused a-part exchange: the PPMM epilogue of the mirrored part stores
+    # every tile locally and into each mirror buffer (peer receive buffers on a
+    # multi-GPU node; same-process buffers here), for device runs and the
+    # modulus-chunked e2e run alike.
+    import torch
+    from paper_2601_17561_b200.ccmm import CcmmEngine, staging_tensors, synth_query
+    n = 96
+    eng = CcmmEngine(parts=2, m=520, k=640, max_n=n)
+    eng.synth_db(seed=4)
+    qd, od = staging_tensors(eng, n)
+    mirrors = [torch.full((eng.nmod, n, 520), 7, dtype=torch.int16, device="cuda") for _ in range(2)]
+    eng.set_mirror_ptrs(1, n, mirrors)
+    q = synth_query(5, eng.K, n, eng.moduli)
+    qd.copy_(torch.from_numpy(q.view(np.int16)))
+    eng.run_device(None, n, None)
+    torch.cuda.synchronize()
+    for mbuf in mirrors:
+        assert torch.equal(mbuf, od[1])
+    # e2e (modulus chunks: mirror offsets follow the chunk)
+    q2 = synth_query(6, eng.K, n, eng.moduli)
+    out = eng.run(q2)
+    torch.cuda.synchronize()
+    for mbuf in mirrors:
+        assert (mbuf.cpu().numpy().view(np.uint16) == out[1]).all()
+    # the receive buffer of an engine, and disabling
+    view, handle = eng.alloc_recv(n)
+    assert len(handle) == 64 and tuple(view.shape) == (eng.nmod, n, 520)
+    eng.set_mirror_ptrs(0, n, [view])
+    eng.run_device(None, n, None)
+    torch.cuda.synchronize()
+    assert torch.equal(view, od[0])
+    eng.set_mirror_ptrs(0, n, [])
+    before = view.clone()
+    qd.copy_(torch.from_numpy(q.view(np.int16)))
+    eng.run_device(None, n, None)
+    torch.cuda.synchronize()
+    assert torch.equal(view, before)
