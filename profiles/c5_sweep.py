@@ -43,6 +43,7 @@ def main():
             eng.synth_db(1)
             q_dev, _ = staging_tensors(eng, N)
             q_dev.copy_(torch.from_numpy(synth_query(2, K, N, eng.moduli).view(np.int16)))
+            torch.cuda.synchronize()
             s = torch.cuda.Stream()
             eng.run_device(None, N, None, stream=s.cuda_stream)
             eng.run_device(None, N, None, q_ready=True, stream=s.cuda_stream)

@@ -137,6 +137,7 @@ def main():
             q_dev.zero_()
             r = run({}, a.secs)
             q_dev.copy_(q_rand)
+            torch.cuda.synchronize()
         elif v == "cluster2":
             r = run({"IRL_PPMM_CLUSTER": "2"}, a.secs)
         elif v == "gate0":

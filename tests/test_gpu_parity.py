@@ -389,6 +389,7 @@ def test_ccmm_rescale_matches_bigint():
     q = synth_query(3, eng.K, 40, eng.moduli)
     qd, od = staging_tensors(eng, 40)
     qd.copy_(torch.from_numpy(q.view(np.int16)))
+    torch.cuda.synchronize()  # the engine runs on its own stream
     eng.run_device(None, 40, None)
     dst = torch.zeros((2, eng.nmod - 3, 40, 300), dtype=torch.int16, device="cuda")
     eng.rescale(40, dst, 3, True)
@@ -421,6 +422,7 @@ def test_ccmm_linearity_full_slice_every_element():
     t2 = torch.from_numpy(q2.astype(np.int32)).cuda()
     for q in (t1, t2, (t1 + t2) % mods):
         qd.copy_(q.to(torch.int16))
+        torch.cuda.synchronize()  # the engine runs on its own stream
         eng.run_device(None, N, None)
         torch.cuda.synchronize()
         outs.append(od.to(torch.int32) & 0xFFFF)
@@ -444,6 +446,7 @@ def test_ccmm_fused_exchange_mirrors():
     eng.set_mirror_ptrs(1, n, mirrors)
     q = synth_query(5, eng.K, n, eng.moduli)
     qd.copy_(torch.from_numpy(q.view(np.int16)))
+    torch.cuda.synchronize()  # the engine runs on its own stream
     eng.run_device(None, n, None)
     torch.cuda.synchronize()
     for mbuf in mirrors:
@@ -464,6 +467,7 @@ def test_ccmm_fused_exchange_mirrors():
     eng.set_mirror_ptrs(0, n, [])
     before = view.clone()
     qd.copy_(torch.from_numpy(q.view(np.int16)))
+    torch.cuda.synchronize()
     eng.run_device(None, n, None)
     torch.cuda.synchronize()
     assert torch.equal(view, before)
