@@ -81,9 +81,11 @@ class CcmmEngine:
 
     def run_device(self, q_res_dev, n: int, out_dev, part0: int = 0, nparts: Optional[int] = None,
                    q_ready: bool = False, stream=None):
-        """Device-resident run on torch CUDA tensors; stream-ordered, non-blocking."""
+        """Device-resident run on torch CUDA tensors; stream-ordered, non-blocking.
+        stream: a raw cudaStream_t handle; default = torch's current stream, so
+        the run is ordered after the torch ops that filled the inputs."""
         nparts = self.parts - part0 if nparts is None else nparts
-        s = C.c_void_p(stream) if stream is not None else None
+        s = C.c_void_p(stream if stream is not None else _torch_stream(self.ctx.device))
         self.ctx.check(capi.lib().irl_ccmm_run_device(
             self.handle, capi.ptr(q_res_dev) if q_res_dev is not None else None, int(q_ready), n,
             part0, nparts, capi.ptr(out_dev) if out_dev is not None else None, s))
@@ -93,7 +95,7 @@ class CcmmEngine:
         """ModDown (f2) of the engine outputs of the last device run: parts
         [part0, part0 + nparts) -> dst [nparts][nmod - drop][n][M] (CUDA tensor)."""
         nparts = self.parts - part0 if nparts is None else nparts
-        s = C.c_void_p(stream) if stream is not None else None
+        s = C.c_void_p(stream if stream is not None else _torch_stream(self.ctx.device))
         self.ctx.check(capi.lib().irl_ccmm_rescale(self.handle, n, part0, nparts, drop, int(round_),
                                                    capi.ptr(dst), s))
 
@@ -130,6 +132,15 @@ class CcmmEngine:
             self.close()
         except Exception:
             pass
+
+
+def _torch_stream(device: int) -> int:
+    """torch's current stream on `device` as a cudaStream_t handle (the legacy
+    default stream is handle 0 in torch, cudaStreamLegacy = 0x1 for the ABI,
+    where NULL means the context's own stream)."""
+    import torch
+    h = torch.cuda.current_stream(device).cuda_stream
+    return h if h else 0x1
 
 
 def synth_query(seed: int, k: int, n: int, moduli, stream: int = 0xFF) -> np.ndarray:
