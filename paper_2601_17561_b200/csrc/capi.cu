@@ -4,6 +4,7 @@
 // value-for-value, including its exception taxonomy and messages; all the
 // arithmetic runs in this library's sm_100a kernels. There is no CPU compute
 // path: validation only reads the split kernels' device-side statistics.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -49,6 +50,12 @@ struct irl_ccmm {
     size_t mirror_part = 0, mirror_n = 0, n_mirror = 0;
     uint16_t* mirror[kMaxMirrors] = {};
     bool mirror_ipc[kMaxMirrors] = {};
+    // part-granular D2H in irl_ccmm_run: per (modulus chunk, part) tile
+    // counters the epilogue bumps; the copy stream waits on them with stream
+    // memory operations (cuStreamWaitValue32) instead of on the whole launch
+    uint32_t* part_cnt = nullptr;       // [nmod][parts]
+    std::vector<cudaEvent_t> cnt_zeroed;  // per modulus chunk
+    bool memops = true;                 // cleared if stream memory ops are unavailable
 };
 
 namespace {
@@ -127,7 +134,9 @@ int run_ppmm(irl_ctx* ctx, PpmmLaunch L, uint32_t kchunk, cudaStream_t s) {
     }
     const int8_t* a0 = L.a_planes;
     const int8_t* b0 = L.b_planes;
+    uint32_t* const part_done = L.part_done;
     for (uint32_t k0 = 0; k0 < K; k0 += kchunk) {
+        L.part_done = k0 + kchunk >= K ? part_done : nullptr;  // the final K chunk completes the outputs
         L.a_planes = a0 + k0;
         L.b_planes = b0 + k0;
         L.K = std::min(kchunk, K - k0);
@@ -809,11 +818,14 @@ int irl_ccmm_create(irl_ctx* ctx, size_t parts, size_t m, size_t k, size_t max_n
     if (err == cudaSuccess) err = cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking);
     if (err == cudaSuccess) err = cudaStreamCreateWithFlags(&e->h2d_stream, cudaStreamNonBlocking);
     if (err == cudaSuccess) err = cudaMemsetAsync(e->db, 0, db_b, ctx->stream);
+    if (err == cudaSuccess) err = cudaMalloc(&e->part_cnt, nmod * parts * sizeof(uint32_t));
     e->part_done.resize(nmod);
     e->h2d_done.resize(nmod);
+    e->cnt_zeroed.resize(nmod);
     for (size_t i = 0; err == cudaSuccess && i < nmod; ++i) {
         err = cudaEventCreateWithFlags(&e->part_done[i], cudaEventDisableTiming);
         if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e->h2d_done[i], cudaEventDisableTiming);
+        if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e->cnt_zeroed[i], cudaEventDisableTiming);
     }
     if (err != cudaSuccess) {
         irl_ccmm_destroy(e);
@@ -834,6 +846,9 @@ int irl_ccmm_destroy(irl_ccmm* e) {
         if (ev) cudaEventDestroy(ev);
     for (auto ev : e->h2d_done)
         if (ev) cudaEventDestroy(ev);
+    for (auto ev : e->cnt_zeroed)
+        if (ev) cudaEventDestroy(ev);
+    cudaFree(e->part_cnt);
     if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
     if (e->h2d_stream) cudaStreamDestroy(e->h2d_stream);
     cudaFree(e->db);
@@ -985,7 +1000,7 @@ int irl_ccmm_synth_db(irl_ccmm* e, uint64_t seed, uint32_t first_part) {
 // PPMMs of parts [part0, part0 + nparts) for moduli [m0, m0 + nm); `out`
 // points at the [part0][0][0][0] corner of a [parts][nmod][n][M] tensor.
 static int ccmm_parts(irl_ccmm* e, size_t n, size_t part0, size_t nparts, uint16_t* out,
-                      cudaStream_t s, size_t m0 = 0, size_t nm = 0) {
+                      cudaStream_t s, size_t m0 = 0, size_t nm = 0, uint32_t* part_done = nullptr) {
     irl_ctx* ctx = e->ctx;
     if (nm == 0) nm = e->nmod;
     ModTable sub{};
@@ -1003,6 +1018,7 @@ static int ccmm_parts(irl_ccmm* e, size_t n, size_t part0, size_t nparts, uint16
     L.a_part_rows = e->nmod * 2 * e->M;
     L.out_part_elems = e->nmod * n * e->M;
     L.progress = e->progress;
+    L.part_done = part_done;
     if (e->n_mirror && n == e->mirror_n && e->mirror_part >= part0 && e->mirror_part < part0 + nparts) {
         L.n_mirror = static_cast<uint32_t>(e->n_mirror);
         L.mirror_part = static_cast<uint32_t>(e->mirror_part - part0);
@@ -1033,6 +1049,22 @@ int irl_ccmm_run_device(irl_ccmm* e, const uint16_t* q_res_dev, int q_ready, siz
 // One column chunk [n0, n0 + w) of an e2e run (query columns of the host
 // batch of width n), pipelined by modulus chunks: H2D of chunk c+1 and D2H of
 // chunk c-1 run on their own streams while chunk c is split and multiplied.
+// cuStreamWaitValue32 (driver API, resolved once); nullptr if unavailable.
+using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static WaitValueFn wait_value_fn() {
+    static WaitValueFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            return static_cast<WaitValueFn>(nullptr);
+        }
+        return reinterpret_cast<WaitValueFn>(p);
+    }();
+    return fn;
+}
+
 static int ccmm_run_columns(irl_ccmm* e, const uint16_t* q_res_host, size_t n, size_t n0, size_t w,
                             uint16_t* out_host) {
     irl_ctx* ctx = e->ctx;
@@ -1057,14 +1089,32 @@ static int ccmm_run_columns(irl_ccmm* e, const uint16_t* q_res_host, size_t n, s
         sizes.insert(sizes.end(), tail.rbegin(), tail.rend());
         for (size_t g : sizes) bounds.push_back(bounds.back() + g);
     }
+    // IRL_E2E_TRACE=1: per-chunk H2D / PPMM / D2H completion times on stderr
+    static const bool trace = std::getenv("IRL_E2E_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    auto mark = [&](cudaStream_t st) {
+        if (!trace) return;
+        cudaEvent_t ev;
+        cudaEventCreate(&ev);
+        cudaEventRecord(ev, st);
+        tev.push_back(ev);
+    };
+    mark(s);
     IRL_CK(ctx, cudaEventRecord(e->part_done[0], s));  // order after prior work on s
     IRL_CK(ctx, cudaStreamWaitEvent(e->h2d_stream, e->part_done[0], 0));
     for (size_t ci = 0; ci + 1 < bounds.size(); ++ci) {
         const size_t c0 = bounds[ci], nc = bounds[ci + 1] - c0;
         // rows (modulus, k) of the host [nmod][K][n] batch, columns [n0, n0 + w)
-        IRL_CK(ctx, cudaMemcpy2DAsync(e->qres + c0 * K * w, w * 2, q_res_host + c0 * K * n + n0, n * 2, w * 2,
-                                      nc * K, cudaMemcpyHostToDevice, e->h2d_stream));
+        // (one linear copy when the batch is a single column chunk: 2-D DMA of
+        // short rows runs at a fraction of PCIe bandwidth)
+        if (w == n)
+            IRL_CK(ctx, cudaMemcpyAsync(e->qres + c0 * K * w, q_res_host + c0 * K * n, nc * K * n * 2,
+                                        cudaMemcpyHostToDevice, e->h2d_stream));
+        else
+            IRL_CK(ctx, cudaMemcpy2DAsync(e->qres + c0 * K * w, w * 2, q_res_host + c0 * K * n + n0, n * 2, w * 2,
+                                          nc * K, cudaMemcpyHostToDevice, e->h2d_stream));
         IRL_CK(ctx, cudaEventRecord(e->h2d_done[ci], e->h2d_stream));
+        mark(e->h2d_stream);
     }
     for (size_t ci = 0; ci + 1 < bounds.size(); ++ci) {
         const size_t c0 = bounds[ci], nc = bounds[ci + 1] - c0;
@@ -1074,19 +1124,75 @@ static int ccmm_run_columns(irl_ccmm* e, const uint16_t* q_res_host, size_t n, s
         for (size_t i = 0; i < nc; ++i) sub.mc[i] = e->mt.mc[c0 + i];
         IRL_LAUNCH(ctx, launch_split_cols<uint16_t>(e->qres + c0 * K * w, w, K * w, uint32_t(K), uint32_t(w), sub,
                                                     e->qplanes + c0 * 2 * w * e->ldk, e->ldk, nullptr, s));
-        int st = ccmm_parts(e, w, 0, e->parts, e->out, s, c0, nc);
+        // part-granular D2H: each part's copy starts once its tiles are stored
+        // (epilogue counters + cuStreamWaitValue32 on the copy stream), so the
+        // copies overlap the rest of the launch instead of waiting for all of it
+        const bool by_part = e->memops && wait_value_fn() != nullptr && e->parts > 1;
+        uint32_t* cnt = e->part_cnt + c0 * e->parts;
+        if (by_part) {
+            IRL_CK(ctx, cudaMemsetAsync(cnt, 0, e->parts * sizeof(uint32_t), s));
+            IRL_CK(ctx, cudaEventRecord(e->cnt_zeroed[ci], s));
+            IRL_CK(ctx, cudaStreamWaitEvent(e->copy_stream, e->cnt_zeroed[ci], 0));
+        }
+        int st = ccmm_parts(e, w, 0, e->parts, e->out, s, c0, nc, by_part ? cnt : nullptr);
         if (st) return st;
+        const uint32_t target = ppmm_last_part_target();
         IRL_CK(ctx, cudaEventRecord(e->part_done[ci], s));
+        bool waited = false;
+        if (by_part && target > 0) {
+            waited = true;
+            for (size_t p = 0; p < e->parts && waited; ++p) {
+                const CUresult r = wait_value_fn()(e->copy_stream, reinterpret_cast<CUdeviceptr>(cnt + p), target,
+                                                   CU_STREAM_WAIT_VALUE_GEQ);
+                if (r != CUDA_SUCCESS) {
+                    if (p != 0) return set_err(ctx, IRL_ERR_CUDA, "cuStreamWaitValue32 failed mid-chunk");
+                    e->memops = false;  // unavailable here: whole-launch events from now on
+                    waited = false;
+                    break;
+                }
+                if (w == n)
+                    IRL_CK(ctx, cudaMemcpyAsync(out_host + (p * nmod + c0) * n * M, e->out + (p * nmod + c0) * w * M,
+                                                nc * n * M * 2, cudaMemcpyDeviceToHost, e->copy_stream));
+                else
+                    IRL_CK(ctx, cudaMemcpy2DAsync(out_host + ((p * nmod + c0) * n + n0) * M, n * M * 2,
+                                                  e->out + (p * nmod + c0) * w * M, w * M * 2, w * M * 2, nc,
+                                                  cudaMemcpyDeviceToHost, e->copy_stream));
+            }
+        }
+        if (waited) {
+            mark(s);
+            mark(e->copy_stream);
+            continue;
+        }
         IRL_CK(ctx, cudaStreamWaitEvent(e->copy_stream, e->part_done[ci], 0));
         for (size_t p = 0; p < e->parts; ++p) {
             // device [p][i][w][M] -> host [p][i][n][M] at column n0
-            IRL_CK(ctx, cudaMemcpy2DAsync(out_host + ((p * nmod + c0) * n + n0) * M, n * M * 2,
-                                          e->out + (p * nmod + c0) * w * M, w * M * 2, w * M * 2, nc,
-                                          cudaMemcpyDeviceToHost, e->copy_stream));
+            if (w == n)
+                IRL_CK(ctx, cudaMemcpyAsync(out_host + (p * nmod + c0) * n * M, e->out + (p * nmod + c0) * w * M,
+                                            nc * n * M * 2, cudaMemcpyDeviceToHost, e->copy_stream));
+            else
+                IRL_CK(ctx, cudaMemcpy2DAsync(out_host + ((p * nmod + c0) * n + n0) * M, n * M * 2,
+                                              e->out + (p * nmod + c0) * w * M, w * M * 2, w * M * 2, nc,
+                                              cudaMemcpyDeviceToHost, e->copy_stream));
         }
+        mark(s);
+        mark(e->copy_stream);
     }
     IRL_CK(ctx, cudaStreamSynchronize(e->copy_stream));
     IRL_CK(ctx, cudaStreamSynchronize(s));
+    if (trace) {
+        const size_t nch = bounds.size() - 1;
+        std::fprintf(stderr, "[irl e2e] chunks %zu (h2d done | ppmm done | d2h done, ms from start)\n", nch);
+        for (size_t ci = 0; ci < nch; ++ci) {
+            float th = 0, tp = 0, td = 0;
+            cudaEventElapsedTime(&th, tev[0], tev[1 + ci]);
+            cudaEventElapsedTime(&tp, tev[0], tev[1 + nch + 2 * ci]);
+            cudaEventElapsedTime(&td, tev[0], tev[2 + nch + 2 * ci]);
+            std::fprintf(stderr, "[irl e2e] chunk %zu (%zu moduli): %8.2f %8.2f %8.2f\n", ci,
+                         bounds[ci + 1] - bounds[ci], th, tp, td);
+        }
+        for (auto ev : tev) cudaEventDestroy(ev);
+    }
     return IRL_OK;
 }
 

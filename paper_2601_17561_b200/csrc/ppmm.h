@@ -57,6 +57,9 @@ struct PpmmLaunch {
     uint16_t* mirror[kMaxMirrors] = {};
     uint32_t n_mirror = 0;
     uint32_t mirror_part = 0;
+    // Optional per-part completion counters (zeroed by the caller): every
+    // epilogue warp adds 1 per finished tile (ppmm_last_part_target() per part).
+    uint32_t* part_done = nullptr;
     int mode = kModePsq;
     int32_t* out_i32[2] = {nullptr, nullptr};  // kModeInner outputs [parts][nprimes][N][M]
     int cluster_pm = 1;
@@ -65,6 +68,9 @@ struct PpmmLaunch {
 };
 
 cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream);
+// Value part_done[g] reaches once every tile of one part of the calling
+// thread's last launch_ppmm_planes is stored.
+uint32_t ppmm_last_part_target();
 // Kernels the calling thread's last launch_ppmm_planes issued (main + filler).
 uint32_t ppmm_kernels_last_launch();
 size_t ppmm_smem_bytes();

@@ -88,6 +88,7 @@ struct __align__(64) GemmArgs {
     int32_t* out_i32[2];              // kMode == kModeInner: acc1 / acc2 as int32 [n][m] (nullable)
     uint16_t* mirror[kMaxMirrors];    // peer copies of part mirror_part's outputs (see PpmmLaunch)
     uint32_t n_mirror, mirror_part;
+    uint32_t* part_done;              // optional [parts] count of (epilogue warp, tile) completions
     uint32_t* progress;               // [clusters] K blocks issued by each pair's leader producer
     uint32_t* counter;                // next unit to hand out (dynamic schedule)
     unsigned long long* mailbox;      // [groups][kMail] ((seq+1) << 32 | unit) published per group
@@ -588,6 +589,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_cluster(leader_tmem_empty);
+            if (args.part_done) {
+                // per-part completion count (stream memory ops start that
+                // part's D2H as soon as all its tiles are stored)
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) atomicAdd(args.part_done + tc.part, 1u);
+            }
             if (diag) busy_epi += static_cast<unsigned long long>(clock64() - e0);
         }
         if (diag) {
@@ -735,11 +743,15 @@ size_t ppmm_smem_bytes() { return kSmemBytes; }
 
 namespace {
 thread_local uint32_t g_last_kernels = 0;
+thread_local uint32_t g_last_part_target = 0;
 }
 uint32_t ppmm_kernels_last_launch() { return g_last_kernels; }
 
+uint32_t ppmm_last_part_target() { return g_last_part_target; }
+
 cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     g_last_kernels = 0;
+    g_last_part_target = 0;
     if (L.nprimes == 0 || L.parts == 0 || L.M == 0 || L.N == 0) return cudaSuccess;
     if (L.nprimes > kMaxPrimesPerLaunch) return cudaErrorInvalidValue;
     if (L.ldk % 16 != 0 || L.ldk < L.K) return cudaErrorInvalidValue;
@@ -789,12 +801,16 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
         if (si != 0 && args.n_blocks % shp.pn != 0) return cudaErrorInvalidValue;
     }
     args.units = args.m_units * args.n_chunks * L.parts * L.nprimes;
+    // every tile of a part (padding tiles included) is finished by 2 CTAs x kEpiWarps warps
+    g_last_part_target = L.nprimes * args.m_units * args.unit_mblocks * args.n_chunks * args.chunk_tiles * 2u *
+                         static_cast<uint32_t>(kEpiWarps);
     args.accumulate = L.accumulate ? 1u : 0u;
     args.a_part_rows = static_cast<uint32_t>(a_part_rows);
     args.out_part = L.out_part_elems ? L.out_part_elems
                                      : static_cast<unsigned long long>(L.nprimes) * L.N * L.M;
     args.out = L.out;
     if (L.n_mirror > kMaxMirrors || (L.n_mirror && L.mode != kModePsq)) return cudaErrorInvalidValue;
+    args.part_done = L.part_done;
     args.n_mirror = L.n_mirror;
     args.mirror_part = L.mirror_part;
     for (uint32_t i = 0; i < L.n_mirror; ++i) args.mirror[i] = L.mirror[i];
