@@ -1070,12 +1070,21 @@ static int ccmm_run_columns(irl_ccmm* e, const uint16_t* q_res_host, size_t n, s
     irl_ctx* ctx = e->ctx;
     cudaStream_t s = ctx->stream;
     const size_t nmod = e->nmod, K = e->K, M = e->M;
-    // Modulus chunks graded 1, 2, 3, ..., 3, 2, 1: the first H2D and the last
-    // D2H (the unhidden head and tail of the pipeline) move one modulus.
+    // Modulus chunks. With stream memory ops (part-granular D2H below) the
+    // pipeline is 1, 3, rest: the first GEMM starts after one modulus of H2D,
+    // the second chunk's GEMMs cover the H2D of everything else, and the big
+    // last launch streams each (modulus, part) block out as soon as its tiles
+    // are stored -- three launches, so three launch tails. Without them the
+    // chunks are graded 1, 2, 3, ..., 3, 2, 1 (whole-chunk D2H, short tail).
+    const bool memops = e->memops && wait_value_fn() != nullptr;
     std::vector<size_t> bounds{0};
     {
         std::vector<size_t> sizes;
         size_t left = nmod;
+        if (memops && nmod >= 6) {
+            sizes = {1, 3, nmod - 4};
+            left = 0;
+        }
         for (size_t g : {1, 2})
             if (left > 2 * g) sizes.push_back(g), left -= g;
         std::vector<size_t> tail;
@@ -1087,6 +1096,19 @@ static int ccmm_run_columns(irl_ccmm* e, const uint16_t* q_res_host, size_t n, s
             left -= g;
         }
         sizes.insert(sizes.end(), tail.rbegin(), tail.rend());
+        if (const char* env = std::getenv("IRL_E2E_CHUNKS")) {  // experiment knob: "1,2,3,6,..."
+            std::vector<size_t> alt;
+            size_t sum = 0;
+            for (const char* c = env; *c;) {
+                char* end = nullptr;
+                const long v = std::strtol(c, &end, 10);
+                if (end == c || v <= 0) break;
+                alt.push_back(static_cast<size_t>(v));
+                sum += static_cast<size_t>(v);
+                c = *end == ',' ? end + 1 : end;
+            }
+            if (sum == nmod) sizes = alt;
+        }
         for (size_t g : sizes) bounds.push_back(bounds.back() + g);
     }
     // IRL_E2E_TRACE=1: per-chunk H2D / PPMM / D2H completion times on stderr
@@ -1127,10 +1149,10 @@ static int ccmm_run_columns(irl_ccmm* e, const uint16_t* q_res_host, size_t n, s
         // part-granular D2H: each part's copy starts once its tiles are stored
         // (epilogue counters + cuStreamWaitValue32 on the copy stream), so the
         // copies overlap the rest of the launch instead of waiting for all of it
-        const bool by_part = e->memops && wait_value_fn() != nullptr && e->parts > 1;
+        const bool by_part = memops && e->memops;
         uint32_t* cnt = e->part_cnt + c0 * e->parts;
         if (by_part) {
-            IRL_CK(ctx, cudaMemsetAsync(cnt, 0, e->parts * sizeof(uint32_t), s));
+            IRL_CK(ctx, cudaMemsetAsync(cnt, 0, nc * e->parts * sizeof(uint32_t), s));
             IRL_CK(ctx, cudaEventRecord(e->cnt_zeroed[ci], s));
             IRL_CK(ctx, cudaStreamWaitEvent(e->copy_stream, e->cnt_zeroed[ci], 0));
         }
@@ -1140,23 +1162,28 @@ static int ccmm_run_columns(irl_ccmm* e, const uint16_t* q_res_host, size_t n, s
         IRL_CK(ctx, cudaEventRecord(e->part_done[ci], s));
         bool waited = false;
         if (by_part && target > 0) {
+            // one (modulus, part) block at a time, in the order the launch
+            // completes them (prime-major units)
             waited = true;
-            for (size_t p = 0; p < e->parts && waited; ++p) {
-                const CUresult r = wait_value_fn()(e->copy_stream, reinterpret_cast<CUdeviceptr>(cnt + p), target,
-                                                   CU_STREAM_WAIT_VALUE_GEQ);
-                if (r != CUDA_SUCCESS) {
-                    if (p != 0) return set_err(ctx, IRL_ERR_CUDA, "cuStreamWaitValue32 failed mid-chunk");
-                    e->memops = false;  // unavailable here: whole-launch events from now on
-                    waited = false;
-                    break;
+            for (size_t i = 0; i < nc && waited; ++i) {
+                for (size_t p = 0; p < e->parts; ++p) {
+                    const CUresult r = wait_value_fn()(e->copy_stream, reinterpret_cast<CUdeviceptr>(cnt + i * e->parts + p),
+                                                       target, CU_STREAM_WAIT_VALUE_GEQ);
+                    if (r != CUDA_SUCCESS) {
+                        if (i != 0 || p != 0) return set_err(ctx, IRL_ERR_CUDA, "cuStreamWaitValue32 failed mid-chunk");
+                        e->memops = false;  // unavailable here: whole-launch events from now on
+                        waited = false;
+                        break;
+                    }
+                    const size_t row = p * nmod + c0 + i;  // [part][modulus] block of n x M
+                    if (w == n)
+                        IRL_CK(ctx, cudaMemcpyAsync(out_host + row * n * M, e->out + row * w * M, n * M * 2,
+                                                    cudaMemcpyDeviceToHost, e->copy_stream));
+                    else
+                        IRL_CK(ctx, cudaMemcpy2DAsync(out_host + (row * n + n0) * M, n * M * 2, e->out + row * w * M,
+                                                      w * M * 2, w * M * 2, 1, cudaMemcpyDeviceToHost,
+                                                      e->copy_stream));
                 }
-                if (w == n)
-                    IRL_CK(ctx, cudaMemcpyAsync(out_host + (p * nmod + c0) * n * M, e->out + (p * nmod + c0) * w * M,
-                                                nc * n * M * 2, cudaMemcpyDeviceToHost, e->copy_stream));
-                else
-                    IRL_CK(ctx, cudaMemcpy2DAsync(out_host + ((p * nmod + c0) * n + n0) * M, n * M * 2,
-                                                  e->out + (p * nmod + c0) * w * M, w * M * 2, w * M * 2, nc,
-                                                  cudaMemcpyDeviceToHost, e->copy_stream));
             }
         }
         if (waited) {

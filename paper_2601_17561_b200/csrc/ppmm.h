@@ -57,8 +57,9 @@ struct PpmmLaunch {
     uint16_t* mirror[kMaxMirrors] = {};
     uint32_t n_mirror = 0;
     uint32_t mirror_part = 0;
-    // Optional per-part completion counters (zeroed by the caller): every
-    // epilogue warp adds 1 per finished tile (ppmm_last_part_target() per part).
+    // Optional [nprimes][parts] completion counters (zeroed by the caller):
+    // every epilogue warp adds 1 per finished tile of that (prime, part);
+    // ppmm_last_part_target() is the final count of each.
     uint32_t* part_done = nullptr;
     int mode = kModePsq;
     int32_t* out_i32[2] = {nullptr, nullptr};  // kModeInner outputs [parts][nprimes][N][M]
@@ -68,8 +69,8 @@ struct PpmmLaunch {
 };
 
 cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream);
-// Value part_done[g] reaches once every tile of one part of the calling
-// thread's last launch_ppmm_planes is stored.
+// Value each part_done[prime][part] reaches once every tile of that (prime,
+// part) of the calling thread's last launch_ppmm_planes is stored.
 uint32_t ppmm_last_part_target();
 // Kernels the calling thread's last launch_ppmm_planes issued (main + filler).
 uint32_t ppmm_kernels_last_launch();

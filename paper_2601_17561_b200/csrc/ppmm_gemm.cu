@@ -88,7 +88,7 @@ struct __align__(64) GemmArgs {
     int32_t* out_i32[2];              // kMode == kModeInner: acc1 / acc2 as int32 [n][m] (nullable)
     uint16_t* mirror[kMaxMirrors];    // peer copies of part mirror_part's outputs (see PpmmLaunch)
     uint32_t n_mirror, mirror_part;
-    uint32_t* part_done;              // optional [parts] count of (epilogue warp, tile) completions
+    uint32_t* part_done;              // optional [nprimes][parts] count of (epilogue warp, tile) completions
     uint32_t* progress;               // [clusters] K blocks issued by each pair's leader producer
     uint32_t* counter;                // next unit to hand out (dynamic schedule)
     unsigned long long* mailbox;      // [groups][kMail] ((seq+1) << 32 | unit) published per group
@@ -594,7 +594,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                 // part's D2H as soon as all its tiles are stored)
                 __threadfence();
                 __syncwarp();
-                if (lane == 0) atomicAdd(args.part_done + tc.part, 1u);
+                if (lane == 0) atomicAdd(args.part_done + tc.prime * args.parts + tc.part, 1u);
             }
             if (diag) busy_epi += static_cast<unsigned long long>(clock64() - e0);
         }
@@ -801,8 +801,8 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
         if (si != 0 && args.n_blocks % shp.pn != 0) return cudaErrorInvalidValue;
     }
     args.units = args.m_units * args.n_chunks * L.parts * L.nprimes;
-    // every tile of a part (padding tiles included) is finished by 2 CTAs x kEpiWarps warps
-    g_last_part_target = L.nprimes * args.m_units * args.unit_mblocks * args.n_chunks * args.chunk_tiles * 2u *
+    // every tile of a (prime, part) (padding tiles included) is finished by 2 CTAs x kEpiWarps warps
+    g_last_part_target = args.m_units * args.unit_mblocks * args.n_chunks * args.chunk_tiles * 2u *
                          static_cast<uint32_t>(kEpiWarps);
     args.accumulate = L.accumulate ? 1u : 0u;
     args.a_part_rows = static_cast<uint32_t>(a_part_rows);
