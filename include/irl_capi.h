@@ -166,7 +166,9 @@ int irl_ccmm_synth_db(irl_ccmm* e, uint64_t seed, uint32_t first_part);
  * Copies in, splits, multiplies every part, copies out; blocks. N may exceed
  * max_n: the batch then streams through the engine in column chunks
  * (max_n rounded down to whole 256-column tiles), e.g. the c5 corner of 256
- * eyes x 31 rotations against 2^17-template slices. */
+ * eyes x 31 rotations against 2^17-template slices. Host buffers should be
+ * pinned (cudaHostAlloc / cudaHostRegister): pageable buffers are staged by the
+ * driver and copy at a fraction of PCIe bandwidth. */
 int irl_ccmm_run(irl_ccmm* e, const uint16_t* q_res_host, size_t n, uint16_t* out_host);
 /* Device-resident variant over parts [part0, part0 + nparts): q_res_dev
  * [nmod][K][N] (split into the engine's query planes unless q_ready != 0),
