@@ -505,7 +505,11 @@ def main():
                              "frac": achieved / peak, "traffic": traffic,
                              "kernel": "ppmm_i8_sm100_kernel", "launch_ms": launch_ms,
                              "ops_per_launch": launch_ops, "peak_source": peak_src,
-                             "frac_of_datasheet_4500": achieved / DATASHEET_INT8_TOPS},
+                             "frac_of_datasheet_4500": achieved / DATASHEET_INT8_TOPS,
+                             "frac_of_2x_bf16_burst": (achieved / (2.0 * float(peaks["bf16_tflops"]))
+                                                       if "bf16_tflops" in peaks else None),
+                             "frac_of_live_cublas_int8": (achieved / int8_ref["sustained_tops"]
+                                                          if int8_ref else None)},
                 "split_roofline": split_roof, "moddown": moddown, "int8_library_ref": int8_ref,
                 "exchange": None if world == 1 else {
                     "kind": "fused P2P stores in the a-part PPMM epilogue (CUDA IPC, NVLink)" if exchange == "mirror"

@@ -25,7 +25,7 @@ constexpr int kModeInner = 1;
 constexpr uint32_t kStatSlots = 16;
 // Device scratch the PPMM launcher needs (progress counters, unit counter,
 // per-group unit mailboxes); zeroed by every launch.
-constexpr size_t kScheduleScratchBytes = 64 * 1024;
+constexpr size_t kScheduleScratchBytes = 4 << 20;
 
 // One batched PPMM launch over `parts` database parts and `nprimes` moduli.
 //   a_planes: [parts][nprimes][2][M][ldk] int8 centred digits (K-major)

@@ -79,6 +79,8 @@ struct __align__(64) GemmArgs {
     // group schedule (see group_of): G = clusters per full group
     uint32_t G, F, L, active_clusters;
     uint32_t dynamic;                 // 1: units from an atomic counter; 0: static super-rounds
+    uint32_t mail_slots;              // per-group mailbox ring (units + 1 when the scratch allows, so a
+                                      // member started late never finds its slot overwritten)
     uint32_t gate_lead;               // max K blocks a pair may lead its group (0: no gating)
     uint32_t a_evict_first;           // DB tiles read exactly once from L2 (G == 1): evict-first policy
     uint32_t accumulate;
@@ -91,13 +93,13 @@ struct __align__(64) GemmArgs {
     uint32_t* part_done;              // optional [nprimes][parts] count of (epilogue warp, tile) completions
     uint32_t* progress;               // [clusters] K blocks issued by each pair's leader producer
     uint32_t* counter;                // next unit to hand out (dynamic schedule)
-    unsigned long long* mailbox;      // [groups][kMail] ((seq+1) << 32 | unit) published per group
+    unsigned long long* mailbox;      // [groups][mail_slots] ((seq+1) << 32 | unit) published per group
     unsigned long long* stats;        // optional [clusters][kStatSlots] diagnostics (see ppmm.h)
     ModConst mc[kMaxPrimesPerLaunch];
 };
 
 constexpr int kRing = 4;              // tile-descriptor ring (producer -> MMA / epilogue)
-constexpr uint32_t kMail = 64;        // mailbox slots per group
+constexpr uint32_t kMinMail = 64;     // mailbox slots per group (at least; see GemmArgs::mail_slots)
 constexpr uint32_t kEnd = 0xFFFFFFFFu;
 
 // Diagnostics: wait on a barrier and add the cycles spent to *acc.
@@ -247,7 +249,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             const bool gate = rank == 0 && grp.size > 1 && args.gate_lead > 0;
             const uint32_t lead = args.gate_lead;
             const bool writer = rank == 0 && grp.member == 0;  // takes units for the group
-            unsigned long long* mbox = args.mailbox + static_cast<size_t>(grp.id) * kMail;
+            unsigned long long* mbox = args.mailbox + static_cast<size_t>(grp.id) * args.mail_slots;
             const uint32_t tiles_per_unit = grp.solo ? args.chunk_tiles / kPN : 1;
             const uint32_t m_passes = args.unit_mblocks / kPM;
             uint32_t issued = 0;  // cumulative K blocks (comparable across the group)
@@ -275,7 +277,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             };
             auto publish = [&](uint32_t seq, uint32_t u) {
                 // tag = seq + 1 so the zeroed mailbox never matches
-                st_relaxed_u64(mbox + seq % kMail,
+                st_relaxed_u64(mbox + seq % args.mail_slots,
                                (static_cast<unsigned long long>(seq + 1) << 32) | u);
             };
             auto push_tile = [&](uint32_t u, uint32_t mb_sub, uint32_t nb) {
@@ -306,7 +308,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                     }
                 } else {
                     unsigned long long v;
-                    while (((v = ld_relaxed_u64(mbox + seq % kMail)) >> 32) != seq + 1) {
+                    while (((v = ld_relaxed_u64(mbox + seq % args.mail_slots)) >> 32) != seq + 1) {
                         __nanosleep(64);
                     }
                     u = static_cast<uint32_t>(v);
@@ -858,8 +860,13 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
                          kShapes[parts[i].si].pm, kShapes[parts[i].si].pn, parts[i].clusters,
                          parts[i].clusters * kShapes[parts[i].si].ctas(), args.units);
     }
-    const size_t scratch = (kProgressWords + 32) * 4 + static_cast<size_t>(groups_used) * kMail * 8;
-    if (scratch > kScheduleScratchBytes || pairs_used > kProgressWords) return cudaErrorInvalidValue;
+    const size_t header = (kProgressWords + 32) * 4;
+    const size_t fit = groups_used ? (kScheduleScratchBytes - header) / (static_cast<size_t>(groups_used) * 8) : 0;
+    const uint32_t mail_slots = static_cast<uint32_t>(std::min<size_t>(static_cast<size_t>(args.units) + 1, fit));
+    if (mail_slots < std::min<uint32_t>(kMinMail, args.units + 1) || pairs_used > kProgressWords)
+        return cudaErrorInvalidValue;
+    args.mail_slots = mail_slots;
+    const size_t scratch = header + static_cast<size_t>(groups_used) * mail_slots * 8;
     cudaError_t e = cudaMemsetAsync(L.progress, 0, scratch, stream);
     if (e != cudaSuccess) return e;
 
@@ -885,7 +892,7 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
         a.a_evict_first = (sh.pn > 1 && a.G == 1 && !std::getenv("IRL_PPMM_A_NORMAL")) ? 1u : 0u;
         a.progress = L.progress + pt.pair0;  // indexed by cluster id (< pairs of this launch)
         a.mailbox = reinterpret_cast<unsigned long long*>(L.progress + kProgressWords + 32) +
-                    static_cast<size_t>(pt.group0) * kMail;
+                    static_cast<size_t>(pt.group0) * mail_slots;
         a.stats = L.stats ? reinterpret_cast<unsigned long long*>(L.stats) + pt.pair0 * kStatSlots
                           : nullptr;
         CUtensorMap ma, mb;
