@@ -1081,8 +1081,29 @@ static int ccmm_run_columns(irl_ccmm* e, const uint16_t* q_res_host, size_t n, s
     {
         std::vector<size_t> sizes;
         size_t left = nmod;
-        if (memops && nmod >= 6) {
-            sizes = {1, 3, nmod - 4};
+        // Chunk planner (stream memory ops available): simulate the pipeline
+        // with per-modulus GEMM time g (6 M w K parts ops at ~2.9 POPS plus a
+        // launch) and H2D time h (2 K w bytes at ~50 GB/s). The first chunk is
+        // one modulus; each next chunk takes every modulus whose residues have
+        // landed by the time the previous chunk's GEMMs end, so the GEMMs never
+        // wait on PCIe when they can help it and launches stay few. c4 on one
+        // GPU plans 1, 7, 16; one part per GPU (N = 8, H2D-bound) plans one
+        // modulus per chunk; two parts 1, 1, 2, 4, 7, 9.
+        if (memops) {
+            const double g = 6.0 * double(M) * double(w) * double(K) * double(e->parts) / 2.9e15 + 5e-5;
+            const double h = 2.0 * double(K) * double(w) / 50e9;
+            double gemm_end = h + g;  // first chunk: one modulus
+            size_t assigned = std::min<size_t>(1, nmod);
+            sizes.push_back(assigned);
+            while (assigned < nmod) {
+                size_t landed = static_cast<size_t>(gemm_end / h);
+                landed = std::min(nmod, std::max(landed, assigned + 1));
+                const size_t c = landed - assigned;
+                const double start = std::max(gemm_end, double(landed) * h);
+                gemm_end = start + double(c) * g;
+                sizes.push_back(c);
+                assigned += c;
+            }
             left = 0;
         }
         for (size_t g : {1, 2})

@@ -99,7 +99,8 @@ struct __align__(64) GemmArgs {
 };
 
 constexpr int kRing = 4;              // tile-descriptor ring (producer -> MMA / epilogue)
-constexpr uint32_t kMinMail = 64;     // mailbox slots per group (at least; see GemmArgs::mail_slots)
+constexpr uint32_t kMinMail = 64;
+constexpr uint64_t kSmallLaunchBlocks = 256;  // below this many (m-block, part, prime) units: plain pairs     // mailbox slots per group (at least; see GemmArgs::mail_slots)
 constexpr uint32_t kEnd = 0xFFFFFFFFu;
 
 // Diagnostics: wait on a barrier and add the cycles spent to *acc.
@@ -779,6 +780,12 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     int si = shape_index(L.cluster_pm, L.cluster_pn);
     if (L.mode == kModeInner && si != 0) si = 2;  // inner-product mode is built for 1x1 and 1x4
     if (si < 0) si = 0;
+    // Short launches (a few waves of units) finish sooner on plain pairs: 74
+    // workers instead of 15 clusters + a filler whose solo pairs sweep a whole
+    // unit alone. Multicast shapes pay off on long launches (DRAM/L2 energy).
+    if (si != 0 && L.mode == kModePsq && !std::getenv("IRL_PPMM_CLUSTER") &&
+        static_cast<uint64_t>(args.m_blocks) * L.parts * L.nprimes < kSmallLaunchBlocks)
+        si = 0;
     if (args.n_blocks < static_cast<uint32_t>(kShapes[si].pn))
         si = (L.mode == kModePsq && args.n_blocks % 2 == 0 && kShapes[si].pm == 1) ? 1 : 0;
     const uint32_t occ2 = max_active_clusters(0, dev);
