@@ -55,7 +55,15 @@ def parse():
     ap.add_argument("--exchange", choices=["auto", "mirror", "broadcast"], default="auto",
                     help="a-part exchange at N>1: fused P2P epilogue stores (mirror, validated in warm-up, "
                          "falls back to broadcast) or the NCCL broadcast")
-    return ap.parse_args()
+    ap.add_argument("--config", choices=["c2", "c3", "c4"], default="c4",
+                    help="BASELINE.json config: c2 one DB slice as one PPMM (K = 2^14), c3 a-part + one "
+                         "b-part, c4 the full 8-part DB (default; the headline metric)")
+    a = ap.parse_args()
+    if a.config == "c2":
+        a.parts, a.k = 1, 1 << 14
+    elif a.config == "c3":
+        a.parts = 2
+    return a
 
 
 # ---------------------------------------------------------------------------
@@ -118,7 +126,7 @@ class Clocks:
 # CPU reference leg (oracle/_ref = unmodified reference modmat.cpp; else the port)
 # ---------------------------------------------------------------------------
 
-def cpu_reference_sample(args, moduli, q_host=None, rows=None, threads=None, parts=(0, 1)):
+def cpu_reference_sample(args, moduli, q_host=None, rows=None, threads=None, parts=None):
     """Times the reference gemm_mod_psq (modmat.cpp:143-160) on a bounded sample
     of the same workload: `rows` DB rows x full K x all N query columns, for
     every modulus of parts `parts`; tasks spread over host threads (the
@@ -129,6 +137,7 @@ def cpu_reference_sample(args, moduli, q_host=None, rows=None, threads=None, par
 
     rows = rows or args.cpu_rows
     threads = threads or os.cpu_count() or 1
+    parts = parts if parts is not None else tuple(range(min(2, args.parts)))
     K, N = args.k, args.eyes * args.rot
     if q_host is None:
         from paper_2601_17561_b200.ccmm import synth_query
@@ -200,9 +209,16 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+WORKLOADS = {
+    "c2": "c2: full-RNS PPMM mod Q on one DB slice, 992 query columns x d = 2^14 x 2^14 templates",
+    "c3": "c3: RGSW CCMM a-part + one b-part (2 K-concatenated PPMMs, N_db = 2^14, K = 2^14 + 2^13)",
+    "c4": "c4: 32x31 query batch vs full DB 7*2^14 templates, 8-part RGSW layout (a-part + 7 b-parts)",
+}
+
+
 def config_dict(args, nmod):
     N = args.eyes * args.rot
-    return {"workload": "c4: 32x31 query batch vs full DB 7*2^14 templates, 8-part RGSW layout (a-part + 7 b-parts)",
+    return {"workload": WORKLOADS[args.config],
             "parts": args.parts, "templates_per_part": args.rows, "K": args.k, "query_columns": N,
             "eyes": args.eyes, "rotations": args.rot, "moduli": nmod, "log2_Q": 360.8156,
             "digit_planes": 2 * nmod, "parallelism": f"db-slices over {args.gpus} GPU(s)",
