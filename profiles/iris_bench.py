@@ -68,6 +68,29 @@ def main():
     print(json.dumps({"stage": "iris_db_match per query batch (registered database)", "n_db": a.n_db,
                       "cols": a.eyes * a.rho, "d": a.d, "ms_e2e": ms2, "tops_e2e": ops / ms2 / 1e9,
                       "h2d_bytes": int(qc.nbytes * 2), "d2h_bytes": int(bits.nbytes)}))
+    # CPU reference (unmodified iris::score, oracle/_ref) on a bounded sample:
+    # 4 templates x all 992 query columns, one thread; extrapolated to the full DB
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "tests"))
+    import oracle_lib as ol
+    if ol.ref_available():
+        sample = 4
+        unpack = lambda w, rows: np.unpackbits(w[:rows].view(np.uint8), axis=1, bitorder="little")[:, :a.d]  # noqa
+        dcs, dms = unpack(dc, sample), unpack(dm, sample)
+        qcs, qms = unpack(qc, a.eyes), unpack(qm, a.eyes)
+        rc = np.zeros((a.eyes * a.rho, a.d), np.uint8)
+        rm = np.zeros_like(rc)
+        for e in range(a.eyes):
+            for r in range(a.rho):
+                idx = (np.arange(a.d) - r) % a.d
+                rc[e * a.rho + r], rm[e * a.rho + r] = qcs[e][idx], qms[e][idx]
+        t0 = time.perf_counter()
+        ref = ol.ref_scores(rc, rm, dcs, dms)
+        secs = time.perf_counter() - t0
+        full = secs * a.n_db / sample
+        print(json.dumps({"stage": "reference iris::score (oracle/_ref), 1 thread", "sample_templates": sample,
+                          "sample_s": secs, "extrapolated_full_db_s": full,
+                          "speedup_vs_registered_gpu": full * 1e3 / ms2,
+                          "scores_finite": int(np.isfinite(ref).sum())}))
 
 
 if __name__ == "__main__":
