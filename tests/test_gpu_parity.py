@@ -471,3 +471,32 @@ def test_ccmm_fused_exchange_mirrors():
     eng.run_device(None, n, None)
     torch.cuda.synchronize()
     assert torch.equal(view, before)
+
+
+def test_blocking_api_is_thread_safe_per_context(mm):
+    # the free functions are pure and reentrant; the C ABI
+    # serialises calls on one context with its mutex, so concurrent host
+    # threads get exact, independent results
+    import threading
+    p = 149
+    rng = np.random.default_rng(11)
+    cases = [(rng.integers(0, p * p, (40, 300)), rng.integers(0, p * p, (300, 50))) for _ in range(6)]
+    want = [mm.gemm_mod_psq(a, b, p) for a, b in cases]
+    got = [None] * len(cases)
+    errors = []
+
+    def work(i):
+        try:
+            for _ in range(5):
+                got[i] = mm.gemm_mod_psq(cases[i][0], cases[i][1], p)
+        except Exception as ex:  # noqa: BLE001
+            errors.append(ex)
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(len(cases))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors
+    for w, g in zip(want, got):
+        assert (w == g).all()
