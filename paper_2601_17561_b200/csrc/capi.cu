@@ -116,7 +116,6 @@ int run_ppmm(irl_ctx* ctx, PpmmLaunch L, uint32_t kchunk, cudaStream_t s) {
     }
     if (kchunk == 0 || kchunk > K) kchunk = K;
     if (!L.progress) L.progress = ctx->d_progress;
-    if (const char* sch = std::getenv("IRL_PPMM_SCHEDULE")) L.dynamic_schedule = std::strcmp(sch, "static") != 0;
     if (const char* gl = std::getenv("IRL_PPMM_GATE")) L.gate_lead = std::atoi(gl);
     if (const char* cl = std::getenv("IRL_PPMM_CLUSTER")) {
         // "PMxPN" (pairs along M x pairs along N) or a CTA count 2/4/8 (1 x count/2)

@@ -41,7 +41,6 @@ struct PpmmLaunch {
     uint32_t max_clusters = 0;   // 0 = one CTA pair per SM pair
     uint32_t* progress = nullptr;  // kScheduleScratchBytes of device scratch (required)
     uint64_t* stats = nullptr;     // optional [pairs][kStatSlots] diagnostics
-    int dynamic_schedule = 1;      // units from an atomic counter (0: static super-rounds)
     int gate_lead = -1;            // K blocks a pair may lead its group; -1 default, 0 off
     // Part strides for launches over a modulus subset of every part
     // (0 = dense: nprimes * 2 * M rows, nprimes * N * M outputs).

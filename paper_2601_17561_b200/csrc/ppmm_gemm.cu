@@ -78,7 +78,6 @@ struct __align__(64) GemmArgs {
     uint32_t m_units;                 // units per (prime, part) = ceil(m_blocks / unit_mblocks)
     // group schedule (see group_of): G = clusters per full group
     uint32_t G, F, L, active_clusters;
-    uint32_t dynamic;                 // 1: units from an atomic counter; 0: static super-rounds
     uint32_t mail_slots;              // per-group mailbox ring (units + 1 when the scratch allows, so a
                                       // member started late never finds its slot overwritten)
     uint32_t gate_lead;               // max K blocks a pair may lead its group (0: no gating)
@@ -92,7 +91,7 @@ struct __align__(64) GemmArgs {
     uint32_t n_mirror, mirror_part;
     uint32_t* part_done;              // optional [nprimes][parts] count of (epilogue warp, tile) completions
     uint32_t* progress;               // [clusters] K blocks issued by each pair's leader producer
-    uint32_t* counter;                // next unit to hand out (dynamic schedule)
+    uint32_t* counter;                // next unit to hand out (shared by the main and filler launches)
     unsigned long long* mailbox;      // [groups][mail_slots] ((seq+1) << 32 | unit) published per group
     unsigned long long* stats;        // optional [clusters][kStatSlots] diagnostics (see ppmm.h)
     ModConst mc[kMaxPrimesPerLaunch];
@@ -268,14 +267,6 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                 const uint32_t u = atomicAdd(args.counter, 1u);
                 return u < args.units ? u : kEnd;
             };
-            // static schedule (args.dynamic == 0): the super-round layout
-            const uint32_t super_units = args.F * args.G + args.L;
-            auto static_unit = [&](uint32_t seq) -> uint32_t {
-                const uint32_t u = cluster_id < args.F * args.G
-                                       ? (seq / args.G) * super_units + grp.id * args.G + seq % args.G
-                                       : seq * super_units + args.F * args.G + (grp.id - args.F);
-                return u < args.units ? u : kEnd;
-            };
             auto publish = [&](uint32_t seq, uint32_t u) {
                 // tag = seq + 1 so the zeroed mailbox never matches
                 st_relaxed_u64(mbox + seq % args.mail_slots,
@@ -293,15 +284,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             };
 
             uint32_t u_next = 0;
-            if (writer && args.dynamic) {
+            if (writer) {
                 u_next = grab();
                 publish(0, u_next);
             }
             for (uint32_t seq = 0;; ++seq) {
                 uint32_t u;
-                if (!args.dynamic) {
-                    u = static_unit(seq);
-                } else if (writer) {
+                if (writer) {
                     u = u_next;
                     if (u != kEnd) {
                         u_next = grab();  // prefetch: members never wait at a unit boundary
@@ -829,7 +818,6 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     for (uint32_t i = 0; i < L.nprimes; ++i) args.mc[i] = L.mc[i];
 
     if (!L.progress) return cudaErrorInvalidValue;
-    args.dynamic = L.dynamic_schedule ? 1u : 0u;
     args.gate_lead = L.gate_lead < 0 ? kGateLead : static_cast<uint32_t>(L.gate_lead);
     args.counter = L.progress + kProgressWords;  // shared by every launch of this call
 

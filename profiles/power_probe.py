@@ -78,7 +78,7 @@ def main():
     ops = 6.0 * eng.nmod * a.rows * a.n * a.k * a.parts
 
     def run(env, secs):
-        for k in ("IRL_PPMM_CLUSTER", "IRL_PPMM_GATE", "IRL_PPMM_SCHEDULE"):
+        for k in ("IRL_PPMM_CLUSTER", "IRL_PPMM_GATE"):
             os.environ.pop(k, None)
         os.environ.update(env)
         eng.run_device(None, a.n, None, q_ready=False)  # split + warm
@@ -146,8 +146,6 @@ def main():
             r = run({"IRL_PPMM_CLUSTER": v[3:]}, a.secs)
         elif v.startswith("gate="):
             r = run({"IRL_PPMM_GATE": v[5:]}, a.secs)
-        elif v == "static":
-            r = run({"IRL_PPMM_SCHEDULE": "static"}, a.secs)
         else:
             r = run({}, a.secs)
         r["variant"] = v
