@@ -12,7 +12,9 @@
 // Both integer sums are int8 GEMMs over K = d: acc1 = X0 Y0 with X0/Y0 the
 // ternary planes c' = m - 2 (c & m) (to_masked, iris_core.cpp:28-35), and
 // acc2 = X1 Y1 with X1/Y1 the 0/1 mask planes. They run through the PPMM
-// kernel in kModeInner (two products per K step, raw int32 epilogue).
+// kernel: kModeInner writes the raw int32 sums (irl_iris_inner_overlap);
+// kModeIrisMatch scores and matches in the epilogue, so only match bits
+// leave the GEMM (irl_iris_match, irl_iris_db_match).
 // Query column c = e * rho + r holds rotate(q_e, r) (iris_core.cpp:65-76),
 // built on the device from the packed eye templates.
 #include <cuda_runtime.h>
@@ -61,41 +63,6 @@ __global__ void iris_planes_kernel(const uint64_t* __restrict__ code, const uint
     *reinterpret_cast<uint4*>(planes + static_cast<size_t>(cols) * ldk + o) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-// inner / overlap [cols][n_db] -> per-(eye, template) match bits (OR over the
-// eye's rho rotations of score in [lo, hi]), optional scores, and per eye the
-// first match / first empty overlap in match_db_reference's iteration order
-// (rotation-major, then template: linear index r * n_db + j).
-__global__ void iris_match_kernel(const int32_t* __restrict__ inner, const int32_t* __restrict__ overlap,
-                                  uint32_t n_db, uint32_t n_eyes, uint32_t rho, double lo, double hi,
-                                  uint8_t* __restrict__ bits, double* __restrict__ scores,
-                                  unsigned long long* __restrict__ first /* [n_eyes][2] */) {
-    const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (tid >= static_cast<size_t>(n_eyes) * n_db) return;
-    const uint32_t e = static_cast<uint32_t>(tid / n_db), j = static_cast<uint32_t>(tid % n_db);
-    unsigned long long fm = ~0ull, fz = ~0ull;
-    uint8_t any = 0;
-    for (uint32_t r = 0; r < rho; ++r) {
-        const size_t idx = static_cast<size_t>(e * rho + r) * n_db + j;
-        const int32_t ov = overlap[idx];
-        const unsigned long long lin = static_cast<unsigned long long>(r) * n_db + j;
-        if (ov == 0) {
-            if (scores) scores[idx] = __longlong_as_double(0x7FF8000000000000ll);  // undefined (ZeroOverlap)
-            fz = min(fz, lin);
-            continue;
-        }
-        // iris_core.cpp:58: static_cast<double>(inner) / static_cast<double>(overlap), IEEE division
-        const double s = __ddiv_rn(static_cast<double>(inner[idx]), static_cast<double>(ov));
-        if (scores) scores[idx] = s;
-        if (s >= lo && s <= hi) {  // Interval::contains (iris_core.hpp)
-            any = 1;
-            fm = min(fm, lin);
-        }
-    }
-    if (bits) bits[tid] = any;
-    if (fm != ~0ull) atomicMin(first + 2 * e, fm);
-    if (fz != ~0ull) atomicMin(first + 2 * e + 1, fz);
-}
-
 size_t round16(size_t x) { return (x + 15) / 16 * 16; }
 
 // kModeInner GEMM of device planes x (DB, [2][n_db][ldk]) and y (queries,
@@ -133,35 +100,54 @@ int build_planes(irl_ctx* ctx, const uint64_t* code, const uint64_t* mask, size_
     return IRL_OK;
 }
 
-// Score + match pass over device inner / overlap (see iris_match_kernel),
-// results to host buffers; blocks. Returns IRL_ERR_ZERO_OVERLAP if any eye's
-// first evaluated score had an empty overlap.
-int match_device(irl_ctx* ctx, const int32_t* di, const int32_t* dov, size_t n_db, size_t n_eyes, size_t rho,
-                 double p_lo, double p_hi, uint8_t* match_bits, int32_t* eye_result, double* scores,
-                 irl::DevBuf& ws, cudaStream_t s) {
+// Scoring fused into the GEMM (kModeIrisMatch): the epilogue divides,
+// matches and folds the first match / first empty overlap per eye; only the
+// match bits (and optional scores) leave the device. Blocks. Returns
+// IRL_ERR_ZERO_OVERLAP if any eye's first evaluated score had an empty overlap.
+int match_fused(irl_ctx* ctx, const int8_t* xp, const int8_t* yp, size_t n_db, size_t n_eyes, size_t rho, size_t d,
+                size_t ldk, double p_lo, double p_hi, uint8_t* match_bits, int32_t* eye_result, double* scores,
+                irl::DevBuf& ws, uint32_t* progress, cudaStream_t s) {
     const size_t cols = n_eyes * rho, nbits = n_eyes * n_db, nsc = cols * n_db;
-    const size_t off_sc = (16 * n_eyes + nbits + 15) / 16 * 16;
+    if (static_cast<unsigned long long>(rho) * n_db >= 0xFFFFFFFFull)
+        return set_err(ctx, IRL_ERR_UNSUPPORTED, "iris: rho * n_db must stay below 2^32");
+    const size_t off_bits = 8 * n_eyes, off_sc = (off_bits + nbits + 15) / 16 * 16;
     IRL_CK(ctx, ws.ensure(off_sc + (scores ? nsc * 8 : 0)));
-    auto* first = ws.as<unsigned long long>();
-    uint8_t* dbits = reinterpret_cast<uint8_t*>(first + 2 * n_eyes);
+    auto* first = ws.as<uint32_t>();
+    uint8_t* dbits = ws.as<uint8_t>() + off_bits;
     double* dsc = scores ? reinterpret_cast<double*>(ws.as<uint8_t>() + off_sc) : nullptr;
-    IRL_CK(ctx, cudaMemsetAsync(first, 0xFF, 16 * n_eyes, s));
-    const uint32_t T = 256;
-    iris_match_kernel<<<static_cast<unsigned>((nbits + T - 1) / T), T, 0, s>>>(
-        di, dov, static_cast<uint32_t>(n_db), static_cast<uint32_t>(n_eyes), static_cast<uint32_t>(rho), p_lo,
-        p_hi, dbits, dsc, first);
-    IRL_LAUNCH(ctx, cudaGetLastError());
-    std::vector<unsigned long long> h(2 * n_eyes);
-    IRL_CK(ctx, cudaMemcpyAsync(h.data(), first, 16 * n_eyes, cudaMemcpyDeviceToHost, s));
+    IRL_CK(ctx, cudaMemsetAsync(first, 0xFF, 8 * n_eyes, s));
+    IRL_CK(ctx, cudaMemsetAsync(dbits, 0, nbits, s));
+    PpmmLaunch L;
+    L.mode = kModeIrisMatch;
+    L.a_planes = xp;
+    L.b_planes = yp;
+    L.M = static_cast<uint32_t>(n_db);
+    L.N = static_cast<uint32_t>(cols);
+    L.K = static_cast<uint32_t>(d);
+    L.ldk = static_cast<uint32_t>(ldk);
+    L.parts = 1;
+    L.nprimes = 1;
+    L.mc[0] = make_modconst(2, 1);  // unused
+    L.progress = progress;
+    L.iris.lo = p_lo;
+    L.iris.hi = p_hi;
+    L.iris.rho = static_cast<uint32_t>(rho);
+    L.iris.bits = dbits;
+    L.iris.first = first;
+    L.iris.scores = dsc;
+    IRL_LAUNCH(ctx, launch_ppmm_planes(L, s));
+    ctx->launches += ppmm_kernels_last_launch() > 1 ? ppmm_kernels_last_launch() - 1 : 0;  // + filler
+    std::vector<uint32_t> h(2 * n_eyes);
+    IRL_CK(ctx, cudaMemcpyAsync(h.data(), first, 8 * n_eyes, cudaMemcpyDeviceToHost, s));
     if (match_bits) IRL_CK(ctx, cudaMemcpyAsync(match_bits, dbits, nbits, cudaMemcpyDeviceToHost, s));
     if (scores) IRL_CK(ctx, cudaMemcpyAsync(scores, dsc, nsc * 8, cudaMemcpyDeviceToHost, s));
     IRL_CK(ctx, cudaStreamSynchronize(s));
     int status = IRL_OK;
     for (size_t e = 0; e < n_eyes; ++e) {
-        const unsigned long long fm = h[2 * e], fz = h[2 * e + 1];
+        const uint32_t fm = h[2 * e], fz = h[2 * e + 1];
         // match_db_reference: the first evaluated score either matches (return
         // true) or throws ZeroOverlap, whichever comes first in loop order
-        const int32_t res = fz < fm ? -1 : (fm != ~0ull ? 1 : 0);
+        const int32_t res = fz < fm ? -1 : (fm != 0xFFFFFFFFu ? 1 : 0);
         if (eye_result) eye_result[e] = res;
         if (res < 0 && status == IRL_OK)
             status = set_err(ctx, IRL_ERR_ZERO_OVERLAP, "mask overlap is empty, score undefined");
@@ -230,7 +216,6 @@ struct irl_iris_db {
     int8_t* planes = nullptr;    // [2][n_db][ldk]
     int8_t* qplanes = nullptr;   // [2][max_cols][ldk]
     uint64_t* qbits = nullptr;   // eyes' code + mask words
-    int32_t* io = nullptr;       // inner, overlap [max_cols][n_db]
     uint32_t* progress = nullptr;
     irl::DevBuf match_ws;
 };
@@ -266,11 +251,26 @@ int irl_iris_match(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db_mas
         if (match_bits) std::memset(match_bits, 0, n_eyes * n_db);
         return IRL_OK;
     }
-    int32_t *di = nullptr, *dov = nullptr;
-    if (int st = inner_overlap_device(ctx, db_code, db_mask, n_db, q_code, q_mask, n_eyes, rho, d, &di, &dov))
-        return st;
-    return match_device(ctx, di, dov, n_db, n_eyes, rho, p_lo, p_hi, match_bits, eye_result, scores, ctx->ws[4],
-                        ctx->stream);
+    cudaStream_t s = ctx->stream;
+    const size_t words = (d + 63) / 64, ldk = round16(d);
+    if (int st = check_dims(ctx, n_db, cols, d)) return st;
+    const size_t db_bits = n_db * words * 8, q_bits = n_eyes * words * 8;
+    IRL_CK(ctx, ctx->ws[0].ensure(2 * db_bits + 2 * q_bits));
+    IRL_CK(ctx, ctx->ws[1].ensure(2 * n_db * ldk));
+    IRL_CK(ctx, ctx->ws[2].ensure(2 * cols * ldk));
+    uint8_t* bitbuf = ctx->ws[0].as<uint8_t>();
+    auto* dc = reinterpret_cast<uint64_t*>(bitbuf);
+    auto* dm = reinterpret_cast<uint64_t*>(bitbuf + db_bits);
+    auto* qc = reinterpret_cast<uint64_t*>(bitbuf + 2 * db_bits);
+    auto* qm = reinterpret_cast<uint64_t*>(bitbuf + 2 * db_bits + q_bits);
+    IRL_CK(ctx, cudaMemcpyAsync(dc, db_code, db_bits, cudaMemcpyHostToDevice, s));
+    IRL_CK(ctx, cudaMemcpyAsync(dm, db_mask, db_bits, cudaMemcpyHostToDevice, s));
+    IRL_CK(ctx, cudaMemcpyAsync(qc, q_code, q_bits, cudaMemcpyHostToDevice, s));
+    IRL_CK(ctx, cudaMemcpyAsync(qm, q_mask, q_bits, cudaMemcpyHostToDevice, s));
+    if (int st = build_planes(ctx, dc, dm, n_db, 1, d, ctx->ws[1].as<int8_t>(), s)) return st;
+    if (int st = build_planes(ctx, qc, qm, n_eyes, rho, d, ctx->ws[2].as<int8_t>(), s)) return st;
+    return match_fused(ctx, ctx->ws[1].as<int8_t>(), ctx->ws[2].as<int8_t>(), n_db, n_eyes, rho, d, ldk, p_lo, p_hi,
+                       match_bits, eye_result, scores, ctx->ws[4], ctx->d_progress, s);
 }
 
 int irl_iris_db_create(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db_mask, size_t n_db, size_t d,
@@ -292,7 +292,6 @@ int irl_iris_db_create(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db
     cudaError_t err = cudaMalloc(&e->planes, 2 * n_db * e->ldk);
     if (err == cudaSuccess) err = cudaMalloc(&e->qplanes, 2 * max_cols * e->ldk);
     if (err == cudaSuccess) err = cudaMalloc(&e->qbits, 2 * max_cols * words * 8);
-    if (err == cudaSuccess) err = cudaMalloc(&e->io, 2 * max_cols * n_db * 4);
     if (err == cudaSuccess) err = cudaMalloc(&e->progress, kScheduleScratchBytes);
     if (err == cudaSuccess) err = cudaMalloc(&staging, 2 * db_bits);
     if (err == cudaSuccess) err = cudaMemcpyAsync(staging, db_code, db_bits, cudaMemcpyHostToDevice, ctx->stream);
@@ -317,7 +316,6 @@ int irl_iris_db_destroy(irl_iris_db* e) {
     cudaFree(e->planes);
     cudaFree(e->qplanes);
     cudaFree(e->qbits);
-    cudaFree(e->io);
     cudaFree(e->progress);
     e->match_ws.release();
     delete e;
@@ -342,13 +340,8 @@ int irl_iris_db_match(irl_iris_db* e, const uint64_t* q_code, const uint64_t* q_
     IRL_CK(ctx, cudaMemcpyAsync(e->qbits, q_code, qb, cudaMemcpyHostToDevice, s));
     IRL_CK(ctx, cudaMemcpyAsync(e->qbits + n_eyes * words, q_mask, qb, cudaMemcpyHostToDevice, s));
     if (int st = build_planes(ctx, e->qbits, e->qbits + n_eyes * words, n_eyes, rho, e->d, e->qplanes, s)) return st;
-    int32_t* inner = e->io;
-    int32_t* ovl = e->io + cols * e->n_db;
-    if (int st = inner_overlap_gemm(ctx, e->planes, e->qplanes, e->n_db, cols, e->d, e->ldk, inner, ovl,
-                                    e->progress, s))
-        return st;
-    return match_device(ctx, inner, ovl, e->n_db, n_eyes, rho, p_lo, p_hi, match_bits, eye_result, scores,
-                        e->match_ws, s);
+    return match_fused(ctx, e->planes, e->qplanes, e->n_db, n_eyes, rho, e->d, e->ldk, p_lo, p_hi, match_bits,
+                       eye_result, scores, e->match_ws, e->progress, s);
 }
 
 }  // extern "C"

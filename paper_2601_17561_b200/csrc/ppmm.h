@@ -18,6 +18,19 @@ constexpr uint32_t kMaxPrimesPerLaunch = 32;
 constexpr int kModePsq = 0;
 constexpr uint32_t kMaxMirrors = 7;
 constexpr int kModeInner = 1;
+// kModeIrisMatch: the kModeInner products with the plaintext scoring fused
+// into the epilogue (score = acc1 / acc2 in IEEE double, match bits and the
+// first match / first empty overlap per eye; see IrisMatchOut).
+constexpr int kModeIrisMatch = 2;
+
+struct IrisMatchOut {
+    double lo = 0, hi = 0;      // the P interval
+    float lo_in = 0, lo_out = 0, hi_in = 0, hi_out = 0;  // float screens lo +- eps, hi -+ eps (set by the launcher)
+    uint32_t rho = 1;           // query column c = eye * rho + rotation
+    uint8_t* bits = nullptr;    // [eyes][M] (zeroed by the caller), nullable
+    uint32_t* first = nullptr;  // [eyes][2]: min rotation * M + m of a match / of an empty overlap (0xFF.. init)
+    double* scores = nullptr;   // [N][M], NaN where the overlap is empty; nullable
+};
 // Diagnostics slots per CTA pair (PpmmLaunch::stats): 0 producer empty-wait
 // cycles, 1 producer gate cycles, 2 MMA full-wait cycles, 3 MMA tmem-empty
 // wait cycles, 4 MMA thread total cycles, 5 epilogue tmem-full wait cycles,
@@ -62,6 +75,7 @@ struct PpmmLaunch {
     uint32_t* part_done = nullptr;
     int mode = kModePsq;
     int32_t* out_i32[2] = {nullptr, nullptr};  // kModeInner outputs [parts][nprimes][N][M]
+    IrisMatchOut iris;                          // kModeIrisMatch outputs (parts = nprimes = 1)
     int cluster_pm = 1;
     int cluster_pn = 4;
     ModConst mc[kMaxPrimesPerLaunch];

@@ -87,6 +87,7 @@ struct __align__(64) GemmArgs {
     unsigned long long out_part;      // output elements between consecutive parts
     uint16_t* out;
     int32_t* out_i32[2];              // kMode == kModeInner: acc1 / acc2 as int32 [n][m] (nullable)
+    IrisMatchOut iris;                // kMode == kModeIrisMatch
     uint16_t* mirror[kMaxMirrors];    // peer copies of part mirror_part's outputs (see PpmmLaunch)
     uint32_t n_mirror, mirror_part;
     uint32_t* part_done;              // optional [nprimes][parts] count of (epilogue warp, tile) completions
@@ -451,7 +452,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                         const uint64_t dy1 =
                             ptx::smem_desc_k_sw128(st + 3 * kPlaneTileBytes + koff);
                         const uint32_t accum = (kb | k) != 0;
-                        if constexpr (kMode == kModeInner) {
+                        if constexpr (kMode != kModePsq) {
                             // two independent products: acc1 = X0 Y0, acc2 = X1 Y1
                             ptx::mma_i8_pair(acc1, dx0, dy0, idesc, accum);
                             ptx::mma_i8_pair(acc2, dx1, dy1, idesc, accum);
@@ -526,6 +527,59 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                 ptx::tmem_ld_32x32b_x16(lane_base + c, a1);
                 ptx::tmem_ld_32x32b_x16(lane_base + kAcc2Col + c, a2);
                 ptx::tmem_ld_wait();
+                if constexpr (kMode == kModeIrisMatch) {
+                    // score = inner / overlap per (column, template); per column,
+                    // the warp's 32 templates fold their first match / first
+                    // empty overlap into one atomicMin per eye
+                    const IrisMatchOut& io = args.iris;
+                    for (int jj = 0; jj < 16; ++jj) {
+                        const uint32_t col = tc.n0 + c + jj;
+                        if (col >= args.N) break;  // uniform across the warp
+                        const uint32_t eye = col / io.rho, rot = col % io.rho;
+                        const int32_t inner = static_cast<int32_t>(a1[jj]), ov = static_cast<int32_t>(a2[jj]);
+                        uint32_t cm = 0xFFFFFFFFu, cz = 0xFFFFFFFFu;
+                        if (row_ok) {
+                            const uint32_t lin = rot * args.M + m;
+                            if (ov == 0) {
+                                cz = lin;
+                                if (io.scores)
+                                    io.scores[static_cast<size_t>(col) * args.M + m] =
+                                        __longlong_as_double(0x7FF8000000000000ll);
+                            } else {
+                                // iris_core.cpp:58, IEEE double division. A float
+                                // quotient (|error| < 1e-6) settles every score
+                                // farther than 1e-5 from a bound; the exact
+                                // division runs only near the bounds or when the
+                                // scores are requested.
+                                bool hit;
+                                const float q = __fdividef(static_cast<float>(inner), static_cast<float>(ov));
+                                if (!io.scores && q >= io.lo_in && q <= io.hi_in) {
+                                    hit = true;
+                                } else if (!io.scores && (q < io.lo_out || q > io.hi_out)) {
+                                    hit = false;
+                                } else {
+                                    const double sc = __ddiv_rn(static_cast<double>(inner), static_cast<double>(ov));
+                                    hit = sc >= io.lo && sc <= io.hi;  // Interval::contains
+                                    if (io.scores) io.scores[static_cast<size_t>(col) * args.M + m] = sc;
+                                }
+                                if (hit) {
+                                    cm = lin;
+                                    if (io.bits) io.bits[static_cast<size_t>(eye) * args.M + m] = 1;
+                                }
+                            }
+                        }
+                        // events (a match, an empty overlap) are rare: vote first
+                        if (__any_sync(0xFFFFFFFFu, (cm & cz) != 0xFFFFFFFFu) && io.first) {
+                            cm = __reduce_min_sync(0xFFFFFFFFu, cm);
+                            cz = __reduce_min_sync(0xFFFFFFFFu, cz);
+                            if (lane == 0) {
+                                if (cm != 0xFFFFFFFFu) atomicMin(io.first + 2 * eye, cm);
+                                if (cz != 0xFFFFFFFFu) atomicMin(io.first + 2 * eye + 1, cz);
+                            }
+                        }
+                    }
+                    continue;
+                }
                 if (!row_ok) continue;
                 if constexpr (kMode == kModeInner) {
                     const size_t base = tc.part * args.out_part + static_cast<size_t>(tc.prime) * args.N * args.M +
@@ -655,6 +709,13 @@ KernelFn kernel_for(int si, int mode = kModePsq) {
         }
         return nullptr;
     }
+    if (mode == kModeIrisMatch) {
+        switch (si) {
+            case 0: return ppmm_i8_sm100_kernel<1, 1, kModeIrisMatch>;
+            case 2: return ppmm_i8_sm100_kernel<1, 4, kModeIrisMatch>;
+        }
+        return nullptr;
+    }
     switch (si) {
         case 0: return ppmm_i8_sm100_kernel<1, 1, kModePsq>;
         case 1: return ppmm_i8_sm100_kernel<1, 2, kModePsq>;
@@ -767,7 +828,7 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     // cluster shape: a multi-pair shape needs at least pn n-tiles; otherwise
     // the widest shape that divides the n-tiles (1x2 or a plain pair)
     int si = shape_index(L.cluster_pm, L.cluster_pn);
-    if (L.mode == kModeInner && si != 0) si = 2;  // inner-product mode is built for 1x1 and 1x4
+    if (L.mode != kModePsq && si != 0) si = 2;  // the inner / iris modes are built for 1x1 and 1x4
     if (si < 0) si = 0;
     // Short launches (a few waves of units) finish sooner on plain pairs: 74
     // workers instead of 15 clusters + a filler whose solo pairs sweep a whole
@@ -814,7 +875,18 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     for (uint32_t i = 0; i < L.n_mirror; ++i) args.mirror[i] = L.mirror[i];
     args.out_i32[0] = L.out_i32[0];
     args.out_i32[1] = L.out_i32[1];
-    if (L.mode == kModeInner && L.accumulate) return cudaErrorInvalidValue;
+    if (L.mode != kModePsq && L.accumulate) return cudaErrorInvalidValue;
+    if (L.mode == kModeIrisMatch && (L.parts != 1 || L.nprimes != 1 || L.iris.rho == 0 ||
+                                     static_cast<uint64_t>(L.iris.rho) * L.M >= 0xFFFFFFFFull))
+        return cudaErrorInvalidValue;
+    args.iris = L.iris;
+    {
+        const double eps = 1e-5;  // >> the float quotient's error for |inner|, overlap <= 2^24
+        args.iris.lo_in = static_cast<float>(L.iris.lo + eps);
+        args.iris.lo_out = static_cast<float>(L.iris.lo - eps);
+        args.iris.hi_in = static_cast<float>(L.iris.hi - eps);
+        args.iris.hi_out = static_cast<float>(L.iris.hi + eps);
+    }
     for (uint32_t i = 0; i < L.nprimes; ++i) args.mc[i] = L.mc[i];
 
     if (!L.progress) return cudaErrorInvalidValue;
