@@ -828,7 +828,8 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     // cluster shape: a multi-pair shape needs at least pn n-tiles; otherwise
     // the widest shape that divides the n-tiles (1x2 or a plain pair)
     int si = shape_index(L.cluster_pm, L.cluster_pn);
-    if (L.mode != kModePsq && si != 0) si = 2;  // the inner / iris modes are built for 1x1 and 1x4
+    // the inner / iris modes are built for 1x1 and 1x4 (2x4 measured 40% slower for iris)
+    if (L.mode != kModePsq && si != 0) si = 2;
     if (si < 0) si = 0;
     // Short launches (a few waves of units) finish sooner on plain pairs: 74
     // workers instead of 15 clusters + a filler whose solo pairs sweep a whole
@@ -982,6 +983,8 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
         if (!kfn) return cudaErrorInvalidValue;
         if (L.mode != kModePsq) {
             e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+            if (e == cudaSuccess && sh.ctas() > 8)
+                e = cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             if (e != cudaSuccess) return e;
         }
         e = cudaLaunchKernelEx(&cfg, kfn, ma, mb, a);
