@@ -10,20 +10,31 @@
 // so no int32 partial ever reaches HBM.
 //
 // Execution model (sm_100a):
-//   * a CTA pair (cluster of 2) owns a 256 x n_tile output tile
-//     (n_tile <= 256): tcgen05.mma.cta_group::2.kind::i8 with M = 256;
-//   * TMEM holds two int32 accumulators per tile: acc1 = X0 Y0 in columns
-//     [0, 256) and acc2 = X0 Y1 + X1 Y0 in [256, 512);
+//   * a CTA pair owns a 256 x n_tile output tile (n_tile <= 256):
+//     tcgen05.mma.cta_group::2.kind::i8 with M = 256, issued by one thread of
+//     the leader CTA; TMEM holds acc1 = X0 Y0 in columns [0, 256) and
+//     acc2 = X0 Y1 + X1 Y0 in [256, 512); X0 stays in the A collector for the
+//     second product (collector::a fill / lastuse);
 //   * warp 0 = TMA producer (both CTAs load their half of A and B),
-//     warp 1 = MMA issuer (leader CTA) + TMEM owner, warps 2..9 = epilogue
+//     warp 1 = MMA issuer (leader CTA) + TMEM owner, warps 2.. = epilogue
 //     (kEpiWarps / 4 warps per TMEM lane quarter, interleaved over 16-column chunks);
 //   * 3-stage smem ring of 128-byte K blocks, 128B-swizzled, mbarrier-paced;
-//   * persistent static schedule over "units" (one 256-row block of one
-//     (prime, part)), ordered prime-major so a prime's query planes stay
-//     L2-resident. The n-tiles of a unit run on a GROUP of CTA pairs at the
-//     same time, and each group's TMA producers are kept within a few K blocks
-//     of each other (progress flags in global memory, bounded spin), so every
-//     database tile crosses HBM once and is re-read from L2 by its peers.
+//   * clusters of kPM x kPN pairs: the kPN pairs sharing an m-block receive
+//     each DB tile by TMA multicast (loaded L2 evict-first when they are its
+//     only reader), the kPM pairs sharing an n-tile each query tile; the
+//     default 1x4 covers all of N = 992 so every DB tile leaves L2 once;
+//   * persistent dynamic schedule: "units" (m-blocks x one n-chunk of one
+//     (prime, part); prime-major, m fastest) come from one atomic counter
+//     shared with a 1x1 filler launch on the SMs the clusters strand. A unit's
+//     n-tiles run on a group of clusters at once whose TMA producers stay
+//     within gate_lead K blocks of each other (bounded spin), so a DB tile is
+//     re-read from L2 by its peers;
+//   * epilogue: (acc1 + p (acc2 mod p)) mod p^2 with exact Barrett steps,
+//     uint16 stores; optional per-(prime, part) completion counters (the e2e
+//     pipeline starts each block's D2H from them) and mirror stores into peer
+//     GPUs' buffers (the fused a-part exchange);
+//   * kModeInner / kModeIrisMatch reuse the pipeline for two independent
+//     products (iris inner products and mask overlaps), raw or scored.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
