@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--exchange", choices=["auto", "mirror", "broadcast"], default="auto",
                     help="a-part exchange at N>1: fused P2P epilogue stores (mirror, validated in warm-up, "
                          "falls back to broadcast) or the NCCL broadcast")
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
+                    help="gloo + --same-device: run the multi-rank paths with every rank on one GPU (tests)")
+    ap.add_argument("--same-device", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--config", choices=["c2", "c3", "c4"], default="c4",
                     help="BASELINE.json config: c2 one DB slice as one PPMM (K = 2^14), c3 a-part + one "
                          "b-part, c4 the full 8-part DB (default; the headline metric)")
@@ -240,10 +243,15 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.same_device:
+        local = 0  # test harness: every rank on GPU 0 (multi-rank code paths on a 1-GPU box)
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
 
     from paper_2601_17561_b200.ccmm import CcmmEngine, staging_tensors, synth_query
     from paper_2601_17561_b200.dist import ShardedStep, part_range

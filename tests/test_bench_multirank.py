@@ -1,0 +1,40 @@
+"""The N>1 code paths of bench.py (part dealing, the fused a-part exchange over
+CUDA IPC with its warm-up checksum validation, the completion signal, the e2e
+loop, max-over-ranks timing) on a one-GPU box: torchrun with every rank on
+GPU 0 and the gloo backend (IPC between processes of one device is legal).
+The 8-GPU NCCL run is the driver's; this pins its logic."""
+import json
+import os
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,exchange", [(2, "auto"), (2, "broadcast"), (4, "auto")])
+def test_bench_multirank_same_device(world, exchange):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", f"--master-port={_port()}", str(ROOT / "bench.py"), "--gpus", str(world),
+           "--steps", "2", "--warmup", "3", "--backend", "gloo", "--same-device", "--parts", "4", "--rows", "2048",
+           "--k", "4096", "--no-cpu-baseline", "--no-int8-ref", "--exchange", exchange]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT,
+                       env={**os.environ, "OMP_NUM_THREADS": "1"})
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1  # rank 0 prints one JSON line
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == world and d["steps"] == 2
+    assert d["exchange"]["kind"].startswith("fused" if exchange == "auto" else "NCCL")
+    assert d["exchange"]["note"] is None
+    assert d["value"] > 0 and d["e2e"]["value"] > 0
