@@ -1,0 +1,84 @@
+// C++ host side of the RGSW CCMM on the B200 (C ABI irl_ccmm_*):
+//   * irislab::emu::CcmmSpec and ccmm_twin_product(): the exact product behind
+//     Emulator::ccmm_twin (emulator.hpp:85-97, 135-140; emulator.cpp:389-447),
+//     same validation order, messages and exception types, computed on the
+//     PPMM engine; returned as the d1*d3/n_db output ciphertexts' messages in
+//     ccmm_twin's order (the plaintext-twin bookkeeping -- level, encoding,
+//     trace -- stays with the caller's emulator);
+//   * irislab::b200::CcmmEngine: RAII over the device-resident engine (the
+//     paper's 8-slice database), one query batch per run().
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+#include "modmat.hpp"  // irislab::Error, ShapeMismatch, ModulusBudget, DeviceError, RnsBasis
+
+struct irl_ccmm;
+
+namespace irislab {
+namespace emu {
+
+enum class Encoding { Coeff, Slot };
+
+/// emulator.hpp:85-97
+struct CcmmSpec {
+    long d1 = 0, d2 = 0, d3 = 0;
+    long n_db = 0;
+    long n_qry = 0;
+    double db_modulus_bits = 0.0;
+    double qry_modulus_bits = 0.0;
+    double scale_bits = 0.0;
+    int out_level = 0;
+    Encoding out_encoding = Encoding::Coeff;
+    bool out_ci = false;
+};
+
+/// Messages of ccmm_twin's outputs: result[k] holds the n_db slots of output
+/// ciphertext k, k = c * (d1 / n_db) + b for column c and row block b
+/// (emulator.cpp:425-439). db is d1 x d2 and qry d2 x d3, row-major,
+/// integer-valued; top_level bounds out_level as the emulator's chain does.
+std::vector<std::vector<double>> ccmm_twin_product(const CcmmSpec& spec, const std::vector<double>& db,
+                                                   const std::vector<double>& qry, int top_level);
+
+}  // namespace emu
+
+namespace b200 {
+
+/// Device-resident CCMM engine over `parts` database parts of m x k entries
+/// (residues of the basis' moduli, registered once) and query batches of up to
+/// max_n columns (wider batches stream through in column chunks).
+class CcmmEngine {
+public:
+    CcmmEngine(std::size_t parts, std::size_t m, std::size_t k, std::size_t max_n,
+               const modmat::RnsBasis& basis = modmat::build_paper_basis());
+    ~CcmmEngine();
+    CcmmEngine(const CcmmEngine&) = delete;
+    CcmmEngine& operator=(const CcmmEngine&) = delete;
+
+    /// residues [nmod][m][k] of one part (host memory)
+    void load_part(std::size_t part, const std::vector<uint16_t>& residues);
+    /// one part as m x k little-endian mod-Q entries of `width` bytes (BigMatrix file form)
+    void load_part_bigint(std::size_t part, const modmat::BigMatrix& entries);
+    /// counter-RNG synthetic database (the bench's inputs)
+    void synth_db(uint64_t seed, uint32_t first_part = 0);
+    /// q_res [nmod][k][n] -> out [parts][nmod][n][m] residues mod p^2 (blocking;
+    /// pinned host memory recommended for large batches)
+    void run(const uint16_t* q_res, std::size_t n, uint16_t* out);
+    std::vector<uint16_t> run(const std::vector<uint16_t>& q_res, std::size_t n);
+
+    std::size_t parts() const { return parts_; }
+    std::size_t rows() const { return m_; }
+    std::size_t inner() const { return k_; }
+    std::size_t moduli() const { return nmod_; }
+    uint64_t device_bytes() const;
+    irl_ccmm* handle() { return e_; }
+
+private:
+    irl_ccmm* e_ = nullptr;
+    std::size_t parts_, m_, k_, max_n_, nmod_;
+};
+
+}  // namespace b200
+}  // namespace irislab

@@ -11,6 +11,7 @@ ROOT = Path(__file__).resolve().parent.parent
 PKG = ROOT / "paper_2601_17561_b200"
 BIN = ROOT / "build" / "test_modmat_b200"
 BIN_IRIS = ROOT / "build" / "test_iris_b200"
+BIN_CCMM = ROOT / "build" / "test_ccmm_b200"
 
 
 def _build_driver(src, out):
@@ -66,6 +67,27 @@ def test_cpp_iris_mirror_builds(iris_binary):
 @pytest.mark.gpu
 def test_cpp_iris_mirror_reference_unit_suite(iris_binary):
     r = subprocess.run([str(iris_binary)], capture_output=True, text=True, timeout=600, cwd=ROOT / "build")
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failed" in r.stdout
+
+
+@pytest.fixture(scope="module")
+def ccmm_binary(binary):
+    _build_driver(ROOT / "tests/cpp/test_ccmm_b200.cpp", BIN_CCMM)
+    return BIN_CCMM
+
+
+def test_cpp_ccmm_mirror_builds(ccmm_binary):
+    assert ccmm_binary.exists()
+    syms = subprocess.run(["nm", "-DC", str(PKG / "libirl_b200.so")], capture_output=True, text=True).stdout
+    for fn in ["irislab::emu::ccmm_twin_product", "irislab::b200::CcmmEngine::run"]:
+        assert fn in syms
+
+
+@pytest.mark.gpu
+def test_cpp_ccmm_mirror_reference_case(ccmm_binary):
+    r = subprocess.run([str(ccmm_binary)], capture_output=True, text=True, timeout=600, cwd=ROOT / "build")
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
