@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
                     help="gloo + --same-device: run the multi-rank paths with every rank on one GPU (tests)")
     ap.add_argument("--same-device", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--e2e-query", choices=["auto", "host"], default="auto",
+                    help="N>1 e2e: auto shards the query H2D over ranks + all-gather when H2D-bound")
     ap.add_argument("--config", choices=["c2", "c3", "c4"], default="c4",
                     help="BASELINE.json config: c2 one DB slice as one PPMM (K = 2^14), c3 a-part + one "
                          "b-part, c4 the full 8-part DB (default; the headline metric)")
@@ -447,16 +449,25 @@ def main():
         out_host = torch.empty((local_parts.count, nmod, N, M), dtype=torch.int16).pin_memory()
         q_np = q_pinned.numpy().view(np.uint16)
         o_np = out_host.numpy().view(np.uint16)
-        if world > 1:
-            dist.barrier()
-        for _ in range(max(1, args.warmup - 1)):
-            eng.run(q_np, o_np)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            eng.run(q_np, o_np)  # H2D query, split, all local PPMMs, D2H outputs
+        # H2D-bound layouts (few parts per GPU: GEMM time per modulus below its
+        # H2D time, the engine's own planner criterion) distribute the query
+        # over NVLink instead: each rank copies 1/N of the moduli from the host
+        # and all-gathers the rest, then runs split + GEMM + part-granular D2H
+        # (irl_ccmm_run_dq). Otherwise irl_ccmm_run pipelines the full H2D.
+        sharded = (world > 1 and local_parts.count * M < 20000 and nmod % world == 0
+                   and args.e2e_query != "host")
+        per = nmod // world if sharded else nmod
+        lo = rank * per if sharded else 0
+        q_bytes = q_dev.view(torch.uint8)  # [nmod][K][2N]: gloo and NCCL both carry uint8
+        q_slices = [q_bytes[r_ * per:(r_ + 1) * per] for r_ in range(world)] if sharded else None
+
+        def e2e_once():
+            if sharded:
+                q_dev[lo:lo + per].copy_(q_pinned.view(nmod, K, N)[lo:lo + per], non_blocking=True)
+                dist.all_gather(q_slices, q_bytes[lo:lo + per].clone() if args.backend == "gloo" else q_bytes[lo:lo + per])
+                eng.run_dq(None, N, o_np, stream=torch.cuda.current_stream().cuda_stream)
+            else:
+                eng.run(q_np, o_np)  # H2D query, split, all local PPMMs, D2H outputs
             if world > 1:
                 # the a-part result exchange stays on the device
                 if exchange == "mirror":  # the owner's epilogue already stored out_A into the peers
@@ -465,15 +476,37 @@ def main():
                     w = dist.broadcast(a_out().view(torch.uint8), src=0, async_op=True)
                 w.wait()
                 torch.cuda.synchronize()
+
+        if world > 1:
+            dist.barrier()
+        for _ in range(max(1, args.warmup - 1)):
+            e2e_once()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_once()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+        # the e2e outputs (host) must equal the device-resident step's (same
+        # query): a 64-row block of every part and modulus, on every rank
+        cols = min(M, 64)
+        same = bool((out_dev[:, :, :, :cols].cpu().numpy().view(np.uint16) == o_np[:, :, :, :cols]).all())
+        ok_t = torch.tensor([1 if same else 0], dtype=torch.int32, device="cuda")
+        if world > 1:
+            dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
+        e2e_exact = bool(ok_t.item())
         tt = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
         e2e = {"value": total_ops / (e2e_ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": int(q_host.nbytes),
+               "h2d_bytes_per_step": int(q_host.nbytes // world if sharded else q_host.nbytes),
                "d2h_bytes_per_step": int(local_parts.count * nmod * N * M * 2),
-               "call": "irl_ccmm_run (include/irl_capi.h) with pinned host buffers"}
+               "outputs_equal_device_step": e2e_exact,
+               "call": ("1/N of the query H2D per rank + NCCL all-gather, then irl_ccmm_run_dq "
+                        "(include/irl_capi.h) with pinned host outputs") if sharded else
+                       "irl_ccmm_run (include/irl_capi.h) with pinned host buffers"}
 
     # ---- CPU baseline (rank 0, N = 1) with a bit-exact check of its rows ----
     cpu = None

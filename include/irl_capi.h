@@ -170,6 +170,13 @@ int irl_ccmm_synth_db(irl_ccmm* e, uint64_t seed, uint32_t first_part);
  * pinned (cudaHostAlloc / cudaHostRegister): pageable buffers are staged by the
  * driver and copy at a fraction of PCIe bandwidth. */
 int irl_ccmm_run(irl_ccmm* e, const uint16_t* q_res_host, size_t n, uint16_t* out_host);
+/* Query already on the device (q_res_dev [nmod][K][n], NULL = the engine's
+ * staging buffer, stream-ordered after `stream`), outputs to HOST memory:
+ * split, one PPMM launch over every part and modulus, and (modulus, part)-
+ * granular D2H overlapped with the launch; blocks. For multi-GPU callers that
+ * distribute the query over NVLink (each rank copies 1/N of it from the host
+ * and all-gathers the rest) instead of N full host copies. n <= max_n. */
+int irl_ccmm_run_dq(irl_ccmm* e, const uint16_t* q_res_dev, size_t n, uint16_t* out_host, void* stream);
 /* Device-resident variant over parts [part0, part0 + nparts): q_res_dev
  * [nmod][K][N] (split into the engine's query planes unless q_ready != 0),
  * out_dev [nparts][nmod][N][M]; stream-ordered, does not block. */

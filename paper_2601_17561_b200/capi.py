@@ -72,6 +72,7 @@ SIGNATURES = {
                                 C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "irl_rescale_residues": (C.c_int, [vp, vp, sz, sz, u32p, u32p, sz, sz, C.c_int, vp, sz, vp]),
     "irl_ccmm_rescale": (C.c_int, [vp, sz, sz, sz, sz, C.c_int, vp, vp]),
+    "irl_ccmm_run_dq": (C.c_int, [vp, vp, sz, vp, vp]),
     "irl_iris_db_create": (C.c_int, [vp, vp, vp, sz, sz, sz, C.POINTER(vp)]),
     "irl_iris_db_destroy": (C.c_int, [vp]),
     "irl_iris_db_match": (C.c_int, [vp, vp, vp, sz, sz, C.c_double, C.c_double, vp, vp, vp]),

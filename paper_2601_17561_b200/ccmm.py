@@ -90,6 +90,16 @@ class CcmmEngine:
             self.handle, capi.ptr(q_res_dev) if q_res_dev is not None else None, int(q_ready), n,
             part0, nparts, capi.ptr(out_dev) if out_dev is not None else None, s))
 
+    def run_dq(self, q_res_dev, n: int, out: np.ndarray, stream=None) -> np.ndarray:
+        """Query on the device (CUDA tensor [nmod][K][n] or None = the staging
+        buffer), outputs to host `out` [parts][nmod][n][M] (pinned for speed);
+        ordered after `stream` (default: torch's current stream); blocks."""
+        assert out.dtype == np.uint16 and out.flags.c_contiguous and out.shape == (self.parts, self.nmod, n, self.M)
+        s = C.c_void_p(stream if stream is not None else _torch_stream(self.ctx.device))
+        self.ctx.check(capi.lib().irl_ccmm_run_dq(self.handle, capi.ptr(q_res_dev) if q_res_dev is not None else None,
+                                                  n, capi.ptr(out), s))
+        return out
+
     def rescale(self, n: int, dst, drop: int, round_: bool = True, part0: int = 0,
                 nparts: Optional[int] = None, stream=None):
         """ModDown (f2) of the engine outputs of the last device run: parts

@@ -1258,6 +1258,52 @@ int irl_ccmm_run(irl_ccmm* e, const uint16_t* q_res_host, size_t n, uint16_t* ou
     return IRL_OK;
 }
 
+int irl_ccmm_run_dq(irl_ccmm* e, const uint16_t* q_res_dev, size_t n, uint16_t* out_host, void* stream) {
+    if (!e || !out_host) return IRL_ERR_INVALID_ARGUMENT;
+    irl_ctx* ctx = e->ctx;
+    Guard g(ctx);
+    if (n == 0 || n > e->max_n) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: query width out of range");
+    cudaStream_t s = pick_stream(ctx, stream);
+    if (!q_res_dev) q_res_dev = e->qres;
+    const size_t nmod = e->nmod, K = e->K, M = e->M;
+    IRL_LAUNCH(ctx, launch_split_cols<uint16_t>(q_res_dev, n, K * n, uint32_t(K), uint32_t(n), e->mt, e->qplanes,
+                                                e->ldk, nullptr, s));
+    const bool by_part = e->memops && wait_value_fn() != nullptr;
+    uint32_t* cnt = e->part_cnt;
+    if (by_part) {
+        IRL_CK(ctx, cudaMemsetAsync(cnt, 0, nmod * e->parts * sizeof(uint32_t), s));
+        IRL_CK(ctx, cudaEventRecord(e->cnt_zeroed[0], s));
+        IRL_CK(ctx, cudaStreamWaitEvent(e->copy_stream, e->cnt_zeroed[0], 0));
+    }
+    int st = ccmm_parts(e, n, 0, e->parts, e->out, s, 0, nmod, by_part ? cnt : nullptr);
+    if (st) return st;
+    const uint32_t target = ppmm_last_part_target();
+    bool waited = by_part && target > 0;
+    for (size_t i = 0; i < nmod && waited; ++i)
+        for (size_t p = 0; p < e->parts; ++p) {
+            const CUresult r = wait_value_fn()(e->copy_stream, reinterpret_cast<CUdeviceptr>(cnt + i * e->parts + p),
+                                               target, CU_STREAM_WAIT_VALUE_GEQ);
+            if (r != CUDA_SUCCESS) {
+                if (i != 0 || p != 0) return set_err(ctx, IRL_ERR_CUDA, "cuStreamWaitValue32 failed");
+                e->memops = false;
+                waited = false;
+                break;
+            }
+            const size_t row = p * nmod + i;
+            IRL_CK(ctx, cudaMemcpyAsync(out_host + row * n * M, e->out + row * n * M, n * M * 2,
+                                        cudaMemcpyDeviceToHost, e->copy_stream));
+        }
+    if (!waited) {
+        IRL_CK(ctx, cudaEventRecord(e->part_done[0], s));
+        IRL_CK(ctx, cudaStreamWaitEvent(e->copy_stream, e->part_done[0], 0));
+        IRL_CK(ctx, cudaMemcpyAsync(out_host, e->out, e->parts * nmod * n * M * 2, cudaMemcpyDeviceToHost,
+                                    e->copy_stream));
+    }
+    IRL_CK(ctx, cudaStreamSynchronize(e->copy_stream));
+    IRL_CK(ctx, cudaStreamSynchronize(s));
+    return IRL_OK;
+}
+
 int irl_ccmm_rescale(irl_ccmm* e, size_t n, size_t part0, size_t nparts, size_t drop, int round, uint16_t* dst,
                      void* stream) {
     if (!e || !dst) return IRL_ERR_INVALID_ARGUMENT;

@@ -38,3 +38,4 @@ def test_bench_multirank_same_device(world, exchange):
     assert d["exchange"]["kind"].startswith("fused" if exchange == "auto" else "NCCL")
     assert d["exchange"]["note"] is None
     assert d["value"] > 0 and d["e2e"]["value"] > 0
+    assert d["e2e"]["outputs_equal_device_step"]

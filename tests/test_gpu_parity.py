@@ -500,3 +500,22 @@ def test_blocking_api_is_thread_safe_per_context(mm):
     assert not errors
     for w, g in zip(want, got):
         assert (w == g).all()
+
+
+def test_ccmm_run_dq_equals_run():
+    # device-resident query, host outputs (the sharded-H2D multi-GPU e2e path)
+    import torch
+    from paper_2601_17561_b200.ccmm import CcmmEngine, staging_tensors, synth_query
+    eng = CcmmEngine(parts=3, m=520, k=700, max_n=96)
+    eng.synth_db(seed=8)
+    q = synth_query(9, eng.K, 96, eng.moduli)
+    want = eng.run(q)
+    qd, _ = staging_tensors(eng, 96)
+    qd.copy_(torch.from_numpy(q.view(np.int16)))
+    out = np.zeros_like(want)
+    eng.run_dq(None, 96, out)  # ordered after the copy on torch's current stream
+    assert (out == want).all()
+    dq = torch.from_numpy(q.view(np.int16)).cuda()
+    out2 = np.zeros_like(want)
+    eng.run_dq(dq, 96, out2)
+    assert (out2 == want).all()
