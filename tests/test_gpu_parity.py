@@ -519,3 +519,28 @@ def test_ccmm_run_dq_equals_run():
     out2 = np.zeros_like(want)
     eng.run_dq(dq, 96, out2)
     assert (out2 == want).all()
+
+
+@pytest.mark.parametrize("n", [1100, 1024, 2000])
+def test_ccmm_cluster_path_padded_n_chunks(n):
+    # >= 256 units so the 1x4 multicast clusters run (not the short-launch
+    # plain pairs); N not a multiple of the 1024-column n-chunk -> a padded
+    # last chunk whose empty tiles store nothing
+    from paper_2601_17561_b200.ccmm import CcmmEngine, synth_query
+    from paper_2601_17561_b200.modmat import Modulus, RnsBasis, build_paper_basis
+    full = build_paper_basis()
+    b = RnsBasis()
+    for md in full.moduli[:4]:
+        b.moduli.append(Modulus(md.p, md.e))
+        b.Q *= md.p ** md.e
+    eng = CcmmEngine(parts=1, m=1 << 14, k=512, max_n=n, basis=b)  # 64 m-blocks x 4 primes = 256 units
+    eng.synth_db(seed=12)
+    q = synth_query(13, eng.K, n, eng.moduli)
+    import torch
+    from paper_2601_17561_b200.ccmm import staging_tensors
+    qd, od = staging_tensors(eng, n)
+    qd.copy_(torch.from_numpy(q.view(np.int16)))
+    eng.run_device(None, n, None)  # one launch over all 4 primes (the e2e path chunks by modulus)
+    torch.cuda.synchronize()
+    out = od.cpu().numpy().view(np.uint16)
+    _check_ccmm(eng, 12, q, out, np.array([0, 255, 256, 9000, 16383], np.uint32))
