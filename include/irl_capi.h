@@ -41,7 +41,9 @@ typedef enum irl_status {
     IRL_ERR_NO_DEVICE = 8,
     IRL_ERR_OUT_OF_MEMORY = 9,
     IRL_ERR_UNSUPPORTED = 10,
-    IRL_ERR_ZERO_OVERLAP = 11               /* irislab::ZeroOverlap              errors.hpp:18 */
+    IRL_ERR_ZERO_OVERLAP = 11,              /* irislab::ZeroOverlap              errors.hpp:18 */
+    IRL_ERR_IO = 12                         /* irislab::Error("cannot open ..." / "truncated matrix file ...")
+                                               modmat.cpp:218, 235, 245 */
 } irl_status;
 
 typedef struct irl_ctx irl_ctx;
@@ -159,6 +161,12 @@ int irl_ccmm_destroy(irl_ccmm* e);
 int irl_ccmm_load_part(irl_ccmm* e, size_t part, const uint16_t* res, int res_on_device);
 /* Register part `part` from width-byte mod-Q entries [M][K] (host pointer). */
 int irl_ccmm_load_part_bigint(irl_ccmm* e, size_t part, const uint8_t* entries, size_t width);
+/* Stream one part from the reference's BigMatrix file (save_big_matrix,
+ * modmat.cpp:216-231): header "rows cols Q" must match (M, K, the basis Q);
+ * entries are read in 256 MB chunks, double-buffered against the H2D and the
+ * residue/digit split, so a part never has to fit in host memory.
+ * Error("truncated matrix file ...") as load_big_matrix (modmat.cpp:233-249). */
+int irl_ccmm_load_part_file(irl_ccmm* e, size_t part, const char* path);
 /* Fill every part with synthetic residues irl_synth_residue(seed, first_part + part,
  * i, row, col, m_i); first_part is the global id of local part 0 (multi-GPU). */
 int irl_ccmm_synth_db(irl_ccmm* e, uint64_t seed, uint32_t first_part);

@@ -32,6 +32,7 @@ IRL_ERR_NO_DEVICE = 8
 IRL_ERR_OUT_OF_MEMORY = 9
 IRL_ERR_UNSUPPORTED = 10
 IRL_ERR_ZERO_OVERLAP = 11
+IRL_ERR_IO = 12
 
 # Every symbol include/irl_capi.h declares, with (restype, argtypes).
 SIGNATURES = {
@@ -63,6 +64,7 @@ SIGNATURES = {
     "irl_ccmm_load_part": (C.c_int, [vp, sz, vp, C.c_int]),
     "irl_ccmm_load_part_bigint": (C.c_int, [vp, sz, u8p, sz]),
     "irl_ccmm_synth_db": (C.c_int, [vp, C.c_uint64, C.c_uint32]),
+    "irl_ccmm_load_part_file": (C.c_int, [vp, sz, C.c_char_p]),
     "irl_ccmm_run": (C.c_int, [vp, vp, sz, vp]),
     "irl_ccmm_run_device": (C.c_int, [vp, vp, C.c_int, sz, sz, sz, vp, vp]),
     "irl_ccmm_buffers": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp)]),

@@ -64,6 +64,10 @@ class CcmmEngine:
         self.ctx.check(capi.lib().irl_ccmm_load_part_bigint(self.handle, part, capi.ptr(entries, capi.u8p),
                                                             width))
 
+    def load_part_file(self, part: int, path):
+        """Stream a part from the reference's BigMatrix file (modmat.cpp:216-231)."""
+        self.ctx.check(capi.lib().irl_ccmm_load_part_file(self.handle, part, str(path).encode()))
+
     def synth_db(self, seed: int, first_part: int = 0):
         """Counter-based synthetic residues, identical to oracle's orc_synth_residue;
         local part g is global part first_part + g."""

@@ -4,6 +4,8 @@
 // value-for-value, including its exception taxonomy and messages; all the
 // arithmetic runs in this library's sm_100a kernels. There is no CPU compute
 // path: validation only reads the split kernels' device-side statistics.
+#include <unistd.h>
+
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -15,6 +17,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/irl_capi.h"
@@ -223,6 +226,7 @@ const char* irl_status_string(int s) {
         case IRL_ERR_OUT_OF_MEMORY: return "OutOfMemory";
         case IRL_ERR_UNSUPPORTED: return "Unsupported";
         case IRL_ERR_ZERO_OVERLAP: return "ZeroOverlap";
+        case IRL_ERR_IO: return "Error";
         default: return "unknown";
     }
 }
@@ -981,6 +985,111 @@ int irl_ccmm_load_part_bigint(irl_ccmm* e, size_t part, const uint8_t* entries, 
                                             uint32_t(r0), nullptr, nullptr, ctx->stream));
         IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
     }
+    return IRL_OK;
+}
+
+// Streaming ingest of one part from the reference's BigMatrix file
+// (save_big_matrix, modmat.cpp:216-231: "rows cols Q\n" then rows*cols
+// little-endian entries of ceil(log256 Q) bytes). Double-buffered: the file
+// read of chunk i+1 into pinned memory overlaps the H2D and residue/digit
+// split of chunk i, so a 2^17-template slice (148 GB of entries) never has to
+// sit in host memory.
+int irl_ccmm_load_part_file(irl_ccmm* e, size_t part, const char* path) {
+    if (!e || !path) return IRL_ERR_INVALID_ARGUMENT;
+    irl_ctx* ctx = e->ctx;
+    Guard g(ctx);
+    if (part >= e->parts) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: part index out of range");
+    for (size_t i = 0; i < e->nmod; ++i)
+        if (e->mt.mc[i].e != 2) return set_err(ctx, IRL_ERR_UNSUPPORTED, "bigint ingest needs e = 2");
+    std::FILE* f = std::fopen(path, "rb");
+    if (!f) return set_err(ctx, IRL_ERR_IO, std::string("cannot open ") + path);
+    struct Closer {
+        std::FILE* f;
+        ~Closer() { std::fclose(f); }
+    } closer{f};
+    unsigned long long rows = 0, cols = 0;
+    char qbuf[256];
+    if (std::fscanf(f, "%llu %llu %255s", &rows, &cols, qbuf) != 3 || std::fgetc(f) != '\n')
+        return set_err(ctx, IRL_ERR_IO, std::string("bad matrix header in ") + path);
+    if (rows != e->M || cols != e->K)
+        return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: file matrix is not M x K for this engine");
+    // the file's modulus must be the engine's Q
+    std::vector<uint32_t> ps(e->nmod), es(e->nmod);
+    for (size_t i = 0; i < e->nmod; ++i) ps[i] = e->mt.mc[i].p, es[i] = e->mt.mc[i].e;
+    const Limbs Q = basis_Q(ps.data(), es.data(), e->nmod);
+    Limbs fq{0};
+    for (const char* c = qbuf; *c; ++c) {
+        if (*c < '0' || *c > '9') return set_err(ctx, IRL_ERR_IO, "bad modulus in matrix header");
+        uint64_t carry = static_cast<uint64_t>(*c - '0');
+        for (auto& limb : fq) {
+            const uint64_t v = static_cast<uint64_t>(limb) * 10 + carry;
+            limb = static_cast<uint32_t>(v);
+            carry = v >> 32;
+        }
+        if (carry) fq.push_back(static_cast<uint32_t>(carry));
+    }
+    while (fq.size() > 1 && fq.back() == 0) fq.pop_back();
+    if (fq != Q) return set_err(ctx, IRL_ERR_IO, "ccmm: file modulus differs from the engine's basis Q");
+    const size_t width = byte_width(Q);
+    if (width > kMaxWidth) return set_err(ctx, IRL_ERR_UNSUPPORTED, "Q too wide");
+    const long data_off = std::ftell(f);
+    const int fd = ::fileno(f);
+    int8_t* dst = e->db + part * e->nmod * 2 * e->M * e->ldk;
+    const size_t row_bytes = e->K * width;
+    const size_t chunk = std::max<size_t>(1, std::min<size_t>(e->M, (size_t(256) << 20) / row_bytes));
+    IRL_CK(ctx, ctx->ws[2].ensure(chunk * row_bytes));
+    IRL_CK(ctx, ctx->ws[3].ensure(chunk * row_bytes));
+    uint8_t* host[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    struct Cleanup {
+        uint8_t** h;
+        cudaEvent_t* ev;
+        ~Cleanup() {
+            for (int i = 0; i < 2; ++i) {
+                if (ev[i]) cudaEventSynchronize(ev[i]), cudaEventDestroy(ev[i]);
+                if (h[i]) cudaFreeHost(h[i]);
+            }
+        }
+    } cleanup{host, done};
+    for (int i = 0; i < 2; ++i) {
+        IRL_CK(ctx, cudaMallocHost(&host[i], chunk * row_bytes));
+        IRL_CK(ctx, cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+    }
+    uint8_t* dev[2] = {ctx->ws[2].as<uint8_t>(), ctx->ws[3].as<uint8_t>()};
+    size_t ci = 0;
+    for (size_t r0 = 0; r0 < e->M; r0 += chunk, ++ci) {
+        const size_t b = ci % 2, nrows = std::min(chunk, e->M - r0), bytes = nrows * row_bytes;
+        IRL_CK(ctx, cudaEventSynchronize(done[b]));  // buffer b's previous chunk is on the device
+        // 4 readers per chunk (pread at disjoint offsets): page-cache copies and
+        // NVMe queues both scale with concurrent requests
+        {
+            constexpr int kReaders = 4;
+            bool ok[kReaders];
+            std::thread th[kReaders];
+            const size_t piece = (bytes + kReaders - 1) / kReaders;
+            for (int t = 0; t < kReaders; ++t) {
+                th[t] = std::thread([&, t] {
+                    const size_t lo = std::min(bytes, t * piece), hi = std::min(bytes, lo + piece);
+                    size_t got = 0;
+                    while (got < hi - lo) {
+                        const ssize_t r = ::pread(fd, host[b] + lo + got, hi - lo - got,
+                                                  static_cast<off_t>(data_off + r0 * row_bytes + lo + got));
+                        if (r <= 0) break;
+                        got += static_cast<size_t>(r);
+                    }
+                    ok[t] = got == hi - lo;
+                });
+            }
+            bool all = true;
+            for (int t = 0; t < kReaders; ++t) th[t].join(), all = all && ok[t];
+            if (!all) return set_err(ctx, IRL_ERR_IO, std::string("truncated matrix file ") + path);
+        }
+        IRL_CK(ctx, cudaMemcpyAsync(dev[b], host[b], bytes, cudaMemcpyHostToDevice, ctx->stream));
+        IRL_LAUNCH(ctx, launch_split_bigint(dev[b], uint32_t(width), uint32_t(nrows), uint32_t(e->K), 0, e->mt, dst,
+                                            e->ldk, uint32_t(e->M), uint32_t(r0), nullptr, nullptr, ctx->stream));
+        IRL_CK(ctx, cudaEventRecord(done[b], ctx->stream));
+    }
+    IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
     return IRL_OK;
 }
 

@@ -80,6 +80,10 @@ void CcmmEngine::load_part_bigint(std::size_t part, const modmat::BigMatrix& ent
     check(irl_ccmm_load_part_bigint(e_, part, entries.a.data(), entries.width));
 }
 
+void CcmmEngine::load_part_file(std::size_t part, const std::string& path) {
+    check(irl_ccmm_load_part_file(e_, part, path.c_str()));
+}
+
 void CcmmEngine::synth_db(uint64_t seed, uint32_t first_part) { check(irl_ccmm_synth_db(e_, seed, first_part)); }
 
 void CcmmEngine::run(const uint16_t* q_res, std::size_t n, uint16_t* out) { check(irl_ccmm_run(e_, q_res, n, out)); }

@@ -11,6 +11,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include "modmat.hpp"  // irislab::Error, ShapeMismatch, ModulusBudget, DeviceError, RnsBasis
@@ -61,6 +62,8 @@ public:
     void load_part(std::size_t part, const std::vector<uint16_t>& residues);
     /// one part as m x k little-endian mod-Q entries of `width` bytes (BigMatrix file form)
     void load_part_bigint(std::size_t part, const modmat::BigMatrix& entries);
+    /// stream one part from the reference's BigMatrix file (save_big_matrix format)
+    void load_part_file(std::size_t part, const std::string& path);
     /// counter-RNG synthetic database (the bench's inputs)
     void synth_db(uint64_t seed, uint32_t first_part = 0);
     /// q_res [nmod][k][n] -> out [parts][nmod][n][m] residues mod p^2 (blocking;

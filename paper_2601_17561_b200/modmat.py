@@ -56,6 +56,7 @@ _STATUS_EXC = {
     capi.IRL_ERR_NOT_COPRIME: Error,
     capi.IRL_ERR_MODULUS_BUDGET: ModulusBudget,
     capi.IRL_ERR_ZERO_OVERLAP: ZeroOverlap,
+    capi.IRL_ERR_IO: Error,
 }
 
 

@@ -544,3 +544,38 @@ def test_ccmm_cluster_path_padded_n_chunks(n):
     torch.cuda.synchronize()
     out = od.cpu().numpy().view(np.uint16)
     _check_ccmm(eng, 12, q, out, np.array([0, 255, 256, 9000, 16383], np.uint32))
+
+
+def test_ccmm_load_part_file_streams_reference_format(tmp_path):
+    # f3: the reference's BigMatrix file (save_big_matrix, modmat.cpp:216-231)
+    # streamed into a part equals load_part_bigint of the same entries; header
+    # and truncation errors as load_big_matrix
+    from paper_2601_17561_b200.ccmm import CcmmEngine, synth_query
+    from paper_2601_17561_b200.modmat import Error, ShapeMismatch
+    m, k, n = 300, 640, 40
+    eng = CcmmEngine(parts=2, m=m, k=k, max_n=n)
+    Q = eng.basis.Q
+    width = (Q.bit_length() + 7) // 8
+    rng = np.random.default_rng(21)
+    ent = rng.integers(0, 256, (m * k, width), dtype=np.uint8)
+    ent[:, -1] = 0                          # every entry below 2^360 < Q (Q has 361 bits)
+    assert 1 << (8 * (width - 1)) < Q
+    path = tmp_path / "part.bin"
+    with open(path, "wb") as f:
+        f.write(f"{m} {k} {Q}\n".encode())
+        f.write(ent.tobytes())
+    eng.load_part_file(0, path)
+    eng.load_part_bigint(1, ent.reshape(m, k, width), width)
+    q = synth_query(3, k, n, eng.moduli)
+    out = eng.run(q)
+    assert (out[0] == out[1]).all()
+    bad = tmp_path / "short.bin"
+    bad.write_bytes(f"{m} {k} {Q}\n".encode() + ent.tobytes()[:1000])
+    with pytest.raises(Error, match="truncated matrix file"):
+        eng.load_part_file(0, bad)
+    wrong = tmp_path / "dims.bin"
+    wrong.write_bytes(f"{m + 1} {k} {Q}\n".encode())
+    with pytest.raises(ShapeMismatch):
+        eng.load_part_file(0, wrong)
+    with pytest.raises(Error, match="cannot open"):
+        eng.load_part_file(0, tmp_path / "missing.bin")
