@@ -260,6 +260,12 @@ int irl_iris_match(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db_mas
  * (same outputs and semantics as irl_iris_match; n_eyes * rho <= max_cols). */
 int irl_iris_db_create(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db_mask, size_t n_db, size_t d,
                        size_t max_cols, irl_iris_db** out);
+/* Same database straight from the reference's template file (save_templates,
+ * iris_core.cpp:183-196: {magic "IRIT", version 1, n_db, d} then the code and
+ * mask planes, little-endian bit order); returns n_db and d. Errors as
+ * load_templates (iris_core.cpp:198-215): bad magic / version / truncated. */
+int irl_iris_db_create_file(irl_ctx* ctx, const char* path, size_t max_cols, irl_iris_db** out, size_t* n_db,
+                            size_t* d);
 int irl_iris_db_destroy(irl_iris_db* e);
 int irl_iris_db_match(irl_iris_db* e, const uint64_t* q_code, const uint64_t* q_mask, size_t n_eyes, size_t rho,
                       double p_lo, double p_hi, uint8_t* match_bits, int32_t* eye_result, double* scores);

@@ -252,6 +252,12 @@ def gen_iris_scores():
     out["intervals"] = np.array(IRIS_INTERVALS)
     out["rho"] = np.array(rho)
     np.savez_compressed(GOLDEN / "iris_scores.npz", **out)
+    # the dense database in the reference's own template file format
+    # (iris::save_templates, iris_core.cpp:183-196)
+    dc, dm = out["dense_db_code"], out["dense_db_mask"]
+    st = ol.ref().ref_save_templates(str(GOLDEN / "dense_db_templates.bin").encode(), ol.ptr(dc, ol.u8p),
+                                     ol.ptr(dm, ol.u8p), dc.shape[0], dc.shape[1])
+    assert st == 0
 
 
 if __name__ == "__main__":

@@ -362,6 +362,16 @@ void ref_iris_rotate(const uint8_t* code, const uint8_t* mask, size_t d, size_t 
     std::memcpy(out_mask, o.mask.data(), d);
 }
 
+// iris::save_templates (iris_core.cpp:183-196) of n templates [n][d].
+int ref_save_templates(const char* path, const uint8_t* code, const uint8_t* mask, size_t n, size_t d) {
+    try {
+        iris::save_templates(path, to_templates(code, mask, n, d));
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
 // iris::match_db_reference (iris_core.cpp:78-90): *out = 0/1; status 11 on ZeroOverlap.
 int ref_match_db_reference(const uint8_t* q_code, const uint8_t* q_mask, size_t nq, const uint8_t* db_code,
                            const uint8_t* db_mask, size_t n_db, size_t d, double n_lo, double n_hi,

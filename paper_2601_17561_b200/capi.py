@@ -77,6 +77,7 @@ SIGNATURES = {
     "irl_ccmm_run_dq": (C.c_int, [vp, vp, sz, vp, vp]),
     "irl_iris_db_create": (C.c_int, [vp, vp, vp, sz, sz, sz, C.POINTER(vp)]),
     "irl_iris_db_destroy": (C.c_int, [vp]),
+    "irl_iris_db_create_file": (C.c_int, [vp, C.c_char_p, sz, C.POINTER(vp), C.POINTER(sz), C.POINTER(sz)]),
     "irl_iris_db_match": (C.c_int, [vp, vp, vp, sz, sz, C.c_double, C.c_double, vp, vp, vp]),
     "irl_ccmm_alloc_recv": (C.c_int, [vp, sz, C.POINTER(vp), vp]),
     "irl_ccmm_set_mirrors": (C.c_int, [vp, sz, sz, vp, sz]),

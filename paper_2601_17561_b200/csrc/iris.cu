@@ -24,6 +24,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "ctx_internal.h"
@@ -63,6 +64,34 @@ __global__ void iris_planes_kernel(const uint64_t* __restrict__ code, const uint
     const size_t o = static_cast<size_t>(c) * ldk + k0;
     *reinterpret_cast<uint4*>(planes + o) = make_uint4(v[0], v[1], v[2], v[3]);
     *reinterpret_cast<uint4*>(planes + static_cast<size_t>(cols) * ldk + o) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// The reference's template file planes (save_templates, iris_core.cpp:148-196):
+// all templates' bits back to back, little-endian bit order (bit i of byte j
+// is element 8 j + i) -- so template t, entry k is global bit t * d + k.
+// Same outputs as iris_planes_kernel for rho = 1.
+__global__ void iris_file_planes_kernel(const uint8_t* __restrict__ code, const uint8_t* __restrict__ mask,
+                                        uint32_t d, uint32_t n, uint32_t ldk, int8_t* __restrict__ planes) {
+    const uint32_t chunks = ldk / 16;
+    const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (tid >= static_cast<size_t>(n) * chunks) return;
+    const uint32_t t = static_cast<uint32_t>(tid / chunks);
+    const uint32_t k0 = static_cast<uint32_t>(tid % chunks) * 16;
+    uint32_t v[4] = {0, 0, 0, 0}, w[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const uint32_t k = k0 + j;
+        if (k >= d) break;
+        const size_t bit = static_cast<size_t>(t) * d + k;
+        const uint32_t cb = (__ldg(code + (bit >> 3)) >> (bit & 7)) & 1u;
+        const uint32_t mb = (__ldg(mask + (bit >> 3)) >> (bit & 7)) & 1u;
+        const int32_t x = static_cast<int32_t>(mb) - 2 * static_cast<int32_t>(cb & mb);
+        v[j / 4] |= (static_cast<uint32_t>(x) & 0xFFu) << (8 * (j % 4));
+        w[j / 4] |= mb << (8 * (j % 4));
+    }
+    const size_t o = static_cast<size_t>(t) * ldk + k0;
+    *reinterpret_cast<uint4*>(planes + o) = make_uint4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<uint4*>(planes + static_cast<size_t>(n) * ldk + o) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 size_t round16(size_t x) { return (x + 15) / 16 * 16; }
@@ -307,6 +336,72 @@ int irl_iris_db_create(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db
         irl_iris_db_destroy(e);
         return err != cudaSuccess ? cuda_fail(ctx, err, "irl_iris_db_create") : st;
     }
+    *out = e;
+    return IRL_OK;
+}
+
+int irl_iris_db_create_file(irl_ctx* ctx, const char* path, size_t max_cols, irl_iris_db** out, size_t* n_db_out,
+                            size_t* d_out) {
+    if (!ctx || !path || !out) return IRL_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    Guard g(ctx);
+    std::FILE* f = std::fopen(path, "rb");
+    if (!f) return set_err(ctx, IRL_ERR_IO, std::string("cannot open ") + path);
+    struct Closer {
+        std::FILE* f;
+        ~Closer() { std::fclose(f); }
+    } closer{f};
+    // header {magic "IRIT", version 1, n_db, d}, little-endian (iris_core.cpp:183-196)
+    uint8_t hdr[24];
+    if (std::fread(hdr, 1, sizeof(hdr), f) != sizeof(hdr))
+        return set_err(ctx, IRL_ERR_IO, std::string("bad template file magic in ") + path);
+    auto u32 = [&](int o) { uint32_t v = 0; for (int i = 0; i < 4; ++i) v |= uint32_t(hdr[o + i]) << (8 * i); return v; };
+    auto u64 = [&](int o) { uint64_t v = 0; for (int i = 0; i < 8; ++i) v |= uint64_t(hdr[o + i]) << (8 * i); return v; };
+    if (u32(0) != 0x49524954u) return set_err(ctx, IRL_ERR_IO, std::string("bad template file magic in ") + path);
+    if (u32(4) != 1u) return set_err(ctx, IRL_ERR_IO, "unsupported template file version");
+    const uint64_t n = u64(8), d = u64(16);
+    if (n == 0 || d == 0) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "iris db: empty template file");
+    if (max_cols == 0) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "iris db: empty database or batch");
+    if (int st = check_dims(ctx, n, max_cols, d)) return st;
+    const size_t plane_bytes = (n * d + 7) / 8;
+    uint8_t* host = nullptr;
+    IRL_CK(ctx, cudaMallocHost(&host, 2 * plane_bytes));
+    struct HostFree {
+        uint8_t* p;
+        ~HostFree() { cudaFreeHost(p); }
+    } hf{host};
+    if (std::fread(host, 1, 2 * plane_bytes, f) != 2 * plane_bytes)
+        return set_err(ctx, IRL_ERR_IO, std::string("truncated template file ") + path);
+    auto* e = new irl_iris_db();
+    e->ctx = ctx;
+    e->n_db = n;
+    e->d = d;
+    e->ldk = round16(d);
+    e->max_cols = max_cols;
+    const size_t words = (d + 63) / 64;
+    uint8_t* staging = nullptr;
+    cudaError_t err = cudaMalloc(&e->planes, 2 * n * e->ldk);
+    if (err == cudaSuccess) err = cudaMalloc(&e->qplanes, 2 * max_cols * e->ldk);
+    if (err == cudaSuccess) err = cudaMalloc(&e->qbits, 2 * max_cols * words * 8);
+    if (err == cudaSuccess) err = cudaMalloc(&e->progress, kScheduleScratchBytes);
+    if (err == cudaSuccess) err = cudaMalloc(&staging, 2 * plane_bytes);
+    if (err == cudaSuccess) err = cudaMemcpyAsync(staging, host, 2 * plane_bytes, cudaMemcpyHostToDevice, ctx->stream);
+    if (err == cudaSuccess) {
+        const size_t total = n * (e->ldk / 16);
+        iris_file_planes_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, ctx->stream>>>(
+            staging, staging + plane_bytes, static_cast<uint32_t>(d), static_cast<uint32_t>(n),
+            static_cast<uint32_t>(e->ldk), e->planes);
+        err = cudaGetLastError();
+        if (err == cudaSuccess) ++ctx->launches;
+    }
+    if (err == cudaSuccess) err = cudaStreamSynchronize(ctx->stream);
+    cudaFree(staging);
+    if (err != cudaSuccess) {
+        irl_iris_db_destroy(e);
+        return cuda_fail(ctx, err, "irl_iris_db_create_file");
+    }
+    if (n_db_out) *n_db_out = n;
+    if (d_out) *d_out = d;
     *out = e;
     return IRL_OK;
 }

@@ -162,6 +162,21 @@ class IrisDatabase:
         self.handle = h
         return self
 
+    @classmethod
+    def from_file(cls, path, max_cols: int, ctx: Optional[Context] = None) -> "IrisDatabase":
+        """The enrolled templates straight from the reference's template file
+        (save_templates, iris_core.cpp:183-196)."""
+        import ctypes as C
+        self = cls.__new__(cls)
+        self.ctx = ctx or default_context()
+        h = C.c_void_p()
+        n, d = C.c_size_t(), C.c_size_t()
+        self.ctx.check(capi.lib().irl_iris_db_create_file(self.ctx.handle, str(path).encode(), max_cols, C.byref(h),
+                                                          C.byref(n), C.byref(d)))
+        self.handle = h
+        self.n_db, self.d, self.max_cols = n.value, d.value, max_cols
+        return self
+
     def match_packed(self, q_code, q_mask, n_eyes: int, rho: int, p_int: Interval, want_scores=False):
         bits = np.zeros((n_eyes, self.n_db), np.uint8)
         res = np.zeros(n_eyes, np.int32)
@@ -189,3 +204,22 @@ class IrisDatabase:
             self.close()
         except Exception:
             pass
+
+
+def save_templates(path, templates: Sequence[IrisTemplate]):
+    """The reference's packed template file (iris_core.cpp:183-196): little-endian
+    header {magic 0x49524954, version 1, n, d}, then the code plane and the mask
+    plane, each n*d bits back to back, bit i of byte j = element 8j + i."""
+    n = len(templates)
+    d = templates[0].size() if n else 0
+    for t in templates:
+        if t.size() != d:
+            raise ShapeMismatch("all templates must share one length")
+    hdr = (0x49524954).to_bytes(4, "little") + (1).to_bytes(4, "little") + n.to_bytes(8, "little") + \
+        d.to_bytes(8, "little")
+    code = np.concatenate([np.asarray(t.code, np.uint8) for t in templates]) if n else np.zeros(0, np.uint8)
+    mask = np.concatenate([np.asarray(t.mask, np.uint8) for t in templates]) if n else np.zeros(0, np.uint8)
+    with open(path, "wb") as f:
+        f.write(hdr)
+        f.write(np.packbits(code, bitorder="little").tobytes())
+        f.write(np.packbits(mask, bitorder="little").tobytes())

@@ -101,6 +101,7 @@ def ref() -> C.CDLL:
         f64p = C.POINTER(C.c_double)
         lib.ref_iris_scores.argtypes = [u8p, u8p, sz, u8p, u8p, sz, sz, f64p]
         lib.ref_iris_rotate.argtypes = [u8p, u8p, sz, sz, u8p, u8p]
+        lib.ref_save_templates.argtypes = [C.c_char_p, u8p, u8p, sz, sz]
         lib.ref_match_db_reference.argtypes = [u8p, u8p, sz, u8p, u8p, sz, sz, C.c_double, C.c_double,
                                                C.c_double, C.c_double, C.POINTER(C.c_int)]
         _ref = lib
