@@ -297,23 +297,34 @@ __global__ void __launch_bounds__(256) rescale_vec_kernel(const uint16_t* __rest
     uint32_t k[8];
 #pragma unroll
     for (int l = 0; l < 8; ++l) k[l] = (S[l] >= t.delta) + (S[l] >= 2 * t.delta);
-    for (uint32_t i = 0; i < keep; ++i) {
-        const uint32_t m = t.m[i], mg = t.magic[i], c32 = t.c32[i], dinv = t.dinv[i], ad = t.add[i];
-        const uint32_t w0 = t.w[0][i], w1 = t.w[1][i], w2 = t.w[2][i];
-        const uint4 q = __ldg(reinterpret_cast<const uint4*>(in + i * ld_in + e0));
-        const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
-        uint32_t y[8];
+    // kept moduli in groups of 4: the 4 loads are in flight together (one
+    // 16-byte load per modulus plane and thread)
+    for (uint32_t i0 = 0; i0 < keep; i0 += 4) {
+        uint4 q[4];
 #pragma unroll
-        for (int l = 0; l < 8; ++l) {
-            const uint32_t x = (qw[l / 2] >> (16 * (l % 2))) & 0xFFFFu;
-            unsigned long long acc = static_cast<unsigned long long>(x + ad) * dinv + k[l];
-            acc += static_cast<unsigned long long>(u[0][l]) * w0;
-            acc += static_cast<unsigned long long>(u[1][l]) * w1;
-            acc += static_cast<unsigned long long>(u[2][l]) * w2;
-            y[l] = mod_u35(acc, m, mg, c32);
+        for (int g = 0; g < 4; ++g)
+            q[g] = i0 + g < keep ? __ldg(reinterpret_cast<const uint4*>(in + (i0 + g) * ld_in + e0))
+                                 : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            const uint32_t i = i0 + g;
+            if (i >= keep) break;
+            const uint32_t m = t.m[i], mg = t.magic[i], c32 = t.c32[i], dinv = t.dinv[i], ad = t.add[i];
+            const uint32_t w0 = t.w[0][i], w1 = t.w[1][i], w2 = t.w[2][i];
+            const uint32_t qw[4] = {q[g].x, q[g].y, q[g].z, q[g].w};
+            uint32_t y[8];
+#pragma unroll
+            for (int l = 0; l < 8; ++l) {
+                const uint32_t x = (qw[l / 2] >> (16 * (l % 2))) & 0xFFFFu;
+                unsigned long long acc = static_cast<unsigned long long>(x + ad) * dinv + k[l];
+                acc += static_cast<unsigned long long>(u[0][l]) * w0;
+                acc += static_cast<unsigned long long>(u[1][l]) * w1;
+                acc += static_cast<unsigned long long>(u[2][l]) * w2;
+                y[l] = mod_u35(acc, m, mg, c32);
+            }
+            *reinterpret_cast<uint4*>(out + i * ld_out + e0) =
+                make_uint4(y[0] | (y[1] << 16), y[2] | (y[3] << 16), y[4] | (y[5] << 16), y[6] | (y[7] << 16));
         }
-        *reinterpret_cast<uint4*>(out + i * ld_out + e0) =
-            make_uint4(y[0] | (y[1] << 16), y[2] | (y[3] << 16), y[4] | (y[5] << 16), y[6] | (y[7] << 16));
     }
 }
 
