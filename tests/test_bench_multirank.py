@@ -22,11 +22,12 @@ def _port():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,exchange", [(2, "auto"), (2, "broadcast"), (4, "auto")])
+@pytest.mark.parametrize("world,exchange", [(2, "auto"), (2, "broadcast"), (4, "auto"), (8, "auto")])
 def test_bench_multirank_same_device(world, exchange):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", f"--master-port={_port()}", str(ROOT / "bench.py"), "--gpus", str(world),
-           "--steps", "2", "--warmup", "3", "--backend", "gloo", "--same-device", "--parts", "4", "--rows", "2048",
+           "--steps", "2", "--warmup", "3", "--backend", "gloo", "--same-device", "--parts", str(max(4, world)),
+           "--rows", "2048",
            "--k", "4096", "--no-cpu-baseline", "--no-int8-ref", "--exchange", exchange]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT,
                        env={**os.environ, "OMP_NUM_THREADS": "1"})
