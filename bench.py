@@ -508,6 +508,25 @@ def main():
                         "(include/irl_capi.h) with pinned host outputs") if sharded else
                        "irl_ccmm_run (include/irl_capi.h) with pinned host buffers"}
 
+    # ---- N > 1: every rank checks sampled rows of its first local part against
+    # the CPU oracle (test infrastructure, oracle/irl_oracle.c), folded with MIN
+    dist_check = None
+    if world > 1 and not args.no_cpu_baseline:
+        sys.path.insert(0, str(ROOT / "tests"))
+        import oracle_lib as ol
+        part_g = local_parts.first
+        rows = np.array([0, M // 2, M - 1], np.uint32)
+        got_all = out_dev[0].cpu().numpy().view(np.uint16)  # [nmod][N][M] of the first local part
+        ok = True
+        for i, m_ in enumerate(moduli):
+            a_blk = ol.synth_block(args.seed, part_g, i, 0, M, 0, K, m_)
+            want = ol.ppmm_rows_direct(a_blk, np.ascontiguousarray(q_host[i].T), rows, m_)
+            ok &= bool((got_all[i][:, rows].T == want).all())
+        ok_t = torch.tensor([1 if ok else 0], dtype=torch.int32, device="cuda")
+        dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
+        dist_check = {"rows_per_rank": int(len(rows)), "moduli": nmod, "bit_exact_all_ranks": bool(ok_t.item()),
+                      "oracle": "oracle/irl_oracle.c (pinned to the reference)"}
+
     # ---- CPU baseline (rank 0, N = 1) with a bit-exact check of its rows ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -571,7 +590,7 @@ def main():
                 "exchange": None if world == 1 else {
                     "kind": "fused P2P stores in the a-part PPMM epilogue (CUDA IPC, NVLink)" if exchange == "mirror"
                     else "NCCL broadcast after the local GEMMs", "note": exch_note},
-                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "dist_check": dist_check,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:
