@@ -519,9 +519,11 @@ def main():
         got_all = out_dev[0].cpu().numpy().view(np.uint16)  # [nmod][N][M] of the first local part
         ok = True
         for i, m_ in enumerate(moduli):
-            a_blk = ol.synth_block(args.seed, part_g, i, 0, M, 0, K, m_)
-            want = ol.ppmm_rows_direct(a_blk, np.ascontiguousarray(q_host[i].T), rows, m_)
-            ok &= bool((got_all[i][:, rows].T == want).all())
+            qt = np.ascontiguousarray(q_host[i].T)
+            for r_ in rows:  # only the sampled DB rows are generated
+                a_row = ol.synth_block(args.seed, part_g, i, int(r_), 1, 0, K, m_)
+                want = ol.ppmm_rows_direct(a_row, qt, np.zeros(1, np.uint32), m_)
+                ok &= bool((got_all[i][:, int(r_)] == want[0]).all())
         ok_t = torch.tensor([1 if ok else 0], dtype=torch.int32, device="cuda")
         dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
         dist_check = {"rows_per_rank": int(len(rows)), "moduli": nmod, "bit_exact_all_ranks": bool(ok_t.item()),
