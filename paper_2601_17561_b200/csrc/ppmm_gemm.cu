@@ -931,7 +931,7 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     if (si != 0) {
         const uint32_t ppc = static_cast<uint32_t>(shp.pm * shp.pn);
         const uint32_t spare_pairs = occ2 > ppc * occ_main ? occ2 - ppc * occ_main : 0;
-        if (L.max_clusters == 0 && spare_pairs > 0) plan(0, spare_pairs);
+        if (L.max_clusters == 0 && spare_pairs > 0 && !std::getenv("IRL_PPMM_NO_FILLER")) plan(0, spare_pairs);
     }
     if (std::getenv("IRL_PPMM_VERBOSE")) {
         for (int i = 0; i < nparts; ++i)
