@@ -208,6 +208,103 @@ bool inv_mod(uint32_t a, uint32_t m, uint32_t* out) {
 
 }  // namespace
 
+namespace irl {
+
+namespace {
+constexpr size_t kBounceBytes = size_t(16) << 20;
+constexpr size_t kDirectCopyBytes = size_t(4) << 20;  // below this the driver's own staging is fine
+constexpr int kCopyThreads = 8;
+
+cudaError_t ensure_bounce(irl_ctx* ctx) {
+    for (int i = 0; i < 2; ++i) {
+        if (!ctx->bounce[i]) {
+            cudaError_t e = cudaMallocHost(&ctx->bounce[i], kBounceBytes);
+            if (e != cudaSuccess) return e;
+        }
+        if (!ctx->bounce_ev[i]) {
+            cudaError_t e = cudaEventCreateWithFlags(&ctx->bounce_ev[i], cudaEventDisableTiming);
+            if (e != cudaSuccess) return e;
+        }
+    }
+    return cudaSuccess;
+}
+
+void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+    if (bytes < (size_t(1) << 20)) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    std::thread th[kCopyThreads];
+    const size_t piece = (bytes + kCopyThreads - 1) / kCopyThreads;
+    for (int t = 0; t < kCopyThreads; ++t) {
+        const size_t lo = std::min(bytes, t * piece), hi = std::min(bytes, lo + piece);
+        th[t] = std::thread([=] {
+            if (hi > lo) std::memcpy(static_cast<uint8_t*>(dst) + lo, static_cast<const uint8_t*>(src) + lo, hi - lo);
+        });
+    }
+    for (auto& t : th) t.join();
+}
+}  // namespace
+
+cudaError_t copy_h2d(irl_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes < kDirectCopyBytes) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+    cudaError_t e = ensure_bounce(ctx);
+    if (e != cudaSuccess) return e;
+    for (size_t off = 0, i = 0; off < bytes; off += kBounceBytes, ++i) {
+        const int b = static_cast<int>(i % 2);
+        const size_t len = std::min(kBounceBytes, bytes - off);
+        e = cudaEventSynchronize(ctx->bounce_ev[b]);  // its previous DMA has read it
+        if (e != cudaSuccess) return e;
+        parallel_memcpy(ctx->bounce[b], static_cast<const uint8_t*>(src) + off, len);
+        e = cudaMemcpyAsync(static_cast<uint8_t*>(dst) + off, ctx->bounce[b], len, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaEventRecord(ctx->bounce_ev[b], s);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t copy_d2h(irl_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    cudaError_t e;
+    if (bytes < kDirectCopyBytes) {
+        e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s);
+        return e == cudaSuccess ? cudaStreamSynchronize(s) : e;
+    }
+    e = ensure_bounce(ctx);
+    if (e != cudaSuccess) return e;
+    // DMA chunk i into bounce i%2 while the host drains chunk i-1
+    size_t prev_off = 0, prev_len = 0;
+    for (size_t off = 0, i = 0;; off += kBounceBytes, ++i) {
+        const int b = static_cast<int>(i % 2);
+        const size_t len = off < bytes ? std::min(kBounceBytes, bytes - off) : 0;
+        if (len) {
+            e = cudaMemcpyAsync(ctx->bounce[b], static_cast<const uint8_t*>(src) + off, len, cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaEventRecord(ctx->bounce_ev[b], s);
+            if (e != cudaSuccess) return e;
+        }
+        if (prev_len) {
+            const int pb = 1 - b;
+            e = cudaEventSynchronize(ctx->bounce_ev[pb]);
+            if (e != cudaSuccess) return e;
+            parallel_memcpy(static_cast<uint8_t*>(dst) + prev_off, ctx->bounce[pb], prev_len);
+        }
+        if (!len) break;
+        prev_off = off;
+        prev_len = len;
+    }
+    return cudaStreamSynchronize(s);
+}
+
+void release_bounce(irl_ctx* ctx) {
+    for (int i = 0; i < 2; ++i) {
+        if (ctx->bounce_ev[i]) cudaEventDestroy(ctx->bounce_ev[i]);
+        if (ctx->bounce[i]) cudaFreeHost(ctx->bounce[i]);
+        ctx->bounce_ev[i] = nullptr;
+        ctx->bounce[i] = nullptr;
+    }
+}
+
+}  // namespace irl
+
 extern "C" {
 
 int irl_abi_version(void) { return IRL_ABI_VERSION; }
@@ -270,6 +367,7 @@ int irl_ctx_destroy(irl_ctx* ctx) {
     cudaFreeHost(ctx->h_absmax);
     cudaFree(ctx->d_progress);
     cudaFree(ctx->d_diag);
+    release_bounce(ctx);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
     return IRL_OK;
@@ -351,10 +449,10 @@ int irl_digit_decompose(irl_ctx* ctx, const int32_t* m, size_t rows, size_t cols
     const size_t bytes = n * sizeof(int32_t);
     IRL_CK(ctx, ctx->ws[0].ensure(3 * bytes));
     int32_t* din = ctx->ws[0].as<int32_t>();
-    IRL_CK(ctx, cudaMemcpyAsync(din, m, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    IRL_CK(ctx, copy_h2d(ctx, din, m, bytes, ctx->stream));
     IRL_LAUNCH(ctx, launch_digit_decompose(din, n, make_modconst(p, 2), din + n, din + 2 * n, ctx->stream));
-    IRL_CK(ctx, cudaMemcpyAsync(d0, din + n, bytes, cudaMemcpyDeviceToHost, ctx->stream));
-    IRL_CK(ctx, cudaMemcpyAsync(d1, din + 2 * n, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    IRL_CK(ctx, copy_d2h(ctx, d0, din + n, bytes, ctx->stream));
+    IRL_CK(ctx, copy_d2h(ctx, d1, din + 2 * n, bytes, ctx->stream));
     IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
     return IRL_OK;
 }
@@ -370,10 +468,10 @@ int irl_digit_recompose(irl_ctx* ctx, const int32_t* d0, const int32_t* d1, size
     const size_t bytes = n * sizeof(int32_t);
     IRL_CK(ctx, ctx->ws[0].ensure(3 * bytes));
     int32_t* b = ctx->ws[0].as<int32_t>();
-    IRL_CK(ctx, cudaMemcpyAsync(b, d0, bytes, cudaMemcpyHostToDevice, ctx->stream));
-    IRL_CK(ctx, cudaMemcpyAsync(b + n, d1, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    IRL_CK(ctx, copy_h2d(ctx, b, d0, bytes, ctx->stream));
+    IRL_CK(ctx, copy_h2d(ctx, b + n, d1, bytes, ctx->stream));
     IRL_LAUNCH(ctx, launch_digit_recompose(b, b + n, n, make_modconst(p, 2), b + 2 * n, ctx->stream));
-    IRL_CK(ctx, cudaMemcpyAsync(out, b + 2 * n, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    IRL_CK(ctx, copy_d2h(ctx, out, b + 2 * n, bytes, ctx->stream));
     IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
     return IRL_OK;
 }
@@ -393,8 +491,8 @@ int irl_small_gemm(irl_ctx* ctx, const int32_t* a, const int32_t* b, int32_t* c,
     int32_t* da = ctx->ws[0].as<int32_t>();
     int32_t* db = da + na;
     int32_t* dc = db + nb;
-    if (na) IRL_CK(ctx, cudaMemcpyAsync(da, a, na * 4, cudaMemcpyHostToDevice, ctx->stream));
-    if (nb) IRL_CK(ctx, cudaMemcpyAsync(db, b, nb * 4, cudaMemcpyHostToDevice, ctx->stream));
+    if (na) IRL_CK(ctx, copy_h2d(ctx, da, a, na * 4, ctx->stream));
+    if (nb) IRL_CK(ctx, copy_h2d(ctx, db, b, nb * 4, ctx->stream));
     IRL_CK(ctx, cudaMemsetAsync(ctx->d_absmax, 0, 2 * sizeof(int32_t), ctx->stream));
     IRL_LAUNCH(ctx, launch_absmax_i32(da, na, ctx->d_absmax, ctx->stream));
     IRL_LAUNCH(ctx, launch_absmax_i32(db, nb, ctx->d_absmax + 1, ctx->stream));
@@ -405,7 +503,7 @@ int irl_small_gemm(irl_ctx* ctx, const int32_t* a, const int32_t* b, int32_t* c,
         return set_err(ctx, IRL_ERR_ACCUMULATION_OVERFLOW_RISK, kOverflowMsg + std::to_string(bound));
     if (nc == 0) return IRL_OK;
     IRL_LAUNCH(ctx, launch_gemm_i32(da, db, dc, uint32_t(m), uint32_t(k), uint32_t(n), ctx->stream));
-    IRL_CK(ctx, cudaMemcpyAsync(c, dc, nc * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    IRL_CK(ctx, copy_d2h(ctx, c, dc, nc * 4, ctx->stream));
     IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
     return IRL_OK;
 }
@@ -442,8 +540,8 @@ int irl_gemm_mod_psq(irl_ctx* ctx, const int32_t* a, const int32_t* b, int32_t* 
     int8_t* plb = reinterpret_cast<int8_t*>(base + off_pb);
     uint16_t* dout = reinterpret_cast<uint16_t*>(base + off_o);
     int32_t* dc = reinterpret_cast<int32_t*>(base + off_c);
-    if (na) IRL_CK(ctx, cudaMemcpyAsync(da, a, na * 4, cudaMemcpyHostToDevice, ctx->stream));
-    if (nb) IRL_CK(ctx, cudaMemcpyAsync(db, b, nb * 4, cudaMemcpyHostToDevice, ctx->stream));
+    if (na) IRL_CK(ctx, copy_h2d(ctx, da, a, na * 4, ctx->stream));
+    if (nb) IRL_CK(ctx, copy_h2d(ctx, db, b, nb * 4, ctx->stream));
     ModTable mt{};
     mt.n = 1;
     mt.mc[0] = make_modconst(p, 2);
@@ -477,7 +575,7 @@ int irl_gemm_mod_psq(irl_ctx* ctx, const int32_t* a, const int32_t* b, int32_t* 
     int st = run_ppmm(ctx, L, safe_kchunk(a0, a1, b0, b1, uint32_t(k)), ctx->stream);
     if (st) return st;
     IRL_LAUNCH(ctx, launch_transpose_u16_to_i32(dout, uint32_t(m), uint32_t(n), dc, ctx->stream));
-    IRL_CK(ctx, cudaMemcpyAsync(c, dc, m * n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    IRL_CK(ctx, copy_d2h(ctx, c, dc, m * n * 4, ctx->stream));
     IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
     return IRL_OK;
 }
@@ -525,8 +623,8 @@ int irl_gemm_mod_Q(irl_ctx* ctx, const uint8_t* a, const uint8_t* b, uint8_t* c,
     int32_t* rc = reinterpret_cast<int32_t*>(base + o_rc);
     uint16_t* dres = reinterpret_cast<uint16_t*>(base + o_res);
     uint8_t* dout = base + o_out;
-    if (ba) IRL_CK(ctx, cudaMemcpyAsync(dA, a, ba, cudaMemcpyHostToDevice, ctx->stream));
-    if (bb) IRL_CK(ctx, cudaMemcpyAsync(dB, b, bb, cudaMemcpyHostToDevice, ctx->stream));
+    if (ba) IRL_CK(ctx, copy_h2d(ctx, dA, a, ba, ctx->stream));
+    if (bb) IRL_CK(ctx, copy_h2d(ctx, dB, b, bb, ctx->stream));
     IRL_CK(ctx, cudaMemsetAsync(pla, 0, pa, ctx->stream));
     IRL_CK(ctx, cudaMemsetAsync(plb, 0, pb, ctx->stream));
     // Two stats tables: A in d_stats[0..], B in the workspace tail.
@@ -616,7 +714,7 @@ int irl_gemm_mod_Q(irl_ctx* ctx, const uint8_t* a, const uint8_t* b, uint8_t* c,
         }
     }
     IRL_LAUNCH(ctx, launch_crt_lift(dres, uint32_t(m), uint32_t(n), t, dout, ctx->stream));
-    IRL_CK(ctx, cudaMemcpyAsync(c, dout, outb, cudaMemcpyDeviceToHost, ctx->stream));
+    IRL_CK(ctx, copy_d2h(ctx, c, dout, outb, ctx->stream));
     IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
     return IRL_OK;
 }
@@ -1477,8 +1575,8 @@ int irl_ccmm_twin(irl_ctx* ctx, long d1, long d2, long d3, long n_db, long n_qry
     double* ddb = reinterpret_cast<double*>(base + o_db);
     double* dq = reinterpret_cast<double*>(base + o_q);
     int* dbad = reinterpret_cast<int*>(base + o_bad);
-    IRL_CK(ctx, cudaMemcpyAsync(ddb, db, M * K * 8, cudaMemcpyHostToDevice, ctx->stream));
-    IRL_CK(ctx, cudaMemcpyAsync(dq, qry, K * N * 8, cudaMemcpyHostToDevice, ctx->stream));
+    IRL_CK(ctx, copy_h2d(ctx, ddb, db, M * K * 8, ctx->stream));
+    IRL_CK(ctx, copy_h2d(ctx, dq, qry, K * N * 8, ctx->stream));
     IRL_CK(ctx, cudaMemsetAsync(dbad, 0, 4, ctx->stream));
     // Modulus count: |product| <= K max|db| max|qry| must stay inside the
     // centred range of Q (validation of the host inputs' magnitudes only;
@@ -1539,7 +1637,7 @@ int irl_ccmm_twin(irl_ctx* ctx, long d1, long d2, long d3, long n_db, long n_qry
     double* dout = reinterpret_cast<double*>(base + o_out);
     IRL_LAUNCH(ctx, launch_crt_centred_double(res, uint32_t(M), uint32_t(N), t, dout, ctx->stream));
     // [N][M] column-major product == ccmm_twin's ciphertext message order
-    IRL_CK(ctx, cudaMemcpyAsync(msgs, dout, N * M * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    IRL_CK(ctx, copy_d2h(ctx, msgs, dout, N * M * 8, ctx->stream));
     IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
     return IRL_OK;
 }

@@ -60,6 +60,9 @@ struct irl_ctx {
     uint32_t* d_progress = nullptr;  // group-gating scratch of the PPMM kernel
     uint64_t* d_diag = nullptr;      // PPMM diagnostics (irl_diag_ppmm), lazily allocated
     bool diag = false;
+    // pinned bounce buffers for large copies of caller (pageable) host memory
+    uint8_t* bounce[2] = {nullptr, nullptr};
+    cudaEvent_t bounce_ev[2] = {nullptr, nullptr};
 };
 
 
@@ -101,5 +104,14 @@ struct Guard {
 inline cudaStream_t pick_stream(irl_ctx* ctx, void* s) {
     return s ? static_cast<cudaStream_t>(s) : ctx->stream;
 }
+
+// Copies between caller host memory (usually pageable) and the device for the
+// blocking host-buffer API. Large copies go through the context's two pinned
+// 16 MB bounce buffers; several host threads fill (drain) one buffer while the
+// DMA of the other runs, instead of the driver's single-threaded staging.
+// h2d is stream-ordered on s; d2h returns once dst holds the data.
+cudaError_t copy_h2d(irl_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t s);
+cudaError_t copy_d2h(irl_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t s);
+void release_bounce(irl_ctx* ctx);
 
 }  // namespace irl
