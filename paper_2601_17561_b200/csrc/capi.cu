@@ -1049,7 +1049,7 @@ int irl_ccmm_load_part(irl_ccmm* e, size_t part, const uint16_t* res, int res_on
         const uint16_t* src = res + i * plane_elems;
         if (!res_on_device) {
             IRL_CK(ctx, ctx->ws[2].ensure(plane_elems * 2));
-            IRL_CK(ctx, cudaMemcpyAsync(ctx->ws[2].p, src, plane_elems * 2, cudaMemcpyHostToDevice, ctx->stream));
+            IRL_CK(ctx, copy_h2d(ctx, ctx->ws[2].p, src, plane_elems * 2, ctx->stream));
             src = ctx->ws[2].as<uint16_t>();
         }
         ModTable one{};
@@ -1076,8 +1076,7 @@ int irl_ccmm_load_part_bigint(irl_ccmm* e, size_t part, const uint8_t* entries, 
     IRL_CK(ctx, ctx->ws[2].ensure(chunk * row_bytes));
     for (size_t r0 = 0; r0 < e->M; r0 += chunk) {
         const size_t rows = std::min(chunk, e->M - r0);
-        IRL_CK(ctx, cudaMemcpyAsync(ctx->ws[2].p, entries + r0 * row_bytes, rows * row_bytes,
-                                    cudaMemcpyHostToDevice, ctx->stream));
+        IRL_CK(ctx, copy_h2d(ctx, ctx->ws[2].p, entries + r0 * row_bytes, rows * row_bytes, ctx->stream));
         IRL_LAUNCH(ctx, launch_split_bigint(ctx->ws[2].as<uint8_t>(), uint32_t(width), uint32_t(rows),
                                             uint32_t(e->K), 0, e->mt, dst, e->ldk, uint32_t(e->M),
                                             uint32_t(r0), nullptr, nullptr, ctx->stream));

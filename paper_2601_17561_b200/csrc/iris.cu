@@ -211,10 +211,10 @@ int inner_overlap_device(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* 
     auto* dm = reinterpret_cast<uint64_t*>(bitbuf + db_bits);
     auto* qc = reinterpret_cast<uint64_t*>(bitbuf + 2 * db_bits);
     auto* qm = reinterpret_cast<uint64_t*>(bitbuf + 2 * db_bits + q_bits);
-    IRL_CK(ctx, cudaMemcpyAsync(dc, db_code, db_bits, cudaMemcpyHostToDevice, s));
-    IRL_CK(ctx, cudaMemcpyAsync(dm, db_mask, db_bits, cudaMemcpyHostToDevice, s));
-    IRL_CK(ctx, cudaMemcpyAsync(qc, q_code, q_bits, cudaMemcpyHostToDevice, s));
-    IRL_CK(ctx, cudaMemcpyAsync(qm, q_mask, q_bits, cudaMemcpyHostToDevice, s));
+    IRL_CK(ctx, copy_h2d(ctx, dc, db_code, db_bits, s));
+    IRL_CK(ctx, copy_h2d(ctx, dm, db_mask, db_bits, s));
+    IRL_CK(ctx, copy_h2d(ctx, qc, q_code, q_bits, s));
+    IRL_CK(ctx, copy_h2d(ctx, qm, q_mask, q_bits, s));
     int8_t* xp = ctx->ws[1].as<int8_t>();
     int8_t* yp = ctx->ws[2].as<int8_t>();
     if (int st = build_planes(ctx, dc, dm, n_db, 1, d, xp, s)) return st;
@@ -294,10 +294,10 @@ int irl_iris_match(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db_mas
     auto* dm = reinterpret_cast<uint64_t*>(bitbuf + db_bits);
     auto* qc = reinterpret_cast<uint64_t*>(bitbuf + 2 * db_bits);
     auto* qm = reinterpret_cast<uint64_t*>(bitbuf + 2 * db_bits + q_bits);
-    IRL_CK(ctx, cudaMemcpyAsync(dc, db_code, db_bits, cudaMemcpyHostToDevice, s));
-    IRL_CK(ctx, cudaMemcpyAsync(dm, db_mask, db_bits, cudaMemcpyHostToDevice, s));
-    IRL_CK(ctx, cudaMemcpyAsync(qc, q_code, q_bits, cudaMemcpyHostToDevice, s));
-    IRL_CK(ctx, cudaMemcpyAsync(qm, q_mask, q_bits, cudaMemcpyHostToDevice, s));
+    IRL_CK(ctx, copy_h2d(ctx, dc, db_code, db_bits, s));
+    IRL_CK(ctx, copy_h2d(ctx, dm, db_mask, db_bits, s));
+    IRL_CK(ctx, copy_h2d(ctx, qc, q_code, q_bits, s));
+    IRL_CK(ctx, copy_h2d(ctx, qm, q_mask, q_bits, s));
     if (int st = build_planes(ctx, dc, dm, n_db, 1, d, ctx->ws[1].as<int8_t>(), s)) return st;
     if (int st = build_planes(ctx, qc, qm, n_eyes, rho, d, ctx->ws[2].as<int8_t>(), s)) return st;
     return match_fused(ctx, ctx->ws[1].as<int8_t>(), ctx->ws[2].as<int8_t>(), n_db, n_eyes, rho, d, ldk, p_lo, p_hi,
@@ -325,9 +325,9 @@ int irl_iris_db_create(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db
     if (err == cudaSuccess) err = cudaMalloc(&e->qbits, 2 * max_cols * words * 8);
     if (err == cudaSuccess) err = cudaMalloc(&e->progress, kScheduleScratchBytes);
     if (err == cudaSuccess) err = cudaMalloc(&staging, 2 * db_bits);
-    if (err == cudaSuccess) err = cudaMemcpyAsync(staging, db_code, db_bits, cudaMemcpyHostToDevice, ctx->stream);
+    if (err == cudaSuccess) err = copy_h2d(ctx, staging, db_code, db_bits, ctx->stream);
     if (err == cudaSuccess)
-        err = cudaMemcpyAsync(staging + db_bits / 8, db_mask, db_bits, cudaMemcpyHostToDevice, ctx->stream);
+        err = copy_h2d(ctx, staging + db_bits / 8, db_mask, db_bits, ctx->stream);
     int st = IRL_OK;
     if (err == cudaSuccess) st = build_planes(ctx, staging, staging + db_bits / 8, n_db, 1, d, e->planes, ctx->stream);
     if (err == cudaSuccess) err = cudaStreamSynchronize(ctx->stream);
