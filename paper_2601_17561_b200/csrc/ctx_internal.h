@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/irl_capi.h"
 #include "kernels_aux.cuh"
@@ -113,5 +114,23 @@ inline cudaStream_t pick_stream(irl_ctx* ctx, void* s) {
 cudaError_t copy_h2d(irl_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t s);
 cudaError_t copy_d2h(irl_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t s);
 void release_bounce(irl_ctx* ctx);
+
+// Shared by the modmat entry points (capi.cu) and the CCMM engine
+// (ccmm_engine.cu); defined in capi.cu.
+int validate_moduli(irl_ctx* ctx, const uint32_t* primes, const uint32_t* exps, size_t nmod);
+ModTable make_table(const uint32_t* primes, const uint32_t* exps, size_t nmod);
+PpmmLaunch make_launch(const ModTable& mt);
+// K chunk keeping the fused int32 accumulators exact for digit maxima (a0, a1, b0, b1)
+uint32_t safe_kchunk(int64_t a0, int64_t a1, int64_t b0, int64_t b1, uint32_t K);
+// one PPMM over digit planes, K-chunked (accumulate mode for chunks > 0)
+int run_ppmm(irl_ctx* ctx, PpmmLaunch L, uint32_t kchunk, cudaStream_t s);
+inline size_t round16(size_t x) { return (x + 15) / 16 * 16; }
+
+// host big integers for CRT constants (32-bit limbs, little-endian)
+using Limbs = std::vector<uint32_t>;
+Limbs basis_Q(const uint32_t* primes, const uint32_t* exps, size_t nmod);
+uint32_t divmod_small(Limbs& x, uint32_t m);  // x /= m, returns x mod m
+size_t byte_width(const Limbs& q);
+bool inv_mod(uint32_t a, uint32_t m, uint32_t* out);
 
 }  // namespace irl

@@ -94,7 +94,6 @@ __global__ void iris_file_planes_kernel(const uint8_t* __restrict__ code, const 
     *reinterpret_cast<uint4*>(planes + static_cast<size_t>(n) * ldk + o) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-size_t round16(size_t x) { return (x + 15) / 16 * 16; }
 
 // kModeInner GEMM of device planes x (DB, [2][n_db][ldk]) and y (queries,
 // [2][cols][ldk]) into inner / overlap [cols][n_db].
