@@ -42,8 +42,9 @@ typedef enum irl_status {
     IRL_ERR_OUT_OF_MEMORY = 9,
     IRL_ERR_UNSUPPORTED = 10,
     IRL_ERR_ZERO_OVERLAP = 11,              /* irislab::ZeroOverlap              errors.hpp:18 */
-    IRL_ERR_IO = 12                         /* irislab::Error("cannot open ..." / "truncated matrix file ...")
+    IRL_ERR_IO = 12,                        /* irislab::Error("cannot open ..." / "truncated matrix file ...")
                                                modmat.cpp:218, 235, 245 */
+    IRL_ERR_CONFIG = 13                     /* irislab::ConfigError              errors.hpp:13 */
 } irl_status;
 
 typedef struct irl_ctx irl_ctx;
@@ -269,6 +270,69 @@ int irl_iris_db_create_file(irl_ctx* ctx, const char* path, size_t max_cols, irl
 int irl_iris_db_destroy(irl_iris_db* e);
 int irl_iris_db_match(irl_iris_db* e, const uint64_t* q_code, const uint64_t* q_mask, size_t n_eyes, size_t rho,
                       double p_lo, double p_hi, uint8_t* match_bits, int32_t* eye_result, double* scores);
+
+/* ---- Alg. 2 fold stage at message level ----------------------
+ * run_alg2 (pipeline.cpp:538-633) after the CCMM: for eye e, DB block b
+ * (blocks = n_db / d) and rotation group g (groups = ceil(rho / fold_k);
+ * group g holds rotations r = g*fold_k .. min(rho, (g+1)*fold_k) - 1):
+ *
+ *   x_r[j]      = inner[c][b*d + j] * (1.0 / overlap[c][b*d + j]),  c = e*rho + r
+ *                 (normalize, pipeline.cpp:359-371: pmult by the inverse overlaps)
+ *   folded[i]   = sum over the group's r, in order, of f(x_r)[(i + r) mod d]
+ *                 (fold_group, pipeline.cpp:391-408: fold_poly, then rot by
+ *                 base_rot + s = r, emulator.cpp:232-245)
+ *   refolded[i] = sum over g of chain(folded_g)[i]   (pipeline.cpp:612-627;
+ *                 eval_chain_ct, pipeline.cpp:379-389: per stage add_const(-center)
+ *                 then the stage polynomial; the bootstrap in between,
+ *                 boot(bts_fold_pre), leaves the message unchanged)
+ *
+ * Every polynomial runs the reference's Paterson-Stockmeyer plan
+ * (poly.hpp:46-119, ring ops of CtRing pipeline.cpp:22-44) in IEEE double
+ * with the same operation order and no contraction, so the outputs equal the
+ * noise-free emulator's messages (Emulator(cfg, inject_noise = false)) bit
+ * for bit. Degrees (index of the last nonzero coefficient, poly.cpp:10-15) up
+ * to 31; up to 8 chain stages. The inner / overlap inputs are the CCMM
+ * product and the mask overlaps in the [c][n_db] layout of
+ * irl_iris_inner_overlap (prepare's overlaps[c*blocks + b][j], pipeline.cpp:140-151).
+ *
+ * assumption_ok = run_alg2's folding-assumption shadow check (pipeline.cpp:565-590):
+ * for every (e, b, i, g), at most one r in the group has overlap 0 or
+ * raw / overlap outside [negative_lo, negative_hi].
+ *
+ * Errors, in the reference's order: ConfigError from PipelineConfig::validate
+ * (pipeline.cpp:232-243: rho, batch >= 1; 1 <= fold_k <= rho; d a power of
+ * two >= 2; n_db a positive multiple of d), ConfigError("eval_chain_ct: empty
+ * chain") if refolded is requested with no stages, UNSUPPORTED for degree > 31
+ * or more than 8 stages, and ZeroOverlap if any overlap is 0 (normalize
+ * throws, pipeline.cpp:367; outputs are still written). */
+typedef struct irl_fold_params {
+    size_t batch, rho, n_db, d, fold_k;  /* PipelineConfig fields (pipeline.hpp:16-40) */
+    const double* fold_coeffs;           /* fold_poly.coeffs, ascending degree */
+    size_t fold_len;
+    size_t chain_stages;                 /* fold_chain.stages.size() */
+    const double* chain_centers;         /* [chain_stages] stage.center */
+    const size_t* chain_lens;            /* [chain_stages] stage.poly.coeffs.size() */
+    const double* chain_coeffs;          /* the stages' coefficients, concatenated */
+    double negative_lo, negative_hi;     /* cfg.model.negative */
+} irl_fold_params;
+
+/* Host buffers, blocking. inner / overlap: int32 [batch*rho][n_db].
+ * folded: [batch][blocks][groups][d], refolded: [batch][blocks][d] (each may
+ * be NULL); assumption_ok (may be NULL) gets 1 / 0. */
+int irl_fold_stage(irl_ctx* ctx, const irl_fold_params* p, const int32_t* inner, const int32_t* overlap,
+                   double* folded, double* refolded, int32_t* assumption_ok);
+/* Device buffers, stream-ordered (stream NULL = the context stream). flags:
+ * device uint32[2], OR-ed into: [0] folding assumption violated, [1] an
+ * overlap was 0 (the host call's ZeroOverlap). */
+int irl_fold_stage_device(irl_ctx* ctx, const irl_fold_params* p, const int32_t* inner, const int32_t* overlap,
+                          double* folded, double* refolded, uint32_t* flags, void* stream);
+/* The whole post-CCMM path of run_alg2 against a registered template
+ * database: prepare's products and overlaps of the query eyes
+ * (p->batch = n_eyes, the database's n_db and template length = p->n_db and
+ * p->d; ShapeMismatch otherwise, pipeline.cpp:100-118) as int8 GEMMs, then
+ * the fold stage on the device; only folded / refolded leave it. */
+int irl_iris_db_fold(irl_iris_db* e, const uint64_t* q_code, const uint64_t* q_mask, const irl_fold_params* p,
+                     double* folded, double* refolded, int32_t* assumption_ok);
 
 #ifdef __cplusplus
 }

@@ -6,7 +6,8 @@ iris_core.cpp) on the inputs of the reference's own known-answer tests and
 writes the results as small fixtures, so parity stays pinned on machines
 where /root/reference is absent (the GPU box). Test infrastructure only.
 
-    python oracle/gen_golden.py
+    python oracle/gen_golden.py              (everything)
+    python oracle/gen_golden.py --fold-only  (tests/golden/fold_stage.npz)
 """
 from __future__ import annotations
 
@@ -216,6 +217,7 @@ def main():
     prod = db.astype(np.int64) @ qry.astype(np.int64)
     np.savez_compressed(GOLDEN / "iris_kat.npz", db=db, qry=qry, prod=prod)
     gen_iris_scores()
+    gen_fold()
     print("wrote", sorted(p.name for p in GOLDEN.iterdir()))
 
 
@@ -260,9 +262,54 @@ def gen_iris_scores():
     assert st == 0
 
 
+FOLD_CASES = (
+    # tag, d, blocks, batch, rho, fold_k, mask density, negative interval, chain kind
+    ("dense", 64, 3, 2, 7, 3, 0.8, (-0.25, 0.25), "step"),
+    ("wide", 128, 2, 2, 8, 4, 0.8, (-0.15, 0.15), "wide"),
+    ("single", 32, 2, 3, 5, 5, 0.8, (-1.0, 1.0), "step"),
+    ("ragged", 64, 2, 1, 7, 4, 0.8, (-0.3, 0.3), "wide"),
+    ("zero", 64, 2, 2, 6, 3, 0.05, (-0.25, 0.25), "step"),
+)
+
+
+def gen_fold():
+    """Alg. 2 fold-stage vectors from the reference's own pipe::normalize,
+    pipe::fold_group and pipe::eval_chain_ct on a noise-free emulator
+    (pipeline.cpp:359-408), with the published folding polynomial
+    (data/fold_poly_appc.json), plus run_alg2's folding-assumption flag
+    (pipeline.cpp:565-590) from a full reference run_alg2 on the same
+    templates. Products and overlaps come from the oracle's
+    orc_iris_inner_overlap (pinned by iris_scores.npz)."""
+    out = {}
+    for k, (tag, d, blocks, batch, rho, fold_k, dens, neg, kind) in enumerate(FOLD_CASES):
+        n_db = d * blocks
+        dc, dm = ol.ref_synth_templates(n_db, d, dens, 31 + 2 * k)
+        qc, qm = ol.ref_synth_templates(batch, d, dens, 32 + 2 * k)
+        if tag == "dense":
+            dc[7], dm[7] = ol.ref_rotate(qc[0], qm[0], 2)  # a genuine match for eye 0
+        inner, ovl = ol.orc_inner_overlap(dc, dm, qc, qm, rho)
+        chain = ol.fold_chain_for_tests(kind)
+        st, folded, refold = ol.ref_fold(inner, ovl, batch, rho, d, fold_k, ol.FOLD_POLY_APPC, chain)
+        flag = -1 if st else ol.ref_alg2_flag(qc, qm, dc, dm, rho, fold_k, ol.FOLD_POLY_APPC, chain, neg)
+        out[f"{tag}_params"] = np.array([d, blocks, batch, rho, fold_k], np.int64)
+        out[f"{tag}_negative"] = np.array(neg)
+        out[f"{tag}_chain"] = np.array(kind)
+        out[f"{tag}_db_code"], out[f"{tag}_db_mask"] = dc, dm
+        out[f"{tag}_q_code"], out[f"{tag}_q_mask"] = qc, qm
+        out[f"{tag}_inner"], out[f"{tag}_overlap"] = inner, ovl
+        out[f"{tag}_status"] = np.array(st)
+        out[f"{tag}_folded"], out[f"{tag}_refolded"] = folded, refold
+        out[f"{tag}_assumption_ok"] = np.array(flag)
+        print(tag, "status", st, "assumption_ok", flag, "zero overlaps", int((ovl == 0).sum()))
+    out["fold_poly"] = ol.FOLD_POLY_APPC
+    np.savez_compressed(GOLDEN / "fold_stage.npz", **out)
+
+
 if __name__ == "__main__":
     import sys as _sys
     if "--iris-only" in _sys.argv:
         gen_iris_scores()
+    elif "--fold-only" in _sys.argv:
+        gen_fold()
     else:
         main()

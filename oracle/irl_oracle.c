@@ -515,3 +515,129 @@ void orc_iris_inner_overlap(const uint8_t* db_code, const uint8_t* db_mask, size
             }
         }
 }
+
+/* ---- Alg. 2 fold stage ------------------------------------------------------ */
+
+/* Polynomial::degree (poly.cpp:10-15): index of the last nonzero coefficient */
+static int orc_poly_degree(const double* c, size_t n) {
+    for (size_t i = n; i-- > 0;)
+        if (c[i] != 0.0) return (int)i;
+    return 0;
+}
+
+/* CtRing::axpb (pipeline.cpp:41-43): pmult_const(x, a), then add_const(b) */
+static double orc_axpb(double a, double x, double b) {
+    const double t = x * a;
+    return t + b;
+}
+
+/* detail::ps_eval_range (poly.hpp:62-86) */
+static double orc_ps_range(const double* c, size_t lo, size_t hi, const double* baby, const double* giant,
+                           size_t m) {
+    const size_t n = hi - lo;
+    if (n <= m) {
+        double acc = orc_axpb(0.0, baby[0], c[lo]);
+        for (size_t i = 1; i < n; ++i) acc = acc + orc_axpb(c[lo + i], baby[i - 1], 0.0);
+        return acc;
+    }
+    size_t split = m, g = 0;
+    while (split * 2 < n) {
+        split *= 2;
+        ++g;
+    }
+    const double low = orc_ps_range(c, lo, lo + split, baby, giant, m);
+    const double high = orc_ps_range(c, lo + split, hi, baby, giant, m);
+    return high * giant[g] + low;
+}
+
+/* ps_execute (poly.hpp:91-119) */
+double orc_ps_execute(const double* coeffs, size_t n, double x) {
+    const int d = orc_poly_degree(coeffs, n);
+    double c[64];
+    if (d >= 64) return NAN;
+    for (int i = 0; i <= d; ++i) c[i] = (size_t)i < n ? coeffs[i] : 0.0;
+    if (d == 0) return orc_axpb(0.0, x, c[0]);
+    int k = 0; /* ps_depth (poly.hpp:50-54) */
+    while ((1 << k) < d + 1) ++k;
+    const size_t m = (size_t)1 << ((k + 1) / 2); /* ps_baby_m */
+    double baby[64], giant[8];
+    baby[0] = x;
+    const size_t nb = m < (size_t)d ? m : (size_t)d;
+    for (size_t j = 2; j <= nb; ++j) baby[j - 1] = baby[(j + 1) / 2 - 1] * baby[j / 2 - 1];
+    size_t ng = 0;
+    if ((size_t)d + 1 > m) {
+        giant[ng++] = baby[m - 1];
+        size_t pw = m;
+        while (pw * 2 < (size_t)d + 1) {
+            giant[ng] = giant[ng - 1] * giant[ng - 1];
+            ++ng;
+            pw *= 2;
+        }
+    }
+    return orc_ps_range(c, 0, (size_t)d + 1, baby, giant, m);
+}
+
+int orc_fold_stage(size_t batch, size_t rho, size_t n_db, size_t d, size_t fold_k, const double* fold_c,
+                   size_t fold_len, size_t nstages, const double* centers, const size_t* lens,
+                   const double* chain_c, double neg_lo, double neg_hi, const int32_t* inner,
+                   const int32_t* overlap, double* folded, double* refolded, int32_t* assumption_ok) {
+    /* PipelineConfig::validate (pipeline.cpp:232-243) */
+    if (rho < 1 || batch < 1) return IRL_ERR_CONFIG;
+    if (fold_k < 1 || fold_k > rho) return IRL_ERR_CONFIG;
+    if (d < 2 || (d & (d - 1)) != 0) return IRL_ERR_CONFIG;
+    if (n_db < d || n_db % d != 0) return IRL_ERR_CONFIG;
+    if (refolded && nstages == 0) return IRL_ERR_CONFIG; /* eval_chain_ct: empty chain */
+    const size_t blocks = n_db / d, groups = (rho + fold_k - 1) / fold_k;
+    int ok = 1, empty = 0;
+    double* t = (double*)malloc(d * sizeof(double));
+    double* acc = (double*)malloc(d * sizeof(double));
+    double* refold = (double*)malloc(d * sizeof(double));
+    for (size_t e = 0; e < batch; ++e)
+        for (size_t b = 0; b < blocks; ++b) {
+            for (size_t g = 0; g < groups; ++g) {
+                const size_t r_end = (g + 1) * fold_k < rho ? (g + 1) * fold_k : rho;
+                /* folding-assumption shadow check (pipeline.cpp:565-590) */
+                for (size_t i = 0; i < d; ++i) {
+                    int non_d = 0;
+                    for (size_t r = g * fold_k; r < r_end; ++r) {
+                        const size_t j = (i + r) % d, off = (e * rho + r) * n_db + b * d + j;
+                        const double raw = (double)inner[off], ov = (double)overlap[off];
+                        if (ov == 0.0 || !(raw / ov >= neg_lo && raw / ov <= neg_hi)) ++non_d;
+                    }
+                    if (non_d > 1) ok = 0;
+                }
+                /* fold_group(normalize(scored[idx]) for the group's r) (pipeline.cpp:391-408) */
+                for (size_t r = g * fold_k; r < r_end; ++r) {
+                    const size_t row = (e * rho + r) * n_db + b * d;
+                    for (size_t j = 0; j < d; ++j) {
+                        const double ov = (double)overlap[row + j];
+                        if (ov == 0.0) empty = 1;
+                        const double inv = 1.0 / ov; /* normalize (pipeline.cpp:364-369) */
+                        t[j] = orc_ps_execute(fold_c, fold_len, (double)inner[row + j] * inv);
+                    }
+                    for (size_t i = 0; i < d; ++i) { /* rot by r (emulator.cpp:232-245), then add */
+                        const double v = t[(i + r) % d];
+                        acc[i] = r == g * fold_k ? v : acc[i] + v;
+                    }
+                }
+                if (folded) memcpy(folded + ((e * blocks + b) * groups + g) * d, acc, d * sizeof(double));
+                if (refolded) {
+                    for (size_t i = 0; i < d; ++i) {
+                        double cls = acc[i];
+                        size_t off = 0;
+                        for (size_t s = 0; s < nstages; ++s) { /* eval_chain_ct (pipeline.cpp:379-389) */
+                            cls = orc_ps_execute(chain_c + off, lens[s], cls + -centers[s]);
+                            off += lens[s];
+                        }
+                        refold[i] = g == 0 ? cls : refold[i] + cls;
+                    }
+                }
+            }
+            if (refolded) memcpy(refolded + (e * blocks + b) * d, refold, d * sizeof(double));
+        }
+    free(t);
+    free(acc);
+    free(refold);
+    if (assumption_ok) *assumption_ok = ok;
+    return empty ? IRL_ERR_ZERO_OVERLAP : IRL_OK;
+}

@@ -74,6 +74,18 @@ void orc_iris_inner_overlap(const uint8_t* db_code, const uint8_t* db_mask, size
                             const uint8_t* q_mask, size_t n_eyes, size_t rho, size_t d, int32_t* inner,
                             int32_t* overlap);
 
+/* ---- Alg. 2 fold stage, message level (pipeline.cpp:359-408, 538-633) ----
+ * Same contract as irl_fold_stage (include/irl_capi.h): normalize, the
+ * folding polynomial, the Rot alignment and group sums (folded, may be NULL),
+ * the fold chain and the refold over groups (refolded, may be NULL), the
+ * folding-assumption check. Polynomials follow ps_execute (poly.hpp:91-119)
+ * operation by operation in IEEE double (built with -ffp-contract=off). */
+double orc_ps_execute(const double* coeffs, size_t n, double x);
+int orc_fold_stage(size_t batch, size_t rho, size_t n_db, size_t d, size_t fold_k, const double* fold_c,
+                   size_t fold_len, size_t nstages, const double* centers, const size_t* lens,
+                   const double* chain_c, double neg_lo, double neg_hi, const int32_t* inner,
+                   const int32_t* overlap, double* folded, double* refolded, int32_t* assumption_ok);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,5 +1,6 @@
 // extern "C" wrappers around the UNMODIFIED reference hot path
-// (/root/reference/proj/src/modmat.cpp, iris_core.cpp), compiled together
+// (/root/reference/proj/src/modmat.cpp, iris_core.cpp, and for the Alg. 2
+// fold stage emulator.cpp, pipeline.cpp, poly.cpp), compiled together
 // into oracle/_ref/libirl_ref.so by oracle/Makefile. TEST INFRASTRUCTURE:
 // used by tests/ (parity pinning, golden-vector generation) and by bench.py's
 // CPU-baseline / --impl reference leg. Never linked by the product.
@@ -19,6 +20,7 @@
 #include "irislab/errors.hpp"
 #include "irislab/iris_core.hpp"
 #include "irislab/modmat.hpp"
+#include "irislab/pipeline.hpp"
 
 using namespace irislab;
 using modmat::BigMatrix;
@@ -46,6 +48,9 @@ int map_exception() {
     } catch (const ZeroOverlap& e) {
         g_err = e.what();
         return 11;
+    } catch (const ConfigError& e) {
+        g_err = e.what();
+        return 13;
     } catch (const Error& e) {
         g_err = e.what();
         return std::string(e.what()).find("coprime") != std::string::npos ? 4 : 6;
@@ -380,6 +385,141 @@ int ref_match_db_reference(const uint8_t* q_code, const uint8_t* q_mask, size_t 
         auto q = to_templates(q_code, q_mask, nq, d);
         auto db = to_templates(db_code, db_mask, n_db, d);
         *out = iris::match_db_reference(q, db, iris::Interval{n_lo, n_hi}, iris::Interval{p_lo, p_hi}) ? 1 : 0;
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// Alg. 2 fold stage through the reference's own pipe::normalize,
+// pipe::fold_group and pipe::eval_chain_ct on a noise-free emulator
+// (Emulator(default_emulator_config()), inject_noise = false), in run_alg2's
+// loop order (pipeline.cpp:594-627). The bootstrap between fold_group and the
+// chain (boot(bts_fold_pre)) only moves levels, so it is left out. inner /
+// overlap: int32 [batch*rho][n_db] (prepare's product and overlaps). The
+// score ciphertexts enter at the top level, as CI slots of ring degree d.
+int ref_fold_stage(size_t batch, size_t rho, size_t n_db, size_t d, size_t fold_k, const double* fold_c,
+                   size_t fold_len, size_t nstages, const double* centers, const size_t* lens,
+                   const double* chain_c, const int32_t* inner, const int32_t* overlap, double* folded,
+                   double* refolded) {
+    try {
+        pipe::PipelineConfig cfg;
+        cfg.rho = static_cast<int>(rho);
+        cfg.batch = static_cast<int>(batch);
+        cfg.n_db = static_cast<long>(n_db);
+        cfg.d = static_cast<long>(d);
+        cfg.fold_k = static_cast<int>(fold_k);
+        cfg.emu_cfg = pipe::default_emulator_config();
+        cfg.validate();
+        emu::Emulator em(cfg.emu_cfg);
+        const polydes::Polynomial fpoly(std::vector<double>(fold_c, fold_c + fold_len));
+        polydes::ClassifierChain chain;
+        size_t off = 0;
+        for (size_t s = 0; s < nstages; ++s) {
+            polydes::ClassifierChain::Stage st;
+            st.poly = polydes::Polynomial(std::vector<double>(chain_c + off, chain_c + off + lens[s]));
+            st.center = centers[s];
+            chain.stages.push_back(st);
+            off += lens[s];
+        }
+        int logn = 0;
+        while ((size_t{1} << logn) < d) ++logn;
+        const int top = cfg.emu_cfg.chain.top_level();
+        const size_t blocks = n_db / d, groups = (rho + fold_k - 1) / fold_k;
+        for (size_t e = 0; e < batch; ++e)
+            for (size_t b = 0; b < blocks; ++b) {
+                emu::EmulatedCiphertext refold;
+                for (size_t g = 0; g < groups; ++g) {
+                    std::vector<emu::EmulatedCiphertext> group;
+                    const size_t r_end = std::min(rho, (g + 1) * fold_k);
+                    for (size_t r = g * fold_k; r < r_end; ++r) {
+                        const size_t row = (e * rho + r) * n_db + b * d;
+                        std::vector<std::complex<double>> msg(d);
+                        std::vector<double> ov(d);
+                        for (size_t j = 0; j < d; ++j) {
+                            msg[j] = {static_cast<double>(inner[row + j]), 0.0};
+                            ov[j] = static_cast<double>(overlap[row + j]);
+                        }
+                        const auto ct = em.ecd(msg, emu::Encoding::Slot, true, logn, cfg.scale_bits, top);
+                        group.push_back(pipe::normalize(em, ct, ov, cfg.scale_bits));
+                    }
+                    const auto f = pipe::fold_group(em, group, fpoly, cfg.scale_bits, static_cast<long>(g * fold_k));
+                    if (folded)
+                        for (size_t i = 0; i < d; ++i) folded[((e * blocks + b) * groups + g) * d + i] = f.message[i].real();
+                    if (refolded) {
+                        auto cls = pipe::eval_chain_ct(em, chain, f, cfg.scale_bits);
+                        if (g == 0) {
+                            refold = std::move(cls);
+                        } else {
+                            const int lv = std::min(refold.level, cls.level);
+                            refold = em.add(em.mod_switch(refold, lv), em.mod_switch(cls, lv));
+                        }
+                    }
+                }
+                if (refolded)
+                    for (size_t i = 0; i < d; ++i) refolded[(e * blocks + b) * d + i] = refold.message[i].real();
+                em.clear_trace();
+            }
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// ps_execute on scalars through the emulator's ring (one slot), for the
+// polynomial unit checks.
+int ref_ps_execute(const double* coeffs, size_t n, double x, double* out) {
+    try {
+        emu::Emulator em(pipe::default_emulator_config());
+        const auto ct = em.ecd({{x, 0.0}, {0.0, 0.0}}, emu::Encoding::Slot, true, 1, 23.0, 24);
+        polydes::ClassifierChain chain;
+        polydes::ClassifierChain::Stage st;
+        st.poly = polydes::Polynomial(std::vector<double>(coeffs, coeffs + n));
+        chain.stages.push_back(st);
+        *out = pipe::eval_chain_ct(em, chain, ct, 23.0).message[0].real();
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// run_alg2's folding-assumption flag (pipeline.cpp:565-590) from the
+// reference's own run, on templates (prepare computes the products and
+// overlaps). The fold chain is the caller's; the post chain is a fixed
+// smooth step (the flag is computed before either is used).
+int ref_alg2_assumption(const uint8_t* q_code, const uint8_t* q_mask, size_t batch, const uint8_t* db_code,
+                        const uint8_t* db_mask, size_t n_db, size_t d, size_t rho, size_t fold_k,
+                        const double* fold_c, size_t fold_len, size_t nstages, const double* centers,
+                        const size_t* lens, const double* chain_c, double neg_lo, double neg_hi, int* ok) {
+    try {
+        pipe::PipelineConfig cfg;
+        cfg.rho = static_cast<int>(rho);
+        cfg.batch = static_cast<int>(batch);
+        cfg.n_db = static_cast<long>(n_db);
+        cfg.d = static_cast<long>(d);
+        cfg.fold_k = static_cast<int>(fold_k);
+        cfg.emu_cfg = pipe::default_emulator_config();
+        cfg.model.negative = {neg_lo, neg_hi};
+        cfg.model.positive = {0.4, 0.475};
+        cfg.fold_poly = polydes::Polynomial(std::vector<double>(fold_c, fold_c + fold_len));
+        size_t off = 0;
+        for (size_t s = 0; s < nstages; ++s) {
+            polydes::ClassifierChain::Stage st;
+            st.poly = polydes::Polynomial(std::vector<double>(chain_c + off, chain_c + off + lens[s]));
+            st.center = centers[s];
+            cfg.fold_chain.stages.push_back(st);
+            off += lens[s];
+        }
+        cfg.alg1_chain = cfg.fold_chain;
+        polydes::ClassifierChain::Stage step;  // (3y - y^3) / 2 around 1/2
+        step.poly = polydes::Polynomial(std::vector<double>{0.5, 0.75, 0.0, -0.5});
+        step.center = 0.5;
+        cfg.post_chain.stages = {step, step};
+        cfg.post_chain.eps_schedule = {1e-3};
+        auto q = to_templates(q_code, q_mask, batch, d);
+        auto db = to_templates(db_code, db_mask, n_db, d);
+        emu::Emulator em(cfg.emu_cfg);
+        *ok = pipe::run_alg2(em, cfg, q, db).folding_assumption_ok ? 1 : 0;
         return 0;
     } catch (...) {
         return map_exception();

@@ -33,6 +33,7 @@ IRL_ERR_OUT_OF_MEMORY = 9
 IRL_ERR_UNSUPPORTED = 10
 IRL_ERR_ZERO_OVERLAP = 11
 IRL_ERR_IO = 12
+IRL_ERR_CONFIG = 13
 
 # Every symbol include/irl_capi.h declares, with (restype, argtypes).
 SIGNATURES = {
@@ -84,7 +85,19 @@ SIGNATURES = {
     "irl_ccmm_set_mirror_ptrs": (C.c_int, [vp, sz, sz, C.POINTER(vp), sz]),
     "irl_iris_inner_overlap": (C.c_int, [vp, vp, vp, sz, vp, vp, sz, sz, sz, vp, vp]),
     "irl_iris_match": (C.c_int, [vp, vp, vp, sz, vp, vp, sz, sz, sz, C.c_double, C.c_double, vp, vp, vp]),
+    "irl_fold_stage": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
+    "irl_fold_stage_device": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),
+    "irl_iris_db_fold": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
 }
+
+
+class FoldParams(C.Structure):
+    """irl_fold_params (include/irl_capi.h)."""
+    _fields_ = [("batch", sz), ("rho", sz), ("n_db", sz), ("d", sz), ("fold_k", sz),
+                ("fold_coeffs", C.POINTER(C.c_double)), ("fold_len", sz),
+                ("chain_stages", sz), ("chain_centers", C.POINTER(C.c_double)),
+                ("chain_lens", C.POINTER(sz)), ("chain_coeffs", C.POINTER(C.c_double)),
+                ("negative_lo", C.c_double), ("negative_hi", C.c_double)]
 
 _lib = None
 

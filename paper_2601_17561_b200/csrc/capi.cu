@@ -291,6 +291,7 @@ const char* irl_status_string(int s) {
         case IRL_ERR_UNSUPPORTED: return "Unsupported";
         case IRL_ERR_ZERO_OVERLAP: return "ZeroOverlap";
         case IRL_ERR_IO: return "Error";
+        case IRL_ERR_CONFIG: return "ConfigError";
         default: return "unknown";
     }
 }

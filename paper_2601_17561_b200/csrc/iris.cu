@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "ctx_internal.h"
+#include "fold.cuh"
 
 using namespace irl;
 
@@ -248,6 +249,7 @@ struct irl_iris_db {
     uint64_t* qbits = nullptr;   // eyes' code + mask words
     uint32_t* progress = nullptr;
     irl::DevBuf match_ws;
+    irl::DevBuf fold_ws;  // inner / overlap [cols][n_db] + fold outputs of irl_iris_db_fold
 };
 
 extern "C" {
@@ -414,6 +416,7 @@ int irl_iris_db_destroy(irl_iris_db* e) {
     cudaFree(e->qbits);
     cudaFree(e->progress);
     e->match_ws.release();
+    e->fold_ws.release();
     delete e;
     return IRL_OK;
 }
@@ -438,6 +441,54 @@ int irl_iris_db_match(irl_iris_db* e, const uint64_t* q_code, const uint64_t* q_
     if (int st = build_planes(ctx, e->qbits, e->qbits + n_eyes * words, n_eyes, rho, e->d, e->qplanes, s)) return st;
     return match_fused(ctx, e->planes, e->qplanes, e->n_db, n_eyes, rho, e->d, e->ldk, p_lo, p_hi, match_bits,
                        eye_result, scores, e->match_ws, e->progress, s);
+}
+
+int irl_iris_db_fold(irl_iris_db* e, const uint64_t* q_code, const uint64_t* q_mask, const irl_fold_params* p,
+                     double* folded, double* refolded, int32_t* assumption_ok) {
+    if (!e || !p) return IRL_ERR_INVALID_ARGUMENT;
+    irl_ctx* ctx = e->ctx;
+    Guard g(ctx);
+    FoldArgs a;
+    if (int st = fold_prepare(ctx, p, refolded != nullptr, &a)) return st;  // run_alg2: cfg.validate() first
+    // prepare (pipeline.cpp:100-118)
+    if (p->n_db != e->n_db) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "pipeline: database size does not match config");
+    if (p->d != e->d)
+        return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "pipeline: database template dimension mismatch");
+    const size_t n_eyes = p->batch, rho = p->rho, cols = n_eyes * rho;
+    if (int st = check_args(ctx, q_code, q_mask, 0, q_code, q_mask, n_eyes, e->d)) return st;
+    if (cols > e->max_cols) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "iris db: query batch wider than max_cols");
+    cudaStream_t s = ctx->stream;
+    const size_t words = (e->d + 63) / 64, qb = n_eyes * words * 8;
+    const size_t in_bytes = cols * e->n_db * sizeof(int32_t);
+    const size_t fold_elems = size_t(a.batch) * a.blocks * a.groups * a.d;
+    const size_t refold_elems = size_t(a.batch) * a.blocks * a.d;
+    const size_t off_f = 2 * in_bytes, off_r = off_f + (folded ? fold_elems * 8 : 0);
+    const size_t off_flags = off_r + (refolded ? refold_elems * 8 : 0);
+    IRL_CK(ctx, e->fold_ws.ensure(off_flags + 16));
+    uint8_t* ws = e->fold_ws.as<uint8_t>();
+    auto* inner = reinterpret_cast<int32_t*>(ws);
+    auto* ovl = reinterpret_cast<int32_t*>(ws + in_bytes);
+    auto* dflags = reinterpret_cast<uint32_t*>(ws + off_flags);
+    IRL_CK(ctx, cudaMemcpyAsync(e->qbits, q_code, qb, cudaMemcpyHostToDevice, s));
+    IRL_CK(ctx, cudaMemcpyAsync(e->qbits + n_eyes * words, q_mask, qb, cudaMemcpyHostToDevice, s));
+    if (int st = build_planes(ctx, e->qbits, e->qbits + n_eyes * words, n_eyes, rho, e->d, e->qplanes, s)) return st;
+    if (int st = inner_overlap_gemm(ctx, e->planes, e->qplanes, e->n_db, cols, e->d, e->ldk, inner, ovl, e->progress, s))
+        return st;
+    IRL_CK(ctx, cudaMemsetAsync(dflags, 0, 8, s));
+    a.inner = inner;
+    a.overlap = ovl;
+    a.folded = folded ? reinterpret_cast<double*>(ws + off_f) : nullptr;
+    a.refolded = refolded ? reinterpret_cast<double*>(ws + off_r) : nullptr;
+    a.flags = dflags;
+    IRL_LAUNCH(ctx, launch_fold_stage(a, s));
+    if (folded) IRL_CK(ctx, copy_d2h(ctx, folded, a.folded, fold_elems * 8, s));
+    if (refolded) IRL_CK(ctx, copy_d2h(ctx, refolded, a.refolded, refold_elems * 8, s));
+    uint32_t hf[2] = {0, 0};
+    IRL_CK(ctx, cudaMemcpyAsync(hf, dflags, 8, cudaMemcpyDeviceToHost, s));
+    IRL_CK(ctx, cudaStreamSynchronize(s));
+    if (assumption_ok) *assumption_ok = hf[0] ? 0 : 1;
+    if (hf[1]) return set_err(ctx, IRL_ERR_ZERO_OVERLAP, "mask overlap is empty, score undefined");
+    return IRL_OK;
 }
 
 }  // extern "C"

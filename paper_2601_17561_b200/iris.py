@@ -194,6 +194,33 @@ class IrisDatabase:
             raise ShapeMismatch("template lengths differ")
         return self.match_packed(qc, qm, len(eyes), rho, p_int, want_scores)
 
+    def fold_packed(self, q_code, q_mask, n_eyes: int, cfg, want_folded: bool = True,
+                    want_refolded: Optional[bool] = None):
+        """run_alg2's post-CCMM stage against this database (irl_iris_db_fold):
+        products and overlaps of the query eyes' rotations as int8 GEMMs, then
+        the fold stage (fold.py) on the device. cfg: fold.FoldConfig with
+        cfg.d == the template length and n_db == len(db)."""
+        import ctypes as C
+
+        from .fold import FoldResult, _Params, shapes
+        if want_refolded is None:
+            want_refolded = bool(cfg.fold_chain)
+        p = _Params(cfg, n_eyes, self.n_db)
+        fshape, rshape = shapes(cfg, n_eyes, self.n_db)
+        folded = np.zeros(fshape) if want_folded and cfg.d > 0 else None
+        refolded = np.zeros(rshape) if want_refolded and cfg.d > 0 else None
+        ok = C.c_int32(-1)
+        self.ctx.check(capi.lib().irl_iris_db_fold(self.handle, _p(q_code), _p(q_mask), p.ref(),
+                                                   _p(folded), _p(refolded), C.byref(ok)))
+        return FoldResult(folded, refolded, bool(ok.value))
+
+    def fold(self, eyes: Sequence[IrisTemplate], cfg, want_folded: bool = True,
+             want_refolded: Optional[bool] = None):
+        qc, qm, d = _stack(eyes)
+        if eyes and d != self.d:
+            raise ShapeMismatch("pipeline: query template dimension mismatch")
+        return self.fold_packed(qc, qm, len(eyes), cfg, want_folded, want_refolded)
+
     def close(self):
         if getattr(self, "handle", None):
             capi.lib().irl_iris_db_destroy(self.handle)

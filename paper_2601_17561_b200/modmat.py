@@ -45,6 +45,10 @@ class ZeroOverlap(Error):
     """errors.hpp:18-20: mask overlap is empty, score undefined."""
 
 
+class ConfigError(Error):
+    """errors.hpp:13-16: invalid pipeline / chain configuration."""
+
+
 class DeviceError(Error):
     """CUDA / device failures (no reference counterpart)."""
 
@@ -57,6 +61,7 @@ _STATUS_EXC = {
     capi.IRL_ERR_MODULUS_BUDGET: ModulusBudget,
     capi.IRL_ERR_ZERO_OVERLAP: ZeroOverlap,
     capi.IRL_ERR_IO: Error,
+    capi.IRL_ERR_CONFIG: ConfigError,
 }
 
 

@@ -63,6 +63,11 @@ def oracle() -> C.CDLL:
         lib.orc_iris_inner_overlap.argtypes = [u8p, u8p, sz, u8p, u8p, sz, sz, sz, i32p, i32p]
         lib.orc_synth_block.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                         C.c_uint32, C.c_uint32, C.c_uint32, u16p]
+        f64p = C.POINTER(C.c_double)
+        lib.orc_ps_execute.restype = C.c_double
+        lib.orc_ps_execute.argtypes = [f64p, sz, C.c_double]
+        lib.orc_fold_stage.argtypes = [sz, sz, sz, sz, sz, f64p, sz, sz, f64p, C.POINTER(sz), f64p,
+                                       C.c_double, C.c_double, i32p, i32p, f64p, f64p, i32p]
         _oracle = lib
     return _oracle
 
@@ -104,6 +109,11 @@ def ref() -> C.CDLL:
         lib.ref_save_templates.argtypes = [C.c_char_p, u8p, u8p, sz, sz]
         lib.ref_match_db_reference.argtypes = [u8p, u8p, sz, u8p, u8p, sz, sz, C.c_double, C.c_double,
                                                C.c_double, C.c_double, C.POINTER(C.c_int)]
+        lib.ref_ps_execute.argtypes = [f64p, sz, C.c_double, f64p]
+        lib.ref_fold_stage.argtypes = [sz, sz, sz, sz, sz, f64p, sz, sz, f64p, C.POINTER(sz), f64p, i32p, i32p,
+                                       f64p, f64p]
+        lib.ref_alg2_assumption.argtypes = [u8p, u8p, sz, u8p, u8p, sz, sz, sz, sz, f64p, sz, sz, f64p,
+                                            C.POINTER(sz), f64p, C.c_double, C.c_double, C.POINTER(C.c_int)]
         _ref = lib
     return _ref
 
@@ -318,3 +328,110 @@ def rescale_oracle(res, moduli, drop, round_):
         for i, m in enumerate(moduli[:len(moduli) - drop]):
             out[i, e] = y % m
     return out
+
+
+# --------------------------------------------------------------------------
+# Alg. 2 fold stage (pipeline.cpp:359-408, 538-633)
+# --------------------------------------------------------------------------
+
+# data/fold_poly_appc.json: the published degree-7 folding polynomial
+FOLD_POLY_APPC = np.array([0.004105, -0.17351, -2.528271, 24.347349, 124.16155, -412.746212,
+                           376.961251, 106.553952])
+
+
+def _compose(p, q):
+    """Coefficients of p(q(y)) (ascending), numpy polynomial arithmetic."""
+    from numpy.polynomial import polynomial as P
+    out = np.array([0.0])
+    for c in p[::-1]:
+        out = P.polyadd(P.polymul(out, q), [c])
+    return out
+
+
+def fold_chain_for_tests(kind: str = "step"):
+    """A stand-in fold classifier chain (list of (center, coeffs)): smooth sign
+    approximants f3 = (3z - z^3)/2, f5 = (15z - 10z^3 + 3z^5)/8 and
+    f7 = (35z - 35z^3 + 21z^5 - 5z^7)/16, composed and scaled, ending in a
+    [0, 1] step. The reference designs its chains offline (compose_classifier,
+    poly_design.cpp); any coefficients exercise the same evaluation path.
+    "step": degrees 7, 21, 3; "wide": degrees 15, 31, 3."""
+    f3 = np.array([0.0, 1.5, 0.0, -0.5])
+    f5 = np.array([0.0, 15, 0, -10, 0, 3]) / 8.0
+    f7 = np.array([0.0, 35, 0, -35, 0, 21, 0, -5]) / 16.0
+    scale = lambda c, a: c * a ** np.arange(len(c))  # noqa: E731
+    step = np.array([0.5, 0.75, 0.0, -0.25])
+    if kind == "wide":
+        f27 = _compose(f3, _compose(f3, f3))
+        f31 = np.r_[f27, 0.0, 0.0, 0.0, 1e-9]
+        return [(0.365, scale(_compose(f3, f5), 1 / 1024)), (0.0, f31), (0.0, step)]
+    return [(0.365, scale(f7, 1 / 256)), (0.0, _compose(f7, f3)), (0.0, step)]
+
+
+def _chain_arrays(chain):
+    centers = np.array([c for c, _ in chain], np.float64)
+    lens = np.array([len(p) for _, p in chain], np.uintp)
+    coeffs = np.concatenate([np.asarray(p, np.float64) for _, p in chain]) if chain else np.zeros(1)
+    return centers, lens, np.ascontiguousarray(coeffs)
+
+
+def orc_fold(inner, overlap, batch, rho, d, fold_k, fold_c, chain, neg, want_folded=True, want_refold=True):
+    """Oracle restatement (oracle/irl_oracle.c orc_fold_stage); returns
+    (status, folded, refolded, assumption_ok)."""
+    f64p = C.POINTER(C.c_double)
+    n_db = inner.shape[1]
+    blocks, groups = n_db // d, -(-rho // fold_k)
+    folded = np.zeros(batch * blocks * groups * d) if want_folded else None
+    refold = np.zeros(batch * blocks * d) if want_refold else None
+    fc = np.ascontiguousarray(fold_c, np.float64)
+    centers, lens, cc = _chain_arrays(chain)
+    ok = C.c_int32(-1)
+    st = oracle().orc_fold_stage(batch, rho, n_db, d, fold_k, ptr(fc, f64p), len(fc), len(chain),
+                                 ptr(centers, f64p), lens.ctypes.data_as(C.POINTER(sz)), ptr(cc, f64p),
+                                 neg[0], neg[1], ptr(np.ascontiguousarray(inner, np.int32), i32p),
+                                 ptr(np.ascontiguousarray(overlap, np.int32), i32p),
+                                 ptr(folded, f64p) if folded is not None else None,
+                                 ptr(refold, f64p) if refold is not None else None, C.byref(ok))
+    return st, folded, refold, ok.value
+
+
+def ref_fold(inner, overlap, batch, rho, d, fold_k, fold_c, chain, want_refold=True):
+    """The reference's own pipe::normalize / fold_group / eval_chain_ct
+    (oracle/_ref); returns (status, folded, refolded)."""
+    f64p = C.POINTER(C.c_double)
+    n_db = inner.shape[1]
+    blocks, groups = n_db // d, -(-rho // fold_k)
+    folded = np.zeros(batch * blocks * groups * d)
+    refold = np.zeros(batch * blocks * d) if want_refold else None
+    fc = np.ascontiguousarray(fold_c, np.float64)
+    centers, lens, cc = _chain_arrays(chain)
+    st = ref().ref_fold_stage(batch, rho, n_db, d, fold_k, ptr(fc, f64p), len(fc), len(chain),
+                              ptr(centers, f64p), lens.ctypes.data_as(C.POINTER(sz)), ptr(cc, f64p),
+                              ptr(np.ascontiguousarray(inner, np.int32), i32p),
+                              ptr(np.ascontiguousarray(overlap, np.int32), i32p), ptr(folded, f64p),
+                              ptr(refold, f64p) if refold is not None else None)
+    return st, folded, refold
+
+
+def ref_alg2_flag(q_code, q_mask, db_code, db_mask, rho, fold_k, fold_c, chain, neg):
+    """run_alg2's folding_assumption_ok from the reference itself."""
+    f64p = C.POINTER(C.c_double)
+    fc = np.ascontiguousarray(fold_c, np.float64)
+    centers, lens, cc = _chain_arrays(chain)
+    ok = C.c_int(-1)
+    st = ref().ref_alg2_assumption(ptr(q_code, u8p), ptr(q_mask, u8p), q_code.shape[0], ptr(db_code, u8p),
+                                   ptr(db_mask, u8p), db_code.shape[0], db_code.shape[1], rho, fold_k,
+                                   ptr(fc, f64p), len(fc), len(chain), ptr(centers, f64p),
+                                   lens.ctypes.data_as(C.POINTER(sz)), ptr(cc, f64p), neg[0], neg[1],
+                                   C.byref(ok))
+    assert st == 0, ref().ref_last_error()
+    return ok.value
+
+
+def orc_inner_overlap(db_code, db_mask, q_code, q_mask, rho):
+    n_db, d = db_code.shape
+    eyes = q_code.shape[0]
+    inner = np.zeros((eyes * rho, n_db), np.int32)
+    ovl = np.zeros_like(inner)
+    oracle().orc_iris_inner_overlap(ptr(db_code, u8p), ptr(db_mask, u8p), n_db, ptr(q_code, u8p),
+                                    ptr(q_mask, u8p), eyes, rho, d, ptr(inner, i32p), ptr(ovl, i32p))
+    return inner, ovl
