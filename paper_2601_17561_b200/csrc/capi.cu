@@ -329,6 +329,7 @@ int irl_ctx_destroy(irl_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     for (auto& b : ctx->ws) b.release();
+    ctx->rcp.release();
     cudaFree(ctx->d_stats);
     cudaFreeHost(ctx->h_stats);
     cudaFree(ctx->d_absmax);

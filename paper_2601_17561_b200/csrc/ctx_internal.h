@@ -54,6 +54,8 @@ struct irl_ctx {
     uint64_t launches = 0;
     std::recursive_mutex mu;
     irl::DevBuf ws[8];
+    irl::DevBuf rcp;       // fold stage: rcp[k] = RN(1 / k) for k < rcp_n (fold.cu)
+    uint32_t rcp_n = 0;
     irl::SplitStats* d_stats = nullptr;
     irl::SplitStats* h_stats = nullptr;
     int32_t* d_absmax = nullptr;

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -69,26 +70,43 @@ __device__ __forceinline__ double ring_axpb(double a, double x, double b) {
     return __dadd_rn(__dmul_rn(x, a), b);
 }
 
+// Two evaluation modes with identical results:
+//  * exact (kFast = false): every ring operation of the reference, including
+//    the axpb(0, x, c) leaf starts and the "+ 0.0" of axpb(c, x, 0);
+//  * fast (kFast = true), valid when no coefficient is -0.0 (fold_prepare
+//    checks): a leaf's running sum never becomes -0 (it starts at
+//    RN(RN(x * 0) + c), which is -0 only for c = -0, and RN(a + b) is -0 only
+//    for a = b = -0), so RN(acc + RN(RN(b * c) + 0)) = RN(acc + RN(b * c)):
+//    the "+ 0.0" only turns a -0 product into +0, which no acc != -0 can see.
+//    That drops 6 of the 27 double operations of a degree-7 evaluation.
+
 // detail::ps_eval_range (poly.hpp:62-86): sum_{i in [LO, HI)} c[i] x^(i-LO)
-template <int LO, int HI, int M>
+template <bool kFast, int LO, int HI, int M>
 __device__ __forceinline__ double ps_range(const double* c, const double* baby, const double* giant) {
     constexpr int N = HI - LO;
     if constexpr (N <= M) {
-        double acc = ring_axpb(0.0, baby[0], c[LO]);
+        double acc;
+        if constexpr (kFast) {
+            acc = ring_axpb(0.0, baby[0], c[LO]);
 #pragma unroll
-        for (int i = 1; i < N; ++i) acc = __dadd_rn(acc, ring_axpb(c[LO + i], baby[i - 1], 0.0));
+            for (int i = 1; i < N; ++i) acc = __dadd_rn(acc, __dmul_rn(baby[i - 1], c[LO + i]));
+        } else {
+            acc = ring_axpb(0.0, baby[0], c[LO]);
+#pragma unroll
+            for (int i = 1; i < N; ++i) acc = __dadd_rn(acc, ring_axpb(c[LO + i], baby[i - 1], 0.0));
+        }
         return acc;
     } else {
         constexpr int S = ps_split(N, M);
         constexpr int G = ps_giant_index(N, M);
-        const double low = ps_range<LO, LO + S, M>(c, baby, giant);
-        const double high = ps_range<LO + S, HI, M>(c, baby, giant);
+        const double low = ps_range<kFast, LO, LO + S, M>(c, baby, giant);
+        const double high = ps_range<kFast, LO + S, HI, M>(c, baby, giant);
         return __dadd_rn(__dmul_rn(high, giant[G]), low);
     }
 }
 
 // ps_execute (poly.hpp:91-119) for a polynomial of degree D (c has D + 1 entries)
-template <int D>
+template <bool kFast, int D>
 __device__ __forceinline__ double ps_eval(const double* c, double x) {
     if constexpr (D == 0) {
         return ring_axpb(0.0, x, c[0]);
@@ -106,35 +124,63 @@ __device__ __forceinline__ double ps_eval(const double* c, double x) {
 #pragma unroll
             for (int g = 1; g < NG; ++g) giant[g] = __dmul_rn(giant[g - 1], giant[g - 1]);
         }
-        return ps_range<0, D + 1, M>(c, baby, giant);
+        return ps_range<kFast, 0, D + 1, M>(c, baby, giant);
     }
 }
 
-template <int D>
+template <bool kFast, int D>
 __device__ __forceinline__ double ps_dispatch_from(int deg, const double* c, double x) {
     if constexpr (D > kFoldMaxDegree) {
         return 0.0;  // unreachable: fold_prepare bounds the degree
     } else {
-        if (deg == D) return ps_eval<D>(c, x);
-        return ps_dispatch_from<D + 1>(deg, c, x);
+        if (deg == D) return ps_eval<kFast, D>(c, x);
+        return ps_dispatch_from<kFast, D + 1>(deg, c, x);
     }
 }
 
+template <bool kFast>
 __device__ __forceinline__ double ps_dispatch(int deg, const double* c, double x) {
     switch (deg) {  // the common degrees first (fold poly 7, classifier stages 15 / 31)
-        case 7: return ps_eval<7>(c, x);
-        case 15: return ps_eval<15>(c, x);
-        case 31: return ps_eval<31>(c, x);
-        default: return ps_dispatch_from<0>(deg, c, x);
+        case 7: return ps_eval<kFast, 7>(c, x);
+        case 15: return ps_eval<kFast, 15>(c, x);
+        case 31: return ps_eval<kFast, 31>(c, x);
+        default: return ps_dispatch_from<kFast, 0>(deg, c, x);
     }
 }
 
+// Folding polynomial of a compile-time degree (kFoldDeg >= 0: the reference's
+// degree-7 polynomial takes this path) or any degree <= 31 (kFoldDeg < 0).
+template <bool kFast, int kFoldDeg>
+__device__ __forceinline__ double fold_poly(const FoldArgs& a, const double* fc, double x) {
+    if constexpr (kFoldDeg >= 0) {
+        return ps_eval<kFast, kFoldDeg>(fc, x);  // coefficients held in registers
+    } else {
+        return ps_dispatch<kFast>(a.fold_deg, a.fold_c, x);
+    }
+}
+
+// !negative.contains(raw / ov) for ov != 0 (pipeline.cpp:580). x = raw *
+// RN(1 / ov) is within 2^-51 |q| of the IEEE quotient q, so outside the
+// bands [lo_out, lo_in] and [hi_in, hi_out] (2^-48 |bound| wide, fold_prepare)
+// x decides; inside a band the quotient is formed.
+__device__ __forceinline__ bool outside_negative(const FoldArgs& a, int32_t raw, int32_t ov, double x) {
+    if (x >= a.lo_in && x <= a.hi_in) return false;
+    if (x < a.lo_out || x > a.hi_out) return true;
+    const double q = __ddiv_rn(static_cast<double>(raw), static_cast<double>(ov));
+    return !(q >= a.neg_lo && q <= a.neg_hi);
+}
+
+template <bool kFast, int kFoldDeg>
 __global__ void __launch_bounds__(256) fold_stage_kernel(const FoldArgs a) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.d) return;
     const uint32_t b = blockIdx.y, e = blockIdx.z;
     const uint32_t dmask = a.d - 1;
-    const size_t base = static_cast<size_t>(b) * a.d;
+    const int32_t* inner = a.inner + static_cast<size_t>(e) * a.rho * a.n_db + static_cast<size_t>(b) * a.d;
+    const int32_t* overlap = a.overlap + static_cast<size_t>(e) * a.rho * a.n_db + static_cast<size_t>(b) * a.d;
+    double fc[kFoldDeg >= 0 ? kFoldDeg + 1 : 1];
+#pragma unroll
+    for (int k = 0; k < (kFoldDeg >= 0 ? kFoldDeg + 1 : 1); ++k) fc[k] = a.fold_c[k];
     double refold = 0.0;
     bool violated = false, empty = false;
     for (uint32_t g = 0; g < a.groups; ++g) {
@@ -142,22 +188,25 @@ __global__ void __launch_bounds__(256) fold_stage_kernel(const FoldArgs a) {
         const uint32_t r_end = min(a.rho, r0 + a.fold_k);
         double acc = 0.0;
         int non_d = 0;
-        for (uint32_t r = r0; r < r_end; ++r) {
-            const size_t c = static_cast<size_t>(e) * a.rho + r;
-            const size_t off = c * a.n_db + base + ((i + r) & dmask);
-            const double raw = static_cast<double>(__ldcs(a.inner + off));
-            const double ov = static_cast<double>(__ldcs(a.overlap + off));
+        const int32_t* in_row = inner + static_cast<size_t>(r0) * a.n_db;
+        const int32_t* ov_row = overlap + static_cast<size_t>(r0) * a.n_db;
+        uint32_t j = (i + r0) & dmask;
+        for (uint32_t r = r0; r < r_end; ++r, in_row += a.n_db, ov_row += a.n_db, j = (j + 1) & dmask) {
+            const int32_t raw = __ldcs(in_row + j);
+            const int32_t ov = __ldcs(ov_row + j);
+            // normalize: message * (1.0 / overlap) (pipeline.cpp:364-369);
+            // rcp[k] = RN(1 / k) for the overlaps a template can have
+            const double inv = static_cast<uint32_t>(ov) <= a.rcp_max ? __ldg(a.rcp + ov)
+                                                                      : __drcp_rn(static_cast<double>(ov));
+            const double x = __dmul_rn(static_cast<double>(raw), inv);
             // folding-assumption shadow check (pipeline.cpp:574-583)
-            if (ov == 0.0) {
+            if (ov == 0) {
                 empty = true;
                 ++non_d;
-            } else {
-                const double q = __ddiv_rn(raw, ov);
-                if (!(q >= a.neg_lo && q <= a.neg_hi)) ++non_d;
+            } else if (outside_negative(a, raw, ov, x)) {
+                ++non_d;
             }
-            // normalize: message * (1.0 / overlap) (pipeline.cpp:364-369)
-            const double x = __dmul_rn(raw, __ddiv_rn(1.0, ov));
-            const double t = ps_dispatch(a.fold_deg, a.fold_c, x);
+            const double t = fold_poly<kFast, kFoldDeg>(a, fc, x);
             acc = r == r0 ? t : __dadd_rn(acc, t);  // fold_group's running sum (pipeline.cpp:397-406)
         }
         if (non_d > 1) violated = true;
@@ -166,13 +215,35 @@ __global__ void __launch_bounds__(256) fold_stage_kernel(const FoldArgs a) {
         if (a.refolded) {
             double cls = acc;
             for (int s = 0; s < a.nstages; ++s)  // eval_chain_ct (pipeline.cpp:383-388)
-                cls = ps_dispatch(a.stage_deg[s], a.chain_c[s], __dadd_rn(cls, -a.center[s]));
+                cls = ps_dispatch<kFast>(a.stage_deg[s], a.chain_c[s], __dadd_rn(cls, -a.center[s]));
             refold = g == 0 ? cls : __dadd_rn(refold, cls);  // refold (pipeline.cpp:620-626)
         }
     }
     if (a.refolded) a.refolded[(static_cast<size_t>(e) * a.blocks + b) * a.d + i] = refold;
     if (violated) atomicOr(a.flags, 1u);
     if (empty) atomicOr(a.flags + 1, 1u);
+}
+
+__global__ void rcp_table_kernel(double* rcp, uint32_t n) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) rcp[k] = __drcp_rn(static_cast<double>(k));  // correctly rounded 1.0 / k
+}
+
+bool has_negative_zero(const double* c, size_t n) {
+    for (size_t i = 0; i < n; ++i)
+        if (c[i] == 0.0 && std::signbit(c[i])) return true;
+    return false;
+}
+
+// Band edges around an interval end v: |x - q| <= 2^-51 |q| near v.
+void band(double v, double* in_side, double* out_side, double dir) {
+    if (!std::isfinite(v)) {
+        *in_side = *out_side = v;
+        return;
+    }
+    const double w = std::fabs(v) * 0x1p-48 + 0x1p-1000;
+    *in_side = v + dir * w;
+    *out_side = v - dir * w;
 }
 
 int degree_of(const double* c, size_t n) {  // Polynomial::degree (poly.cpp:10-15)
@@ -223,6 +294,10 @@ int fold_prepare(irl_ctx* ctx, const irl_fold_params* p, bool want_refold, FoldA
     }
     a->neg_lo = p->negative_lo;
     a->neg_hi = p->negative_hi;
+    band(a->neg_lo, &a->lo_in, &a->lo_out, 1.0);
+    band(a->neg_hi, &a->hi_in, &a->hi_out, -1.0);
+    a->fast = !has_negative_zero(a->fold_c, kFoldMaxDegree + 1);
+    for (int s = 0; s < a->nstages; ++s) a->fast = a->fast && !has_negative_zero(a->chain_c[s], kFoldMaxDegree + 1);
     a->batch = static_cast<uint32_t>(p->batch);
     a->rho = static_cast<uint32_t>(p->rho);
     a->blocks = static_cast<uint32_t>(blocks);
@@ -233,10 +308,26 @@ int fold_prepare(irl_ctx* ctx, const irl_fold_params* p, bool want_refold, FoldA
     return IRL_OK;
 }
 
-cudaError_t launch_fold_stage(const FoldArgs& a, cudaStream_t s) {
+int launch_fold_stage(irl_ctx* ctx, FoldArgs& a, cudaStream_t s) {
+    const uint32_t need = a.d + 1;  // an overlap never exceeds the template length d
+    if (ctx->rcp_n < need) {
+        IRL_CK(ctx, ctx->rcp.ensure(size_t(need) * sizeof(double)));
+        rcp_table_kernel<<<(need + 255) / 256, 256, 0, s>>>(ctx->rcp.as<double>(), need);
+        IRL_LAUNCH(ctx, cudaGetLastError());
+        IRL_CK(ctx, cudaStreamSynchronize(s));  // later calls may read it from other streams
+        ctx->rcp_n = need;
+    }
+    a.rcp = ctx->rcp.as<double>();
+    a.rcp_max = ctx->rcp_n - 1;
     const dim3 grid((a.d + 255) / 256, a.blocks, a.batch);
-    fold_stage_kernel<<<grid, 256, 0, s>>>(a);
-    return cudaGetLastError();
+    if (a.fast && a.fold_deg == 7)
+        fold_stage_kernel<true, 7><<<grid, 256, 0, s>>>(a);
+    else if (a.fast)
+        fold_stage_kernel<true, -1><<<grid, 256, 0, s>>>(a);
+    else
+        fold_stage_kernel<false, -1><<<grid, 256, 0, s>>>(a);
+    IRL_LAUNCH(ctx, cudaGetLastError());
+    return IRL_OK;
 }
 
 }  // namespace irl
@@ -257,8 +348,7 @@ int irl_fold_stage_device(irl_ctx* ctx, const irl_fold_params* p, const int32_t*
     a.folded = folded;
     a.refolded = refolded;
     a.flags = flags;
-    IRL_LAUNCH(ctx, launch_fold_stage(a, pick_stream(ctx, stream)));
-    return IRL_OK;
+    return launch_fold_stage(ctx, a, pick_stream(ctx, stream));
 }
 
 int irl_fold_stage(irl_ctx* ctx, const irl_fold_params* p, const int32_t* inner, const int32_t* overlap,
@@ -287,7 +377,7 @@ int irl_fold_stage(irl_ctx* ctx, const irl_fold_params* p, const int32_t* inner,
     a.folded = folded ? reinterpret_cast<double*>(out + off_f) : nullptr;
     a.refolded = refolded ? reinterpret_cast<double*>(out + off_r) : nullptr;
     a.flags = dflags;
-    IRL_LAUNCH(ctx, launch_fold_stage(a, s));
+    if (int st = launch_fold_stage(ctx, a, s)) return st;
     if (folded) IRL_CK(ctx, copy_d2h(ctx, folded, a.folded, fold_elems * 8, s));
     if (refolded) IRL_CK(ctx, copy_d2h(ctx, refolded, a.refolded, refold_elems * 8, s));
     uint32_t hf[2] = {0, 0};

@@ -27,6 +27,10 @@ struct FoldArgs {
     int fold_deg = 0;
     int nstages = 0;
     double neg_lo = 0.0, neg_hi = 0.0;
+    double lo_in = 0.0, lo_out = 0.0, hi_in = 0.0, hi_out = 0.0;  // shadow-check bands (fold.cu)
+    bool fast = false;                 // no -0.0 coefficient: the reduced evaluation (fold.cu)
+    const double* rcp = nullptr;       // rcp[k] = RN(1 / k), k <= rcp_max
+    uint32_t rcp_max = 0;
     uint32_t batch = 0, rho = 0, blocks = 0, d = 0, fold_k = 0, groups = 0;
     unsigned long long n_db = 0;  // row length of inner / overlap
     const int32_t* inner = nullptr;    // [batch * rho][n_db]
@@ -41,6 +45,8 @@ struct FoldArgs {
 // the refolded output, which runs the chain (eval_chain_ct rejects an empty
 // one, pipeline.cpp:382).
 int fold_prepare(irl_ctx* ctx, const irl_fold_params* p, bool want_refold, FoldArgs* a);
-cudaError_t launch_fold_stage(const FoldArgs& a, cudaStream_t s);
+// Fills the context's reciprocal table up to a.d (once, synchronously) and
+// launches the fold kernel on s. Counts its launches in ctx.
+int launch_fold_stage(irl_ctx* ctx, FoldArgs& a, cudaStream_t s);
 
 }  // namespace irl

@@ -480,7 +480,7 @@ int irl_iris_db_fold(irl_iris_db* e, const uint64_t* q_code, const uint64_t* q_m
     a.folded = folded ? reinterpret_cast<double*>(ws + off_f) : nullptr;
     a.refolded = refolded ? reinterpret_cast<double*>(ws + off_r) : nullptr;
     a.flags = dflags;
-    IRL_LAUNCH(ctx, launch_fold_stage(a, s));
+    if (int st = launch_fold_stage(ctx, a, s)) return st;
     if (folded) IRL_CK(ctx, copy_d2h(ctx, folded, a.folded, fold_elems * 8, s));
     if (refolded) IRL_CK(ctx, copy_d2h(ctx, refolded, a.refolded, refold_elems * 8, s));
     uint32_t hf[2] = {0, 0};

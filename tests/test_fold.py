@@ -267,3 +267,68 @@ def test_gpu_fold_paper_scale_eyes_vs_oracle():
     assert st == 0
     assert np.array_equal(res.folded[:sub].ravel(), f_o)
     assert np.array_equal(res.refolded[:sub].ravel(), r_o)
+
+
+def _boundary_pairs():
+    """(raw, ov) pairs whose quotient RN(raw/ov) differs from raw * RN(1/ov):
+    one with the product below the quotient, one above."""
+    below = above = None
+    for ov in range(3, 200):
+        for raw in range(1, 400):
+            x, q = raw * (1.0 / ov), raw / ov
+            if x < q and below is None:
+                below = (raw, ov, q)
+            if x > q and above is None:
+                above = (raw, ov, q)
+        if below and above:
+            return below, above
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("side", ["lo", "hi"])
+def test_gpu_fold_shadow_check_uses_the_ieee_quotient(side):
+    """The folding-assumption check compares raw / ov (IEEE quotient,
+    pipeline.cpp:580) with the interval ends. Both rotations of every slot sit
+    exactly on an end, where raw * RN(1/ov) would land one ulp outside: the
+    reference counts them inside, so the assumption holds."""
+    from paper_2601_17561_b200.fold import FoldConfig, fold_stage
+    below, above = _boundary_pairs()
+    raw, ov, q = below if side == "lo" else above
+    neg = (q, q + 1.0) if side == "lo" else (q - 1.0, q)
+    d = 2
+    inner = np.full((2, d), raw, np.int32)
+    ovl = np.full((2, d), ov, np.int32)
+    cfg = FoldConfig(rho=2, fold_k=2, d=d, fold_chain=[], negative=neg)
+    res = fold_stage(inner, ovl, 1, cfg)
+    _, f_o, _, ok = ol.orc_fold(inner, ovl, 1, 2, d, 2, cfg.fold_poly, [], neg, want_refold=False)
+    assert ok == 1 and res.assumption_ok
+    assert np.array_equal(res.folded.ravel(), f_o)
+    # one ulp further in, the pair is outside for both
+    neg2 = (np.nextafter(q, np.inf), q + 1.0) if side == "lo" else (q - 1.0, np.nextafter(q, -np.inf))
+    res = fold_stage(inner, ovl, 1, FoldConfig(rho=2, fold_k=2, d=d, fold_chain=[], negative=neg2))
+    _, _, _, ok = ol.orc_fold(inner, ovl, 1, 2, d, 2, cfg.fold_poly, [], neg2, want_refold=False)
+    assert ok == 0 and not res.assumption_ok
+
+
+@pytest.mark.gpu
+def test_gpu_fold_negative_zero_coefficients_take_the_exact_path():
+    """A -0.0 coefficient (here the constant terms, where the reference's
+    axpb(0, x, c0) leaf start yields -0 for negative x) switches the kernel to
+    the operation-for-operation evaluation; still bit-exact with the oracle,
+    including the signs of zeros."""
+    from paper_2601_17561_b200.fold import FoldConfig, fold_stage
+    rng = np.random.default_rng(9)
+    d, blocks, batch, rho, fold_k = 128, 2, 2, 6, 3
+    ovl = rng.integers(1, 100, size=(batch * rho, d * blocks)).astype(np.int32)
+    inner = (rng.integers(-100, 101, size=ovl.shape) % (ovl + 1)).astype(np.int32)
+    inner *= np.where(rng.random(ovl.shape) < 0.5, -1, 1).astype(np.int32)
+    inner[:, ::7] = 0  # x = +-0 inputs
+    fold_c = np.array([-0.0, 0.0, -0.0, 0.5, 0.0, -0.0, 0.25, -1.0])
+    chain = [(0.0, np.array([-0.0, 1.0, -0.0, 0.0])), (0.0, np.array([-0.0, -0.0, 2.0]))]
+    cfg = FoldConfig(rho=rho, fold_k=fold_k, d=d, fold_poly=fold_c, fold_chain=chain, negative=(-0.5, 0.5))
+    res = fold_stage(inner, ovl, batch, cfg)
+    st, f_o, r_o, ok = ol.orc_fold(inner, ovl, batch, rho, d, fold_k, fold_c, chain, (-0.5, 0.5))
+    assert st == 0
+    assert np.array_equal(res.folded.ravel().view(np.uint64), f_o.view(np.uint64))
+    assert np.array_equal(res.refolded.ravel().view(np.uint64), r_o.view(np.uint64))
+    assert res.assumption_ok == bool(ok)
