@@ -171,7 +171,7 @@ __device__ __forceinline__ bool outside_negative(const FoldArgs& a, int32_t raw,
 }
 
 template <bool kFast, int kFoldDeg>
-__global__ void __launch_bounds__(256) fold_stage_kernel(const FoldArgs a) {
+__global__ void __launch_bounds__(256, 8) fold_stage_kernel(const FoldArgs a) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.d) return;
     const uint32_t b = blockIdx.y, e = blockIdx.z;
