@@ -20,6 +20,7 @@ void check(int st) {
     switch (st) {
         case IRL_ERR_SHAPE_MISMATCH: throw ShapeMismatch(m);
         case IRL_ERR_ZERO_OVERLAP: throw ZeroOverlap();
+        case IRL_ERR_CONFIG: throw ConfigError(m);
         case IRL_ERR_CUDA:
         case IRL_ERR_NO_DEVICE:
         case IRL_ERR_OUT_OF_MEMORY: throw DeviceError(m);
@@ -146,4 +147,104 @@ bool match_db_reference(const std::vector<IrisTemplate>& query, const std::vecto
 }
 
 }  // namespace iris
+namespace pipe {
+namespace {
+
+using iris::check;
+
+// irl_fold_params over cfg; the vectors it points into live in the holder.
+struct Params {
+    irl_fold_params p{};
+    std::vector<double> centers, coeffs;
+    std::vector<size_t> lens;
+    explicit Params(const FoldConfig& cfg) {
+        for (const ChainStage& st : cfg.fold_chain) {
+            centers.push_back(st.center);
+            lens.push_back(st.coeffs.size());
+            coeffs.insert(coeffs.end(), st.coeffs.begin(), st.coeffs.end());
+        }
+        p.batch = cfg.batch < 0 ? 0 : static_cast<size_t>(cfg.batch);
+        p.rho = cfg.rho < 0 ? 0 : static_cast<size_t>(cfg.rho);
+        p.n_db = cfg.n_db < 0 ? 0 : static_cast<size_t>(cfg.n_db);
+        p.d = cfg.d < 0 ? 0 : static_cast<size_t>(cfg.d);
+        p.fold_k = cfg.fold_k < 0 ? 0 : static_cast<size_t>(cfg.fold_k);
+        p.fold_coeffs = cfg.fold_poly.data();
+        p.fold_len = cfg.fold_poly.size();
+        p.chain_stages = cfg.fold_chain.size();
+        p.chain_centers = centers.data();
+        p.chain_lens = lens.data();
+        p.chain_coeffs = coeffs.data();
+        p.negative_lo = cfg.negative.lo;
+        p.negative_hi = cfg.negative.hi;
+    }
+};
+
+// PipelineConfig::validate (pipeline.cpp:232-243) for the fields the stage
+// reads, then eval_chain_ct's empty-chain check; the C ABI repeats them.
+void validate(const FoldConfig& cfg, bool want_refolded) {
+    if (cfg.rho < 1 || cfg.batch < 1) throw ConfigError("pipeline: rho and batch must be >= 1");
+    if (cfg.fold_k < 1 || cfg.fold_k > cfg.rho) throw ConfigError("pipeline: fold_k must satisfy 1 <= k <= rho");
+    if (cfg.d < 2 || (cfg.d & (cfg.d - 1)) != 0) throw ConfigError("pipeline: d must be a power of two");
+    if (cfg.n_db < cfg.d || cfg.n_db % cfg.d != 0)
+        throw ConfigError("pipeline: n_db must be a positive multiple of d");
+    if (want_refolded && cfg.fold_chain.empty()) throw ConfigError("eval_chain_ct: empty chain");
+}
+
+void size_outputs(const FoldConfig& cfg, bool want_refolded, FoldMessages* out) {
+    const bool valid = cfg.d > 0 && cfg.fold_k > 0 && cfg.batch > 0 && cfg.n_db >= cfg.d;
+    const size_t blocks = valid ? static_cast<size_t>(cfg.n_db / cfg.d) : 0;
+    const size_t groups = valid ? static_cast<size_t>((cfg.rho + cfg.fold_k - 1) / cfg.fold_k) : 0;
+    const size_t slots = valid ? static_cast<size_t>(cfg.batch) * blocks * static_cast<size_t>(cfg.d) : 0;
+    out->folded.assign(slots * groups, 0.0);
+    out->refolded.assign(want_refolded ? slots : 0, 0.0);
+}
+
+}  // namespace
+
+FoldMessages fold_stage(const FoldConfig& cfg, const std::vector<int32_t>& inner,
+                        const std::vector<int32_t>& overlap, bool want_refolded) {
+    Params prm(cfg);
+    validate(cfg, want_refolded);
+    const size_t need = prm.p.batch * prm.p.rho * prm.p.n_db;
+    if (inner.size() < need || overlap.size() < need)
+        throw ShapeMismatch("fold_stage: product / overlap smaller than batch * rho * n_db");
+    FoldMessages out;
+    size_outputs(cfg, want_refolded, &out);
+    int32_t ok = 1;
+    check(irl_fold_stage(b200::context(), &prm.p, inner.data(), overlap.data(), out.folded.data(),
+                         want_refolded ? out.refolded.data() : nullptr, &ok));
+    out.folding_assumption_ok = ok != 0;
+    return out;
+}
+
+FoldMessages fold_stage(const FoldConfig& cfg, const std::vector<iris::IrisTemplate>& queries,
+                        const std::vector<iris::IrisTemplate>& db, bool want_refolded) {
+    Params prm(cfg);
+    validate(cfg, want_refolded);  // run_alg2: cfg.validate() before prepare
+    // prepare (pipeline.cpp:100-118)
+    if (static_cast<long>(db.size()) != cfg.n_db) throw ShapeMismatch("pipeline: database size does not match config");
+    if (static_cast<int>(queries.size()) != cfg.batch) throw ShapeMismatch("pipeline: query count does not match batch");
+    for (const iris::IrisTemplate& t : db)
+        if (static_cast<long>(t.size()) != cfg.d) throw ShapeMismatch("pipeline: database template dimension mismatch");
+    for (const iris::IrisTemplate& q : queries)
+        if (static_cast<long>(q.size()) != cfg.d) throw ShapeMismatch("pipeline: query template dimension mismatch");
+    const size_t d = static_cast<size_t>(cfg.d);
+    std::vector<uint64_t> dc, dm, qc, qm;
+    iris::pack(db, d, &dc, &dm);
+    iris::pack(queries, d, &qc, &qm);
+    irl_iris_db* h = nullptr;
+    check(irl_iris_db_create(b200::context(), dc.data(), dm.data(), db.size(), d,
+                             queries.size() * static_cast<size_t>(cfg.rho), &h));
+    FoldMessages out;
+    size_outputs(cfg, want_refolded, &out);
+    int32_t ok = 1;
+    const int st = irl_iris_db_fold(h, qc.data(), qm.data(), &prm.p, out.folded.data(),
+                                    want_refolded ? out.refolded.data() : nullptr, &ok);
+    irl_iris_db_destroy(h);
+    check(st);
+    out.folding_assumption_ok = ok != 0;
+    return out;
+}
+
+}  // namespace pipe
 }  // namespace irislab

@@ -68,4 +68,49 @@ void inner_and_overlap(const std::vector<IrisTemplate>& db, const std::vector<Ir
                        std::size_t rho, std::vector<int32_t>* inner, std::vector<int32_t>* overlap);
 
 }  // namespace iris
+
+namespace pipe {
+
+/// ClassifierChain::Stage (poly_design.hpp:66-72): poly in y = x - center.
+struct ChainStage {
+    std::vector<double> coeffs;
+    double center = 0.0;
+};
+
+/// The PipelineConfig fields Alg. 2's fold stage reads (pipeline.hpp:16-45).
+struct FoldConfig {
+    int rho = 31;
+    int batch = 4;
+    long n_db = 4096;
+    long d = 1024;
+    int fold_k = 16;
+    std::vector<double> fold_poly;         // cfg.fold_poly.coeffs
+    std::vector<ChainStage> fold_chain;    // cfg.fold_chain.stages
+    iris::Interval negative{-0.25, 0.25};  // cfg.model.negative
+};
+
+/// Messages of run_alg2's post-CCMM stage (pipeline.cpp:594-627), equal bit
+/// for bit to the noise-free emulator's:
+///   folded[((e * blocks + b) * groups + g) * d + i]  = fold_group(normalize(...)) message
+///   refolded[(e * blocks + b) * d + i]              = sum over g of eval_chain_ct(folded_g)
+/// plus PipelineResult::folding_assumption_ok (pipeline.cpp:565-590).
+struct FoldMessages {
+    std::vector<double> folded;
+    std::vector<double> refolded;  // empty unless requested
+    bool folding_assumption_ok = true;
+};
+
+/// From the CCMM product and the overlaps, int32 [batch * rho][n_db] (the
+/// layout of iris::inner_and_overlap). Throws ConfigError
+/// (PipelineConfig::validate, "eval_chain_ct: empty chain") and ZeroOverlap
+/// (normalize) as the reference does.
+FoldMessages fold_stage(const FoldConfig& cfg, const std::vector<int32_t>& inner,
+                        const std::vector<int32_t>& overlap, bool want_refolded = true);
+
+/// From templates: prepare's products and overlaps as int8 GEMMs, then the
+/// fold stage, without leaving the device (irl_iris_db_fold).
+FoldMessages fold_stage(const FoldConfig& cfg, const std::vector<iris::IrisTemplate>& queries,
+                        const std::vector<iris::IrisTemplate>& db, bool want_refolded = true);
+
+}  // namespace pipe
 }  // namespace irislab
