@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--same-device", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--e2e-query", choices=["auto", "host"], default="auto",
                     help="N>1 e2e: auto shards the query H2D over ranks + all-gather when H2D-bound")
+    ap.add_argument("--moddown", type=int, default=0, metavar="DROP",
+                    help="f2 in the step: ModDown every local output to Q/Delta (drop the last DROP moduli) "
+                         "and exchange the rescaled a-part (NCCL broadcast of (24-DROP)/24 of the bytes)")
     ap.add_argument("--config", choices=["c2", "c3", "c4"], default="c4",
                     help="BASELINE.json config: c2 one DB slice as one PPMM (K = 2^14), c3 a-part + one "
                          "b-part, c4 the full 8-part DB (default; the headline metric)")
@@ -228,7 +231,12 @@ WORKLOADS = {
 
 def config_dict(args, nmod):
     N = args.eyes * args.rot
-    return {"workload": WORKLOADS[args.config],
+    extra = {}
+    if args.moddown:
+        extra = {"moddown_drop": args.moddown,
+                 "moddown": f"every local output rescaled to Q/Delta (last {args.moddown} moduli dropped) inside "
+                            "the step; the a-part exchange carries the rescaled result"}
+    return {"workload": WORKLOADS[args.config] + (" + ModDown" if args.moddown else ""), **extra,
             "parts": args.parts, "templates_per_part": args.rows, "K": args.k, "query_columns": N,
             "eyes": args.eyes, "rotations": args.rot, "moduli": nmod, "log2_Q": 360.8156,
             "digit_planes": 2 * nmod, "parallelism": f"db-slices over {args.gpus} GPU(s)",
@@ -285,8 +293,13 @@ def main():
     # mapping fails or the warm-up checksum disagrees.
     a_recv = None
     exchange, exch_note = "broadcast", None
+    md_drop = max(0, min(args.moddown, nmod - 1))
+    # --moddown: the step ends with the rescaled outputs [part][nmod - drop][N][M]
+    # (f2), and the a-part exchange carries the rescaled copy
+    out_md = (torch.empty((local_parts.count, nmod - md_drop, N, M), dtype=torch.int16, device="cuda")
+              if md_drop else None)
     if world > 1:
-        if args.exchange != "broadcast":
+        if args.exchange != "broadcast" and not md_drop:
             handle = None
             try:
                 if rank != 0:
@@ -308,7 +321,7 @@ def main():
             elif rank == 0:
                 eng.set_mirrors(0, N, [])
         if rank != 0 and a_recv is None:
-            a_recv = torch.empty((nmod, N, M), dtype=torch.int16, device="cuda")
+            a_recv = torch.empty((nmod - md_drop, N, M), dtype=torch.int16, device="cuda")
     # a dedicated stream: the engine runs on the stream it is handed, and the
     # CUDA events below are recorded on that same stream
     stream = torch.cuda.Stream()
@@ -326,9 +339,14 @@ def main():
         eng.run_device(None, N, None, part0=first_local, nparts=count, q_ready=True, stream=stream.cuda_stream)
         e1.record(stream)
         gemm_events.append((e0, e1, count))
+        if md_drop:
+            eng.rescale(N, out_md[first_local:first_local + count], md_drop, True, part0=first_local,
+                        nparts=count, stream=stream.cuda_stream)
 
     def a_out():
-        return out_dev[0] if rank == 0 else a_recv
+        if rank != 0:
+            return a_recv
+        return out_md[0] if md_drop else out_dev[0]
 
     step = ShardedStep(rank, world, run_parts, a_out, parts=args.parts, exchange=exchange)
 
@@ -473,6 +491,8 @@ def main():
                 eng.run_dq(None, N, o_np, stream=torch.cuda.current_stream().cuda_stream)
             else:
                 eng.run(q_np, o_np)  # H2D query, split, all local PPMMs, D2H outputs
+            if md_drop:  # the engine's device outputs of the run, rescaled for the exchange
+                eng.rescale(N, out_md, md_drop, True, stream=torch.cuda.current_stream().cuda_stream)
             if world > 1:
                 # the a-part result exchange stays on the device
                 if exchange == "mirror":  # the owner's epilogue already stored out_A into the peers
@@ -533,6 +553,11 @@ def main():
         dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
         dist_check = {"rows_per_rank": int(len(rows)), "moduli": nmod, "bit_exact_all_ranks": bool(ok_t.item()),
                       "oracle": "oracle/irl_oracle.c (pinned to the reference)"}
+        # every rank holds the same a-part result after the exchange
+        a_sum = torch.sum(a_out().to(torch.int64)).view(1)
+        sums = [torch.zeros_like(a_sum) for _ in range(world)]
+        dist.all_gather(sums, a_sum)
+        dist_check["a_part_identical_all_ranks"] = len({int(x.item()) for x in sums}) == 1
 
     # ---- CPU baseline (rank 0, N = 1) with a bit-exact check of its rows ----
     cpu = None
@@ -596,7 +621,8 @@ def main():
                 "split_roofline": split_roof, "moddown": moddown, "int8_library_ref": int8_ref,
                 "exchange": None if world == 1 else {
                     "kind": "fused P2P stores in the a-part PPMM epilogue (CUDA IPC, NVLink)" if exchange == "mirror"
-                    else "NCCL broadcast after the local GEMMs", "note": exch_note},
+                    else "NCCL broadcast after the local GEMMs", "note": exch_note,
+                    "bytes": int(a_out().numel() * 2)},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "dist_check": dist_check,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)

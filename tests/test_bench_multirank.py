@@ -41,3 +41,23 @@ def test_bench_multirank_same_device(world, exchange):
     assert d["value"] > 0 and d["e2e"]["value"] > 0
     assert d["e2e"]["outputs_equal_device_step"]
     assert d["dist_check"]["bit_exact_all_ranks"]  # sampled rows of every rank vs the CPU oracle
+
+
+@pytest.mark.gpu
+def test_bench_multirank_moddown_exchange():
+    """--moddown 3: every rank rescales its outputs to Q/Delta inside the step
+    and the a-part broadcast carries the 21-modulus result (f2: "shrinks the
+    broadcast"); all ranks end with the same a-part."""
+    world = 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", f"--master-port={_port()}", str(ROOT / "bench.py"), "--gpus", str(world),
+           "--steps", "2", "--warmup", "3", "--backend", "gloo", "--same-device", "--parts", "4",
+           "--rows", "2048", "--k", "4096", "--no-int8-ref", "--moddown", "3"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT,
+                       env={**os.environ, "OMP_NUM_THREADS": "1"})
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
+    assert d["config"]["moddown_drop"] == 3
+    assert d["exchange"]["kind"].startswith("NCCL") and d["exchange"]["bytes"] == 21 * 31 * 32 * 2048 * 2
+    assert d["dist_check"]["bit_exact_all_ranks"] and d["dist_check"]["a_part_identical_all_ranks"]
+    assert d["e2e"]["outputs_equal_device_step"]
