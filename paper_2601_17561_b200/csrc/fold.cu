@@ -279,7 +279,7 @@ int fold_prepare(irl_ctx* ctx, const irl_fold_params* p, bool want_refold, FoldA
     std::memset(a->stage_deg, 0, sizeof(a->stage_deg));
     a->fold_deg = degree_of(p->fold_coeffs, p->fold_len);
     if (a->fold_deg > kFoldMaxDegree) return set_err(ctx, IRL_ERR_UNSUPPORTED, "fold: polynomial degree above 31");
-    for (int k = 0; k <= a->fold_deg; ++k) a->fold_c[k] = p->fold_coeffs[k];
+    for (int k = 0; k <= a->fold_deg && static_cast<size_t>(k) < p->fold_len; ++k) a->fold_c[k] = p->fold_coeffs[k];
     size_t off = 0;
     a->nstages = static_cast<int>(p->chain_stages);
     for (size_t s = 0; s < p->chain_stages; ++s) {

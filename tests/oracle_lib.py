@@ -382,10 +382,10 @@ def orc_fold(inner, overlap, batch, rho, d, fold_k, fold_c, chain, neg, want_fol
     blocks, groups = n_db // d, -(-rho // fold_k)
     folded = np.zeros(batch * blocks * groups * d) if want_folded else None
     refold = np.zeros(batch * blocks * d) if want_refold else None
-    fc = np.ascontiguousarray(fold_c, np.float64)
+    fc = np.ascontiguousarray(fold_c, np.float64) if len(fold_c) else np.zeros(1)
     centers, lens, cc = _chain_arrays(chain)
     ok = C.c_int32(-1)
-    st = oracle().orc_fold_stage(batch, rho, n_db, d, fold_k, ptr(fc, f64p), len(fc), len(chain),
+    st = oracle().orc_fold_stage(batch, rho, n_db, d, fold_k, ptr(fc, f64p), len(fold_c), len(chain),
                                  ptr(centers, f64p), lens.ctypes.data_as(C.POINTER(sz)), ptr(cc, f64p),
                                  neg[0], neg[1], ptr(np.ascontiguousarray(inner, np.int32), i32p),
                                  ptr(np.ascontiguousarray(overlap, np.int32), i32p),

@@ -332,3 +332,20 @@ def test_gpu_fold_negative_zero_coefficients_take_the_exact_path():
     assert np.array_equal(res.folded.ravel().view(np.uint64), f_o.view(np.uint64))
     assert np.array_equal(res.refolded.ravel().view(np.uint64), r_o.view(np.uint64))
     assert res.assumption_ok == bool(ok)
+
+
+@pytest.mark.gpu
+def test_gpu_fold_empty_and_constant_polynomials():
+    """An empty coefficient vector is the zero polynomial (degree 0, poly.cpp:10-15);
+    a constant evaluates as axpb(0, x, c0) (poly.hpp:94)."""
+    from paper_2601_17561_b200.fold import FoldConfig, fold_stage
+    c = case("single")
+    for fold_c in ([], [0.75], [0.0, 0.0, 0.0]):
+        cfg = FoldConfig(rho=c["rho"], fold_k=c["fold_k"], d=c["d"], fold_poly=fold_c, fold_chain=c["chain"],
+                         negative=c["neg"])
+        res = fold_stage(c["inner"], c["overlap"], c["batch"], cfg)
+        st, f_o, r_o, ok = ol.orc_fold(c["inner"], c["overlap"], c["batch"], c["rho"], c["d"], c["fold_k"],
+                                       np.array(fold_c, np.float64), c["chain"], c["neg"])
+        assert st == 0
+        assert np.array_equal(res.folded.ravel().view(np.uint64), f_o.view(np.uint64))
+        assert np.array_equal(res.refolded.ravel(), r_o)
