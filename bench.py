@@ -24,6 +24,7 @@ import subprocess
 import sys
 import threading
 import time
+from types import SimpleNamespace
 from pathlib import Path
 
 import numpy as np
@@ -247,6 +248,213 @@ def config_dict(args, nmod):
 # B200 arm
 # ---------------------------------------------------------------------------
 
+def measure_split(R):
+    """The query split kernel alone (HBM-bound): 10 back-to-back launches."""
+    torch, eng, N, K, nmod, stream, hbm_peak = R.torch, R.eng, R.N, R.K, R.nmod, R.stream, R.hbm_peak
+    # ---- the query split (HBM-bound): 2 B read + 2 B written per (entry, modulus)
+    s0 = torch.cuda.Event(enable_timing=True)
+    s1 = torch.cuda.Event(enable_timing=True)
+    eng.run_device(None, N, None, part0=0, nparts=0, q_ready=False, stream=stream.cuda_stream)
+    s0.record(stream)
+    for _ in range(10):
+        eng.run_device(None, N, None, part0=0, nparts=0, q_ready=False, stream=stream.cuda_stream)
+    s1.record(stream)
+    torch.cuda.synchronize()
+    split_ms = s0.elapsed_time(s1) / 10
+    split_bytes = 4.0 * nmod * K * N
+    split_roof = {"bound": "hbm", "kernel": "split_cols_u16_vec_kernel", "launch_ms": split_ms,
+                  "achieved": split_bytes / (split_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                  "frac": split_bytes / (split_ms * 1e-3) / 1e9 / hbm_peak, "bytes_per_launch": split_bytes,
+                  "note": "10 back-to-back query splits, CUDA events; input and output (1.17 GB each) "
+                          "exceed L2"}
+    return split_roof
+
+
+def measure_moddown(R):
+    """f2 ModDown of all local outputs (HBM-bound), outside the step."""
+    torch, eng, N, M, nmod, stream, local_parts = R.torch, R.eng, R.N, R.M, R.nmod, R.stream, R.local_parts
+    hbm_peak = R.hbm_peak
+    # ---- ModDown of the step's outputs (f2; HBM-bound): drop the last 3 moduli
+    s0 = torch.cuda.Event(enable_timing=True)
+    s1 = torch.cuda.Event(enable_timing=True)
+    drop = 3
+    md_dst = torch.empty((1, nmod - drop, N, M), dtype=torch.int16, device="cuda")
+    for p_ in range(local_parts.count):
+        eng.rescale(N, md_dst, drop, True, part0=p_, nparts=1, stream=stream.cuda_stream)
+    s0.record(stream)
+    for p_ in range(local_parts.count):
+        eng.rescale(N, md_dst, drop, True, part0=p_, nparts=1, stream=stream.cuda_stream)
+    s1.record(stream)
+    torch.cuda.synchronize()
+    md_ms = s0.elapsed_time(s1)
+    md_bytes = 2.0 * (2 * nmod - drop) * N * M * local_parts.count
+    moddown = {"bound": "hbm", "kernel": "rescale_kernel", "drop_moduli": drop, "ms_per_step": md_ms,
+               "achieved": md_bytes / (md_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+               "frac": md_bytes / (md_ms * 1e-3) / 1e9 / hbm_peak, "bytes": md_bytes,
+               "note": "not part of the CCMM step: f2 rescale of all local outputs to Q/Delta, "
+                       "Delta = product of the last 3 moduli (~2^47)"}
+    del md_dst
+    return moddown
+
+
+def measure_e2e(R):
+    """The same step end to end through the public C ABI with host buffers."""
+    args, torch, dist, eng, N, M, K, nmod, world = R.args, R.torch, R.dist, R.eng, R.N, R.M, R.K, R.nmod, R.world
+    rank, local_parts, out_dev, q_dev, q_pinned = R.rank, R.local_parts, R.out_dev, R.q_dev, R.q_pinned
+    q_host, a_out, exchange, md_drop, out_md, total_ops = R.q_host, R.a_out, R.exchange, R.md_drop, R.out_md, R.total_ops
+    # ---- end to end through the public C ABI with host buffers -------------
+    e2e = None
+    if not args.no_e2e:
+        out_host = torch.empty((local_parts.count, nmod, N, M), dtype=torch.int16).pin_memory()
+        q_np = q_pinned.numpy().view(np.uint16)
+        o_np = out_host.numpy().view(np.uint16)
+        # H2D-bound layouts (few parts per GPU: GEMM time per modulus below its
+        # H2D time, the engine's own planner criterion) distribute the query
+        # over NVLink instead: each rank copies 1/N of the moduli from the host
+        # and all-gathers the rest, then runs split + GEMM + part-granular D2H
+        # (irl_ccmm_run_dq). Otherwise irl_ccmm_run pipelines the full H2D.
+        sharded = (world > 1 and local_parts.count * M < 20000 and nmod % world == 0
+                   and args.e2e_query != "host")
+        per = nmod // world if sharded else nmod
+        lo = rank * per if sharded else 0
+        q_bytes = q_dev.view(torch.uint8)  # [nmod][K][2N]: gloo and NCCL both carry uint8
+        q_slices = [q_bytes[r_ * per:(r_ + 1) * per] for r_ in range(world)] if sharded else None
+
+        def e2e_once():
+            if sharded:
+                q_dev[lo:lo + per].copy_(q_pinned.view(nmod, K, N)[lo:lo + per], non_blocking=True)
+                dist.all_gather(q_slices, q_bytes[lo:lo + per].clone() if args.backend == "gloo" else q_bytes[lo:lo + per])
+                eng.run_dq(None, N, o_np, stream=torch.cuda.current_stream().cuda_stream)
+            else:
+                eng.run(q_np, o_np)  # H2D query, split, all local PPMMs, D2H outputs
+            if md_drop:  # the engine's device outputs of the run, rescaled for the exchange
+                eng.rescale(N, out_md, md_drop, True, stream=torch.cuda.current_stream().cuda_stream)
+            if world > 1:
+                # the a-part result exchange stays on the device (PAPER.md:58)
+                if exchange == "mirror":  # the owner's epilogue already stored out_A into the peers
+                    w = dist.all_reduce(torch.zeros(1, dtype=torch.int32, device="cuda"), async_op=True)
+                else:
+                    w = dist.broadcast(a_out().view(torch.uint8), src=0, async_op=True)
+                w.wait()
+                torch.cuda.synchronize()
+
+        if world > 1:
+            dist.barrier()
+        for _ in range(max(1, args.warmup - 1)):
+            e2e_once()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_once()
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+        # the e2e outputs (host) must equal the device-resident step's (same
+        # query): a 64-row block of every part and modulus, on every rank
+        cols = min(M, 64)
+        same = bool((out_dev[:, :, :, :cols].cpu().numpy().view(np.uint16) == o_np[:, :, :, :cols]).all())
+        ok_t = torch.tensor([1 if same else 0], dtype=torch.int32, device="cuda")
+        if world > 1:
+            dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
+        e2e_exact = bool(ok_t.item())
+        tt = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+        e2e = {"value": total_ops / (e2e_ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(q_host.nbytes // world if sharded else q_host.nbytes),
+               "d2h_bytes_per_step": int(local_parts.count * nmod * N * M * 2),
+               "outputs_equal_device_step": e2e_exact,
+               "call": ("1/N of the query H2D per rank + NCCL all-gather, then irl_ccmm_run_dq "
+                        "(include/irl_capi.h) with pinned host outputs") if sharded else
+                       "irl_ccmm_run (include/irl_capi.h) with pinned host buffers"}
+    return e2e
+
+
+def measure_dist_check(R):
+    """N > 1: sampled rows of every rank against the CPU oracle; a-part consistency."""
+    args, torch, dist, M, K, nmod, world, local_parts = R.args, R.torch, R.dist, R.M, R.K, R.nmod, R.world, R.local_parts
+    out_dev, q_host, moduli, a_out = R.out_dev, R.q_host, R.moduli, R.a_out
+    # ---- N > 1: every rank checks sampled rows of its first local part against
+    # the CPU oracle (test infrastructure, oracle/irl_oracle.c), folded with MIN
+    dist_check = None
+    if world > 1 and not args.no_cpu_baseline:
+        sys.path.insert(0, str(ROOT / "tests"))
+        import oracle_lib as ol
+        part_g = local_parts.first
+        rows = np.array([0, M // 2, M - 1], np.uint32)
+        got_all = out_dev[0].cpu().numpy().view(np.uint16)  # [nmod][N][M] of the first local part
+        ok = True
+        for i, m_ in enumerate(moduli):
+            qt = np.ascontiguousarray(q_host[i].T)
+            for r_ in rows:  # only the sampled DB rows are generated
+                a_row = ol.synth_block(args.seed, part_g, i, int(r_), 1, 0, K, m_)
+                want = ol.ppmm_rows_direct(a_row, qt, np.zeros(1, np.uint32), m_)
+                ok &= bool((got_all[i][:, int(r_)] == want[0]).all())
+        ok_t = torch.tensor([1 if ok else 0], dtype=torch.int32, device="cuda")
+        dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
+        dist_check = {"rows_per_rank": int(len(rows)), "moduli": nmod, "bit_exact_all_ranks": bool(ok_t.item()),
+                      "oracle": "oracle/irl_oracle.c (pinned to the reference)"}
+        # every rank holds the same a-part result after the exchange
+        a_sum = torch.sum(a_out().to(torch.int64)).view(1)
+        sums = [torch.zeros_like(a_sum) for _ in range(world)]
+        dist.all_gather(sums, a_sum)
+        dist_check["a_part_identical_all_ranks"] = len({int(x.item()) for x in sums}) == 1
+    return dist_check
+
+
+def measure_cpu(R):
+    """The CPU baseline (rank 0, N = 1) with a bit-exact check of its rows."""
+    args, nmod, world, rank, out_dev, q_host = R.args, R.nmod, R.world, R.rank, R.out_dev, R.q_host
+    moduli, total_ops = R.moduli, R.total_ops
+    # ---- CPU baseline (rank 0, N = 1) with a bit-exact check of its rows ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = cpu_reference_sample(args, moduli, q_host=q_host)
+        gpu_rows = out_dev[:, :, :, : r["rows"]].cpu().numpy().view(np.uint16)
+        exact = True
+        j = 0
+        for part in r["parts"]:
+            for i in range(nmod):
+                exact &= bool((r["outputs"][j] == gpu_rows[part, i].T).all())
+                j += 1
+        cpu = {"value": r["tops"], "unit": UNIT, "cores": r["threads"], "kind": r["kind"],
+               "sample": r["sample"], "seconds": r["seconds"], "bit_exact_vs_gpu": exact,
+               "extrapolated_ccmm_latency_s": total_ops / (r["tops"] * 1e12)}
+    return cpu
+
+
+def measure_int8(R):
+    """Live library comparison: cuBLASLt int8 GEMM on this box."""
+    args, torch, rank = R.args, R.torch, R.rank
+    # ---- live library comparison: cuBLASLt int8 GEMM (torch._int_mm) on this box,
+    # same operand distribution, back to back for 3 s after the timed region
+    int8_ref = None
+    if rank == 0 and not args.no_int8_ref:
+        torch.cuda.set_stream(torch.cuda.default_stream())
+        A8 = torch.randint(-125, 126, (8192, 8192), dtype=torch.int8, device="cuda")
+        B8 = torch.randint(-125, 126, (8192, 8192), dtype=torch.int8, device="cuda").t()
+        for _ in range(3):
+            torch._int_mm(A8, B8)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        cnt, t0 = 0, time.time()
+        e0.record()
+        while time.time() - t0 < 3.0:
+            for _ in range(8):
+                torch._int_mm(A8, B8)
+            cnt += 8
+            torch.cuda.synchronize()
+        e1.record()
+        torch.cuda.synchronize()
+        int8_ref = {"library": "cuBLASLt int8 GEMM via torch._int_mm, 8192^3, operands uniform in [-125, 125]",
+                    "sustained_tops": 2.0 * 8192 ** 3 / (e0.elapsed_time(e1) / cnt) / 1e9,
+                    "note": "a plain int8 GEMM (1 product); the PPMM does 3 fused products + mod-p^2 epilogue"}
+        del A8, B8
+    return int8_ref
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -429,176 +637,18 @@ def main():
         tr = json.loads(tr_path.read_text())
         traffic = tr.get("bytes_per_part", 0) * statistics.mean(g_parts) or None
 
-    # ---- the query split (HBM-bound): 2 B read + 2 B written per (entry, modulus)
-    s0 = torch.cuda.Event(enable_timing=True)
-    s1 = torch.cuda.Event(enable_timing=True)
-    eng.run_device(None, N, None, part0=0, nparts=0, q_ready=False, stream=stream.cuda_stream)
-    s0.record(stream)
-    for _ in range(10):
-        eng.run_device(None, N, None, part0=0, nparts=0, q_ready=False, stream=stream.cuda_stream)
-    s1.record(stream)
-    torch.cuda.synchronize()
-    split_ms = s0.elapsed_time(s1) / 10
-    split_bytes = 4.0 * nmod * K * N
     hbm_peak = float(peaks.get("hbm_gbs", 6457.4))
-    split_roof = {"bound": "hbm", "kernel": "split_cols_u16_vec_kernel", "launch_ms": split_ms,
-                  "achieved": split_bytes / (split_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                  "frac": split_bytes / (split_ms * 1e-3) / 1e9 / hbm_peak, "bytes_per_launch": split_bytes,
-                  "note": "10 back-to-back query splits, CUDA events; input and output (1.17 GB each) "
-                          "exceed L2"}
-
-    # ---- ModDown of the step's outputs (f2; HBM-bound): drop the last 3 moduli
-    drop = 3
-    md_dst = torch.empty((1, nmod - drop, N, M), dtype=torch.int16, device="cuda")
-    for p_ in range(local_parts.count):
-        eng.rescale(N, md_dst, drop, True, part0=p_, nparts=1, stream=stream.cuda_stream)
-    s0.record(stream)
-    for p_ in range(local_parts.count):
-        eng.rescale(N, md_dst, drop, True, part0=p_, nparts=1, stream=stream.cuda_stream)
-    s1.record(stream)
-    torch.cuda.synchronize()
-    md_ms = s0.elapsed_time(s1)
-    md_bytes = 2.0 * (2 * nmod - drop) * N * M * local_parts.count
-    moddown = {"bound": "hbm", "kernel": "rescale_kernel", "drop_moduli": drop, "ms_per_step": md_ms,
-               "achieved": md_bytes / (md_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
-               "frac": md_bytes / (md_ms * 1e-3) / 1e9 / hbm_peak, "bytes": md_bytes,
-               "note": "not part of the CCMM step: f2 rescale of all local outputs to Q/Delta, "
-                       "Delta = product of the last 3 moduli (~2^47)"}
-    del md_dst
-
-    # ---- end to end through the public C ABI with host buffers -------------
-    e2e = None
-    if not args.no_e2e:
-        out_host = torch.empty((local_parts.count, nmod, N, M), dtype=torch.int16).pin_memory()
-        q_np = q_pinned.numpy().view(np.uint16)
-        o_np = out_host.numpy().view(np.uint16)
-        # H2D-bound layouts (few parts per GPU: GEMM time per modulus below its
-        # H2D time, the engine's own planner criterion) distribute the query
-        # over NVLink instead: each rank copies 1/N of the moduli from the host
-        # and all-gathers the rest, then runs split + GEMM + part-granular D2H
-        # (irl_ccmm_run_dq). Otherwise irl_ccmm_run pipelines the full H2D.
-        sharded = (world > 1 and local_parts.count * M < 20000 and nmod % world == 0
-                   and args.e2e_query != "host")
-        per = nmod // world if sharded else nmod
-        lo = rank * per if sharded else 0
-        q_bytes = q_dev.view(torch.uint8)  # [nmod][K][2N]: gloo and NCCL both carry uint8
-        q_slices = [q_bytes[r_ * per:(r_ + 1) * per] for r_ in range(world)] if sharded else None
-
-        def e2e_once():
-            if sharded:
-                q_dev[lo:lo + per].copy_(q_pinned.view(nmod, K, N)[lo:lo + per], non_blocking=True)
-                dist.all_gather(q_slices, q_bytes[lo:lo + per].clone() if args.backend == "gloo" else q_bytes[lo:lo + per])
-                eng.run_dq(None, N, o_np, stream=torch.cuda.current_stream().cuda_stream)
-            else:
-                eng.run(q_np, o_np)  # H2D query, split, all local PPMMs, D2H outputs
-            if md_drop:  # the engine's device outputs of the run, rescaled for the exchange
-                eng.rescale(N, out_md, md_drop, True, stream=torch.cuda.current_stream().cuda_stream)
-            if world > 1:
-                # the a-part result exchange stays on the device
-                if exchange == "mirror":  # the owner's epilogue already stored out_A into the peers
-                    w = dist.all_reduce(torch.zeros(1, dtype=torch.int32, device="cuda"), async_op=True)
-                else:
-                    w = dist.broadcast(a_out().view(torch.uint8), src=0, async_op=True)
-                w.wait()
-                torch.cuda.synchronize()
-
-        if world > 1:
-            dist.barrier()
-        for _ in range(max(1, args.warmup - 1)):
-            e2e_once()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            e2e_once()
-        e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
-        # the e2e outputs (host) must equal the device-resident step's (same
-        # query): a 64-row block of every part and modulus, on every rank
-        cols = min(M, 64)
-        same = bool((out_dev[:, :, :, :cols].cpu().numpy().view(np.uint16) == o_np[:, :, :, :cols]).all())
-        ok_t = torch.tensor([1 if same else 0], dtype=torch.int32, device="cuda")
-        if world > 1:
-            dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
-        e2e_exact = bool(ok_t.item())
-        tt = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
-        e2e = {"value": total_ops / (e2e_ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": int(q_host.nbytes // world if sharded else q_host.nbytes),
-               "d2h_bytes_per_step": int(local_parts.count * nmod * N * M * 2),
-               "outputs_equal_device_step": e2e_exact,
-               "call": ("1/N of the query H2D per rank + NCCL all-gather, then irl_ccmm_run_dq "
-                        "(include/irl_capi.h) with pinned host outputs") if sharded else
-                       "irl_ccmm_run (include/irl_capi.h) with pinned host buffers"}
-
-    # ---- N > 1: every rank checks sampled rows of its first local part against
-    # the CPU oracle (test infrastructure, oracle/irl_oracle.c), folded with MIN
-    dist_check = None
-    if world > 1 and not args.no_cpu_baseline:
-        sys.path.insert(0, str(ROOT / "tests"))
-        import oracle_lib as ol
-        part_g = local_parts.first
-        rows = np.array([0, M // 2, M - 1], np.uint32)
-        got_all = out_dev[0].cpu().numpy().view(np.uint16)  # [nmod][N][M] of the first local part
-        ok = True
-        for i, m_ in enumerate(moduli):
-            qt = np.ascontiguousarray(q_host[i].T)
-            for r_ in rows:  # only the sampled DB rows are generated
-                a_row = ol.synth_block(args.seed, part_g, i, int(r_), 1, 0, K, m_)
-                want = ol.ppmm_rows_direct(a_row, qt, np.zeros(1, np.uint32), m_)
-                ok &= bool((got_all[i][:, int(r_)] == want[0]).all())
-        ok_t = torch.tensor([1 if ok else 0], dtype=torch.int32, device="cuda")
-        dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
-        dist_check = {"rows_per_rank": int(len(rows)), "moduli": nmod, "bit_exact_all_ranks": bool(ok_t.item()),
-                      "oracle": "oracle/irl_oracle.c (pinned to the reference)"}
-        # every rank holds the same a-part result after the exchange
-        a_sum = torch.sum(a_out().to(torch.int64)).view(1)
-        sums = [torch.zeros_like(a_sum) for _ in range(world)]
-        dist.all_gather(sums, a_sum)
-        dist_check["a_part_identical_all_ranks"] = len({int(x.item()) for x in sums}) == 1
-
-    # ---- CPU baseline (rank 0, N = 1) with a bit-exact check of its rows ----
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r = cpu_reference_sample(args, moduli, q_host=q_host)
-        gpu_rows = out_dev[:, :, :, : r["rows"]].cpu().numpy().view(np.uint16)
-        exact = True
-        j = 0
-        for part in r["parts"]:
-            for i in range(nmod):
-                exact &= bool((r["outputs"][j] == gpu_rows[part, i].T).all())
-                j += 1
-        cpu = {"value": r["tops"], "unit": UNIT, "cores": r["threads"], "kind": r["kind"],
-               "sample": r["sample"], "seconds": r["seconds"], "bit_exact_vs_gpu": exact,
-               "extrapolated_ccmm_latency_s": total_ops / (r["tops"] * 1e12)}
-
-    # ---- live library comparison: cuBLASLt int8 GEMM (torch._int_mm) on this box,
-    # same operand distribution, back to back for 3 s after the timed region
-    int8_ref = None
-    if rank == 0 and not args.no_int8_ref:
-        torch.cuda.set_stream(torch.cuda.default_stream())
-        A8 = torch.randint(-125, 126, (8192, 8192), dtype=torch.int8, device="cuda")
-        B8 = torch.randint(-125, 126, (8192, 8192), dtype=torch.int8, device="cuda").t()
-        for _ in range(3):
-            torch._int_mm(A8, B8)
-        torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        cnt, t0 = 0, time.time()
-        e0.record()
-        while time.time() - t0 < 3.0:
-            for _ in range(8):
-                torch._int_mm(A8, B8)
-            cnt += 8
-            torch.cuda.synchronize()
-        e1.record()
-        torch.cuda.synchronize()
-        int8_ref = {"library": "cuBLASLt int8 GEMM via torch._int_mm, 8192^3, operands uniform in [-125, 125]",
-                    "sustained_tops": 2.0 * 8192 ** 3 / (e0.elapsed_time(e1) / cnt) / 1e9,
-                    "note": "a plain int8 GEMM (1 product); the PPMM does 3 fused products + mod-p^2 epilogue"}
-        del A8, B8
+    R = SimpleNamespace(
+        args=args, torch=torch, dist=dist, eng=eng, ctx=ctx, N=N, M=M, K=K, nmod=nmod, stream=stream,
+        world=world, rank=rank, local_parts=local_parts, out_dev=out_dev, q_dev=q_dev, q_pinned=q_pinned,
+        q_host=q_host, moduli=moduli, a_out=a_out, exchange=exchange, md_drop=md_drop, out_md=out_md,
+        total_ops=total_ops, peaks=peaks, hbm_peak=hbm_peak)
+    split_roof = measure_split(R)
+    moddown = measure_moddown(R)
+    e2e = measure_e2e(R)
+    dist_check = measure_dist_check(R)
+    cpu = measure_cpu(R)
+    int8_ref = measure_int8(R)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
