@@ -424,6 +424,64 @@ def measure_cpu(R):
     return cpu
 
 
+def stand_in_fold_chain():
+    """Three classifier stages of degrees 15, 31 and 3 (smooth sign approximants,
+    composed): the reference designs its chains offline (compose_classifier,
+    poly_design.cpp); the evaluation cost depends only on the degrees."""
+    from numpy.polynomial import polynomial as P
+
+    def compose(p, q):
+        out = np.array([0.0])
+        for c in p[::-1]:
+            out = P.polyadd(P.polymul(out, q), [c])
+        return out
+    f3 = np.array([0.0, 1.5, 0.0, -0.5])
+    f5 = np.array([0.0, 15, 0, -10, 0, 3]) / 8.0
+    f15 = compose(f3, f5) * (1 / 1024.0) ** np.arange(16)
+    f31 = np.r_[compose(f3, compose(f3, f3)), 0.0, 0.0, 0.0, 1e-9]
+    return [(0.365, f15), (0.0, f31), (0.0, np.array([0.5, 0.75, 0.0, -0.25]))]
+
+
+def measure_fold(R):
+    """The next stage after the CCMM (f4, csrc/fold.cu): Alg. 2's fold stage on
+    this step's geometry -- the query columns against the b-part templates
+    (blocks of d = 2^14), fold_k = 16 -- on device-resident products and
+    overlaps, 10 launches, CUDA events. 8 B read per (column, template) + 8 B
+    written per output slot; the inputs (0.9 GB at c4) exceed L2."""
+    args, torch, N, M, rank, hbm_peak = R.args, R.torch, R.N, R.M, R.rank, R.hbm_peak
+    if rank != 0 or args.rot < 1:
+        return None
+    from paper_2601_17561_b200.fold import FoldConfig, fold_stage_device
+    d = 1 << 14
+    n_db = max(1, (args.parts - 1) * M // d) * d  # the b-part templates, whole blocks
+    eyes, rho, fold_k = args.eyes, args.rot, min(16, args.rot)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    ovl = torch.randint(1, d, (N, n_db), dtype=torch.int32, device="cuda", generator=g)
+    inner = (torch.rand((N, n_db), device="cuda", generator=g) * (2 * ovl + 1)).to(torch.int32) - ovl
+    refolded = torch.empty(eyes * (n_db // d) * d, dtype=torch.float64, device="cuda")
+    flags = torch.zeros(2, dtype=torch.int32, device="cuda")
+    cfg = FoldConfig(rho=rho, fold_k=fold_k, d=d, fold_chain=stand_in_fold_chain(), negative=(-0.05, 0.05))
+    s = torch.cuda.current_stream()
+    for _ in range(3):
+        fold_stage_device(inner, ovl, eyes, cfg, None, refolded, flags, stream=s.cuda_stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(10):
+        fold_stage_device(inner, ovl, eyes, cfg, None, refolded, flags, stream=s.cuda_stream)
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 10
+    nbytes = 8.0 * N * n_db + 8.0 * refolded.numel()
+    del inner, ovl, refolded
+    return {"bound": "hbm", "kernel": "fold_stage_kernel", "launch_ms": ms,
+            "achieved": nbytes / (ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+            "frac": nbytes / (ms * 1e-3) / 1e9 / hbm_peak, "bytes_per_launch": nbytes,
+            "pairs": N * n_db,
+            "note": f"not part of the CCMM step: Alg. 2 fold stage (normalize, degree-7 fold polynomial with "
+                    f"Rot alignment, 3-stage fold chain, refold) on {N} columns x {n_db} templates, fold_k "
+                    f"{fold_k}; exact IEEE double, FP64/issue-bound (DESIGN.md 3)"}
+
+
 def measure_int8(R):
     """Live library comparison: cuBLASLt int8 GEMM on this box."""
     args, torch, rank = R.args, R.torch, R.rank
@@ -648,6 +706,7 @@ def main():
     e2e = measure_e2e(R)
     dist_check = measure_dist_check(R)
     cpu = measure_cpu(R)
+    fold = measure_fold(R)
     int8_ref = measure_int8(R)
 
     if rank == 0:
@@ -668,7 +727,7 @@ def main():
                                                        if "bf16_tflops" in peaks else None),
                              "frac_of_live_cublas_int8": (achieved / int8_ref["sustained_tops"]
                                                           if int8_ref else None)},
-                "split_roofline": split_roof, "moddown": moddown, "int8_library_ref": int8_ref,
+                "split_roofline": split_roof, "moddown": moddown, "fold_stage": fold, "int8_library_ref": int8_ref,
                 "exchange": None if world == 1 else {
                     "kind": "fused P2P stores in the a-part PPMM epilogue (CUDA IPC, NVLink)" if exchange == "mirror"
                     else "NCCL broadcast after the local GEMMs", "note": exch_note,

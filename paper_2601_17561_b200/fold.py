@@ -110,7 +110,9 @@ def fold_stage_device(inner, overlap, batch: int, cfg: FoldConfig, folded=None, 
     if flags is None:
         flags = torch.zeros(2, dtype=torch.int32, device=inner.device)
     if stream is None:
-        stream = torch.cuda.current_stream(inner.device).cuda_stream or 0x1
+        stream = torch.cuda.current_stream(inner.device).cuda_stream
+    if not stream:
+        stream = 0x1  # torch's default stream is the legacy stream (NULL would mean the context stream)
     ctx.check(capi.lib().irl_fold_stage_device(
         ctx.handle, p.ref(), capi.ptr(inner), capi.ptr(overlap), capi.ptr(folded) if folded is not None else None,
         capi.ptr(refolded) if refolded is not None else None, capi.ptr(flags), C.c_void_p(stream)))
