@@ -50,6 +50,7 @@ typedef enum irl_status {
 typedef struct irl_ctx irl_ctx;
 typedef struct irl_ccmm irl_ccmm;
 typedef struct irl_iris_db irl_iris_db;
+typedef struct irl_ccmm_group irl_ccmm_group;
 
 /* ---- context ------------------------------------------------------------ */
 int irl_abi_version(void);
@@ -230,6 +231,29 @@ int irl_ccmm_rescale(irl_ccmm* e, size_t n, size_t part0, size_t nparts, size_t 
                      void* stream);
 /* Bytes of HBM the engine holds (planes + workspace). */
 uint64_t irl_ccmm_device_bytes(const irl_ccmm* e);
+/* ---- single-process multi-GPU CCMM (SURVEY §8(b) irl_ccmm_full)
+ * One context and engine per entry of devices[] (an entry may repeat a device).
+ * The parts are dealt in contiguous blocks, rank r holding parts
+ * [first_r, first_r + count_r) with first_r = r*(parts/ndev) + min(r, parts%ndev),
+ * so the a-part (part 0) sits on rank 0. Register each rank's parts through its
+ * engine (irl_ccmm_group_engine; local part i is global part first_r + i).
+ * ShapeMismatch if ndev > parts. */
+int irl_ccmm_group_create(const int* devices, size_t ndev, size_t parts, size_t m, size_t k, size_t max_n,
+                          const uint32_t* primes, const uint32_t* exps, size_t nmod, irl_ccmm_group** out);
+int irl_ccmm_group_destroy(irl_ccmm_group* g);
+int irl_ccmm_group_engine(irl_ccmm_group* g, size_t rank, irl_ccmm** e, size_t* first_part, size_t* nparts);
+/* Context of a rank (irl_last_error of group calls is on rank 0's). */
+irl_ctx* irl_ccmm_group_ctx(irl_ccmm_group* g, size_t rank);
+/* The full CCMM across the devices with HOST buffers: q_res [nmod][K][n] ->
+ * out [parts][nmod][n][M] (every part, in global order); each rank runs its
+ * parts end to end (irl_ccmm_run) concurrently with the others. The a-part
+ * result also lands on every rank: rank 0's PPMM epilogue stores it into the
+ * other ranks' receive buffers over peer memory while it computes (*fused = 1),
+ * or, without peer access, a cudaMemcpyPeer follows the runs (*fused = 0).
+ * a_out (nullable, ndev entries) receives each rank's device pointer to its
+ * copy [nmod][n][M]. n <= max_n. Blocks. */
+int irl_ccmm_full(irl_ccmm_group* g, const uint16_t* q_res_host, size_t n, uint16_t* out_host, void** a_out,
+                  int* fused);
 
 /* ---- plaintext iris scoring stage ---------------------------
  * Templates are packed bit planes in pack_bits order (pipeline.cpp:70-76):

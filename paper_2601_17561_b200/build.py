@@ -22,7 +22,7 @@ HOST = PKG / "host"
 OUT = PKG / "libirl_b200.so"
 BUILD = ROOT / "build"
 
-CUDA_SOURCES = ["ppmm_gemm.cu", "kernels_aux.cu", "capi.cu", "ccmm_engine.cu", "iris.cu", "fold.cu"]
+CUDA_SOURCES = ["ppmm_gemm.cu", "kernels_aux.cu", "capi.cu", "ccmm_engine.cu", "ccmm_group.cu", "iris.cu", "fold.cu"]
 HOST_SOURCES = ["modmat_b200.cpp", "iris_b200.cpp", "ccmm_b200.cpp"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

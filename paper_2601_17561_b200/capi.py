@@ -88,6 +88,11 @@ SIGNATURES = {
     "irl_fold_stage": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
     "irl_fold_stage_device": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),
     "irl_iris_db_fold": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
+    "irl_ccmm_group_create": (C.c_int, [vp, sz, sz, sz, sz, sz, vp, vp, sz, C.POINTER(vp)]),
+    "irl_ccmm_group_destroy": (C.c_int, [vp]),
+    "irl_ccmm_group_engine": (C.c_int, [vp, sz, C.POINTER(vp), C.POINTER(sz), C.POINTER(sz)]),
+    "irl_ccmm_group_ctx": (vp, [vp, sz]),
+    "irl_ccmm_full": (C.c_int, [vp, vp, sz, vp, C.POINTER(vp), C.POINTER(C.c_int)]),
 }
 
 

@@ -136,9 +136,86 @@ class CcmmEngine:
         arr = (C.c_void_p * max(1, len(tensors)))(*[t.data_ptr() for t in tensors])
         self.ctx.check(capi.lib().irl_ccmm_set_mirror_ptrs(self.handle, part, n, arr, len(tensors)))
 
+    @classmethod
+    def borrowed(cls, handle, ctx: Context, parts: int, m: int, k: int, max_n: int, basis: RnsBasis):
+        """A view of an engine owned elsewhere (a rank of CcmmGroup)."""
+        self = cls.__new__(cls)
+        self.ctx, self.basis, self.handle, self._borrowed = ctx, basis, handle, True
+        self.parts, self.M, self.K, self.max_n = parts, m, k, max_n
+        self.primes, self.exps = basis.arrays()
+        self.nmod = len(self.primes)
+        return self
+
+    def close(self):
+        if getattr(self, "handle", None) and not getattr(self, "_borrowed", False):
+            capi.lib().irl_ccmm_destroy(self.handle)
+        self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class CcmmGroup:
+    """The CCMM across several devices in one process (irl_ccmm_group_*,
+    irl_ccmm_full): one engine per entry of `devices`, parts dealt as
+    dist.part_range (the a-part on rank 0), the a-part result stored into every
+    other rank by rank 0's PPMM epilogue over peer memory."""
+
+    def __init__(self, devices, parts: int, m: int, k: int, max_n: int, basis: Optional[RnsBasis] = None):
+        self.basis = basis or build_paper_basis()
+        self.primes, self.exps = self.basis.arrays()
+        self.nmod = len(self.primes)
+        self.devices = list(devices)
+        self.parts, self.M, self.K, self.max_n = parts, m, k, max_n
+        devs = (C.c_int * len(self.devices))(*self.devices)
+        h = C.c_void_p()
+        st = capi.lib().irl_ccmm_group_create(devs, len(self.devices), parts, m, k, max_n,
+                                              capi.ptr(self.primes, capi.u32p), capi.ptr(self.exps, capi.u32p),
+                                              self.nmod, C.byref(h))
+        if st != capi.IRL_OK:
+            from .modmat import _STATUS_EXC, DeviceError
+            raise _STATUS_EXC.get(st, DeviceError)(f"irl_ccmm_group_create: {capi.lib().irl_status_string(st).decode()}")
+        self.handle = h
+        self.ctx = Context.borrowed(capi.lib().irl_ccmm_group_ctx(h, 0), self.devices[0])
+
+    def engine(self, rank: int):
+        """(engine view, first global part, part count) of a rank."""
+        e, first, count = C.c_void_p(), C.c_size_t(), C.c_size_t()
+        self.ctx.check(capi.lib().irl_ccmm_group_engine(self.handle, rank, C.byref(e), C.byref(first),
+                                                        C.byref(count)))
+        ctx = Context.borrowed(capi.lib().irl_ccmm_group_ctx(self.handle, rank), self.devices[rank])
+        eng = CcmmEngine.borrowed(e, ctx, count.value, self.M, self.K, self.max_n, self.basis)
+        return eng, first.value, count.value
+
+    def synth_db(self, seed: int):
+        for r in range(len(self.devices)):
+            eng, first, _ = self.engine(r)
+            eng.synth_db(seed, first_part=first)
+
+    def run(self, q_res: np.ndarray, out: Optional[np.ndarray] = None):
+        """q_res [nmod][K][n] -> (out [parts][nmod][n][M], per-rank device
+        pointers of the a-part result, fused exchange used)."""
+        assert q_res.dtype == np.uint16 and q_res.flags.c_contiguous
+        n = q_res.shape[2]
+        if out is None:
+            out = np.empty((self.parts, self.nmod, n, self.M), np.uint16)
+        ptrs = (C.c_void_p * len(self.devices))()
+        fused = C.c_int(0)
+        self.ctx.check(capi.lib().irl_ccmm_full(self.handle, capi.ptr(q_res), n, capi.ptr(out), ptrs,
+                                                C.byref(fused)))
+        return out, [p for p in ptrs], bool(fused.value)
+
+    def a_part(self, rank: int, ptr: int, n: int):
+        """torch view (int16 bit patterns) of a rank's copy of the a-part result."""
+        import torch
+        return torch.as_tensor(_CudaArray(ptr, (self.nmod, n, self.M), "<i2"), device=f"cuda:{self.devices[rank]}")
+
     def close(self):
         if getattr(self, "handle", None):
-            capi.lib().irl_ccmm_destroy(self.handle)
+            capi.lib().irl_ccmm_group_destroy(self.handle)
             self.handle = None
 
     def __del__(self):

@@ -92,10 +92,17 @@ class Context:
     def launches(self) -> int:
         return int(capi.lib().irl_kernel_launches(self.handle))
 
+    @classmethod
+    def borrowed(cls, handle, device: int) -> "Context":
+        """A view of a context owned elsewhere (e.g. a rank of an irl_ccmm_group)."""
+        self = cls.__new__(cls)
+        self.handle, self.device, self._borrowed = handle, device, True
+        return self
+
     def close(self):
-        if self.handle:
+        if self.handle and not getattr(self, "_borrowed", False):
             capi.lib().irl_ctx_destroy(self.handle)
-            self.handle = None
+        self.handle = None
 
     def __del__(self):
         try:

@@ -579,3 +579,46 @@ def test_ccmm_load_part_file_streams_reference_format(tmp_path):
         eng.load_part_file(0, wrong)
     with pytest.raises(Error, match="cannot open"):
         eng.load_part_file(0, tmp_path / "missing.bin")
+
+
+@pytest.mark.parametrize("devices,parts", [([0, 0], 3), ([0, 0, 0], 3), ([0, 0, 0, 0], 8)])
+def test_ccmm_group_full_equals_one_engine_and_exchanges_the_a_part(devices, parts):
+    """irl_ccmm_full (single-process multi-GPU; here every rank on device 0):
+    the parts dealt as dist.part_range, every rank's outputs in global order,
+    equal to one engine holding all parts; every rank ends with the a-part
+    result, stored into it by rank 0's PPMM epilogue (fused exchange)."""
+    import torch
+
+    from paper_2601_17561_b200.ccmm import CcmmEngine, CcmmGroup, synth_query
+    from paper_2601_17561_b200.dist import part_range
+    m, k, n = 384, 1024, 96
+    g = CcmmGroup(devices, parts=parts, m=m, k=k, max_n=n)
+    try:
+        for r in range(len(devices)):
+            _, first, count = g.engine(r)
+            pr = part_range(r, len(devices), parts)
+            assert (first, count) == (pr.first, pr.count)
+        g.synth_db(seed=1)
+        eng = CcmmEngine(parts=parts, m=m, k=k, max_n=n)
+        eng.synth_db(seed=1)
+        q = synth_query(2, k, n, eng.moduli)
+        want = eng.run(q)
+        eng.close()
+        out, ptrs, fused = g.run(q)
+        assert fused
+        assert np.array_equal(out, want)
+        torch.cuda.synchronize()
+        for r in range(len(devices)):
+            a = g.a_part(r, ptrs[r], n).cpu().numpy().view(np.uint16)
+            assert np.array_equal(a, want[0]), r
+        out2, _, _ = g.run(q)  # a second call reuses the exchange set-up
+        assert np.array_equal(out2, want)
+    finally:
+        g.close()
+
+
+def test_ccmm_group_rejects_more_devices_than_parts():
+    from paper_2601_17561_b200.ccmm import CcmmGroup
+    from paper_2601_17561_b200.modmat import ShapeMismatch
+    with pytest.raises(ShapeMismatch):
+        CcmmGroup([0, 0, 0], parts=2, m=128, k=256, max_n=32)
