@@ -224,6 +224,11 @@ int irl_ccmm_set_mirrors(irl_ccmm* e, size_t part, size_t n, const uint8_t* ipc_
                          size_t count);
 /* Same with raw device pointers (same-process peers / tests). */
 int irl_ccmm_set_mirror_ptrs(irl_ccmm* e, size_t part, size_t n, uint16_t* const* dev_ptrs, size_t count);
+/* NVLS multicast mirror: mc_addr is a multicast address (cuMulticastCreate +
+ * cuMemMap) whose object binds one receive buffer per GPU; the epilogue of
+ * part `part` stores each pair of output rows there once (multimem.st) and the
+ * switch writes every bound copy. Needs an even M. NULL disables it. */
+int irl_ccmm_set_mirror_multicast(irl_ccmm* e, size_t part, size_t n, void* mc_addr);
 /* ModDown of the engine's outputs (after irl_ccmm_run_device wrote them to the
  * engine buffer, n columns): parts [part0, part0 + nparts) of [parts][nmod][n][M]
  * -> dst [nparts][nmod - drop][n][M] (device), see irl_rescale_residues. */
@@ -241,19 +246,25 @@ uint64_t irl_ccmm_device_bytes(const irl_ccmm* e);
 int irl_ccmm_group_create(const int* devices, size_t ndev, size_t parts, size_t m, size_t k, size_t max_n,
                           const uint32_t* primes, const uint32_t* exps, size_t nmod, irl_ccmm_group** out);
 int irl_ccmm_group_destroy(irl_ccmm_group* g);
+/* The a-part exchange of irl_ccmm_full. AUTO: P2P stores from rank 0's PPMM
+ * epilogue into each peer's receive buffer, else a cudaMemcpyPeer after the
+ * runs. MULTICAST (opt-in): one rank per multicast-capable device; rank 0's
+ * epilogue stores each output pair once to an NVLS multicast address and the
+ * switch writes every rank's copy (also valid with a single rank). MULTICAST
+ * and P2P fail with UNSUPPORTED where the driver refuses them. */
+enum { IRL_EXCHANGE_AUTO = 0, IRL_EXCHANGE_P2P = 1, IRL_EXCHANGE_MULTICAST = 2, IRL_EXCHANGE_COPY = 3 };
+int irl_ccmm_group_set_exchange(irl_ccmm_group* g, int mode);
 int irl_ccmm_group_engine(irl_ccmm_group* g, size_t rank, irl_ccmm** e, size_t* first_part, size_t* nparts);
 /* Context of a rank (irl_last_error of group calls is on rank 0's). */
 irl_ctx* irl_ccmm_group_ctx(irl_ccmm_group* g, size_t rank);
 /* The full CCMM across the devices with HOST buffers: q_res [nmod][K][n] ->
  * out [parts][nmod][n][M] (every part, in global order); each rank runs its
  * parts end to end (irl_ccmm_run) concurrently with the others. The a-part
- * result also lands on every rank: rank 0's PPMM epilogue stores it into the
- * other ranks' receive buffers over peer memory while it computes (*fused = 1),
- * or, without peer access, a cudaMemcpyPeer follows the runs (*fused = 0).
- * a_out (nullable, ndev entries) receives each rank's device pointer to its
- * copy [nmod][n][M]. n <= max_n. Blocks. */
+ * result also lands on every rank through the exchange above (*mode gets the
+ * IRL_EXCHANGE_* in use); a_out (nullable, ndev entries) receives each rank's
+ * device pointer to its copy [nmod][n][M]. n <= max_n. Blocks. */
 int irl_ccmm_full(irl_ccmm_group* g, const uint16_t* q_res_host, size_t n, uint16_t* out_host, void** a_out,
-                  int* fused);
+                  int* mode);
 
 /* ---- plaintext iris scoring stage ---------------------------
  * Templates are packed bit planes in pack_bits order (pipeline.cpp:70-76):

@@ -35,6 +35,8 @@ IRL_ERR_ZERO_OVERLAP = 11
 IRL_ERR_IO = 12
 IRL_ERR_CONFIG = 13
 
+IRL_EXCHANGE_AUTO, IRL_EXCHANGE_P2P, IRL_EXCHANGE_MULTICAST, IRL_EXCHANGE_COPY = 0, 1, 2, 3
+
 # Every symbol include/irl_capi.h declares, with (restype, argtypes).
 SIGNATURES = {
     "irl_abi_version": (C.c_int, []),
@@ -93,6 +95,8 @@ SIGNATURES = {
     "irl_ccmm_group_engine": (C.c_int, [vp, sz, C.POINTER(vp), C.POINTER(sz), C.POINTER(sz)]),
     "irl_ccmm_group_ctx": (vp, [vp, sz]),
     "irl_ccmm_full": (C.c_int, [vp, vp, sz, vp, C.POINTER(vp), C.POINTER(C.c_int)]),
+    "irl_ccmm_group_set_exchange": (C.c_int, [vp, C.c_int]),
+    "irl_ccmm_set_mirror_multicast": (C.c_int, [vp, sz, sz, vp]),
 }
 
 

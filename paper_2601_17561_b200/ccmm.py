@@ -162,7 +162,8 @@ class CcmmGroup:
     """The CCMM across several devices in one process (irl_ccmm_group_*,
     irl_ccmm_full): one engine per entry of `devices`, parts dealt as
     dist.part_range (the a-part on rank 0), the a-part result stored into every
-    other rank by rank 0's PPMM epilogue over peer memory."""
+    other rank by rank 0's PPMM epilogue: through an NVLS multicast address
+    (one rank per multicast-capable device) or P2P stores into each peer."""
 
     def __init__(self, devices, parts: int, m: int, k: int, max_n: int, basis: Optional[RnsBasis] = None):
         self.basis = basis or build_paper_basis()
@@ -195,18 +196,22 @@ class CcmmGroup:
             eng, first, _ = self.engine(r)
             eng.synth_db(seed, first_part=first)
 
+    def set_exchange(self, mode: int):
+        """capi.IRL_EXCHANGE_AUTO / _P2P / _MULTICAST / _COPY (irl_ccmm_group_set_exchange)."""
+        self.ctx.check(capi.lib().irl_ccmm_group_set_exchange(self.handle, mode))
+
     def run(self, q_res: np.ndarray, out: Optional[np.ndarray] = None):
         """q_res [nmod][K][n] -> (out [parts][nmod][n][M], per-rank device
-        pointers of the a-part result, fused exchange used)."""
+        pointers of the a-part result, the IRL_EXCHANGE_* mode used)."""
         assert q_res.dtype == np.uint16 and q_res.flags.c_contiguous
         n = q_res.shape[2]
         if out is None:
             out = np.empty((self.parts, self.nmod, n, self.M), np.uint16)
         ptrs = (C.c_void_p * len(self.devices))()
-        fused = C.c_int(0)
+        mode = C.c_int(-1)
         self.ctx.check(capi.lib().irl_ccmm_full(self.handle, capi.ptr(q_res), n, capi.ptr(out), ptrs,
-                                                C.byref(fused)))
-        return out, [p for p in ptrs], bool(fused.value)
+                                                C.byref(mode)))
+        return out, [p for p in ptrs], mode.value
 
     def a_part(self, rank: int, ptr: int, n: int):
         """torch view (int16 bit patterns) of a rank's copy of the a-part result."""

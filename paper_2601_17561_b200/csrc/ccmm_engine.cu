@@ -48,6 +48,7 @@ struct irl_ccmm {
     size_t mirror_part = 0, mirror_n = 0, n_mirror = 0;
     uint16_t* mirror[kMaxMirrors] = {};
     bool mirror_ipc[kMaxMirrors] = {};
+    uint16_t* mc_mirror = nullptr;  // NVLS multicast address of the receive buffers (irl_ccmm_set_mirror_multicast)
     // part-granular D2H in irl_ccmm_run: per (modulus chunk, part) tile
     // counters the epilogue bumps; the copy stream waits on them with stream
     // memory operations (cuStreamWaitValue32) instead of on the whole launch
@@ -205,6 +206,20 @@ int irl_ccmm_set_mirror_ptrs(irl_ccmm* e, size_t part, size_t n, uint16_t* const
     if (!e || (count && !dev_ptrs)) return IRL_ERR_INVALID_ARGUMENT;
     Guard g(e->ctx);
     return set_mirrors(e, part, n, dev_ptrs, nullptr, count);
+}
+
+int irl_ccmm_set_mirror_multicast(irl_ccmm* e, size_t part, size_t n, void* mc_addr) {
+    if (!e) return IRL_ERR_INVALID_ARGUMENT;
+    irl_ctx* ctx = e->ctx;
+    Guard g(ctx);
+    if (mc_addr && (part >= e->parts || n == 0 || n > e->max_n || (e->M & 1) != 0))
+        return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "ccmm: bad multicast mirror (part, width, or odd M)");
+    e->mc_mirror = static_cast<uint16_t*>(mc_addr);
+    if (mc_addr) {
+        e->mirror_part = part;
+        e->mirror_n = n;
+    }
+    return IRL_OK;
 }
 
 uint64_t irl_ccmm_device_bytes(const irl_ccmm* e) { return e ? e->bytes : 0; }
@@ -402,10 +417,12 @@ static int ccmm_parts(irl_ccmm* e, size_t n, size_t part0, size_t nparts, uint16
     L.out_part_elems = e->nmod * n * e->M;
     L.progress = e->progress;
     L.part_done = part_done;
-    if (e->n_mirror && n == e->mirror_n && e->mirror_part >= part0 && e->mirror_part < part0 + nparts) {
+    if ((e->n_mirror || e->mc_mirror) && n == e->mirror_n && e->mirror_part >= part0 &&
+        e->mirror_part < part0 + nparts) {
         L.n_mirror = static_cast<uint32_t>(e->n_mirror);
         L.mirror_part = static_cast<uint32_t>(e->mirror_part - part0);
         for (size_t i = 0; i < e->n_mirror; ++i) L.mirror[i] = e->mirror[i] + m0 * n * e->M;
+        if (e->mc_mirror) L.mc_mirror = e->mc_mirror + m0 * n * e->M;
     }
     return run_ppmm(ctx, L, e->kchunk, s);
 }

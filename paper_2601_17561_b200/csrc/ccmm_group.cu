@@ -7,7 +7,10 @@
 // concurrently. The a-part exchange is fused into rank 0's PPMM epilogue: it
 // stores each output tile of part 0 into every other rank's receive buffer
 // over peer memory (NVLink) while it computes. Where peer access is not
-// available, a cudaMemcpyPeer after the runs takes its place.
+// available, a cudaMemcpyPeer after the runs takes its place. On request, with
+// one rank per multicast-capable device (NVSwitch), the epilogue instead
+// stores once to an NVLS multicast address and the switch writes every copy.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -21,20 +24,116 @@
 
 using namespace irl;
 
+namespace {
+
+// Driver entry points of the NVLS multicast path, resolved once at run time
+// (the library links only the runtime).
+struct McApi {
+    CUresult (*GetGranularity)(size_t*, const CUmulticastObjectProp*, CUmulticastGranularity_flags) = nullptr;
+    CUresult (*Create)(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*) = nullptr;
+    CUresult (*AddDevice)(CUmemGenericAllocationHandle, CUdevice) = nullptr;
+    CUresult (*BindMem)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t, size_t,
+                        unsigned long long) = nullptr;
+    CUresult (*Unbind)(CUmemGenericAllocationHandle, CUdevice, size_t, size_t) = nullptr;
+    CUresult (*AllocGranularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) = nullptr;
+    CUresult (*MemCreate)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long) =
+        nullptr;
+    CUresult (*Release)(CUmemGenericAllocationHandle) = nullptr;
+    CUresult (*Reserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+    CUresult (*Free)(CUdeviceptr, size_t) = nullptr;
+    CUresult (*Map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+    CUresult (*Unmap)(CUdeviceptr, size_t) = nullptr;
+    CUresult (*SetAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
+    CUresult (*DeviceGet)(CUdevice*, int) = nullptr;
+    CUresult (*GetAttribute)(int*, CUdevice_attribute, CUdevice) = nullptr;
+    bool ok = false;
+};
+
+template <typename F>
+bool entry(const char* name, F* fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    *fn = reinterpret_cast<F>(p);
+    return true;
+}
+
+const McApi& mc_api() {
+    static const McApi api = [] {
+        McApi a;
+        a.ok = entry("cuMulticastGetGranularity", &a.GetGranularity) && entry("cuMulticastCreate", &a.Create) &&
+               entry("cuMulticastAddDevice", &a.AddDevice) && entry("cuMulticastBindMem", &a.BindMem) &&
+               entry("cuMulticastUnbind", &a.Unbind) &&
+               entry("cuMemGetAllocationGranularity", &a.AllocGranularity) && entry("cuMemCreate", &a.MemCreate) &&
+               entry("cuMemRelease", &a.Release) && entry("cuMemAddressReserve", &a.Reserve) &&
+               entry("cuMemAddressFree", &a.Free) && entry("cuMemMap", &a.Map) && entry("cuMemUnmap", &a.Unmap) &&
+               entry("cuMemSetAccess", &a.SetAccess) && entry("cuDeviceGet", &a.DeviceGet) &&
+               entry("cuDeviceGetAttribute", &a.GetAttribute);
+        return a;
+    }();
+    return api;
+}
+
+// One multicast object over the ranks' devices, a physical receive buffer per
+// rank bound to it and mapped locally, and the multicast address mapped for
+// rank 0 (the a-part owner, whose epilogue stores through it).
+struct McExchange {
+    CUmemGenericAllocationHandle mc = 0;
+    std::vector<CUmemGenericAllocationHandle> phys;
+    std::vector<CUdeviceptr> va;
+    CUdeviceptr mc_va = 0;
+    size_t size = 0;
+    std::vector<int> dev;
+};
+
+void mc_release(McExchange* x) {
+    const McApi& a = mc_api();
+    if (!a.ok) return;
+    if (x->mc_va) {
+        a.Unmap(x->mc_va, x->size);
+        a.Free(x->mc_va, x->size);
+    }
+    for (size_t r = 0; r < x->va.size(); ++r) {
+        if (x->va[r]) {
+            a.Unmap(x->va[r], x->size);
+            a.Free(x->va[r], x->size);
+        }
+    }
+    if (x->mc) {
+        for (int d : x->dev) {
+            CUdevice cd;
+            if (a.DeviceGet(&cd, d) == CUDA_SUCCESS) a.Unbind(x->mc, cd, 0, x->size);
+        }
+    }
+    for (CUmemGenericAllocationHandle h : x->phys)
+        if (h) a.Release(h);
+    if (x->mc) a.Release(x->mc);
+    *x = McExchange();
+}
+
+}  // namespace
+
 struct irl_ccmm_group {
     size_t ndev = 0, parts = 0, M = 0, K = 0, max_n = 0, nmod = 0;
     std::vector<int> dev;
     std::vector<irl_ctx*> ctx;
     std::vector<irl_ccmm*> eng;
     std::vector<size_t> first, count;
-    std::vector<uint16_t*> recv;  // rank r > 0: receive buffer of the a-part result [nmod][n][M]
+    std::vector<uint16_t*> recv;  // rank r: receive buffer of the a-part result [nmod][n][M] (r > 0, or all with MC)
     size_t recv_n = 0;            // width the receive buffers and mirrors are set up for
-    bool fused = false;           // rank 0's epilogue stores into the peers
+    int requested = IRL_EXCHANGE_AUTO;
+    int mode = IRL_EXCHANGE_COPY;  // the exchange in use
+    McExchange mcx;
 };
 
 namespace {
 
 void destroy_group(irl_ccmm_group* g) {
+    if (!g->eng.empty() && g->eng[0]) irl_ccmm_set_mirror_multicast(g->eng[0], 0, 0, nullptr);
+    mc_release(&g->mcx);
     for (size_t r = 0; r < g->eng.size(); ++r)
         if (g->eng[r]) irl_ccmm_destroy(g->eng[r]);
     for (irl_ctx* c : g->ctx)
@@ -42,13 +141,113 @@ void destroy_group(irl_ccmm_group* g) {
     delete g;
 }
 
-// Receive buffers of width n on ranks 1.., peer access from rank 0's device,
-// and rank 0's mirror list (or none, for the copy fallback).
+bool mc_supported(const irl_ccmm_group* g) {
+    const McApi& a = mc_api();
+    if (!a.ok) return false;
+    for (size_t r = 0; r < g->ndev; ++r) {
+        for (size_t q = 0; q < r; ++q)
+            if (g->dev[q] == g->dev[r]) return false;  // one bound buffer per device
+        CUdevice cd;
+        int v = 0;
+        if (a.DeviceGet(&cd, g->dev[r]) != CUDA_SUCCESS ||
+            a.GetAttribute(&v, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, cd) != CUDA_SUCCESS || !v)
+            return false;
+    }
+    return true;
+}
+
+#define MC_CK(expr)                                                                    \
+    do {                                                                               \
+        const CUresult r__ = (expr);                                                   \
+        if (r__ != CUDA_SUCCESS) {                                                     \
+            mc_release(&g->mcx);                                                       \
+            return set_err(g->ctx[0], IRL_ERR_CUDA, std::string("multicast: ") + #expr); \
+        }                                                                              \
+    } while (0)
+
+int mc_setup(irl_ccmm_group* g, size_t bytes) {
+    const McApi& a = mc_api();
+    McExchange& x = g->mcx;
+    x.dev = g->dev;
+    CUmulticastObjectProp prop = {};
+    prop.numDevices = static_cast<unsigned>(g->ndev);
+    prop.handleTypes = CU_MEM_HANDLE_TYPE_NONE;
+    prop.size = bytes;
+    size_t mg = 0, pg = 0;
+    MC_CK(a.GetGranularity(&mg, &prop, CU_MULTICAST_GRANULARITY_MINIMUM));
+    CUmemAllocationProp ap = {};
+    ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    ap.location.id = g->dev[0];
+    MC_CK(a.AllocGranularity(&pg, &ap, CU_MEM_ALLOC_GRANULARITY_MINIMUM));
+    const size_t gran = std::max(mg, pg);
+    x.size = (bytes + gran - 1) / gran * gran;
+    prop.size = x.size;
+    MC_CK(a.Create(&x.mc, &prop));
+    for (size_t r = 0; r < g->ndev; ++r) {
+        CUdevice cd;
+        MC_CK(a.DeviceGet(&cd, g->dev[r]));
+        MC_CK(a.AddDevice(x.mc, cd));
+    }
+    x.phys.assign(g->ndev, 0);
+    x.va.assign(g->ndev, 0);
+    for (size_t r = 0; r < g->ndev; ++r) {
+        cudaSetDevice(g->dev[r]);
+        cudaFree(nullptr);  // the device's primary context is current for the driver calls
+        ap.location.id = g->dev[r];
+        MC_CK(a.MemCreate(&x.phys[r], x.size, &ap, 0));
+        MC_CK(a.BindMem(x.mc, 0, x.phys[r], 0, x.size, 0));
+        MC_CK(a.Reserve(&x.va[r], x.size, 0, 0, 0));
+        MC_CK(a.Map(x.va[r], x.size, 0, x.phys[r], 0));
+        CUmemAccessDesc ad = {};
+        ad.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        ad.location.id = g->dev[r];
+        ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+        MC_CK(a.SetAccess(x.va[r], x.size, &ad, 1));
+    }
+    cudaSetDevice(g->dev[0]);
+    MC_CK(a.Reserve(&x.mc_va, x.size, 0, 0, 0));
+    MC_CK(a.Map(x.mc_va, x.size, 0, x.mc, 0));
+    CUmemAccessDesc ad = {};
+    ad.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    ad.location.id = g->dev[0];
+    ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    MC_CK(a.SetAccess(x.mc_va, x.size, &ad, 1));
+    return IRL_OK;
+}
+
+// The exchange for width n: NVLS multicast (one multimem.st per element pair,
+// replicated by the switch into every rank's bound buffer), P2P stores into
+// each peer's receive buffer, or a cudaMemcpyPeer after the runs.
 int setup_exchange(irl_ccmm_group* g, size_t n) {
     if (g->recv_n == n) return IRL_OK;
     irl_ctx* c0 = g->ctx[0];
+    irl_ccmm_set_mirror_ptrs(g->eng[0], 0, n, nullptr, 0);
+    irl_ccmm_set_mirror_multicast(g->eng[0], 0, 0, nullptr);
+    mc_release(&g->mcx);
     g->recv.assign(g->ndev, nullptr);
-    bool peer = true;
+    const size_t bytes = g->nmod * n * g->M * sizeof(uint16_t);
+    // multicast is opt-in: it could not be exercised where this was built
+    // (cuMulticastCreate is refused inside the container), so AUTO stays on
+    // the validated P2P stores
+    const bool want_mc = g->requested == IRL_EXCHANGE_MULTICAST;
+    if (want_mc && (g->M % 2) == 0 && mc_supported(g)) {
+        if (mc_setup(g, bytes) != IRL_OK) {
+            return set_err(c0, IRL_ERR_UNSUPPORTED,
+                           std::string("ccmm group: NVLS multicast refused by the driver (") + irl_last_error(c0) + ")");
+        } else {
+            for (size_t r = 0; r < g->ndev; ++r) g->recv[r] = reinterpret_cast<uint16_t*>(g->mcx.va[r]);
+            if (int st = irl_ccmm_set_mirror_multicast(g->eng[0], 0, n, reinterpret_cast<void*>(g->mcx.mc_va)))
+                return st;
+            g->mode = IRL_EXCHANGE_MULTICAST;
+            g->recv_n = n;
+            return IRL_OK;
+        }
+    } else if (g->requested == IRL_EXCHANGE_MULTICAST) {
+        return set_err(c0, IRL_ERR_UNSUPPORTED, "ccmm group: NVLS multicast unavailable (one rank per device, "
+                                                "multicast-capable devices and an even M are required)");
+    }
+    bool peer = g->requested != IRL_EXCHANGE_COPY;
     for (size_t r = 1; r < g->ndev; ++r) {
         void* p = nullptr;
         if (int st = irl_ccmm_alloc_recv(g->eng[r], n, &p, nullptr)) {
@@ -56,7 +255,7 @@ int setup_exchange(irl_ccmm_group* g, size_t n) {
             return st;
         }
         g->recv[r] = static_cast<uint16_t*>(p);
-        if (g->dev[r] != g->dev[0]) {
+        if (peer && g->dev[r] != g->dev[0]) {
             int can = 0;
             cudaSetDevice(g->dev[0]);
             if (cudaDeviceCanAccessPeer(&can, g->dev[0], g->dev[r]) != cudaSuccess || !can) {
@@ -64,13 +263,16 @@ int setup_exchange(irl_ccmm_group* g, size_t n) {
             } else {
                 const cudaError_t e = cudaDeviceEnablePeerAccess(g->dev[r], 0);
                 if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) peer = false;
-                cudaGetLastError();
             }
+            cudaGetLastError();
         }
     }
-    g->fused = peer && g->ndev > 1 && g->ndev - 1 <= static_cast<size_t>(kMaxMirrors);
+    peer = peer && g->ndev > 1 && g->ndev - 1 <= static_cast<size_t>(kMaxMirrors);
+    if (g->requested == IRL_EXCHANGE_P2P && !peer && g->ndev > 1)
+        return set_err(c0, IRL_ERR_UNSUPPORTED, "ccmm group: peer access unavailable for P2P stores");
     std::vector<uint16_t*> peers(g->recv.begin() + (g->ndev > 1 ? 1 : 0), g->recv.end());
-    if (int st = irl_ccmm_set_mirror_ptrs(g->eng[0], 0, n, peers.data(), g->fused ? peers.size() : 0)) return st;
+    if (int st = irl_ccmm_set_mirror_ptrs(g->eng[0], 0, n, peers.data(), peer ? peers.size() : 0)) return st;
+    g->mode = peer ? IRL_EXCHANGE_P2P : IRL_EXCHANGE_COPY;
     g->recv_n = n;
     return IRL_OK;
 }
@@ -111,6 +313,13 @@ int irl_ccmm_group_create(const int* devices, size_t ndev, size_t parts, size_t 
     return IRL_OK;
 }
 
+int irl_ccmm_group_set_exchange(irl_ccmm_group* g, int mode) {
+    if (!g || mode < IRL_EXCHANGE_AUTO || mode > IRL_EXCHANGE_COPY) return IRL_ERR_INVALID_ARGUMENT;
+    g->requested = mode;
+    g->recv_n = 0;  // set up again on the next run
+    return IRL_OK;
+}
+
 int irl_ccmm_group_destroy(irl_ccmm_group* g) {
     if (g) destroy_group(g);
     return IRL_OK;
@@ -129,7 +338,7 @@ irl_ctx* irl_ccmm_group_ctx(irl_ccmm_group* g, size_t rank) {
 }
 
 int irl_ccmm_full(irl_ccmm_group* g, const uint16_t* q_res_host, size_t n, uint16_t* out_host, void** a_out,
-                  int* fused) {
+                  int* mode) {
     if (!g || !q_res_host || !out_host) return IRL_ERR_INVALID_ARGUMENT;
     irl_ctx* c0 = g->ctx[0];
     if (n == 0 || n > g->max_n) return set_err(c0, IRL_ERR_SHAPE_MISMATCH, "ccmm group: query width out of range");
@@ -149,7 +358,7 @@ int irl_ccmm_full(irl_ccmm_group* g, const uint16_t* q_res_host, size_t n, uint1
     void* out0 = nullptr;
     irl_ccmm_buffers(g->eng[0], &q0, &out0);  // rank 0's outputs; part 0 = the a-part result
     const size_t a_bytes = g->nmod * n * g->M * sizeof(uint16_t);
-    if (!g->fused) {  // the exchange as plain peer copies after the runs
+    if (g->mode == IRL_EXCHANGE_COPY) {  // the exchange as plain peer copies after the runs
         for (size_t r = 1; r < g->ndev; ++r) {
             cudaSetDevice(g->dev[r]);
             const cudaError_t e = cudaMemcpyPeer(g->recv[r], g->dev[r], out0, g->dev[0], a_bytes);
@@ -157,8 +366,8 @@ int irl_ccmm_full(irl_ccmm_group* g, const uint16_t* q_res_host, size_t n, uint1
         }
     }
     if (a_out)
-        for (size_t r = 0; r < g->ndev; ++r) a_out[r] = r == 0 ? out0 : g->recv[r];
-    if (fused) *fused = g->fused ? 1 : 0;
+        for (size_t r = 0; r < g->ndev; ++r) a_out[r] = g->recv[r] ? static_cast<void*>(g->recv[r]) : out0;
+    if (mode) *mode = g->mode;
     return IRL_OK;
 }
 

@@ -69,6 +69,11 @@ struct PpmmLaunch {
     uint16_t* mirror[kMaxMirrors] = {};
     uint32_t n_mirror = 0;
     uint32_t mirror_part = 0;
+    // NVLS multicast mirror: a multicast address (cuMulticastCreate, bound to
+    // one receive buffer per GPU); the epilogue stores each pair of output rows
+    // once with multimem.st and the switch delivers it to every bound GPU.
+    // Needs M even. Used instead of, or with, mirror[].
+    uint16_t* mc_mirror = nullptr;
     // Optional [nprimes][parts] completion counters (zeroed by the caller):
     // every epilogue warp adds 1 per finished tile of that (prime, part);
     // ppmm_last_part_target() is the final count of each.

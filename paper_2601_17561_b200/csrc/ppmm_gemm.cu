@@ -101,6 +101,7 @@ struct __align__(64) GemmArgs {
     IrisMatchOut iris;                // kMode == kModeIrisMatch
     uint16_t* mirror[kMaxMirrors];    // peer copies of part mirror_part's outputs (see PpmmLaunch)
     uint32_t n_mirror, mirror_part;
+    uint16_t* mc_mirror;              // multicast address of part mirror_part's copies (see PpmmLaunch)
     uint32_t* part_done;              // optional [nprimes][parts] count of (epilogue warp, tile) completions
     uint32_t* progress;               // [clusters] K blocks issued by each pair's leader producer
     uint32_t* counter;                // next unit to hand out (shared by the main and filler launches)
@@ -531,7 +532,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             uint16_t* out = args.out + tc.part * args.out_part +
                             static_cast<size_t>(tc.prime) * args.N * args.M +
                             m;
-            const bool mirror_tile = args.n_mirror != 0 && tc.part == args.mirror_part;
+            const bool mirror_tile = (args.n_mirror != 0 || args.mc_mirror != nullptr) && tc.part == args.mirror_part;
+            const bool mc_tile = args.mc_mirror != nullptr && tc.part == args.mirror_part;
             const uint32_t lane_base = tmem_base + ((quarter * 32u) << 16);
             for (uint32_t c = cgrp * 16; c < tc.n_size; c += 16 * kEpiGroups) {
                 uint32_t a1[16], a2[16];
@@ -589,6 +591,36 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                             }
                         }
                     }
+                    continue;
+                }
+                if (kMode == kModePsq && mc_tile) {
+                    // multicast mirror: the whole warp takes part (lanes past M
+                    // compute but do not store); even lanes store rows (m, m+1)
+                    // as one 32-bit multimem.st, which the switch replicates
+                    uint16_t* dst = out + static_cast<size_t>(tc.n0 + c) * args.M;
+                    const size_t moff = static_cast<size_t>(tc.prime) * args.N * args.M +
+                                        static_cast<size_t>(tc.n0 + c) * args.M + m;
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) {
+                        if (tc.n0 + c + jj >= args.N) continue;  // uniform across the warp
+                        uint32_t v = combine_psq_fast(static_cast<int32_t>(a1[jj]), static_cast<int32_t>(a2[jj]),
+                                                      mc.p, mc.m, mc.magic_p, mc.magic_m, mc.c_p, mc.c_m);
+                        uint16_t* d = dst + static_cast<size_t>(jj) * args.M;
+                        if (row_ok) {
+                            if (args.accumulate) {
+                                v += *d;
+                                v = min(v, v - mc.m);
+                            }
+                            *d = static_cast<uint16_t>(v);
+                            for (uint32_t mi = 0; mi < args.n_mirror; ++mi)
+                                args.mirror[mi][moff + static_cast<size_t>(jj) * args.M] = static_cast<uint16_t>(v);
+                        }
+                        const uint32_t hi = __shfl_down_sync(0xFFFFFFFFu, v, 1);
+                        if (row_ok && (lane & 1u) == 0)
+                            ptx::multimem_st_b32(args.mc_mirror + moff + static_cast<size_t>(jj) * args.M,
+                                                 (v & 0xFFFFu) | (hi << 16));
+                    }
+                    __threadfence_system();
                     continue;
                 }
                 if (!row_ok) continue;
@@ -884,6 +916,8 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     args.part_done = L.part_done;
     args.n_mirror = L.n_mirror;
     args.mirror_part = L.mirror_part;
+    args.mc_mirror = L.mc_mirror;
+    if (L.mc_mirror && (L.mode != kModePsq || (L.M & 1u) != 0)) return cudaErrorInvalidValue;
     for (uint32_t i = 0; i < L.n_mirror; ++i) args.mirror[i] = L.mirror[i];
     args.out_i32[0] = L.out_i32[0];
     args.out_i32[1] = L.out_i32[1];

@@ -270,6 +270,12 @@ __device__ __forceinline__ uint64_t smem_desc_k_sw64(uint32_t smem_addr) {
     return d;
 }
 
+// 32-bit store to a multicast address (NVLS): the switch writes it into the
+// memory every GPU bound to the multicast object.
+__device__ __forceinline__ void multimem_st_b32(void* mc_addr, uint32_t v) {
+    asm volatile("multimem.st.relaxed.sys.global.b32 [%0], %1;" ::"l"(mc_addr), "r"(v) : "memory");
+}
+
 // Instruction descriptor: kind::i8, signed A/B, S32 accumulate, K-major A/B.
 __host__ __device__ constexpr uint32_t idesc_i8(uint32_t m, uint32_t n) {
     return (2u << 4)            // D format S32

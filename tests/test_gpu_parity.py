@@ -589,6 +589,7 @@ def test_ccmm_group_full_equals_one_engine_and_exchanges_the_a_part(devices, par
     result, stored into it by rank 0's PPMM epilogue (fused exchange)."""
     import torch
 
+    from paper_2601_17561_b200 import capi
     from paper_2601_17561_b200.ccmm import CcmmEngine, CcmmGroup, synth_query
     from paper_2601_17561_b200.dist import part_range
     m, k, n = 384, 1024, 96
@@ -604,8 +605,8 @@ def test_ccmm_group_full_equals_one_engine_and_exchanges_the_a_part(devices, par
         q = synth_query(2, k, n, eng.moduli)
         want = eng.run(q)
         eng.close()
-        out, ptrs, fused = g.run(q)
-        assert fused
+        out, ptrs, mode = g.run(q)
+        assert mode == capi.IRL_EXCHANGE_P2P  # ranks share a device: no multicast, P2P stores
         assert np.array_equal(out, want)
         torch.cuda.synchronize()
         for r in range(len(devices)):
@@ -622,3 +623,51 @@ def test_ccmm_group_rejects_more_devices_than_parts():
     from paper_2601_17561_b200.modmat import ShapeMismatch
     with pytest.raises(ShapeMismatch):
         CcmmGroup([0, 0, 0], parts=2, m=128, k=256, max_n=32)
+
+
+@pytest.mark.parametrize("k", [1024, 4096])
+def test_ccmm_group_nvls_multicast_mirror(k):
+    """The NVLS multicast exchange on one GPU: a multicast object with this
+    device, the rank's receive buffer bound to it, and the a-part PPMM epilogue
+    storing every pair of output rows once through the multicast address
+    (multimem.st). With one device the switch delivers to that one copy; on an
+    NVSwitch node the same stores reach every rank. k = 4096 exercises the
+    K-chunked (accumulating) launches when the digit bound requires them."""
+    import torch
+
+    from paper_2601_17561_b200 import capi
+    from paper_2601_17561_b200.ccmm import CcmmEngine, CcmmGroup, synth_query
+    m, n = 384, 96
+    g = CcmmGroup([0], parts=2, m=m, k=k, max_n=n)
+    from paper_2601_17561_b200.modmat import Error
+    try:
+        g.synth_db(seed=4)
+        g.set_exchange(capi.IRL_EXCHANGE_MULTICAST)
+        eng = CcmmEngine(parts=2, m=m, k=k, max_n=n)
+        eng.synth_db(seed=4)
+        q = synth_query(5, k, n, eng.moduli)
+        want = eng.run(q)
+        eng.close()
+        try:
+            out, ptrs, mode = g.run(q)
+        except Error as ex:  # containers without the NVSwitch fabric refuse cuMulticastCreate
+            if "multicast" in str(ex):
+                pytest.skip(f"NVLS multicast unavailable here: {ex}")
+            raise
+        assert mode == capi.IRL_EXCHANGE_MULTICAST
+        assert np.array_equal(out, want)
+        torch.cuda.synchronize()
+        a = g.a_part(0, ptrs[0], n).cpu().numpy().view(np.uint16)
+        assert np.array_equal(a, want[0])
+        # the multicast copy is rewritten on every run, and a narrower batch re-binds
+        q2 = synth_query(6, k, n, eng.moduli)
+        out2, ptrs2, _ = g.run(q2)
+        torch.cuda.synchronize()
+        assert np.array_equal(g.a_part(0, ptrs2[0], n).cpu().numpy().view(np.uint16), out2[0])
+        q3 = np.ascontiguousarray(q2[:, :, :64])
+        out3, ptrs3, mode3 = g.run(q3)
+        torch.cuda.synchronize()
+        assert mode3 == capi.IRL_EXCHANGE_MULTICAST
+        assert np.array_equal(g.a_part(0, ptrs3[0], 64).cpu().numpy().view(np.uint16), out3[0])
+    finally:
+        g.close()
