@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -127,6 +128,7 @@ struct irl_ccmm_group {
     int requested = IRL_EXCHANGE_AUTO;
     int mode = IRL_EXCHANGE_COPY;  // the exchange in use
     McExchange mcx;
+    std::mutex mu;  // one irl_ccmm_full / set_exchange at a time
 };
 
 namespace {
@@ -315,6 +317,7 @@ int irl_ccmm_group_create(const int* devices, size_t ndev, size_t parts, size_t 
 
 int irl_ccmm_group_set_exchange(irl_ccmm_group* g, int mode) {
     if (!g || mode < IRL_EXCHANGE_AUTO || mode > IRL_EXCHANGE_COPY) return IRL_ERR_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(g->mu);
     g->requested = mode;
     g->recv_n = 0;  // set up again on the next run
     return IRL_OK;
@@ -340,6 +343,7 @@ irl_ctx* irl_ccmm_group_ctx(irl_ccmm_group* g, size_t rank) {
 int irl_ccmm_full(irl_ccmm_group* g, const uint16_t* q_res_host, size_t n, uint16_t* out_host, void** a_out,
                   int* mode) {
     if (!g || !q_res_host || !out_host) return IRL_ERR_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(g->mu);
     irl_ctx* c0 = g->ctx[0];
     if (n == 0 || n > g->max_n) return set_err(c0, IRL_ERR_SHAPE_MISMATCH, "ccmm group: query width out of range");
     if (int st = setup_exchange(g, n)) return st;
