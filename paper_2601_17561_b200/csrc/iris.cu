@@ -34,35 +34,63 @@ using namespace irl;
 
 namespace {
 
+// The iris products run on the block-scaled FP4 tensor path unless
+// IRL_IRIS_I8 is set: ternary values and mask bits are exact in e2m1 and the
+// FP32 accumulators are exact below 2^24, at twice the int8 rate with half
+// the plane bytes (profiles/fp4_probe.cu).
+bool iris_f4() {
+    static const bool f4 = std::getenv("IRL_IRIS_I8") == nullptr;
+    return f4;
+}
+// Bytes of one plane row holding d entries (int8: one per byte; e2m1: two).
+size_t plane_kbytes(size_t d) { return iris_f4() ? (d + 1) / 2 : d; }
+size_t plane_ldk(size_t d) { return round16(plane_kbytes(d)); }
+
+// One entry of a plane row into the 16-byte chunk being assembled: int8
+// value t / mask mb at position j, or their e2m1 nibbles (+1 = 0x2, -1 = 0xA).
+template <bool kF4>
+__device__ __forceinline__ void put_entry(uint32_t (&v)[4], uint32_t (&w)[4], int j, int32_t t, uint32_t mb) {
+    if constexpr (kF4) {
+        const uint32_t tv = t == 0 ? 0u : (t > 0 ? 0x2u : 0xAu);
+        v[j / 8] |= tv << (4 * (j % 8));
+        w[j / 8] |= (mb ? 0x2u : 0u) << (4 * (j % 8));
+    } else {
+        v[j / 4] |= (static_cast<uint32_t>(t) & 0xFFu) << (8 * (j % 4));
+        w[j / 4] |= mb << (8 * (j % 4));
+    }
+}
+
 // Packed templates (little-endian bit order, `words` uint64 per template) ->
-// K-major int8 planes: planes[0][c][ldk] = to_masked(rotate(t_e, r)),
+// K-major planes: planes[0][c][ldk] = to_masked(rotate(t_e, r)),
 // planes[1][c][ldk] = its mask, for column c = e * rho + r. Entries k >= d are 0.
-// One thread writes 16 consecutive k of one column to each plane.
+// One thread writes one 16-byte chunk of one column to each plane (16 entries
+// as int8, 32 as e2m1 nibbles, low nibble first).
+template <bool kF4>
 __global__ void iris_planes_kernel(const uint64_t* __restrict__ code, const uint64_t* __restrict__ mask,
                                    uint32_t words, uint32_t d, uint32_t rho, uint32_t cols, uint32_t ldk,
                                    int8_t* __restrict__ planes) {
+    constexpr int kPer = kF4 ? 32 : 16;
     const uint32_t chunks = ldk / 16;
     const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (tid >= static_cast<size_t>(cols) * chunks) return;
     const uint32_t c = static_cast<uint32_t>(tid / chunks);
-    const uint32_t k0 = static_cast<uint32_t>(tid % chunks) * 16;
+    const uint32_t chunk = static_cast<uint32_t>(tid % chunks);
+    const uint32_t k0 = chunk * kPer;
     const uint32_t e = c / rho, r = c % rho % d;
     const uint64_t* cw = code + static_cast<size_t>(e) * words;
     const uint64_t* mw = mask + static_cast<size_t>(e) * words;
     uint32_t v[4] = {0, 0, 0, 0}, w[4] = {0, 0, 0, 0};
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < kPer; ++j) {
         const uint32_t k = k0 + j;
         if (k >= d) break;
         // rotate: out[(i + r) % d] = t[i]  =>  out[k] = t[(k - r) mod d]
         const uint32_t i = k >= r ? k - r : k + d - r;
         const uint32_t cb = static_cast<uint32_t>((__ldg(cw + (i >> 6)) >> (i & 63)) & 1u);
         const uint32_t mb = static_cast<uint32_t>((__ldg(mw + (i >> 6)) >> (i & 63)) & 1u);
-        const int32_t t = static_cast<int32_t>(mb) - 2 * static_cast<int32_t>(cb & mb);
-        v[j / 4] |= (static_cast<uint32_t>(t) & 0xFFu) << (8 * (j % 4));
-        w[j / 4] |= mb << (8 * (j % 4));
+        put_entry<kF4>(v, w, j, static_cast<int32_t>(mb) - 2 * static_cast<int32_t>(cb & mb), mb);
     }
-    const size_t o = static_cast<size_t>(c) * ldk + k0;
+    const size_t o = static_cast<size_t>(c) * ldk + chunk * 16;
     *reinterpret_cast<uint4*>(planes + o) = make_uint4(v[0], v[1], v[2], v[3]);
     *reinterpret_cast<uint4*>(planes + static_cast<size_t>(cols) * ldk + o) = make_uint4(w[0], w[1], w[2], w[3]);
 }
@@ -71,44 +99,44 @@ __global__ void iris_planes_kernel(const uint64_t* __restrict__ code, const uint
 // all templates' bits back to back, little-endian bit order (bit i of byte j
 // is element 8 j + i) -- so template t, entry k is global bit t * d + k.
 // Same outputs as iris_planes_kernel for rho = 1.
+template <bool kF4>
 __global__ void iris_file_planes_kernel(const uint8_t* __restrict__ code, const uint8_t* __restrict__ mask,
                                         uint32_t d, uint32_t n, uint32_t ldk, int8_t* __restrict__ planes) {
+    constexpr int kPer = kF4 ? 32 : 16;
     const uint32_t chunks = ldk / 16;
     const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (tid >= static_cast<size_t>(n) * chunks) return;
     const uint32_t t = static_cast<uint32_t>(tid / chunks);
-    const uint32_t k0 = static_cast<uint32_t>(tid % chunks) * 16;
+    const uint32_t chunk = static_cast<uint32_t>(tid % chunks);
+    const uint32_t k0 = chunk * kPer;
     uint32_t v[4] = {0, 0, 0, 0}, w[4] = {0, 0, 0, 0};
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < kPer; ++j) {
         const uint32_t k = k0 + j;
         if (k >= d) break;
         const size_t bit = static_cast<size_t>(t) * d + k;
         const uint32_t cb = (__ldg(code + (bit >> 3)) >> (bit & 7)) & 1u;
         const uint32_t mb = (__ldg(mask + (bit >> 3)) >> (bit & 7)) & 1u;
-        const int32_t x = static_cast<int32_t>(mb) - 2 * static_cast<int32_t>(cb & mb);
-        v[j / 4] |= (static_cast<uint32_t>(x) & 0xFFu) << (8 * (j % 4));
-        w[j / 4] |= mb << (8 * (j % 4));
+        put_entry<kF4>(v, w, j, static_cast<int32_t>(mb) - 2 * static_cast<int32_t>(cb & mb), mb);
     }
-    const size_t o = static_cast<size_t>(t) * ldk + k0;
+    const size_t o = static_cast<size_t>(t) * ldk + chunk * 16;
     *reinterpret_cast<uint4*>(planes + o) = make_uint4(v[0], v[1], v[2], v[3]);
     *reinterpret_cast<uint4*>(planes + static_cast<size_t>(n) * ldk + o) = make_uint4(w[0], w[1], w[2], w[3]);
 }
-
 
 // kModeInner GEMM of device planes x (DB, [2][n_db][ldk]) and y (queries,
 // [2][cols][ldk]) into inner / overlap [cols][n_db].
 int inner_overlap_gemm(irl_ctx* ctx, const int8_t* xp, const int8_t* yp, size_t n_db, size_t cols, size_t d,
                        size_t ldk, int32_t* inner, int32_t* ovl, uint32_t* progress, cudaStream_t s) {
     PpmmLaunch L;
-    L.mode = kModeInner;
+    L.mode = iris_f4() ? kModeInnerF4 : kModeInner;
     L.a_planes = xp;
     L.b_planes = yp;
     L.out_i32[0] = inner;
     L.out_i32[1] = ovl;
     L.M = static_cast<uint32_t>(n_db);
     L.N = static_cast<uint32_t>(cols);
-    L.K = static_cast<uint32_t>(d);
+    L.K = static_cast<uint32_t>(plane_kbytes(d));
     L.ldk = static_cast<uint32_t>(ldk);
     L.parts = 1;
     L.nprimes = 1;
@@ -121,10 +149,11 @@ int inner_overlap_gemm(irl_ctx* ctx, const int8_t* xp, const int8_t* yp, size_t 
 
 int build_planes(irl_ctx* ctx, const uint64_t* code, const uint64_t* mask, size_t n, size_t rho, size_t d,
                  int8_t* planes, cudaStream_t s) {
-    const size_t words = (d + 63) / 64, ldk = round16(d), cols = n * rho;
+    const size_t words = (d + 63) / 64, ldk = plane_ldk(d), cols = n * rho;
     const size_t total = cols * (ldk / 16);
     if (total == 0) return IRL_OK;
-    iris_planes_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
+    auto kern = iris_f4() ? iris_planes_kernel<true> : iris_planes_kernel<false>;
+    kern<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
         code, mask, static_cast<uint32_t>(words), static_cast<uint32_t>(d), static_cast<uint32_t>(rho),
         static_cast<uint32_t>(cols), static_cast<uint32_t>(ldk), planes);
     IRL_LAUNCH(ctx, cudaGetLastError());
@@ -149,12 +178,12 @@ int match_fused(irl_ctx* ctx, const int8_t* xp, const int8_t* yp, size_t n_db, s
     IRL_CK(ctx, cudaMemsetAsync(first, 0xFF, 8 * n_eyes, s));
     IRL_CK(ctx, cudaMemsetAsync(dbits, 0, nbits, s));
     PpmmLaunch L;
-    L.mode = kModeIrisMatch;
+    L.mode = iris_f4() ? kModeIrisMatchF4 : kModeIrisMatch;
     L.a_planes = xp;
     L.b_planes = yp;
     L.M = static_cast<uint32_t>(n_db);
     L.N = static_cast<uint32_t>(cols);
-    L.K = static_cast<uint32_t>(d);
+    L.K = static_cast<uint32_t>(plane_kbytes(d));
     L.ldk = static_cast<uint32_t>(ldk);
     L.parts = 1;
     L.nprimes = 1;
@@ -199,7 +228,7 @@ int inner_overlap_device(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* 
                          const uint64_t* q_code, const uint64_t* q_mask, size_t n_eyes, size_t rho, size_t d,
                          int32_t** d_inner, int32_t** d_overlap) {
     cudaStream_t s = ctx->stream;
-    const size_t words = (d + 63) / 64, ldk = round16(d), cols = n_eyes * rho;
+    const size_t words = (d + 63) / 64, ldk = plane_ldk(d), cols = n_eyes * rho;
     if (int st = check_dims(ctx, n_db, cols, d)) return st;
     const size_t db_bits = n_db * words * 8, q_bits = n_eyes * words * 8;
     IRL_CK(ctx, ctx->ws[0].ensure(2 * db_bits + 2 * q_bits));
@@ -284,7 +313,7 @@ int irl_iris_match(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db_mas
         return IRL_OK;
     }
     cudaStream_t s = ctx->stream;
-    const size_t words = (d + 63) / 64, ldk = round16(d);
+    const size_t words = (d + 63) / 64, ldk = plane_ldk(d);
     if (int st = check_dims(ctx, n_db, cols, d)) return st;
     const size_t db_bits = n_db * words * 8, q_bits = n_eyes * words * 8;
     IRL_CK(ctx, ctx->ws[0].ensure(2 * db_bits + 2 * q_bits));
@@ -317,7 +346,7 @@ int irl_iris_db_create(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db
     e->ctx = ctx;
     e->n_db = n_db;
     e->d = d;
-    e->ldk = round16(d);
+    e->ldk = plane_ldk(d);
     e->max_cols = max_cols;
     const size_t words = (d + 63) / 64, db_bits = n_db * words * 8;
     uint64_t* staging = nullptr;
@@ -377,7 +406,7 @@ int irl_iris_db_create_file(irl_ctx* ctx, const char* path, size_t max_cols, irl
     e->ctx = ctx;
     e->n_db = n;
     e->d = d;
-    e->ldk = round16(d);
+    e->ldk = plane_ldk(d);
     e->max_cols = max_cols;
     const size_t words = (d + 63) / 64;
     uint8_t* staging = nullptr;
@@ -389,7 +418,8 @@ int irl_iris_db_create_file(irl_ctx* ctx, const char* path, size_t max_cols, irl
     if (err == cudaSuccess) err = cudaMemcpyAsync(staging, host, 2 * plane_bytes, cudaMemcpyHostToDevice, ctx->stream);
     if (err == cudaSuccess) {
         const size_t total = n * (e->ldk / 16);
-        iris_file_planes_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, ctx->stream>>>(
+        auto kern = iris_f4() ? iris_file_planes_kernel<true> : iris_file_planes_kernel<false>;
+        kern<<<static_cast<unsigned>((total + 255) / 256), 256, 0, ctx->stream>>>(
             staging, staging + plane_bytes, static_cast<uint32_t>(d), static_cast<uint32_t>(n),
             static_cast<uint32_t>(e->ldk), e->planes);
         err = cudaGetLastError();

@@ -22,6 +22,13 @@ constexpr int kModeInner = 1;
 // into the epilogue (score = acc1 / acc2 in IEEE double, match bits and the
 // first match / first empty overlap per eye; see IrisMatchOut).
 constexpr int kModeIrisMatch = 2;
+// The same two modes on the block-scaled FP4 tensor path: planes are packed
+// e2m1 nibbles (2 per byte, K in bytes = ceil(d / 2)), tcgen05.mma
+// kind::mxf4.block_scale with unit UE8M0 scales, FP32 accumulators (exact for
+// the ternary / mask products below 2^24), 240-column tiles (the scale factors
+// take TMEM columns 240..255). Twice the int8 rate, half the operand bytes.
+constexpr int kModeInnerF4 = 3;
+constexpr int kModeIrisMatchF4 = 4;
 
 struct IrisMatchOut {
     double lo = 0, hi = 0;      // the P interval

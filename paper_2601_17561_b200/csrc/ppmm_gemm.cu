@@ -75,6 +75,9 @@ constexpr int kEpiGroups = kEpiWarps / 4;
 constexpr int kNumThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kAcc2Col = 256;
+constexpr uint32_t kF4TileN = 240;   // FP4 modes: accumulator columns 0..239 and 256..495
+constexpr uint32_t kF4SfaCol = 240;  // unit scale factors (0x7F bytes) for A ...
+constexpr uint32_t kF4SfbCol = 248;  // ... and B, in both CTAs' TMEM
 constexpr size_t kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 constexpr uint32_t kGateLead = 48;                // max K blocks a pair may lead its group (swept: 6..96)
 constexpr long long kGateSpinCycles = 200000;     // then proceed ungated (forward progress)
@@ -144,6 +147,7 @@ struct TileCoord {
 // streams through once per n-chunk. A tile is (unit, m-block within the unit,
 // n-tile within the chunk). Tiles past N (padding of the last chunk) get
 // n_size 32 and store nothing.
+template <uint32_t kTileN = kMaxTileN, uint32_t kNAlign = 32>
 __device__ __forceinline__ TileCoord decode(const GemmArgs& a, uint32_t unit, uint32_t mb_sub,
                                             uint32_t nb) {
     TileCoord t;
@@ -154,10 +158,10 @@ __device__ __forceinline__ TileCoord decode(const GemmArgs& a, uint32_t unit, ui
     t.part = rest % a.parts;
     t.prime = rest / a.parts;
     t.m0 = (mu * a.unit_mblocks + mb_sub) * 2 * kRowsPerCta;
-    t.n0 = (nc * a.chunk_tiles + nb) * kMaxTileN;
+    t.n0 = (nc * a.chunk_tiles + nb) * kTileN;
     const uint32_t rem = a.N > t.n0 ? a.N - t.n0 : 1u;
-    const uint32_t ns = rem < kMaxTileN ? rem : kMaxTileN;
-    t.n_size = (ns + 31u) & ~31u;  // cta_group::2 kind::i8 needs N % 32 == 0
+    const uint32_t ns = rem < kTileN ? rem : kTileN;
+    t.n_size = (ns + kNAlign - 1) & ~(kNAlign - 1);  // cta_group::2: kind::i8 N % 32, kind::mxf4 N % 16
     return t;
 }
 
@@ -222,6 +226,11 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     uint32_t* ring_tile = reinterpret_cast<uint32_t*>(ring_empty + kRing);  // [kRing][2]
     uint32_t* tmem_base_slot = ring_tile + 2 * kRing;
 
+    constexpr bool kF4 = kMode == kModeInnerF4 || kMode == kModeIrisMatchF4;
+    constexpr bool kInner = kMode == kModeInner || kMode == kModeInnerF4;
+    constexpr bool kMatch = kMode == kModeIrisMatch || kMode == kModeIrisMatchF4;
+    constexpr uint32_t kTileN = kF4 ? kF4TileN : kMaxTileN;
+    constexpr uint32_t kNAlign = kF4 ? 16u : 32u;
     const uint32_t warp = threadIdx.x / 32;
     const uint32_t lane = threadIdx.x % 32;
     const uint32_t rank = ptx::cluster_ctarank();
@@ -248,6 +257,19 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
     if (warp == 1) {
         ptx::tmem_alloc_pair(ptx::smem_u32(tmem_base_slot), kTmemCols);
+    }
+    if constexpr (kF4) {
+        // every byte of the scale-factor columns = 2^0 (UE8M0 127): one
+        // epilogue warp per TMEM lane quarter writes them after the alloc
+        ptx::tc_fence_before();
+        __syncthreads();
+        ptx::tc_fence_after();
+        if (warp >= 2 && warp < 6) {
+            const uint32_t lb = *tmem_base_slot + (((warp % 4) * 32u) << 16);
+            for (uint32_t c = kF4SfaCol; c < kAcc2Col; c += 4) ptx::tmem_st_32x32b_x4(lb + c, 0x7F7F7F7Fu);
+            for (uint32_t c = kAcc2Col + kF4TileN; c < kTmemCols; c += 4) ptx::tmem_st_32x32b_x4(lb + c, 0x7F7F7F7Fu);
+            ptx::tmem_st_wait();
+        }
     }
     ptx::tc_fence_before();
     ptx::cluster_sync();
@@ -325,7 +347,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                     const uint32_t mb_sub = (t / tiles_per_unit) * kPM + pm;
                     const uint32_t nb = (grp.solo ? r : grp.member) * kPN + pn;
                     push_tile(u, mb_sub, nb);
-                    const TileCoord tc = decode(args, u, mb_sub, nb);
+                    const TileCoord tc = decode<kTileN, kNAlign>(args, u, mb_sub, nb);
                     const uint32_t a_row0 = tc.part * args.a_part_rows + tc.prime * 2 * args.M +
                                             tc.m0 + half_rank * kRowsPerCta;
                     const uint32_t half_n = tc.n_size / 2;
@@ -445,8 +467,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                                  ptx::smem_u32(&ring_empty[slot]))
                              : "memory");
                 if (u == kEnd) break;
-                const TileCoord tc = decode(args, u, nbm >> 16, nbm & 0xFFFFu);
-                const uint32_t idesc = ptx::idesc_i8(2 * kRowsPerCta, tc.n_size);
+                const TileCoord tc = decode<kTileN, kNAlign>(args, u, nbm >> 16, nbm & 0xFFFFu);
+                const uint32_t idesc = kF4 ? ptx::idesc_mxf4(2 * kRowsPerCta, tc.n_size)
+                                           : ptx::idesc_i8(2 * kRowsPerCta, tc.n_size);
                 // Wait until the epilogue of the previous tile drained TMEM.
                 timed_wait(tmem_empty_bar, (j & 1) ^ 1, diag, w_tmem);
                 ptx::tc_fence_after();
@@ -464,7 +487,14 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                         const uint64_t dy1 =
                             ptx::smem_desc_k_sw128(st + 3 * kPlaneTileBytes + koff);
                         const uint32_t accum = (kb | k) != 0;
-                        if constexpr (kMode != kModePsq) {
+                        if constexpr (kF4) {
+                            // the same two products on packed e2m1 operands (64 k per 32 B)
+                            ptx::mma_mxf4_pair(acc1, dx0, dy0, idesc, accum, tmem_base + kF4SfaCol,
+                                               tmem_base + kF4SfbCol);
+                            ptx::mma_mxf4_pair(acc2, dx1, dy1, idesc, accum, tmem_base + kF4SfaCol,
+                                               tmem_base + kF4SfbCol);
+                            continue;
+                        } else if constexpr (kMode != kModePsq) {
                             // two independent products: acc1 = X0 Y0, acc2 = X1 Y1
                             ptx::mma_i8_pair(acc1, dx0, dy0, idesc, accum);
                             ptx::mma_i8_pair(acc2, dx1, dy1, idesc, accum);
@@ -521,7 +551,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                                  ptx::smem_u32(&ring_empty[slot]))
                              : "memory");
             if (u == kEnd) break;
-            const TileCoord tc = decode(args, u, nbm >> 16, nbm & 0xFFFFu);
+            const TileCoord tc = decode<kTileN, kNAlign>(args, u, nbm >> 16, nbm & 0xFFFFu);
             const ModConst mc = args.mc[tc.prime];
             timed_wait(tmem_full_bar, j & 1, diag, w_epi);
             const long long e0 = clock64();
@@ -540,7 +570,14 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                 ptx::tmem_ld_32x32b_x16(lane_base + c, a1);
                 ptx::tmem_ld_32x32b_x16(lane_base + kAcc2Col + c, a2);
                 ptx::tmem_ld_wait();
-                if constexpr (kMode == kModeIrisMatch) {
+                if constexpr (kF4) {  // FP32 accumulators of exact integers
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) {
+                        a1[jj] = static_cast<uint32_t>(__float2int_rn(__uint_as_float(a1[jj])));
+                        a2[jj] = static_cast<uint32_t>(__float2int_rn(__uint_as_float(a2[jj])));
+                    }
+                }
+                if constexpr (kMatch) {
                     // score = inner / overlap per (column, template); per column,
                     // the warp's 32 templates fold their first match / first
                     // empty overlap into one atomicMin per eye
@@ -624,7 +661,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                     continue;
                 }
                 if (!row_ok) continue;
-                if constexpr (kMode == kModeInner) {
+                if constexpr (kInner) {
                     const size_t base = tc.part * args.out_part + static_cast<size_t>(tc.prime) * args.N * args.M +
                                         static_cast<size_t>(tc.n0 + c) * args.M + m;
                     for (int jj = 0; jj < 16; ++jj) {
@@ -752,6 +789,20 @@ KernelFn kernel_for(int si, int mode = kModePsq) {
         }
         return nullptr;
     }
+    if (mode == kModeInnerF4) {
+        switch (si) {
+            case 0: return ppmm_i8_sm100_kernel<1, 1, kModeInnerF4>;
+            case 2: return ppmm_i8_sm100_kernel<1, 4, kModeInnerF4>;
+            default: return nullptr;
+        }
+    }
+    if (mode == kModeIrisMatchF4) {
+        switch (si) {
+            case 0: return ppmm_i8_sm100_kernel<1, 1, kModeIrisMatchF4>;
+            case 2: return ppmm_i8_sm100_kernel<1, 4, kModeIrisMatchF4>;
+            default: return nullptr;
+        }
+    }
     if (mode == kModeIrisMatch) {
         switch (si) {
             case 0: return ppmm_i8_sm100_kernel<1, 1, kModeIrisMatch>;
@@ -864,7 +915,8 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     args.parts = L.parts;
     args.nprimes = L.nprimes;
     args.m_blocks = (L.M + 2 * kRowsPerCta - 1) / (2 * kRowsPerCta);
-    args.n_blocks = (L.N + kMaxTileN - 1) / kMaxTileN;
+    const uint32_t tile_n = (L.mode == kModeInnerF4 || L.mode == kModeIrisMatchF4) ? kF4TileN : kMaxTileN;
+    args.n_blocks = (L.N + tile_n - 1) / tile_n;
 
     int dev = 0;
     cudaGetDevice(&dev);
@@ -922,7 +974,7 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     args.out_i32[0] = L.out_i32[0];
     args.out_i32[1] = L.out_i32[1];
     if (L.mode != kModePsq && L.accumulate) return cudaErrorInvalidValue;
-    if (L.mode == kModeIrisMatch && (L.parts != 1 || L.nprimes != 1 || L.iris.rho == 0 ||
+    if ((L.mode == kModeIrisMatch || L.mode == kModeIrisMatchF4) && (L.parts != 1 || L.nprimes != 1 || L.iris.rho == 0 ||
                                      static_cast<uint64_t>(L.iris.rho) * L.M >= 0xFFFFFFFFull))
         return cudaErrorInvalidValue;
     args.iris = L.iris;

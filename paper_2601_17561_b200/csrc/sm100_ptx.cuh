@@ -207,6 +207,25 @@ __device__ __forceinline__ void mma_i8_pair(uint32_t d_tmem, uint64_t a_desc, ui
         : "memory");
 }
 
+// Block-scaled FP4 product for the pair: D (fp32) (+)= A * B^T with packed
+// e2m1 operands (64 k per 32 B of a K-major row) and per-32-k UE8M0 scale
+// factors read from TMEM at sfa / sfb.
+__device__ __forceinline__ void mma_mxf4_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                              uint32_t accumulate, uint32_t sfa_tmem, uint32_t sfb_tmem) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa_tmem), "r"(sfb_tmem)
+        : "memory");
+}
+
+// 32 lanes x 4 consecutive 32-bit columns, every one set to v.
+__device__ __forceinline__ void tmem_st_32x32b_x4(uint32_t taddr, uint32_t v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %1, %1, %1};" ::"r"(taddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 // Arrive (once) on the mbarrier at the same smem offset in every CTA of
 // `cta_mask` when all previously issued tcgen05.mma of this thread finish.
 __device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t cta_mask) {
@@ -274,6 +293,12 @@ __device__ __forceinline__ uint64_t smem_desc_k_sw64(uint32_t smem_addr) {
 // memory every GPU bound to the multicast object.
 __device__ __forceinline__ void multimem_st_b32(void* mc_addr, uint32_t v) {
     asm volatile("multimem.st.relaxed.sys.global.b32 [%0], %1;" ::"l"(mc_addr), "r"(v) : "memory");
+}
+
+// Block-scaled instruction descriptor: A/B e2m1 (MXF4 format 1), UE8M0
+// scales, K-major, dense K = 64, FP32 accumulate (implied).
+__host__ __device__ constexpr uint32_t idesc_mxf4(uint32_t m, uint32_t n) {
+    return (1u << 7) | (1u << 10) | ((n >> 3) << 17) | (1u << 23) | ((m >> 4) << 24);
 }
 
 // Instruction descriptor: kind::i8, signed A/B, S32 accumulate, K-major A/B.
