@@ -43,6 +43,7 @@ def test_library_is_sm100a_cuda(lib):
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", str(lib._name)], capture_output=True, text=True).stdout
     assert "UTCIMMA" in sass  # tcgen05.mma kind::i8
+    assert "UTCOMMA" in sass  # tcgen05.mma kind::mxf4.block_scale (iris products on FP4)
     assert "UTMALDG" in sass  # TMA tile loads
     assert "LDTM" in sass     # tcgen05.ld (TMEM -> registers)
 
