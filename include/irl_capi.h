@@ -272,7 +272,8 @@ int irl_ccmm_full(irl_ccmm_group* g, const uint16_t* q_res_host, size_t n, uint1
  * ceil(d/64); code and mask planes separate. The query side is n_eyes
  * templates; column c = e*rho + r of the query batch is rotate(q_e, r)
  * (iris_core.cpp:65-76), as in pipeline::prepare (pipeline.cpp:121-138).
- * Both sums are int8 GEMMs on the tensor cores (PPMM kernel, inner mode).
+ * Both sums are tensor-core GEMMs (PPMM kernel): e2m1 operands on the
+ * block-scaled FP4 path, exact in FP32 accumulation (int8 with IRL_IRIS_I8=1).
  *
  * inner[c][j]   = <to_masked(q_c), to_masked(db_j)>    (iris_core.cpp:37-51)
  * overlap[c][j] = |m_q(c) AND m_db(j)|                  (overlap_count, pipeline.cpp:78-82;
@@ -364,7 +365,7 @@ int irl_fold_stage_device(irl_ctx* ctx, const irl_fold_params* p, const int32_t*
 /* The whole post-CCMM path of run_alg2 against a registered template
  * database: prepare's products and overlaps of the query eyes
  * (p->batch = n_eyes, the database's n_db and template length = p->n_db and
- * p->d; ShapeMismatch otherwise, pipeline.cpp:100-118) as int8 GEMMs, then
+ *  p->d; ShapeMismatch otherwise, pipeline.cpp:100-118) as tensor-core GEMMs, then
  * the fold stage on the device; only folded / refolded leave it. */
 int irl_iris_db_fold(irl_iris_db* e, const uint64_t* q_code, const uint64_t* q_mask, const irl_fold_params* p,
                      double* folded, double* refolded, int32_t* assumption_ok);

@@ -1,7 +1,7 @@
 // C++ host mirror of the reference's irislab::iris scoring API
 // (/root/reference/proj/include/irislab/iris_core.hpp) with every score
 // computed on the B200: the inner products <a', b'> and mask overlaps of a
-// whole query batch are two int8 GEMMs on the tensor cores (C ABI
+// whole query batch are two exact GEMMs on the FP4 tensor cores (C ABI
 // irl_iris_inner_overlap / irl_iris_match, csrc/iris.cu). Template handling
 // (to_masked, rotate, synth_db, pad_to) is host bookkeeping, as in the
 // reference. Same names, value semantics and exception types.
@@ -107,7 +107,7 @@ struct FoldMessages {
 FoldMessages fold_stage(const FoldConfig& cfg, const std::vector<int32_t>& inner,
                         const std::vector<int32_t>& overlap, bool want_refolded = true);
 
-/// From templates: prepare's products and overlaps as int8 GEMMs, then the
+/// From templates: prepare's products and overlaps as tensor-core GEMMs, then the
 /// fold stage, without leaving the device (irl_iris_db_fold).
 FoldMessages fold_stage(const FoldConfig& cfg, const std::vector<iris::IrisTemplate>& queries,
                         const std::vector<iris::IrisTemplate>& db, bool want_refolded = true);

@@ -197,7 +197,7 @@ class IrisDatabase:
     def fold_packed(self, q_code, q_mask, n_eyes: int, cfg, want_folded: bool = True,
                     want_refolded: Optional[bool] = None):
         """run_alg2's post-CCMM stage against this database (irl_iris_db_fold):
-        products and overlaps of the query eyes' rotations as int8 GEMMs, then
+        products and overlaps of the query eyes' rotations as tensor-core GEMMs (FP4), then
         the fold stage (fold.py) on the device. cfg: fold.FoldConfig with
         cfg.d == the template length and n_db == len(db)."""
         import ctypes as C
