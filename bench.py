@@ -482,6 +482,45 @@ def measure_fold(R):
                     f"{fold_k}; exact IEEE double, FP64/issue-bound (DESIGN.md 3)"}
 
 
+def measure_iris(R):
+    """The plaintext scoring stage on the same query geometry (f4, csrc/iris.cu):
+    a registered database of the 7 * 2^14 b-part templates (d = 2^14), the
+    eyes x rotations batch, match bits out; the ternary / mask products run on
+    the block-scaled FP4 tensor path. Host wall clock per call (query bits in,
+    match bits out), median of 10."""
+    args, rank, M = R.args, R.rank, R.M
+    if rank != 0:
+        return None
+    import os as _os
+
+    from paper_2601_17561_b200.iris import IrisDatabase, Interval
+    d = 1 << 14
+    n_db = max(1, (args.parts - 1) * M // d) * d
+    eyes, rho = args.eyes, args.rot
+    rng = np.random.default_rng(5)
+    words = d // 64
+    bits = lambda n: rng.integers(0, 1 << 63, size=(n, words), dtype=np.uint64)  # noqa: E731
+    dc, dm, qc, qm = bits(n_db), bits(n_db) | bits(n_db), bits(eyes), bits(eyes) | bits(eyes)
+    db = IrisDatabase.from_packed(dc, dm, d, eyes * rho)
+    try:
+        for _ in range(3):
+            db.match_packed(qc, qm, eyes, rho, Interval(0.35, 1.0))
+        ts = []
+        for _ in range(10):
+            t0 = time.perf_counter()
+            db.match_packed(qc, qm, eyes, rho, Interval(0.35, 1.0))
+            ts.append((time.perf_counter() - t0) * 1e3)
+    finally:
+        db.close()
+    ms = statistics.median(ts)
+    ops = 4.0 * n_db * eyes * rho * d  # two products, 2 ops per multiply-add
+    return {"stage": "irl_iris_db_match (registered database, host buffers)", "ms": ms,
+            "effective_tops": ops / (ms * 1e-3) / 1e12, "n_db": n_db, "columns": eyes * rho, "d": d,
+            "tensor_path": "int8 (IRL_IRIS_I8)" if _os.environ.get("IRL_IRIS_I8") else
+                           "FP4 e2m1, tcgen05 kind::mxf4.block_scale, unit scales, FP32 accumulate (exact)",
+            "note": "not part of the CCMM step"}
+
+
 def measure_int8(R):
     """Live library comparison: cuBLASLt int8 GEMM on this box."""
     args, torch, rank = R.args, R.torch, R.rank
@@ -707,6 +746,7 @@ def main():
     dist_check = measure_dist_check(R)
     cpu = measure_cpu(R)
     fold = measure_fold(R)
+    iris = measure_iris(R)
     int8_ref = measure_int8(R)
 
     if rank == 0:
@@ -727,7 +767,8 @@ def main():
                                                        if "bf16_tflops" in peaks else None),
                              "frac_of_live_cublas_int8": (achieved / int8_ref["sustained_tops"]
                                                           if int8_ref else None)},
-                "split_roofline": split_roof, "moddown": moddown, "fold_stage": fold, "int8_library_ref": int8_ref,
+                "split_roofline": split_roof, "moddown": moddown, "fold_stage": fold, "iris_stage": iris,
+                "int8_library_ref": int8_ref,
                 "exchange": None if world == 1 else {
                     "kind": "fused P2P stores in the a-part PPMM epilogue (CUDA IPC, NVLink)" if exchange == "mirror"
                     else "NCCL broadcast after the local GEMMs", "note": exch_note,
