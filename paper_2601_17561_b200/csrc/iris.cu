@@ -46,6 +46,19 @@ bool iris_f4() {
 size_t plane_kbytes(size_t d) { return iris_f4() ? (d + 1) / 2 : d; }
 size_t plane_ldk(size_t d) { return round16(plane_kbytes(d)); }
 
+// Column split of the FP4 query batch. A 1 x 4 cluster covers four 240-column
+// tiles (960 columns) per pass over the database; a remainder (992 = 960 + 32
+// for the paper's batch) would cost a second, mostly padding pass of the
+// whole cluster, so it runs as its own launch on plain pairs. Returns the
+// columns of the main launch, 0 = no split.
+size_t col_split(size_t cols) {
+    if (!iris_f4() || std::getenv("IRL_IRIS_NO_SPLIT")) return 0;
+    const size_t pass = 4 * kF4TileCols;
+    const size_t main = cols / pass * pass;
+    return main > 0 && main < cols ? main : 0;
+}
+
+
 // One entry of a plane row into the 16-byte chunk being assembled: int8
 // value t / mask mb at position j, or their e2m1 nibbles (+1 = 0x2, -1 = 0xA).
 template <bool kF4>
@@ -67,13 +80,14 @@ __device__ __forceinline__ void put_entry(uint32_t (&v)[4], uint32_t (&w)[4], in
 // as int8, 32 as e2m1 nibbles, low nibble first).
 template <bool kF4>
 __global__ void iris_planes_kernel(const uint64_t* __restrict__ code, const uint64_t* __restrict__ mask,
-                                   uint32_t words, uint32_t d, uint32_t rho, uint32_t cols, uint32_t ldk,
-                                   int8_t* __restrict__ planes) {
+                                   uint32_t words, uint32_t d, uint32_t rho, uint32_t c0, uint32_t cols,
+                                   uint32_t ldk, int8_t* __restrict__ planes) {
     constexpr int kPer = kF4 ? 32 : 16;
     const uint32_t chunks = ldk / 16;
     const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (tid >= static_cast<size_t>(cols) * chunks) return;
-    const uint32_t c = static_cast<uint32_t>(tid / chunks);
+    const uint32_t cl = static_cast<uint32_t>(tid / chunks);  // column within [c0, c0 + cols)
+    const uint32_t c = c0 + cl;
     const uint32_t chunk = static_cast<uint32_t>(tid % chunks);
     const uint32_t k0 = chunk * kPer;
     const uint32_t e = c / rho, r = c % rho % d;
@@ -90,7 +104,7 @@ __global__ void iris_planes_kernel(const uint64_t* __restrict__ code, const uint
         const uint32_t mb = static_cast<uint32_t>((__ldg(mw + (i >> 6)) >> (i & 63)) & 1u);
         put_entry<kF4>(v, w, j, static_cast<int32_t>(mb) - 2 * static_cast<int32_t>(cb & mb), mb);
     }
-    const size_t o = static_cast<size_t>(c) * ldk + chunk * 16;
+    const size_t o = static_cast<size_t>(cl) * ldk + chunk * 16;
     *reinterpret_cast<uint4*>(planes + o) = make_uint4(v[0], v[1], v[2], v[3]);
     *reinterpret_cast<uint4*>(planes + static_cast<size_t>(cols) * ldk + o) = make_uint4(w[0], w[1], w[2], w[3]);
 }
@@ -128,36 +142,60 @@ __global__ void iris_file_planes_kernel(const uint8_t* __restrict__ code, const 
 // [2][cols][ldk]) into inner / overlap [cols][n_db].
 int inner_overlap_gemm(irl_ctx* ctx, const int8_t* xp, const int8_t* yp, size_t n_db, size_t cols, size_t d,
                        size_t ldk, int32_t* inner, int32_t* ovl, uint32_t* progress, cudaStream_t s) {
-    PpmmLaunch L;
-    L.mode = iris_f4() ? kModeInnerF4 : kModeInner;
-    L.a_planes = xp;
-    L.b_planes = yp;
-    L.out_i32[0] = inner;
-    L.out_i32[1] = ovl;
-    L.M = static_cast<uint32_t>(n_db);
-    L.N = static_cast<uint32_t>(cols);
-    L.K = static_cast<uint32_t>(plane_kbytes(d));
-    L.ldk = static_cast<uint32_t>(ldk);
-    L.parts = 1;
-    L.nprimes = 1;
-    L.mc[0] = make_modconst(2, 1);  // unused by kModeInner
-    L.progress = progress;
-    IRL_LAUNCH(ctx, launch_ppmm_planes(L, s));
-    ctx->launches += ppmm_kernels_last_launch() > 1 ? ppmm_kernels_last_launch() - 1 : 0;  // + filler
+    // one launch per column range of build_query_planes (see col_split)
+    const size_t split = col_split(cols);
+    const size_t ranges[2][2] = {{0, split ? split : cols}, {split, split ? cols - split : 0}};
+    for (const auto& rg : ranges) {
+        const size_t c0 = rg[0], nc = rg[1];
+        if (nc == 0) continue;
+        PpmmLaunch L;
+        L.mode = iris_f4() ? kModeInnerF4 : kModeInner;
+        L.a_planes = xp;
+        L.b_planes = yp + 2 * c0 * ldk;
+        L.out_i32[0] = inner ? inner + c0 * n_db : nullptr;
+        L.out_i32[1] = ovl ? ovl + c0 * n_db : nullptr;
+        L.M = static_cast<uint32_t>(n_db);
+        L.N = static_cast<uint32_t>(nc);
+        L.K = static_cast<uint32_t>(plane_kbytes(d));
+        L.ldk = static_cast<uint32_t>(ldk);
+        L.parts = 1;
+        L.nprimes = 1;
+        L.mc[0] = make_modconst(2, 1);  // unused by the inner modes
+        L.progress = progress;
+        if (c0 > 0) L.cluster_pm = L.cluster_pn = 1;  // the remainder on plain pairs
+        IRL_LAUNCH(ctx, launch_ppmm_planes(L, s));
+        ctx->launches += ppmm_kernels_last_launch() > 1 ? ppmm_kernels_last_launch() - 1 : 0;  // + filler
+    }
+    return IRL_OK;
+}
+
+// Planes [2][ncols][ldk] of query columns [c0, c0 + ncols) (column c =
+// e * rho + r is rotate(t_e, r)); the database is the case rho = 1.
+int build_planes_range(irl_ctx* ctx, const uint64_t* code, const uint64_t* mask, size_t rho, size_t d, size_t c0,
+                       size_t ncols, int8_t* planes, cudaStream_t s) {
+    const size_t words = (d + 63) / 64, ldk = plane_ldk(d);
+    const size_t total = ncols * (ldk / 16);
+    if (total == 0) return IRL_OK;
+    auto kern = iris_f4() ? iris_planes_kernel<true> : iris_planes_kernel<false>;
+    kern<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
+        code, mask, static_cast<uint32_t>(words), static_cast<uint32_t>(d), static_cast<uint32_t>(rho),
+        static_cast<uint32_t>(c0), static_cast<uint32_t>(ncols), static_cast<uint32_t>(ldk), planes);
+    IRL_LAUNCH(ctx, cudaGetLastError());
     return IRL_OK;
 }
 
 int build_planes(irl_ctx* ctx, const uint64_t* code, const uint64_t* mask, size_t n, size_t rho, size_t d,
                  int8_t* planes, cudaStream_t s) {
-    const size_t words = (d + 63) / 64, ldk = plane_ldk(d), cols = n * rho;
-    const size_t total = cols * (ldk / 16);
-    if (total == 0) return IRL_OK;
-    auto kern = iris_f4() ? iris_planes_kernel<true> : iris_planes_kernel<false>;
-    kern<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
-        code, mask, static_cast<uint32_t>(words), static_cast<uint32_t>(d), static_cast<uint32_t>(rho),
-        static_cast<uint32_t>(cols), static_cast<uint32_t>(ldk), planes);
-    IRL_LAUNCH(ctx, cudaGetLastError());
-    return IRL_OK;
+    return build_planes_range(ctx, code, mask, rho, d, 0, n * rho, planes, s);
+}
+
+// Query planes, laid out per launch: [2][main][ldk] then [2][rest][ldk].
+int build_query_planes(irl_ctx* ctx, const uint64_t* code, const uint64_t* mask, size_t n_eyes, size_t rho,
+                       size_t d, int8_t* planes, cudaStream_t s) {
+    const size_t cols = n_eyes * rho, split = col_split(cols);
+    if (!split) return build_planes_range(ctx, code, mask, rho, d, 0, cols, planes, s);
+    if (int st = build_planes_range(ctx, code, mask, rho, d, 0, split, planes, s)) return st;
+    return build_planes_range(ctx, code, mask, rho, d, split, cols - split, planes + 2 * split * plane_ldk(d), s);
 }
 
 // Scoring fused into the GEMM (kModeIrisMatch): the epilogue divides,
@@ -177,26 +215,36 @@ int match_fused(irl_ctx* ctx, const int8_t* xp, const int8_t* yp, size_t n_db, s
     double* dsc = scores ? reinterpret_cast<double*>(ws.as<uint8_t>() + off_sc) : nullptr;
     IRL_CK(ctx, cudaMemsetAsync(first, 0xFF, 8 * n_eyes, s));
     IRL_CK(ctx, cudaMemsetAsync(dbits, 0, nbits, s));
-    PpmmLaunch L;
-    L.mode = iris_f4() ? kModeIrisMatchF4 : kModeIrisMatch;
-    L.a_planes = xp;
-    L.b_planes = yp;
-    L.M = static_cast<uint32_t>(n_db);
-    L.N = static_cast<uint32_t>(cols);
-    L.K = static_cast<uint32_t>(plane_kbytes(d));
-    L.ldk = static_cast<uint32_t>(ldk);
-    L.parts = 1;
-    L.nprimes = 1;
-    L.mc[0] = make_modconst(2, 1);  // unused
-    L.progress = progress;
-    L.iris.lo = p_lo;
-    L.iris.hi = p_hi;
-    L.iris.rho = static_cast<uint32_t>(rho);
-    L.iris.bits = dbits;
-    L.iris.first = first;
-    L.iris.scores = dsc;
-    IRL_LAUNCH(ctx, launch_ppmm_planes(L, s));
-    ctx->launches += ppmm_kernels_last_launch() > 1 ? ppmm_kernels_last_launch() - 1 : 0;  // + filler
+    // one launch per column range of build_query_planes (see col_split); the
+    // launches fold into the same first-event indices and match bits
+    const size_t split = col_split(cols);
+    const size_t ranges[2][2] = {{0, split ? split : cols}, {split, split ? cols - split : 0}};
+    for (const auto& rg : ranges) {
+        const size_t c0 = rg[0], nc = rg[1];
+        if (nc == 0) continue;
+        PpmmLaunch L;
+        L.mode = iris_f4() ? kModeIrisMatchF4 : kModeIrisMatch;
+        L.a_planes = xp;
+        L.b_planes = yp + 2 * c0 * ldk;
+        L.M = static_cast<uint32_t>(n_db);
+        L.N = static_cast<uint32_t>(nc);
+        L.K = static_cast<uint32_t>(plane_kbytes(d));
+        L.ldk = static_cast<uint32_t>(ldk);
+        L.parts = 1;
+        L.nprimes = 1;
+        L.mc[0] = make_modconst(2, 1);  // unused
+        L.progress = progress;
+        if (c0 > 0) L.cluster_pm = L.cluster_pn = 1;  // the remainder on plain pairs
+        L.iris.lo = p_lo;
+        L.iris.hi = p_hi;
+        L.iris.rho = static_cast<uint32_t>(rho);
+        L.iris.col0 = static_cast<uint32_t>(c0);
+        L.iris.bits = dbits;
+        L.iris.first = first;
+        L.iris.scores = dsc;
+        IRL_LAUNCH(ctx, launch_ppmm_planes(L, s));
+        ctx->launches += ppmm_kernels_last_launch() > 1 ? ppmm_kernels_last_launch() - 1 : 0;  // + filler
+    }
     std::vector<uint32_t> h(2 * n_eyes);
     IRL_CK(ctx, cudaMemcpyAsync(h.data(), first, 8 * n_eyes, cudaMemcpyDeviceToHost, s));
     if (match_bits) IRL_CK(ctx, cudaMemcpyAsync(match_bits, dbits, nbits, cudaMemcpyDeviceToHost, s));
@@ -247,7 +295,7 @@ int inner_overlap_device(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* 
     int8_t* xp = ctx->ws[1].as<int8_t>();
     int8_t* yp = ctx->ws[2].as<int8_t>();
     if (int st = build_planes(ctx, dc, dm, n_db, 1, d, xp, s)) return st;
-    if (int st = build_planes(ctx, qc, qm, n_eyes, rho, d, yp, s)) return st;
+    if (int st = build_query_planes(ctx, qc, qm, n_eyes, rho, d, yp, s)) return st;
     int32_t* inner = ctx->ws[3].as<int32_t>();
     int32_t* ovl = inner + cols * n_db;
     if (int st = inner_overlap_gemm(ctx, xp, yp, n_db, cols, d, ldk, inner, ovl, ctx->d_progress, s)) return st;
@@ -329,7 +377,7 @@ int irl_iris_match(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db_mas
     IRL_CK(ctx, copy_h2d(ctx, qc, q_code, q_bits, s));
     IRL_CK(ctx, copy_h2d(ctx, qm, q_mask, q_bits, s));
     if (int st = build_planes(ctx, dc, dm, n_db, 1, d, ctx->ws[1].as<int8_t>(), s)) return st;
-    if (int st = build_planes(ctx, qc, qm, n_eyes, rho, d, ctx->ws[2].as<int8_t>(), s)) return st;
+    if (int st = build_query_planes(ctx, qc, qm, n_eyes, rho, d, ctx->ws[2].as<int8_t>(), s)) return st;
     return match_fused(ctx, ctx->ws[1].as<int8_t>(), ctx->ws[2].as<int8_t>(), n_db, n_eyes, rho, d, ldk, p_lo, p_hi,
                        match_bits, eye_result, scores, ctx->ws[4], ctx->d_progress, s);
 }
@@ -468,7 +516,7 @@ int irl_iris_db_match(irl_iris_db* e, const uint64_t* q_code, const uint64_t* q_
     const size_t words = (e->d + 63) / 64, qb = n_eyes * words * 8;
     IRL_CK(ctx, cudaMemcpyAsync(e->qbits, q_code, qb, cudaMemcpyHostToDevice, s));
     IRL_CK(ctx, cudaMemcpyAsync(e->qbits + n_eyes * words, q_mask, qb, cudaMemcpyHostToDevice, s));
-    if (int st = build_planes(ctx, e->qbits, e->qbits + n_eyes * words, n_eyes, rho, e->d, e->qplanes, s)) return st;
+    if (int st = build_query_planes(ctx, e->qbits, e->qbits + n_eyes * words, n_eyes, rho, e->d, e->qplanes, s)) return st;
     return match_fused(ctx, e->planes, e->qplanes, e->n_db, n_eyes, rho, e->d, e->ldk, p_lo, p_hi, match_bits,
                        eye_result, scores, e->match_ws, e->progress, s);
 }
@@ -501,7 +549,7 @@ int irl_iris_db_fold(irl_iris_db* e, const uint64_t* q_code, const uint64_t* q_m
     auto* dflags = reinterpret_cast<uint32_t*>(ws + off_flags);
     IRL_CK(ctx, cudaMemcpyAsync(e->qbits, q_code, qb, cudaMemcpyHostToDevice, s));
     IRL_CK(ctx, cudaMemcpyAsync(e->qbits + n_eyes * words, q_mask, qb, cudaMemcpyHostToDevice, s));
-    if (int st = build_planes(ctx, e->qbits, e->qbits + n_eyes * words, n_eyes, rho, e->d, e->qplanes, s)) return st;
+    if (int st = build_query_planes(ctx, e->qbits, e->qbits + n_eyes * words, n_eyes, rho, e->d, e->qplanes, s)) return st;
     if (int st = inner_overlap_gemm(ctx, e->planes, e->qplanes, e->n_db, cols, e->d, e->ldk, inner, ovl, e->progress, s))
         return st;
     IRL_CK(ctx, cudaMemsetAsync(dflags, 0, 8, s));

@@ -28,12 +28,14 @@ constexpr int kModeIrisMatch = 2;
 // the ternary / mask products below 2^24), 240-column tiles (the scale factors
 // take TMEM columns 240..255). Twice the int8 rate, half the operand bytes.
 constexpr int kModeInnerF4 = 3;
+constexpr uint32_t kF4TileCols = 240;  // N of one FP4 tile
 constexpr int kModeIrisMatchF4 = 4;
 
 struct IrisMatchOut {
     double lo = 0, hi = 0;      // the P interval
     float lo_in = 0, lo_out = 0, hi_in = 0, hi_out = 0;  // float screens lo +- eps, hi -+ eps (set by the launcher)
     uint32_t rho = 1;           // query column c = eye * rho + rotation
+    uint32_t col0 = 0;          // global index of this launch's column 0 (column-split launches)
     uint8_t* bits = nullptr;    // [eyes][M] (zeroed by the caller), nullable
     uint32_t* first = nullptr;  // [eyes][2]: min rotation * M + m of a match / of an empty overlap (0xFF.. init)
     double* scores = nullptr;   // [N][M], NaN where the overlap is empty; nullable

@@ -75,7 +75,7 @@ constexpr int kEpiGroups = kEpiWarps / 4;
 constexpr int kNumThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kAcc2Col = 256;
-constexpr uint32_t kF4TileN = 240;   // FP4 modes: accumulator columns 0..239 and 256..495
+constexpr uint32_t kF4TileN = kF4TileCols;  // FP4 modes: accumulator columns 0..239 and 256..495
 constexpr uint32_t kF4SfaCol = 240;  // unit scale factors (0x7F bytes) for A ...
 constexpr uint32_t kF4SfbCol = 248;  // ... and B, in both CTAs' TMEM
 constexpr size_t kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
@@ -585,7 +585,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                     for (int jj = 0; jj < 16; ++jj) {
                         const uint32_t col = tc.n0 + c + jj;
                         if (col >= args.N) break;  // uniform across the warp
-                        const uint32_t eye = col / io.rho, rot = col % io.rho;
+                        const uint32_t gcol = col + io.col0;  // global query column
+                        const uint32_t eye = gcol / io.rho, rot = gcol % io.rho;
                         const int32_t inner = static_cast<int32_t>(a1[jj]), ov = static_cast<int32_t>(a2[jj]);
                         uint32_t cm = 0xFFFFFFFFu, cz = 0xFFFFFFFFu;
                         if (row_ok) {
@@ -593,7 +594,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                             if (ov == 0) {
                                 cz = lin;
                                 if (io.scores)
-                                    io.scores[static_cast<size_t>(col) * args.M + m] =
+                                    io.scores[static_cast<size_t>(gcol) * args.M + m] =
                                         __longlong_as_double(0x7FF8000000000000ll);
                             } else {
                                 // iris_core.cpp:58, IEEE double division. A float
@@ -610,7 +611,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                                 } else {
                                     const double sc = __ddiv_rn(static_cast<double>(inner), static_cast<double>(ov));
                                     hit = sc >= io.lo && sc <= io.hi;  // Interval::contains
-                                    if (io.scores) io.scores[static_cast<size_t>(col) * args.M + m] = sc;
+                                    if (io.scores) io.scores[static_cast<size_t>(gcol) * args.M + m] = sc;
                                 }
                                 if (hit) {
                                     cm = lin;
