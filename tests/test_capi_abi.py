@@ -82,3 +82,22 @@ def test_no_device_fails_loudly(lib):
     from paper_2601_17561_b200 import modmat
     with pytest.raises(modmat.DeviceError):
         modmat.Context(0)
+
+
+def test_fold_params_struct_layout_matches_header(tmp_path):
+    """capi.FoldParams (ctypes) has the size and field offsets the C compiler
+    gives irl_fold_params."""
+    import ctypes as C
+
+    from paper_2601_17561_b200 import capi
+    fields = [f for f, _ in capi.FoldParams._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stddef.h>\n#include <stdio.h>\n#include "irl_capi.h"\nint main(void) {\n'
+                   '    printf("%zu", sizeof(irl_fold_params));\n' +
+                   "".join(f'    printf(" %zu", offsetof(irl_fold_params, {f}));\n' for f in fields) +
+                   "    return 0;\n}\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["/usr/bin/gcc", "-std=c11", f"-I{ROOT / 'include'}", str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    assert got[0] == C.sizeof(capi.FoldParams)
+    assert got[1:] == [getattr(capi.FoldParams, f).offset for f in fields]
