@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-rows", type=int, default=32, help="DB rows per task in the CPU sample")
+    ap.add_argument("--cpu-rows", type=int, default=32, help="DB rows per (part, modulus) task in the CPU sample")
     ap.add_argument("--no-int8-ref", action="store_true", help="skip the live cuBLASLt int8 comparison")
     ap.add_argument("--exchange", choices=["auto", "mirror", "broadcast"], default="auto",
                     help="a-part exchange at N>1: fused P2P epilogue stores (mirror, validated in warm-up, "
@@ -140,22 +140,61 @@ class Clocks:
 # CPU reference leg (oracle/_ref = unmodified reference modmat.cpp; else the port)
 # ---------------------------------------------------------------------------
 
-def cpu_reference_sample(args, moduli, q_host=None, rows=None, threads=None, parts=None):
+def host_cpu():
+    """Host CPU model and the threads this process may use (lscpu)."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:  # noqa: BLE001
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except Exception:  # noqa: BLE001
+        usable = os.cpu_count() or 1
+    return {"model": model, "threads_usable": usable, "cpu_count": os.cpu_count()}
+
+
+def loaded_repo_libs():
+    """Shared objects under this repo mapped into the process (evidence of
+    which native code ran)."""
+    libs = set()
+    try:
+        for ln in open("/proc/self/maps"):
+            f = ln.split()
+            if len(f) >= 6 and f[-1].endswith(".so") and str(ROOT) in os.path.realpath(f[-1]):
+                libs.add(os.path.relpath(os.path.realpath(f[-1]), os.path.realpath(ROOT)))
+    except OSError:
+        pass
+    return sorted(libs)
+
+
+def query_residues_oracle(K, N, moduli):
+    """The step's query residues [nmod][K][N] from the oracle's copy of the
+    counter generator (seed 2, stream 0xFF; identical to ccmm.synth_query), so
+    the reference arm never loads the product library."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as ol
+    return np.stack([ol.synth_block(2, 0xFF, i, 0, K, 0, N, m) for i, m in enumerate(moduli)])
+
+
+def cpu_reference_sample(args, moduli, q_host, rows=None, threads=None, parts=None):
     """Times the reference gemm_mod_psq (modmat.cpp:143-160) on a bounded sample
     of the same workload: `rows` DB rows x full K x all N query columns, for
-    every modulus of parts `parts`; tasks spread over host threads (the
-    function is pure). Returns rates in the bench's unit."""
+    every modulus of parts `parts` (one task per (part, modulus)); tasks spread
+    over host threads (the function is pure). Test
+    infrastructure only (tests/oracle_lib.py -> oracle/_ref, else the port)."""
     import ctypes as C
     sys.path.insert(0, str(ROOT / "tests"))
     import oracle_lib as ol
 
     rows = rows or args.cpu_rows
-    threads = threads or os.cpu_count() or 1
-    parts = parts if parts is not None else tuple(range(min(2, args.parts)))
+    threads = threads or host_cpu()["threads_usable"]
+    parts = tuple(parts) if parts is not None else tuple(range(args.parts))
     K, N = args.k, args.eyes * args.rot
-    if q_host is None:
-        from paper_2601_17561_b200.ccmm import synth_query
-        q_host = synth_query(2, K, N, moduli)
     kind = "reference" if ol.ref_available() else "port"
     A, B, Cc, P = [], [], [], []
     for part in parts:
@@ -191,34 +230,43 @@ def cpu_reference_sample(args, moduli, q_host=None, rows=None, threads=None, par
 
 
 def run_reference_arm(args):
+    """The reference's own CPU implementation (oracle/_ref: unmodified
+    modmat.cpp gemm_mod_psq) on the box's host cores, same metric/config. Loads
+    only oracle/ libraries (never the product package). Each step samples
+    args.cpu_rows DB rows of two parts (rotating over the 8) x every modulus."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2601_17561_b200.modmat import build_paper_basis
-    b = build_paper_basis()
-    moduli = [m.value() for m in b.moduli]
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as ol
+    pr, ex = ol.paper_basis()
+    moduli = [int(p) ** int(e) for p, e in zip(pr, ex)]
     N = args.eyes * args.rot
     total_ops = 6.0 * len(moduli) * args.rows * N * args.k * args.parts
-    sys.path.insert(0, str(ROOT / "tests"))
-    from paper_2601_17561_b200.ccmm import synth_query  # host-side generator only
-    q = synth_query(2, args.k, N, moduli)
-    rates = []
+    q = query_residues_oracle(args.k, N, moduli)
+    rates, secs = [], []
     last = None
     for it in range(args.warmup + args.steps):
-        r = cpu_reference_sample(args, moduli, q_host=q, rows=max(8, args.cpu_rows // 2))
+        parts = [(2 * it + j) % args.parts for j in range(min(2, args.parts))]
+        r = cpu_reference_sample(args, moduli, q, parts=parts)
         if it >= args.warmup:
             rates.append(r["tops"])
+            secs.append(r["seconds"])
         last = r
     v = statistics.median(rates)
-    ms = total_ops / (v * 1e12) * 1e3
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "int32 (int8 digits)", "data": "synthetic",
+            "warmup": args.warmup, "ms_per_step": statistics.mean(secs) * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32 (int8 digits)", "data": "synthetic",
             "impl": "reference",
             "config": config_dict(args, len(moduli)),
-            "ccmm_latency_ms": ms,
+            "step_definition": "one bounded CPU sample (see cpu_baseline.sample); ms_per_step is its measured time",
+            "ccmm_latency_ms_extrapolated": total_ops / (v * 1e12) * 1e3,
+            "host_cpu": host_cpu(),
+            "loaded_repo_libs": loaded_repo_libs(),
+            "product_package_imported": "paper_2601_17561_b200" in sys.modules,
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": last["threads"], "kind": last["kind"],
-                             "sample": last["sample"]},
+                             "sample": last["sample"].replace(f"parts {list(last['parts'])}",
+                                                              "2 parts per step (rotating over all)")},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -420,6 +468,8 @@ def measure_cpu(R):
                 j += 1
         cpu = {"value": r["tops"], "unit": UNIT, "cores": r["threads"], "kind": r["kind"],
                "sample": r["sample"], "seconds": r["seconds"], "bit_exact_vs_gpu": exact,
+               "bit_exact_parts": list(r["parts"]), "bit_exact_rows_per_part": r["rows"],
+               "host_cpu": host_cpu(),
                "extrapolated_ccmm_latency_s": total_ops / (r["tops"] * 1e12)}
     return cpu
 

@@ -200,11 +200,14 @@ int irl_ccmm_buffers(irl_ccmm* e, void** qres, void** out);
  * Validates exactly like ccmm_twin (ShapeMismatch for non-positive dims,
  * d1 % n_db, d2 % n_qry, slot output without ci; ModulusBudget for
  * db_bits < 2 q_bits - delta and out_level outside [0, top_level]) and
- * computes the exact product db (d1 x d2) . qry (d2 x d3) of integer-valued
- * doubles on the PPMM engine (residues mod a prefix of the paper basis, centred
- * CRT on device). msgs receives the d1*d3/n_db output ciphertext messages in
- * ccmm_twin's order: msgs[(c*(d1/n_db) + b)*n_db + i] = prod[(b*n_db + i)*d3 + c].
- * IRL_ERR_UNSUPPORTED if an entry is not an integer or |product| could reach 2^53. */
+ * computes the product db (d1 x d2) . qry (d2 x d3) bit-identical to the
+ * reference's double loop (emulator.cpp:411-421): integer-valued operands with
+ * K max|db| max|qry| < 2^52 (every partial sum exact) on the int8 tensor-core
+ * PPMM (residues mod a prefix of the paper basis, centred CRT on device); any
+ * other doubles (fractions, larger magnitudes, inf/NaN) on an FP64 kernel that
+ * replays the loop's rounded multiply and add per k in order, skipping zero
+ * database entries. msgs receives the d1*d3/n_db output ciphertext messages in
+ * ccmm_twin's order: msgs[(c*(d1/n_db) + b)*n_db + i] = prod[(b*n_db + i)*d3 + c]. */
 int irl_ccmm_twin(irl_ctx* ctx, long d1, long d2, long d3, long n_db, long n_qry,
                   double db_modulus_bits, double qry_modulus_bits, double scale_bits,
                   int out_level, int top_level, int out_slot_encoding, int out_ci,

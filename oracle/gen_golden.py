@@ -8,6 +8,7 @@ where /root/reference is absent (the GPU box). Test infrastructure only.
 
     python oracle/gen_golden.py              (everything)
     python oracle/gen_golden.py --fold-only  (tests/golden/fold_stage.npz)
+    python oracle/gen_golden.py --digests    (tests/golden/c1_crit2_digests.json)
 """
 from __future__ import annotations
 
@@ -305,9 +306,83 @@ def gen_fold():
     np.savez_compressed(GOLDEN / "fold_stage.npz", **out)
 
 
+C1_P, C1_M, C1_K, C1_N = 127, 256, 4096, 4096
+
+
+def c1_inputs():
+    """BASELINE configs[0]: uniform residues mod 127^2 from the counter
+    generator (seed 1: A = stream 0, B = stream 1)."""
+    m = C1_P * C1_P
+    a = ol.synth_block(1, 0, 0, 0, C1_M, 0, C1_K, m).astype(np.int32)
+    b = ol.synth_block(1, 1, 0, 0, C1_K, 0, C1_N, m).astype(np.int32)
+    return a, b
+
+
+def ref_gemm_mod_psq_threaded(a, b, p, threads=16):
+    """The unmodified reference gemm_mod_psq (modmat.cpp:143-160) on row blocks
+    of A spread over host threads (the function is pure)."""
+    import ctypes as C
+    R = ol.ref()
+    m, k = a.shape
+    n = b.shape[1]
+    rows = max(1, m // threads)
+    A = [np.ascontiguousarray(a[r:r + rows]) for r in range(0, m, rows)]
+    assert all(x.shape[0] == rows for x in A)
+    B = [b] * len(A)
+    Cc = [np.zeros((rows, n), np.int32) for _ in A]
+    arr = lambda xs: (ol.i32p * len(xs))(*[x.ctypes.data_as(ol.i32p) for x in xs])  # noqa: E731
+    st = R.ref_gemm_mod_psq_batch(arr(A), arr(B), arr(Cc), (C.c_uint32 * len(A))(*([p] * len(A))), len(A),
+                                  rows, k, n, threads)
+    assert st == 0, R.ref_last_error()
+    return np.concatenate(Cc)
+
+
+def gen_digests():
+    """c1 (BASELINE configs[0]) output digest, and acceptance criterion 2
+    (acceptance.cpp:96-120) in full: all 1000 instances of the
+    gmp_randclass(seed 2) stream, the reference's gemm_mod_Q output of each
+    checked against its oracle_gemm_mod_Q, as sha256 digests of the inputs
+    and outputs."""
+    out = {}
+    a, b = c1_inputs()
+    c = ref_gemm_mod_psq_threaded(a, b, C1_P)
+    out["c1"] = {"p": C1_P, "m": C1_M, "k": C1_K, "n": C1_N, "inputs": "ol.synth_block(1, 0|1, 0, ...) mod 127^2",
+                 "a_sha256": hashlib.sha256(a.tobytes()).hexdigest(),
+                 "b_sha256": hashlib.sha256(b.tobytes()).hexdigest(),
+                 "c_sha256": hashlib.sha256(c.tobytes()).hexdigest(),
+                 "c_rows16_sha256": hashlib.sha256(c[:16].tobytes()).hexdigest(),
+                 "c_head": c[0, :8].tolist(), "c_tail": c[-1, -8:].tolist()}
+    primes, exps = ol.paper_basis()
+    width = ol.width_of(ol.basis_Q(primes, exps))
+    R = ol.ref()
+    R.ref_crit2_reset()
+    inst = []
+    abuf = np.zeros((64 * 64, width), np.uint8)
+    bbuf = np.zeros((64 * 64, width), np.uint8)
+    for idx in range(1000):
+        m_, k_, n_ = ol.sz(), ol.sz(), ol.sz()
+        R.ref_crit2_next(m_, k_, n_, ol.ptr(abuf, ol.u8p), ol.ptr(bbuf, ol.u8p), width)
+        m, kk, nn = m_.value, k_.value, n_.value
+        a_ = abuf[: m * kk].copy()
+        b_ = bbuf[: kk * nn].copy()
+        c_ = ref_gemm_mod_Q(a_, b_, m, kk, nn, width, primes, exps)
+        c2 = np.zeros_like(c_)
+        R.ref_oracle_gemm_mod_Q(ol.ptr(a_, ol.u8p), ol.ptr(b_, ol.u8p), ol.ptr(c2, ol.u8p), m, kk, nn,
+                                width, ol.ptr(primes, ol.u32p), ol.ptr(exps, ol.u32p), len(primes))
+        assert (c_ == c2).all(), idx  # criterion 2 itself, on the reference
+        inst.append([m, kk, nn, hashlib.sha256(a_.tobytes() + b_.tobytes()).hexdigest()[:32],
+                     hashlib.sha256(c_.tobytes()).hexdigest()[:32]])
+    out["crit2"] = {"width": width, "fields": ["m", "k", "n", "sha256(A||B)[:32]", "sha256(C)[:32]"],
+                    "instances": inst}
+    (GOLDEN / "c1_crit2_digests.json").write_text(json.dumps(out, separators=(",", ":")))
+    print("c1", out["c1"]["c_sha256"], "crit2", len(inst))
+
+
 if __name__ == "__main__":
     import sys as _sys
-    if "--iris-only" in _sys.argv:
+    if "--digests" in _sys.argv:
+        gen_digests()
+    elif "--iris-only" in _sys.argv:
         gen_iris_scores()
     elif "--fold-only" in _sys.argv:
         gen_fold()

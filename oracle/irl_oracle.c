@@ -478,6 +478,23 @@ uint32_t orc_synth_residue(uint64_t seed, uint32_t stream, uint32_t plane, uint3
     return (uint32_t)(((x >> 32) * (uint64_t)m) >> 32);
 }
 
+/* emulator.cpp:411-421 (built with -ffp-contract=off, like the reference's
+ * baseline x86-64 build: a * q and the += round separately). */
+void orc_ccmm_twin_product(const double* db, const double* qry, size_t d1, size_t d2, size_t d3, double* out) {
+    double* prow = (double*)malloc((d3 ? d3 : 1) * sizeof(double));
+    for (size_t i = 0; i < d1; ++i) {
+        for (size_t j = 0; j < d3; ++j) prow[j] = 0.0;
+        for (size_t k = 0; k < d2; ++k) {
+            const double a = db[i * d2 + k];
+            if (a == 0.0) continue;
+            const double* qrow = qry + k * d3;
+            for (size_t j = 0; j < d3; ++j) prow[j] += a * qrow[j];
+        }
+        for (size_t j = 0; j < d3; ++j) out[j * d1 + i] = prow[j];
+    }
+    free(prow);
+}
+
 void orc_synth_block(uint64_t seed, uint32_t stream, uint32_t plane, uint32_t row0,
                      uint32_t nrows, uint32_t col0, uint32_t ncols, uint32_t m, uint16_t* out) {
     for (uint32_t r = 0; r < nrows; ++r)

@@ -63,6 +63,12 @@ void orc_ppmm_rows_direct(const uint16_t* a, size_t lda, const uint16_t* bt, siz
  * uniform in [0, m) keyed by (seed, stream, plane, row, col). */
 uint32_t orc_synth_residue(uint64_t seed, uint32_t stream, uint32_t plane, uint32_t row,
                            uint32_t col, uint32_t m);
+/* Emulator::ccmm_twin's product (emulator.cpp:411-421): i-k-j loop over
+ * row-major doubles, zero database entries skipped, each multiply and add
+ * rounded (no contraction); written transposed, out[j*d1 + i], which is
+ * ccmm_twin's message order. */
+void orc_ccmm_twin_product(const double* db, const double* qry, size_t d1, size_t d2, size_t d3, double* out);
+
 void orc_synth_block(uint64_t seed, uint32_t stream, uint32_t plane, uint32_t row0,
                      uint32_t nrows, uint32_t col0, uint32_t ncols, uint32_t m,
                      uint16_t* out /* [nrows][ncols] */);

@@ -466,6 +466,39 @@ int ref_fold_stage(size_t batch, size_t rho, size_t n_db, size_t d, size_t fold_
     }
 }
 
+// Emulator::ccmm_twin (emulator.cpp:389-447) itself, noise-free default
+// emulator: msgs receives its outputs' real parts in output order
+// (d1*d3/n_db ciphertexts of n_db slots). top_level = the chain's top level.
+int ref_ccmm_twin(long d1, long d2, long d3, long n_db, long n_qry, double db_bits, double q_bits,
+                  double scale_bits, int out_level, int out_slot, int out_ci, const double* db,
+                  const double* qry, double* msgs, int* top_level) {
+    try {
+        emu::Emulator em(pipe::default_emulator_config());
+        *top_level = em.config().chain.top_level();
+        emu::CcmmSpec spec;
+        spec.d1 = d1;
+        spec.d2 = d2;
+        spec.d3 = d3;
+        spec.n_db = n_db;
+        spec.n_qry = n_qry;
+        spec.db_modulus_bits = db_bits;
+        spec.qry_modulus_bits = q_bits;
+        spec.scale_bits = scale_bits;
+        spec.out_level = out_level;
+        spec.out_encoding = out_slot ? emu::Encoding::Slot : emu::Encoding::Coeff;
+        spec.out_ci = out_ci != 0;
+        const std::vector<double> a(db, db + (d1 > 0 && d2 > 0 ? d1 * d2 : 0));
+        const std::vector<double> b(qry, qry + (d2 > 0 && d3 > 0 ? d2 * d3 : 0));
+        const auto out = em.ccmm_twin(spec, a, b);
+        size_t k = 0;
+        for (const auto& ct : out)
+            for (const auto& m : ct.message) msgs[k++] = m.real();
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
 // ps_execute on scalars through the emulator's ring (one slot), for the
 // polynomial unit checks.
 int ref_ps_execute(const double* coeffs, size_t n, double x, double* out) {

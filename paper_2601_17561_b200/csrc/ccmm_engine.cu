@@ -750,6 +750,44 @@ int irl_ccmm_twin(irl_ctx* ctx, long d1, long d2, long d3, long n_db, long n_qry
     if (d1 >= (1l << 30) || d2 >= (1l << 30) || d3 >= (1l << 30))
         return set_err(ctx, IRL_ERR_UNSUPPORTED, "ccmm: dimension above 2^30");
     const size_t M = size_t(d1), K = size_t(d2), N = size_t(d3);
+    // Route: integer-valued operands whose partial sums stay below 2^52 in
+    // magnitude (every partial sum of the reference's double loop is then an
+    // exact integer, so its result is the exact product) run on the int8
+    // tensor-core PPMM; anything else runs the ordered FP64 kernel, which
+    // replays the reference loop's IEEE operations one for one.
+    double amax = 0, bmax = 0;
+    bool integral = true;
+    for (size_t i = 0; i < M * K; ++i) {
+        const double v = db[i];
+        integral = integral && v == std::nearbyint(v);
+        amax = std::max(amax, std::fabs(v));
+    }
+    for (size_t i = 0; i < K * N; ++i) {
+        const double v = qry[i];
+        integral = integral && v == std::nearbyint(v);
+        bmax = std::max(bmax, std::fabs(v));
+    }
+    const double bound = double(K) * amax * bmax;
+    if (!integral || !(bound < 4503599627370496.0)) {  // 2^52 (NaN / inf land here too)
+        size_t off = 0;
+        auto take = [&](size_t bytes) {
+            const size_t o = off;
+            off = (off + bytes + 127) / 128 * 128;
+            return o;
+        };
+        const size_t o_db = take(M * K * 8), o_q = take(K * N * 8), o_out = take(N * M * 8);
+        IRL_CK(ctx, ctx->ws[0].ensure(off));
+        uint8_t* base = ctx->ws[0].as<uint8_t>();
+        double* ddb = reinterpret_cast<double*>(base + o_db);
+        double* dq = reinterpret_cast<double*>(base + o_q);
+        double* dout = reinterpret_cast<double*>(base + o_out);
+        IRL_CK(ctx, copy_h2d(ctx, ddb, db, M * K * 8, ctx->stream));
+        IRL_CK(ctx, copy_h2d(ctx, dq, qry, K * N * 8, ctx->stream));
+        IRL_LAUNCH(ctx, launch_ordered_dgemm_t(ddb, dq, uint32_t(M), uint32_t(K), uint32_t(N), dout, ctx->stream));
+        IRL_CK(ctx, copy_d2h(ctx, msgs, dout, N * M * 8, ctx->stream));
+        IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
+        return IRL_OK;
+    }
     // Device buffers: inputs, residues, planes, output residues, doubles.
     // Paper-basis prefix with Q > 2 * bound, Q < 2^64 (<= 4 moduli).
     uint32_t P[64], E[64];
@@ -772,16 +810,9 @@ int irl_ccmm_twin(irl_ctx* ctx, long d1, long d2, long d3, long n_db, long n_qry
     IRL_CK(ctx, copy_h2d(ctx, ddb, db, M * K * 8, ctx->stream));
     IRL_CK(ctx, copy_h2d(ctx, dq, qry, K * N * 8, ctx->stream));
     IRL_CK(ctx, cudaMemsetAsync(dbad, 0, 4, ctx->stream));
-    // Modulus count: |product| <= K max|db| max|qry| must stay inside the
-    // centred range of Q (validation of the host inputs' magnitudes only;
-    // integrality is checked on device by the residue kernel).
+    // Modulus count: |product| <= K max|db| max|qry| < 2^52 must stay inside
+    // the centred range of Q.
     ModTable mt{};
-    double amax = 0, bmax = 0;
-    for (size_t i = 0; i < M * K; ++i) amax = std::max(amax, std::fabs(db[i]));
-    for (size_t i = 0; i < K * N; ++i) bmax = std::max(bmax, std::fabs(qry[i]));
-    const double bound = double(K) * amax * bmax;
-    if (bound >= 4503599627370496.0)  // 2^52: keep the centred result exact in double
-        return set_err(ctx, IRL_ERR_UNSUPPORTED, "ccmm: |product| may exceed 2^52");
     uint32_t nm = 1;
     double q = double(P[0]) * P[0];
     while (q <= 2.0 * bound + 1.0 && nm < 4) {
@@ -797,7 +828,7 @@ int irl_ccmm_twin(irl_ctx* ctx, long d1, long d2, long d3, long n_db, long n_qry
     int bad = 0;
     IRL_CK(ctx, cudaMemcpyAsync(&bad, dbad, 4, cudaMemcpyDeviceToHost, ctx->stream));
     IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
-    if (bad) return set_err(ctx, IRL_ERR_UNSUPPORTED, "ccmm: messages must be integers below 2^53");
+    if (bad) return set_err(ctx, IRL_ERR_CUDA, "ccmm: residue conversion rejected a checked integer entry");
     int8_t* pa = reinterpret_cast<int8_t*>(base + o_pa);
     int8_t* pb = reinterpret_cast<int8_t*>(base + o_pb);
     IRL_LAUNCH(ctx, launch_split_rows<uint16_t>(ra, K, M * K, uint32_t(M), uint32_t(K), mt, pa, ldk, nullptr, ctx->stream));

@@ -224,6 +224,10 @@ int mc_setup(irl_ccmm_group* g, size_t bytes) {
 int setup_exchange(irl_ccmm_group* g, size_t n) {
     if (g->recv_n == n) return IRL_OK;
     irl_ctx* c0 = g->ctx[0];
+    // invalidate first: a rebuild that fails part way must be retried by the
+    // next call, never mistaken for a ready exchange of the old width
+    g->recv_n = 0;
+    g->mode = IRL_EXCHANGE_COPY;
     irl_ccmm_set_mirror_ptrs(g->eng[0], 0, n, nullptr, 0);
     irl_ccmm_set_mirror_multicast(g->eng[0], 0, 0, nullptr);
     mc_release(&g->mcx);

@@ -850,6 +850,52 @@ cudaError_t launch_crt_centred_double(const uint16_t* res, uint32_t M, uint32_t 
     return cudaGetLastError();
 }
 
+// 32 rows (one per lane) x 32 columns per block; each thread keeps 4 column
+// accumulators. K is walked in 32-wide shared-memory tiles, strictly in order,
+// with explicitly rounded multiplies and adds (the reference's loop body
+// `prow[j] += a * qrow[j]`, which baseline x86-64 never contracts).
+__global__ void __launch_bounds__(256) ordered_dgemm_t_kernel(const double* __restrict__ a,
+                                                              const double* __restrict__ q, uint32_t M,
+                                                              uint32_t K, uint32_t N, double* __restrict__ out) {
+    __shared__ double as[32][33];  // [k][i]
+    __shared__ double qs[32][32];  // [k][j]
+    const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const uint32_t i = blockIdx.x * 32 + tx;
+    const uint32_t j0 = blockIdx.y * 32 + ty * 4;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (uint32_t k0 = 0; k0 < K; k0 += 32) {
+        for (uint32_t e = threadIdx.x; e < 32 * 32; e += 256) {
+            const uint32_t r = e >> 5, c = e & 31;  // a: row r of the tile, column k0 + c
+            const uint32_t gi = blockIdx.x * 32 + r, gk = k0 + c;
+            as[c][r] = (gi < M && gk < K) ? a[size_t(gi) * K + gk] : 0.0;
+            const uint32_t qk = k0 + r, qj = blockIdx.y * 32 + c;
+            qs[r][c] = (qk < K && qj < N) ? q[size_t(qk) * N + qj] : 0.0;
+        }
+        __syncthreads();
+        const uint32_t kn = min(32u, K - k0);
+        for (uint32_t kk = 0; kk < kn; ++kk) {
+            const double av = as[kk][tx];
+            if (!(av == 0.0)) {  // emulator.cpp:415: `if (a == 0.0) continue;`
+#pragma unroll
+                for (int r = 0; r < 4; ++r) acc[r] = __dadd_rn(acc[r], __dmul_rn(av, qs[kk][ty * 4 + r]));
+            }
+        }
+        __syncthreads();
+    }
+    if (i < M)
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+            if (j0 + r < N) out[size_t(j0 + r) * M + i] = acc[r];
+}
+
+cudaError_t launch_ordered_dgemm_t(const double* a, const double* q, uint32_t M, uint32_t K, uint32_t N,
+                                   double* out, cudaStream_t s) {
+    if (M == 0 || N == 0) return cudaSuccess;
+    const dim3 grid((M + 31) / 32, (N + 31) / 32);
+    ordered_dgemm_t_kernel<<<grid, 256, 0, s>>>(a, q, M, K, N, out);
+    return cudaGetLastError();
+}
+
 uint32_t synth_residue_host(uint64_t seed, uint32_t stream, uint32_t plane, uint32_t row,
                             uint32_t col, uint32_t m) {
     return synth_residue(mix64(seed), stream, plane, row, col, m);

@@ -126,6 +126,14 @@ struct Crt64Table {
 cudaError_t launch_crt_centred_double(const uint16_t* res, uint32_t M, uint32_t N,
                                       const Crt64Table& t, double* out, cudaStream_t s);
 
+// Emulator::ccmm_twin's product for arbitrary doubles, in the reference's own
+// IEEE operation order (emulator.cpp:411-421): for each output (i, j), k runs
+// 0..K-1 and acc = RN(acc + RN(a[i][k] * q[k][j])), skipping a[i][k] == 0.0;
+// no fused multiply-add. Output transposed, out[j][i] (ccmm_twin's
+// column-major message order).
+cudaError_t launch_ordered_dgemm_t(const double* a, const double* q, uint32_t M, uint32_t K, uint32_t N,
+                                   double* out, cudaStream_t s);
+
 // Host mirror of the device generator.
 uint32_t synth_residue_host(uint64_t seed, uint32_t stream, uint32_t plane, uint32_t row,
                             uint32_t col, uint32_t m);

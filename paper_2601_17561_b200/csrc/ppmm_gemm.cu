@@ -239,6 +239,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     const uint32_t half_rank = rank & 1;      // CTA within the pair
     const bool leader = half_rank == 0;       // pair leader (issues the MMAs)
     const uint32_t cluster_id = blockIdx.x / kCtas;
+    // The filler launch (same stream, programmatic stream serialization) may
+    // start on the SMs this grid leaves free as soon as every CTA got here.
+    ptx::griddep_launch_dependents();
 
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmap_a);
@@ -738,6 +741,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         ptx::tc_fence_after();
         ptx::tmem_dealloc_pair(tmem_base, kTmemCols);
     }
+    // A filler grid ends only after the main grid it overlapped: the stream's
+    // next operation waits for the filler, so it then also follows the main
+    // grid (no-op in the main grid, which is an ordinary launch).
+    ptx::griddep_wait();
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
@@ -866,25 +873,6 @@ uint32_t max_active_clusters(int si, int dev) {
     return static_cast<uint32_t>(n);
 }
 
-// Per-device side stream + fork/join events for the filler launch.
-cudaError_t side_stream(int dev, cudaStream_t* s, cudaEvent_t* fork, cudaEvent_t* join) {
-    static std::mutex mu;
-    static cudaStream_t streams[64] = {};
-    static cudaEvent_t forks[64] = {}, joins[64] = {};
-    std::lock_guard<std::mutex> lk(mu);
-    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-    if (!streams[dev]) {
-        cudaError_t e = cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&forks[dev], cudaEventDisableTiming);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&joins[dev], cudaEventDisableTiming);
-        if (e != cudaSuccess) return e;
-    }
-    *s = streams[dev];
-    *fork = forks[dev];
-    *join = joins[dev];
-    return cudaSuccess;
-}
-
 }  // namespace
 
 size_t ppmm_smem_bytes() { return kSmemBytes; }
@@ -994,7 +982,7 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
 
     // Cluster layouts: the main launch uses the requested multi-pair shape;
     // those strand SMs (e.g. 132 of 148 CTAs with 4-CTA clusters on B200), so
-    // a 1x1 "filler" launch on a side stream takes the remaining SM pairs.
+    // a 1x1 "filler" launch (same stream, programmatic overlap) takes the remaining SM pairs.
     // Both pull units from the same counter.
     struct Part {
         int si;
@@ -1036,15 +1024,12 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     cudaError_t e = cudaMemsetAsync(L.progress, 0, scratch, stream);
     if (e != cudaSuccess) return e;
 
-    cudaStream_t side = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
-    if (nparts > 1) {
-        e = side_stream(dev, &side, &fork, &join);
-        if (e != cudaSuccess) return e;
-        e = cudaEventRecord(fork, stream);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(side, fork, 0);
-        if (e != cudaSuccess) return e;
-    }
+    // The filler (parts[1]) goes into the SAME stream right behind the main
+    // grid, with programmatic stream serialization: it starts once every main
+    // CTA has executed griddepcontrol.launch_dependents (their first
+    // instruction), so both grids share the unit counter from the start. No
+    // side stream: nothing else queued on the device (copies, other streams
+    // aliased onto the same hardware queue) can delay or reorder it.
     for (int i = 0; i < nparts; ++i) {
         const Part& pt = parts[i];
         GemmArgs a = args;
@@ -1069,14 +1054,16 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
         cfg.gridDim = dim3(static_cast<unsigned>(sh.ctas()) * pt.clusters);
         cfg.blockDim = dim3(kNumThreads);
         cfg.dynamicSmemBytes = kSmemBytes;
-        cfg.stream = i == 0 ? stream : side;
-        cudaLaunchAttribute attr[1];
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[2];
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = static_cast<unsigned>(sh.ctas());
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = i == 0 ? 1 : 2;
         KernelFn kfn = kernel_for(pt.si, L.mode);
         if (!kfn) return cudaErrorInvalidValue;
         if (L.mode != kModePsq) {
@@ -1088,10 +1075,6 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
         e = cudaLaunchKernelEx(&cfg, kfn, ma, mb, a);
         if (e != cudaSuccess) return e;
         ++g_last_kernels;
-    }
-    if (nparts > 1) {
-        e = cudaEventRecord(join, side);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, join, 0);
     }
     return e;
 }

@@ -58,6 +58,8 @@ def oracle() -> C.CDLL:
         lib.orc_gemm_mod_Q.argtypes = [u8p, u8p, u8p, sz, sz, sz, sz, u32p, u32p, sz]
         lib.orc_oracle_gemm_mod_Q.argtypes = [u8p, u8p, u8p, sz, sz, sz, sz, u32p, u32p, sz]
         lib.orc_ppmm_rows_direct.argtypes = [u16p, sz, u16p, sz, u32p, sz, sz, sz, C.c_uint32, u16p]
+        lib.orc_ccmm_twin_product.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double), sz, sz, sz,
+                                              C.POINTER(C.c_double)]
         lib.orc_synth_residue.restype = C.c_uint32
         lib.orc_synth_residue.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]
         lib.orc_iris_inner_overlap.argtypes = [u8p, u8p, sz, u8p, u8p, sz, sz, sz, i32p, i32p]
@@ -110,12 +112,40 @@ def ref() -> C.CDLL:
         lib.ref_match_db_reference.argtypes = [u8p, u8p, sz, u8p, u8p, sz, sz, C.c_double, C.c_double,
                                                C.c_double, C.c_double, C.POINTER(C.c_int)]
         lib.ref_ps_execute.argtypes = [f64p, sz, C.c_double, f64p]
+        lib.ref_ccmm_twin.argtypes = [C.c_long, C.c_long, C.c_long, C.c_long, C.c_long, C.c_double, C.c_double,
+                                      C.c_double, C.c_int, C.c_int, C.c_int, f64p, f64p, f64p, C.POINTER(C.c_int)]
         lib.ref_fold_stage.argtypes = [sz, sz, sz, sz, sz, f64p, sz, sz, f64p, C.POINTER(sz), f64p, i32p, i32p,
                                        f64p, f64p]
         lib.ref_alg2_assumption.argtypes = [u8p, u8p, sz, u8p, u8p, sz, sz, sz, sz, f64p, sz, sz, f64p,
                                             C.POINTER(sz), f64p, C.c_double, C.c_double, C.POINTER(C.c_int)]
         _ref = lib
     return _ref
+
+
+PIPE_SO = {"ref": ROOT / "oracle" / "_ref" / "libirl_pipe_ref.so",
+           "b200": ROOT / "oracle" / "_ref" / "libirl_pipe_b200.so"}
+_pipe = {}
+
+
+def pipe_available() -> bool:
+    return all(p.exists() for p in PIPE_SO.values())
+
+
+def pipe(kind: str) -> C.CDLL:
+    """The reference's end-to-end pipeline (oracle/pipe_capi.cpp over the
+    unmodified emulator/pipeline sources): kind "ref" = stock ccmm_twin,
+    "b200" = ccmm_twin's product from the B200 engine (link-time wrap)."""
+    if kind not in _pipe:
+        lib = C.CDLL(str(PIPE_SO[kind]))
+        lib.pipe_last_error.restype = C.c_char_p
+        lib.pipe_planted_small.argtypes = [i64p]
+        lib.pipe_instances.argtypes = [C.c_int, C.c_int, C.c_long, C.c_int, C.c_uint64, C.POINTER(C.c_double), sz,
+                                       i64p, sz]
+        lib.irl_hook_digest.restype = C.c_uint64
+        lib.irl_hook_calls.restype = C.c_long
+        lib.irl_hook_slots.restype = C.c_long
+        _pipe[kind] = lib
+    return _pipe[kind]
 
 
 # --------------------------------------------------------------------------
@@ -225,6 +255,48 @@ def orc_gemm_mod_Q(a_le, b_le, m, k, n, width, primes, exps):
     st = oracle().orc_gemm_mod_Q(ptr(a_le, u8p), ptr(b_le, u8p), ptr(c, u8p), m, k, n, width,
                                  ptr(primes, u32p), ptr(exps, u32p), len(primes))
     return st, c
+
+
+def orc_ccmm_twin_product(db: np.ndarray, qry: np.ndarray) -> np.ndarray:
+    """emulator.cpp:411-421 restated in C: db (d1 x d2) . qry (d2 x d3) in the
+    reference's operation order, returned in message order [d3][d1]."""
+    db = np.ascontiguousarray(db, np.float64)
+    qry = np.ascontiguousarray(qry, np.float64)
+    d1, d2 = db.shape
+    d3 = qry.shape[1]
+    out = np.zeros((d3, d1), np.float64)
+    f64p = C.POINTER(C.c_double)
+    oracle().orc_ccmm_twin_product(db.ctypes.data_as(f64p), qry.ctypes.data_as(f64p), d1, d2, d3,
+                                   out.ctypes.data_as(f64p))
+    return out
+
+
+def ref_ccmm_twin(db: np.ndarray, qry: np.ndarray, n_db: int, n_qry: int, db_bits=100.0, q_bits=50.0,
+                  scale=23.0, out_level=0, out_slot=0, out_ci=0):
+    """The reference's Emulator::ccmm_twin (noise-free default emulator):
+    (status, messages [d3][d1] real parts, chain top level)."""
+    db = np.ascontiguousarray(db, np.float64)
+    qry = np.ascontiguousarray(qry, np.float64)
+    d1, d2 = db.shape
+    d3 = qry.shape[1]
+    out = np.zeros((d3, d1), np.float64)
+    top = C.c_int(0)
+    f64p = C.POINTER(C.c_double)
+    st = ref().ref_ccmm_twin(d1, d2, d3, n_db, n_qry, db_bits, q_bits, scale, out_level, out_slot, out_ci,
+                             db.ctypes.data_as(f64p), qry.ctypes.data_as(f64p), out.ctypes.data_as(f64p),
+                             C.byref(top))
+    return st, out, top.value
+
+
+def twin_doubles(d1, d2, d3, seed):
+    """Non-integer operands exercising the rounding order: mixed magnitudes,
+    exact zeros and negative zeros in the database, an inf in the query."""
+    rng = np.random.default_rng(seed)
+    db = rng.standard_normal((d1, d2)) * np.exp2(rng.integers(-30, 30, (d1, d2)))
+    db[rng.random((d1, d2)) < 0.2] = 0.0
+    db[rng.random((d1, d2)) < 0.05] = -0.0
+    qry = rng.standard_normal((d2, d3)) * np.exp2(rng.integers(-20, 20, (d2, d3)))
+    return db, qry
 
 
 def synth_block(seed, stream, plane, row0, nrows, col0, ncols, m):

@@ -136,6 +136,59 @@ def test_acceptance_criterion2_instances():
         assert (got2.reshape(c.shape) == c).all(), i
 
 
+DIG = json.loads((ol.ROOT / "tests" / "golden" / "c1_crit2_digests.json").read_text())
+
+
+def test_oracle_c1_rows_match_reference_digest():
+    # BASELINE configs[0] (p = 127, 256 x 4096 . 4096 x 4096): the oracle's
+    # first 16 output rows equal the reference's (digest from oracle/_ref)
+    g = DIG["c1"]
+    m = 127 * 127
+    a = ol.synth_block(1, 0, 0, 0, 16, 0, 4096, m).astype(np.int32)
+    b = ol.synth_block(1, 1, 0, 0, 4096, 0, 4096, m).astype(np.int32)
+    assert hashlib.sha256(b.tobytes()).hexdigest() == g["b_sha256"]
+    st, c = ol.orc_gemm_mod_psq(a, b, 127)
+    assert st == 0 and c[0, :8].tolist() == g["c_head"]
+    assert hashlib.sha256(c.tobytes()).hexdigest() == g["c_rows16_sha256"]
+
+
+@pytest.mark.skipif(not ol.ref_available(), reason="oracle/_ref not built")
+def test_oracle_crit2_stream_matches_reference_digests():
+    # acceptance.cpp:96-120: the oracle's gemm_mod_Q on every 10th instance of
+    # the reference's own 1000-instance stream equals the reference's digest
+    R = ol.ref()
+    R.ref_crit2_reset()
+    abuf = np.zeros((64 * 64, W), np.uint8)
+    bbuf = np.zeros((64 * 64, W), np.uint8)
+    for idx, (m, k, n, in_dig, out_dig) in enumerate(DIG["crit2"]["instances"]):
+        m_, k_, n_ = ol.sz(), ol.sz(), ol.sz()
+        R.ref_crit2_next(m_, k_, n_, ol.ptr(abuf, ol.u8p), ol.ptr(bbuf, ol.u8p), W)
+        assert (m_.value, k_.value, n_.value) == (m, k, n)
+        if idx % 10:
+            continue
+        a, b = abuf[: m * k].copy(), bbuf[: k * n].copy()
+        assert hashlib.sha256(a.tobytes() + b.tobytes()).hexdigest()[:32] == in_dig
+        st, c = ol.orc_gemm_mod_Q(a, b, m, k, n, W, P, E)
+        assert st == 0 and hashlib.sha256(c.tobytes()).hexdigest()[:32] == out_dig, idx
+
+
+@pytest.mark.skipif(not ol.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("seed", [1, 2])
+def test_oracle_ccmm_twin_product_equals_reference_on_doubles(seed):
+    # emulator.cpp:411-421 on arbitrary doubles (fractions, 2^+-30 magnitude
+    # spread, +-0 database entries, an inf in the query): the C restatement
+    # reproduces the reference's messages bit for bit
+    d1, d2, d3, n_db = 64, 48, 6, 16
+    db, qry = ol.twin_doubles(d1, d2, d3, seed)
+    qry[3, 2] = np.inf             # +-inf in output column 2
+    db[0, 0], qry[0, 4] = np.inf, 0.0  # inf * 0 = NaN in output (0, 4)
+    st, want, _ = ol.ref_ccmm_twin(db, qry, n_db, 16)
+    assert st == 0
+    got = ol.orc_ccmm_twin_product(db, qry)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+    assert np.isnan(got[4, 0]) and np.isinf(got[2]).any()
+
+
 def test_ccmm_composition_on_iris_kat():
     # Our RGSW composition restatement on the reference's own iris inputs
     # (synth_db/to_masked/rotate): per-prime products of ternary matrices,
