@@ -213,24 +213,34 @@ int irl_ccmm_twin(irl_ctx* ctx, long d1, long d2, long d3, long n_db, long n_qry
                   int out_level, int top_level, int out_slot_encoding, int out_ci,
                   const double* db, const double* qry, double* msgs);
 /* ---- fused a-part exchange (replaces the NCCL broadcast) -----
- * Receivers allocate an engine-owned receive buffer [nmod][n][M] uint16 and
- * export its CUDA IPC handle (64 bytes); the owner of part `part` opens the
- * peers' handles, and from then on the epilogue of that part's PPMM stores
- * every output tile both locally and into each peer buffer (NVLink P2P
+ * Receivers allocate an engine-owned receive buffer of IRL_RECV_SLOTS slots
+ * [slot][nmod][n][M] uint16 and export its CUDA IPC handle (64 bytes); the
+ * owner of part `part` opens the peers' handles, and from then on the epilogue
+ * of that part's PPMM stores every output tile both locally and into slot
+ * `mirror_slot` (irl_ccmm_set_mirror_slot) of each peer buffer (NVLink P2P
  * stores, overlapped with the GEMM; a system-scope fence per tile). The data
  * is complete in a peer once the owner's launch has completed: order the
  * peers' reads after it with any cross-GPU signal (e.g. a tiny NCCL
- * all-reduce posted after the GEMM). Mirroring applies to device runs and
- * single-column-chunk e2e runs of width n; count 0 disables it. At most 7. */
+ * all-reduce posted after the GEMM). Alternating the slot per step makes the
+ * buffer double-buffered: step s+1 writes the other slot while peers still
+ * read step s, and step s+2 may overwrite slot s once every peer has posted
+ * its step-(s+1) signal after consuming step s. Mirroring applies to device
+ * runs and single-column-chunk e2e runs of width n; count 0 disables it. At
+ * most 7 peers. */
+#define IRL_RECV_SLOTS 2
 int irl_ccmm_alloc_recv(irl_ccmm* e, size_t n, void** dev_ptr, uint8_t* ipc_handle /* 64 B, nullable */);
 int irl_ccmm_set_mirrors(irl_ccmm* e, size_t part, size_t n, const uint8_t* ipc_handles /* count x 64 B */,
                          size_t count);
 /* Same with raw device pointers (same-process peers / tests). */
 int irl_ccmm_set_mirror_ptrs(irl_ccmm* e, size_t part, size_t n, uint16_t* const* dev_ptrs, size_t count);
+/* Slot (< IRL_RECV_SLOTS) of the peers' receive buffers the next runs store
+ * into; peer buffers given by pointer must hold slot + 1 slots. */
+int irl_ccmm_set_mirror_slot(irl_ccmm* e, size_t slot);
 /* NVLS multicast mirror: mc_addr is a multicast address (cuMulticastCreate +
  * cuMemMap) whose object binds one receive buffer per GPU; the epilogue of
  * part `part` stores each pair of output rows there once (multimem.st) and the
- * switch writes every bound copy. Needs an even M. NULL disables it. */
+ * switch writes every bound copy (at slot `mirror_slot`, so the bound
+ * buffers hold IRL_RECV_SLOTS slots). Needs an even M. NULL disables it. */
 int irl_ccmm_set_mirror_multicast(irl_ccmm* e, size_t part, size_t n, void* mc_addr);
 /* ModDown of the engine's outputs (after irl_ccmm_run_device wrote them to the
  * engine buffer, n columns): parts [part0, part0 + nparts) of [parts][nmod][n][M]

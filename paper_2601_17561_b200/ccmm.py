@@ -115,16 +115,23 @@ class CcmmEngine:
 
     # ---- fused a-part exchange (irl_ccmm_alloc_recv / set_mirrors) ----------
 
+    RECV_SLOTS = 2  # IRL_RECV_SLOTS
+
     def alloc_recv(self, n: int):
-        """Engine-owned receive buffer [nmod][n][M] for the a-part: returns a
-        torch view (int16 bit patterns) and its 64-byte CUDA IPC handle."""
+        """Engine-owned double-buffered receive buffer [2][nmod][n][M] for the
+        a-part: returns a torch view (int16 bit patterns) and its 64-byte CUDA
+        IPC handle. The owner stores step s into slot set_mirror_slot(s % 2)."""
         import torch
         p = C.c_void_p()
         h = (C.c_uint8 * 64)()
         self.ctx.check(capi.lib().irl_ccmm_alloc_recv(self.handle, n, C.byref(p), h))
-        view = torch.as_tensor(_CudaArray(p.value, (self.nmod, n, self.M), "<i2"),
+        view = torch.as_tensor(_CudaArray(p.value, (self.RECV_SLOTS, self.nmod, n, self.M), "<i2"),
                                device=f"cuda:{self.ctx.device}")
         return view, bytes(h)
+
+    def set_mirror_slot(self, slot: int):
+        """Receive slot of the peers' buffers the next runs store into."""
+        self.ctx.check(capi.lib().irl_ccmm_set_mirror_slot(self.handle, slot))
 
     def set_mirrors(self, part: int, n: int, handles):
         """Store part `part`'s outputs also into the peers' buffers (IPC handles)."""

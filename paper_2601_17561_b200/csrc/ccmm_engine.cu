@@ -45,7 +45,7 @@ struct irl_ccmm {
     // and the peers' buffers this engine stores into (IPC-mapped or raw)
     uint16_t* recv = nullptr;
     size_t recv_n = 0;
-    size_t mirror_part = 0, mirror_n = 0, n_mirror = 0;
+    size_t mirror_part = 0, mirror_n = 0, n_mirror = 0, mirror_slot = 0;
     uint16_t* mirror[kMaxMirrors] = {};
     bool mirror_ipc[kMaxMirrors] = {};
     uint16_t* mc_mirror = nullptr;  // NVLS multicast address of the receive buffers (irl_ccmm_set_mirror_multicast)
@@ -153,8 +153,9 @@ int irl_ccmm_alloc_recv(irl_ccmm* e, size_t n, void** dev_ptr, uint8_t* ipc_hand
     if (n == 0 || n > e->max_n) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: receive width out of range");
     if (e->recv) cudaFree(e->recv);
     e->recv = nullptr;
-    IRL_CK(ctx, cudaMalloc(&e->recv, e->nmod * n * e->M * sizeof(uint16_t)));
-    IRL_CK(ctx, cudaMemset(e->recv, 0, e->nmod * n * e->M * sizeof(uint16_t)));
+    const size_t slot_bytes = e->nmod * n * e->M * sizeof(uint16_t);
+    IRL_CK(ctx, cudaMalloc(&e->recv, IRL_RECV_SLOTS * slot_bytes));
+    IRL_CK(ctx, cudaMemset(e->recv, 0, IRL_RECV_SLOTS * slot_bytes));
     e->recv_n = n;
     *dev_ptr = e->recv;
     if (ipc_handle) {
@@ -206,6 +207,14 @@ int irl_ccmm_set_mirror_ptrs(irl_ccmm* e, size_t part, size_t n, uint16_t* const
     if (!e || (count && !dev_ptrs)) return IRL_ERR_INVALID_ARGUMENT;
     Guard g(e->ctx);
     return set_mirrors(e, part, n, dev_ptrs, nullptr, count);
+}
+
+int irl_ccmm_set_mirror_slot(irl_ccmm* e, size_t slot) {
+    if (!e) return IRL_ERR_INVALID_ARGUMENT;
+    Guard g(e->ctx);
+    if (slot >= IRL_RECV_SLOTS) return set_err(e->ctx, IRL_ERR_INVALID_ARGUMENT, "ccmm: mirror slot out of range");
+    e->mirror_slot = slot;
+    return IRL_OK;
 }
 
 int irl_ccmm_set_mirror_multicast(irl_ccmm* e, size_t part, size_t n, void* mc_addr) {
@@ -421,8 +430,9 @@ static int ccmm_parts(irl_ccmm* e, size_t n, size_t part0, size_t nparts, uint16
         e->mirror_part < part0 + nparts) {
         L.n_mirror = static_cast<uint32_t>(e->n_mirror);
         L.mirror_part = static_cast<uint32_t>(e->mirror_part - part0);
-        for (size_t i = 0; i < e->n_mirror; ++i) L.mirror[i] = e->mirror[i] + m0 * n * e->M;
-        if (e->mc_mirror) L.mc_mirror = e->mc_mirror + m0 * n * e->M;
+        const size_t at = (e->mirror_slot * e->nmod + m0) * n * e->M;  // [slot][modulus][n][M]
+        for (size_t i = 0; i < e->n_mirror; ++i) L.mirror[i] = e->mirror[i] + at;
+        if (e->mc_mirror) L.mc_mirror = e->mc_mirror + at;
     }
     return run_ppmm(ctx, L, e->kchunk, s);
 }

@@ -125,6 +125,7 @@ struct irl_ccmm_group {
     std::vector<size_t> first, count;
     std::vector<uint16_t*> recv;  // rank r: receive buffer of the a-part result [nmod][n][M] (r > 0, or all with MC)
     size_t recv_n = 0;            // width the receive buffers and mirrors are set up for
+    size_t slot = 0;              // receive slot of the last irl_ccmm_full (alternates per call)
     int requested = IRL_EXCHANGE_AUTO;
     int mode = IRL_EXCHANGE_COPY;  // the exchange in use
     McExchange mcx;
@@ -232,7 +233,7 @@ int setup_exchange(irl_ccmm_group* g, size_t n) {
     irl_ccmm_set_mirror_multicast(g->eng[0], 0, 0, nullptr);
     mc_release(&g->mcx);
     g->recv.assign(g->ndev, nullptr);
-    const size_t bytes = g->nmod * n * g->M * sizeof(uint16_t);
+    const size_t bytes = IRL_RECV_SLOTS * g->nmod * n * g->M * sizeof(uint16_t);
     // multicast is opt-in: it could not be exercised where this was built
     // (cuMulticastCreate is refused inside the container), so AUTO stays on
     // the validated P2P stores
@@ -351,6 +352,10 @@ int irl_ccmm_full(irl_ccmm_group* g, const uint16_t* q_res_host, size_t n, uint1
     irl_ctx* c0 = g->ctx[0];
     if (n == 0 || n > g->max_n) return set_err(c0, IRL_ERR_SHAPE_MISMATCH, "ccmm group: query width out of range");
     if (int st = setup_exchange(g, n)) return st;
+    // double-buffered receive: this call stores into the other slot, so a
+    // consumer still reading the previous call's a-part is never overwritten
+    g->slot = (g->slot + 1) % IRL_RECV_SLOTS;
+    if (int st = irl_ccmm_set_mirror_slot(g->eng[0], g->slot)) return st;
     std::vector<int> st(g->ndev, IRL_OK);
     std::vector<std::thread> th;
     for (size_t r = 0; r < g->ndev; ++r)
@@ -365,16 +370,17 @@ int irl_ccmm_full(irl_ccmm_group* g, const uint16_t* q_res_host, size_t n, uint1
     void* q0 = nullptr;
     void* out0 = nullptr;
     irl_ccmm_buffers(g->eng[0], &q0, &out0);  // rank 0's outputs; part 0 = the a-part result
-    const size_t a_bytes = g->nmod * n * g->M * sizeof(uint16_t);
+    const size_t a_elems = g->nmod * n * g->M, a_bytes = a_elems * sizeof(uint16_t);
     if (g->mode == IRL_EXCHANGE_COPY) {  // the exchange as plain peer copies after the runs
         for (size_t r = 1; r < g->ndev; ++r) {
             cudaSetDevice(g->dev[r]);
-            const cudaError_t e = cudaMemcpyPeer(g->recv[r], g->dev[r], out0, g->dev[0], a_bytes);
+            const cudaError_t e = cudaMemcpyPeer(g->recv[r] + g->slot * a_elems, g->dev[r], out0, g->dev[0], a_bytes);
             if (e != cudaSuccess) return cuda_fail(c0, e, "cudaMemcpyPeer (a-part exchange)");
         }
     }
     if (a_out)
-        for (size_t r = 0; r < g->ndev; ++r) a_out[r] = g->recv[r] ? static_cast<void*>(g->recv[r]) : out0;
+        for (size_t r = 0; r < g->ndev; ++r)
+            a_out[r] = g->recv[r] ? static_cast<void*>(g->recv[r] + g->slot * a_elems) : out0;
     if (mode) *mode = g->mode;
     return IRL_OK;
 }

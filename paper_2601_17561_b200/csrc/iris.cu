@@ -35,15 +35,19 @@ using namespace irl;
 namespace {
 
 // The iris products run on the block-scaled FP4 tensor path unless
-// IRL_IRIS_I8 is set: ternary values and mask bits are exact in e2m1 and the
-// FP32 accumulators are exact below 2^24, at twice the int8 rate with half
-// the plane bytes (profiles/fp4_probe.cu).
-bool iris_f4() {
+// IRL_IRIS_I8 is set: ternary values and mask bits are exact in e2m1, and the
+// FP32 accumulators hold every partial sum exactly while |sum| <= d < 2^24,
+// at twice the int8 rate with half the plane bytes (profiles/fp4_probe.cu;
+// all-ones masks at d = 40000 and d = 2^20 checked against the oracle in
+// tests/test_iris.py). Longer templates (d >= 2^24, sums no longer exact in
+// FP32) run on the int8 path, whose int32 accumulators are exact to 2^31.
+constexpr size_t kF4ExactD = size_t(1) << 24;
+bool iris_f4(size_t d) {
     static const bool f4 = std::getenv("IRL_IRIS_I8") == nullptr;
-    return f4;
+    return f4 && d < kF4ExactD;
 }
 // Bytes of one plane row holding d entries (int8: one per byte; e2m1: two).
-size_t plane_kbytes(size_t d) { return iris_f4() ? (d + 1) / 2 : d; }
+size_t plane_kbytes(size_t d) { return iris_f4(d) ? (d + 1) / 2 : d; }
 size_t plane_ldk(size_t d) { return round16(plane_kbytes(d)); }
 
 // Column split of the FP4 query batch. A 1 x 4 cluster covers four 240-column
@@ -51,8 +55,8 @@ size_t plane_ldk(size_t d) { return round16(plane_kbytes(d)); }
 // for the paper's batch) would cost a second, mostly padding pass of the
 // whole cluster, so it runs as its own launch on plain pairs. Returns the
 // columns of the main launch, 0 = no split.
-size_t col_split(size_t cols) {
-    if (!iris_f4() || std::getenv("IRL_IRIS_NO_SPLIT")) return 0;
+size_t col_split(size_t cols, size_t d) {
+    if (!iris_f4(d) || std::getenv("IRL_IRIS_NO_SPLIT")) return 0;
     const size_t pass = 4 * kF4TileCols;
     const size_t main = cols / pass * pass;
     return main > 0 && main < cols ? main : 0;
@@ -143,13 +147,13 @@ __global__ void iris_file_planes_kernel(const uint8_t* __restrict__ code, const 
 int inner_overlap_gemm(irl_ctx* ctx, const int8_t* xp, const int8_t* yp, size_t n_db, size_t cols, size_t d,
                        size_t ldk, int32_t* inner, int32_t* ovl, uint32_t* progress, cudaStream_t s) {
     // one launch per column range of build_query_planes (see col_split)
-    const size_t split = col_split(cols);
+    const size_t split = col_split(cols, d);
     const size_t ranges[2][2] = {{0, split ? split : cols}, {split, split ? cols - split : 0}};
     for (const auto& rg : ranges) {
         const size_t c0 = rg[0], nc = rg[1];
         if (nc == 0) continue;
         PpmmLaunch L;
-        L.mode = iris_f4() ? kModeInnerF4 : kModeInner;
+        L.mode = iris_f4(d) ? kModeInnerF4 : kModeInner;
         L.a_planes = xp;
         L.b_planes = yp + 2 * c0 * ldk;
         L.out_i32[0] = inner ? inner + c0 * n_db : nullptr;
@@ -176,7 +180,7 @@ int build_planes_range(irl_ctx* ctx, const uint64_t* code, const uint64_t* mask,
     const size_t words = (d + 63) / 64, ldk = plane_ldk(d);
     const size_t total = ncols * (ldk / 16);
     if (total == 0) return IRL_OK;
-    auto kern = iris_f4() ? iris_planes_kernel<true> : iris_planes_kernel<false>;
+    auto kern = iris_f4(d) ? iris_planes_kernel<true> : iris_planes_kernel<false>;
     kern<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
         code, mask, static_cast<uint32_t>(words), static_cast<uint32_t>(d), static_cast<uint32_t>(rho),
         static_cast<uint32_t>(c0), static_cast<uint32_t>(ncols), static_cast<uint32_t>(ldk), planes);
@@ -192,7 +196,7 @@ int build_planes(irl_ctx* ctx, const uint64_t* code, const uint64_t* mask, size_
 // Query planes, laid out per launch: [2][main][ldk] then [2][rest][ldk].
 int build_query_planes(irl_ctx* ctx, const uint64_t* code, const uint64_t* mask, size_t n_eyes, size_t rho,
                        size_t d, int8_t* planes, cudaStream_t s) {
-    const size_t cols = n_eyes * rho, split = col_split(cols);
+    const size_t cols = n_eyes * rho, split = col_split(cols, d);
     if (!split) return build_planes_range(ctx, code, mask, rho, d, 0, cols, planes, s);
     if (int st = build_planes_range(ctx, code, mask, rho, d, 0, split, planes, s)) return st;
     return build_planes_range(ctx, code, mask, rho, d, split, cols - split, planes + 2 * split * plane_ldk(d), s);
@@ -217,13 +221,13 @@ int match_fused(irl_ctx* ctx, const int8_t* xp, const int8_t* yp, size_t n_db, s
     IRL_CK(ctx, cudaMemsetAsync(dbits, 0, nbits, s));
     // one launch per column range of build_query_planes (see col_split); the
     // launches fold into the same first-event indices and match bits
-    const size_t split = col_split(cols);
+    const size_t split = col_split(cols, d);
     const size_t ranges[2][2] = {{0, split ? split : cols}, {split, split ? cols - split : 0}};
     for (const auto& rg : ranges) {
         const size_t c0 = rg[0], nc = rg[1];
         if (nc == 0) continue;
         PpmmLaunch L;
-        L.mode = iris_f4() ? kModeIrisMatchF4 : kModeIrisMatch;
+        L.mode = iris_f4(d) ? kModeIrisMatchF4 : kModeIrisMatch;
         L.a_planes = xp;
         L.b_planes = yp + 2 * c0 * ldk;
         L.M = static_cast<uint32_t>(n_db);
@@ -466,7 +470,7 @@ int irl_iris_db_create_file(irl_ctx* ctx, const char* path, size_t max_cols, irl
     if (err == cudaSuccess) err = cudaMemcpyAsync(staging, host, 2 * plane_bytes, cudaMemcpyHostToDevice, ctx->stream);
     if (err == cudaSuccess) {
         const size_t total = n * (e->ldk / 16);
-        auto kern = iris_f4() ? iris_file_planes_kernel<true> : iris_file_planes_kernel<false>;
+        auto kern = iris_f4(d) ? iris_file_planes_kernel<true> : iris_file_planes_kernel<false>;
         kern<<<static_cast<unsigned>((total + 255) / 256), 256, 0, ctx->stream>>>(
             staging, staging + plane_bytes, static_cast<uint32_t>(d), static_cast<uint32_t>(n),
             static_cast<uint32_t>(e->ldk), e->planes);

@@ -457,13 +457,24 @@ def test_ccmm_fused_exchange_mirrors():
     torch.cuda.synchronize()
     for mbuf in mirrors:
         assert (mbuf.cpu().numpy().view(np.uint16) == out[1]).all()
-    # the receive buffer of an engine, and disabling
+    # the double-buffered receive buffer of an engine: slot 0, then slot 1
+    # while slot 0 keeps the previous step, and disabling
     view, handle = eng.alloc_recv(n)
-    assert len(handle) == 64 and tuple(view.shape) == (eng.nmod, n, 520)
+    assert len(handle) == 64 and tuple(view.shape) == (2, eng.nmod, n, 520)
     eng.set_mirror_ptrs(0, n, [view])
     eng.run_device(None, n, None)
     torch.cuda.synchronize()
-    assert torch.equal(view, od[0])
+    assert torch.equal(view[0], od[0])
+    step0 = view[0].clone()
+    eng.set_mirror_slot(1)
+    qd.copy_(torch.from_numpy(q2.view(np.int16)))
+    torch.cuda.synchronize()
+    eng.run_device(None, n, None)
+    torch.cuda.synchronize()
+    assert torch.equal(view[1], od[0]) and torch.equal(view[0], step0) and not torch.equal(view[0], view[1])
+    with pytest.raises(Exception):
+        eng.set_mirror_slot(2)
+    eng.set_mirror_slot(0)
     eng.set_mirror_ptrs(0, n, [])
     before = view.clone()
     qd.copy_(torch.from_numpy(q.view(np.int16)))
@@ -581,8 +592,9 @@ def test_ccmm_load_part_file_streams_reference_format(tmp_path):
         eng.load_part_file(0, tmp_path / "missing.bin")
 
 
-@pytest.mark.parametrize("devices,parts", [([0, 0], 3), ([0, 0, 0], 3), ([0, 0, 0, 0], 8)])
-def test_ccmm_group_full_equals_one_engine_and_exchanges_the_a_part(devices, parts):
+@pytest.mark.parametrize("devices,parts,m", [([0, 0], 3, 384), ([0, 0, 0], 3, 384), ([0, 0, 0, 0], 8, 384),
+                                             ([0, 0], 4, 2560)])
+def test_ccmm_group_full_equals_one_engine_and_exchanges_the_a_part(devices, parts, m):
     """irl_ccmm_full (single-process multi-GPU; here every rank on device 0):
     the parts dealt as dist.part_range, every rank's outputs in global order,
     equal to one engine holding all parts; every rank ends with the a-part
@@ -592,7 +604,10 @@ def test_ccmm_group_full_equals_one_engine_and_exchanges_the_a_part(devices, par
     from paper_2601_17561_b200 import capi
     from paper_2601_17561_b200.ccmm import CcmmEngine, CcmmGroup, synth_query
     from paper_2601_17561_b200.dist import part_range
-    m, k, n = 384, 1024, 96
+    # m = 2560: 10 row blocks x 2 parts x 24 moduli = 480 units per rank, so
+    # every rank's launch plans the 1x4-cluster grid plus its filler grid,
+    # concurrently on one device from two host threads
+    k, n = 1024, 96
     g = CcmmGroup(devices, parts=parts, m=m, k=k, max_n=n)
     try:
         for r in range(len(devices)):
@@ -604,6 +619,8 @@ def test_ccmm_group_full_equals_one_engine_and_exchanges_the_a_part(devices, par
         eng.synth_db(seed=1)
         q = synth_query(2, k, n, eng.moduli)
         want = eng.run(q)
+        q2 = synth_query(3, k, n, eng.moduli)
+        want2 = eng.run(q2)
         eng.close()
         out, ptrs, mode = g.run(q)
         assert mode == capi.IRL_EXCHANGE_P2P  # ranks share a device: no multicast, P2P stores
@@ -612,8 +629,17 @@ def test_ccmm_group_full_equals_one_engine_and_exchanges_the_a_part(devices, par
         for r in range(len(devices)):
             a = g.a_part(r, ptrs[r], n).cpu().numpy().view(np.uint16)
             assert np.array_equal(a, want[0]), r
-        out2, _, _ = g.run(q)  # a second call reuses the exchange set-up
-        assert np.array_equal(out2, want)
+        # a second call reuses the exchange set-up and stores the a-part into
+        # the other receive slot: the first call's copy stays intact
+        out2, ptrs2, _ = g.run(q2)
+        assert np.array_equal(out2, want2)
+        torch.cuda.synchronize()
+        for r in range(1, len(devices)):
+            assert ptrs2[r] != ptrs[r]
+            assert np.array_equal(g.a_part(r, ptrs2[r], n).cpu().numpy().view(np.uint16), want2[0]), r
+            assert np.array_equal(g.a_part(r, ptrs[r], n).cpu().numpy().view(np.uint16), want[0]), r
+        out3, ptrs3, _ = g.run(q)  # third call: back to the first slot
+        assert np.array_equal(out3, want) and ptrs3[-1] == ptrs[-1]
     finally:
         g.close()
 
