@@ -271,6 +271,23 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def nccl_summary(path, world):
+    """What NCCL_DEBUG=INFO recorded about the communicator (rank 0's file)."""
+    if not path or world < 2:
+        return None
+    try:
+        lines = Path(path).read_text(errors="replace").splitlines()
+    except OSError:
+        return {"debug_file": path, "read": False}
+    init = [ln for ln in lines if "Init COMPLETE" in ln]
+    return {"debug_file": path, "lines": len(lines), "init_complete": init[:1],
+            "nranks_seen": sorted({int(t.split()[1]) for ln in init for t in [ln[ln.find("nranks"):]]
+                                   if t.startswith("nranks ") and t.split()[1].isdigit()}),
+            "nvls": any("NVLS" in ln and "enabled" in ln.lower() for ln in lines) or
+                    any("NVLS multicast support is available" in ln for ln in lines),
+            "version": next((ln.split("NCCL version", 1)[1].strip() for ln in lines if "NCCL version" in ln), None)}
+
+
 WORKLOADS = {
     "c2": "c2: full-RNS PPMM mod Q on one DB slice, 992 query columns x d = 2^14 x 2^14 templates",
     "c3": "c3: RGSW CCMM a-part + one b-part (2 K-concatenated PPMMs, N_db = 2^14, K = 2^14 + 2^13)",
@@ -369,6 +386,7 @@ def measure_e2e(R):
         q_slices = [q_bytes[r_ * per:(r_ + 1) * per] for r_ in range(world)] if sharded else None
 
         def e2e_once():
+            R.next_slot()
             if sharded:
                 q_dev[lo:lo + per].copy_(q_pinned.view(nmod, K, N)[lo:lo + per], non_blocking=True)
                 dist.all_gather(q_slices, q_bytes[lo:lo + per].clone() if args.backend == "gloo" else q_bytes[lo:lo + per])
@@ -616,9 +634,14 @@ def main():
     if args.same_device:
         local = 0  # test harness: every rank on GPU 0 (multi-rank code paths on a 1-GPU box)
     torch.cuda.set_device(local)
+    nccl_log = None
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         if args.backend == "nccl":
+            # NCCL's own record of the communicator (ranks, channels, NVLS),
+            # to a per-rank file so stdout keeps the one JSON line
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            nccl_log = os.environ.setdefault("NCCL_DEBUG_FILE", f"/tmp/irl_bench_nccl.{os.getpid()}.log")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group("gloo")
@@ -676,7 +699,16 @@ def main():
             elif rank == 0:
                 eng.set_mirrors(0, N, [])
         if rank != 0 and a_recv is None:
-            a_recv = torch.empty((nmod - md_drop, N, M), dtype=torch.int16, device="cuda")
+            a_recv = torch.empty((2, nmod - md_drop, N, M), dtype=torch.int16, device="cuda")
+    # The a-part receive buffers are double-buffered ([2] slots, alternating per
+    # step): the owner's step s+1 stores into the other slot, so a consumer of
+    # step s on a peer is never overwritten mid-read (irl_ccmm_set_mirror_slot).
+    slot = [1]
+
+    def next_slot():
+        slot[0] ^= 1
+        if world > 1 and rank == 0 and exchange == "mirror":
+            eng.set_mirror_slot(slot[0])
     # a dedicated stream: the engine runs on the stream it is handed, and the
     # CUDA events below are recorded on that same stream
     stream = torch.cuda.Stream()
@@ -700,15 +732,21 @@ def main():
 
     def a_out():
         if rank != 0:
-            return a_recv
+            return a_recv[slot[0]]
         return out_md[0] if md_drop else out_dev[0]
 
     step = ShardedStep(rank, world, run_parts, a_out, parts=args.parts, exchange=exchange)
+    step_events = []
 
     def one_step():
+        next_slot()
         w = step()
         if w is not None:
             w.wait()
+        if world > 1:  # the exchange's completion on this rank's stream
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(stream)
+            step_events.append(ev)
 
     def a_checksum():
         # sum + exact head/tail samples of this rank's copy of the a-part result
@@ -737,6 +775,7 @@ def main():
         one_step()
     torch.cuda.synchronize()
     gemm_events.clear()
+    step_events.clear()
     if world > 1:
         dist.barrier()
     launches0 = ctx.launches
@@ -758,6 +797,18 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     total_ops = 6.0 * nmod * M * N * K * args.parts
+    # per-rank breakdown of the timed steps: local GEMM launches, and the wait
+    # from the last local GEMM to the exchange's completion on this rank
+    per_rank = None
+    if world > 1:
+        runs = len(gemm_events) // max(1, args.steps)
+        mine = {"rank": rank, "parts": [local_parts.first, local_parts.count], "step_ms": ms,
+                "gemm_ms": sum(a.elapsed_time(b) for a, b, _ in gemm_events) / args.steps,
+                "exchange_wait_ms": statistics.mean(
+                    gemm_events[(i + 1) * runs - 1][1].elapsed_time(step_events[i]) for i in range(args.steps))
+                if runs and len(step_events) == args.steps else None}
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, mine)
     value = total_ops / (ms_max * 1e-3) / 1e12
 
     # dominant kernel: the PPMM launch (split is fused into the first launch's
@@ -789,7 +840,7 @@ def main():
         args=args, torch=torch, dist=dist, eng=eng, ctx=ctx, N=N, M=M, K=K, nmod=nmod, stream=stream,
         world=world, rank=rank, local_parts=local_parts, out_dev=out_dev, q_dev=q_dev, q_pinned=q_pinned,
         q_host=q_host, moduli=moduli, a_out=a_out, exchange=exchange, md_drop=md_drop, out_md=out_md,
-        total_ops=total_ops, peaks=peaks, hbm_peak=hbm_peak)
+        total_ops=total_ops, peaks=peaks, hbm_peak=hbm_peak, next_slot=next_slot)
     split_roof = measure_split(R)
     moddown = measure_moddown(R)
     e2e = measure_e2e(R)
@@ -824,6 +875,7 @@ def main():
                     else "NCCL broadcast after the local GEMMs", "note": exch_note,
                     "bytes": int(a_out().numel() * 2)},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "dist_check": dist_check,
+                "per_rank": per_rank, "nccl": nccl_summary(nccl_log, world),
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -41,6 +41,12 @@ def test_bench_multirank_same_device(world, exchange):
     assert d["value"] > 0 and d["e2e"]["value"] > 0
     assert d["e2e"]["outputs_equal_device_step"]
     assert d["dist_check"]["bit_exact_all_ranks"]  # sampled rows of every rank vs the CPU oracle
+    # per-rank breakdown (diagnosable scaling runs): every rank's GEMM time and
+    # its wait for the exchange after its last local GEMM
+    pr = d["per_rank"]
+    assert [x["rank"] for x in pr] == list(range(world))
+    assert all(x["gemm_ms"] > 0 and x["exchange_wait_ms"] is not None for x in pr)
+    assert sum(x["parts"][1] for x in pr) == max(4, world)
 
 
 @pytest.mark.gpu

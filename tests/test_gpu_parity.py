@@ -467,7 +467,7 @@ def test_ccmm_fused_exchange_mirrors():
     assert torch.equal(view[0], od[0])
     step0 = view[0].clone()
     eng.set_mirror_slot(1)
-    qd.copy_(torch.from_numpy(q2.view(np.int16)))
+    qd.copy_(torch.from_numpy(q.view(np.int16)))  # staging held q2 (the e2e run above)
     torch.cuda.synchronize()
     eng.run_device(None, n, None)
     torch.cuda.synchronize()
