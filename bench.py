@@ -44,7 +44,12 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--parts", type=int, default=8)
-    ap.add_argument("--rows", type=int, default=1 << 14, help="templates per part (M)")
+    ap.add_argument("--rows", type=int, default=1 << 14, help="templates per part (M; the a-part's rows)")
+    ap.add_argument("--b-rows", type=int, default=0,
+                    help="templates per b-part (default --rows; c5 grows them to 2^17)")
+    ap.add_argument("--deal", choices=["auto", "parts", "blocks"], default="auto",
+                    help="multi-GPU dealing: whole parts, or balanced row blocks (dist.deal_blocks; auto = blocks "
+                         "when b-parts are taller than the a-part)")
     ap.add_argument("--k", type=int, default=(1 << 14) + (1 << 13), help="d2 + N_qry")
     ap.add_argument("--eyes", type=int, default=32)
     ap.add_argument("--rot", type=int, default=31)
@@ -68,6 +73,7 @@ def parse():
                     help="BASELINE.json config: c2 one DB slice as one PPMM (K = 2^14), c3 a-part + one "
                          "b-part, c4 the full 8-part DB (default; the headline metric)")
     a = ap.parse_args()
+    a.b_rows = a.b_rows or a.rows
     if a.config == "c2":
         a.parts, a.k = 1, 1 << 14
     elif a.config == "c3":
@@ -242,7 +248,7 @@ def run_reference_arm(args):
     pr, ex = ol.paper_basis()
     moduli = [int(p) ** int(e) for p, e in zip(pr, ex)]
     N = args.eyes * args.rot
-    total_ops = 6.0 * len(moduli) * args.rows * N * args.k * args.parts
+    total_ops = 6.0 * len(moduli) * total_rows(args) * N * args.k
     q = query_residues_oracle(args.k, N, moduli)
     rates, secs = [], []
     last = None
@@ -295,6 +301,11 @@ WORKLOADS = {
 }
 
 
+def total_rows(args):
+    """Database rows over all parts: the a-part plus parts - 1 b-parts."""
+    return args.rows + (args.parts - 1) * args.b_rows
+
+
 def config_dict(args, nmod):
     N = args.eyes * args.rot
     extra = {}
@@ -303,7 +314,9 @@ def config_dict(args, nmod):
                  "moddown": f"every local output rescaled to Q/Delta (last {args.moddown} moduli dropped) inside "
                             "the step; the a-part exchange carries the rescaled result"}
     return {"workload": WORKLOADS[args.config] + (" + ModDown" if args.moddown else ""), **extra,
-            "parts": args.parts, "templates_per_part": args.rows, "K": args.k, "query_columns": N,
+            "parts": args.parts, "templates_per_part": args.rows,
+            **({"templates_per_b_part": args.b_rows} if args.b_rows != args.rows else {}),
+            "K": args.k, "query_columns": N,
             "eyes": args.eyes, "rotations": args.rot, "moduli": nmod, "log2_Q": 360.8156,
             "digit_planes": 2 * nmod, "parallelism": f"db-slices over {args.gpus} GPU(s)",
             "l2": "inputs larger than L2 (DB digit planes, 18 GiB per part)"}
@@ -447,14 +460,14 @@ def measure_dist_check(R):
     if world > 1 and not args.no_cpu_baseline:
         sys.path.insert(0, str(ROOT / "tests"))
         import oracle_lib as ol
-        part_g = local_parts.first
+        part_g, row0 = R.unit_map[0]  # global part and first row of the first local unit
         rows = np.array([0, M // 2, M - 1], np.uint32)
-        got_all = out_dev[0].cpu().numpy().view(np.uint16)  # [nmod][N][M] of the first local part
+        got_all = out_dev[0].cpu().numpy().view(np.uint16)  # [nmod][N][M] of the first local unit
         ok = True
         for i, m_ in enumerate(moduli):
             qt = np.ascontiguousarray(q_host[i].T)
             for r_ in rows:  # only the sampled DB rows are generated
-                a_row = ol.synth_block(args.seed, part_g, i, int(r_), 1, 0, K, m_)
+                a_row = ol.synth_block(args.seed, part_g, i, row0 + int(r_), 1, 0, K, m_)
                 want = ol.ppmm_rows_direct(a_row, qt, np.zeros(1, np.uint32), m_)
                 ok &= bool((got_all[i][:, int(r_)] == want[0]).all())
         ok_t = torch.tensor([1 if ok else 0], dtype=torch.int32, device="cuda")
@@ -481,8 +494,9 @@ def measure_cpu(R):
         exact = True
         j = 0
         for part in r["parts"]:
+            unit = R.unit_map.index((part, 0))  # rows [0, cpu_rows) of global part `part`
             for i in range(nmod):
-                exact &= bool((r["outputs"][j] == gpu_rows[part, i].T).all())
+                exact &= bool((r["outputs"][j] == gpu_rows[unit, i].T).all())
                 j += 1
         cpu = {"value": r["tops"], "unit": UNIT, "cores": r["threads"], "kind": r["kind"],
                "sample": r["sample"], "seconds": r["seconds"], "bit_exact_vs_gpu": exact,
@@ -521,7 +535,7 @@ def measure_fold(R):
         return None
     from paper_2601_17561_b200.fold import FoldConfig, fold_stage_device
     d = 1 << 14
-    n_db = max(1, (args.parts - 1) * M // d) * d  # the b-part templates, whole blocks
+    n_db = max(1, (args.parts - 1) * args.b_rows // d) * d  # the b-part templates, whole blocks
     eyes, rho, fold_k = args.eyes, args.rot, min(16, args.rot)
     g = torch.Generator(device="cuda").manual_seed(3)
     ovl = torch.randint(1, d, (N, n_db), dtype=torch.int32, device="cuda", generator=g)
@@ -563,7 +577,7 @@ def measure_iris(R):
 
     from paper_2601_17561_b200.iris import IrisDatabase, Interval
     d = 1 << 14
-    n_db = max(1, (args.parts - 1) * M // d) * d
+    n_db = max(1, (args.parts - 1) * args.b_rows // d) * d
     eyes, rho = args.eyes, args.rot
     rng = np.random.default_rng(5)
     words = d // 64
@@ -647,17 +661,33 @@ def main():
             dist.init_process_group("gloo")
 
     from paper_2601_17561_b200.ccmm import CcmmEngine, staging_tensors, synth_query
-    from paper_2601_17561_b200.dist import ShardedStep, part_range
+    from paper_2601_17561_b200.dist import PartRange, ShardedStep, deal_blocks, part_range
     from paper_2601_17561_b200.modmat import Context, build_paper_basis
 
     basis = build_paper_basis()
     nmod = len(basis.moduli)
     N = args.eyes * args.rot
-    M, K = args.rows, args.k
-    local_parts = part_range(rank, world, args.parts)
+    K = args.k
+    # Dealing: whole parts (the paper's 8-slice layout), or balanced row blocks
+    # when the b-parts are taller than the a-part (c5). Either way
+    # the engine holds `local_parts.count` units of M rows; unit_map[j] is the
+    # (global part, first row) of local unit j, a_units the owner's a-part units.
+    use_blocks = args.deal == "blocks" or (args.deal == "auto" and args.b_rows != args.rows)
+    if use_blocks:
+        bd = deal_blocks(rank, world, args.rows, args.b_rows, args.parts)
+        # every rank sizes its a-part buffer by the a-part's block count
+        M, local_parts, unit_map, a_units = bd.block, PartRange(bd.first, bd.count), list(bd.blocks), args.rows // bd.block
+    else:
+        M = args.rows
+        local_parts = part_range(rank, world, args.parts)
+        unit_map, a_units = [(p, 0) for p in local_parts], 1
     ctx = Context(local)
     eng = CcmmEngine(parts=local_parts.count, m=M, k=K, max_n=N, basis=basis, ctx=ctx)
-    eng.synth_db(seed=args.seed, first_part=local_parts.first)
+    if use_blocks:
+        for j, (gp, r0) in enumerate(unit_map):
+            eng.synth_part(j, args.seed, gp, r0)
+    else:
+        eng.synth_db(seed=args.seed, first_part=local_parts.first)
     moduli = eng.moduli
     q_host = synth_query(2, K, N, moduli)
     q_pinned = torch.from_numpy(q_host.view(np.int16)).pin_memory()
@@ -681,7 +711,7 @@ def main():
             handle = None
             try:
                 if rank != 0:
-                    a_recv, handle = eng.alloc_recv(N)
+                    a_recv, handle = eng.alloc_recv(N, parts=a_units)
             except Exception as ex:  # noqa: BLE001
                 exch_note = f"receive buffer: {ex}"
             handles = [None] * world
@@ -690,6 +720,8 @@ def main():
             if ok and rank == 0:
                 try:
                     eng.set_mirrors(0, N, [h for r, h in enumerate(handles) if r != 0])
+                    if a_units > 1:
+                        eng.set_mirror_parts(a_units)
                 except Exception as ex:  # noqa: BLE001
                     ok, exch_note = False, f"peer mapping: {ex}"
             flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device="cuda")
@@ -699,7 +731,7 @@ def main():
             elif rank == 0:
                 eng.set_mirrors(0, N, [])
         if rank != 0 and a_recv is None:
-            a_recv = torch.empty((2, nmod - md_drop, N, M), dtype=torch.int16, device="cuda")
+            a_recv = torch.empty((2, a_units, nmod - md_drop, N, M), dtype=torch.int16, device="cuda")
     # The a-part receive buffers are double-buffered ([2] slots, alternating per
     # step): the owner's step s+1 stores into the other slot, so a consumer of
     # step s on a peer is never overwritten mid-read (irl_ccmm_set_mirror_slot).
@@ -733,9 +765,13 @@ def main():
     def a_out():
         if rank != 0:
             return a_recv[slot[0]]
-        return out_md[0] if md_drop else out_dev[0]
+        return out_md[:a_units] if md_drop else out_dev[:a_units]
 
-    step = ShardedStep(rank, world, run_parts, a_out, parts=args.parts, exchange=exchange)
+    def make_step(kind):
+        return ShardedStep(rank, world, run_parts, a_out, parts=args.parts, exchange=kind,
+                           local=PartRange(0, local_parts.count) if use_blocks else None, a_parts=a_units)
+
+    step = make_step(exchange)
     step_events = []
 
     def one_step():
@@ -769,7 +805,7 @@ def main():
             exchange, exch_note = "broadcast", "warm-up checksum mismatch on a receiver"
             if rank == 0:
                 eng.set_mirrors(0, N, [])
-            step = ShardedStep(rank, world, run_parts, a_out, parts=args.parts, exchange=exchange)
+            step = make_step(exchange)
 
     for _ in range(args.warmup):
         one_step()
@@ -796,7 +832,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    total_ops = 6.0 * nmod * M * N * K * args.parts
+    total_ops = 6.0 * nmod * total_rows(args) * N * K
     # per-rank breakdown of the timed steps: local GEMM launches, and the wait
     # from the last local GEMM to the exchange's completion on this rank
     per_rank = None
@@ -829,18 +865,28 @@ def main():
     else:
         peak = 2.0 * 1400.0
         peak_src = "2 x fallback bf16 sustained 1.4 PF/s (B200_PROFILING.md)"
-    traffic = None
+    # roofline.traffic: ncu DRAM bytes of the PPMM (profiles/ppmm_traffic.json,
+    # from the capture named there), scaled to this launch's parts; flagged
+    # stale when the kernel source changed since that capture
+    traffic, traffic_src = None, None
     tr_path = ROOT / "profiles" / "ppmm_traffic.json"
     if tr_path.exists():
+        import hashlib
         tr = json.loads(tr_path.read_text())
-        traffic = tr.get("bytes_per_part", 0) * statistics.mean(g_parts) or None
+        if (M, K, N) == (1 << 14, 24576, 992):  # the captured geometry (one c4 slice per part)
+            traffic = tr.get("bytes_per_part", 0) * statistics.mean(g_parts) or None
+        cur = hashlib.sha256((ROOT / "paper_2601_17561_b200" / "csrc" / "ppmm_gemm.cu").read_bytes()).hexdigest()
+        traffic_src = {"capture": tr.get("source"), "per_part_bytes": tr.get("bytes_per_part"),
+                       "algorithmic_per_part": tr.get("algorithmic_bytes_per_part"),
+                       "kernel_source_matches_capture": tr.get("kernel_source_sha256") == cur}
 
     hbm_peak = float(peaks.get("hbm_gbs", 6457.4))
     R = SimpleNamespace(
         args=args, torch=torch, dist=dist, eng=eng, ctx=ctx, N=N, M=M, K=K, nmod=nmod, stream=stream,
         world=world, rank=rank, local_parts=local_parts, out_dev=out_dev, q_dev=q_dev, q_pinned=q_pinned,
         q_host=q_host, moduli=moduli, a_out=a_out, exchange=exchange, md_drop=md_drop, out_md=out_md,
-        total_ops=total_ops, peaks=peaks, hbm_peak=hbm_peak, next_slot=next_slot)
+        total_ops=total_ops, peaks=peaks, hbm_peak=hbm_peak, next_slot=next_slot, unit_map=unit_map,
+        use_blocks=use_blocks)
     split_roof = measure_split(R)
     moddown = measure_moddown(R)
     e2e = measure_e2e(R)
@@ -860,7 +906,7 @@ def main():
                 "tensor_peak_frac": value / peak,
                 "tensor_peak_frac_datasheet": value / DATASHEET_INT8_TOPS,
                 "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS",
-                             "frac": achieved / peak, "traffic": traffic,
+                             "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                              "kernel": "ppmm_i8_sm100_kernel", "launch_ms": launch_ms,
                              "ops_per_launch": launch_ops, "peak_source": peak_src,
                              "frac_of_datasheet_4500": achieved / DATASHEET_INT8_TOPS,
@@ -870,6 +916,9 @@ def main():
                                                           if int8_ref else None)},
                 "split_roofline": split_roof, "moddown": moddown, "fold_stage": fold, "iris_stage": iris,
                 "int8_library_ref": int8_ref,
+                "dealing": ({"kind": "row blocks (dist.deal_blocks)", "block_rows": M,
+                             "units_per_rank": [x["parts"][1] for x in per_rank] if per_rank else [local_parts.count]}
+                            if use_blocks else {"kind": "whole parts (dist.part_range)"}),
                 "exchange": None if world == 1 else {
                     "kind": "fused P2P stores in the a-part PPMM epilogue (CUDA IPC, NVLink)" if exchange == "mirror"
                     else "NCCL broadcast after the local GEMMs", "note": exch_note,

@@ -172,6 +172,10 @@ int irl_ccmm_load_part_file(irl_ccmm* e, size_t part, const char* path);
 /* Fill every part with synthetic residues irl_synth_residue(seed, first_part + part,
  * i, row, col, m_i); first_part is the global id of local part 0 (multi-GPU). */
 int irl_ccmm_synth_db(irl_ccmm* e, uint64_t seed, uint32_t first_part);
+/* Fill local part `part` with rows [row0, row0 + M) of global part
+ * global_part of the same synthetic database (a row block of a taller part:
+ * the balanced row-block dealing of dist.deal_blocks). */
+int irl_ccmm_synth_part(irl_ccmm* e, size_t part, uint64_t seed, uint32_t global_part, uint32_t row0);
 /* End-to-end call with HOST buffers: q_res [nmod][K][N] -> out [parts][nmod][N][M].
  * Copies in, splits, multiplies every part, copies out; blocks. N may exceed
  * max_n: the batch then streams through the engine in column chunks
@@ -236,6 +240,14 @@ int irl_ccmm_set_mirror_ptrs(irl_ccmm* e, size_t part, size_t n, uint16_t* const
 /* Slot (< IRL_RECV_SLOTS) of the peers' receive buffers the next runs store
  * into; peer buffers given by pointer must hold slot + 1 slots. */
 int irl_ccmm_set_mirror_slot(irl_ccmm* e, size_t slot);
+/* Mirror local parts [part, part + count) (part from the last set_mirrors /
+ * set_mirror_ptrs, which reset count to 1): the a-part spans several local
+ * parts when the database is dealt in row blocks (dist.deal_blocks). Peer
+ * buffers then hold [slot][count][nmod][n][M]; receivers allocate them with
+ * irl_ccmm_alloc_recv_parts. */
+int irl_ccmm_set_mirror_parts(irl_ccmm* e, size_t count);
+int irl_ccmm_alloc_recv_parts(irl_ccmm* e, size_t n, size_t parts, void** dev_ptr,
+                              uint8_t* ipc_handle /* 64 B, nullable */);
 /* NVLS multicast mirror: mc_addr is a multicast address (cuMulticastCreate +
  * cuMemMap) whose object binds one receive buffer per GPU; the epilogue of
  * part `part` stores each pair of output rows there once (multimem.st) and the

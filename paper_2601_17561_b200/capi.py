@@ -86,6 +86,9 @@ SIGNATURES = {
     "irl_ccmm_set_mirrors": (C.c_int, [vp, sz, sz, vp, sz]),
     "irl_ccmm_set_mirror_ptrs": (C.c_int, [vp, sz, sz, C.POINTER(vp), sz]),
     "irl_ccmm_set_mirror_slot": (C.c_int, [vp, sz]),
+    "irl_ccmm_set_mirror_parts": (C.c_int, [vp, sz]),
+    "irl_ccmm_alloc_recv_parts": (C.c_int, [vp, sz, sz, C.POINTER(vp), vp]),
+    "irl_ccmm_synth_part": (C.c_int, [vp, sz, C.c_uint64, C.c_uint32, C.c_uint32]),
     "irl_iris_inner_overlap": (C.c_int, [vp, vp, vp, sz, vp, vp, sz, sz, sz, vp, vp]),
     "irl_iris_match": (C.c_int, [vp, vp, vp, sz, vp, vp, sz, sz, sz, C.c_double, C.c_double, vp, vp, vp]),
     "irl_fold_stage": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),

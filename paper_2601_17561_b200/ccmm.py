@@ -117,17 +117,28 @@ class CcmmEngine:
 
     RECV_SLOTS = 2  # IRL_RECV_SLOTS
 
-    def alloc_recv(self, n: int):
-        """Engine-owned double-buffered receive buffer [2][nmod][n][M] for the
-        a-part: returns a torch view (int16 bit patterns) and its 64-byte CUDA
-        IPC handle. The owner stores step s into slot set_mirror_slot(s % 2)."""
+    def alloc_recv(self, n: int, parts: int = 1):
+        """Engine-owned double-buffered receive buffer [2][nmod][n][M] (or
+        [2][parts][nmod][n][M] for an a-part spanning `parts` row blocks) for
+        the a-part: returns a torch view (int16 bit patterns) and its 64-byte
+        CUDA IPC handle. The owner stores step s into slot set_mirror_slot(s % 2)."""
         import torch
         p = C.c_void_p()
         h = (C.c_uint8 * 64)()
-        self.ctx.check(capi.lib().irl_ccmm_alloc_recv(self.handle, n, C.byref(p), h))
-        view = torch.as_tensor(_CudaArray(p.value, (self.RECV_SLOTS, self.nmod, n, self.M), "<i2"),
-                               device=f"cuda:{self.ctx.device}")
+        self.ctx.check(capi.lib().irl_ccmm_alloc_recv_parts(self.handle, n, parts, C.byref(p), h))
+        shape = (self.RECV_SLOTS,) + ((parts,) if parts > 1 else ()) + (self.nmod, n, self.M)
+        view = torch.as_tensor(_CudaArray(p.value, shape, "<i2"), device=f"cuda:{self.ctx.device}")
         return view, bytes(h)
+
+    def set_mirror_parts(self, count: int):
+        """Mirror `count` consecutive local parts from the mirrored part on
+        (an a-part dealt as several row blocks)."""
+        self.ctx.check(capi.lib().irl_ccmm_set_mirror_parts(self.handle, count))
+
+    def synth_part(self, part: int, seed: int, global_part: int, row0: int):
+        """Local part `part` = rows [row0, row0 + M) of global part global_part
+        of the synthetic database (row-block dealing)."""
+        self.ctx.check(capi.lib().irl_ccmm_synth_part(self.handle, part, seed, global_part, row0))
 
     def set_mirror_slot(self, slot: int):
         """Receive slot of the peers' buffers the next runs store into."""

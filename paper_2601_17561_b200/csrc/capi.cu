@@ -833,9 +833,11 @@ int irl_rescale_residues(irl_ctx* ctx, const uint16_t* in, size_t ld_in, size_t 
         t.add[i] = round ? static_cast<uint32_t>((delta / 2) % m) : 0;
         if (i < nmod - drop) {
             if (!inv(delta, m, &t.dinv[i])) return set_err(ctx, IRL_ERR_NOT_COPRIME, "CRT basis is not coprime");
+            t.dinv_sh[i] = static_cast<uint32_t>((static_cast<unsigned long long>(t.dinv[i]) << 32) / m);
         } else {
             t.cq[i] = delta / m;
             if (!inv(t.cq[i], m, &t.cinv[i])) return set_err(ctx, IRL_ERR_NOT_COPRIME, "CRT basis is not coprime");
+            t.cinv_sh[i] = static_cast<uint32_t>((static_cast<unsigned long long>(t.cinv[i]) << 32) / m);
         }
     }
     for (size_t jj = 0; jj < drop && jj < 3; ++jj) {

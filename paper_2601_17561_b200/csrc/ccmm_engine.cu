@@ -46,6 +46,7 @@ struct irl_ccmm {
     uint16_t* recv = nullptr;
     size_t recv_n = 0;
     size_t mirror_part = 0, mirror_n = 0, n_mirror = 0, mirror_slot = 0;
+    size_t mirror_parts = 1;  // local parts [mirror_part, mirror_part + mirror_parts) are mirrored
     uint16_t* mirror[kMaxMirrors] = {};
     bool mirror_ipc[kMaxMirrors] = {};
     uint16_t* mc_mirror = nullptr;  // NVLS multicast address of the receive buffers (irl_ccmm_set_mirror_multicast)
@@ -147,13 +148,17 @@ int irl_ccmm_destroy(irl_ccmm* e) {
 // tiles straight into the peers' receive buffers over NVLink ------------------
 
 int irl_ccmm_alloc_recv(irl_ccmm* e, size_t n, void** dev_ptr, uint8_t* ipc_handle) {
-    if (!e || !dev_ptr) return IRL_ERR_INVALID_ARGUMENT;
+    return irl_ccmm_alloc_recv_parts(e, n, 1, dev_ptr, ipc_handle);
+}
+
+int irl_ccmm_alloc_recv_parts(irl_ccmm* e, size_t n, size_t parts, void** dev_ptr, uint8_t* ipc_handle) {
+    if (!e || !dev_ptr || parts == 0) return IRL_ERR_INVALID_ARGUMENT;
     irl_ctx* ctx = e->ctx;
     Guard g(ctx);
     if (n == 0 || n > e->max_n) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: receive width out of range");
     if (e->recv) cudaFree(e->recv);
     e->recv = nullptr;
-    const size_t slot_bytes = e->nmod * n * e->M * sizeof(uint16_t);
+    const size_t slot_bytes = parts * e->nmod * n * e->M * sizeof(uint16_t);
     IRL_CK(ctx, cudaMalloc(&e->recv, IRL_RECV_SLOTS * slot_bytes));
     IRL_CK(ctx, cudaMemset(e->recv, 0, IRL_RECV_SLOTS * slot_bytes));
     e->recv_n = n;
@@ -193,6 +198,7 @@ static int set_mirrors(irl_ccmm* e, size_t part, size_t n, uint16_t* const* ptrs
     }
     e->n_mirror = count;
     e->mirror_part = part;
+    e->mirror_parts = 1;
     e->mirror_n = n;
     return IRL_OK;
 }
@@ -207,6 +213,15 @@ int irl_ccmm_set_mirror_ptrs(irl_ccmm* e, size_t part, size_t n, uint16_t* const
     if (!e || (count && !dev_ptrs)) return IRL_ERR_INVALID_ARGUMENT;
     Guard g(e->ctx);
     return set_mirrors(e, part, n, dev_ptrs, nullptr, count);
+}
+
+int irl_ccmm_set_mirror_parts(irl_ccmm* e, size_t count) {
+    if (!e) return IRL_ERR_INVALID_ARGUMENT;
+    Guard g(e->ctx);
+    if (count == 0 || e->mirror_part + count > e->parts)
+        return set_err(e->ctx, IRL_ERR_INVALID_ARGUMENT, "ccmm: mirrored part range out of range");
+    e->mirror_parts = count;
+    return IRL_OK;
 }
 
 int irl_ccmm_set_mirror_slot(irl_ccmm* e, size_t slot) {
@@ -404,6 +419,17 @@ int irl_ccmm_synth_db(irl_ccmm* e, uint64_t seed, uint32_t first_part) {
     return IRL_OK;
 }
 
+int irl_ccmm_synth_part(irl_ccmm* e, size_t part, uint64_t seed, uint32_t global_part, uint32_t row0) {
+    if (!e) return IRL_ERR_INVALID_ARGUMENT;
+    irl_ctx* ctx = e->ctx;
+    Guard g(ctx);
+    if (part >= e->parts) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: part index out of range");
+    IRL_LAUNCH(ctx, launch_synth_planes(seed, global_part, 1, uint32_t(e->M), uint32_t(e->K), e->mt,
+                                        e->db + part * e->nmod * 2 * e->M * e->ldk, e->ldk, ctx->stream, row0));
+    IRL_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    return IRL_OK;
+}
+
 // PPMMs of parts [part0, part0 + nparts) for moduli [m0, m0 + nm); `out`
 // points at the [part0][0][0][0] corner of a [parts][nmod][n][M] tensor.
 static int ccmm_parts(irl_ccmm* e, size_t n, size_t part0, size_t nparts, uint16_t* out,
@@ -426,11 +452,14 @@ static int ccmm_parts(irl_ccmm* e, size_t n, size_t part0, size_t nparts, uint16
     L.out_part_elems = e->nmod * n * e->M;
     L.progress = e->progress;
     L.part_done = part_done;
-    if ((e->n_mirror || e->mc_mirror) && n == e->mirror_n && e->mirror_part >= part0 &&
-        e->mirror_part < part0 + nparts) {
+    const size_t mfirst = std::max(part0, e->mirror_part);
+    const size_t mlast = std::min(part0 + nparts, e->mirror_part + e->mirror_parts);
+    if ((e->n_mirror || e->mc_mirror) && n == e->mirror_n && mfirst < mlast) {
         L.n_mirror = static_cast<uint32_t>(e->n_mirror);
-        L.mirror_part = static_cast<uint32_t>(e->mirror_part - part0);
-        const size_t at = (e->mirror_slot * e->nmod + m0) * n * e->M;  // [slot][modulus][n][M]
+        L.mirror_part = static_cast<uint32_t>(mfirst - part0);
+        L.mirror_parts = static_cast<uint32_t>(mlast - mfirst);
+        // peer buffers: [slot][mirrored part][modulus][n][M]
+        const size_t at = ((e->mirror_slot * e->mirror_parts + (mfirst - e->mirror_part)) * e->nmod + m0) * n * e->M;
         for (size_t i = 0; i < e->n_mirror; ++i) L.mirror[i] = e->mirror[i] + at;
         if (e->mc_mirror) L.mc_mirror = e->mc_mirror + at;
     }

@@ -328,6 +328,76 @@ __global__ void __launch_bounds__(256) rescale_vec_kernel(const uint16_t* __rest
     }
 }
 
+// a * w mod m for a constant w < m (Shoup): w_sh = floor(w 2^32 / m), any a <
+// 2^32; the result lies in [0, 2m) (one conditional subtraction from reduced).
+__device__ __forceinline__ uint32_t shoup_mul(uint32_t a, uint32_t w, uint32_t w_sh, uint32_t m) {
+    return a * w - __umulhi(a, w_sh) * m;
+}
+
+// Vectorised rescale, all 32-bit: r = x' mod Delta once per element (64-bit,
+// from the dropped residues), then per kept modulus r mod m_i from its two
+// 32-bit halves (two Barrett reductions) and one Shoup multiplication by
+// Delta^-1 -- 8 integer multiplies per output residue instead of four 64-bit
+// multiply-accumulates plus a 35-bit reduction.
+__global__ void __launch_bounds__(256) rescale_r_kernel(const uint16_t* __restrict__ in, size_t ld_in,
+                                                        size_t groups, const __grid_constant__ RescaleTable t,
+                                                        uint16_t* __restrict__ out, size_t ld_out) {
+    const size_t g = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (g >= groups) return;
+    const size_t e0 = g * 8;
+    const uint32_t keep = t.nmod - t.drop;
+    unsigned long long S[8];
+#pragma unroll
+    for (int l = 0; l < 8; ++l) S[l] = 0;
+    for (uint32_t j = keep; j < t.nmod; ++j) {
+        const uint32_t m = t.m[j], ad = t.add[j], ci = t.cinv[j], cs = t.cinv_sh[j];
+        const unsigned long long cq = t.cq[j];
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(in + j * ld_in + e0));
+        const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int l = 0; l < 8; ++l) {
+            uint32_t xa = ((qw[l / 2] >> (16 * (l % 2))) & 0xFFFFu) + ad;  // < 2m
+            xa = min(xa, xa - m);
+            uint32_t u = shoup_mul(xa, ci, cs, m);
+            u = min(u, u - m);
+            S[l] += static_cast<unsigned long long>(u) * cq;
+        }
+    }
+    uint32_t rlo[8], rhi[8];
+#pragma unroll
+    for (int l = 0; l < 8; ++l) {
+        const unsigned long long k = (S[l] >= t.delta) + (S[l] >= 2 * t.delta);
+        const unsigned long long r = S[l] - k * t.delta;  // x' mod Delta < 2^48
+        rlo[l] = static_cast<uint32_t>(r);
+        rhi[l] = static_cast<uint32_t>(r >> 32);
+    }
+    for (uint32_t i0 = 0; i0 < keep; i0 += 4) {
+        uint4 q[4];
+#pragma unroll
+        for (int gg = 0; gg < 4; ++gg)
+            q[gg] = i0 + gg < keep ? __ldg(reinterpret_cast<const uint4*>(in + (i0 + gg) * ld_in + e0))
+                                   : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int gg = 0; gg < 4; ++gg) {
+            const uint32_t i = i0 + gg;
+            if (i >= keep) break;
+            const uint32_t m = t.m[i], mg = t.magic[i], c32 = t.c32[i], ad = t.add[i];
+            const uint32_t dv = t.dinv[i], ds = t.dinv_sh[i];
+            const uint32_t qw[4] = {q[gg].x, q[gg].y, q[gg].z, q[gg].w};
+            uint32_t y[8];
+#pragma unroll
+            for (int l = 0; l < 8; ++l) {
+                const uint32_t x = (qw[l / 2] >> (16 * (l % 2))) & 0xFFFFu;
+                const uint32_t rm = mod_u32(rhi[l] * c32 + mod_u32(rlo[l], m, mg), m, mg);  // r mod m_i
+                uint32_t v = shoup_mul(x + ad + m - rm, dv, ds, m);  // (x' - r) Delta^-1, in [0, 2m)
+                y[l] = min(v, v - m);
+            }
+            *reinterpret_cast<uint4*>(out + i * ld_out + e0) =
+                make_uint4(y[0] | (y[1] << 16), y[2] | (y[3] << 16), y[4] | (y[5] << 16), y[6] | (y[7] << 16));
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) rescale_kernel(const uint16_t* __restrict__ in, size_t ld_in, size_t count,
                                                       const __grid_constant__ RescaleTable t,
                                                       uint16_t* __restrict__ out, size_t ld_out) {
@@ -362,52 +432,78 @@ __global__ void __launch_bounds__(256) rescale_kernel(const uint16_t* __restrict
 // ---------------------------------------------------------------------------
 struct BigSplitArgs {
     ModTable mt;
-    uint32_t coef[kMaxModuli][kMaxWidth];  // 256^j mod m_i
+    uint32_t coef[kMaxModuli][kMaxWidth / 4];  // 2^(32 k) mod m_i
+    uint32_t c32[kMaxModuli];                  // 2^32 mod m_i
 };
 
-__global__ void __launch_bounds__(256) split_bigint_kernel(
+// Residue of a width-byte little-endian integer held as 32-bit words w[k]:
+// sum_k w_k (2^32k mod m) accumulated exactly in 64 bits (< 12 * 2^48), then
+// reduced through its two 32-bit halves.
+__device__ __forceinline__ uint32_t words_mod(const uint32_t* w, uint32_t nw, const uint32_t* coef, uint32_t m,
+                                              uint32_t magic, uint32_t c32) {
+    unsigned long long acc = 0;
+#pragma unroll
+    for (uint32_t k = 0; k < kMaxWidth / 4; ++k)
+        if (k < nw) acc += static_cast<unsigned long long>(w[k]) * coef[k];
+    const uint32_t hi = mod_u32(static_cast<uint32_t>(acc >> 32), m, magic);  // < m < 2^16
+    return mod_u32(hi * c32 + mod_u32(static_cast<uint32_t>(acc), m, magic), m, magic);
+}
+
+// Entries -> residues -> digit planes, 256 entries per block. The DB layout
+// (transpose = 0) stages the block's 256 * width contiguous bytes through
+// shared memory with 16-byte loads; each thread then folds its entry as 32-bit
+// words (12 wide multiply-adds per modulus for the 46-byte paper width,
+// instead of 46 byte multiply-adds). Plane writes are coalesced along K.
+__global__ void __launch_bounds__(256) split_bigint_words_kernel(
     const uint8_t* __restrict__ in, uint32_t width, uint32_t rows, uint32_t cols, int transpose,
     const __grid_constant__ BigSplitArgs a, int8_t* __restrict__ planes, size_t ldk,
     uint32_t dst_rows, uint32_t dst_row0, int32_t* __restrict__ raw_out, SplitStats* stats) {
-    const size_t gid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    __shared__ __align__(16) uint8_t stage[256 * kMaxWidth];
     const size_t total = static_cast<size_t>(rows) * cols;
+    const size_t base = static_cast<size_t>(blockIdx.x) * 256;
+    const size_t gid = base + threadIdx.x;
     const bool ok = gid < total;
-    // transpose: threads walk k fastest so plane writes stay coalesced.
+    const uint32_t nw = (width + 3) / 4;
+    uint32_t w[kMaxWidth / 4];
+#pragma unroll
+    for (uint32_t k = 0; k < kMaxWidth / 4; ++k) w[k] = 0;
     uint32_t r = 0, cidx = 0;
-    if (ok) {
-        if (transpose) {
-            r = static_cast<uint32_t>(gid % rows);     // k
-            cidx = static_cast<uint32_t>(gid / rows);  // n
+    if (!transpose) {
+        const size_t nbytes = (total - base < 256 ? total - base : 256) * width;
+        const uint8_t* src = in + base * width;
+        if ((reinterpret_cast<uintptr_t>(src) & 15) == 0 && nbytes % 16 == 0) {
+            for (size_t o = threadIdx.x * 16; o < nbytes; o += 256 * 16)
+                *reinterpret_cast<uint4*>(stage + o) = __ldg(reinterpret_cast<const uint4*>(src + o));
         } else {
+            for (size_t o = threadIdx.x; o < nbytes; o += 256) stage[o] = src[o];
+        }
+        __syncthreads();
+        if (ok) {
+            const uint8_t* b = stage + threadIdx.x * width;
+            for (uint32_t j = 0; j < width; ++j) w[j >> 2] |= static_cast<uint32_t>(b[j]) << (8 * (j & 3));
             r = static_cast<uint32_t>(gid / cols);
             cidx = static_cast<uint32_t>(gid % cols);
         }
+    } else if (ok) {  // K x N query: threads walk k fastest so plane writes stay coalesced
+        r = static_cast<uint32_t>(gid % rows);     // k
+        cidx = static_cast<uint32_t>(gid / rows);  // n
+        const uint8_t* b = in + (static_cast<size_t>(r) * cols + cidx) * width;
+        for (uint32_t j = 0; j < width; ++j) w[j >> 2] |= static_cast<uint32_t>(b[j]) << (8 * (j & 3));
     }
-    uint8_t bytes[kMaxWidth];
-    if (ok) {
-        const uint8_t* src = in + (static_cast<size_t>(r) * cols + cidx) * width;
-#pragma unroll 8
-        for (uint32_t j = 0; j < width; ++j) bytes[j] = src[j];
-    }
+    const uint32_t prow = (transpose ? cidx : r) + dst_row0;
+    const uint32_t pcol = transpose ? r : cidx;
     for (uint32_t i = 0; i < a.mt.n; ++i) {
         const ModConst c = a.mt.mc[i];
         int32_t d0 = 0, d1 = 0, v = 0;
         if (ok) {
-            uint32_t s = 0;
-            for (uint32_t j = 0; j < width; ++j) s += bytes[j] * a.coef[i][j];
-            v = static_cast<int32_t>(mod_u32(s, c.m, c.magic_m));
-            if (c.e == 2) {
-                digit_split(static_cast<uint32_t>(v), c, d0, d1);
-            }
+            v = static_cast<int32_t>(words_mod(w, nw, a.coef[i], c.m, c.magic_m, a.c32[i]));
+            if (c.e == 2) digit_split(static_cast<uint32_t>(v), c, d0, d1);
         }
         if (c.e == 2) {
             if (ok) {
-                const uint32_t prow = (transpose ? cidx : r) + dst_row0;
-                const uint32_t pcol = transpose ? r : cidx;
-                const uint32_t prows = dst_rows;
-                int8_t* p0 = planes + (static_cast<size_t>(i) * 2 * prows + prow) * ldk + pcol;
+                int8_t* p0 = planes + (static_cast<size_t>(i) * 2 * dst_rows + prow) * ldk + pcol;
                 p0[0] = static_cast<int8_t>(d0);
-                p0[static_cast<size_t>(prows) * ldk] = static_cast<int8_t>(d1);
+                p0[static_cast<size_t>(dst_rows) * ldk] = static_cast<int8_t>(d1);
             }
             if (stats) {
                 warp_max_atomic(abs(d0), &stats->v[i][0]);
@@ -509,7 +605,7 @@ __host__ __device__ __forceinline__ uint32_t synth_residue(uint64_t seed_mixed, 
 }
 
 __global__ void __launch_bounds__(256) synth_planes_kernel(uint64_t seed_mixed, uint32_t part0,
-                                                           uint32_t rows, uint32_t cols,
+                                                           uint32_t row0, uint32_t rows, uint32_t cols,
                                                            uint32_t groups,
                                                            const __grid_constant__ ModTable mt,
                                                            int8_t* __restrict__ planes,
@@ -524,7 +620,7 @@ __global__ void __launch_bounds__(256) synth_planes_kernel(uint64_t seed_mixed, 
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
         if (c0 + j < cols) {
-            const uint32_t v = synth_residue(seed_mixed, part0 + g, i, r, c0 + j, c.m);
+            const uint32_t v = synth_residue(seed_mixed, part0 + g, i, row0 + r, c0 + j, c.m);
             split_value(v, c, d0[j], d1[j]);
         } else {
             d0[j] = 0;
@@ -742,13 +838,15 @@ cudaError_t launch_split_bigint(const uint8_t* in, uint32_t width, uint32_t rows
     BigSplitArgs a{};
     a.mt = mt;
     for (uint32_t i = 0; i < mt.n; ++i) {
-        uint64_t pw = 1 % mt.mc[i].m;
-        for (uint32_t j = 0; j < width; ++j) {
-            a.coef[i][j] = static_cast<uint32_t>(pw);
-            pw = (pw * 256) % mt.mc[i].m;
+        const uint64_t m = mt.mc[i].m;
+        a.c32[i] = static_cast<uint32_t>((1ull << 32) % m);
+        uint64_t pw = 1 % m;
+        for (uint32_t k = 0; k < kMaxWidth / 4; ++k) {
+            a.coef[i][k] = static_cast<uint32_t>(pw);
+            pw = (pw << 32) % m;
         }
     }
-    split_bigint_kernel<<<blocks_for(total, 256), 256, 0, s>>>(
+    split_bigint_words_kernel<<<blocks_for(total, 256), 256, 0, s>>>(
         in, width, rows, cols, transpose, a, planes, ldk, dst_rows, dst_row0, raw_out, stats);
     return cudaGetLastError();
 }
@@ -758,7 +856,11 @@ cudaError_t launch_rescale(const uint16_t* in, size_t ld_in, size_t count, const
     if (count == 0) return cudaSuccess;
     if (count % 8 == 0 && ld_in % 8 == 0 && ld_out % 8 == 0 && t.drop <= 3 &&
         ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
-        rescale_vec_kernel<<<blocks_for(count / 8, 256), 256, 0, s>>>(in, ld_in, count / 8, t, out, ld_out);
+        static const bool r_form = std::getenv("IRL_RESCALE_FOLDED") == nullptr;
+        if (r_form)
+            rescale_r_kernel<<<blocks_for(count / 8, 256), 256, 0, s>>>(in, ld_in, count / 8, t, out, ld_out);
+        else
+            rescale_vec_kernel<<<blocks_for(count / 8, 256), 256, 0, s>>>(in, ld_in, count / 8, t, out, ld_out);
         return cudaGetLastError();
     }
     rescale_kernel<<<blocks_for(count, 256), 256, 0, s>>>(in, ld_in, count, t, out, ld_out);
@@ -780,11 +882,11 @@ cudaError_t launch_crt_lift(const uint16_t* res, uint32_t M, uint32_t N, const C
 
 cudaError_t launch_synth_planes(uint64_t seed, uint32_t part0, uint32_t parts, uint32_t rows,
                                 uint32_t cols, const ModTable& mt, int8_t* planes, size_t ldk,
-                                cudaStream_t s) {
+                                cudaStream_t s, uint32_t row0) {
     if (rows == 0 || parts == 0 || mt.n == 0) return cudaSuccess;
     const uint32_t groups = static_cast<uint32_t>(ldk / 16);
     const dim3 grid(blocks_for(static_cast<size_t>(rows) * groups, 256), mt.n, parts);
-    synth_planes_kernel<<<grid, 256, 0, s>>>(mix64(seed), part0, rows, cols, groups, mt, planes, ldk);
+    synth_planes_kernel<<<grid, 256, 0, s>>>(mix64(seed), part0, row0, rows, cols, groups, mt, planes, ldk);
     return cudaGetLastError();
 }
 

@@ -82,15 +82,18 @@ struct RescaleTable {
     // u_j = (x_j + add_j) cinv_j mod m_j, k = floor(sum_j u_j cq_j / Delta),
     // w[j][i] = -(cq_j dinv_i) mod m_i (j indexes the dropped moduli)
     uint32_t w[3][kMaxModuli];
+    // Shoup constants floor(c * 2^32 / m) of dinv (kept) and cinv (dropped)
+    uint32_t dinv_sh[kMaxModuli], cinv_sh[kMaxModuli];
 };
 cudaError_t launch_rescale(const uint16_t* in, size_t ld_in, size_t count, const RescaleTable& t, uint16_t* out,
                            size_t ld_out, cudaStream_t s);
 
 // Synthetic database planes: planes[g][i][d][r][ldk] from the counter RNG,
 // residue = synth(seed, stream=part0+g, plane=i, row, col, m_i).
+// Rows [row0, row0 + rows) of parts part0.. (row0: a row block of a larger part).
 cudaError_t launch_synth_planes(uint64_t seed, uint32_t part0, uint32_t parts, uint32_t rows,
                                 uint32_t cols, const ModTable& mt, int8_t* planes, size_t ldk,
-                                cudaStream_t s);
+                                cudaStream_t s, uint32_t row0 = 0);
 
 // int32 GEMM with int32 (wrapping) accumulation, row-major: C = A B.
 cudaError_t launch_gemm_i32(const int32_t* a, const int32_t* b, int32_t* c, uint32_t m,

@@ -78,6 +78,7 @@ struct PpmmLaunch {
     uint16_t* mirror[kMaxMirrors] = {};
     uint32_t n_mirror = 0;
     uint32_t mirror_part = 0;
+    uint32_t mirror_parts = 1;  // parts [mirror_part, mirror_part + mirror_parts), back to back in the mirrors
     // NVLS multicast mirror: a multicast address (cuMulticastCreate, bound to
     // one receive buffer per GPU); the epilogue stores each pair of output rows
     // once with multimem.st and the switch delivers it to every bound GPU.

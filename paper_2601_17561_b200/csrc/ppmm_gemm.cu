@@ -103,7 +103,7 @@ struct __align__(64) GemmArgs {
     int32_t* out_i32[2];              // kMode == kModeInner: acc1 / acc2 as int32 [n][m] (nullable)
     IrisMatchOut iris;                // kMode == kModeIrisMatch
     uint16_t* mirror[kMaxMirrors];    // peer copies of part mirror_part's outputs (see PpmmLaunch)
-    uint32_t n_mirror, mirror_part;
+    uint32_t n_mirror, mirror_part, mirror_parts;
     uint16_t* mc_mirror;              // multicast address of part mirror_part's copies (see PpmmLaunch)
     uint32_t* part_done;              // optional [nprimes][parts] count of (epilogue warp, tile) completions
     uint32_t* progress;               // [clusters] K blocks issued by each pair's leader producer
@@ -565,8 +565,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             uint16_t* out = args.out + tc.part * args.out_part +
                             static_cast<size_t>(tc.prime) * args.N * args.M +
                             m;
-            const bool mirror_tile = (args.n_mirror != 0 || args.mc_mirror != nullptr) && tc.part == args.mirror_part;
-            const bool mc_tile = args.mc_mirror != nullptr && tc.part == args.mirror_part;
+            // parts [mirror_part, mirror_part + mirror_parts) are mirrored; the
+            // peers' buffers hold them back to back in the output layout
+            const bool mirror_tile = (args.n_mirror != 0 || args.mc_mirror != nullptr) &&
+                                     tc.part - args.mirror_part < args.mirror_parts;
+            const bool mc_tile = args.mc_mirror != nullptr && mirror_tile;
+            const size_t mpart = mirror_tile ? static_cast<size_t>(tc.part - args.mirror_part) * args.out_part : 0;
             const uint32_t lane_base = tmem_base + ((quarter * 32u) << 16);
             for (uint32_t c = cgrp * 16; c < tc.n_size; c += 16 * kEpiGroups) {
                 uint32_t a1[16], a2[16];
@@ -639,7 +643,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                     // compute but do not store); even lanes store rows (m, m+1)
                     // as one 32-bit multimem.st, which the switch replicates
                     uint16_t* dst = out + static_cast<size_t>(tc.n0 + c) * args.M;
-                    const size_t moff = static_cast<size_t>(tc.prime) * args.N * args.M +
+                    const size_t moff = mpart + static_cast<size_t>(tc.prime) * args.N * args.M +
                                         static_cast<size_t>(tc.n0 + c) * args.M + m;
 #pragma unroll
                     for (int jj = 0; jj < 16; ++jj) {
@@ -678,7 +682,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                 }
                 uint16_t* dst = out + static_cast<size_t>(tc.n0 + c) * args.M;
                 // offset of this chunk inside its part (same in the peers' mirrors)
-                const size_t moff = static_cast<size_t>(tc.prime) * args.N * args.M +
+                const size_t moff = mpart + static_cast<size_t>(tc.prime) * args.N * args.M +
                                     static_cast<size_t>(tc.n0 + c) * args.M + m;
                 if (!args.accumulate && tc.n0 + c + 16 <= args.N) {
                     // fast path: whole 16-column chunk in range, overwrite
@@ -957,6 +961,7 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     args.part_done = L.part_done;
     args.n_mirror = L.n_mirror;
     args.mirror_part = L.mirror_part;
+    args.mirror_parts = L.mirror_parts;
     args.mc_mirror = L.mc_mirror;
     if (L.mc_mirror && (L.mode != kModePsq || (L.M & 1u) != 0)) return cudaErrorInvalidValue;
     for (uint32_t i = 0; i < L.n_mirror; ++i) args.mirror[i] = L.mirror[i];

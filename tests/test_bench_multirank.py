@@ -67,3 +67,26 @@ def test_bench_multirank_moddown_exchange():
     assert d["exchange"]["kind"].startswith("NCCL") and d["exchange"]["bytes"] == 21 * 31 * 32 * 2048 * 2
     assert d["dist_check"]["bit_exact_all_ranks"] and d["dist_check"]["a_part_identical_all_ranks"]
     assert d["e2e"]["outputs_equal_device_step"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("exchange", ["auto", "broadcast"])
+def test_bench_multirank_row_blocks(exchange):
+    """b-parts taller than the a-part (c5's shape, scaled down): balanced
+    row-block dealing (dist.deal_blocks), the a-part spanning several blocks on
+    rank 0 and mirrored / broadcast as a whole; every rank bit-exact."""
+    world = 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", f"--master-port={_port()}", str(ROOT / "bench.py"), "--gpus", str(world),
+           "--steps", "2", "--warmup", "3", "--backend", "gloo", "--same-device", "--parts", "4",
+           "--rows", "2048", "--b-rows", "8192", "--k", "4096", "--no-int8-ref", "--exchange", exchange]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT,
+                       env={**os.environ, "OMP_NUM_THREADS": "1"})
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
+    assert d["dealing"]["kind"].startswith("row blocks") and d["dealing"]["block_rows"] == 512
+    assert d["dealing"]["units_per_rank"] == [26, 26]   # (4 + 3 * 16) blocks of 512 rows
+    assert d["exchange"]["note"] is None and d["exchange"]["bytes"] == 4 * 24 * 31 * 32 * 512 * 2
+    assert d["dist_check"]["bit_exact_all_ranks"] and d["dist_check"]["a_part_identical_all_ranks"]
+    assert d["e2e"]["outputs_equal_device_step"]
+    assert d["config"]["templates_per_b_part"] == 8192

@@ -118,3 +118,65 @@ def test_sharded_step_mirror_signal_gloo():
     assert results[0][1] == 0 and results[1][1] == 0
     with pytest.raises(ValueError):
         ShardedStep(0, 1, lambda a, b: None, lambda: None, exchange="nccl")
+
+
+# ---------------------------------------------- row-block dealing (c5) -------
+
+def test_deal_blocks_balanced_and_complete():
+    from paper_2601_17561_b200.dist import deal_blocks
+    for a_rows, b_rows in [(1 << 14, 1 << 17), (1 << 14, 1 << 15), (2048, 8192), (1 << 14, 1 << 14)]:
+        for world in (1, 2, 3, 4, 8):
+            deals = [deal_blocks(r, world, a_rows, b_rows) for r in range(world)]
+            block = deals[0].block
+            assert block % 256 == 0 and a_rows % block == 0 and b_rows % block == 0
+            got = [b for d in deals for b in d.blocks]
+            want = [(0, r) for r in range(0, a_rows, block)] + \
+                   [(p, r) for p in range(1, PAPER_PARTS) for r in range(0, b_rows, block)]
+            assert got == want                                   # every row once, in order
+            counts = [d.count for d in deals]
+            assert max(counts) - min(counts) <= 1                # balanced to one block
+            assert deals[0].a_blocks == a_rows // block          # the a-part stays on rank 0
+            assert all(d.a_blocks == 0 for d in deals[1:])
+            assert deals[0].locate(0, a_rows - 1) == (a_rows // block - 1, block - 1)
+    # c5 on 8 GPUs: the largest share falls from a whole 2^17-row b-part to
+    # 29 blocks of 4096 rows (the even split is 116736 rows)
+    c5 = [deal_blocks(r, 8, 1 << 14, 1 << 17) for r in range(8)]
+    assert max(d.count * d.block for d in c5) == 118784 < (1 << 17)
+
+
+def _worker_blocks(rank, world, port, results):
+    # ShardedStep over row blocks: the owner runs its a-part blocks first, and
+    # the broadcast carries all of them
+    from paper_2601_17561_b200.dist import PartRange, deal_blocks
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    bd = deal_blocks(rank, world, 512, 1024, parts=4, block=256)
+    calls = []
+    out = torch.zeros((bd.count, 4), dtype=torch.int32)
+    a_units = max(1, bd.a_blocks)
+    recv = torch.zeros((a_units if rank == 0 else 2, 4), dtype=torch.int32)
+
+    def run_parts(first_local, count):
+        calls.append((first_local, count))
+        for j in range(first_local, first_local + count):
+            gp, r0 = bd.blocks[j]
+            out[j] = torch.tensor([gp, r0, rank, 7], dtype=torch.int32)
+
+    def a_out():
+        return out[:a_units] if rank == 0 else recv
+
+    step = ShardedStep(rank, world, run_parts, a_out, local=PartRange(0, bd.count), a_parts=a_units)
+    step().wait()
+    results[rank] = (calls, bd.count, recv.tolist() if rank else out[:a_units].tolist())
+    dist.destroy_process_group()
+
+
+def test_sharded_step_row_blocks_gloo():
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_worker_blocks, args=(2, _free_port(), results), nprocs=2, join=True)
+    # 2 + 3 * 4 = 14 blocks of 256 rows: 7 per rank; rank 0 runs its 2 a-part blocks first
+    assert results[0][0] == [(0, 2), (2, 5)] and results[1][0] == [(0, 7)]
+    assert results[0][1] == results[1][1] == 7
+    assert results[1][2] == results[0][2] == [[0, 0, 0, 7], [0, 256, 0, 7]]

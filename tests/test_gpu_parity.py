@@ -697,3 +697,35 @@ def test_ccmm_group_nvls_multicast_mirror(k):
         assert np.array_equal(g.a_part(0, ptrs3[0], 64).cpu().numpy().view(np.uint16), out3[0])
     finally:
         g.close()
+
+
+def test_ccmm_row_blocks_synth_and_multi_part_mirror():
+    """Row-block units (dist.deal_blocks): synth_part fills a unit with rows
+    [row0, row0 + M) of a taller global part, identical to the same rows of a
+    whole-part engine; a mirror spanning several units (an a-part dealt as
+    blocks) lands back to back in the peer buffer, in the double-buffered slot."""
+    import torch
+    from paper_2601_17561_b200.ccmm import CcmmEngine, staging_tensors, synth_query
+    k, n, blk = 640, 64, 256
+    whole = CcmmEngine(parts=2, m=4 * blk, k=k, max_n=n)
+    whole.synth_db(seed=6)
+    q = synth_query(7, k, n, whole.moduli)
+    want = whole.run(q)                      # [2][nmod][n][1024]
+    whole.close()
+    units = [(0, 0), (0, 256), (0, 512), (1, 768), (1, 0)]
+    eng = CcmmEngine(parts=len(units), m=blk, k=k, max_n=n)
+    for j, (gp, r0) in enumerate(units):
+        eng.synth_part(j, 6, gp, r0)
+    view, _ = eng.alloc_recv(n, parts=3)
+    assert tuple(view.shape) == (2, 3, eng.nmod, n, blk)
+    eng.set_mirror_ptrs(0, n, [view])
+    eng.set_mirror_parts(3)
+    eng.set_mirror_slot(1)
+    got = eng.run(q)
+    torch.cuda.synchronize()
+    for j, (gp, r0) in enumerate(units):
+        assert np.array_equal(got[j], want[gp][:, :, r0:r0 + blk]), j
+    mv = view.cpu().numpy().view(np.uint16)
+    assert np.array_equal(mv[1], got[:3]) and not mv[0].any()
+    with pytest.raises(Exception):
+        eng.set_mirror_parts(6)
