@@ -388,8 +388,12 @@ __global__ void __launch_bounds__(256) rescale_r_kernel(const uint16_t* __restri
 #pragma unroll
             for (int l = 0; l < 8; ++l) {
                 const uint32_t x = (qw[l / 2] >> (16 * (l % 2))) & 0xFFFFu;
-                const uint32_t rm = mod_u32(rhi[l] * c32 + mod_u32(rlo[l], m, mg), m, mg);  // r mod m_i
-                uint32_t v = shoup_mul(x + ad + m - rm, dv, ds, m);  // (x' - r) Delta^-1, in [0, 2m)
+                // r mod m_i, left in [0, 2m) by both (unconditioned) Barrett steps:
+                // rhi * c32 + [0, 2m) < 2^32 since rhi, c32 < 2^16
+                const uint32_t r1 = rlo[l] - __umulhi(rlo[l], mg) * m;
+                const uint32_t t = rhi[l] * c32 + r1;
+                const uint32_t rm = t - __umulhi(t, mg) * m;
+                uint32_t v = shoup_mul(x + ad + 2 * m - rm, dv, ds, m);  // (x' - r) Delta^-1, in [0, 2m)
                 y[l] = min(v, v - m);
             }
             *reinterpret_cast<uint4*>(out + i * ld_out + e0) =
