@@ -91,3 +91,15 @@ def test_cpp_ccmm_mirror_reference_case(ccmm_binary):
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
+
+
+def test_cpp_costmodel_mirror_reference_vectors():
+    """irislab_b200/costmodel.hpp against the reference's test_costmodel.cpp
+    vectors (36/18 GiB, 62 packed cts, 37 clusters at 2^22) and the B200
+    residency plan (a whole 8-part cluster per 180 GB GPU). Header-only: CPU."""
+    out = ROOT / "build" / "test_costmodel_b200"
+    out.parent.mkdir(exist_ok=True)
+    subprocess.run(["/usr/bin/g++", "-O2", "-std=c++17", f"-I{PKG / 'host'}",
+                    str(ROOT / "tests/cpp/test_costmodel_b200.cpp"), "-o", str(out)], check=True)
+    r = subprocess.run([str(out)], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0 and "0 failed" in r.stdout, r.stdout
