@@ -50,18 +50,6 @@ bool iris_f4(size_t d) {
 size_t plane_kbytes(size_t d) { return iris_f4(d) ? (d + 1) / 2 : d; }
 size_t plane_ldk(size_t d) { return round16(plane_kbytes(d)); }
 
-// Cluster shape of the iris launches: 1 x 4 pairs (the four pairs of an
-// m-block share its database tile by multicast); IRL_IRIS_CLUSTER=2x4 also
-// shares each query tile between two m-blocks (FP4 only; experiment knob).
-void iris_cluster(PpmmLaunch& L, size_t d) {
-    static const char* env = std::getenv("IRL_IRIS_CLUSTER");
-    int pm = 1, pn = 4;
-    if (env && iris_f4(d) && std::sscanf(env, "%dx%d", &pm, &pn) == 2) {
-        L.cluster_pm = pm;
-        L.cluster_pn = pn;
-    }
-}
-
 // Column split of the FP4 query batch. A 1 x 4 cluster covers four 240-column
 // tiles (960 columns) per pass over the database; a remainder (992 = 960 + 32
 // for the paper's batch) would cost a second, mostly padding pass of the
@@ -178,7 +166,6 @@ int inner_overlap_gemm(irl_ctx* ctx, const int8_t* xp, const int8_t* yp, size_t 
         L.nprimes = 1;
         L.mc[0] = make_modconst(2, 1);  // unused by the inner modes
         L.progress = progress;
-        iris_cluster(L, d);
         if (c0 > 0) L.cluster_pm = L.cluster_pn = 1;  // the remainder on plain pairs
         IRL_LAUNCH(ctx, launch_ppmm_planes(L, s));
         ctx->launches += ppmm_kernels_last_launch() > 1 ? ppmm_kernels_last_launch() - 1 : 0;  // + filler
@@ -251,7 +238,6 @@ int match_fused(irl_ctx* ctx, const int8_t* xp, const int8_t* yp, size_t n_db, s
         L.nprimes = 1;
         L.mc[0] = make_modconst(2, 1);  // unused
         L.progress = progress;
-        iris_cluster(L, d);
         if (c0 > 0) L.cluster_pm = L.cluster_pn = 1;  // the remainder on plain pairs
         L.iris.lo = p_lo;
         L.iris.hi = p_hi;

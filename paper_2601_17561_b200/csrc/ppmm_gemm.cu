@@ -805,7 +805,6 @@ KernelFn kernel_for(int si, int mode = kModePsq) {
         switch (si) {
             case 0: return ppmm_i8_sm100_kernel<1, 1, kModeInnerF4>;
             case 2: return ppmm_i8_sm100_kernel<1, 4, kModeInnerF4>;
-            case 4: return ppmm_i8_sm100_kernel<2, 4, kModeInnerF4>;
             default: return nullptr;
         }
     }
@@ -813,7 +812,6 @@ KernelFn kernel_for(int si, int mode = kModePsq) {
         switch (si) {
             case 0: return ppmm_i8_sm100_kernel<1, 1, kModeIrisMatchF4>;
             case 2: return ppmm_i8_sm100_kernel<1, 4, kModeIrisMatchF4>;
-            case 4: return ppmm_i8_sm100_kernel<2, 4, kModeIrisMatchF4>;
             default: return nullptr;
         }
     }

@@ -1,9 +1,9 @@
 """Registered-database iris match at the paper's scale (7 * 2^14 templates of
 d = 2^14, 32 eyes x 31 rotations), host query bits in, match bits out: median
 of --reps calls. Run once per setting of an environment knob (IRL_IRIS_I8,
-IRL_IRIS_CLUSTER, ...) and alternate processes for an A/B.
+IRL_IRIS_NO_SPLIT) and alternate processes for an A/B.
 
-    IRL_IRIS_CLUSTER=2x4 python profiles/iris_match_ab.py [--reps 20]
+    IRL_IRIS_I8=1 python profiles/iris_match_ab.py [--reps 20]
 """
 import argparse
 import json
@@ -40,7 +40,7 @@ def main():
         res, b, _ = db.match_packed(qc, qm, eyes, rho, Interval(0.35, 1.0))
         ts.append((time.perf_counter() - t0) * 1e3)
     digest = int(np.bitwise_xor.reduce(np.packbits(b).view(np.uint8)))
-    print(json.dumps({"cluster": os.environ.get("IRL_IRIS_CLUSTER", "1x4"), "i8": bool(os.environ.get("IRL_IRIS_I8")),
+    print(json.dumps({"no_split": bool(os.environ.get("IRL_IRIS_NO_SPLIT")), "i8": bool(os.environ.get("IRL_IRIS_I8")),
                       "ms_median": statistics.median(ts), "ms_min": min(ts), "matches": int(b.sum()),
                       "res": res.tolist()[-2:], "bits_xor": digest}), flush=True)
     db.close()
