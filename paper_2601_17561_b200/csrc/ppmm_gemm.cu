@@ -570,7 +570,6 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             const bool mirror_tile = (args.n_mirror != 0 || args.mc_mirror != nullptr) &&
                                      tc.part - args.mirror_part < args.mirror_parts;
             const bool mc_tile = args.mc_mirror != nullptr && mirror_tile;
-            const size_t mpart = mirror_tile ? static_cast<size_t>(tc.part - args.mirror_part) * args.out_part : 0;
             const uint32_t lane_base = tmem_base + ((quarter * 32u) << 16);
             for (uint32_t c = cgrp * 16; c < tc.n_size; c += 16 * kEpiGroups) {
                 uint32_t a1[16], a2[16];
@@ -643,7 +642,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                     // compute but do not store); even lanes store rows (m, m+1)
                     // as one 32-bit multimem.st, which the switch replicates
                     uint16_t* dst = out + static_cast<size_t>(tc.n0 + c) * args.M;
-                    const size_t moff = mpart + static_cast<size_t>(tc.prime) * args.N * args.M +
+                    const size_t moff = static_cast<size_t>(tc.part - args.mirror_part) * args.out_part +
+                                        static_cast<size_t>(tc.prime) * args.N * args.M +
                                         static_cast<size_t>(tc.n0 + c) * args.M + m;
 #pragma unroll
                     for (int jj = 0; jj < 16; ++jj) {
@@ -682,7 +682,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                 }
                 uint16_t* dst = out + static_cast<size_t>(tc.n0 + c) * args.M;
                 // offset of this chunk inside its part (same in the peers' mirrors)
-                const size_t moff = mpart + static_cast<size_t>(tc.prime) * args.N * args.M +
+                const size_t moff = static_cast<size_t>(tc.part - args.mirror_part) * args.out_part +
+                                    static_cast<size_t>(tc.prime) * args.N * args.M +
                                     static_cast<size_t>(tc.n0 + c) * args.M + m;
                 if (!args.accumulate && tc.n0 + c + 16 <= args.N) {
                     // fast path: whole 16-column chunk in range, overwrite

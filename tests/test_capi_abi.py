@@ -101,3 +101,16 @@ def test_fold_params_struct_layout_matches_header(tmp_path):
     got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
     assert got[0] == C.sizeof(capi.FoldParams)
     assert got[1:] == [getattr(capi.FoldParams, f).offset for f in fields]
+
+
+def test_ppmm_psq_kernels_keep_everything_in_registers(lib):
+    """The mod-p^2 PPMM kernels (mode 0) must not touch local memory: a stack
+    frame for the TMEM accumulator arrays (seen once in r2, after a change
+    lengthened a live range in the epilogue) doubled the kernel's DRAM writes."""
+    sass = subprocess.run(["cuobjdump", "-sass", str(lib._name)], capture_output=True, text=True).stdout
+    funcs = sass.split("Function : ")
+    psq = [f for f in funcs if "ppmm_i8_sm100_kernelILi" in f.split("\n", 1)[0] and "ELi0EEE" in f.split("\n", 1)[0]]
+    assert len(psq) >= 4
+    for f in psq:
+        body = f.split("\n", 1)[1]
+        assert " STL" not in body and " LDL" not in body, f.split("\n", 1)[0]
