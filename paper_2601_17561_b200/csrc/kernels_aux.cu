@@ -453,6 +453,19 @@ __device__ __forceinline__ uint32_t words_mod(const uint32_t* w, uint32_t nw, co
     return mod_u32(hi * c32 + mod_u32(static_cast<uint32_t>(acc), m, magic), m, magic);
 }
 
+// Little-endian bytes b[0, width) as 32-bit words, zero above width; every
+// index compile-time so the words stay in registers.
+__device__ __forceinline__ void load_words(const uint8_t* b, uint32_t width, uint32_t* w) {
+#pragma unroll
+    for (uint32_t k = 0; k < kMaxWidth / 4; ++k) {
+        uint32_t v = 0;
+#pragma unroll
+        for (uint32_t t = 0; t < 4; ++t)
+            if (4 * k + t < width) v |= static_cast<uint32_t>(b[4 * k + t]) << (8 * t);
+        w[k] = v;
+    }
+}
+
 // Entries -> residues -> digit planes, 256 entries per block. The DB layout
 // (transpose = 0) stages the block's 256 * width contiguous bytes through
 // shared memory with 16-byte loads; each thread then folds its entry as 32-bit
@@ -471,7 +484,7 @@ __global__ void __launch_bounds__(256) split_bigint_words_kernel(
     uint32_t w[kMaxWidth / 4];
 #pragma unroll
     for (uint32_t k = 0; k < kMaxWidth / 4; ++k) w[k] = 0;
-    uint32_t r = 0, cidx = 0;
+    uint32_t r = 0, cidx = 0;  // (w: registers only -- every index below is compile-time)
     if (!transpose) {
         const size_t nbytes = (total - base < 256 ? total - base : 256) * width;
         const uint8_t* src = in + base * width;
@@ -483,16 +496,14 @@ __global__ void __launch_bounds__(256) split_bigint_words_kernel(
         }
         __syncthreads();
         if (ok) {
-            const uint8_t* b = stage + threadIdx.x * width;
-            for (uint32_t j = 0; j < width; ++j) w[j >> 2] |= static_cast<uint32_t>(b[j]) << (8 * (j & 3));
+            load_words(stage + threadIdx.x * width, width, w);
             r = static_cast<uint32_t>(gid / cols);
             cidx = static_cast<uint32_t>(gid % cols);
         }
     } else if (ok) {  // K x N query: threads walk k fastest so plane writes stay coalesced
         r = static_cast<uint32_t>(gid % rows);     // k
         cidx = static_cast<uint32_t>(gid / rows);  // n
-        const uint8_t* b = in + (static_cast<size_t>(r) * cols + cidx) * width;
-        for (uint32_t j = 0; j < width; ++j) w[j >> 2] |= static_cast<uint32_t>(b[j]) << (8 * (j & 3));
+        load_words(in + (static_cast<size_t>(r) * cols + cidx) * width, width, w);
     }
     const uint32_t prow = (transpose ? cidx : r) + dst_row0;
     const uint32_t pcol = transpose ? r : cidx;
@@ -554,37 +565,48 @@ __global__ void __launch_bounds__(256) crt_lift_kernel(const uint16_t* __restric
                 carry = s >> 32;
             }
         }
-        // propagate into the top limb(s)
-        for (uint32_t j = L; j <= kMaxQLimbs && carry; ++j) {
-            const uint64_t s = static_cast<uint64_t>(acc[j]) + carry;
-            acc[j] = static_cast<uint32_t>(s);
-            carry = s >> 32;
+        // propagate into the top limb(s); every limb index is compile-time
+        // (predicated on L) so acc stays in registers
+#pragma unroll
+        for (uint32_t j = 0; j <= kMaxQLimbs; ++j) {
+            if (j >= L) {
+                const uint64_t s = static_cast<uint64_t>(acc[j]) + carry;
+                acc[j] = static_cast<uint32_t>(s);
+                carry = s >> 32;
+            }
         }
     }
+#pragma unroll
     for (int s = 0; s < 5; ++s) {
         const uint32_t* q = a.t.qmul[s];
-        // compare acc (L+1 limbs) >= q
+        // compare acc (L+1 limbs) >= q, most significant limb first
         int ge = 1;
-        for (int j = static_cast<int>(L); j >= 0; --j) {
-            if (acc[j] != q[j]) {
+        bool decided = false;
+#pragma unroll
+        for (int j = static_cast<int>(kMaxQLimbs); j >= 0; --j) {
+            if (j <= static_cast<int>(L) && !decided && acc[j] != q[j]) {
                 ge = acc[j] > q[j];
-                break;
+                decided = true;
             }
         }
         if (ge) {
             uint64_t borrow = 0;
-            for (uint32_t j = 0; j <= L; ++j) {
-                const uint64_t d = static_cast<uint64_t>(acc[j]) - q[j] - borrow;
-                acc[j] = static_cast<uint32_t>(d);
-                borrow = (d >> 63) & 1;
+#pragma unroll
+            for (uint32_t j = 0; j <= kMaxQLimbs; ++j) {
+                if (j <= L) {
+                    const uint64_t d = static_cast<uint64_t>(acc[j]) - q[j] - borrow;
+                    acc[j] = static_cast<uint32_t>(d);
+                    borrow = (d >> 63) & 1;
+                }
             }
         }
     }
     uint8_t* dst = out + (static_cast<size_t>(m) * N + n) * a.t.width;
-    for (uint32_t b = 0; b < a.t.width; ++b) {
-        const uint32_t limb = b / 4;
-        dst[b] = limb <= L ? static_cast<uint8_t>(acc[limb] >> (8 * (b % 4))) : 0;
-    }
+#pragma unroll
+    for (uint32_t limb = 0; limb <= kMaxQLimbs; ++limb)
+#pragma unroll
+        for (uint32_t t = 0; t < 4; ++t)
+            if (4 * limb + t < a.t.width) dst[4 * limb + t] = limb <= L ? static_cast<uint8_t>(acc[limb] >> (8 * t)) : 0;
 }
 
 // ---------------------------------------------------------------------------
