@@ -130,3 +130,53 @@ def test_acceptance_criteria_6_7_through_b200(rho, batch, n_db, instances, seed0
             assert a1[2] == k * a2[2]
         else:
             assert 0 <= k * a2[2] - a1[2] <= (k - 1) * (n_db // 1024) * batch
+
+
+@needs_pipe
+@pytest.mark.slow
+def test_acceptance_criteria_6_7_in_full_through_b200():
+    """acceptance.cpp:268-312 criteria 6 and 7 exactly as the reference states
+    them, with every CCMM product from the B200: 100 full_config instances from
+    seed 60000 all agree with the plaintext oracle with the folding assumption
+    held; pre-classification bootstraps alg1 = k * alg2 up to the ceiling slack
+    (k - 1) per (block, eye); total ratio >= k; the rho = 32 run exactly k."""
+    fc = np.ascontiguousarray(ol.FOLD_POLY_APPC, np.float64)
+    lib = ol.pipe("b200")
+    f64p = ol.C.POINTER(ol.C.c_double)
+
+    def run(rho, batch, n_db, instances, seed0):
+        stride = 7 + 2 * batch
+        out = np.zeros((instances, 2, stride), np.int64)
+        st = lib.pipe_instances(rho, batch, n_db, instances, seed0, fc.ctypes.data_as(f64p), len(fc),
+                                ol.ptr(out, ol.i64p), stride)
+        assert st == 0, lib.pipe_last_error()
+        return out
+
+    k, batch, n_db, d = 16, 4, 4096, 1024
+    out = run(31, batch, n_db, 100, 60000)
+    a1, a2 = out[:, 0], out[:, 1]
+    # criterion 6: r1, r2 agree with the oracle and with each other; folding ok
+    assert (a1[:, 0] == 1).all() and (a2[:, 0] == 1).all() and (a2[:, 1] == 1).all()
+    assert (a1[:, 7:7 + batch] == a2[:, 7:7 + batch]).all()
+    assert a1[:, 7:7 + batch].any()          # planted matches were found
+    # criterion 7: bootstrap accounting
+    alg1_pre, alg2_pre = int(a1[:, 2].sum()), int(a2[:, 2].sum())
+    b_units = (n_db // d) * batch * 100
+    deficit = k * alg2_pre - alg1_pre
+    assert 0 <= deficit <= (k - 1) * b_units
+    total1 = int(a1[:, 2:5].sum())
+    total2 = int(a2[:, 2:5].sum())
+    assert total1 / max(1, total2) >= k
+    ex = run(32, 1, 1024, 1, 70000)
+    assert ex[0, 1, 2] > 0 and ex[0, 0, 2] == k * ex[0, 1, 2]
+    # the first instances equal the stock reference's, message digest included
+    ref = ol.pipe("ref")
+    for libx in (lib, ref):
+        libx.irl_hook_reset()
+    head_b = run(31, batch, n_db, 3, 60000)
+    stride = 7 + 2 * batch
+    head_r = np.zeros_like(head_b)
+    assert ref.pipe_instances(31, batch, n_db, 3, 60000, fc.ctypes.data_as(f64p), len(fc),
+                              ol.ptr(head_r, ol.i64p), stride) == 0
+    assert (head_b == head_r).all() and (head_b == out[:3]).all()
+    assert lib.irl_hook_digest() == ref.irl_hook_digest()
