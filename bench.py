@@ -348,6 +348,49 @@ def measure_split(R):
     return split_roof
 
 
+def measure_ingest(R):
+    """The mod-Q ingest kernel (f3: 46-byte BigMatrix entries -> residues ->
+    digit planes, irl_split_bigint) on 2048 x K device-resident entries, 5
+    launches, CUDA events: 46 B read + 48 B written per entry. Not part of the
+    step (a database is ingested once)."""
+    import ctypes as C
+    torch, ctx, K, hbm_peak, rank = R.torch, R.ctx, R.K, R.hbm_peak, R.rank
+    if rank != 0:
+        return None
+    from paper_2601_17561_b200 import capi
+    from paper_2601_17561_b200.modmat import build_paper_basis
+    b = build_paper_basis()
+    p, e = b.arrays()
+    w, rows = b.width(), 2048
+    g = torch.Generator(device="cuda").manual_seed(7)
+    ent = torch.randint(0, 256, (rows * K, w), dtype=torch.uint8, device="cuda", generator=g)
+    ent[:, -1] = 0  # below 2^360 < Q
+    ldk = (K + 15) // 16 * 16
+    planes = torch.empty((len(p), 2, rows, ldk), dtype=torch.int8, device="cuda")
+    s = torch.cuda.current_stream()
+
+    def run():
+        ctx.check(capi.lib().irl_split_bigint(ctx.handle, C.c_void_p(ent.data_ptr()), w, rows, K, 0,
+                                               capi.ptr(p, capi.u32p), capi.ptr(e, capi.u32p), len(p),
+                                               C.c_void_p(planes.data_ptr()), ldk, C.c_void_p(s.cuda_stream)))
+    run()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(5):
+        run()
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    nbytes = rows * K * (w + 2 * len(p))
+    del ent, planes
+    return {"bound": "hbm", "kernel": "split_bigint_words_kernel", "launch_ms": ms,
+            "achieved": nbytes / (ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+            "frac": nbytes / (ms * 1e-3) / 1e9 / hbm_peak, "bytes_per_launch": nbytes,
+            "entries_per_s": rows * K / (ms * 1e-3),
+            "note": "not part of the CCMM step: f3 ingest of 46-byte mod-Q entries into digit planes "
+                    "(integer-multiply bound; the file reads that feed it run at ~13-15 GB/s)"}
+
+
 def measure_moddown(R):
     """f2 ModDown of all local outputs (HBM-bound), outside the step."""
     torch, eng, N, M, nmod, stream, local_parts = R.torch, R.eng, R.N, R.M, R.nmod, R.stream, R.local_parts
@@ -398,12 +441,19 @@ def measure_e2e(R):
         q_bytes = q_dev.view(torch.uint8)  # [nmod][K][2N]: gloo and NCCL both carry uint8
         q_slices = [q_bytes[r_ * per:(r_ + 1) * per] for r_ in range(world)] if sharded else None
 
+        q_events = []
+
         def e2e_once():
             R.next_slot()
             if sharded:
+                cs = torch.cuda.current_stream()
+                ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                ev[0].record(cs)
                 q_dev[lo:lo + per].copy_(q_pinned.view(nmod, K, N)[lo:lo + per], non_blocking=True)
                 dist.all_gather(q_slices, q_bytes[lo:lo + per].clone() if args.backend == "gloo" else q_bytes[lo:lo + per])
-                eng.run_dq(None, N, o_np, stream=torch.cuda.current_stream().cuda_stream)
+                ev[1].record(cs)
+                q_events.append(ev)
+                eng.run_dq(None, N, o_np, stream=cs.cuda_stream)
             else:
                 eng.run(q_np, o_np)  # H2D query, split, all local PPMMs, D2H outputs
             if md_drop:  # the engine's device outputs of the run, rescaled for the exchange
@@ -424,10 +474,17 @@ def measure_e2e(R):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        q_events.clear()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             e2e_once()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+        per_rank_e2e = None
+        if world > 1:  # this rank's e2e and, when sharded, its query H2D + all-gather time
+            mine = {"rank": rank, "e2e_ms": e2e_ms,
+                    "query_in_ms": statistics.mean(a.elapsed_time(b) for a, b in q_events) if q_events else None}
+            per_rank_e2e = [None] * world
+            dist.all_gather_object(per_rank_e2e, mine)
         # the e2e outputs (host) must equal the device-resident step's (same
         # query): a 64-row block of every part and modulus, on every rank
         cols = min(M, 64)
@@ -443,7 +500,7 @@ def measure_e2e(R):
         e2e = {"value": total_ops / (e2e_ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": int(q_host.nbytes // world if sharded else q_host.nbytes),
                "d2h_bytes_per_step": int(local_parts.count * nmod * N * M * 2),
-               "outputs_equal_device_step": e2e_exact,
+               "outputs_equal_device_step": e2e_exact, "per_rank": per_rank_e2e,
                "call": ("1/N of the query H2D per rank + NCCL all-gather, then irl_ccmm_run_dq "
                         "(include/irl_capi.h) with pinned host outputs") if sharded else
                        "irl_ccmm_run (include/irl_capi.h) with pinned host buffers"}
@@ -888,6 +945,7 @@ def main():
         total_ops=total_ops, peaks=peaks, hbm_peak=hbm_peak, next_slot=next_slot, unit_map=unit_map,
         use_blocks=use_blocks)
     split_roof = measure_split(R)
+    ingest = measure_ingest(R)
     moddown = measure_moddown(R)
     e2e = measure_e2e(R)
     dist_check = measure_dist_check(R)
@@ -914,7 +972,8 @@ def main():
                                                        if "bf16_tflops" in peaks else None),
                              "frac_of_live_cublas_int8": (achieved / int8_ref["sustained_tops"]
                                                           if int8_ref else None)},
-                "split_roofline": split_roof, "moddown": moddown, "fold_stage": fold, "iris_stage": iris,
+                "split_roofline": split_roof, "ingest": ingest, "moddown": moddown, "fold_stage": fold,
+                "iris_stage": iris,
                 "int8_library_ref": int8_ref,
                 "dealing": ({"kind": "row blocks (dist.deal_blocks)", "block_rows": M,
                              "units_per_rank": [x["parts"][1] for x in per_rank] if per_rank else [local_parts.count]}

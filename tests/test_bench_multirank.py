@@ -47,6 +47,10 @@ def test_bench_multirank_same_device(world, exchange):
     assert [x["rank"] for x in pr] == list(range(world))
     assert all(x["gemm_ms"] > 0 and x["exchange_wait_ms"] is not None for x in pr)
     assert sum(x["parts"][1] for x in pr) == max(4, world)
+    # e2e per rank, with the sharded query distribution timed (H2D slice + all-gather)
+    pe = d["e2e"]["per_rank"]
+    assert [x["rank"] for x in pe] == list(range(world))
+    assert all(x["e2e_ms"] > 0 and x["query_in_ms"] is not None and x["query_in_ms"] > 0 for x in pe)
 
 
 @pytest.mark.gpu
