@@ -246,6 +246,10 @@ int match_fused(irl_ctx* ctx, const int8_t* xp, const int8_t* yp, size_t n_db, s
         L.iris.bits = dbits;
         L.iris.first = first;
         L.iris.scores = dsc;
+        if (ctx->diag && ctx->d_diag && c0 == 0) {  // irl_diag_ppmm: counters of the main launch
+            L.stats = ctx->d_diag;
+            IRL_CK(ctx, cudaMemsetAsync(ctx->d_diag, 0, 1024 * kStatSlots * sizeof(uint64_t), s));
+        }
         IRL_LAUNCH(ctx, launch_ppmm_planes(L, s));
         ctx->launches += ppmm_kernels_last_launch() > 1 ? ppmm_kernels_last_launch() - 1 : 0;  // + filler
     }

@@ -67,6 +67,9 @@ constexpr int kStageBytes = 4 * kPlaneTileBytes;                // X0 X1 Y0 Y1
 #ifndef IRL_A_REUSE
 #define IRL_A_REUSE 1  // reuse X0 from the tensor core's A collector (tcgen05 collector::a)
 #endif
+#ifndef IRL_SPLIT_SLOTS
+#define IRL_SPLIT_SLOTS 0  // 1: two-product modes use one 32 KB ring slot per product (6 slots; measured slower)
+#endif
 #ifndef IRL_EPI_WARPS
 #define IRL_EPI_WARPS 16
 #endif
@@ -217,18 +220,26 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    constexpr bool kF4 = kMode == kModeInnerF4 || kMode == kModeIrisMatchF4;
+    constexpr bool kInner = kMode == kModeInner || kMode == kModeInnerF4;
+    constexpr bool kMatch = kMode == kModeIrisMatch || kMode == kModeIrisMatchF4;
+    // The modes with two independent products (acc1 = X0 Y0, acc2 = X1 Y1)
+    // give each product of a K block its own ring slot (X_p, Y_p: 32 KB), so
+    // the same 192 KB ring holds six slots and the MMAs hold only one sixth of
+    // it while five slots are in flight (three 64 KB stages left two). The
+    // psq products share X0 and Y0, so they keep whole-K-block stages.
+    constexpr bool kSplitSlots = IRL_SPLIT_SLOTS && kMode != kModePsq;
+    constexpr uint32_t kSlots = kSplitSlots ? 2 * kStages : kStages;
+    constexpr uint32_t kSlotBytes = kSplitSlots ? kStageBytes / 2 : kStageBytes;
     uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-    uint64_t* empty_bar = full_bar + kStages;
-    uint64_t* tmem_full_bar = empty_bar + kStages;
+    uint64_t* empty_bar = full_bar + kSlots;
+    uint64_t* tmem_full_bar = empty_bar + kSlots;
     uint64_t* tmem_empty_bar = tmem_full_bar + 1;
     uint64_t* ring_full = tmem_empty_bar + 1;
     uint64_t* ring_empty = ring_full + kRing;
     uint32_t* ring_tile = reinterpret_cast<uint32_t*>(ring_empty + kRing);  // [kRing][2]
     uint32_t* tmem_base_slot = ring_tile + 2 * kRing;
 
-    constexpr bool kF4 = kMode == kModeInnerF4 || kMode == kModeIrisMatchF4;
-    constexpr bool kInner = kMode == kModeInner || kMode == kModeInnerF4;
-    constexpr bool kMatch = kMode == kModeIrisMatch || kMode == kModeIrisMatchF4;
     constexpr uint32_t kTileN = kF4 ? kF4TileN : kMaxTileN;
     constexpr uint32_t kNAlign = kF4 ? 16u : 32u;
     const uint32_t warp = threadIdx.x / 32;
@@ -246,7 +257,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmap_a);
         ptx::prefetch_tmap(&tmap_b);
-        for (int s = 0; s < kStages; ++s) {
+        for (uint32_t s = 0; s < kSlots; ++s) {
             ptx::mbar_init(&full_bar[s], 1);
             ptx::mbar_init(&empty_bar[s], kPairs);  // one commit per pair reading this stage
         }
@@ -355,92 +366,88 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                                             tc.m0 + half_rank * kRowsPerCta;
                     const uint32_t half_n = tc.n_size / 2;
                     const uint32_t b_row0 = (tc.prime * 2) * args.N + tc.n0 + half_rank * half_n;
-                    for (uint32_t kb = 0; kb < num_kb; ++kb, ++issued) {
-                        timed_wait(&empty_bar[stage], phase ^ 1, diag, w_empty);
-                        if (gate && issued > seen + lead) {
-                            // Stay within kGateLead K blocks of the slowest group peer.
-                            // `seen` caches the last observed minimum, so the L2
-                            // round trip is paid about once per kGateLead blocks.
-                            const long long t0 = clock64();
-                            for (;;) {
-                                uint32_t lo = 0xFFFFFFFFu;
-                                for (uint32_t p = grp.first; p < grp.first + grp.size; ++p)
-                                    if (p != cluster_id)
-                                        lo = min(lo, ptx::ld_relaxed_gpu(args.progress + p));
-                                seen = lo;
-                                if (lo + lead >= issued) break;
-                                if (clock64() - t0 > kGateSpinCycles) {
-                                    seen = issued;  // give up for kGateLead blocks (forward progress)
-                                    break;
-                                }
-                                __nanosleep(32);
-                            }
-                            if (diag) w_gate += static_cast<unsigned long long>(clock64() - t0);
-                        }
-                        // completion bytes land on the pair leader's barrier
-                        const uint32_t leader_full = ptx::smem_u32(&full_bar[stage]) & 0xFEFFFFFFu;
-                        if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * kStageBytes);
-                        uint8_t* st = smem + stage * kStageBytes;
-                        const int32_t k0 = static_cast<int32_t>(kb * kBlockK);
+                    // one plane tile of A (this CTA's 128 DB rows; with kPN > 1 a 1/kPN
+                    // share, multicast to the same-role CTAs of the pairs sharing pm)
+                    auto load_a = [&](uint32_t dst, uint32_t row, uint32_t bar, int32_t k0) {
                         if constexpr (kPN == 1) {
-                            ptx::tma_load_2d_pair(ptx::smem_u32(st), &tmap_a, leader_full, k0,
-                                                  static_cast<int32_t>(a_row0));
-                            ptx::tma_load_2d_pair(ptx::smem_u32(st + kPlaneTileBytes), &tmap_a,
-                                                  leader_full, k0,
-                                                  static_cast<int32_t>(a_row0 + args.M));
+                            ptx::tma_load_2d_pair(dst, &tmap_a, bar, k0, static_cast<int32_t>(row));
                         } else {
-                            // rows [pn * kSubA, +kSubA) of this CTA's A block, for
-                            // itself and the same-role CTAs of the pairs sharing pm
                             constexpr uint32_t kSubA = kRowsPerCta / kPN;
                             uint16_t mask = 0;
 #pragma unroll
                             for (uint32_t j = 0; j < kPN; ++j) mask |= 1u << (2 * (pm * kPN + j) + half_rank);
                             const uint32_t sub = pn * kSubA * kBlockK;
-                            if (args.a_evict_first) {
-                                ptx::tma_load_2d_pair_mcast_hint(ptx::smem_u32(st) + sub, &tmap_a, leader_full, k0,
-                                                                 static_cast<int32_t>(a_row0 + pn * kSubA), mask,
+                            if (args.a_evict_first)
+                                ptx::tma_load_2d_pair_mcast_hint(dst + sub, &tmap_a, bar, k0,
+                                                                 static_cast<int32_t>(row + pn * kSubA), mask,
                                                                  ptx::kL2EvictFirst);
-                                ptx::tma_load_2d_pair_mcast_hint(
-                                    ptx::smem_u32(st + kPlaneTileBytes) + sub, &tmap_a, leader_full, k0,
-                                    static_cast<int32_t>(a_row0 + args.M + pn * kSubA), mask, ptx::kL2EvictFirst);
-                            } else {
-                                ptx::tma_load_2d_pair_mcast(ptx::smem_u32(st) + sub, &tmap_a, leader_full, k0,
-                                                            static_cast<int32_t>(a_row0 + pn * kSubA), mask);
-                                ptx::tma_load_2d_pair_mcast(ptx::smem_u32(st + kPlaneTileBytes) + sub, &tmap_a,
-                                                            leader_full, k0,
-                                                            static_cast<int32_t>(a_row0 + args.M + pn * kSubA),
-                                                            mask);
-                            }
+                            else
+                                ptx::tma_load_2d_pair_mcast(dst + sub, &tmap_a, bar, k0,
+                                                            static_cast<int32_t>(row + pn * kSubA), mask);
                         }
+                    };
+                    // one plane tile of B (this CTA's half of the n-tile; with kPM > 1
+                    // a 1/kPM share, multicast to the pairs sharing pn)
+                    auto load_b = [&](uint32_t dst, uint32_t row, uint32_t bar, int32_t k0) {
                         if constexpr (kPM == 1) {
-                            ptx::tma_load_2d_pair_hint(ptx::smem_u32(st + 2 * kPlaneTileBytes),
-                                                       &tmap_b, leader_full, k0,
-                                                       static_cast<int32_t>(b_row0), ptx::kL2EvictLast);
-                            ptx::tma_load_2d_pair_hint(ptx::smem_u32(st + 3 * kPlaneTileBytes),
-                                                       &tmap_b, leader_full, k0,
-                                                       static_cast<int32_t>(b_row0 + args.N),
+                            ptx::tma_load_2d_pair_hint(dst, &tmap_b, bar, k0, static_cast<int32_t>(row),
                                                        ptx::kL2EvictLast);
                         } else {
-                            // rows [pm * kSubB, +kSubB) of this CTA's B block, shared
-                            // with the same-role CTAs of the pairs sharing pn
                             constexpr uint32_t kSubB = kRowsPerCta / kPM;
                             uint16_t mask = 0;
 #pragma unroll
                             for (uint32_t j = 0; j < kPM; ++j) mask |= 1u << (2 * (j * kPN + pn) + half_rank);
                             const uint32_t sub = pm * kSubB * kBlockK;
-                            ptx::tma_load_2d_pair_mcast(ptx::smem_u32(st + 2 * kPlaneTileBytes) + sub, &tmap_b,
-                                                        leader_full, k0,
-                                                        static_cast<int32_t>(b_row0 + pm * kSubB), mask);
-                            ptx::tma_load_2d_pair_mcast(ptx::smem_u32(st + 3 * kPlaneTileBytes) + sub, &tmap_b,
-                                                        leader_full, k0,
-                                                        static_cast<int32_t>(b_row0 + args.N + pm * kSubB),
-                                                        mask);
+                            ptx::tma_load_2d_pair_mcast(dst + sub, &tmap_b, bar, k0,
+                                                        static_cast<int32_t>(row + pm * kSubB), mask);
+                        }
+                    };
+                    for (uint32_t kb = 0; kb < num_kb; ++kb, ++issued) {
+#pragma unroll
+                        for (uint32_t prod = 0; prod < kSlots / kStages; ++prod) {
+                            timed_wait(&empty_bar[stage], phase ^ 1, diag, w_empty);
+                            if (prod == 0 && gate && issued > seen + lead) {
+                                // Stay within kGateLead K blocks of the slowest group peer.
+                                // `seen` caches the last observed minimum, so the L2
+                                // round trip is paid about once per kGateLead blocks.
+                                const long long t0 = clock64();
+                                for (;;) {
+                                    uint32_t lo = 0xFFFFFFFFu;
+                                    for (uint32_t p = grp.first; p < grp.first + grp.size; ++p)
+                                        if (p != cluster_id)
+                                            lo = min(lo, ptx::ld_relaxed_gpu(args.progress + p));
+                                    seen = lo;
+                                    if (lo + lead >= issued) break;
+                                    if (clock64() - t0 > kGateSpinCycles) {
+                                        seen = issued;  // give up for kGateLead blocks (forward progress)
+                                        break;
+                                    }
+                                    __nanosleep(32);
+                                }
+                                if (diag) w_gate += static_cast<unsigned long long>(clock64() - t0);
+                            }
+                            // completion bytes land on the pair leader's barrier
+                            const uint32_t leader_full = ptx::smem_u32(&full_bar[stage]) & 0xFEFFFFFFu;
+                            if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * kSlotBytes);
+                            const uint32_t st = ptx::smem_u32(smem + stage * kSlotBytes);
+                            const int32_t k0 = static_cast<int32_t>(kb * kBlockK);
+                            if constexpr (kSplitSlots) {
+                                // slot = product `prod` of this K block: X_prod, then Y_prod
+                                load_a(st, a_row0 + prod * args.M, leader_full, k0);
+                                load_b(st + kPlaneTileBytes, b_row0 + prod * args.N, leader_full, k0);
+                            } else {
+                                // stage = X0 X1 Y0 Y1 of this K block
+                                load_a(st, a_row0, leader_full, k0);
+                                load_a(st + kPlaneTileBytes, a_row0 + args.M, leader_full, k0);
+                                load_b(st + 2 * kPlaneTileBytes, b_row0, leader_full, k0);
+                                load_b(st + 3 * kPlaneTileBytes, b_row0 + args.N, leader_full, k0);
+                            }
+                            if (++stage == kSlots) {
+                                stage = 0;
+                                phase ^= 1;
+                            }
                         }
                         if (gate) ptx::st_relaxed_gpu(args.progress + cluster_id, issued + 1);
-                        if (++stage == kStages) {
-                            stage = 0;
-                            phase ^= 1;
-                        }
                     }
                 }
             }
@@ -477,6 +484,34 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                 timed_wait(tmem_empty_bar, (j & 1) ^ 1, diag, w_tmem);
                 ptx::tc_fence_after();
                 for (uint32_t kb = 0; kb < num_kb; ++kb) {
+                    if constexpr (kSplitSlots) {
+                        // two independent products, one slot each: acc1 = X0 Y0, acc2 = X1 Y1
+#pragma unroll
+                        for (uint32_t prod = 0; prod < 2; ++prod) {
+                            timed_wait(&full_bar[stage], phase, diag, w_full);
+                            ptx::tc_fence_after();
+                            const uint32_t st = ptx::smem_u32(smem + stage * kSlotBytes);
+                            const uint32_t acc = prod ? acc2 : acc1;
+#pragma unroll
+                            for (int k = 0; k < kBlockK / kUmmaK; ++k) {
+                                const uint32_t koff = k * kUmmaK;
+                                const uint64_t dx = ptx::smem_desc_k_sw128(st + koff);
+                                const uint64_t dy = ptx::smem_desc_k_sw128(st + kPlaneTileBytes + koff);
+                                const uint32_t accum = (kb | k) != 0;
+                                if constexpr (kF4)  // packed e2m1 operands, 64 k per 32 B
+                                    ptx::mma_mxf4_pair(acc, dx, dy, idesc, accum, tmem_base + kF4SfaCol,
+                                                       tmem_base + kF4SfbCol);
+                                else
+                                    ptx::mma_i8_pair(acc, dx, dy, idesc, accum);
+                            }
+                            ptx::mma_commit_pair(&empty_bar[stage], static_cast<uint16_t>((1u << kCtas) - 1));
+                            if (++stage == kSlots) {
+                                stage = 0;
+                                phase ^= 1;
+                            }
+                        }
+                        continue;
+                    }
                     timed_wait(&full_bar[stage], phase, diag, w_full);
                     ptx::tc_fence_after();
                     const uint32_t st = ptx::smem_u32(smem + stage * kStageBytes);
@@ -490,15 +525,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                         const uint64_t dy1 =
                             ptx::smem_desc_k_sw128(st + 3 * kPlaneTileBytes + koff);
                         const uint32_t accum = (kb | k) != 0;
-                        if constexpr (kF4) {
-                            // the same two products on packed e2m1 operands (64 k per 32 B)
+                        if constexpr (kF4) {  // IRL_SPLIT_SLOTS=0: both products from one stage
                             ptx::mma_mxf4_pair(acc1, dx0, dy0, idesc, accum, tmem_base + kF4SfaCol,
                                                tmem_base + kF4SfbCol);
                             ptx::mma_mxf4_pair(acc2, dx1, dy1, idesc, accum, tmem_base + kF4SfaCol,
                                                tmem_base + kF4SfbCol);
                             continue;
                         } else if constexpr (kMode != kModePsq) {
-                            // two independent products: acc1 = X0 Y0, acc2 = X1 Y1
                             ptx::mma_i8_pair(acc1, dx0, dy0, idesc, accum);
                             ptx::mma_i8_pair(acc2, dx1, dy1, idesc, accum);
                             continue;
@@ -576,26 +609,47 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                 ptx::tmem_ld_32x32b_x16(lane_base + c, a1);
                 ptx::tmem_ld_32x32b_x16(lane_base + kAcc2Col + c, a2);
                 ptx::tmem_ld_wait();
-                if constexpr (kF4) {  // FP32 accumulators of exact integers
+                if constexpr (kMatch) {
+                    // Screen first: almost every (column, template) score misses the
+                    // interval by far. A miss is decided exactly from the products
+                    // (inner < lo_out * ov or inner > hi_out * ov, ov > 0; see the
+                    // launcher's margins), with no division. Everything else (a
+                    // possible match, an empty overlap, and every element when the
+                    // scores are requested) takes the exact path below, once per
+                    // warp per chunk that has one.
+                    const IrisMatchOut& io = args.iris;
+                    uint32_t ev = 0;
 #pragma unroll
                     for (int jj = 0; jj < 16; ++jj) {
-                        a1[jj] = static_cast<uint32_t>(__float2int_rn(__uint_as_float(a1[jj])));
-                        a2[jj] = static_cast<uint32_t>(__float2int_rn(__uint_as_float(a2[jj])));
+                        float fi, fo;  // exact integers (|value| <= d < 2^24)
+                        if constexpr (kF4) {
+                            fi = __uint_as_float(a1[jj]);
+                            fo = __uint_as_float(a2[jj]);
+                        } else {
+                            fi = static_cast<float>(static_cast<int32_t>(a1[jj]));
+                            fo = static_cast<float>(static_cast<int32_t>(a2[jj]));
+                        }
+                        const bool miss = fo > 0.0f && (fi < io.lo_out * fo || fi > io.hi_out * fo);
+                        if (!miss || io.scores) ev |= 1u << jj;
                     }
-                }
-                if constexpr (kMatch) {
-                    // score = inner / overlap per (column, template); per column,
-                    // the warp's 32 templates fold their first match / first
-                    // empty overlap into one atomicMin per eye
-                    const IrisMatchOut& io = args.iris;
+                    if (!row_ok) ev = 0;
+                    if (tc.n0 + c + 16 > args.N) ev &= (1u << (args.N > tc.n0 + c ? args.N - tc.n0 - c : 0u)) - 1u;
+                    if (!__any_sync(0xFFFFFFFFu, ev != 0)) continue;
                     for (int jj = 0; jj < 16; ++jj) {
                         const uint32_t col = tc.n0 + c + jj;
                         if (col >= args.N) break;  // uniform across the warp
                         const uint32_t gcol = col + io.col0;  // global query column
                         const uint32_t eye = gcol / io.rho, rot = gcol % io.rho;
-                        const int32_t inner = static_cast<int32_t>(a1[jj]), ov = static_cast<int32_t>(a2[jj]);
+                        int32_t inner, ov;
+                        if constexpr (kF4) {
+                            inner = __float2int_rn(__uint_as_float(a1[jj]));
+                            ov = __float2int_rn(__uint_as_float(a2[jj]));
+                        } else {
+                            inner = static_cast<int32_t>(a1[jj]);
+                            ov = static_cast<int32_t>(a2[jj]);
+                        }
                         uint32_t cm = 0xFFFFFFFFu, cz = 0xFFFFFFFFu;
-                        if (row_ok) {
+                        if ((ev >> jj) & 1u) {
                             const uint32_t lin = rot * args.M + m;
                             if (ov == 0) {
                                 cz = lin;
@@ -636,6 +690,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                         }
                     }
                     continue;
+                }
+                if constexpr (kF4) {  // FP32 accumulators of exact integers
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) {
+                        a1[jj] = static_cast<uint32_t>(__float2int_rn(__uint_as_float(a1[jj])));
+                        a2[jj] = static_cast<uint32_t>(__float2int_rn(__uint_as_float(a2[jj])));
+                    }
                 }
                 if (kMode == kModePsq && mc_tile) {
                     // multicast mirror: the whole warp takes part (lanes past M
@@ -974,11 +1035,21 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
         return cudaErrorInvalidValue;
     args.iris = L.iris;
     {
-        const double eps = 1e-5;  // >> the float quotient's error for |inner|, overlap <= 2^24
-        args.iris.lo_in = static_cast<float>(L.iris.lo + eps);
-        args.iris.lo_out = static_cast<float>(L.iris.lo - eps);
-        args.iris.hi_in = static_cast<float>(L.iris.hi - eps);
-        args.iris.hi_out = static_cast<float>(L.iris.hi + eps);
+        // Float screens with a 1e-5 margin. Scores lie in [-1, 1] (|inner| <=
+        // overlap), and inner, overlap are exact in float below 2^24. So the
+        // float quotient (error < 1e-6) and the float products lo_out * ov,
+        // hi_out * ov (relative error 2^-23 with the bound's own rounding, i.e.
+        // below 1e-5 * ov for |bound| < 84; a bound outside that range is
+        // never reached by a score or decided the same way) settle every
+        // score farther than 1e-5 from a bound. Longer rows (int8 planes with
+        // K >= 2^23 bytes) are not exact in float: no screen, every score divides.
+        const double eps = 1e-5;
+        const float inf = __builtin_huge_valf();
+        const bool exact_f32 = L.K < (1u << 23);
+        args.iris.lo_in = exact_f32 ? static_cast<float>(L.iris.lo + eps) : inf;
+        args.iris.lo_out = exact_f32 ? static_cast<float>(L.iris.lo - eps) : -inf;
+        args.iris.hi_in = exact_f32 ? static_cast<float>(L.iris.hi - eps) : -inf;
+        args.iris.hi_out = exact_f32 ? static_cast<float>(L.iris.hi + eps) : inf;
     }
     for (uint32_t i = 0; i < L.nprimes; ++i) args.mc[i] = L.mc[i];
 
