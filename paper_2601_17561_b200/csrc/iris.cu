@@ -55,6 +55,11 @@ size_t plane_ldk(size_t d) { return round16(plane_kbytes(d)); }
 // for the paper's batch) would cost a second, mostly padding pass of the
 // whole cluster, so it runs as its own launch on plain pairs. Returns the
 // columns of the main launch, 0 = no split.
+// The fused FP4 match puts the query columns on M (IrisMatchOut::query_rows):
+// one 4x1-cluster pass over the database covers up to 1024 columns, so the
+// query planes are not split. IRL_IRIS_DB_ON_M=1 keeps the database on M.
+bool match_query_rows(size_t d) { return iris_f4(d) && !std::getenv("IRL_IRIS_DB_ON_M"); }
+
 size_t col_split(size_t cols, size_t d) {
     if (!iris_f4(d) || std::getenv("IRL_IRIS_NO_SPLIT")) return 0;
     const size_t pass = 4 * kF4TileCols;
@@ -195,8 +200,8 @@ int build_planes(irl_ctx* ctx, const uint64_t* code, const uint64_t* mask, size_
 
 // Query planes, laid out per launch: [2][main][ldk] then [2][rest][ldk].
 int build_query_planes(irl_ctx* ctx, const uint64_t* code, const uint64_t* mask, size_t n_eyes, size_t rho,
-                       size_t d, int8_t* planes, cudaStream_t s) {
-    const size_t cols = n_eyes * rho, split = col_split(cols, d);
+                       size_t d, int8_t* planes, cudaStream_t s, bool allow_split = true) {
+    const size_t cols = n_eyes * rho, split = allow_split ? col_split(cols, d) : 0;
     if (!split) return build_planes_range(ctx, code, mask, rho, d, 0, cols, planes, s);
     if (int st = build_planes_range(ctx, code, mask, rho, d, 0, split, planes, s)) return st;
     return build_planes_range(ctx, code, mask, rho, d, split, cols - split, planes + 2 * split * plane_ldk(d), s);
@@ -219,19 +224,35 @@ int match_fused(irl_ctx* ctx, const int8_t* xp, const int8_t* yp, size_t n_db, s
     double* dsc = scores ? reinterpret_cast<double*>(ws.as<uint8_t>() + off_sc) : nullptr;
     IRL_CK(ctx, cudaMemsetAsync(first, 0xFF, 8 * n_eyes, s));
     IRL_CK(ctx, cudaMemsetAsync(dbits, 0, nbits, s));
-    // one launch per column range of build_query_planes (see col_split); the
-    // launches fold into the same first-event indices and match bits
-    const size_t split = col_split(cols, d);
+    // Query columns on M (match_query_rows): one launch, the query planes
+    // unsplit. Otherwise one launch per column range of build_query_planes
+    // (see col_split); the launches fold into the same first-event indices
+    // and match bits.
+    const bool qrows = match_query_rows(d);
+    const size_t split = qrows ? 0 : col_split(cols, d);
     const size_t ranges[2][2] = {{0, split ? split : cols}, {split, split ? cols - split : 0}};
     for (const auto& rg : ranges) {
         const size_t c0 = rg[0], nc = rg[1];
         if (nc == 0) continue;
         PpmmLaunch L;
         L.mode = iris_f4(d) ? kModeIrisMatchF4 : kModeIrisMatch;
-        L.a_planes = xp;
-        L.b_planes = yp + 2 * c0 * ldk;
-        L.M = static_cast<uint32_t>(n_db);
-        L.N = static_cast<uint32_t>(nc);
+        if (qrows) {
+            // A = the query planes (992 rows), B = the database, streamed once
+            // by 4x1 clusters that multicast each database tile to their pairs
+            L.a_planes = yp;
+            L.b_planes = xp;
+            L.M = static_cast<uint32_t>(nc);
+            L.N = static_cast<uint32_t>(n_db);
+            L.cluster_pm = 4;
+            L.cluster_pn = 1;
+            L.b_streamed = 1;
+            L.iris.query_rows = 1;
+        } else {
+            L.a_planes = xp;
+            L.b_planes = yp + 2 * c0 * ldk;
+            L.M = static_cast<uint32_t>(n_db);
+            L.N = static_cast<uint32_t>(nc);
+        }
         L.K = static_cast<uint32_t>(plane_kbytes(d));
         L.ldk = static_cast<uint32_t>(ldk);
         L.parts = 1;
@@ -255,8 +276,9 @@ int match_fused(irl_ctx* ctx, const int8_t* xp, const int8_t* yp, size_t n_db, s
     }
     std::vector<uint32_t> h(2 * n_eyes);
     IRL_CK(ctx, cudaMemcpyAsync(h.data(), first, 8 * n_eyes, cudaMemcpyDeviceToHost, s));
-    if (match_bits) IRL_CK(ctx, cudaMemcpyAsync(match_bits, dbits, nbits, cudaMemcpyDeviceToHost, s));
-    if (scores) IRL_CK(ctx, cudaMemcpyAsync(scores, dsc, nsc * 8, cudaMemcpyDeviceToHost, s));
+    // pageable host outputs go through the context's pinned bounce buffers
+    if (match_bits) IRL_CK(ctx, copy_d2h(ctx, match_bits, dbits, nbits, s));
+    if (scores) IRL_CK(ctx, copy_d2h(ctx, scores, dsc, nsc * 8, s));
     IRL_CK(ctx, cudaStreamSynchronize(s));
     int status = IRL_OK;
     for (size_t e = 0; e < n_eyes; ++e) {
@@ -385,7 +407,8 @@ int irl_iris_match(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db_mas
     IRL_CK(ctx, copy_h2d(ctx, qc, q_code, q_bits, s));
     IRL_CK(ctx, copy_h2d(ctx, qm, q_mask, q_bits, s));
     if (int st = build_planes(ctx, dc, dm, n_db, 1, d, ctx->ws[1].as<int8_t>(), s)) return st;
-    if (int st = build_query_planes(ctx, qc, qm, n_eyes, rho, d, ctx->ws[2].as<int8_t>(), s)) return st;
+    if (int st = build_query_planes(ctx, qc, qm, n_eyes, rho, d, ctx->ws[2].as<int8_t>(), s, !match_query_rows(d)))
+        return st;
     return match_fused(ctx, ctx->ws[1].as<int8_t>(), ctx->ws[2].as<int8_t>(), n_db, n_eyes, rho, d, ldk, p_lo, p_hi,
                        match_bits, eye_result, scores, ctx->ws[4], ctx->d_progress, s);
 }
@@ -524,7 +547,9 @@ int irl_iris_db_match(irl_iris_db* e, const uint64_t* q_code, const uint64_t* q_
     const size_t words = (e->d + 63) / 64, qb = n_eyes * words * 8;
     IRL_CK(ctx, cudaMemcpyAsync(e->qbits, q_code, qb, cudaMemcpyHostToDevice, s));
     IRL_CK(ctx, cudaMemcpyAsync(e->qbits + n_eyes * words, q_mask, qb, cudaMemcpyHostToDevice, s));
-    if (int st = build_query_planes(ctx, e->qbits, e->qbits + n_eyes * words, n_eyes, rho, e->d, e->qplanes, s)) return st;
+    if (int st = build_query_planes(ctx, e->qbits, e->qbits + n_eyes * words, n_eyes, rho, e->d, e->qplanes, s,
+                                    !match_query_rows(e->d)))
+        return st;
     return match_fused(ctx, e->planes, e->qplanes, e->n_db, n_eyes, rho, e->d, e->ldk, p_lo, p_hi, match_bits,
                        eye_result, scores, e->match_ws, e->progress, s);
 }

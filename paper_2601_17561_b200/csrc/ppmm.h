@@ -39,6 +39,13 @@ struct IrisMatchOut {
     uint8_t* bits = nullptr;    // [eyes][M] (zeroed by the caller), nullable
     uint32_t* first = nullptr;  // [eyes][2]: min rotation * M + m of a match / of an empty overlap (0xFF.. init)
     double* scores = nullptr;   // [N][M], NaN where the overlap is empty; nullable
+    // 0: A = database templates (M), B = query columns (N), as above.
+    // 1: A = query columns (M rows, column c = eye * rho + rotation), B =
+    //    database templates (N): bits [eyes][N], first-event index rotation * N
+    //    + template, scores [M][N]. A 4x1 cluster then covers up to 1024
+    //    columns in one pass over the database (the FP4 tile is 240 wide, so
+    //    992 columns on N needed a second, 32-column pass over it).
+    uint32_t query_rows = 0;
 };
 // Diagnostics slots per CTA pair (PpmmLaunch::stats): 0 producer empty-wait
 // cycles, 1 producer gate cycles, 2 MMA full-wait cycles, 3 MMA tmem-empty
@@ -93,6 +100,9 @@ struct PpmmLaunch {
     IrisMatchOut iris;                          // kModeIrisMatch outputs (parts = nprimes = 1)
     int cluster_pm = 1;
     int cluster_pn = 4;
+    // B is the operand streamed once (read by one cluster) and A the small one
+    // every unit re-reads: load B evict-first, A evict-last (with cluster_pm > 1)
+    int b_streamed = 0;
     ModConst mc[kMaxPrimesPerLaunch];
 };
 

@@ -99,6 +99,7 @@ struct __align__(64) GemmArgs {
                                       // member started late never finds its slot overwritten)
     uint32_t gate_lead;               // max K blocks a pair may lead its group (0: no gating)
     uint32_t a_evict_first;           // DB tiles read exactly once from L2 (G == 1): evict-first policy
+    uint32_t b_evict_first;           // B is the streamed operand (PpmmLaunch::b_streamed): B evict-first, A evict-last
     uint32_t accumulate;
     uint32_t a_part_rows;             // plane rows between consecutive parts of A
     unsigned long long out_part;      // output elements between consecutive parts
@@ -370,7 +371,11 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                     // share, multicast to the same-role CTAs of the pairs sharing pm)
                     auto load_a = [&](uint32_t dst, uint32_t row, uint32_t bar, int32_t k0) {
                         if constexpr (kPN == 1) {
-                            ptx::tma_load_2d_pair(dst, &tmap_a, bar, k0, static_cast<int32_t>(row));
+                            if (args.b_evict_first)
+                                ptx::tma_load_2d_pair_hint(dst, &tmap_a, bar, k0, static_cast<int32_t>(row),
+                                                           ptx::kL2EvictLast);
+                            else
+                                ptx::tma_load_2d_pair(dst, &tmap_a, bar, k0, static_cast<int32_t>(row));
                         } else {
                             constexpr uint32_t kSubA = kRowsPerCta / kPN;
                             uint16_t mask = 0;
@@ -398,8 +403,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 #pragma unroll
                             for (uint32_t j = 0; j < kPM; ++j) mask |= 1u << (2 * (j * kPN + pn) + half_rank);
                             const uint32_t sub = pm * kSubB * kBlockK;
-                            ptx::tma_load_2d_pair_mcast(dst + sub, &tmap_b, bar, k0,
-                                                        static_cast<int32_t>(row + pm * kSubB), mask);
+                            if (args.b_evict_first)
+                                ptx::tma_load_2d_pair_mcast_hint(dst + sub, &tmap_b, bar, k0,
+                                                                 static_cast<int32_t>(row + pm * kSubB), mask,
+                                                                 ptx::kL2EvictFirst);
+                            else
+                                ptx::tma_load_2d_pair_mcast(dst + sub, &tmap_b, bar, k0,
+                                                            static_cast<int32_t>(row + pm * kSubB), mask);
                         }
                     };
                     for (uint32_t kb = 0; kb < num_kb; ++kb, ++issued) {
@@ -635,6 +645,53 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                     if (!row_ok) ev = 0;
                     if (tc.n0 + c + 16 > args.N) ev &= (1u << (args.N > tc.n0 + c ? args.N - tc.n0 - c : 0u)) - 1u;
                     if (!__any_sync(0xFFFFFFFFu, ev != 0)) continue;
+                    if (io.query_rows) {
+                        // this thread's row is query column m (one eye, one
+                        // rotation); its 16 columns are templates. Events are
+                        // rare: each thread folds its own into the per-eye minima.
+                        const uint32_t gcol = m + io.col0;
+                        const uint32_t eye = gcol / io.rho, rot = gcol % io.rho;
+                        uint32_t cm = 0xFFFFFFFFu, cz = 0xFFFFFFFFu;
+                        for (int jj = 0; jj < 16; ++jj) {
+                            if (!((ev >> jj) & 1u)) continue;
+                            const uint32_t t = tc.n0 + c + jj;
+                            int32_t inner, ov;
+                            if constexpr (kF4) {
+                                inner = __float2int_rn(__uint_as_float(a1[jj]));
+                                ov = __float2int_rn(__uint_as_float(a2[jj]));
+                            } else {
+                                inner = static_cast<int32_t>(a1[jj]);
+                                ov = static_cast<int32_t>(a2[jj]);
+                            }
+                            const uint32_t lin = rot * args.N + t;
+                            double* sc_out = io.scores ? io.scores + static_cast<size_t>(gcol) * args.N + t : nullptr;
+                            if (ov == 0) {
+                                cz = min(cz, lin);
+                                if (sc_out) *sc_out = __longlong_as_double(0x7FF8000000000000ll);
+                                continue;
+                            }
+                            bool hit;  // iris_core.cpp:58; the screens as below
+                            const float q = __fdividef(static_cast<float>(inner), static_cast<float>(ov));
+                            if (!sc_out && q >= io.lo_in && q <= io.hi_in) {
+                                hit = true;
+                            } else if (!sc_out && (q < io.lo_out || q > io.hi_out)) {
+                                hit = false;
+                            } else {
+                                const double sc = __ddiv_rn(static_cast<double>(inner), static_cast<double>(ov));
+                                hit = sc >= io.lo && sc <= io.hi;  // Interval::contains
+                                if (sc_out) *sc_out = sc;
+                            }
+                            if (hit) {
+                                cm = min(cm, lin);
+                                if (io.bits) io.bits[static_cast<size_t>(eye) * args.N + t] = 1;
+                            }
+                        }
+                        if (io.first) {
+                            if (cm != 0xFFFFFFFFu) atomicMin(io.first + 2 * eye, cm);
+                            if (cz != 0xFFFFFFFFu) atomicMin(io.first + 2 * eye + 1, cz);
+                        }
+                        continue;
+                    }
                     for (int jj = 0; jj < 16; ++jj) {
                         const uint32_t col = tc.n0 + c + jj;
                         if (col >= args.N) break;  // uniform across the warp
@@ -846,7 +903,8 @@ struct Shape {
     int ctas() const { return 2 * pm * pn; }
 };
 using KernelFn = void (*)(CUtensorMap, CUtensorMap, GemmArgs);
-constexpr Shape kShapes[] = {{1, 1}, {1, 2}, {1, 4}, {2, 2}, {2, 4}, {1, 8}};
+constexpr Shape kShapes[] = {{1, 1}, {1, 2}, {1, 4}, {2, 2}, {2, 4}, {1, 8}, {4, 1}};
+constexpr int kShape4x1 = 6;  // the FP4 iris match with the query on M (IrisMatchOut::query_rows)
 constexpr int kNumShapes = sizeof(kShapes) / sizeof(kShapes[0]);
 
 int shape_index(int pm, int pn) {
@@ -874,6 +932,7 @@ KernelFn kernel_for(int si, int mode = kModePsq) {
         switch (si) {
             case 0: return ppmm_i8_sm100_kernel<1, 1, kModeIrisMatchF4>;
             case 2: return ppmm_i8_sm100_kernel<1, 4, kModeIrisMatchF4>;
+            case kShape4x1: return ppmm_i8_sm100_kernel<4, 1, kModeIrisMatchF4>;
             default: return nullptr;
         }
     }
@@ -896,7 +955,7 @@ KernelFn kernel_for(int si, int mode = kModePsq) {
 }
 
 // Co-resident clusters of a shape with this kernel's footprint (cached per device).
-uint32_t max_active_clusters(int si, int dev) {
+uint32_t max_active_clusters(int si, int dev, int mode = kModePsq) {
     static std::mutex mu;
     static int cache[64][kNumShapes];
     static bool init = false;
@@ -909,7 +968,9 @@ uint32_t max_active_clusters(int si, int dev) {
     if (dev < 0 || dev >= 64 || si < 0) return 0;
     if (cache[dev][si] >= 0) return static_cast<uint32_t>(cache[dev][si]);
     const int ctas = kShapes[si].ctas();
-    KernelFn kfn = kernel_for(si);
+    KernelFn kfn = kernel_for(si);  // every mode has the same footprint; psq has the most shapes
+    if (!kfn) kfn = kernel_for(si, mode);
+    if (!kfn) return 0;
     if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(kSmemBytes)) != cudaSuccess)
         return 0;
@@ -978,8 +1039,11 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     // cluster shape: a multi-pair shape needs at least pn n-tiles; otherwise
     // the widest shape that divides the n-tiles (1x2 or a plain pair)
     int si = shape_index(L.cluster_pm, L.cluster_pn);
-    // the inner / iris modes are built for 1x1 and 1x4 (2x4 measured 40% slower for iris)
-    if (L.mode != kModePsq && si != 0) si = 2;
+    // the inner / iris modes are built for 1x1 and 1x4 (2x4 measured 40% slower
+    // for iris); the FP4 match with the query on M runs on 4x1 (the four pairs
+    // share each database tile and cover 1024 query columns)
+    const bool query_rows = (L.mode == kModeIrisMatch || L.mode == kModeIrisMatchF4) && L.iris.query_rows;
+    if (L.mode != kModePsq && si != 0) si = query_rows && L.mode == kModeIrisMatchF4 ? kShape4x1 : 2;
     if (si < 0) si = 0;
     // Short launches (a few waves of units) finish sooner on plain pairs: 74
     // workers instead of 15 clusters + a filler whose solo pairs sweep a whole
@@ -990,7 +1054,7 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     if (args.n_blocks < static_cast<uint32_t>(kShapes[si].pn))
         si = (L.mode == kModePsq && args.n_blocks % 2 == 0 && kShapes[si].pm == 1) ? 1 : 0;
     const uint32_t occ2 = max_active_clusters(0, dev);
-    uint32_t occ_main = si == 0 ? occ2 : max_active_clusters(si, dev);
+    uint32_t occ_main = si == 0 ? occ2 : max_active_clusters(si, dev, L.mode);
     if (occ_main == 0) {
         si = 0;
         occ_main = occ2;
@@ -1030,8 +1094,9 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     args.out_i32[0] = L.out_i32[0];
     args.out_i32[1] = L.out_i32[1];
     if (L.mode != kModePsq && L.accumulate) return cudaErrorInvalidValue;
-    if ((L.mode == kModeIrisMatch || L.mode == kModeIrisMatchF4) && (L.parts != 1 || L.nprimes != 1 || L.iris.rho == 0 ||
-                                     static_cast<uint64_t>(L.iris.rho) * L.M >= 0xFFFFFFFFull))
+    if ((L.mode == kModeIrisMatch || L.mode == kModeIrisMatchF4) &&
+        (L.parts != 1 || L.nprimes != 1 || L.iris.rho == 0 ||
+         static_cast<uint64_t>(L.iris.rho) * (query_rows ? L.N : L.M) >= 0xFFFFFFFFull))
         return cudaErrorInvalidValue;
     args.iris = L.iris;
     {
@@ -1118,6 +1183,8 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
         // a cluster that covers a whole n-chunk (G == 1, multi-pair) is the only
         // reader of its DB tile: stream it evict-first so the query stays in L2
         a.a_evict_first = (sh.pn > 1 && a.G == 1 && !std::getenv("IRL_PPMM_A_NORMAL")) ? 1u : 0u;
+        // likewise B when the launch streams it through clusters along M
+        a.b_evict_first = (L.b_streamed && sh.pm > 1 && sh.pn == 1) ? 1u : 0u;
         a.progress = L.progress + pt.pair0;  // indexed by cluster id (< pairs of this launch)
         a.mailbox = reinterpret_cast<unsigned long long*>(L.progress + kProgressWords + 32) +
                     static_cast<size_t>(pt.group0) * mail_slots;

@@ -177,8 +177,17 @@ class IrisDatabase:
         self.n_db, self.d, self.max_cols = n.value, d.value, max_cols
         return self
 
-    def match_packed(self, q_code, q_mask, n_eyes: int, rho: int, p_int: Interval, want_scores=False):
-        bits = np.zeros((n_eyes, self.n_db), np.uint8)
+    def match_packed(self, q_code, q_mask, n_eyes: int, rho: int, p_int: Interval, want_scores=False,
+                     out_bits=None):
+        """out_bits: optional C-contiguous uint8 [n_eyes][n_db] array the match bits are
+        written into (and returned), so a caller matching batch after batch reuses one
+        buffer instead of faulting in fresh pages every call."""
+        if out_bits is None:
+            bits = np.zeros((n_eyes, self.n_db), np.uint8)
+        else:
+            bits = out_bits
+            if bits.dtype != np.uint8 or bits.shape != (n_eyes, self.n_db) or not bits.flags.c_contiguous:
+                raise ValueError("out_bits must be a C-contiguous uint8 array of shape (n_eyes, n_db)")
         res = np.zeros(n_eyes, np.int32)
         sc = np.zeros((n_eyes * rho, self.n_db), np.float64) if want_scores else None
         st = capi.lib().irl_iris_db_match(self.handle, _p(q_code), _p(q_mask), n_eyes, rho, float(p_int.lo),
