@@ -346,7 +346,7 @@ const char* irl_last_error(const irl_ctx* ctx) { return ctx ? ctx->err.c_str() :
 
 int irl_diag_ppmm(irl_ctx* ctx, int enable, uint64_t* out, size_t cap) {
     if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     if (enable && !ctx->d_diag) IRL_CK(ctx, cudaMalloc(&ctx->d_diag, 1024 * kStatSlots * sizeof(uint64_t)));
     if (out && ctx->d_diag) {
         IRL_CK(ctx, cudaDeviceSynchronize());
@@ -410,7 +410,7 @@ void irl_synth_residues_host(uint64_t seed, uint32_t stream, uint32_t plane, uin
 int irl_digit_decompose(irl_ctx* ctx, const int32_t* m, size_t rows, size_t cols, uint32_t p,
                         int32_t* d0, int32_t* d1) {
     if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     if (p >= 256) return set_err(ctx, IRL_ERR_MODULUS_TOO_LARGE, "digit base must be < 2^8");
     if (p == 0) return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "digit base must be positive");
     const size_t n = rows * cols;
@@ -429,7 +429,7 @@ int irl_digit_decompose(irl_ctx* ctx, const int32_t* m, size_t rows, size_t cols
 int irl_digit_recompose(irl_ctx* ctx, const int32_t* d0, const int32_t* d1, size_t rows,
                         size_t cols, uint32_t p, int32_t* out) {
     if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     if (p == 0 || p > 46340)
         return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "p^2 must fit a positive int32");
     const size_t n = rows * cols;
@@ -452,7 +452,7 @@ int irl_digit_recompose(irl_ctx* ctx, const int32_t* d0, const int32_t* d1, size
 int irl_small_gemm(irl_ctx* ctx, const int32_t* a, const int32_t* b, int32_t* c, size_t m,
                    size_t k, size_t n) {
     if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     if (m > UINT32_MAX || k > UINT32_MAX || n > UINT32_MAX)
         return set_err(ctx, IRL_ERR_UNSUPPORTED, "dimension above 2^32");
     const size_t na = m * k, nb = k * n, nc = m * n;
@@ -484,7 +484,7 @@ int irl_small_gemm(irl_ctx* ctx, const int32_t* a, const int32_t* b, int32_t* c,
 int irl_gemm_mod_psq(irl_ctx* ctx, const int32_t* a, const int32_t* b, int32_t* c, size_t m,
                      size_t k, size_t n, uint32_t p) {
     if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     // digit_decompose(a, p) throws first (modmat.cpp:87, :145).
     if (p >= 256) return set_err(ctx, IRL_ERR_MODULUS_TOO_LARGE, "digit base must be < 2^8");
     if (p == 0) return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "digit base must be positive");
@@ -557,7 +557,7 @@ int irl_gemm_mod_Q(irl_ctx* ctx, const uint8_t* a, const uint8_t* b, uint8_t* c,
                    size_t k, size_t n, size_t width, const uint32_t* primes, const uint32_t* exps,
                    size_t nmod) {
     if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     int st = validate_moduli(ctx, primes, exps, nmod);
     if (st) return st;
     const Limbs Q = basis_Q(primes, exps, nmod);
@@ -696,7 +696,7 @@ int irl_split_rows_u16(irl_ctx* ctx, const uint16_t* res, size_t ld_res, size_t 
                        size_t rows, size_t cols, const uint32_t* primes, const uint32_t* exps,
                        size_t nmod, int8_t* planes, size_t ldk, void* stream) {
     if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     int st = validate_moduli(ctx, primes, exps, nmod);
     if (st) return st;
     if (ldk % 16 || ldk < cols) return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "ldk must be >= cols and a multiple of 16");
@@ -710,7 +710,7 @@ int irl_split_cols_u16(irl_ctx* ctx, const uint16_t* res, size_t ld_res, size_t 
                        size_t k, size_t n, const uint32_t* primes, const uint32_t* exps,
                        size_t nmod, int8_t* planes, size_t ldk, void* stream) {
     if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     int st = validate_moduli(ctx, primes, exps, nmod);
     if (st) return st;
     if (ldk % 16 || ldk < k) return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "ldk must be >= k and a multiple of 16");
@@ -724,7 +724,7 @@ int irl_split_bigint(irl_ctx* ctx, const uint8_t* entries, size_t width, size_t 
                      int transpose, const uint32_t* primes, const uint32_t* exps, size_t nmod,
                      int8_t* planes, size_t ldk, void* stream) {
     if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     int st = validate_moduli(ctx, primes, exps, nmod);
     if (st) return st;
     for (size_t i = 0; i < nmod; ++i)
@@ -743,7 +743,7 @@ int irl_ppmm_planes(irl_ctx* ctx, const int8_t* a_planes, const int8_t* b_planes
                     const uint32_t* primes, const uint32_t* exps, size_t nmod, int accumulate,
                     void* stream) {
     if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     int st = validate_moduli(ctx, primes, exps, nmod);
     if (st) return st;
     if (ldk % 16 || ldk < k) return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "ldk must be >= k and a multiple of 16");
@@ -767,7 +767,7 @@ int irl_crt_lift(irl_ctx* ctx, const uint16_t* res, size_t m, size_t n, uint8_t*
                  size_t width, const uint32_t* primes, const uint32_t* exps, size_t nmod,
                  void* stream) {
     if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     int st = validate_moduli(ctx, primes, exps, nmod);
     if (st) return st;
     const Limbs Q = basis_Q(primes, exps, nmod);
@@ -803,7 +803,7 @@ int irl_rescale_residues(irl_ctx* ctx, const uint16_t* in, size_t ld_in, size_t 
                          const uint32_t* exps, size_t nmod, size_t drop, int round, uint16_t* out, size_t ld_out,
                          void* stream) {
     if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     int st = validate_moduli(ctx, primes, exps, nmod);
     if (st) return st;
     if (drop == 0 || drop >= nmod) return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "rescale: need 0 < drop < nmod");

@@ -67,7 +67,7 @@ extern "C" {
 int irl_ccmm_create(irl_ctx* ctx, size_t parts, size_t m, size_t k, size_t max_n,
                     const uint32_t* primes, const uint32_t* exps, size_t nmod, irl_ccmm** out) {
     if (!ctx || !out) return IRL_ERR_INVALID_ARGUMENT;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     *out = nullptr;
     int st = validate_moduli(ctx, primes, exps, nmod);
     if (st) return st;
@@ -154,7 +154,7 @@ int irl_ccmm_alloc_recv(irl_ccmm* e, size_t n, void** dev_ptr, uint8_t* ipc_hand
 int irl_ccmm_alloc_recv_parts(irl_ccmm* e, size_t n, size_t parts, void** dev_ptr, uint8_t* ipc_handle) {
     if (!e || !dev_ptr || parts == 0) return IRL_ERR_INVALID_ARGUMENT;
     irl_ctx* ctx = e->ctx;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     if (n == 0 || n > e->max_n) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: receive width out of range");
     if (e->recv) cudaFree(e->recv);
     e->recv = nullptr;
@@ -205,19 +205,19 @@ static int set_mirrors(irl_ccmm* e, size_t part, size_t n, uint16_t* const* ptrs
 
 int irl_ccmm_set_mirrors(irl_ccmm* e, size_t part, size_t n, const uint8_t* ipc_handles, size_t count) {
     if (!e || (count && !ipc_handles)) return IRL_ERR_INVALID_ARGUMENT;
-    Guard g(e->ctx);
+    Guard g(e->ctx, __func__);
     return set_mirrors(e, part, n, nullptr, ipc_handles, count);
 }
 
 int irl_ccmm_set_mirror_ptrs(irl_ccmm* e, size_t part, size_t n, uint16_t* const* dev_ptrs, size_t count) {
     if (!e || (count && !dev_ptrs)) return IRL_ERR_INVALID_ARGUMENT;
-    Guard g(e->ctx);
+    Guard g(e->ctx, __func__);
     return set_mirrors(e, part, n, dev_ptrs, nullptr, count);
 }
 
 int irl_ccmm_set_mirror_parts(irl_ccmm* e, size_t count) {
     if (!e) return IRL_ERR_INVALID_ARGUMENT;
-    Guard g(e->ctx);
+    Guard g(e->ctx, __func__);
     if (count == 0 || e->mirror_part + count > e->parts)
         return set_err(e->ctx, IRL_ERR_INVALID_ARGUMENT, "ccmm: mirrored part range out of range");
     e->mirror_parts = count;
@@ -226,7 +226,7 @@ int irl_ccmm_set_mirror_parts(irl_ccmm* e, size_t count) {
 
 int irl_ccmm_set_mirror_slot(irl_ccmm* e, size_t slot) {
     if (!e) return IRL_ERR_INVALID_ARGUMENT;
-    Guard g(e->ctx);
+    Guard g(e->ctx, __func__);
     if (slot >= IRL_RECV_SLOTS) return set_err(e->ctx, IRL_ERR_INVALID_ARGUMENT, "ccmm: mirror slot out of range");
     e->mirror_slot = slot;
     return IRL_OK;
@@ -235,7 +235,7 @@ int irl_ccmm_set_mirror_slot(irl_ccmm* e, size_t slot) {
 int irl_ccmm_set_mirror_multicast(irl_ccmm* e, size_t part, size_t n, void* mc_addr) {
     if (!e) return IRL_ERR_INVALID_ARGUMENT;
     irl_ctx* ctx = e->ctx;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     if (mc_addr && (part >= e->parts || n == 0 || n > e->max_n || (e->M & 1) != 0))
         return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "ccmm: bad multicast mirror (part, width, or odd M)");
     e->mc_mirror = static_cast<uint16_t*>(mc_addr);
@@ -258,7 +258,7 @@ int irl_ccmm_buffers(irl_ccmm* e, void** qres, void** out) {
 int irl_ccmm_load_part(irl_ccmm* e, size_t part, const uint16_t* res, int res_on_device) {
     if (!e) return IRL_ERR_INVALID_ARGUMENT;
     irl_ctx* ctx = e->ctx;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     if (part >= e->parts) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: part index out of range");
     const size_t plane_elems = e->M * e->K;
     int8_t* dst = e->db + part * e->nmod * 2 * e->M * e->ldk;
@@ -282,7 +282,7 @@ int irl_ccmm_load_part(irl_ccmm* e, size_t part, const uint16_t* res, int res_on
 int irl_ccmm_load_part_bigint(irl_ccmm* e, size_t part, const uint8_t* entries, size_t width) {
     if (!e) return IRL_ERR_INVALID_ARGUMENT;
     irl_ctx* ctx = e->ctx;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     if (part >= e->parts) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: part index out of range");
     if (width == 0 || width > kMaxWidth) return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "width must be 1..48");
     for (size_t i = 0; i < e->nmod; ++i)
@@ -311,7 +311,7 @@ int irl_ccmm_load_part_bigint(irl_ccmm* e, size_t part, const uint8_t* entries, 
 int irl_ccmm_load_part_file(irl_ccmm* e, size_t part, const char* path) {
     if (!e || !path) return IRL_ERR_INVALID_ARGUMENT;
     irl_ctx* ctx = e->ctx;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     if (part >= e->parts) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: part index out of range");
     for (size_t i = 0; i < e->nmod; ++i)
         if (e->mt.mc[i].e != 2) return set_err(ctx, IRL_ERR_UNSUPPORTED, "bigint ingest needs e = 2");
@@ -410,7 +410,7 @@ int irl_ccmm_load_part_file(irl_ccmm* e, size_t part, const char* path) {
 int irl_ccmm_synth_db(irl_ccmm* e, uint64_t seed, uint32_t first_part) {
     if (!e) return IRL_ERR_INVALID_ARGUMENT;
     irl_ctx* ctx = e->ctx;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     for (size_t p = 0; p < e->parts; ++p) {
         IRL_LAUNCH(ctx, launch_synth_planes(seed, first_part + uint32_t(p), 1, uint32_t(e->M), uint32_t(e->K), e->mt,
                                             e->db + p * e->nmod * 2 * e->M * e->ldk, e->ldk, ctx->stream));
@@ -422,7 +422,7 @@ int irl_ccmm_synth_db(irl_ccmm* e, uint64_t seed, uint32_t first_part) {
 int irl_ccmm_synth_part(irl_ccmm* e, size_t part, uint64_t seed, uint32_t global_part, uint32_t row0) {
     if (!e) return IRL_ERR_INVALID_ARGUMENT;
     irl_ctx* ctx = e->ctx;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     if (part >= e->parts) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: part index out of range");
     IRL_LAUNCH(ctx, launch_synth_planes(seed, global_part, 1, uint32_t(e->M), uint32_t(e->K), e->mt,
                                         e->db + part * e->nmod * 2 * e->M * e->ldk, e->ldk, ctx->stream, row0));
@@ -470,7 +470,7 @@ int irl_ccmm_run_device(irl_ccmm* e, const uint16_t* q_res_dev, int q_ready, siz
                         size_t part0, size_t nparts, uint16_t* out_dev, void* stream) {
     if (!e) return IRL_ERR_INVALID_ARGUMENT;
     irl_ctx* ctx = e->ctx;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     if (n == 0 || n > e->max_n) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: query width out of range");
     if (part0 + nparts > e->parts) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: part range out of range");
     cudaStream_t s = pick_stream(ctx, stream);
@@ -686,7 +686,7 @@ static int ccmm_run_columns(irl_ccmm* e, const uint16_t* q_res_host, size_t n, s
 int irl_ccmm_run(irl_ccmm* e, const uint16_t* q_res_host, size_t n, uint16_t* out_host) {
     if (!e) return IRL_ERR_INVALID_ARGUMENT;
     irl_ctx* ctx = e->ctx;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     if (n == 0) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: query width out of range");
     // Query batches wider than the engine's staging capacity stream through it
     // in column chunks (whole 256-column tiles when max_n allows).
@@ -701,7 +701,7 @@ int irl_ccmm_run(irl_ccmm* e, const uint16_t* q_res_host, size_t n, uint16_t* ou
 int irl_ccmm_run_dq(irl_ccmm* e, const uint16_t* q_res_dev, size_t n, uint16_t* out_host, void* stream) {
     if (!e || !out_host) return IRL_ERR_INVALID_ARGUMENT;
     irl_ctx* ctx = e->ctx;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     if (n == 0 || n > e->max_n) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: query width out of range");
     cudaStream_t s = pick_stream(ctx, stream);
     if (!q_res_dev) q_res_dev = e->qres;
@@ -748,7 +748,7 @@ int irl_ccmm_rescale(irl_ccmm* e, size_t n, size_t part0, size_t nparts, size_t 
                      void* stream) {
     if (!e || !dst) return IRL_ERR_INVALID_ARGUMENT;
     irl_ctx* ctx = e->ctx;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     if (n == 0 || n > e->max_n || part0 + nparts > e->parts)
         return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: rescale range out of range");
     std::vector<uint32_t> primes(e->nmod), exps(e->nmod);
@@ -775,7 +775,7 @@ int irl_ccmm_twin(irl_ctx* ctx, long d1, long d2, long d3, long n_db, long n_qry
                   int out_level, int top_level, int out_slot_encoding, int out_ci,
                   const double* db, const double* qry, double* msgs) {
     if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     // emulator.cpp:392-410, same order and messages
     if (d1 <= 0 || d2 <= 0 || d3 <= 0) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "ccmm: nonpositive dimensions");
     if (n_db <= 0 || n_qry <= 0 || d1 % n_db != 0 || d2 % n_qry != 0)

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstdint>
@@ -95,13 +96,25 @@ inline int cuda_fail(irl_ctx* ctx, cudaError_t e, const char* where) {
         ++(ctx)->launches;                                             \
     } while (0)
 
+// Every C-ABI entry point holds one: the context's lock, its device, a cleared
+// error string, and an NVTX range named after the entry point (visible to
+// ncu --nvtx / Nsight Systems; a no-op without an attached tool).
 struct Guard {
     irl_ctx* c;
     std::lock_guard<std::recursive_mutex> lk;
-    explicit Guard(irl_ctx* ctx) : c(ctx), lk(ctx->mu) {
+    explicit Guard(irl_ctx* ctx, const char* range = nullptr) : c(ctx), lk(ctx->mu), named(range != nullptr) {
         cudaSetDevice(ctx->device);
         ctx->err.clear();
+        if (named) nvtxRangePushA(range);
     }
+    ~Guard() {
+        if (named) nvtxRangePop();
+    }
+    Guard(const Guard&) = delete;
+    Guard& operator=(const Guard&) = delete;
+
+   private:
+    bool named;
 };
 
 inline cudaStream_t pick_stream(irl_ctx* ctx, void* s) {

@@ -339,7 +339,7 @@ extern "C" {
 int irl_fold_stage_device(irl_ctx* ctx, const irl_fold_params* p, const int32_t* inner, const int32_t* overlap,
                           double* folded, double* refolded, uint32_t* flags, void* stream) {
     if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     FoldArgs a;
     if (int st = fold_prepare(ctx, p, refolded != nullptr, &a)) return st;
     if (!inner || !overlap || !flags) return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "fold: null buffer");
@@ -354,7 +354,7 @@ int irl_fold_stage_device(irl_ctx* ctx, const irl_fold_params* p, const int32_t*
 int irl_fold_stage(irl_ctx* ctx, const irl_fold_params* p, const int32_t* inner, const int32_t* overlap,
                    double* folded, double* refolded, int32_t* assumption_ok) {
     if (!ctx) return IRL_ERR_INVALID_ARGUMENT;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     FoldArgs a;
     if (int st = fold_prepare(ctx, p, refolded != nullptr, &a)) return st;
     if (!inner || !overlap) return set_err(ctx, IRL_ERR_INVALID_ARGUMENT, "fold: null buffer");

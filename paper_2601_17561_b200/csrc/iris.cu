@@ -365,7 +365,7 @@ int irl_iris_inner_overlap(irl_ctx* ctx, const uint64_t* db_code, const uint64_t
                            const uint64_t* q_code, const uint64_t* q_mask, size_t n_eyes, size_t rho, size_t d,
                            int32_t* inner, int32_t* overlap) {
     if (int st = check_args(ctx, db_code, db_mask, n_db, q_code, q_mask, n_eyes, d)) return st;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     const size_t cols = n_eyes * rho;
     if (cols == 0 || n_db == 0) return IRL_OK;
     int32_t *di = nullptr, *dov = nullptr;
@@ -382,7 +382,7 @@ int irl_iris_match(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db_mas
                    const uint64_t* q_code, const uint64_t* q_mask, size_t n_eyes, size_t rho, size_t d,
                    double p_lo, double p_hi, uint8_t* match_bits, int32_t* eye_result, double* scores) {
     if (int st = check_args(ctx, db_code, db_mask, n_db, q_code, q_mask, n_eyes, d)) return st;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     const size_t cols = n_eyes * rho;
     if (cols == 0 || n_db == 0) {
         // match_db_reference over an empty product: no score is evaluated
@@ -418,7 +418,7 @@ int irl_iris_db_create(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db
     if (!out) return IRL_ERR_INVALID_ARGUMENT;
     *out = nullptr;
     if (int st = check_args(ctx, db_code, db_mask, n_db, db_code, db_mask, 0, d)) return st;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     if (n_db == 0 || max_cols == 0) return set_err(ctx, IRL_ERR_SHAPE_MISMATCH, "iris db: empty database or batch");
     if (int st = check_dims(ctx, n_db, max_cols, d)) return st;
     auto* e = new irl_iris_db();
@@ -453,7 +453,7 @@ int irl_iris_db_create_file(irl_ctx* ctx, const char* path, size_t max_cols, irl
                             size_t* d_out) {
     if (!ctx || !path || !out) return IRL_ERR_INVALID_ARGUMENT;
     *out = nullptr;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     std::FILE* f = std::fopen(path, "rb");
     if (!f) return set_err(ctx, IRL_ERR_IO, std::string("cannot open ") + path);
     struct Closer {
@@ -535,7 +535,7 @@ int irl_iris_db_match(irl_iris_db* e, const uint64_t* q_code, const uint64_t* q_
     if (!e) return IRL_ERR_INVALID_ARGUMENT;
     irl_ctx* ctx = e->ctx;
     if (int st = check_args(ctx, q_code, q_mask, 0, q_code, q_mask, n_eyes, e->d)) return st;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     const size_t cols = n_eyes * rho;
     if (cols == 0) {
         if (eye_result) std::memset(eye_result, 0, n_eyes * sizeof(int32_t));
@@ -558,7 +558,7 @@ int irl_iris_db_fold(irl_iris_db* e, const uint64_t* q_code, const uint64_t* q_m
                      double* folded, double* refolded, int32_t* assumption_ok) {
     if (!e || !p) return IRL_ERR_INVALID_ARGUMENT;
     irl_ctx* ctx = e->ctx;
-    Guard g(ctx);
+    Guard g(ctx, __func__);
     FoldArgs a;
     if (int st = fold_prepare(ctx, p, refolded != nullptr, &a)) return st;  // run_alg2: cfg.validate() first
     // prepare (pipeline.cpp:100-118)
