@@ -55,10 +55,16 @@ size_t plane_ldk(size_t d) { return round16(plane_kbytes(d)); }
 // for the paper's batch) would cost a second, mostly padding pass of the
 // whole cluster, so it runs as its own launch on plain pairs. Returns the
 // columns of the main launch, 0 = no split.
-// The fused FP4 match puts the query columns on M (IrisMatchOut::query_rows):
-// one 4x1-cluster pass over the database covers up to 1024 columns, so the
-// query planes are not split. IRL_IRIS_DB_ON_M=1 keeps the database on M.
-bool match_query_rows(size_t d) { return iris_f4(d) && !std::getenv("IRL_IRIS_DB_ON_M"); }
+// The fused FP4 match puts the query columns on M (IrisMatchOut::query_rows)
+// for batches of more than 768 columns: one 4x1-cluster pass over the
+// database covers up to 1024 columns (four 256-row blocks), so the query
+// planes are not split. Smaller batches would leave blocks of the cluster
+// idle and keep the database on M. IRL_IRIS_DB_ON_M=1 / IRL_IRIS_QUERY_ON_M=1
+// force either layout.
+bool match_query_rows(size_t d, size_t cols) {
+    if (!iris_f4(d) || std::getenv("IRL_IRIS_DB_ON_M")) return false;
+    return cols > 3 * 256 || std::getenv("IRL_IRIS_QUERY_ON_M") != nullptr;
+}
 
 size_t col_split(size_t cols, size_t d) {
     if (!iris_f4(d) || std::getenv("IRL_IRIS_NO_SPLIT")) return 0;
@@ -228,7 +234,7 @@ int match_fused(irl_ctx* ctx, const int8_t* xp, const int8_t* yp, size_t n_db, s
     // unsplit. Otherwise one launch per column range of build_query_planes
     // (see col_split); the launches fold into the same first-event indices
     // and match bits.
-    const bool qrows = match_query_rows(d);
+    const bool qrows = match_query_rows(d, cols);
     const size_t split = qrows ? 0 : col_split(cols, d);
     const size_t ranges[2][2] = {{0, split ? split : cols}, {split, split ? cols - split : 0}};
     for (const auto& rg : ranges) {
@@ -407,7 +413,8 @@ int irl_iris_match(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db_mas
     IRL_CK(ctx, copy_h2d(ctx, qc, q_code, q_bits, s));
     IRL_CK(ctx, copy_h2d(ctx, qm, q_mask, q_bits, s));
     if (int st = build_planes(ctx, dc, dm, n_db, 1, d, ctx->ws[1].as<int8_t>(), s)) return st;
-    if (int st = build_query_planes(ctx, qc, qm, n_eyes, rho, d, ctx->ws[2].as<int8_t>(), s, !match_query_rows(d)))
+    if (int st = build_query_planes(ctx, qc, qm, n_eyes, rho, d, ctx->ws[2].as<int8_t>(), s,
+                                    !match_query_rows(d, n_eyes * rho)))
         return st;
     return match_fused(ctx, ctx->ws[1].as<int8_t>(), ctx->ws[2].as<int8_t>(), n_db, n_eyes, rho, d, ldk, p_lo, p_hi,
                        match_bits, eye_result, scores, ctx->ws[4], ctx->d_progress, s);
@@ -548,7 +555,7 @@ int irl_iris_db_match(irl_iris_db* e, const uint64_t* q_code, const uint64_t* q_
     IRL_CK(ctx, cudaMemcpyAsync(e->qbits, q_code, qb, cudaMemcpyHostToDevice, s));
     IRL_CK(ctx, cudaMemcpyAsync(e->qbits + n_eyes * words, q_mask, qb, cudaMemcpyHostToDevice, s));
     if (int st = build_query_planes(ctx, e->qbits, e->qbits + n_eyes * words, n_eyes, rho, e->d, e->qplanes, s,
-                                    !match_query_rows(e->d)))
+                                    !match_query_rows(e->d, n_eyes * rho)))
         return st;
     return match_fused(ctx, e->planes, e->qplanes, e->n_db, n_eyes, rho, e->d, e->ldk, p_lo, p_hi, match_bits,
                        eye_result, scores, e->match_ws, e->progress, s);
