@@ -213,8 +213,20 @@ void parallel_memcpy(void* dst, const void* src, size_t bytes) {
 }
 }  // namespace
 
+// Page-locked host memory (cudaMallocHost / cudaHostRegister, e.g. a pinned
+// torch tensor) is DMA'd directly; pageable memory goes through the bounce
+// buffers from kDirectCopyBytes up.
+bool host_pinned(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
 cudaError_t copy_h2d(irl_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t s) {
-    if (bytes < kDirectCopyBytes) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+    if (bytes < kDirectCopyBytes || host_pinned(src)) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
     cudaError_t e = ensure_bounce(ctx);
     if (e != cudaSuccess) return e;
     for (size_t off = 0, i = 0; off < bytes; off += kBounceBytes, ++i) {
@@ -232,7 +244,7 @@ cudaError_t copy_h2d(irl_ctx* ctx, void* dst, const void* src, size_t bytes, cud
 
 cudaError_t copy_d2h(irl_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t s) {
     cudaError_t e;
-    if (bytes < kDirectCopyBytes) {
+    if (bytes < kDirectCopyBytes || host_pinned(dst)) {
         e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s);
         return e == cudaSuccess ? cudaStreamSynchronize(s) : e;
     }

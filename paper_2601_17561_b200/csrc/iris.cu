@@ -55,15 +55,21 @@ size_t plane_ldk(size_t d) { return round16(plane_kbytes(d)); }
 // for the paper's batch) would cost a second, mostly padding pass of the
 // whole cluster, so it runs as its own launch on plain pairs. Returns the
 // columns of the main launch, 0 = no split.
-// The fused FP4 match puts the query columns on M (IrisMatchOut::query_rows)
-// for batches of more than 768 columns: one 4x1-cluster pass over the
-// database covers up to 1024 columns (four 256-row blocks), so the query
-// planes are not split. Smaller batches would leave blocks of the cluster
-// idle and keep the database on M. IRL_IRIS_DB_ON_M=1 / IRL_IRIS_QUERY_ON_M=1
-// force either layout.
-bool match_query_rows(size_t d, size_t cols) {
+// The FP4 iris products (the fused match and the raw inner products /
+// overlaps) put the query columns on M (IrisMatchOut::query_rows) for batches
+// of more than 768 columns: one 4x1-cluster pass over the database covers up
+// to 1024 columns (four 256-row blocks), so the query planes are not split.
+// Smaller batches would leave blocks of the cluster idle and keep the
+// database on M. IRL_IRIS_DB_ON_M=1 / IRL_IRIS_QUERY_ON_M=1 force either layout.
+// The raw products (inner = true) default to the database on M: with the
+// query on M each thread stores 16 consecutive templates of one column, a
+// 64-byte run per row instead of the warp's coalesced 128-byte rows, and the
+// launch measured slower (1.78 ms against 1.32 + 0.32 ms at the paper's
+// scale, profiles/iris_diag.py --inner); it stays available forced.
+bool iris_query_rows(size_t d, size_t cols, bool inner = false) {
     if (!iris_f4(d) || std::getenv("IRL_IRIS_DB_ON_M")) return false;
-    return cols > 3 * 256 || std::getenv("IRL_IRIS_QUERY_ON_M") != nullptr;
+    if (std::getenv("IRL_IRIS_QUERY_ON_M")) return true;
+    return !inner && cols > 3 * 256;
 }
 
 size_t col_split(size_t cols, size_t d) {
@@ -157,6 +163,35 @@ __global__ void iris_file_planes_kernel(const uint8_t* __restrict__ code, const 
 // [2][cols][ldk]) into inner / overlap [cols][n_db].
 int inner_overlap_gemm(irl_ctx* ctx, const int8_t* xp, const int8_t* yp, size_t n_db, size_t cols, size_t d,
                        size_t ldk, int32_t* inner, int32_t* ovl, uint32_t* progress, cudaStream_t s) {
+    if (iris_query_rows(d, cols, true)) {
+        // one launch, the query planes on M: the outputs [cols][n_db] are the
+        // launch's [M][N], each thread storing 16 consecutive templates
+        PpmmLaunch L;
+        L.mode = kModeInnerF4;
+        L.a_planes = yp;
+        L.b_planes = xp;
+        L.out_i32[0] = inner;
+        L.out_i32[1] = ovl;
+        L.M = static_cast<uint32_t>(cols);
+        L.N = static_cast<uint32_t>(n_db);
+        L.K = static_cast<uint32_t>(plane_kbytes(d));
+        L.ldk = static_cast<uint32_t>(ldk);
+        L.parts = 1;
+        L.nprimes = 1;
+        L.mc[0] = make_modconst(2, 1);  // unused by the inner modes
+        L.progress = progress;
+        L.cluster_pm = 4;
+        L.cluster_pn = 1;
+        L.b_streamed = 1;
+        L.iris.query_rows = 1;
+        if (ctx->diag && ctx->d_diag) {
+            L.stats = ctx->d_diag;
+            IRL_CK(ctx, cudaMemsetAsync(ctx->d_diag, 0, 1024 * kStatSlots * sizeof(uint64_t), s));
+        }
+        IRL_LAUNCH(ctx, launch_ppmm_planes(L, s));
+        ctx->launches += ppmm_kernels_last_launch() > 1 ? ppmm_kernels_last_launch() - 1 : 0;  // + filler
+        return IRL_OK;
+    }
     // one launch per column range of build_query_planes (see col_split)
     const size_t split = col_split(cols, d);
     const size_t ranges[2][2] = {{0, split ? split : cols}, {split, split ? cols - split : 0}};
@@ -178,6 +213,10 @@ int inner_overlap_gemm(irl_ctx* ctx, const int8_t* xp, const int8_t* yp, size_t 
         L.mc[0] = make_modconst(2, 1);  // unused by the inner modes
         L.progress = progress;
         if (c0 > 0) L.cluster_pm = L.cluster_pn = 1;  // the remainder on plain pairs
+        if (ctx->diag && ctx->d_diag && c0 == 0) {  // irl_diag_ppmm: counters of the main launch
+            L.stats = ctx->d_diag;
+            IRL_CK(ctx, cudaMemsetAsync(ctx->d_diag, 0, 1024 * kStatSlots * sizeof(uint64_t), s));
+        }
         IRL_LAUNCH(ctx, launch_ppmm_planes(L, s));
         ctx->launches += ppmm_kernels_last_launch() > 1 ? ppmm_kernels_last_launch() - 1 : 0;  // + filler
     }
@@ -230,11 +269,11 @@ int match_fused(irl_ctx* ctx, const int8_t* xp, const int8_t* yp, size_t n_db, s
     double* dsc = scores ? reinterpret_cast<double*>(ws.as<uint8_t>() + off_sc) : nullptr;
     IRL_CK(ctx, cudaMemsetAsync(first, 0xFF, 8 * n_eyes, s));
     IRL_CK(ctx, cudaMemsetAsync(dbits, 0, nbits, s));
-    // Query columns on M (match_query_rows): one launch, the query planes
+    // Query columns on M (iris_query_rows): one launch, the query planes
     // unsplit. Otherwise one launch per column range of build_query_planes
     // (see col_split); the launches fold into the same first-event indices
     // and match bits.
-    const bool qrows = match_query_rows(d, cols);
+    const bool qrows = iris_query_rows(d, cols);
     const size_t split = qrows ? 0 : col_split(cols, d);
     const size_t ranges[2][2] = {{0, split ? split : cols}, {split, split ? cols - split : 0}};
     for (const auto& rg : ranges) {
@@ -331,7 +370,7 @@ int inner_overlap_device(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* 
     int8_t* xp = ctx->ws[1].as<int8_t>();
     int8_t* yp = ctx->ws[2].as<int8_t>();
     if (int st = build_planes(ctx, dc, dm, n_db, 1, d, xp, s)) return st;
-    if (int st = build_query_planes(ctx, qc, qm, n_eyes, rho, d, yp, s)) return st;
+    if (int st = build_query_planes(ctx, qc, qm, n_eyes, rho, d, yp, s, !iris_query_rows(d, cols, true))) return st;
     int32_t* inner = ctx->ws[3].as<int32_t>();
     int32_t* ovl = inner + cols * n_db;
     if (int st = inner_overlap_gemm(ctx, xp, yp, n_db, cols, d, ldk, inner, ovl, ctx->d_progress, s)) return st;
@@ -414,7 +453,7 @@ int irl_iris_match(irl_ctx* ctx, const uint64_t* db_code, const uint64_t* db_mas
     IRL_CK(ctx, copy_h2d(ctx, qm, q_mask, q_bits, s));
     if (int st = build_planes(ctx, dc, dm, n_db, 1, d, ctx->ws[1].as<int8_t>(), s)) return st;
     if (int st = build_query_planes(ctx, qc, qm, n_eyes, rho, d, ctx->ws[2].as<int8_t>(), s,
-                                    !match_query_rows(d, n_eyes * rho)))
+                                    !iris_query_rows(d, n_eyes * rho)))
         return st;
     return match_fused(ctx, ctx->ws[1].as<int8_t>(), ctx->ws[2].as<int8_t>(), n_db, n_eyes, rho, d, ldk, p_lo, p_hi,
                        match_bits, eye_result, scores, ctx->ws[4], ctx->d_progress, s);
@@ -555,7 +594,7 @@ int irl_iris_db_match(irl_iris_db* e, const uint64_t* q_code, const uint64_t* q_
     IRL_CK(ctx, cudaMemcpyAsync(e->qbits, q_code, qb, cudaMemcpyHostToDevice, s));
     IRL_CK(ctx, cudaMemcpyAsync(e->qbits + n_eyes * words, q_mask, qb, cudaMemcpyHostToDevice, s));
     if (int st = build_query_planes(ctx, e->qbits, e->qbits + n_eyes * words, n_eyes, rho, e->d, e->qplanes, s,
-                                    !match_query_rows(e->d, n_eyes * rho)))
+                                    !iris_query_rows(e->d, n_eyes * rho)))
         return st;
     return match_fused(ctx, e->planes, e->qplanes, e->n_db, n_eyes, rho, e->d, e->ldk, p_lo, p_hi, match_bits,
                        eye_result, scores, e->match_ws, e->progress, s);
@@ -589,7 +628,9 @@ int irl_iris_db_fold(irl_iris_db* e, const uint64_t* q_code, const uint64_t* q_m
     auto* dflags = reinterpret_cast<uint32_t*>(ws + off_flags);
     IRL_CK(ctx, cudaMemcpyAsync(e->qbits, q_code, qb, cudaMemcpyHostToDevice, s));
     IRL_CK(ctx, cudaMemcpyAsync(e->qbits + n_eyes * words, q_mask, qb, cudaMemcpyHostToDevice, s));
-    if (int st = build_query_planes(ctx, e->qbits, e->qbits + n_eyes * words, n_eyes, rho, e->d, e->qplanes, s)) return st;
+    if (int st = build_query_planes(ctx, e->qbits, e->qbits + n_eyes * words, n_eyes, rho, e->d, e->qplanes, s,
+                                    !iris_query_rows(e->d, cols, true)))
+        return st;
     if (int st = inner_overlap_gemm(ctx, e->planes, e->qplanes, e->n_db, cols, e->d, e->ldk, inner, ovl, e->progress, s))
         return st;
     IRL_CK(ctx, cudaMemsetAsync(dflags, 0, 8, s));

@@ -788,6 +788,33 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                 }
                 if (!row_ok) continue;
                 if constexpr (kInner) {
+                    if (args.iris.query_rows) {
+                        // outputs [M][N] (query column m, template n): 16
+                        // consecutive templates per thread, as 16-byte stores
+                        // when the row and chunk are aligned and in range
+                        const uint32_t n = tc.n0 + c;
+                        const size_t o = static_cast<size_t>(m) * args.N + n;
+                        const bool vec = n + 16 <= args.N && (args.N & 3u) == 0;
+                        // (the accumulator arrays are passed by reference and
+                        // indexed with constants, so they stay in registers)
+                        auto store_row = [&](int32_t* dst, const uint32_t (&v)[16]) {
+                            if (!dst) return;
+                            if (vec) {
+                                int4* d4 = reinterpret_cast<int4*>(dst + o);
+#pragma unroll
+                                for (int q = 0; q < 4; ++q)
+                                    d4[q] = make_int4(static_cast<int32_t>(v[4 * q]), static_cast<int32_t>(v[4 * q + 1]),
+                                                      static_cast<int32_t>(v[4 * q + 2]), static_cast<int32_t>(v[4 * q + 3]));
+                            } else {
+#pragma unroll
+                                for (int jj = 0; jj < 16; ++jj)
+                                    if (n + jj < args.N) dst[o + jj] = static_cast<int32_t>(v[jj]);
+                            }
+                        };
+                        store_row(args.out_i32[0], a1);
+                        store_row(args.out_i32[1], a2);
+                        continue;
+                    }
                     const size_t base = tc.part * args.out_part + static_cast<size_t>(tc.prime) * args.N * args.M +
                                         static_cast<size_t>(tc.n0 + c) * args.M + m;
                     for (int jj = 0; jj < 16; ++jj) {
@@ -925,6 +952,7 @@ KernelFn kernel_for(int si, int mode = kModePsq) {
         switch (si) {
             case 0: return ppmm_i8_sm100_kernel<1, 1, kModeInnerF4>;
             case 2: return ppmm_i8_sm100_kernel<1, 4, kModeInnerF4>;
+            case kShape4x1: return ppmm_i8_sm100_kernel<4, 1, kModeInnerF4>;
             default: return nullptr;
         }
     }
@@ -1042,8 +1070,9 @@ cudaError_t launch_ppmm_planes(const PpmmLaunch& L, cudaStream_t stream) {
     // the inner / iris modes are built for 1x1 and 1x4 (2x4 measured 40% slower
     // for iris); the FP4 match with the query on M runs on 4x1 (the four pairs
     // share each database tile and cover 1024 query columns)
-    const bool query_rows = (L.mode == kModeIrisMatch || L.mode == kModeIrisMatchF4) && L.iris.query_rows;
-    if (L.mode != kModePsq && si != 0) si = query_rows && L.mode == kModeIrisMatchF4 ? kShape4x1 : 2;
+    const bool query_rows = L.mode != kModePsq && L.iris.query_rows;
+    const bool f4 = L.mode == kModeIrisMatchF4 || L.mode == kModeInnerF4;
+    if (L.mode != kModePsq && si != 0) si = query_rows && f4 ? kShape4x1 : 2;
     if (si < 0) si = 0;
     // Short launches (a few waves of units) finish sooner on plain pairs: 74
     // workers instead of 15 clusters + a filler whose solo pairs sweep a whole

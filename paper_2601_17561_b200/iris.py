@@ -204,11 +204,13 @@ class IrisDatabase:
         return self.match_packed(qc, qm, len(eyes), rho, p_int, want_scores)
 
     def fold_packed(self, q_code, q_mask, n_eyes: int, cfg, want_folded: bool = True,
-                    want_refolded: Optional[bool] = None):
+                    want_refolded: Optional[bool] = None, out_folded=None, out_refolded=None):
         """run_alg2's post-CCMM stage against this database (irl_iris_db_fold):
         products and overlaps of the query eyes' rotations as tensor-core GEMMs (FP4), then
         the fold stage (fold.py) on the device. cfg: fold.FoldConfig with
-        cfg.d == the template length and n_db == len(db)."""
+        cfg.d == the template length and n_db == len(db). out_folded / out_refolded:
+        optional C-contiguous float64 arrays of the result shapes to write into and
+        return (reused across batches; page-locked ones are copied to by DMA directly)."""
         import ctypes as C
 
         from .fold import FoldResult, _Params, shapes
@@ -216,8 +218,17 @@ class IrisDatabase:
             want_refolded = bool(cfg.fold_chain)
         p = _Params(cfg, n_eyes, self.n_db)
         fshape, rshape = shapes(cfg, n_eyes, self.n_db)
-        folded = np.zeros(fshape) if want_folded and cfg.d > 0 else None
-        refolded = np.zeros(rshape) if want_refolded and cfg.d > 0 else None
+
+        def out(want, given, shape):
+            if not want or cfg.d <= 0:
+                return None
+            if given is None:
+                return np.zeros(shape)
+            if given.dtype != np.float64 or given.shape != tuple(shape) or not given.flags.c_contiguous:
+                raise ValueError(f"output buffer must be a C-contiguous float64 array of shape {tuple(shape)}")
+            return given
+        folded = out(want_folded, out_folded, fshape)
+        refolded = out(want_refolded, out_refolded, rshape)
         ok = C.c_int32(-1)
         self.ctx.check(capi.lib().irl_iris_db_fold(self.handle, _p(q_code), _p(q_mask), p.ref(),
                                                    _p(folded), _p(refolded), C.byref(ok)))

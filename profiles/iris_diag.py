@@ -19,6 +19,7 @@ sys.path.insert(0, str(ROOT))
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--runs", type=int, default=3)
+    ap.add_argument("--inner", action="store_true", help="the fold path's raw inner-product / overlap launch")
     a = ap.parse_args()
     from paper_2601_17561_b200 import capi
     from paper_2601_17561_b200.iris import Interval, IrisDatabase
@@ -30,15 +31,23 @@ def main():
     db = IrisDatabase.from_packed(dc, dm, d, eyes * rho)
     L = capi.lib()
     h = db.ctx.handle
-    db.match_packed(qc, qm, eyes, rho, Interval(0.35, 1.0))
+    from paper_2601_17561_b200.fold import FoldConfig
+    cfg = FoldConfig(rho=rho, fold_k=16, d=d)
+
+    def call():
+        if a.inner:  # the fold path: inner products and overlaps (kModeInnerF4), then the fold stage
+            db.fold_packed(qc, qm, eyes, cfg, want_folded=True, want_refolded=False)
+        else:
+            db.match_packed(qc, qm, eyes, rho, Interval(0.35, 1.0))
+    call()
     L.irl_diag_ppmm(h, 1, None, 0)
     buf = (C.c_uint64 * (1024 * 16))()
     for _ in range(a.runs):
-        db.match_packed(qc, qm, eyes, rho, Interval(0.35, 1.0))
+        call()
         L.irl_diag_ppmm(h, 1, buf, len(buf))
         st = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 16).astype(np.float64)
         act = st[:, 4] > 0
-        for name, sel in (("main 1x4 pairs", np.arange(1024) < 60), ("filler pairs", np.arange(1024) >= 60)):
+        for name, sel in (("main cluster pairs", np.arange(1024) < 60), ("filler pairs", np.arange(1024) >= 60)):
             g = st[act & sel]
             if len(g):
                 c = g[:, 4]
