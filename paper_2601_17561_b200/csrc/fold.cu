@@ -27,6 +27,10 @@
 #include "ctx_internal.h"
 #include "fold.cuh"
 
+#ifndef IRL_FOLD_PREFETCH
+#define IRL_FOLD_PREFETCH 1  // 0: the r07 loop (A/B variant builds)
+#endif
+
 namespace irl {
 
 namespace {
@@ -191,15 +195,48 @@ __global__ void __launch_bounds__(256, 8) fold_stage_kernel(const FoldArgs a) {
         const int32_t* in_row = inner + static_cast<size_t>(r0) * a.n_db;
         const int32_t* ov_row = overlap + static_cast<size_t>(r0) * a.n_db;
         uint32_t j = (i + r0) & dmask;
-        for (uint32_t r = r0; r < r_end; ++r, in_row += a.n_db, ov_row += a.n_db, j = (j + 1) & dmask) {
-            const int32_t raw = __ldcs(in_row + j);
-            const int32_t ov = __ldcs(ov_row + j);
+#if IRL_FOLD_PREFETCH
+        // Software-pipelined: the next rotation's product and overlap are
+        // loaded while this one is evaluated (its row is the current one again
+        // on the group's last rotation, so no load leaves the group's rows),
+        // and the shadow check is predicated, with the exact quotient behind
+        // one rarely taken branch.
+        int32_t raw_n = __ldcs(in_row + j), ov_n = __ldcs(ov_row + j);
+        for (uint32_t r = r0; r < r_end; ++r) {
+            const int32_t raw = raw_n, ov = ov_n;
+            const size_t step = r + 1 < r_end ? a.n_db : 0;
+            in_row += step;
+            ov_row += step;
+            j = step ? (j + 1) & dmask : j;
+            raw_n = __ldcs(in_row + j);
+            ov_n = __ldcs(ov_row + j);
             // normalize: message * (1.0 / overlap) (pipeline.cpp:364-369);
             // rcp[k] = RN(1 / k) for the overlaps a template can have
             const double inv = static_cast<uint32_t>(ov) <= a.rcp_max ? __ldg(a.rcp + ov)
                                                                       : __drcp_rn(static_cast<double>(ov));
             const double x = __dmul_rn(static_cast<double>(raw), inv);
-            // folding-assumption shadow check (pipeline.cpp:574-583)
+            // folding-assumption shadow check (pipeline.cpp:574-583): x decides
+            // outside the bands around the interval ends (see outside_negative)
+            const bool zero = ov == 0;
+            const bool sure_in = x >= a.lo_in && x <= a.hi_in;
+            const bool sure_out = x < a.lo_out || x > a.hi_out;
+            bool outside = sure_out;
+            if (!zero && !sure_in && !sure_out) {
+                const double q = __ddiv_rn(static_cast<double>(raw), static_cast<double>(ov));
+                outside = !(q >= a.neg_lo && q <= a.neg_hi);
+            }
+            non_d += (zero || outside) ? 1 : 0;
+            empty = empty || zero;
+            const double t = fold_poly<kFast, kFoldDeg>(a, fc, x);
+            acc = r == r0 ? t : __dadd_rn(acc, t);  // fold_group's running sum (pipeline.cpp:397-406)
+        }
+#else
+        for (uint32_t r = r0; r < r_end; ++r, in_row += a.n_db, ov_row += a.n_db, j = (j + 1) & dmask) {
+            const int32_t raw = __ldcs(in_row + j);
+            const int32_t ov = __ldcs(ov_row + j);
+            const double inv = static_cast<uint32_t>(ov) <= a.rcp_max ? __ldg(a.rcp + ov)
+                                                                      : __drcp_rn(static_cast<double>(ov));
+            const double x = __dmul_rn(static_cast<double>(raw), inv);
             if (ov == 0) {
                 empty = true;
                 ++non_d;
@@ -209,6 +246,7 @@ __global__ void __launch_bounds__(256, 8) fold_stage_kernel(const FoldArgs a) {
             const double t = fold_poly<kFast, kFoldDeg>(a, fc, x);
             acc = r == r0 ? t : __dadd_rn(acc, t);  // fold_group's running sum (pipeline.cpp:397-406)
         }
+#endif
         if (non_d > 1) violated = true;
         const size_t eb = static_cast<size_t>(e) * a.blocks + b;
         if (a.folded) a.folded[(eb * a.groups + g) * a.d + i] = acc;
