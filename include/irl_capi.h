@@ -282,6 +282,14 @@ int irl_ccmm_group_set_exchange(irl_ccmm_group* g, int mode);
 int irl_ccmm_group_engine(irl_ccmm_group* g, size_t rank, irl_ccmm** e, size_t* first_part, size_t* nparts);
 /* Context of a rank (irl_last_error of group calls is on rank 0's). */
 irl_ctx* irl_ccmm_group_ctx(irl_ccmm_group* g, size_t rank);
+/* Query distribution of irl_ccmm_full. -1 (default, auto): sharded when
+ * every rank holds about one paper-size part (parts x M < 20000 rows), where a
+ * rank's GEMM per modulus is shorter than its H2D; 0: every rank copies the
+ * whole query from the host (irl_ccmm_run); 1: sharded -- rank r copies its
+ * 1/ndev of the moduli from the host and pushes it to every other rank over
+ * peer memory (the paper's query AllGather), then every rank runs
+ * on the staged query (irl_ccmm_run_dq). Outputs are identical. */
+int irl_ccmm_group_set_query_shard(irl_ccmm_group* g, int mode);
 /* The full CCMM across the devices with HOST buffers: q_res [nmod][K][n] ->
  * out [parts][nmod][n][M] (every part, in global order); each rank runs its
  * parts end to end (irl_ccmm_run) concurrently with the others. The a-part

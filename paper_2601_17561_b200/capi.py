@@ -100,6 +100,7 @@ SIGNATURES = {
     "irl_ccmm_group_ctx": (vp, [vp, sz]),
     "irl_ccmm_full": (C.c_int, [vp, vp, sz, vp, C.POINTER(vp), C.POINTER(C.c_int)]),
     "irl_ccmm_group_set_exchange": (C.c_int, [vp, C.c_int]),
+    "irl_ccmm_group_set_query_shard": (C.c_int, [vp, C.c_int]),
     "irl_ccmm_set_mirror_multicast": (C.c_int, [vp, sz, sz, vp]),
 }
 

@@ -218,6 +218,11 @@ class CcmmGroup:
         """capi.IRL_EXCHANGE_AUTO / _P2P / _MULTICAST / _COPY (irl_ccmm_group_set_exchange)."""
         self.ctx.check(capi.lib().irl_ccmm_group_set_exchange(self.handle, mode))
 
+    def set_query_shard(self, mode: int):
+        """-1 auto, 0 every rank copies the whole query, 1 sharded host copies plus a
+        peer all-gather (irl_ccmm_group_set_query_shard)."""
+        self.ctx.check(capi.lib().irl_ccmm_group_set_query_shard(self.handle, mode))
+
     def run(self, q_res: np.ndarray, out: Optional[np.ndarray] = None):
         """q_res [nmod][K][n] -> (out [parts][nmod][n][M], per-rank device
         pointers of the a-part result, the IRL_EXCHANGE_* mode used)."""

@@ -128,6 +128,8 @@ struct irl_ccmm_group {
     size_t slot = 0;              // receive slot of the last irl_ccmm_full (alternates per call)
     int requested = IRL_EXCHANGE_AUTO;
     int mode = IRL_EXCHANGE_COPY;  // the exchange in use
+    int shard = -1;                // query distribution: -1 auto, 0 every rank copies it all, 1 sharded
+    bool peers_enabled = false;    // all-pairs peer access attempted (sharded query)
     McExchange mcx;
     std::mutex mu;  // one irl_ccmm_full / set_exchange at a time
 };
@@ -284,9 +286,96 @@ int setup_exchange(irl_ccmm_group* g, size_t n) {
     return IRL_OK;
 }
 
+// Sharded query distribution (PAPER.md:72's query AllGather): rank r copies
+// moduli [lo_r, hi_r) of the host query into its staging buffer, pushes that
+// slice into every other rank's staging buffer over peer memory (NVLink), and
+// each rank then runs its parts on the staged query (irl_ccmm_run_dq). The
+// host sends the query across PCIe once in total instead of once per GPU,
+// which pays when a rank's GEMM per modulus is shorter than its H2D (one
+// 2^14-row part per GPU: 18 ms of GEMM against 21.7 ms to copy 1.17 GB).
+bool shard_query(const irl_ccmm_group* g) {
+    if (g->ndev < 2 || g->shard == 0) return false;
+    if (g->shard == 1) return true;
+    size_t most = 0;
+    for (size_t c : g->count) most = std::max(most, c);
+    return most * g->M < 20000;  // about one paper-size part per rank (bench.py uses the same rule)
+}
+
+void enable_all_peers(irl_ccmm_group* g) {
+    if (g->peers_enabled) return;
+    for (size_t a = 0; a < g->ndev; ++a)
+        for (size_t b = 0; b < g->ndev; ++b) {
+            if (g->dev[a] == g->dev[b]) continue;
+            int can = 0;
+            cudaSetDevice(g->dev[a]);
+            if (cudaDeviceCanAccessPeer(&can, g->dev[a], g->dev[b]) == cudaSuccess && can)
+                cudaDeviceEnablePeerAccess(g->dev[b], 0);  // AlreadyEnabled is fine
+            cudaGetLastError();
+        }
+    g->peers_enabled = true;
+}
+
+// Runs f(r) on one host thread per rank; the first failing rank's status.
+template <typename F>
+int on_ranks(irl_ccmm_group* g, F f) {
+    std::vector<int> st(g->ndev, IRL_OK);
+    std::vector<std::thread> th;
+    for (size_t r = 0; r < g->ndev; ++r) th.emplace_back([&, r] { st[r] = f(r); });
+    for (auto& t : th) t.join();
+    for (size_t r = 0; r < g->ndev; ++r)
+        if (st[r] != IRL_OK)
+            return set_err(g->ctx[0], st[r], std::string("rank ") + std::to_string(r) + ": " + irl_last_error(g->ctx[r]));
+    return IRL_OK;
+}
+
+int run_sharded(irl_ccmm_group* g, const uint16_t* q_res_host, size_t n, uint16_t* out_host) {
+    enable_all_peers(g);
+    const size_t slice = g->K * n;  // elements of one modulus' query [K][n]
+    std::vector<uint16_t*> q(g->ndev);
+    for (size_t r = 0; r < g->ndev; ++r) {
+        void* p = nullptr;
+        irl_ccmm_buffers(g->eng[r], &p, nullptr);
+        q[r] = static_cast<uint16_t*>(p);
+    }
+    auto lo = [&](size_t r) { return r * g->nmod / g->ndev; };
+    // 1. each rank's share of the moduli, host -> its own staging buffer
+    if (int st = on_ranks(g, [&](size_t r) -> int {
+            irl_ctx* c = g->ctx[r];
+            Guard gd(c, "irl_ccmm_full: query shard H2D");
+            const size_t off = lo(r) * slice, elems = (lo(r + 1) - lo(r)) * slice;
+            IRL_CK(c, copy_h2d(c, q[r] + off, q_res_host + off, elems * 2, c->stream));
+            IRL_CK(c, cudaStreamSynchronize(c->stream));
+            return IRL_OK;
+        }))
+        return st;
+    // 2. all-gather: every rank pushes its share into the other ranks' buffers
+    if (int st = on_ranks(g, [&](size_t r) -> int {
+            irl_ctx* c = g->ctx[r];
+            Guard gd(c, "irl_ccmm_full: query all-gather");
+            const size_t off = lo(r) * slice, bytes = (lo(r + 1) - lo(r)) * slice * 2;
+            for (size_t t = 0; t < g->ndev; ++t)
+                if (t != r && bytes)
+                    IRL_CK(c, cudaMemcpyPeerAsync(q[t] + off, g->dev[t], q[r] + off, g->dev[r], bytes, c->stream));
+            IRL_CK(c, cudaStreamSynchronize(c->stream));
+            return IRL_OK;
+        }))
+        return st;
+    // 3. every rank's parts on the staged query
+    return on_ranks(g, [&](size_t r) -> int {
+        return irl_ccmm_run_dq(g->eng[r], nullptr, n, out_host + g->first[r] * g->nmod * n * g->M, nullptr);
+    });
+}
+
 }  // namespace
 
 extern "C" {
+
+int irl_ccmm_group_set_query_shard(irl_ccmm_group* g, int mode) {
+    if (!g || mode < -1 || mode > 1) return IRL_ERR_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(g->mu);
+    g->shard = mode;
+    return IRL_OK;
+}
 
 int irl_ccmm_group_create(const int* devices, size_t ndev, size_t parts, size_t m, size_t k, size_t max_n,
                           const uint32_t* primes, const uint32_t* exps, size_t nmod, irl_ccmm_group** out) {
@@ -356,17 +445,13 @@ int irl_ccmm_full(irl_ccmm_group* g, const uint16_t* q_res_host, size_t n, uint1
     // consumer still reading the previous call's a-part is never overwritten
     g->slot = (g->slot + 1) % IRL_RECV_SLOTS;
     if (int st = irl_ccmm_set_mirror_slot(g->eng[0], g->slot)) return st;
-    std::vector<int> st(g->ndev, IRL_OK);
-    std::vector<std::thread> th;
-    for (size_t r = 0; r < g->ndev; ++r)
-        th.emplace_back([&, r] {
-            uint16_t* dst = out_host + g->first[r] * g->nmod * n * g->M;
-            st[r] = irl_ccmm_run(g->eng[r], q_res_host, n, dst);
-        });
-    for (auto& t : th) t.join();
-    for (size_t r = 0; r < g->ndev; ++r)
-        if (st[r] != IRL_OK)
-            return set_err(c0, st[r], std::string("rank ") + std::to_string(r) + ": " + irl_last_error(g->ctx[r]));
+    if (shard_query(g)) {
+        if (int st = run_sharded(g, q_res_host, n, out_host)) return st;
+    } else if (int st = on_ranks(g, [&](size_t r) -> int {
+                   return irl_ccmm_run(g->eng[r], q_res_host, n, out_host + g->first[r] * g->nmod * n * g->M);
+               })) {
+        return st;
+    }
     void* q0 = nullptr;
     void* out0 = nullptr;
     irl_ccmm_buffers(g->eng[0], &q0, &out0);  // rank 0's outputs; part 0 = the a-part result

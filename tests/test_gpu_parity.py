@@ -640,6 +640,16 @@ def test_ccmm_group_full_equals_one_engine_and_exchanges_the_a_part(devices, par
             assert np.array_equal(g.a_part(r, ptrs[r], n).cpu().numpy().view(np.uint16), want[0]), r
         out3, ptrs3, _ = g.run(q)  # third call: back to the first slot
         assert np.array_equal(out3, want) and ptrs3[-1] == ptrs[-1]
+        # the sharded query distribution (each rank's moduli from the host, then
+        # a peer all-gather, then irl_ccmm_run_dq) and the whole-query copies
+        # give the same outputs and the same a-part on every rank
+        for shard in (1, 0, -1):
+            g.set_query_shard(shard)
+            outs, ptrs_s, mode_s = g.run(q2)
+            assert mode_s == capi.IRL_EXCHANGE_P2P and np.array_equal(outs, want2), shard
+            torch.cuda.synchronize()
+            for r in range(len(devices)):
+                assert np.array_equal(g.a_part(r, ptrs_s[r], n).cpu().numpy().view(np.uint16), want2[0]), (shard, r)
     finally:
         g.close()
 
