@@ -627,7 +627,7 @@ def measure_iris(R):
     eyes x rotations batch, match bits out; the ternary / mask products run on
     the block-scaled FP4 tensor path, the query columns on M (one pass over the
     database). Host wall clock per call (query bits in, match bits out into a
-    reused pageable buffer), median of 10."""
+    reused pinned buffer), median of 10."""
     args, rank, M = R.args, R.rank, R.M
     if rank != 0:
         return None
@@ -642,7 +642,9 @@ def measure_iris(R):
     bits = lambda n: rng.integers(0, 1 << 63, size=(n, words), dtype=np.uint64)  # noqa: E731
     dc, dm, qc, qm = bits(n_db), bits(n_db) | bits(n_db), bits(eyes), bits(eyes) | bits(eyes)
     db = IrisDatabase.from_packed(dc, dm, d, eyes * rho)
-    out_bits = np.zeros((eyes, n_db), np.uint8)  # one caller-owned output buffer, reused per batch
+    # one caller-owned, page-locked output buffer reused per batch (as the CCMM
+    # e2e uses pinned host buffers): the match bits are DMA'd straight into it
+    out_bits = R.torch.zeros((eyes, n_db), dtype=R.torch.uint8).pin_memory().numpy()
     try:
         for _ in range(3):
             db.match_packed(qc, qm, eyes, rho, Interval(0.35, 1.0), out_bits=out_bits)
@@ -655,7 +657,8 @@ def measure_iris(R):
         db.close()
     ms = statistics.median(ts)
     ops = 4.0 * n_db * eyes * rho * d  # two products, 2 ops per multiply-add
-    return {"stage": "irl_iris_db_match (registered database, host buffers)", "ms": ms,
+    return {"stage": "irl_iris_db_match (registered database, host buffers: query bits in, "
+                     "match bits out into a reused pinned buffer)", "ms": ms,
             "effective_tops": ops / (ms * 1e-3) / 1e12, "n_db": n_db, "columns": eyes * rho, "d": d,
             "tensor_path": "int8 (IRL_IRIS_I8)" if _os.environ.get("IRL_IRIS_I8") else
                            "FP4 e2m1, tcgen05 kind::mxf4.block_scale, unit scales, FP32 accumulate (exact)",
