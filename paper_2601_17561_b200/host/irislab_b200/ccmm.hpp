@@ -6,7 +6,10 @@
 //     ccmm_twin's order (the plaintext-twin bookkeeping -- level, encoding,
 //     trace -- stays with the caller's emulator);
 //   * irislab::b200::CcmmEngine: RAII over the device-resident engine (the
-//     paper's 8-slice database), one query batch per run().
+//     paper's 8-slice database), one query batch per run();
+//   * irislab::b200::CcmmGroup: the same over several GPUs from one process
+//     (irl_ccmm_group_* / irl_ccmm_full): the parts dealt across the devices,
+//     the a-part result exchanged to every rank, the query sharded over them.
 #pragma once
 
 #include <cstddef>
@@ -17,6 +20,7 @@
 #include "modmat.hpp"  // irislab::Error, ShapeMismatch, ModulusBudget, DeviceError, RnsBasis
 
 struct irl_ccmm;
+struct irl_ccmm_group;
 
 namespace irislab {
 namespace emu {
@@ -81,6 +85,40 @@ public:
 private:
     irl_ccmm* e_ = nullptr;
     std::size_t parts_, m_, k_, max_n_, nmod_;
+};
+
+/// The whole CCMM across devices from one process: one engine per entry of
+/// `devices` (a device may repeat), parts dealt in contiguous blocks with the
+/// a-part (part 0) on rank 0 (dist.part_range); ShapeMismatch if there are
+/// more devices than parts.
+class CcmmGroup {
+public:
+    CcmmGroup(const std::vector<int>& devices, std::size_t parts, std::size_t m, std::size_t k, std::size_t max_n,
+              const modmat::RnsBasis& basis = modmat::build_paper_basis());
+    ~CcmmGroup();
+    CcmmGroup(const CcmmGroup&) = delete;
+    CcmmGroup& operator=(const CcmmGroup&) = delete;
+
+    std::size_t ranks() const { return ranks_; }
+    std::size_t first_part(std::size_t rank) const;
+    std::size_t rank_parts(std::size_t rank) const;
+    /// counter-RNG synthetic database, every rank its global parts
+    void synth_db(uint64_t seed);
+    /// global part `part` streamed from the reference's BigMatrix file into its rank
+    void load_part_file(std::size_t part, const std::string& path);
+    /// IRL_EXCHANGE_* (irl_ccmm_group_set_exchange) / -1, 0, 1 (irl_ccmm_group_set_query_shard)
+    void set_exchange(int mode);
+    void set_query_shard(int mode);
+    /// q_res [nmod][k][n] -> out [parts][nmod][n][m] (every part, global order);
+    /// returns the IRL_EXCHANGE_* the a-part exchange used; a_out (nullable,
+    /// ranks() entries): each rank's device copy of the a-part result
+    int run(const uint16_t* q_res, std::size_t n, uint16_t* out, void** a_out = nullptr);
+    std::vector<uint16_t> run(const std::vector<uint16_t>& q_res, std::size_t n);
+
+private:
+    void check(int st) const;
+    irl_ccmm_group* g_ = nullptr;
+    std::size_t ranks_, parts_, m_, k_, max_n_, nmod_;
 };
 
 }  // namespace b200

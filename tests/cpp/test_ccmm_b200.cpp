@@ -112,6 +112,22 @@ void engine_vs_oracle() {
     for (size_t x = 0; x < out1.size(); ++x) same = same && out1[x] == out[x];
     CHECK(same);
     CHECK_THROWS_AS(one.load_part(0, std::vector<uint16_t>(3)), ShapeMismatch);
+
+    // the same database over a group of two ranks (both on device 0 here):
+    // parts dealt 2 + 1, outputs in global order equal to the one engine's,
+    // with the query copied whole per rank and sharded with a peer all-gather
+    b200::CcmmGroup grp({0, 0}, parts, m, k, n, basis);
+    CHECK(grp.ranks() == 2 && grp.first_part(0) == 0 && grp.rank_parts(0) == 2 && grp.first_part(1) == 2 &&
+          grp.rank_parts(1) == 1);
+    grp.synth_db(1);
+    for (int shard : {0, 1}) {
+        grp.set_query_shard(shard);
+        const auto outg = grp.run(q, n);
+        bool eq = outg.size() == out.size();
+        for (size_t x = 0; eq && x < out.size(); ++x) eq = outg[x] == out[x];
+        CHECK(eq);
+    }
+    CHECK_THROWS_AS(b200::CcmmGroup({0, 0, 0, 0}, parts, m, k, n, basis), ShapeMismatch);
 }
 
 }  // namespace

@@ -81,7 +81,7 @@ def ccmm_binary(binary):
 def test_cpp_ccmm_mirror_builds(ccmm_binary):
     assert ccmm_binary.exists()
     syms = subprocess.run(["nm", "-DC", str(PKG / "libirl_b200.so")], capture_output=True, text=True).stdout
-    for fn in ["irislab::emu::ccmm_twin_product", "irislab::b200::CcmmEngine::run"]:
+    for fn in ["irislab::emu::ccmm_twin_product", "irislab::b200::CcmmEngine::run", "irislab::b200::CcmmGroup::run"]:
         assert fn in syms
 
 
