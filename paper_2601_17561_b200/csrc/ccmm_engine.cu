@@ -374,12 +374,18 @@ int irl_ccmm_load_part_file(irl_ccmm* e, size_t part, const char* path) {
     for (size_t r0 = 0; r0 < e->M; r0 += chunk, ++ci) {
         const size_t b = ci % 2, nrows = std::min(chunk, e->M - r0), bytes = nrows * row_bytes;
         IRL_CK(ctx, cudaEventSynchronize(done[b]));  // buffer b's previous chunk is on the device
-        // 4 readers per chunk (pread at disjoint offsets): page-cache copies and
-        // NVMe queues both scale with concurrent requests
+        // 8 readers per chunk (pread at disjoint offsets): page-cache copies and
+        // NVMe queues both scale with concurrent requests (r2, 16-CPU host, one
+        // 18.5 GB part from the page cache: 4 readers 9-15 GB/s, 8 readers
+        // 15-23 GB/s, 16 readers 17-22 GB/s; profiles/r2_ingest_readers.txt)
         {
-            constexpr int kReaders = 4;
-            bool ok[kReaders];
-            std::thread th[kReaders];
+            static const int kReaders = [] {
+                const char* v = std::getenv("IRL_INGEST_READERS");
+                const int n = v ? std::atoi(v) : 8;
+                return n < 1 ? 1 : (n > 32 ? 32 : n);
+            }();
+            std::vector<char> ok(kReaders, 0);
+            std::vector<std::thread> th(kReaders);
             const size_t piece = (bytes + kReaders - 1) / kReaders;
             for (int t = 0; t < kReaders; ++t) {
                 th[t] = std::thread([&, t] {
