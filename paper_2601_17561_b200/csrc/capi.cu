@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -196,20 +197,63 @@ cudaError_t ensure_bounce(irl_ctx* ctx) {
     return cudaSuccess;
 }
 
+// Persistent host copy workers for the bounce-buffer path: a pageable caller
+// buffer is copied by kCopyThreads threads at once (one thread cannot saturate
+// host memory), without starting threads per 16 MB chunk. One job at a time;
+// process-wide, never torn down (the workers only sleep between jobs).
+class CopyPool {
+public:
+    CopyPool() {
+        for (int t = 0; t < kCopyThreads; ++t) std::thread([this, t] { work(t); }).detach();
+    }
+    void run(void* dst, const void* src, size_t bytes) {
+        std::lock_guard<std::mutex> job(run_mu_);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            dst_ = static_cast<uint8_t*>(dst);
+            src_ = static_cast<const uint8_t*>(src);
+            bytes_ = bytes;
+            piece_ = (bytes + kCopyThreads - 1) / kCopyThreads;
+            pending_ = kCopyThreads;
+            ++gen_;
+        }
+        go_.notify_all();
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [this] { return pending_ == 0; });
+    }
+
+private:
+    void work(int t) {
+        uint64_t seen = 0;
+        std::unique_lock<std::mutex> lk(mu_);
+        for (;;) {
+            go_.wait(lk, [&] { return gen_ != seen; });
+            seen = gen_;
+            uint8_t* d = dst_;
+            const uint8_t* s = src_;
+            const size_t lo = std::min(bytes_, t * piece_), hi = std::min(bytes_, lo + piece_);
+            lk.unlock();
+            if (hi > lo) std::memcpy(d + lo, s + lo, hi - lo);
+            lk.lock();
+            if (--pending_ == 0) done_.notify_one();
+        }
+    }
+    std::mutex run_mu_, mu_;
+    std::condition_variable go_, done_;
+    uint8_t* dst_ = nullptr;
+    const uint8_t* src_ = nullptr;
+    size_t bytes_ = 0, piece_ = 0;
+    int pending_ = 0;
+    uint64_t gen_ = 0;
+};
+
 void parallel_memcpy(void* dst, const void* src, size_t bytes) {
     if (bytes < (size_t(1) << 20)) {
         std::memcpy(dst, src, bytes);
         return;
     }
-    std::thread th[kCopyThreads];
-    const size_t piece = (bytes + kCopyThreads - 1) / kCopyThreads;
-    for (int t = 0; t < kCopyThreads; ++t) {
-        const size_t lo = std::min(bytes, t * piece), hi = std::min(bytes, lo + piece);
-        th[t] = std::thread([=] {
-            if (hi > lo) std::memcpy(static_cast<uint8_t*>(dst) + lo, static_cast<const uint8_t*>(src) + lo, hi - lo);
-        });
-    }
-    for (auto& t : th) t.join();
+    static CopyPool* pool = new CopyPool();  // intentionally leaked: detached workers outlive statics
+    pool->run(dst, src, bytes);
 }
 }  // namespace
 
