@@ -9,7 +9,10 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <pthread.h>
+
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <condition_variable>
 #include <cstdint>
@@ -247,12 +250,30 @@ private:
     uint64_t gen_ = 0;
 };
 
+// The pool is intentionally leaked (its detached workers outlive static
+// destruction). A forked child has none of the parent's threads, so it drops
+// the inherited pool and starts its own on first use.
+std::atomic<CopyPool*> g_copy_pool{nullptr};
+std::mutex g_copy_pool_mu;
+
 void parallel_memcpy(void* dst, const void* src, size_t bytes) {
     if (bytes < (size_t(1) << 20)) {
         std::memcpy(dst, src, bytes);
         return;
     }
-    static CopyPool* pool = new CopyPool();  // intentionally leaked: detached workers outlive statics
+    CopyPool* pool = g_copy_pool.load(std::memory_order_acquire);
+    if (!pool) {
+        std::lock_guard<std::mutex> lk(g_copy_pool_mu);
+        pool = g_copy_pool.load(std::memory_order_relaxed);
+        if (!pool) {
+            static const bool registered = [] {
+                return pthread_atfork(nullptr, nullptr, [] { g_copy_pool.store(nullptr); }) == 0;
+            }();
+            (void)registered;
+            pool = new CopyPool();
+            g_copy_pool.store(pool, std::memory_order_release);
+        }
+    }
     pool->run(dst, src, bytes);
 }
 }  // namespace
