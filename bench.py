@@ -501,7 +501,7 @@ def measure_e2e(R):
                "h2d_bytes_per_step": int(q_host.nbytes // world if sharded else q_host.nbytes),
                "d2h_bytes_per_step": int(local_parts.count * nmod * N * M * 2),
                "outputs_equal_device_step": e2e_exact, "per_rank": per_rank_e2e,
-               "call": ("1/N of the query H2D per rank + NCCL all-gather, then irl_ccmm_run_dq "
+               "call": (f"1/N of the query H2D per rank + {args.backend.upper()} all-gather, then irl_ccmm_run_dq "
                         "(include/irl_capi.h) with pinned host outputs") if sharded else
                        "irl_ccmm_run (include/irl_capi.h) with pinned host buffers"}
     return e2e
