@@ -281,6 +281,8 @@ void parallel_memcpy(void* dst, const void* src, size_t bytes) {
 // Page-locked host memory (cudaMallocHost / cudaHostRegister, e.g. a pinned
 // torch tensor) is DMA'd directly; pageable memory goes through the bounce
 // buffers from kDirectCopyBytes up.
+void host_parallel_copy(void* dst, const void* src, size_t bytes) { parallel_memcpy(dst, src, bytes); }
+
 bool host_pinned(const void* p) {
     cudaPointerAttributes at{};
     if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {

@@ -128,6 +128,10 @@ inline cudaStream_t pick_stream(irl_ctx* ctx, void* s) {
 // h2d is stream-ordered on s; d2h returns once dst holds the data.
 cudaError_t copy_h2d(irl_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t s);
 cudaError_t copy_d2h(irl_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t s);
+// Host memory page-locked for CUDA (cudaMallocHost / cudaHostRegister)?
+bool host_pinned(const void* p);
+// Host-to-host copy on the process-wide pool of copy workers (capi.cu).
+void host_parallel_copy(void* dst, const void* src, size_t bytes);
 void release_bounce(irl_ctx* ctx);
 
 // Shared by the modmat entry points (capi.cu) and the CCMM engine
