@@ -739,3 +739,25 @@ def test_ccmm_row_blocks_synth_and_multi_part_mirror():
     assert np.array_equal(mv[1], got[:3]) and not mv[0].any()
     with pytest.raises(Exception):
         eng.set_mirror_parts(6)
+
+
+def test_ccmm_run_pageable_and_pinned_buffers_agree():
+    """irl_ccmm_run stages pageable caller buffers in page-locked memory (query
+    up front, each D2H block copied out as it lands); page-locked buffers are
+    DMA'd directly. Both give the same outputs, and the pinned output buffer
+    is written in place."""
+    import torch
+
+    from paper_2601_17561_b200.ccmm import CcmmEngine, synth_query
+    eng = CcmmEngine(parts=3, m=640, k=1536, max_n=160)
+    eng.synth_db(seed=9)
+    q = synth_query(10, eng.K, 160, eng.moduli)
+    out_pageable = eng.run(q)
+    qp = torch.from_numpy(q.view(np.int16)).pin_memory().numpy().view(np.uint16)
+    op = torch.zeros(out_pageable.shape, dtype=torch.int16).pin_memory().numpy().view(np.uint16)
+    out_pinned = eng.run(qp, op)
+    assert out_pinned is op and np.array_equal(out_pinned, out_pageable)
+    again = eng.run(q)  # the staging buffers are reused
+    assert np.array_equal(again, out_pageable)
+    _check_ccmm(eng, 9, q, out_pageable, np.array([0, 333, 639], np.uint32))
+    eng.close()
