@@ -70,8 +70,9 @@ public:
     void load_part_file(std::size_t part, const std::string& path);
     /// counter-RNG synthetic database (the bench's inputs)
     void synth_db(uint64_t seed, uint32_t first_part = 0);
-    /// q_res [nmod][k][n] -> out [parts][nmod][n][m] residues mod p^2 (blocking;
-    /// pinned host memory recommended for large batches)
+    /// q_res [nmod][k][n] -> out [parts][nmod][n][m] residues mod p^2 (blocking).
+    /// Page-locked buffers are DMA'd directly; pageable ones (std::vector) are
+    /// staged through the engine's page-locked buffers (c4: 244 ms against 153 ms)
     void run(const uint16_t* q_res, std::size_t n, uint16_t* out);
     std::vector<uint16_t> run(const std::vector<uint16_t>& q_res, std::size_t n);
 
