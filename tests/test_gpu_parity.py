@@ -761,3 +761,17 @@ def test_ccmm_run_pageable_and_pinned_buffers_agree():
     assert np.array_equal(again, out_pageable)
     _check_ccmm(eng, 9, q, out_pageable, np.array([0, 333, 639], np.uint32))
     eng.close()
+
+
+@pytest.mark.parametrize("m,k,n", [(0, 5, 3), (2, 0, 3), (2, 3, 0), (1, 1, 1)])
+def test_gemm_mod_Q_empty_and_unit_shapes(mm, basis, m, k, n):
+    """gemm_mod_Q (modmat.cpp:162-195) on empty and 1x1x1 shapes: same shape
+    and entries as the oracle (an empty inner dimension gives zeros mod Q)."""
+    rng = np.random.default_rng(m * 100 + k * 10 + n)
+    Q = basis.Q
+    a = mm.BigMatrix(m, k, [int(rng.integers(0, 1 << 62)) * int(rng.integers(1, 1 << 62)) % Q for _ in range(m * k)])
+    b = mm.BigMatrix(k, n, [int(rng.integers(0, 1 << 62)) * int(rng.integers(1, 1 << 62)) % Q for _ in range(k * n)])
+    c = mm.gemm_mod_Q(a, b, basis)
+    assert (c.rows, c.cols) == (m, n)
+    want = [sum(a.a[i * k + t] * b.a[t * n + j] for t in range(k)) % Q for i in range(m) for j in range(n)]
+    assert c.a == want
