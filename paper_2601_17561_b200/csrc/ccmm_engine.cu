@@ -793,6 +793,24 @@ int irl_ccmm_run_dq(irl_ccmm* e, const uint16_t* q_res_dev, size_t n, uint16_t* 
     }
     int st = ccmm_parts(e, n, 0, e->parts, e->out, s, 0, nmod, by_part ? cnt : nullptr);
     if (st) return st;
+    // pageable outputs: D2H into page-locked staging, each block copied out by
+    // the host workers as its event fires (as irl_ccmm_run does)
+    static const bool no_staging = std::getenv("IRL_E2E_NO_STAGING") != nullptr;
+    const bool stage_out = !no_staging && !host_pinned(out_host) &&
+                           ensure_staging(&e->hout, &e->hout_elems, e->parts * nmod * n * M);
+    uint16_t* out_dst = stage_out ? e->hout : out_host;
+    std::vector<std::pair<size_t, size_t>> landed;  // (element offset, elements) per staged block
+    auto staged_block = [&](size_t off, size_t elems) -> cudaError_t {
+        if (!stage_out) return cudaSuccess;
+        if (landed.size() == e->blk_done.size()) {
+            cudaEvent_t ev;
+            const cudaError_t er = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+            if (er != cudaSuccess) return er;
+            e->blk_done.push_back(ev);
+        }
+        landed.push_back({off, elems});
+        return cudaEventRecord(e->blk_done[landed.size() - 1], e->copy_stream);
+    };
     const uint32_t target = ppmm_last_part_target();
     bool waited = by_part && target > 0;
     for (size_t i = 0; i < nmod && waited; ++i)
@@ -806,14 +824,20 @@ int irl_ccmm_run_dq(irl_ccmm* e, const uint16_t* q_res_dev, size_t n, uint16_t* 
                 break;
             }
             const size_t row = p * nmod + i;
-            IRL_CK(ctx, cudaMemcpyAsync(out_host + row * n * M, e->out + row * n * M, n * M * 2,
+            IRL_CK(ctx, cudaMemcpyAsync(out_dst + row * n * M, e->out + row * n * M, n * M * 2,
                                         cudaMemcpyDeviceToHost, e->copy_stream));
+            IRL_CK(ctx, staged_block(row * n * M, n * M));
         }
     if (!waited) {
         IRL_CK(ctx, cudaEventRecord(e->part_done[0], s));
         IRL_CK(ctx, cudaStreamWaitEvent(e->copy_stream, e->part_done[0], 0));
-        IRL_CK(ctx, cudaMemcpyAsync(out_host, e->out, e->parts * nmod * n * M * 2, cudaMemcpyDeviceToHost,
+        IRL_CK(ctx, cudaMemcpyAsync(out_dst, e->out, e->parts * nmod * n * M * 2, cudaMemcpyDeviceToHost,
                                     e->copy_stream));
+        IRL_CK(ctx, staged_block(0, e->parts * nmod * n * M));
+    }
+    for (size_t j = 0; j < landed.size(); ++j) {
+        IRL_CK(ctx, cudaEventSynchronize(e->blk_done[j]));
+        host_parallel_copy(out_host + landed[j].first, e->hout + landed[j].first, landed[j].second * sizeof(uint16_t));
     }
     IRL_CK(ctx, cudaStreamSynchronize(e->copy_stream));
     IRL_CK(ctx, cudaStreamSynchronize(s));
