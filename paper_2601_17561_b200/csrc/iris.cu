@@ -16,7 +16,10 @@
 // kModeIrisMatch scores and matches in the epilogue, so only match bits
 // leave the GEMM (irl_iris_match, irl_iris_db_match).
 // Query column c = e * rho + r holds rotate(q_e, r) (iris_core.cpp:65-76),
-// built on the device from the packed eye templates.
+// built on the device from the packed eye templates. By default both run on
+// the block-scaled FP4 path (kModeInnerF4 / kModeIrisMatchF4, e2m1 planes);
+// the fused match of more than 768 columns puts the query columns on M
+// (4x1 clusters, one pass over the database; iris_query_rows).
 #include <cuda_runtime.h>
 
 #include <cmath>
